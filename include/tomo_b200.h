@@ -1,0 +1,193 @@
+/*
+ * tomo_b200.h — C ABI of the B200-native (sm_100a) CT normal-operator library
+ *               (libtomo_b200.so, built from paper_1705_07497_b200/csrc).
+ *
+ * Drop-in boundary for the reference's operator/solver API (proj/include/tomo/*.hpp),
+ * which has no FFI of its own: build-operator, apply, CG, split-Bregman driver. Each entry
+ * point below names the reference interface it replaces. Plain pointers and sizes only; no
+ * exceptions cross the ABI (status codes mirror the reference's exception classes and CLI
+ * exit codes, proj/include/tomo/errors.hpp:9-30, proj/tools/tomo_main.cpp:88-97).
+ *
+ * Memory: every array argument may be a DEVICE pointer (cudaMalloc / torch CUDA tensor on
+ * the op's device; the call is asynchronous on `stream`) or a HOST pointer (the library
+ * stages through device scratch and synchronizes `stream` before returning). Complex data
+ * is interleaved float32 (re, im) — complex64. Images are row-major n x n, slice samples
+ * angle-major (row j = a*n_b + t), exactly the reference's layouts
+ * (proj/include/tomo/image.hpp:11-13, proj/include/tomo/fourier_slice.hpp:20-27).
+ * `batch` independent slices are stored back to back.
+ *
+ * Threading: an op is immutable after tomo_op_create except for internal scratch; calls
+ * on the same op must be serialized by the caller (one stream at a time). Distinct ops may
+ * be used concurrently.
+ */
+#ifndef TOMO_B200_H
+#define TOMO_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define TOMO_OK 0
+#define TOMO_ERR_CONFIG 2    /* tomo::ConfigError    */
+#define TOMO_ERR_NUMERICAL 3 /* tomo::NumericalError */
+#define TOMO_ERR_IO 4        /* tomo::IoError        */
+#define TOMO_ERR_CUDA 5      /* CUDA / NCCL failure (no reference analogue) */
+
+/* backends — tomo::BackendKind (proj/include/tomo/normal_ops.hpp:10) */
+#define TOMO_BACKEND_DIRECT 0    /* W / W^T sparse interpolation pair (the GPU form of "direct") */
+#define TOMO_BACKEND_SURROGATE 2 /* truncated translated stencil T */
+
+/* Geometry: SliceGrid + NufftParams (fourier_slice.hpp:24-28, nufft.hpp:16-21) with the
+ * documented extensions: n_b radial samples (0 -> n), oversampling R (0 -> 2), window
+ * offsets [win_lo, win_hi] (reference: [-m_sp, m_sp]), explicit tau, explicit angles
+ * (NULL -> theta_a = a*pi/n_angles, fourier_slice.cpp:18). Same layout as the oracle's. */
+typedef struct tomo_geom_desc {
+  int n;
+  int n_angles;
+  int n_b;
+  int oversample;
+  int win_lo, win_hi;
+  double tau;
+  const double* angles;
+} tomo_geom_desc;
+
+typedef struct tomo_op_desc {
+  int backend;      /* TOMO_BACKEND_* */
+  int surrogate_r;  /* SurrogateConfig::radius_r (normal_ops.hpp:14), 1..4 */
+  int euclidean;    /* SurrogateConfig::euclidean */
+  int device;       /* CUDA device ordinal */
+  int angle_begin;  /* angle-block row shard [begin, end) of W; 0,0 -> all angles */
+  int angle_end;
+  int max_batch;    /* slices per call the scratch is sized for (>= 1) */
+} tomo_op_desc;
+
+typedef struct tomo_op tomo_op;
+
+typedef struct tomo_op_info {
+  int n, m, n_b, n_angles_local, window;
+  int64_t P;            /* local slice samples (rows of W) */
+  int64_t nnz;          /* W non-zeros (= P * window^2) */
+  int64_t wt_rows;      /* touched grid nodes (non-empty W^T rows) */
+  int64_t wt_slots;     /* SELL-32 slots of W^T incl. padding */
+  int64_t bytes_w;      /* device bytes of the W tables */
+  int64_t bytes_wt;     /* device bytes of the W^T tables */
+  double stencil[81];   /* surrogate stencil (2r+1)^2, fp64 host copy */
+  int surrogate_r;
+} tomo_op_info;
+
+const char* tomo_last_error(void);
+
+/* make_direct_backend / make_surrogate_backend (normal_ops.hpp:35-39) over a
+ * SliceTransform(SliceGrid, NufftParams) (fourier_slice.hpp:39). Builds W (SELL-32 ELL),
+ * its transpose, deapodisation and FFT tables on `device`; for the surrogate also the
+ * stencil (build_surrogate, normal_ops.hpp:60). */
+int tomo_op_create(const tomo_geom_desc* geom, const tomo_op_desc* desc, tomo_op** out);
+void tomo_op_destroy(tomo_op* op);
+int tomo_op_get_info(const tomo_op* op, tomo_op_info* info);
+
+/* apply_normal (normal_ops.hpp:65): complex64 n^2 -> complex64 n^2, batch slices. */
+int tomo_apply_normal(tomo_op* op, const void* in, void* out, int batch, void* stream);
+/* apply_normal_real (normal_ops.hpp:69): Re(N u) for real u (surrogate: T u). */
+int tomo_apply_normal_real(tomo_op* op, const float* in, float* out, int batch, void* stream);
+/* SliceTransform::forward (type-2, fourier_slice.hpp:43): image c64 n^2 -> samples c64 P. */
+int tomo_forward(tomo_op* op, const void* image, void* samples, int batch, void* stream);
+/* SliceTransform::adjoint (type-1, fourier_slice.hpp:46): samples c64 P -> image c64 n^2. */
+int tomo_adjoint(tomo_op* op, const void* samples, void* image, int batch, void* stream);
+/* interpolate (W, nufft.hpp:66) / spread (W^T, nufft.hpp:62) alone, on the op's internal
+ * grid layout: node = iy*m + ix (the reference's grid[ix*m + iy] transposed). */
+int tomo_spmv_w(tomo_op* op, const void* grid, void* samples, int batch, void* stream);
+int tomo_spmv_wt(tomo_op* op, const void* samples, void* grid, int batch, void* stream);
+/* Back-projection of make_subproblem (solver.cpp:200-213): alpha*Re(F_NU f); weighted=1
+ * multiplies samples by the radial density weights first (surrogate fidelity). */
+int tomo_backproject(tomo_op* op, double alpha, int weighted, const void* slice_data, float* out, int batch,
+                     void* stream);
+
+/* ---- CG (cg_solve, solver.hpp:43-44) on op(u) = alpha*B(u) + lambda*K'K u + shift*u, with
+ * B = Re(N) (direct) or T (surrogate). The reference's systems: split Bregman
+ * (alpha, lambda, sigma); Tikhonov identity-K: (alpha, 0, 1 + sigma). */
+typedef struct tomo_system {
+  double alpha, lambda, shift;
+} tomo_system;
+
+typedef struct tomo_cg_stats { /* CgStats (solver.hpp:34-38) */
+  int steps_run;
+  double min_ritz;
+  double final_rs;
+} tomo_cg_stats;
+
+/* x0 may be NULL (zero start). stats: host array of `batch` entries or NULL. */
+int tomo_cg(tomo_op* op, const tomo_system* sys, const float* rhs, const float* x0, float* x, int steps,
+            double rel_tol, int batch, tomo_cg_stats* stats, void* stream);
+
+/* ---- split_bregman_tv (solver.hpp:83-85) */
+typedef struct tomo_sb_config { /* SolverConfig (solver.hpp:51-65) */
+  double alpha, lambda;
+  int max_iters;        /* max_bregman_iters */
+  int cg_steps;         /* cg_steps_per_update */
+  double update_tol_rel;
+  int warm_start;
+  double sigma_override; /* < 0: surrogate sigma from Lanczos (solver.cpp:175-192) */
+} tomo_sb_config;
+
+typedef struct tomo_sb_trace { /* SolveTrace (solver.hpp:67-80), per slice */
+  int iterations;
+  double first_update_l1;
+  double sigma;
+  double min_ritz;
+  double imag_leakage;
+  int stopped_on_tolerance;
+} tomo_sb_trace;
+
+/* slice_data: batch x P complex64; mu: batch x n^2 float. update_l1: host, batch x
+ * max_iters (or NULL); trace: host, batch entries (or NULL). Synchronizes `stream`. */
+int tomo_split_bregman(tomo_op* op, const tomo_sb_config* cfg, const void* slice_data, float* mu, int batch,
+                       double* update_l1, tomo_sb_trace* trace, void* stream);
+
+/* ---- tikhonov_solve with K = identity (solver.cpp:309-337) at a fixed step count:
+ * cg_solve(alpha N + I, alpha Re(F_NU f), 0, steps, rel_tol). */
+int tomo_tikhonov(tomo_op* op, double alpha, const void* slice_data, float* mu, int steps, double rel_tol,
+                  int batch, void* stream);
+
+/* ---- Chambolle-Pock anisotropic TV (extension): prox of the data term
+ * (I + tau_cp*alpha*Re N) u = u~ + tau_cp*alpha*Re(F_NU f) by `cg_steps` CG steps. */
+typedef struct tomo_cp_config {
+  double alpha, lambda, tau_cp, sigma_cp, theta;
+  int iters, cg_steps;
+} tomo_cp_config;
+int tomo_chambolle_pock(tomo_op* op, const tomo_cp_config* cfg, const void* slice_data, float* mu, int batch,
+                        void* stream);
+
+/* ---- angle-row sharding across GPUs: the partial adjoint images of each rank's angle
+ * block are summed by this hook (in place, float32, on `stream`) after every type-1
+ * transform. tomo_op_attach_nccl installs an NCCL all-reduce over a communicator built from
+ * a unique id obtained with tomo_nccl_unique_id on one rank and broadcast by the caller. */
+typedef int (*tomo_allreduce_fn)(float* buf, size_t count, void* stream, void* user);
+int tomo_op_set_allreduce(tomo_op* op, tomo_allreduce_fn fn, void* user);
+int tomo_nccl_unique_id(char out[128]);
+int tomo_op_attach_nccl(tomo_op* op, const char id[128], int nranks, int rank);
+
+/* ---- element pieces (solver.cpp:12-54), device or host pointers */
+int tomo_grad(int n, const float* u, float* gx, float* gy, int batch, void* stream);
+int tomo_grad_adjoint(int n, const float* gx, const float* gy, float* out, int batch, void* stream);
+int tomo_shrink(int64_t len, const float* x, double gamma, float* out, void* stream);
+
+/* ---- synthetic inputs (host): image.cpp:22-67 rasteriser; random-ellipse table (extension,
+ * same mapping as the oracle: centre 1.2u-0.6, semi-axes 0.05+0.35u, rotation pi(2u-1),
+ * intensity u, u = (mt19937_64() >> 11) * 2^-53). */
+int tomo_shepp_logan(int n, float* img);
+int tomo_random_ellipses(int n, int count, uint64_t seed, float* img);
+
+/* Test hook: one batch of length-m FFT rows through the in-CTA Stockham kernel. */
+int tomo_fft_rows(int m, int rows, const void* in, void* out, int inverse, void* stream);
+
+/* Number of library kernels launched since load (for the bench's gpu_launches claim). */
+int64_t tomo_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

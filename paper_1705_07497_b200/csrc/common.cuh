@@ -1,0 +1,106 @@
+// common.cuh — shared device helpers for the B200 (sm_100a) normal-operator path.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define TOMO_DEV __device__ __forceinline__
+
+namespace tomo_b200 {
+
+TOMO_DEV float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+TOMO_DEV float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+TOMO_DEV float2 cmul(float2 a, float2 b) { return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+TOMO_DEV float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+TOMO_DEV float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
+TOMO_DEV float2 cmul_negi(float2 a) { return make_float2(a.y, -a.x); }  // a * (-i)
+
+// Shared-memory padding: one float2 of slack every 16 so the Stockham stride-16 stores of
+// the first radix-16 pass and the transposed row stores are bank-conflict free.
+TOMO_DEV int pad16(int i) { return i + (i >> 4); }
+__host__ __device__ constexpr int padded_len(int m) { return m + m / 16 + 4; }
+
+// Warp/block reductions in a fixed order (deterministic: every replica and every CTA that
+// re-reduces the same partials gets bit-identical scalars).
+TOMO_DEV double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum of one double per thread; result valid in all threads. blockDim.x must
+// be a multiple of 32 and <= 1024. `scratch` needs 32 doubles.
+TOMO_DEV double block_sum(double v, double* scratch) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nw = (blockDim.x + 31) >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) scratch[wid] = v;
+  __syncthreads();
+  double t = (threadIdx.x < nw) ? scratch[threadIdx.x] : 0.0;
+  if (wid == 0) t = warp_sum(t);
+  if (threadIdx.x == 0) scratch[0] = t;
+  __syncthreads();
+  const double r = scratch[0];
+  __syncthreads();
+  return r;
+}
+
+// Sum `count` per-block partials. Warp 0 reduces in a fixed lane-strided order that does
+// not depend on blockDim, so every kernel (and every replica) that re-reduces the same
+// partials obtains bit-identical scalars. All threads get the sum.
+TOMO_DEV double reduce_partials(const double* part, int count, double* scratch) {
+  if (threadIdx.x < 32) {
+    double v = 0.0;
+    for (int i = threadIdx.x; i < count; i += 32) v += part[i];
+    v = warp_sum(v);
+    if (threadIdx.x == 0) scratch[0] = v;
+  }
+  __syncthreads();
+  const double r = scratch[0];
+  __syncthreads();
+  return r;
+}
+
+// Two-value block reduction with "last block finishes": every block writes its partial
+// pair to part[2*blk..], takes a ticket; the block that takes the last ticket sums all
+// nblk pairs in fixed order (so the result is deterministic), resets the ticket counter
+// and returns true with the totals in t0/t1 (valid in all of its threads).
+TOMO_DEV bool reduce2_last(double v0, double v1, double* part, int nblk, int blk, unsigned* counter,
+                           double* scratch, double& t0, double& t1) {
+  __shared__ int s_last;
+  v0 = block_sum(v0, scratch);
+  v1 = block_sum(v1, scratch);
+  if (threadIdx.x == 0) {
+    part[2 * blk] = v0;
+    part[2 * blk + 1] = v1;
+    __threadfence();
+    const unsigned ticket = atomicAdd(counter, 1u);
+    s_last = (ticket == static_cast<unsigned>(nblk - 1));
+  }
+  __syncthreads();
+  const bool last = s_last != 0;
+  if (!last) return false;
+  __threadfence();
+  if (threadIdx.x < 32) {
+    double a = 0.0, b = 0.0;
+    for (int i = threadIdx.x; i < nblk; i += 32) {
+      a += __ldcg(&part[2 * i]);
+      b += __ldcg(&part[2 * i + 1]);
+    }
+    a = warp_sum(a);
+    b = warp_sum(b);
+    if (threadIdx.x == 0) {
+      scratch[0] = a;
+      scratch[1] = b;
+      *counter = 0u;
+    }
+  }
+  __syncthreads();
+  t0 = scratch[0];
+  t1 = scratch[1];
+  return true;
+}
+
+TOMO_DEV bool finite_f(float v) { return isfinite(v); }
+
+}  // namespace tomo_b200
