@@ -10,8 +10,10 @@
  *
  * Memory: every array argument may be a DEVICE pointer (cudaMalloc / torch CUDA tensor on
  * the op's device; the call is asynchronous on `stream`) or a HOST pointer (the library
- * stages through device scratch and synchronizes `stream` before returning). Complex data
- * is interleaved float32 (re, im) — complex64. Images are row-major n x n, slice samples
+ * stages through device scratch and synchronizes `stream` before returning).
+ * Precision: an op is created TOMO_F32 (real arrays float32, complex arrays interleaved
+ * complex64) or TOMO_F64 (float64 / complex128); every array passed to that op uses its
+ * element type. Images are row-major n x n, slice samples
  * angle-major (row j = a*n_b + t), exactly the reference's layouts
  * (proj/include/tomo/image.hpp:11-13, proj/include/tomo/fourier_slice.hpp:20-27).
  * `batch` independent slices are stored back to back.
@@ -36,6 +38,10 @@ extern "C" {
 #define TOMO_ERR_NUMERICAL 3 /* tomo::NumericalError */
 #define TOMO_ERR_IO 4        /* tomo::IoError        */
 #define TOMO_ERR_CUDA 5      /* CUDA / NCCL failure (no reference analogue) */
+
+/* precisions (the reference computes in fp64, proj/include/tomo/image.hpp:11-13) */
+#define TOMO_F32 0
+#define TOMO_F64 1
 
 /* backends — tomo::BackendKind (proj/include/tomo/normal_ops.hpp:10) */
 #define TOMO_BACKEND_DIRECT 0    /* W / W^T sparse interpolation pair (the GPU form of "direct") */
@@ -63,6 +69,7 @@ typedef struct tomo_op_desc {
   int angle_begin;  /* angle-block row shard [begin, end) of W; 0,0 -> all angles */
   int angle_end;
   int max_batch;    /* slices per call the scratch is sized for (>= 1) */
+  int precision;    /* TOMO_F32 | TOMO_F64 */
 } tomo_op_desc;
 
 typedef struct tomo_op tomo_op;
@@ -77,6 +84,7 @@ typedef struct tomo_op_info {
   int64_t bytes_wt;     /* device bytes of the W^T tables */
   double stencil[81];   /* surrogate stencil (2r+1)^2, fp64 host copy */
   int surrogate_r;
+  int precision;
 } tomo_op_info;
 
 const char* tomo_last_error(void);
@@ -89,13 +97,13 @@ int tomo_op_create(const tomo_geom_desc* geom, const tomo_op_desc* desc, tomo_op
 void tomo_op_destroy(tomo_op* op);
 int tomo_op_get_info(const tomo_op* op, tomo_op_info* info);
 
-/* apply_normal (normal_ops.hpp:65): complex64 n^2 -> complex64 n^2, batch slices. */
+/* apply_normal (normal_ops.hpp:65): complex n^2 -> complex n^2, batch slices. */
 int tomo_apply_normal(tomo_op* op, const void* in, void* out, int batch, void* stream);
 /* apply_normal_real (normal_ops.hpp:69): Re(N u) for real u (surrogate: T u). */
-int tomo_apply_normal_real(tomo_op* op, const float* in, float* out, int batch, void* stream);
-/* SliceTransform::forward (type-2, fourier_slice.hpp:43): image c64 n^2 -> samples c64 P. */
+int tomo_apply_normal_real(tomo_op* op, const void* in, void* out, int batch, void* stream);
+/* SliceTransform::forward (type-2, fourier_slice.hpp:43): complex image n^2 -> samples P. */
 int tomo_forward(tomo_op* op, const void* image, void* samples, int batch, void* stream);
-/* SliceTransform::adjoint (type-1, fourier_slice.hpp:46): samples c64 P -> image c64 n^2. */
+/* SliceTransform::adjoint (type-1, fourier_slice.hpp:46): complex samples P -> image n^2. */
 int tomo_adjoint(tomo_op* op, const void* samples, void* image, int batch, void* stream);
 /* interpolate (W, nufft.hpp:66) / spread (W^T, nufft.hpp:62) alone, on the op's internal
  * grid layout: node = iy*m + ix (the reference's grid[ix*m + iy] transposed). */
@@ -103,7 +111,7 @@ int tomo_spmv_w(tomo_op* op, const void* grid, void* samples, int batch, void* s
 int tomo_spmv_wt(tomo_op* op, const void* samples, void* grid, int batch, void* stream);
 /* Back-projection of make_subproblem (solver.cpp:200-213): alpha*Re(F_NU f); weighted=1
  * multiplies samples by the radial density weights first (surrogate fidelity). */
-int tomo_backproject(tomo_op* op, double alpha, int weighted, const void* slice_data, float* out, int batch,
+int tomo_backproject(tomo_op* op, double alpha, int weighted, const void* slice_data, void* out, int batch,
                      void* stream);
 
 /* ---- CG (cg_solve, solver.hpp:43-44) on op(u) = alpha*B(u) + lambda*K'K u + shift*u, with
@@ -120,7 +128,7 @@ typedef struct tomo_cg_stats { /* CgStats (solver.hpp:34-38) */
 } tomo_cg_stats;
 
 /* x0 may be NULL (zero start). stats: host array of `batch` entries or NULL. */
-int tomo_cg(tomo_op* op, const tomo_system* sys, const float* rhs, const float* x0, float* x, int steps,
+int tomo_cg(tomo_op* op, const tomo_system* sys, const void* rhs, const void* x0, void* x, int steps,
             double rel_tol, int batch, tomo_cg_stats* stats, void* stream);
 
 /* ---- split_bregman_tv (solver.hpp:83-85) */
@@ -142,14 +150,14 @@ typedef struct tomo_sb_trace { /* SolveTrace (solver.hpp:67-80), per slice */
   int stopped_on_tolerance;
 } tomo_sb_trace;
 
-/* slice_data: batch x P complex64; mu: batch x n^2 float. update_l1: host, batch x
+/* slice_data: batch x P complex; mu: batch x n^2 real. update_l1: host, batch x
  * max_iters (or NULL); trace: host, batch entries (or NULL). Synchronizes `stream`. */
-int tomo_split_bregman(tomo_op* op, const tomo_sb_config* cfg, const void* slice_data, float* mu, int batch,
+int tomo_split_bregman(tomo_op* op, const tomo_sb_config* cfg, const void* slice_data, void* mu, int batch,
                        double* update_l1, tomo_sb_trace* trace, void* stream);
 
 /* ---- tikhonov_solve with K = identity (solver.cpp:309-337) at a fixed step count:
  * cg_solve(alpha N + I, alpha Re(F_NU f), 0, steps, rel_tol). */
-int tomo_tikhonov(tomo_op* op, double alpha, const void* slice_data, float* mu, int steps, double rel_tol,
+int tomo_tikhonov(tomo_op* op, double alpha, const void* slice_data, void* mu, int steps, double rel_tol,
                   int batch, void* stream);
 
 /* ---- Chambolle-Pock anisotropic TV (extension): prox of the data term
@@ -158,22 +166,22 @@ typedef struct tomo_cp_config {
   double alpha, lambda, tau_cp, sigma_cp, theta;
   int iters, cg_steps;
 } tomo_cp_config;
-int tomo_chambolle_pock(tomo_op* op, const tomo_cp_config* cfg, const void* slice_data, float* mu, int batch,
+int tomo_chambolle_pock(tomo_op* op, const tomo_cp_config* cfg, const void* slice_data, void* mu, int batch,
                         void* stream);
 
 /* ---- angle-row sharding across GPUs: the partial adjoint images of each rank's angle
  * block are summed by this hook (in place, float32, on `stream`) after every type-1
- * transform. tomo_op_attach_nccl installs an NCCL all-reduce over a communicator built from
+ * transform (`count` elements of the op's precision). tomo_op_attach_nccl installs an NCCL all-reduce over a communicator built from
  * a unique id obtained with tomo_nccl_unique_id on one rank and broadcast by the caller. */
-typedef int (*tomo_allreduce_fn)(float* buf, size_t count, void* stream, void* user);
+typedef int (*tomo_allreduce_fn)(void* buf, size_t count, int precision, void* stream, void* user);
 int tomo_op_set_allreduce(tomo_op* op, tomo_allreduce_fn fn, void* user);
 int tomo_nccl_unique_id(char out[128]);
 int tomo_op_attach_nccl(tomo_op* op, const char id[128], int nranks, int rank);
 
-/* ---- element pieces (solver.cpp:12-54), device or host pointers */
-int tomo_grad(int n, const float* u, float* gx, float* gy, int batch, void* stream);
-int tomo_grad_adjoint(int n, const float* gx, const float* gy, float* out, int batch, void* stream);
-int tomo_shrink(int64_t len, const float* x, double gamma, float* out, void* stream);
+/* ---- element pieces (solver.cpp:12-54), device pointers of the given precision */
+int tomo_grad(int n, int precision, const void* u, void* gx, void* gy, int batch, void* stream);
+int tomo_grad_adjoint(int n, int precision, const void* gx, const void* gy, void* out, int batch, void* stream);
+int tomo_shrink(int64_t len, int precision, const void* x, double gamma, void* out, void* stream);
 
 /* ---- synthetic inputs (host): image.cpp:22-67 rasteriser; random-ellipse table (extension,
  * same mapping as the oracle: centre 1.2u-0.6, semi-axes 0.05+0.35u, rotation pi(2u-1),
@@ -182,7 +190,19 @@ int tomo_shepp_logan(int n, float* img);
 int tomo_random_ellipses(int n, int count, uint64_t seed, float* img);
 
 /* Test hook: one batch of length-m FFT rows through the in-CTA Stockham kernel. */
-int tomo_fft_rows(int m, int rows, const void* in, void* out, int inverse, void* stream);
+int tomo_fft_rows(int m, int rows, int precision, const void* in, void* out, int inverse, void* stream);
+
+/* Stage profiler (measurement, not part of the reference API): runs `reps` solver steps of
+ * the op's hot path on internal scratch with CUDA events between kernels on `stream` and
+ * returns, per stage, the mean device time (ms) and the algorithmic HBM bytes one launch
+ * moves. Stage ids:
+ *   0 t2_rows (P1: p-update + deapod + pad + row iFFT)   1 t2_cols (P2: column iFFT)
+ *   2 w (W SELL-32 SpMV)   3 wt_rows (W^T SpMV + first type-1 FFT pass)
+ *   4 t1_rows (PB: FFT + crop + deapod + CG epilogue)   5 cg_update   6 sb_post
+ *   7 stencil (surrogate T + K'K + CG dots)
+ * Stages that do not apply to the backend report 0. Returns TOMO_OK. */
+#define TOMO_NUM_STAGES 8
+int tomo_profile_stages(tomo_op* op, int batch, int reps, double* ms, double* bytes, void* stream);
 
 /* Number of library kernels launched since load (for the bench's gpu_launches claim). */
 int64_t tomo_kernel_launches(void);

@@ -21,6 +21,10 @@ TOMO_ERR_CUDA = 5
 
 BACKEND_DIRECT = 0
 BACKEND_SURROGATE = 2
+F32 = 0
+F64 = 1
+NUM_STAGES = 8
+STAGE_NAMES = ["t2_rows", "t2_cols", "w_spmv", "wt_rows", "t1_rows", "cg_update", "sb_post", "stencil"]
 
 
 class GeomDesc(C.Structure):
@@ -31,14 +35,14 @@ class GeomDesc(C.Structure):
 
 class OpDesc(C.Structure):
     _fields_ = [("backend", C.c_int), ("surrogate_r", C.c_int), ("euclidean", C.c_int), ("device", C.c_int),
-                ("angle_begin", C.c_int), ("angle_end", C.c_int), ("max_batch", C.c_int)]
+                ("angle_begin", C.c_int), ("angle_end", C.c_int), ("max_batch", C.c_int), ("precision", C.c_int)]
 
 
 class OpInfo(C.Structure):
     _fields_ = [("n", C.c_int), ("m", C.c_int), ("n_b", C.c_int), ("n_angles_local", C.c_int),
                 ("window", C.c_int), ("P", C.c_int64), ("nnz", C.c_int64), ("wt_rows", C.c_int64),
                 ("wt_slots", C.c_int64), ("bytes_w", C.c_int64), ("bytes_wt", C.c_int64),
-                ("stencil", C.c_double * 81), ("surrogate_r", C.c_int)]
+                ("stencil", C.c_double * 81), ("surrogate_r", C.c_int), ("precision", C.c_int)]
 
 
 class System(C.Structure):
@@ -64,7 +68,7 @@ class CpConfig(C.Structure):
                 ("sigma_cp", C.c_double), ("theta", C.c_double), ("iters", C.c_int), ("cg_steps", C.c_int)]
 
 
-ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p, C.c_void_p)
 
 VP = C.c_void_p
 EXPORTS = {
@@ -88,12 +92,13 @@ EXPORTS = {
     "tomo_op_set_allreduce": (C.c_int, [VP, ALLREDUCE_FN, VP]),
     "tomo_nccl_unique_id": (C.c_int, [C.c_char_p]),
     "tomo_op_attach_nccl": (C.c_int, [VP, C.c_char_p, C.c_int, C.c_int]),
-    "tomo_grad": (C.c_int, [C.c_int, VP, VP, VP, C.c_int, VP]),
-    "tomo_grad_adjoint": (C.c_int, [C.c_int, VP, VP, VP, C.c_int, VP]),
-    "tomo_shrink": (C.c_int, [C.c_int64, VP, C.c_double, VP, VP]),
+    "tomo_grad": (C.c_int, [C.c_int, C.c_int, VP, VP, VP, C.c_int, VP]),
+    "tomo_grad_adjoint": (C.c_int, [C.c_int, C.c_int, VP, VP, VP, C.c_int, VP]),
+    "tomo_shrink": (C.c_int, [C.c_int64, C.c_int, VP, C.c_double, VP, VP]),
     "tomo_shepp_logan": (C.c_int, [C.c_int, VP]),
     "tomo_random_ellipses": (C.c_int, [C.c_int, C.c_int, C.c_uint64, VP]),
-    "tomo_fft_rows": (C.c_int, [C.c_int, C.c_int, VP, VP, C.c_int, VP]),
+    "tomo_fft_rows": (C.c_int, [C.c_int, C.c_int, C.c_int, VP, VP, C.c_int, VP]),
+    "tomo_profile_stages": (C.c_int, [VP, C.c_int, C.c_int, VP, VP, VP]),
 }
 
 

@@ -1,4 +1,6 @@
 // common.cuh — shared device helpers for the B200 (sm_100a) normal-operator path.
+// Everything is templated on the real type R (float: the complex64 path; double: the
+// complex128 path used where CG must track the fp64 reference).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -7,14 +9,42 @@
 
 namespace tomo_b200 {
 
-TOMO_DEV float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-TOMO_DEV float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
-TOMO_DEV float2 cmul(float2 a, float2 b) { return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
-TOMO_DEV float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
-TOMO_DEV float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
-TOMO_DEV float2 cmul_negi(float2 a) { return make_float2(a.y, -a.x); }  // a * (-i)
+template <typename R>
+struct CplxT;
+template <>
+struct CplxT<float> {
+  using T = float2;
+};
+template <>
+struct CplxT<double> {
+  using T = double2;
+};
+template <typename R>
+using cplx = typename CplxT<R>::T;
 
-// Shared-memory padding: one float2 of slack every 16 so the Stockham stride-16 stores of
+template <typename C2>
+TOMO_DEV C2 mk(decltype(C2::x) a, decltype(C2::x) b) {
+  C2 r;
+  r.x = a;
+  r.y = b;
+  return r;
+}
+template <typename C2>
+TOMO_DEV C2 cadd(C2 a, C2 b) { return mk<C2>(a.x + b.x, a.y + b.y); }
+template <typename C2>
+TOMO_DEV C2 csub(C2 a, C2 b) { return mk<C2>(a.x - b.x, a.y - b.y); }
+template <typename C2>
+TOMO_DEV C2 cmul(C2 a, C2 b) { return mk<C2>(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+template <typename C2>
+TOMO_DEV C2 cscale(C2 a, decltype(C2::x) s) { return mk<C2>(a.x * s, a.y * s); }
+template <typename C2>
+TOMO_DEV C2 cconj(C2 a) { return mk<C2>(a.x, -a.y); }
+template <typename C2>
+TOMO_DEV C2 cmul_negi(C2 a) { return mk<C2>(a.y, -a.x); }  // a * (-i)
+template <typename C2>
+TOMO_DEV C2 czero() { return mk<C2>(0, 0); }
+
+// Shared-memory padding: one element of slack every 16 so the Stockham stride-16 stores of
 // the first radix-16 pass and the transposed row stores are bank-conflict free.
 TOMO_DEV int pad16(int i) { return i + (i >> 4); }
 __host__ __device__ constexpr int padded_len(int m) { return m + m / 16 + 4; }
@@ -39,22 +69,6 @@ TOMO_DEV double block_sum(double v, double* scratch) {
   double t = (threadIdx.x < nw) ? scratch[threadIdx.x] : 0.0;
   if (wid == 0) t = warp_sum(t);
   if (threadIdx.x == 0) scratch[0] = t;
-  __syncthreads();
-  const double r = scratch[0];
-  __syncthreads();
-  return r;
-}
-
-// Sum `count` per-block partials. Warp 0 reduces in a fixed lane-strided order that does
-// not depend on blockDim, so every kernel (and every replica) that re-reduces the same
-// partials obtains bit-identical scalars. All threads get the sum.
-TOMO_DEV double reduce_partials(const double* part, int count, double* scratch) {
-  if (threadIdx.x < 32) {
-    double v = 0.0;
-    for (int i = threadIdx.x; i < count; i += 32) v += part[i];
-    v = warp_sum(v);
-    if (threadIdx.x == 0) scratch[0] = v;
-  }
   __syncthreads();
   const double r = scratch[0];
   __syncthreads();
@@ -101,6 +115,7 @@ TOMO_DEV bool reduce2_last(double v0, double v1, double* part, int nblk, int blk
   return true;
 }
 
-TOMO_DEV bool finite_f(float v) { return isfinite(v); }
+template <typename R>
+TOMO_DEV bool finite_r(R v) { return isfinite(v); }
 
 }  // namespace tomo_b200

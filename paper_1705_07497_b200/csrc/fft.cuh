@@ -15,78 +15,88 @@
 
 namespace tomo_b200 {
 
-template <int R>
-TOMO_DEV void dft(float2* v);
+template <int RADIX, typename C2>
+struct Dft;
 
-template <>
-TOMO_DEV void dft<2>(float2* v) {
-  const float2 a = v[0], b = v[1];
-  v[0] = cadd(a, b);
-  v[1] = csub(a, b);
-}
-
-template <>
-TOMO_DEV void dft<4>(float2* v) {
-  const float2 a0 = cadd(v[0], v[2]), a1 = csub(v[0], v[2]);
-  const float2 a2 = cadd(v[1], v[3]), a3 = cmul_negi(csub(v[1], v[3]));
-  v[0] = cadd(a0, a2);
-  v[2] = csub(a0, a2);
-  v[1] = cadd(a1, a3);
-  v[3] = csub(a1, a3);
-}
-
-template <>
-TOMO_DEV void dft<8>(float2* v) {
-  constexpr float h = 0.70710678118654752440f;
-  float2 e[4] = {v[0], v[2], v[4], v[6]};
-  float2 o[4] = {v[1], v[3], v[5], v[7]};
-  dft<4>(e);
-  dft<4>(o);
-  // o[k] *= W8^k
-  o[1] = make_float2(h * (o[1].x + o[1].y), h * (o[1].y - o[1].x));
-  o[2] = cmul_negi(o[2]);
-  o[3] = make_float2(h * (o[3].y - o[3].x), -h * (o[3].x + o[3].y));
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    v[k] = cadd(e[k], o[k]);
-    v[k + 4] = csub(e[k], o[k]);
+template <typename C2>
+struct Dft<2, C2> {
+  static TOMO_DEV void run(C2* v) {
+    const C2 a = v[0], b = v[1];
+    v[0] = cadd(a, b);
+    v[1] = csub(a, b);
   }
-}
+};
 
-template <>
-TOMO_DEV void dft<16>(float2* v) {
+template <typename C2>
+struct Dft<4, C2> {
+  static TOMO_DEV void run(C2* v) {
+    const C2 a0 = cadd(v[0], v[2]), a1 = csub(v[0], v[2]);
+    const C2 a2 = cadd(v[1], v[3]), a3 = cmul_negi(csub(v[1], v[3]));
+    v[0] = cadd(a0, a2);
+    v[2] = csub(a0, a2);
+    v[1] = cadd(a1, a3);
+    v[3] = csub(a1, a3);
+  }
+};
+
+template <typename C2>
+struct Dft<8, C2> {
+  static TOMO_DEV void run(C2* v) {
+    using R = decltype(C2::x);
+    const R h = R(0.70710678118654752440);
+    C2 e[4] = {v[0], v[2], v[4], v[6]};
+    C2 o[4] = {v[1], v[3], v[5], v[7]};
+    Dft<4, C2>::run(e);
+    Dft<4, C2>::run(o);
+    // o[k] *= W8^k
+    o[1] = mk<C2>(h * (o[1].x + o[1].y), h * (o[1].y - o[1].x));
+    o[2] = cmul_negi(o[2]);
+    o[3] = mk<C2>(h * (o[3].y - o[3].x), -h * (o[3].x + o[3].y));
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[k] = cadd(e[k], o[k]);
+      v[k + 4] = csub(e[k], o[k]);
+    }
+  }
+};
+
+template <typename C2>
+struct Dft<16, C2> {
+  static TOMO_DEV void run(C2* v) {
   // n = n1 + 4 n2, k = k2 + 4 k1:  inner DFT4 over n2, twiddle W16^{n1 k2}, outer DFT4 over n1.
-  constexpr float c1 = 0.92387953251128675613f, s1 = 0.38268343236508977173f;
-  constexpr float h = 0.70710678118654752440f;
-  float2 x[4][4];
+  using R = decltype(C2::x);
+  const R c1 = R(0.92387953251128675613), s1 = R(0.38268343236508977173);
+  const R h = R(0.70710678118654752440);
+  C2 x[4][4];
 #pragma unroll
   for (int n1 = 0; n1 < 4; ++n1) {
     x[n1][0] = v[n1];
     x[n1][1] = v[n1 + 4];
     x[n1][2] = v[n1 + 8];
     x[n1][3] = v[n1 + 12];
-    dft<4>(x[n1]);
+    Dft<4, C2>::run(x[n1]);
   }
   // twiddles W16^{n1*k2}, n1,k2 in 1..3
-  x[1][1] = cmul(x[1][1], make_float2(c1, -s1));
-  x[1][2] = cmul(x[1][2], make_float2(h, -h));
-  x[1][3] = cmul(x[1][3], make_float2(s1, -c1));
-  x[2][1] = cmul(x[2][1], make_float2(h, -h));
+  x[1][1] = cmul(x[1][1], mk<C2>(c1, -s1));
+  x[1][2] = cmul(x[1][2], mk<C2>(h, -h));
+  x[1][3] = cmul(x[1][3], mk<C2>(s1, -c1));
+  x[2][1] = cmul(x[2][1], mk<C2>(h, -h));
   x[2][2] = cmul_negi(x[2][2]);
-  x[2][3] = cmul(x[2][3], make_float2(-h, -h));
-  x[3][1] = cmul(x[3][1], make_float2(s1, -c1));
-  x[3][2] = cmul(x[3][2], make_float2(-h, -h));
-  x[3][3] = cmul(x[3][3], make_float2(-c1, s1));
+  x[2][3] = cmul(x[2][3], mk<C2>(-h, -h));
+  x[3][1] = cmul(x[3][1], mk<C2>(s1, -c1));
+  x[3][2] = cmul(x[3][2], mk<C2>(-h, -h));
+  x[3][3] = cmul(x[3][3], mk<C2>(-c1, s1));
 #pragma unroll
   for (int k2 = 0; k2 < 4; ++k2) {
-    float2 y[4] = {x[0][k2], x[1][k2], x[2][k2], x[3][k2]};
-    dft<4>(y);
+    C2 y[4] = {x[0][k2], x[1][k2], x[2][k2], x[3][k2]};
+    Dft<4, C2>::run(y);
     v[k2] = y[0];
     v[k2 + 4] = y[1];
     v[k2 + 8] = y[2];
     v[k2 + 12] = y[3];
   }
-}
+  }
+};
 
 template <int M>
 struct FftShape {
@@ -102,12 +112,12 @@ struct FftShape {
 // One Stockham pass of radix R with sub-transform size Ns over a row in smem.
 // Thread `t` (0..T-1) of the row handles butterflies j = t, t+T, ... (M/R of them).
 // Every thread of the CTA executes both barriers; `active` gates the work only.
-template <int M, int R>
-TOMO_DEV void stockham_pass(float2* row, const float2* __restrict__ tw, int Ns, int t, bool active) {
+template <int M, int R, typename C2>
+TOMO_DEV void stockham_pass(C2* row, const C2* __restrict__ tw, int Ns, int t, bool active) {
   constexpr int T = M / 16;
   constexpr int NB = M / R;        // butterflies per pass
   constexpr int PER = NB / T;      // butterflies per thread (16/R)
-  float2 v[PER][R];
+  C2 v[PER][R];
   if (active) {
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
@@ -120,7 +130,7 @@ TOMO_DEV void stockham_pass(float2* row, const float2* __restrict__ tw, int Ns, 
 #pragma unroll
         for (int r = 1; r < R; ++r) v[q][r] = cmul(v[q][r], __ldg(&tw[r * step]));
       }
-      dft<R>(v[q]);
+      Dft<R, C2>::run(v[q]);
     }
   }
   __syncthreads();
@@ -140,17 +150,17 @@ TOMO_DEV void stockham_pass(float2* row, const float2* __restrict__ tw, int Ns, 
 // Forward FFT of one row per thread group, in place in smem. All threads of the CTA must
 // call it (it contains barriers); `t` = thread index within the row (0..M/16-1), and
 // threads without a row pass active = false.
-template <int M>
-TOMO_DEV void fft_row_smem(float2* row, const float2* __restrict__ tw, int t, bool active) {
+template <int M, typename C2>
+TOMO_DEV void fft_row_smem(C2* row, const C2* __restrict__ tw, int t, bool active) {
   using S = FftShape<M>;
   __syncthreads();
   int Ns = 1;
 #pragma unroll
   for (int p = 0; p < S::N16; ++p) {
-    stockham_pass<M, 16>(row, tw, Ns, t, active);
+    stockham_pass<M, 16, C2>(row, tw, Ns, t, active);
     Ns *= 16;
   }
-  if constexpr (S::RL > 1) stockham_pass<M, S::RL>(row, tw, Ns, t, active);
+  if constexpr (S::RL > 1) stockham_pass<M, S::RL, C2>(row, tw, Ns, t, active);
 }
 
 }  // namespace tomo_b200

@@ -10,11 +10,11 @@
 // grad / grad_adjoint / shrink (solver.cpp:12-54) and the Bregman update + next right-hand
 // side (solver.cpp:264-282) are one fused pass (k_sb_post); the surrogate T (a translated
 // stencil, normal_ops.cpp:266-281) is applied as a shared-memory tiled stencil fused with
-// lambda K'K + sigma I and the CG dots.
+// lambda K'K + sigma I and the CG dots. Templated on the real type R; dots in fp64.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
-
-#include <algorithm>
 
 namespace tomo_b200 {
 
@@ -23,8 +23,8 @@ namespace {
 constexpr int kVecThreads = 256;
 
 int vec_blocks(int64_t L, int B) {
-  // ~2-4 float4 per thread; fewer when the batch already fills the GPU
-  int64_t per_block = static_cast<int64_t>(kVecThreads) * 4;
+  // ~4 elements per thread; fewer blocks when the batch already fills the GPU
+  const int64_t per_block = static_cast<int64_t>(kVecThreads) * 4;
   int64_t nb = (L + per_block - 1) / per_block;
   if (nb * B > 8 * 148) nb = std::max<int64_t>(1, (8 * 148 + B - 1) / B);
   return static_cast<int>(std::min<int64_t>(std::max<int64_t>(nb, 1), MAX_PART_BLOCKS));
@@ -34,11 +34,14 @@ __device__ __forceinline__ bool slice_live(const SliceScalars& sc, int step) {
   return !sc.done && !sc.frozen && sc.rr[step & 1] != 0.0;
 }
 
+__device__ __forceinline__ int64_t gtid() { return static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; }
+__device__ __forceinline__ int64_t gstride() { return static_cast<int64_t>(gridDim.x) * blockDim.x; }
+
 // ------------------------------------------------------------------ CG x/r update
-__global__ void __launch_bounds__(kVecThreads) k_cg_update(int64_t L, const float* __restrict__ p,
-                                                           const float* __restrict__ ap, float* __restrict__ x,
-                                                           float* __restrict__ r, SysParams sys, int step,
-                                                           Reduce red) {
+template <typename R>
+__global__ void __launch_bounds__(kVecThreads) k_cg_update(int64_t L, const R* __restrict__ p, const R* __restrict__ ap,
+                                                           R* __restrict__ x, R* __restrict__ r, SysParams sys,
+                                                           int step, Reduce red) {
   __shared__ double scratch[32];
   const int b = blockIdx.y;
   SliceScalars& sc = red.sc[b];
@@ -53,25 +56,17 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_update(int64_t L, const floa
     }
     return;
   }
-  const float alpha = static_cast<float>(rs / pap);
+  const R alpha = static_cast<R>(rs / pap);
   const size_t off = static_cast<size_t>(b) * L;
-  const float4* p4 = reinterpret_cast<const float4*>(p + off);
-  const float4* ap4 = reinterpret_cast<const float4*>(ap + off);
-  float4* x4 = reinterpret_cast<float4*>(x + off);
-  float4* r4 = reinterpret_cast<float4*>(r + off);
   double rr = 0.0;
   bool fin = true;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < L / 4;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const float4 pv = p4[i], av = ap4[i];
-    float4 xv = x4[i], rv = r4[i];
-    xv.x += alpha * pv.x; xv.y += alpha * pv.y; xv.z += alpha * pv.z; xv.w += alpha * pv.w;
-    rv.x -= alpha * av.x; rv.y -= alpha * av.y; rv.z -= alpha * av.z; rv.w -= alpha * av.w;
-    x4[i] = xv;
-    r4[i] = rv;
-    fin = fin && finite_f(xv.x) && finite_f(xv.y) && finite_f(xv.z) && finite_f(xv.w);
-    rr += static_cast<double>(rv.x) * rv.x + static_cast<double>(rv.y) * rv.y +
-          static_cast<double>(rv.z) * rv.z + static_cast<double>(rv.w) * rv.w;
+  for (int64_t i = gtid(); i < L; i += gstride()) {
+    const R xv = x[off + i] + alpha * p[off + i];
+    const R rv = r[off + i] - alpha * ap[off + i];
+    x[off + i] = xv;
+    r[off + i] = rv;
+    fin = fin && finite_r(xv);
+    rr += static_cast<double>(rv) * rv;
   }
   if (!fin) sc.nonfinite = 1;
   double t0, t1;
@@ -91,18 +86,19 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_update(int64_t L, const floa
 // Tile of 32x32 outputs, 256 threads (32 x 8, 4 rows each). Halo H = max(rad, 1).
 constexpr int kTile = 32;
 
-template <int RAD>
-__global__ void __launch_bounds__(256) k_stencil(int n, StencilCoef coef, int mode, const float* __restrict__ in,
-                                                 const float* __restrict__ r_in, float* __restrict__ p_out,
-                                                 float* __restrict__ ap_out, const float* __restrict__ bvec,
-                                                 float* __restrict__ x_out, SysParams sys, int step, Reduce red) {
+template <int RAD, typename R>
+__global__ void __launch_bounds__(256) k_stencil(int n, StencilCoef coef, int mode, const R* __restrict__ in,
+                                                 const R* __restrict__ r_in, R* __restrict__ p_out,
+                                                 R* __restrict__ ap_out, const R* __restrict__ bvec,
+                                                 R* __restrict__ x_out, SysParams sys, int step, Reduce red) {
   constexpr int HALO = RAD > 1 ? RAD : 1;
   constexpr int W = kTile + 2 * HALO;
   constexpr int SIDE = 2 * RAD + 1;
-  __shared__ float q[W][W + 1];
+  __shared__ R q[W][W + 1];
+  __shared__ R cf[SIDE * SIDE];
   __shared__ double scratch[32];
   const int b = blockIdx.z;
-  float beta = 0.f;
+  R beta = 0;
   if (mode != 2 && red.sc[b].frozen) return;
   if (mode == 0) {
     SliceScalars& sc = red.sc[b];
@@ -112,14 +108,15 @@ __global__ void __launch_bounds__(256) k_stencil(int n, StencilCoef coef, int mo
       sc.done = 1;
       return;
     }
-    if (step > 0) beta = static_cast<float>(rs / sc.rr[(step + 1) & 1]);
+    if (step > 0) beta = static_cast<R>(rs / sc.rr[(step + 1) & 1]);
   }
+  for (int k = threadIdx.x; k < SIDE * SIDE; k += blockDim.x) cf[k] = static_cast<R>(coef.c[k]);
   const size_t off = static_cast<size_t>(b) * n * n;
   const int i0 = blockIdx.y * kTile - HALO, j0 = blockIdx.x * kTile - HALO;
   for (int idx = threadIdx.x; idx < W * W; idx += blockDim.x) {
     const int li = idx / W, lj = idx - li * W;
     const int gi = i0 + li, gj = j0 + lj;
-    float v = 0.f;
+    R v = 0;
     if (gi >= 0 && gi < n && gj >= 0 && gj < n) {
       const size_t o = off + static_cast<size_t>(gi) * n + gj;
       v = in[o];
@@ -129,24 +126,25 @@ __global__ void __launch_bounds__(256) k_stencil(int n, StencilCoef coef, int mo
   }
   __syncthreads();
   const int tj = threadIdx.x & 31, ti = threadIdx.x >> 5;
+  const R alpha = static_cast<R>(sys.alpha), lam = static_cast<R>(sys.lambda), shift = static_cast<R>(sys.shift);
   double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int li = ti + 8 * k + HALO, lj = tj + HALO;
     const int gi = i0 + li, gj = j0 + lj;
     if (gi >= n || gj >= n) continue;
-    const float c = q[li][lj];
-    float tq = 0.f;
+    const R c = q[li][lj];
+    R tq = 0;
 #pragma unroll
     for (int di = -RAD; di <= RAD; ++di)
 #pragma unroll
-      for (int dj = -RAD; dj <= RAD; ++dj) tq += coef.c[(di + RAD) * SIDE + (dj + RAD)] * q[li + di][lj + dj];
-    float kk = 0.f;
+      for (int dj = -RAD; dj <= RAD; ++dj) tq += cf[(di + RAD) * SIDE + (dj + RAD)] * q[li + di][lj + dj];
+    R kk = 0;
     if (gj >= 1) kk += c - q[li][lj - 1];
     if (gj <= n - 2) kk -= q[li][lj + 1] - c;
     if (gi >= 1) kk += c - q[li - 1][lj];
     if (gi <= n - 2) kk -= q[li + 1][lj] - c;
-    const float ax = sys.alpha * tq + sys.lambda * kk + sys.shift * c;
+    const R ax = alpha * tq + lam * kk + shift * c;
     const size_t o = off + static_cast<size_t>(gi) * n + gj;
     if (mode == 0) {
       if (step > 0) p_out[o] = c;
@@ -154,8 +152,8 @@ __global__ void __launch_bounds__(256) k_stencil(int n, StencilCoef coef, int mo
       acc0 += static_cast<double>(c) * ax;
       acc1 += static_cast<double>(c) * c;
     } else if (mode == 1) {
-      const float bv = bvec[o];
-      const float rv = bv - ax;
+      const R bv = bvec[o];
+      const R rv = bv - ax;
       ap_out[o] = rv;
       p_out[o] = rv;
       x_out[o] = c;
@@ -184,10 +182,11 @@ __global__ void __launch_bounds__(256) k_stencil(int n, StencilCoef coef, int mo
   }
 }
 
-__device__ __forceinline__ float ktk_g(const float* __restrict__ p, int n, int i, int j) {
+template <typename R>
+__device__ __forceinline__ R ktk_g(const R* __restrict__ p, int n, int i, int j) {
   const size_t o = static_cast<size_t>(i) * n + j;
-  const float c = p[o];
-  float v = 0.f;
+  const R c = p[o];
+  R v = 0;
   if (j >= 1) v += c - p[o - 1];
   if (j <= n - 2) v -= p[o + 1] - c;
   if (i >= 1) v += c - p[o - n];
@@ -196,10 +195,11 @@ __device__ __forceinline__ float ktk_g(const float* __restrict__ p, int n, int i
 }
 
 // Sharded-operator epilogue: nred = all-reduced alpha*Re(N p) partial sums.
-__global__ void __launch_bounds__(kVecThreads) k_cg_epilogue(int n, int mode, const float* __restrict__ nred,
-                                                             const float* __restrict__ p, const float* __restrict__ bvec,
-                                                             float* __restrict__ ap, float* __restrict__ p_out,
-                                                             float* __restrict__ x_out, SysParams sys, int step,
+template <typename R>
+__global__ void __launch_bounds__(kVecThreads) k_cg_epilogue(int n, int mode, const R* __restrict__ nred,
+                                                             const R* __restrict__ p, const R* __restrict__ bvec,
+                                                             R* __restrict__ ap, R* __restrict__ p_out,
+                                                             R* __restrict__ x_out, SysParams sys, int step,
                                                              Reduce red) {
   __shared__ double scratch[32];
   const int b = blockIdx.y;
@@ -207,22 +207,22 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_epilogue(int n, int mode, co
   if (sc.frozen || (mode == 0 && !slice_live(sc, step))) return;
   const int64_t L = static_cast<int64_t>(n) * n;
   const size_t off = static_cast<size_t>(b) * L;
-  const float* pb = p + off;
+  const R* pb = p + off;
+  const R lam = static_cast<R>(sys.lambda), shift = static_cast<R>(sys.shift);
   double acc0 = 0.0, acc1 = 0.0;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < L;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  for (int64_t i = gtid(); i < L; i += gstride()) {
     const int ii = static_cast<int>(i / n), jj = static_cast<int>(i - static_cast<int64_t>(ii) * n);
-    const float pv = pb[i];
-    float ax = nred[off + i];
-    if (sys.lambda != 0.f) ax += sys.lambda * ktk_g(pb, n, ii, jj);
-    ax += sys.shift * pv;
+    const R pv = pb[i];
+    R ax = nred[off + i];
+    if (lam != R(0)) ax += lam * ktk_g(pb, n, ii, jj);
+    ax += shift * pv;
     if (mode == 0) {
       ap[off + i] = ax;
       acc0 += static_cast<double>(pv) * ax;
       acc1 += static_cast<double>(pv) * pv;
     } else {
-      const float bv = bvec[off + i];
-      const float rv = bv - ax;
+      const R bv = bvec[off + i];
+      const R rv = bv - ax;
       ap[off + i] = rv;
       p_out[off + i] = rv;
       x_out[off + i] = pv;
@@ -251,60 +251,60 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_epilogue(int n, int mode, co
 // (solver.cpp:278-282), next rhs = fid + lambda grad^T(d - b_new) (solver.cpp:264-265),
 // and ||mu_new - mu_old||_1 (solver.cpp:288). d is never stored: d - b_new is recomputed at
 // the two neighbours grad^T needs.
-__device__ __forceinline__ float shrinkf(float x, float gamma) {
-  const float m = fabsf(x) - gamma;
-  return m > 0.f ? (x > 0.f ? m : -m) : 0.f;
+template <typename R>
+__device__ __forceinline__ R shrinkr(R x, R gamma) {
+  const R m = fabs(x) - gamma;
+  return m > R(0) ? (x > R(0) ? m : -m) : R(0);
 }
 
-__global__ void __launch_bounds__(kVecThreads) k_sb_post(int n, float* __restrict__ mu_new,
-                                                         const float* __restrict__ mu_old, const float* __restrict__ bx_old,
-                                                         const float* __restrict__ by_old, float* __restrict__ bx_new,
-                                                         float* __restrict__ by_new, const float* __restrict__ fid,
-                                                         float* __restrict__ rhs, float lambda, Reduce red) {
+template <typename R>
+__global__ void __launch_bounds__(kVecThreads) k_sb_post(int n, R* __restrict__ mu_new, const R* __restrict__ mu_old,
+                                                         const R* __restrict__ bx_old, const R* __restrict__ by_old,
+                                                         R* __restrict__ bx_new, R* __restrict__ by_new,
+                                                         const R* __restrict__ fid, R* __restrict__ rhs,
+                                                         double lambda_d, Reduce red) {
   __shared__ double scratch[32];
   const int b = blockIdx.y;
   const int64_t L = static_cast<int64_t>(n) * n;
   const size_t off = static_cast<size_t>(b) * L;
   SliceScalars& sc = red.sc[b];
   if (sc.frozen) {  // stopped on tolerance: carry the state through unchanged
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < L;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    for (int64_t i = gtid(); i < L; i += gstride()) {
       mu_new[off + i] = mu_old[off + i];
       bx_new[off + i] = bx_old[off + i];
       by_new[off + i] = by_old[off + i];
     }
     return;
   }
-  const float* mu = mu_new + off;
-  const float* bxo = bx_old + off;
-  const float* byo = by_old + off;
-  const float gamma = 1.0f / lambda;
+  const R* mu = mu_new + off;
+  const R* bxo = bx_old + off;
+  const R* byo = by_old + off;
+  const R lambda = static_cast<R>(lambda_d);
+  const R gamma = static_cast<R>(1.0 / lambda_d);
   double upd = 0.0;
   bool fin = true;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < L;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  for (int64_t i = gtid(); i < L; i += gstride()) {
     const int ii = static_cast<int>(i / n), jj = static_cast<int>(i - static_cast<int64_t>(ii) * n);
-    const float c = mu[i];
-    fin = fin && finite_f(c);
+    const R c = mu[i];
+    fin = fin && finite_r(c);
     upd += fabs(static_cast<double>(c) - static_cast<double>(mu_old[off + i]));
-    // own pixel
-    const float gx = jj < n - 1 ? mu[i + 1] - c : 0.f;
-    const float gy = ii < n - 1 ? mu[i + n] - c : 0.f;
-    const float dx = shrinkf(gx + bxo[i], gamma), dy = shrinkf(gy + byo[i], gamma);
-    const float bxn = bxo[i] + gx - dx, byn = byo[i] + gy - dy;
+    const R gx = jj < n - 1 ? mu[i + 1] - c : R(0);
+    const R gy = ii < n - 1 ? mu[i + n] - c : R(0);
+    const R dx = shrinkr(gx + bxo[i], gamma), dy = shrinkr(gy + byo[i], gamma);
+    const R bxn = bxo[i] + gx - dx, byn = byo[i] + gy - dy;
     bx_new[off + i] = bxn;
     by_new[off + i] = byn;
-    float div = 0.f;
+    R div = 0;
     if (jj <= n - 2) div -= dx - bxn;
     if (ii <= n - 2) div -= dy - byn;
     if (jj >= 1) {  // tx at (ii, jj-1)
-      const float gxl = c - mu[i - 1];
-      const float dxl = shrinkf(gxl + bxo[i - 1], gamma);
+      const R gxl = c - mu[i - 1];
+      const R dxl = shrinkr(gxl + bxo[i - 1], gamma);
       div += dxl - (bxo[i - 1] + gxl - dxl);
     }
     if (ii >= 1) {  // ty at (ii-1, jj)
-      const float gyu = c - mu[i - n];
-      const float dyu = shrinkf(gyu + byo[i - n], gamma);
+      const R gyu = c - mu[i - n];
+      const R dyu = shrinkr(gyu + byo[i - n], gamma);
       div += dyu - (byo[i - n] + gyu - dyu);
     }
     rhs[off + i] = fid[off + i] + lambda * div;
@@ -321,30 +321,29 @@ __global__ void __launch_bounds__(kVecThreads) k_sb_post(int n, float* __restric
 }
 
 // ------------------------------------------------------------------ Chambolle-Pock dual step
-__global__ void __launch_bounds__(kVecThreads) k_cp_dual(int n, const float* __restrict__ u_cur,
-                                                         const float* __restrict__ u_prev, const float* __restrict__ yx_old,
-                                                         const float* __restrict__ yy_old, float* __restrict__ yx_new,
-                                                         float* __restrict__ yy_new, const float* __restrict__ bp,
-                                                         float* __restrict__ rhs, float tau, float sigma, float theta,
-                                                         float lambda) {
+template <typename R>
+__global__ void __launch_bounds__(kVecThreads) k_cp_dual(int n, const R* __restrict__ u_cur, const R* __restrict__ u_prev,
+                                                         const R* __restrict__ yx_old, const R* __restrict__ yy_old,
+                                                         R* __restrict__ yx_new, R* __restrict__ yy_new,
+                                                         const R* __restrict__ bp, R* __restrict__ rhs, R tau, R sigma,
+                                                         R theta, R lambda) {
   const int b = blockIdx.y;
   const int64_t L = static_cast<int64_t>(n) * n;
   const size_t off = static_cast<size_t>(b) * L;
-  const float* uc = u_cur + off;
-  const float* up = u_prev + off;
+  const R* uc = u_cur + off;
+  const R* up = u_prev + off;
   auto ubar = [&](int64_t k) { return uc[k] + theta * (uc[k] - up[k]); };
-  auto clampl = [&](float v) { return fminf(lambda, fmaxf(-lambda, v)); };
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < L;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  auto clampl = [&](R v) { return fmin(lambda, fmax(-lambda, v)); };
+  for (int64_t i = gtid(); i < L; i += gstride()) {
     const int ii = static_cast<int>(i / n), jj = static_cast<int>(i - static_cast<int64_t>(ii) * n);
-    const float c = ubar(i);
-    const float gx = jj < n - 1 ? ubar(i + 1) - c : 0.f;
-    const float gy = ii < n - 1 ? ubar(i + n) - c : 0.f;
-    const float yxn = clampl(yx_old[off + i] + sigma * gx);
-    const float yyn = clampl(yy_old[off + i] + sigma * gy);
+    const R c = ubar(i);
+    const R gx = jj < n - 1 ? ubar(i + 1) - c : R(0);
+    const R gy = ii < n - 1 ? ubar(i + n) - c : R(0);
+    const R yxn = clampl(yx_old[off + i] + sigma * gx);
+    const R yyn = clampl(yy_old[off + i] + sigma * gy);
     yx_new[off + i] = yxn;
     yy_new[off + i] = yyn;
-    float div = 0.f;
+    R div = 0;
     if (jj <= n - 2) div -= yxn;
     if (ii <= n - 2) div -= yyn;
     if (jj >= 1) div += clampl(yx_old[off + i - 1] + sigma * (c - ubar(i - 1)));
@@ -354,39 +353,32 @@ __global__ void __launch_bounds__(kVecThreads) k_cp_dual(int n, const float* __r
 }
 
 // ------------------------------------------------------------------ small helpers
-__global__ void k_scale_real(int64_t len, const float2* __restrict__ in, float* __restrict__ out, float alpha) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < len) out[i] = alpha * in[i].x;
+template <typename R>
+__global__ void k_axpby(int64_t len, R a, const R* __restrict__ x, R b, const R* __restrict__ y, R* __restrict__ out) {
+  for (int64_t i = gtid(); i < len; i += gstride()) out[i] = a * x[i] + b * y[i];
 }
 
-__global__ void k_axpby(int64_t len, float a, const float* __restrict__ x, float b, const float* __restrict__ y,
-                        float* __restrict__ out) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < len) out[i] = a * x[i] + b * y[i];
-}
-
-__global__ void __launch_bounds__(kVecThreads) k_dot(int64_t L, const float* __restrict__ x, const float* __restrict__ y,
-                                                     double* out, Reduce red) {
+template <typename R>
+__global__ void __launch_bounds__(kVecThreads) k_dot(int64_t L, const R* __restrict__ x, const R* __restrict__ y,
+                                                     Reduce red) {
   __shared__ double scratch[32];
   const int b = blockIdx.y;
   const size_t off = static_cast<size_t>(b) * L;
   double acc = 0.0;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < L;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    acc += static_cast<double>(x[off + i]) * y[off + i];
+  for (int64_t i = gtid(); i < L; i += gstride()) acc += static_cast<double>(x[off + i]) * y[off + i];
   double t0, t1;
   double* part = red.part + static_cast<size_t>(b) * MAX_PART_BLOCKS * 2;
   if (reduce2_last(acc, 0.0, part, gridDim.x, blockIdx.x, &red.sc[b].counter[3], scratch, t0, t1) &&
       threadIdx.x == 0)
-    out[b] = t0;
+    red.sc[b].dot = t0;
 }
 
-__global__ void __launch_bounds__(kVecThreads) k_leak(int64_t len, const float2* __restrict__ v, Reduce red) {
+template <typename R>
+__global__ void __launch_bounds__(kVecThreads) k_leak(int64_t len, const cplx<R>* __restrict__ v, Reduce red) {
   __shared__ double scratch[32];
   double a = 0.0, im = 0.0;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < len;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const float2 z = v[i];
+  for (int64_t i = gtid(); i < len; i += gstride()) {
+    const cplx<R> z = v[i];
     a += static_cast<double>(z.x) * z.x + static_cast<double>(z.y) * z.y;
     im += static_cast<double>(z.y) * z.y;
   }
@@ -398,27 +390,25 @@ __global__ void __launch_bounds__(kVecThreads) k_leak(int64_t len, const float2*
   }
 }
 
-__global__ void k_grad(int n, const float* __restrict__ u, float* __restrict__ gx, float* __restrict__ gy) {
+template <typename R>
+__global__ void k_grad(int n, const R* __restrict__ u, R* __restrict__ gx, R* __restrict__ gy) {
   const int64_t L = static_cast<int64_t>(n) * n;
-  const int b = blockIdx.y;
-  const size_t off = static_cast<size_t>(b) * L;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < L;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  const size_t off = static_cast<size_t>(blockIdx.y) * L;
+  for (int64_t i = gtid(); i < L; i += gstride()) {
     const int ii = static_cast<int>(i / n), jj = static_cast<int>(i % n);
-    const float c = u[off + i];
-    gx[off + i] = jj < n - 1 ? u[off + i + 1] - c : 0.f;
-    gy[off + i] = ii < n - 1 ? u[off + i + n] - c : 0.f;
+    const R c = u[off + i];
+    gx[off + i] = jj < n - 1 ? u[off + i + 1] - c : R(0);
+    gy[off + i] = ii < n - 1 ? u[off + i + n] - c : R(0);
   }
 }
 
-__global__ void k_grad_adjoint(int n, const float* __restrict__ gx, const float* __restrict__ gy, float* __restrict__ out) {
+template <typename R>
+__global__ void k_grad_adjoint(int n, const R* __restrict__ gx, const R* __restrict__ gy, R* __restrict__ out) {
   const int64_t L = static_cast<int64_t>(n) * n;
-  const int b = blockIdx.y;
-  const size_t off = static_cast<size_t>(b) * L;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < L;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  const size_t off = static_cast<size_t>(blockIdx.y) * L;
+  for (int64_t i = gtid(); i < L; i += gstride()) {
     const int ii = static_cast<int>(i / n), jj = static_cast<int>(i % n);
-    float v = 0.f;
+    R v = 0;
     if (jj >= 1) v += gx[off + i - 1];
     if (jj <= n - 2) v -= gx[off + i];
     if (ii >= 1) v += gy[off + i - n];
@@ -427,106 +417,125 @@ __global__ void k_grad_adjoint(int n, const float* __restrict__ gx, const float*
   }
 }
 
-__global__ void k_shrink(int64_t len, const float* __restrict__ x, float gamma, float* __restrict__ out) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < len) out[i] = shrinkf(x[i], gamma);
+template <typename R>
+__global__ void k_shrink(int64_t len, const R* __restrict__ x, R gamma, R* __restrict__ out) {
+  for (int64_t i = gtid(); i < len; i += gstride()) out[i] = shrinkr(x[i], gamma);
 }
 
-unsigned blocks_for(int64_t len, int threads) { return static_cast<unsigned>((len + threads - 1) / threads); }
+unsigned blocks_for(int64_t len, int threads) {
+  return static_cast<unsigned>(std::min<int64_t>((len + threads - 1) / threads, 16 * 148));
+}
 
 }  // namespace
 
-void launch_cg_update(int n, int B, const float* p, const float* ap, float* x, float* r, const SysParams& sys,
-                      int step, const Reduce& red, cudaStream_t st) {
+template <typename R>
+void launch_cg_update(int n, int B, const R* p, const R* ap, R* x, R* r, const SysParams& sys, int step,
+                      const Reduce& red, cudaStream_t st) {
   const int64_t L = static_cast<int64_t>(n) * n;
-  dim3 grid(vec_blocks(L / 4, B) , B);
-  k_cg_update<<<grid, kVecThreads, 0, st>>>(L, p, ap, x, r, sys, step, red);
+  k_cg_update<R><<<dim3(vec_blocks(L, B), B), kVecThreads, 0, st>>>(L, p, ap, x, r, sys, step, red);
   note_launch();
 }
 
-void launch_stencil(int n, int B, int rad, int euclid, const StencilCoef& coef, int mode, const float* in,
-                    const float* r_in, float* p_out, float* ap_out, const float* b, float* x_out,
-                    const SysParams& sys, int step, const Reduce& red, cudaStream_t st) {
-  (void)euclid;  // masked taps carry zero coefficients
+template <typename R>
+void launch_stencil(int n, int B, int rad, const StencilCoef& coef, int mode, const R* in, const R* r_in, R* p_out,
+                    R* ap_out, const R* b, R* x_out, const SysParams& sys, int step, const Reduce& red,
+                    cudaStream_t st) {
   dim3 grid((n + kTile - 1) / kTile, (n + kTile - 1) / kTile, B);
   switch (rad) {
-    case 1: k_stencil<1><<<grid, 256, 0, st>>>(n, coef, mode, in, r_in, p_out, ap_out, b, x_out, sys, step, red); break;
-    case 2: k_stencil<2><<<grid, 256, 0, st>>>(n, coef, mode, in, r_in, p_out, ap_out, b, x_out, sys, step, red); break;
-    case 3: k_stencil<3><<<grid, 256, 0, st>>>(n, coef, mode, in, r_in, p_out, ap_out, b, x_out, sys, step, red); break;
-    default: k_stencil<4><<<grid, 256, 0, st>>>(n, coef, mode, in, r_in, p_out, ap_out, b, x_out, sys, step, red); break;
+    case 1: k_stencil<1, R><<<grid, 256, 0, st>>>(n, coef, mode, in, r_in, p_out, ap_out, b, x_out, sys, step, red); break;
+    case 2: k_stencil<2, R><<<grid, 256, 0, st>>>(n, coef, mode, in, r_in, p_out, ap_out, b, x_out, sys, step, red); break;
+    case 3: k_stencil<3, R><<<grid, 256, 0, st>>>(n, coef, mode, in, r_in, p_out, ap_out, b, x_out, sys, step, red); break;
+    default: k_stencil<4, R><<<grid, 256, 0, st>>>(n, coef, mode, in, r_in, p_out, ap_out, b, x_out, sys, step, red); break;
   }
   note_launch();
 }
 
-void launch_cg_epilogue(int n, int B, int mode, const float* nred, const float* p, const float* b, float* ap,
-                        float* p_out, float* x_out, const SysParams& sys, int step, const Reduce& red,
-                        cudaStream_t st) {
+template <typename R>
+void launch_cg_epilogue(int n, int B, int mode, const R* nred, const R* p, const R* b, R* ap, R* p_out, R* x_out,
+                        const SysParams& sys, int step, const Reduce& red, cudaStream_t st) {
   const int64_t L = static_cast<int64_t>(n) * n;
-  dim3 grid(vec_blocks(L, B), B);
-  k_cg_epilogue<<<grid, kVecThreads, 0, st>>>(n, mode, nred, p, b, ap, p_out, x_out, sys, step, red);
+  k_cg_epilogue<R><<<dim3(vec_blocks(L, B), B), kVecThreads, 0, st>>>(n, mode, nred, p, b, ap, p_out, x_out, sys, step,
+                                                                      red);
   note_launch();
 }
 
-void launch_sb_post(int n, int B, float* mu_new, const float* mu_old, const float* bx_old,
-                    const float* by_old, float* bx_new, float* by_new, const float* fid, float* rhs,
-                    float lambda, const Reduce& red, cudaStream_t st) {
+template <typename R>
+void launch_sb_post(int n, int B, R* mu_new, const R* mu_old, const R* bx_old, const R* by_old, R* bx_new, R* by_new,
+                    const R* fid, R* rhs, double lambda, const Reduce& red, cudaStream_t st) {
   const int64_t L = static_cast<int64_t>(n) * n;
-  dim3 grid(vec_blocks(L, B), B);
-  k_sb_post<<<grid, kVecThreads, 0, st>>>(n, mu_new, mu_old, bx_old, by_old, bx_new, by_new, fid, rhs, lambda, red);
+  k_sb_post<R><<<dim3(vec_blocks(L, B), B), kVecThreads, 0, st>>>(n, mu_new, mu_old, bx_old, by_old, bx_new, by_new,
+                                                                  fid, rhs, lambda, red);
   note_launch();
 }
 
-void launch_cp_dual(int n, int B, const float* u_cur, const float* u_prev, const float* yx_old,
-                    const float* yy_old, float* yx_new, float* yy_new, const float* bp, float* rhs, float tau,
-                    float sigma, float theta, float lambda, cudaStream_t st) {
+template <typename R>
+void launch_cp_dual(int n, int B, const R* u_cur, const R* u_prev, const R* yx_old, const R* yy_old, R* yx_new,
+                    R* yy_new, const R* bp, R* rhs, double tau, double sigma, double theta, double lambda,
+                    cudaStream_t st) {
   const int64_t L = static_cast<int64_t>(n) * n;
-  dim3 grid(vec_blocks(L, B), B);
-  k_cp_dual<<<grid, kVecThreads, 0, st>>>(n, u_cur, u_prev, yx_old, yy_old, yx_new, yy_new, bp, rhs, tau, sigma,
-                                          theta, lambda);
+  k_cp_dual<R><<<dim3(vec_blocks(L, B), B), kVecThreads, 0, st>>>(n, u_cur, u_prev, yx_old, yy_old, yx_new, yy_new, bp,
+                                                                  rhs, R(tau), R(sigma), R(theta), R(lambda));
   note_launch();
 }
 
-void launch_scale_real(int64_t len, const float2* in, float* out, float alpha, cudaStream_t st) {
-  k_scale_real<<<blocks_for(len, 256), 256, 0, st>>>(len, in, out, alpha);
+template <typename R>
+void launch_axpby(int64_t len, double a, const R* x, double b, const R* y, R* out, cudaStream_t st) {
+  k_axpby<R><<<blocks_for(len, 256), 256, 0, st>>>(len, R(a), x, R(b), y, out);
   note_launch();
 }
 
-void launch_axpby(int64_t len, float a, const float* x, float b, const float* y, float* out, cudaStream_t st) {
-  k_axpby<<<blocks_for(len, 256), 256, 0, st>>>(len, a, x, b, y, out);
-  note_launch();
-}
-
-void launch_dot(int n, int B, const float* x, const float* y, double* out, const Reduce& red, cudaStream_t st) {
+template <typename R>
+void launch_dot(int n, int B, const R* x, const R* y, const Reduce& red, cudaStream_t st) {
   const int64_t L = static_cast<int64_t>(n) * n;
-  dim3 grid(vec_blocks(L, B), B);
-  k_dot<<<grid, kVecThreads, 0, st>>>(L, x, y, out, red);
+  k_dot<R><<<dim3(vec_blocks(L, B), B), kVecThreads, 0, st>>>(L, x, y, red);
   note_launch();
 }
 
-void launch_leak(int64_t len, const float2* v, const Reduce& red, cudaStream_t st) {
-  k_leak<<<vec_blocks(len, 1), kVecThreads, 0, st>>>(len, v, red);
+template <typename R>
+void launch_leak(int64_t len, const cplx<R>* v, const Reduce& red, cudaStream_t st) {
+  k_leak<R><<<vec_blocks(len, 1), kVecThreads, 0, st>>>(len, v, red);
   note_launch();
 }
 
-void launch_grad(int n, int B, const float* u, float* gx, float* gy, cudaStream_t st) {
+template <typename R>
+void launch_grad(int n, int B, const R* u, R* gx, R* gy, cudaStream_t st) {
   const int64_t L = static_cast<int64_t>(n) * n;
-  k_grad<<<dim3(vec_blocks(L, B), B), kVecThreads, 0, st>>>(n, u, gx, gy);
+  k_grad<R><<<dim3(vec_blocks(L, B), B), kVecThreads, 0, st>>>(n, u, gx, gy);
   note_launch();
 }
 
-void launch_grad_adjoint(int n, int B, const float* gx, const float* gy, float* out, cudaStream_t st) {
+template <typename R>
+void launch_grad_adjoint(int n, int B, const R* gx, const R* gy, R* out, cudaStream_t st) {
   const int64_t L = static_cast<int64_t>(n) * n;
-  k_grad_adjoint<<<dim3(vec_blocks(L, B), B), kVecThreads, 0, st>>>(n, gx, gy, out);
+  k_grad_adjoint<R><<<dim3(vec_blocks(L, B), B), kVecThreads, 0, st>>>(n, gx, gy, out);
   note_launch();
 }
 
-void launch_shrink(int64_t len, const float* x, float gamma, float* out, cudaStream_t st) {
-  k_shrink<<<blocks_for(len, 256), 256, 0, st>>>(len, x, gamma, out);
+template <typename R>
+void launch_shrink(int64_t len, const R* x, double gamma, R* out, cudaStream_t st) {
+  k_shrink<R><<<blocks_for(len, 256), 256, 0, st>>>(len, x, R(gamma), out);
   note_launch();
 }
 
-void launch_reset_scalars(SliceScalars* sc, int B, cudaStream_t st) {
-  cudaMemsetAsync(sc, 0, sizeof(SliceScalars) * B, st);
-}
+#define TOMO_INST_SOLVER(R)                                                                                        \
+  template void launch_cg_update<R>(int, int, const R*, const R*, R*, R*, const SysParams&, int, const Reduce&,     \
+                                    cudaStream_t);                                                                 \
+  template void launch_stencil<R>(int, int, int, const StencilCoef&, int, const R*, const R*, R*, R*, const R*, R*, \
+                                  const SysParams&, int, const Reduce&, cudaStream_t);                             \
+  template void launch_cg_epilogue<R>(int, int, int, const R*, const R*, const R*, R*, R*, R*, const SysParams&, int, \
+                                      const Reduce&, cudaStream_t);                                                \
+  template void launch_sb_post<R>(int, int, R*, const R*, const R*, const R*, R*, R*, const R*, R*, double,          \
+                                  const Reduce&, cudaStream_t);                                                    \
+  template void launch_cp_dual<R>(int, int, const R*, const R*, const R*, const R*, R*, R*, const R*, R*, double,    \
+                                  double, double, double, cudaStream_t);                                           \
+  template void launch_axpby<R>(int64_t, double, const R*, double, const R*, R*, cudaStream_t);                    \
+  template void launch_dot<R>(int, int, const R*, const R*, const Reduce&, cudaStream_t);                          \
+  template void launch_leak<R>(int64_t, const cplx<R>*, const Reduce&, cudaStream_t);                              \
+  template void launch_grad<R>(int, int, const R*, R*, R*, cudaStream_t);                                          \
+  template void launch_grad_adjoint<R>(int, int, const R*, const R*, R*, cudaStream_t);                            \
+  template void launch_shrink<R>(int64_t, const R*, double, R*, cudaStream_t);
+
+TOMO_INST_SOLVER(float)
+TOMO_INST_SOLVER(double)
 
 }  // namespace tomo_b200

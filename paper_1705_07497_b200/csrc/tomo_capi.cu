@@ -6,12 +6,16 @@
 // (normal_ops.cpp:321-340, solver.cpp:56-337) as sequences of sm_100a kernels, captured into
 // CUDA graphs for the iterative loops. No compute runs on the host: every hot-path call
 // requires the CUDA kernels and fails with TOMO_ERR_CUDA if they cannot run.
+//
+// An op has one precision (fp32: complex64 data, or fp64: complex128 data) fixed at
+// creation; all drivers are templates over the real type R and dispatched at the ABI.
 #include <cuda_runtime.h>
 #include <nccl.h>
 
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -57,28 +61,33 @@ void note_launch() {
     if (e_ != cudaSuccess) throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
-template <typename T>
-struct DevBuf {
-  T* p = nullptr;
-  size_t n = 0;
-  DevBuf() = default;
-  DevBuf(const DevBuf&) = delete;
-  DevBuf& operator=(const DevBuf&) = delete;
-  ~DevBuf() { release(); }
+// Raw device allocation, viewed as any element type.
+struct Raw {
+  void* p = nullptr;
+  size_t bytes = 0;
+  Raw() = default;
+  Raw(const Raw&) = delete;
+  Raw& operator=(const Raw&) = delete;
+  ~Raw() { release(); }
   void release() {
     if (p) cudaFree(p);
     p = nullptr;
-    n = 0;
+    bytes = 0;
   }
-  void ensure(size_t count) {
-    if (count <= n) return;
+  void ensure(size_t nbytes) {
+    if (nbytes <= bytes) return;
     release();
-    CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
-    n = count;
+    CK(cudaMalloc(&p, std::max<size_t>(nbytes, 16)));
+    bytes = nbytes;
   }
-  void upload(const std::vector<T>& v, cudaStream_t st = 0) {
-    ensure(v.size());
-    CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+  template <typename T>
+  void upload(const std::vector<T>& v) {
+    ensure(v.size() * sizeof(T));
+    CK(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
   }
 };
 
@@ -150,6 +159,7 @@ Geom make_geom(const tomo_geom_desc* d, const tomo_op_desc* od) {
     g.a1 = od->angle_end;
   }
   g.P = static_cast<int64_t>(g.a1 - g.a0) * g.nb;
+  if (static_cast<int64_t>(g.m) * g.m * 8 > (int64_t(1) << 40)) throw ConfigError("grid too large");
   return g;
 }
 
@@ -206,21 +216,16 @@ Plan make_plan(const Geom& g) {
 
 inline int wrapi(int idx, int m) { return idx < 0 ? idx + m : (idx >= m ? idx - m : idx); }
 
-// Allocation-level scratch of an op, sized for `cap` slices.
+constexpr int kMaxLoggedIters = 8192;
+
+// Device scratch of an op, sized for `cap` slices (element type = op precision).
 struct Scratch {
   int cap = 0;
-  DevBuf<float2> H, g, s, K;
-  DevBuf<float2> cin, cout;  // staging for host pointers / complex temporaries
-  DevBuf<float> fin, fout;
-  // solver vectors
-  DevBuf<float> r, p0, p1, ap, x, rhs, fid, mu0, mu1, bx0, bx1, by0, by1, nred, zero, u2;
-  DevBuf<double> upd_log;
-  DevBuf<SliceScalars> sc;
-  DevBuf<double> part;
-  DevBuf<double> dots;
+  Raw H, g, s, K;                 // complex
+  Raw cin, cout, fin, fout;       // staging for host pointers / temporaries
+  Raw r, p0, p1, ap, x, rhs, fid, mu0, mu1, bx0, bx1, by0, by1, nred, zero, u2;  // real vectors
+  Raw upd_log, sc, part;
 };
-
-constexpr int kMaxLoggedIters = 8192;
 
 struct GraphEntry {
   cudaGraphExec_t exec = nullptr;
@@ -235,14 +240,11 @@ struct tomo_op {
   Geom g;
   tomo_op_desc desc{};
   int device = 0;
+  bool f64 = false;
+  size_t rsz = 4;  // sizeof(R)
   int64_t nnz = 0, wt_rows = 0, wt_slots = 0;
   int nq = 0, Ppad = 0;
-  DevBuf<float> apod;
-  DevBuf<float2> tw;
-  DevBuf<int4> wcols;
-  DevBuf<float4> wvals;
-  DevBuf<uint32_t> wtchunk;
-  DevBuf<int2> wtent;
+  Raw apod, tw, wcols, wvals, wtchunk, wtent;
   Scratch sc;
   // surrogate
   int rad = 0;
@@ -257,17 +259,23 @@ struct tomo_op {
   std::map<std::string, GraphEntry> graphs;
 
   ~tomo_op() {
+    clear_graphs();
+    if (comm) ncclCommDestroy(comm);
+  }
+  void clear_graphs() {
     for (auto& kv : graphs)
       if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
-    if (comm) ncclCommDestroy(comm);
+    graphs.clear();
   }
 
   bool sharded() const { return g.a0 != 0 || g.a1 != g.A; }
+  bool surrogate() const { return desc.backend == TOMO_BACKEND_SURROGATE; }
   int64_t L() const { return static_cast<int64_t>(g.n) * g.n; }
 
-  OpDev dev(int B) {
+  template <typename R>
+  OpDev<R> dev(int B) {
     ensure_batch(B);
-    OpDev d{};
+    OpDev<R> d{};
     d.n = g.n;
     d.m = g.m;
     d.nb = g.nb;
@@ -275,51 +283,52 @@ struct tomo_op {
     d.Ppad = Ppad;
     d.nq = nq;
     d.G32 = static_cast<int>(static_cast<int64_t>(g.m) * g.m / 32);
-    d.apod = apod.p;
-    d.tw = tw.p;
-    d.w_cols = wcols.p;
-    d.w_vals = wvals.p;
-    d.wt_chunk = wtchunk.p;
-    d.wt_ent = wtent.p;
-    d.H = sc.H.p;
-    d.g = sc.g.p;
-    d.s = sc.s.p;
-    d.K = sc.K.p;
+    d.apod = apod.as<R>();
+    d.tw = tw.as<cplx<R>>();
+    d.w_cols = wcols.as<int4>();
+    d.w_vals = wvals.as<Quad<R>>();
+    d.wt_chunk = wtchunk.as<uint32_t>();
+    d.wt_ent = wtent.as<WtEnt<R>>();
+    d.H = sc.H.as<cplx<R>>();
+    d.g = sc.g.as<cplx<R>>();
+    d.s = sc.s.as<cplx<R>>();
+    d.K = sc.K.as<cplx<R>>();
     return d;
   }
 
   void ensure_batch(int B) {
     if (B <= sc.cap) return;
-    const size_t m = g.m, n = g.n;
-    sc.H.ensure(B * m * n);
-    sc.g.ensure(B * m * m);
-    sc.s.ensure(B * static_cast<size_t>(g.P));
-    sc.K.ensure(B * n * m);
-    sc.sc.ensure(B);
+    const size_t m = g.m, n = g.n, cz = 2 * rsz;
+    sc.H.ensure(B * m * n * cz);
+    sc.g.ensure(B * m * m * cz);
+    sc.s.ensure(B * static_cast<size_t>(g.P) * cz);
+    sc.K.ensure(B * n * m * cz);
+    sc.sc.ensure(sizeof(SliceScalars) * B);
     CK(cudaMemset(sc.sc.p, 0, sizeof(SliceScalars) * B));
-    sc.part.ensure(static_cast<size_t>(B) * MAX_PART_BLOCKS * 2);
-    sc.dots.ensure(B * 4);
-    const size_t vl = static_cast<size_t>(B) * n * n;
+    sc.part.ensure(sizeof(double) * static_cast<size_t>(B) * MAX_PART_BLOCKS * 2);
+    const size_t vl = static_cast<size_t>(B) * n * n * rsz;
     for (auto* v : {&sc.r, &sc.p0, &sc.p1, &sc.ap, &sc.x, &sc.rhs, &sc.fid, &sc.mu0, &sc.mu1, &sc.bx0, &sc.bx1,
                     &sc.by0, &sc.by1, &sc.nred, &sc.zero, &sc.u2})
       v->ensure(vl);
-    CK(cudaMemset(sc.zero.p, 0, sizeof(float) * vl));
-    sc.upd_log.ensure(static_cast<size_t>(B) * kMaxLoggedIters);
+    CK(cudaMemset(sc.zero.p, 0, vl));
+    sc.upd_log.ensure(sizeof(double) * static_cast<size_t>(B) * kMaxLoggedIters);
     sc.cap = B;
-    for (auto& kv : graphs)
-      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
-    graphs.clear();  // buffers moved
+    clear_graphs();  // buffers moved
   }
 
-  Reduce red() { return Reduce{sc.sc.p, sc.part.p}; }
+  Reduce red() { return Reduce{sc.sc.as<SliceScalars>(), sc.part.as<double>()}; }
+  SliceScalars* scal() { return sc.sc.as<SliceScalars>(); }
 };
 
 namespace tomo_b200 {
 namespace {
 
 // ------------------------------------------------------------------------------------------
-// Operator construction
+// Operator construction: W as SELL-32 ELL (row j, entry e = a*w + b -> node iy*m + ix, value
+// wx[a]*wy[b], nufft.cpp:185-200), W^T as SELL-32 over consecutive grid nodes (entries sorted
+// by sample index: the exact transpose of the same products, spread nufft.cpp:142-157).
 // ------------------------------------------------------------------------------------------
+template <typename R>
 void build_tables(tomo_op* op) {
   const Geom& g = op->g;
   const Plan pl = make_plan(g);
@@ -330,11 +339,10 @@ void build_tables(tomo_op* op) {
   const int m = g.m;
   op->nnz = g.P * w2;
 
-  // W as SELL-32 ELL: row j, entry e = a*w + b -> node (iy*m + ix), value wx[a]*wy[b]
   std::vector<int4> cols(static_cast<size_t>(op->Ppad) * op->nq);
-  std::vector<float4> vals(cols.size());
+  std::vector<Quad<R>> vals(cols.size());
   std::vector<int32_t> rc(w2pad);
-  std::vector<float> rv(w2pad);
+  std::vector<double> rv(w2pad);
   std::vector<int> cnt(static_cast<size_t>(m) * m, 0);
   for (int64_t j = 0; j < op->Ppad; ++j) {
     if (j < g.P) {
@@ -345,32 +353,31 @@ void build_tables(tomo_op* op) {
         for (int b = 0; b < w; ++b) {
           const int iy = wrapi(pl.mjy[j] + g.lo + b, m);
           rc[a * w + b] = iy * m + ix;
-          rv[a * w + b] = static_cast<float>(wx[a] * wy[b]);
+          rv[a * w + b] = wx[a] * wy[b];
           cnt[static_cast<size_t>(iy) * m + ix]++;
         }
       }
       for (int e = w2; e < w2pad; ++e) {
         rc[e] = rc[0];
-        rv[e] = 0.f;
+        rv[e] = 0.0;
       }
     } else {
       std::fill(rc.begin(), rc.end(), 0);
-      std::fill(rv.begin(), rv.end(), 0.f);
+      std::fill(rv.begin(), rv.end(), 0.0);
     }
     const int64_t blk = j / 32, lane = j % 32;
     for (int q = 0; q < op->nq; ++q) {
       const size_t o = (static_cast<size_t>(blk) * op->nq + q) * 32 + lane;
       cols[o] = make_int4(rc[4 * q], rc[4 * q + 1], rc[4 * q + 2], rc[4 * q + 3]);
-      vals[o] = make_float4(rv[4 * q], rv[4 * q + 1], rv[4 * q + 2], rv[4 * q + 3]);
+      for (int k = 0; k < 4; ++k) vals[o].v[k] = static_cast<R>(rv[4 * q + k]);
     }
   }
 
-  // W^T: CSR by node (sorted by sample index), then SELL-32 over consecutive nodes.
   const int64_t G = static_cast<int64_t>(m) * m;
   std::vector<int64_t> off(G + 1, 0);
   for (int64_t i = 0; i < G; ++i) off[i + 1] = off[i] + cnt[i];
   std::vector<int32_t> tj(off[G]);
-  std::vector<float> tv(off[G]);
+  std::vector<R> tv(off[G]);
   std::vector<int64_t> fillp(off.begin(), off.end() - 1);
   for (int64_t j = 0; j < g.P; ++j) {
     const int64_t blk = j / 32, lane = j % 32;
@@ -378,44 +385,42 @@ void build_tables(tomo_op* op) {
       const int q = e / 4, c = e % 4;
       const size_t o = (static_cast<size_t>(blk) * op->nq + q) * 32 + lane;
       const int node = (&cols[o].x)[c];
-      const float val = (&vals[o].x)[c];
       const int64_t k = fillp[node]++;
       tj[k] = static_cast<int32_t>(j);
-      tv[k] = val;
+      tv[k] = vals[o].v[c];
     }
   }
   const int64_t G32 = G / 32;
   std::vector<uint32_t> chunk(G32 + 1, 0);
   int64_t touched = 0;
   for (int64_t bk = 0; bk < G32; ++bk) {
-    int L = 0;
+    int Lb = 0;
     for (int l = 0; l < 32; ++l) {
       const int c = cnt[bk * 32 + l];
-      L = std::max(L, c);
+      Lb = std::max(Lb, c);
       touched += c > 0;
     }
-    if (static_cast<uint64_t>(chunk[bk]) + L > 0xffffffffull / 32) throw ConfigError("W^T too large");
-    chunk[bk + 1] = chunk[bk] + L;
+    if (static_cast<uint64_t>(chunk[bk]) + Lb > 0xffffffffull / 32) throw ConfigError("W^T too large");
+    chunk[bk + 1] = chunk[bk] + Lb;
   }
   op->wt_rows = touched;
   op->wt_slots = static_cast<int64_t>(chunk[G32]) * 32;
-  std::vector<int2> ent(std::max<int64_t>(op->wt_slots, 1));
+  std::vector<WtEnt<R>> ent(std::max<int64_t>(op->wt_slots, 1));
   for (int64_t bk = 0; bk < G32; ++bk) {
-    const int L = static_cast<int>(chunk[bk + 1] - chunk[bk]);
+    const int Lb = static_cast<int>(chunk[bk + 1] - chunk[bk]);
     for (int l = 0; l < 32; ++l) {
       const int64_t node = bk * 32 + l;
       const int c = cnt[node];
       int lastj = c > 0 ? tj[off[node]] : 0;
-      for (int k = 0; k < L; ++k) {
-        int2 e;
+      for (int k = 0; k < Lb; ++k) {
+        WtEnt<R> e{};
         if (k < c) {
           lastj = tj[off[node] + k];
-          e.x = lastj;
-          float f = tv[off[node] + k];
-          std::memcpy(&e.y, &f, 4);
+          e.j = lastj;
+          e.w = tv[off[node] + k];
         } else {
-          e.x = lastj;
-          e.y = 0;  // +0.0f
+          e.j = lastj;  // padding: re-read a sample already in cache, weight 0
+          e.w = R(0);
         }
         ent[(static_cast<size_t>(chunk[bk]) + k) * 32 + l] = e;
       }
@@ -423,16 +428,17 @@ void build_tables(tomo_op* op) {
   }
 
   // deapodisation a[t]/m (nufft.cpp:204-227 with the 1/m per-axis FFT scale folded in)
-  std::vector<float> apod(g.n);
+  std::vector<R> apod(g.n);
   const double root = std::sqrt(M_PI / g.tau);
   for (int t = 0; t < g.n; ++t) {
     const double k = t - g.n / 2;
-    apod[t] = static_cast<float>(root * std::exp(k * k * g.tau) / m);
+    apod[t] = static_cast<R>(root * std::exp(k * k * g.tau) / m);
   }
-  std::vector<float2> tw(m);
+  std::vector<cplx<R>> tw(m);
   for (int k = 0; k < m; ++k) {
     const double ang = -2.0 * M_PI * static_cast<double>(k) / m;
-    tw[k] = make_float2(static_cast<float>(std::cos(ang)), static_cast<float>(std::sin(ang)));
+    tw[k].x = static_cast<R>(std::cos(ang));
+    tw[k].y = static_cast<R>(std::sin(ang));
   }
   op->wcols.upload(cols);
   op->wvals.upload(vals);
@@ -440,171 +446,161 @@ void build_tables(tomo_op* op) {
   op->wtent.upload(ent);
   op->apod.upload(apod);
   op->tw.upload(tw);
-  CK(cudaStreamSynchronize(0));
 }
 
 // ------------------------------------------------------------------------------------------
 // Pipelines (all device pointers, stream-ordered)
 // ------------------------------------------------------------------------------------------
-void allreduce(tomo_op* op, float* buf, size_t count, cudaStream_t st) {
+template <typename R>
+void allreduce(tomo_op* op, R* buf, size_t count, cudaStream_t st) {
   if (!op->sharded()) return;
   if (op->comm) {
-    const ncclResult_t r = ncclAllReduce(buf, buf, count, ncclFloat32, ncclSum, op->comm, st);
+    const ncclResult_t r = ncclAllReduce(buf, buf, count, sizeof(R) == 8 ? ncclFloat64 : ncclFloat32, ncclSum,
+                                         op->comm, st);
     if (r != ncclSuccess) throw CudaError(std::string("ncclAllReduce: ") + ncclGetErrorString(r));
   } else if (op->ar_fn) {
-    if (op->ar_fn(buf, count, st, op->ar_user) != 0) throw CudaError("allreduce hook failed");
+    if (op->ar_fn(buf, count, sizeof(R) == 8 ? TOMO_F64 : TOMO_F32, st, op->ar_user) != 0)
+      throw CudaError("allreduce hook failed");
   } else {
     throw ConfigError("sharded op needs an all-reduce (tomo_op_attach_nccl / tomo_op_set_allreduce)");
   }
 }
 
-void type2(tomo_op* op, int B, const void* in, bool complex_in, const PUpd& pu, float2* samples_out,
+template <typename R>
+void type2(tomo_op* op, int B, const void* in, bool complex_in, const PUpd<R>& pu, cplx<R>* samples_out,
            const SliceScalars* skip, cudaStream_t st) {
-  OpDev d = op->dev(B);
-  launch_t2_rows(d, B, in, complex_in, pu, st);
-  launch_t2_cols(d, B, skip, st);
-  launch_w(d, B, d.g, samples_out ? samples_out : d.s, skip, st);
+  OpDev<R> d = op->dev<R>(B);
+  launch_t2_rows<R>(d, B, in, complex_in, pu, st);
+  launch_t2_cols<R>(d, B, skip, st);
+  launch_w<R>(d, B, d.g, samples_out ? samples_out : d.s, skip, st);
 }
 
-void type1(tomo_op* op, int B, const float2* samples, const PbEpi& e, const SliceScalars* skip, cudaStream_t st) {
-  OpDev d = op->dev(B);
-  if (samples) d.s = const_cast<float2*>(samples);
-  launch_wt_rows(d, B, skip, st);
-  launch_t1_rows(d, B, e, st);
+template <typename R>
+void type1(tomo_op* op, int B, const cplx<R>* samples, const PbEpi<R>& e, const SliceScalars* skip, cudaStream_t st) {
+  OpDev<R> d = op->dev<R>(B);
+  if (samples) d.s = const_cast<cplx<R>*>(samples);
+  launch_wt_rows<R>(d, B, skip, st);
+  launch_t1_rows<R>(d, B, e, st);
 }
 
-PbEpi plain_epi(int mode, float scale) {
-  PbEpi e{};
+template <typename R>
+PbEpi<R> plain_epi(int mode, double scale) {
+  PbEpi<R> e{};
   e.mode = mode;
-  e.scale = scale;
+  e.scale = static_cast<R>(scale);
   return e;
 }
 
 // Re(N u) (or N u complex) for the W/W^T backend, incl. the cross-rank sum when sharded.
-void normal_direct(tomo_op* op, int B, const void* in, bool cplx, void* out, cudaStream_t st) {
-  PUpd pu{};
-  type2(op, B, in, cplx, pu, nullptr, nullptr, st);
-  PbEpi e = plain_epi(cplx ? PB_COMPLEX : PB_REAL, 1.0f);
-  if (cplx)
-    e.out_c = static_cast<float2*>(out);
+template <typename R>
+void normal_direct(tomo_op* op, int B, const void* in, bool cplx_io, void* out, cudaStream_t st) {
+  PUpd<R> pu{};
+  type2<R>(op, B, in, cplx_io, pu, nullptr, nullptr, st);
+  PbEpi<R> e = plain_epi<R>(cplx_io ? PB_COMPLEX : PB_REAL, 1.0);
+  if (cplx_io)
+    e.out_c = static_cast<cplx<R>*>(out);
   else
-    e.out_r = static_cast<float*>(out);
-  type1(op, B, nullptr, e, nullptr, st);
-  allreduce(op, static_cast<float*>(out), static_cast<size_t>(B) * op->L() * (cplx ? 2 : 1), st);
+    e.out_r = static_cast<R*>(out);
+  type1<R>(op, B, nullptr, e, nullptr, st);
+  allreduce<R>(op, static_cast<R*>(out), static_cast<size_t>(B) * op->L() * (cplx_io ? 2 : 1), st);
 }
 
-SysParams sysp(double alpha, double lambda, double shift, double tol) {
-  SysParams s;
-  s.alpha = static_cast<float>(alpha);
-  s.lambda = static_cast<float>(lambda);
-  s.shift = static_cast<float>(shift);
-  s.tol = tol;
-  return s;
-}
-
-bool surrogate(const tomo_op* op) { return op->desc.backend == TOMO_BACKEND_SURROGATE; }
-
-// Plain system apply out = alpha*B(u) + lambda*K'K u + shift*u (used by Lanczos).
-void system_apply(tomo_op* op, int B, const SysParams& s, const float* in, float* out, cudaStream_t st) {
-  if (surrogate(op)) {
-    launch_stencil(op->g.n, B, op->rad, op->desc.euclidean, op->coef, 2, in, nullptr, nullptr, out, nullptr,
-                   nullptr, s, 0, op->red(), st);
-    return;
-  }
-  throw ConfigError("system_apply: only the surrogate system is applied standalone");
-}
+SysParams sysp(double alpha, double lambda, double shift, double tol) { return SysParams{alpha, lambda, shift, tol}; }
 
 // cg_solve (solver.cpp:56-95) for B slices: rhs, x0 -> x (device, B x L each).
-void cg_run(tomo_op* op, int B, const SysParams& s, const float* rhs, const float* x0, float* x, int steps,
-            cudaStream_t st) {
+template <typename R>
+void cg_run(tomo_op* op, int B, const SysParams& s, const R* rhs, const R* x0, R* x, int steps, cudaStream_t st) {
   const int n = op->g.n;
   const int64_t L = op->L();
   Scratch& S = op->sc;
   Reduce red = op->red();
-  const SliceScalars* skip = op->sc.sc.p;
-  if (surrogate(op)) {
-    launch_stencil(n, B, op->rad, op->desc.euclidean, op->coef, 1, x0, nullptr, S.p0.p, S.r.p, rhs, x, s, 0, red,
-                   st);
-    float* cur = S.p0.p;
-    float* other = S.p1.p;
+  const SliceScalars* skip = op->scal();
+  R* r = S.r.as<R>();
+  R* p0 = S.p0.as<R>();
+  R* p1 = S.p1.as<R>();
+  R* ap = S.ap.as<R>();
+  if (op->surrogate()) {
+    launch_stencil<R>(n, B, op->rad, op->coef, 1, x0, nullptr, p0, r, rhs, x, s, 0, red, st);
+    R* cur = p0;
+    R* other = p1;
     for (int k = 0; k < steps; ++k) {
       if (k == 0) {
-        launch_stencil(n, B, op->rad, op->desc.euclidean, op->coef, 0, cur, S.r.p, cur, S.ap.p, nullptr, nullptr,
-                       s, k, red, st);
+        launch_stencil<R>(n, B, op->rad, op->coef, 0, cur, r, cur, ap, nullptr, nullptr, s, k, red, st);
       } else {
-        launch_stencil(n, B, op->rad, op->desc.euclidean, op->coef, 0, cur, S.r.p, other, S.ap.p, nullptr,
-                       nullptr, s, k, red, st);
+        launch_stencil<R>(n, B, op->rad, op->coef, 0, cur, r, other, ap, nullptr, nullptr, s, k, red, st);
         std::swap(cur, other);
       }
-      launch_cg_update(n, B, cur, S.ap.p, x, S.r.p, s, k, red, st);
+      launch_cg_update<R>(n, B, cur, ap, x, r, s, k, red, st);
     }
     return;
   }
   // W / W^T backend: init r = b - A x0, p = r, x = x0
   const bool shard = op->sharded();
+  R* nred = S.nred.as<R>();
   {
-    PUpd pu{};
+    PUpd<R> pu{};
     pu.red = red;
-    type2(op, B, x0, false, pu, nullptr, nullptr, st);
+    type2<R>(op, B, x0, false, pu, nullptr, nullptr, st);
     if (!shard) {
-      PbEpi e = plain_epi(PB_CG_INIT, s.alpha);
+      PbEpi<R> e = plain_epi<R>(PB_CG_INIT, s.alpha);
       e.p = x0;
       e.b = rhs;
-      e.ap = S.r.p;
-      e.p_out = S.p0.p;
+      e.ap = r;
+      e.p_out = p0;
       e.x_out = x;
       e.sys = s;
       e.step = 0;
       e.red = red;
-      type1(op, B, nullptr, e, nullptr, st);
+      type1<R>(op, B, nullptr, e, nullptr, st);
     } else {
-      PbEpi e = plain_epi(PB_REAL, s.alpha);
-      e.out_r = S.nred.p;
-      type1(op, B, nullptr, e, nullptr, st);
-      allreduce(op, S.nred.p, static_cast<size_t>(B) * L, st);
-      launch_cg_epilogue(n, B, 1, S.nred.p, x0, rhs, S.r.p, S.p0.p, x, s, 0, red, st);
+      PbEpi<R> e = plain_epi<R>(PB_REAL, s.alpha);
+      e.out_r = nred;
+      type1<R>(op, B, nullptr, e, nullptr, st);
+      allreduce<R>(op, nred, static_cast<size_t>(B) * L, st);
+      launch_cg_epilogue<R>(n, B, 1, nred, x0, rhs, r, p0, x, s, 0, red, st);
     }
   }
   for (int k = 0; k < steps; ++k) {
-    PUpd pu{};
+    PUpd<R> pu{};
     pu.enabled = 1;
-    pu.r = S.r.p;
-    pu.p = S.p0.p;
+    pu.r = r;
+    pu.p = p0;
     pu.step = k;
     pu.red = red;
-    type2(op, B, S.p0.p, false, pu, nullptr, skip, st);
+    type2<R>(op, B, p0, false, pu, nullptr, skip, st);
     if (!shard) {
-      PbEpi e = plain_epi(PB_CG_STEP, s.alpha);
-      e.p = S.p0.p;
-      e.ap = S.ap.p;
+      PbEpi<R> e = plain_epi<R>(PB_CG_STEP, s.alpha);
+      e.p = p0;
+      e.ap = ap;
       e.sys = s;
       e.step = k;
       e.red = red;
-      type1(op, B, nullptr, e, skip, st);
+      type1<R>(op, B, nullptr, e, skip, st);
     } else {
-      PbEpi e = plain_epi(PB_REAL, s.alpha);
-      e.out_r = S.nred.p;
-      type1(op, B, nullptr, e, skip, st);
-      allreduce(op, S.nred.p, static_cast<size_t>(B) * L, st);
-      launch_cg_epilogue(n, B, 0, S.nred.p, S.p0.p, nullptr, S.ap.p, nullptr, nullptr, s, k, red, st);
+      PbEpi<R> e = plain_epi<R>(PB_REAL, s.alpha);
+      e.out_r = nred;
+      type1<R>(op, B, nullptr, e, skip, st);
+      allreduce<R>(op, nred, static_cast<size_t>(B) * L, st);
+      launch_cg_epilogue<R>(n, B, 0, nred, p0, nullptr, ap, nullptr, nullptr, s, k, red, st);
     }
-    launch_cg_update(n, B, S.p0.p, S.ap.p, x, S.r.p, s, k, red, st);
+    launch_cg_update<R>(n, B, p0, ap, x, r, s, k, red, st);
   }
 }
 
 // Back-projection alpha*Re(F_NU f) (solver.cpp:200-213), optionally density weighted.
-void backproject(tomo_op* op, int B, double alpha, bool weighted, const float2* f, float* out, cudaStream_t st) {
-  const float2* src = f;
+template <typename R>
+void backproject(tomo_op* op, int B, double alpha, bool weighted, const cplx<R>* f, R* out, cudaStream_t st) {
+  const cplx<R>* src = f;
   if (weighted) {
-    OpDev d = op->dev(B);
-    CK(cudaMemcpyAsync(d.s, f, sizeof(float2) * B * op->g.P, cudaMemcpyDeviceToDevice, st));
-    launch_weight_samples(d.s, B, static_cast<int>(op->g.P), op->g.nb, op->g.a0, st);
+    OpDev<R> d = op->dev<R>(B);
+    CK(cudaMemcpyAsync(d.s, f, sizeof(cplx<R>) * B * op->g.P, cudaMemcpyDeviceToDevice, st));
+    launch_weight_samples<R>(d.s, B, static_cast<int>(op->g.P), op->g.nb, st);
     src = d.s;
   }
-  PbEpi e = plain_epi(PB_REAL, static_cast<float>(alpha));
+  PbEpi<R> e = plain_epi<R>(PB_REAL, alpha);
   e.out_r = out;
-  type1(op, B, src, e, nullptr, st);
-  allreduce(op, out, static_cast<size_t>(B) * op->L(), st);
+  type1<R>(op, B, src, e, nullptr, st);
+  allreduce<R>(op, out, static_cast<size_t>(B) * op->L(), st);
 }
 
 // ---- graph capture of a solver loop -------------------------------------------------------
@@ -679,6 +675,16 @@ double tridiag_min(const std::vector<double>& a, const std::vector<double>& b) {
   return 0.5 * (lo + hi);
 }
 
+template <typename R>
+double device_dot(tomo_op* op, const R* x, const R* y, cudaStream_t st) {
+  launch_dot<R>(op->g.n, 1, x, y, op->red(), st);
+  double v = 0.0;
+  CK(cudaMemcpyAsync(&v, &op->scal()[0].dot, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return v;
+}
+
+template <typename R>
 double surrogate_sigma(tomo_op* op, double alpha, double lambda, cudaStream_t st) {
   auto key = std::make_pair(alpha, lambda);
   auto it = op->sigma_cache.find(key);
@@ -696,36 +702,28 @@ double surrogate_sigma(tomo_op* op, double alpha, double lambda, cudaStream_t st
     nn += e * e;
   }
   nn = std::sqrt(nn);
-  std::vector<float> vf(L);
-  for (int64_t i = 0; i < L; ++i) vf[i] = static_cast<float>(v[i] / nn);
-  float* vcur = S.x.p;
-  float* vprev = S.p0.p;
-  float* w = S.ap.p;
-  CK(cudaMemcpyAsync(vcur, vf.data(), sizeof(float) * L, cudaMemcpyHostToDevice, st));
-  CK(cudaMemsetAsync(vprev, 0, sizeof(float) * L, st));
+  std::vector<R> vf(L);
+  for (int64_t i = 0; i < L; ++i) vf[i] = static_cast<R>(v[i] / nn);
+  R* vcur = S.x.as<R>();
+  R* vprev = S.p0.as<R>();
+  R* w = S.ap.as<R>();
+  CK(cudaMemcpyAsync(vcur, vf.data(), sizeof(R) * L, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(vprev, 0, sizeof(R) * L, st));
   const SysParams sp = sysp(alpha, lambda, 0.0, 0.0);
   std::vector<double> alphas, betas;
   double beta = 0.0, extreme = 0.0;
-  double host_dot = 0.0;
-  Reduce red = op->red();
   for (int itr = 0; itr < 40; ++itr) {
-    system_apply(op, 1, sp, vcur, w, st);
-    launch_dot(n, 1, vcur, w, S.dots.p, red, st);
-    CK(cudaMemcpyAsync(&host_dot, S.dots.p, sizeof(double), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    const double a = host_dot;
+    launch_stencil<R>(n, 1, op->rad, op->coef, 2, vcur, nullptr, nullptr, w, nullptr, nullptr, sp, 0, op->red(), st);
+    const double a = device_dot<R>(op, vcur, w, st);
     alphas.push_back(a);
-    launch_axpby(L, 1.0f, w, static_cast<float>(-a), vcur, w, st);
-    launch_axpby(L, 1.0f, w, static_cast<float>(-beta), vprev, w, st);
-    launch_dot(n, 1, w, w, S.dots.p, red, st);
-    CK(cudaMemcpyAsync(&host_dot, S.dots.p, sizeof(double), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    beta = std::sqrt(host_dot);
+    launch_axpby<R>(L, 1.0, w, -a, vcur, w, st);
+    launch_axpby<R>(L, 1.0, w, -beta, vprev, w, st);
+    beta = std::sqrt(device_dot<R>(op, w, w, st));
     extreme = tridiag_min(alphas, betas);
     if (beta < 1e-12) break;
     betas.push_back(beta);
-    std::swap(vprev, vcur);  // vprev <- v
-    launch_axpby(L, static_cast<float>(1.0 / beta), w, 0.0f, w, vcur, st);  // v <- w / beta
+    std::swap(vprev, vcur);                                    // vprev <- v
+    launch_axpby<R>(L, 1.0 / beta, w, 0.0, w, vcur, st);       // v <- w / beta
   }
   const double sigma = 1.2 * std::max(0.0, -extreme);
   op->sigma_cache[key] = sigma;
@@ -734,6 +732,7 @@ double surrogate_sigma(tomo_op* op, double alpha, double lambda, cudaStream_t st
 
 // Surrogate stencil: centre response of the density-weighted normal operator
 // (normal_ops.cpp:232-264), computed through the GPU W/W^T path, symmetrised on the host.
+template <typename R>
 void build_stencil(tomo_op* op, cudaStream_t st) {
   const int n = op->g.n, r = op->desc.surrogate_r;
   if (r < 1 || r > 4 || r >= n / 2) throw ConfigError("build_surrogate: radius out of range (GPU supports 1..4)");
@@ -742,20 +741,21 @@ void build_stencil(tomo_op* op, cudaStream_t st) {
   const int64_t L = op->L();
   op->ensure_batch(1);
   Scratch& S = op->sc;
-  S.cin.ensure(L);
-  S.fout.ensure(L);
-  std::vector<float2> delta(L, make_float2(0.f, 0.f));
-  delta[static_cast<int64_t>(n / 2) * n + n / 2] = make_float2(1.f, 0.f);
-  CK(cudaMemcpyAsync(S.cin.p, delta.data(), sizeof(float2) * L, cudaMemcpyHostToDevice, st));
-  OpDev d = op->dev(1);
-  PUpd pu{};
-  type2(op, 1, S.cin.p, true, pu, d.s, nullptr, st);
-  launch_weight_samples(d.s, 1, static_cast<int>(op->g.P), op->g.nb, op->g.a0, st);
-  PbEpi e = plain_epi(PB_REAL, 1.0f);
-  e.out_r = S.fout.p;
-  type1(op, 1, d.s, e, nullptr, st);
-  std::vector<float> resp(L);
-  CK(cudaMemcpyAsync(resp.data(), S.fout.p, sizeof(float) * L, cudaMemcpyDeviceToHost, st));
+  S.cin.ensure(L * sizeof(cplx<R>));
+  S.fout.ensure(L * sizeof(R));
+  std::vector<cplx<R>> delta(L);
+  for (auto& z : delta) z.x = z.y = R(0);
+  delta[static_cast<int64_t>(n / 2) * n + n / 2].x = R(1);
+  CK(cudaMemcpyAsync(S.cin.p, delta.data(), sizeof(cplx<R>) * L, cudaMemcpyHostToDevice, st));
+  OpDev<R> d = op->dev<R>(1);
+  PUpd<R> pu{};
+  type2<R>(op, 1, S.cin.p, true, pu, d.s, nullptr, st);
+  launch_weight_samples<R>(d.s, 1, static_cast<int>(op->g.P), op->g.nb, st);
+  PbEpi<R> e = plain_epi<R>(PB_REAL, 1.0);
+  e.out_r = S.fout.as<R>();
+  type1<R>(op, 1, d.s, e, nullptr, st);
+  std::vector<R> resp(L);
+  CK(cudaMemcpyAsync(resp.data(), S.fout.p, sizeof(R) * L, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   const int side = 2 * r + 1;
   for (int di = -r; di <= r; ++di)
@@ -765,58 +765,89 @@ void build_stencil(tomo_op* op, cudaStream_t st) {
       double v = 0.5 * (fwd + bwd);
       op->stencil64[(di + r) * side + (dj + r)] = v;
       if (op->desc.euclidean && di * di + dj * dj > r * r) v = 0.0;
-      op->coef.c[(di + r) * side + (dj + r)] = static_cast<float>(v);
+      op->coef.c[(di + r) * side + (dj + r)] = v;
     }
 }
 
+template <typename R>
 double leak_probe(tomo_op* op, cudaStream_t st) {
   if (op->leak >= 0.0) return op->leak;
   const int64_t L = op->L();
   op->ensure_batch(1);
   Scratch& S = op->sc;
-  S.cin.ensure(L);
-  S.cout.ensure(L);
-  std::vector<float2> ones(L, make_float2(1.f, 0.f));
-  CK(cudaMemcpyAsync(S.cin.p, ones.data(), sizeof(float2) * L, cudaMemcpyHostToDevice, st));
-  normal_direct(op, 1, S.cin.p, true, S.cout.p, st);
-  launch_leak(L, S.cout.p, op->red(), st);
+  S.cin.ensure(L * sizeof(cplx<R>));
+  S.cout.ensure(L * sizeof(cplx<R>));
+  std::vector<cplx<R>> ones(L);
+  for (auto& z : ones) {
+    z.x = R(1);
+    z.y = R(0);
+  }
+  CK(cudaMemcpyAsync(S.cin.p, ones.data(), sizeof(cplx<R>) * L, cudaMemcpyHostToDevice, st));
+  normal_direct<R>(op, 1, S.cin.p, true, S.cout.p, st);
+  launch_leak<R>(L, S.cout.as<cplx<R>>(), op->red(), st);
   SliceScalars h{};
-  CK(cudaMemcpyAsync(&h, op->sc.sc.p, sizeof(SliceScalars), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&h, op->scal(), sizeof(SliceScalars), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   op->leak = h.leak_den > 0.0 ? std::sqrt(h.leak_num) / std::sqrt(h.leak_den) : 0.0;
   return op->leak;
 }
 
 // ---- host/device staging for the C ABI -----------------------------------------------------
-struct InArg {
-  const void* dev = nullptr;
-};
-
-template <typename T>
-const T* stage_in(const void* p, size_t count, DevBuf<T>& buf, cudaStream_t st) {
+const void* stage_in(const void* p, size_t bytes, Raw& buf, cudaStream_t st) {
   if (!p) return nullptr;
-  if (is_device_ptr(p)) return static_cast<const T*>(p);
-  buf.ensure(count);
-  CK(cudaMemcpyAsync(buf.p, p, sizeof(T) * count, cudaMemcpyHostToDevice, st));
+  if (is_device_ptr(p)) return p;
+  buf.ensure(bytes);
+  CK(cudaMemcpyAsync(buf.p, p, bytes, cudaMemcpyHostToDevice, st));
   return buf.p;
 }
+
+// Output either straight into a device pointer, or into `buf` and back to the host pointer.
+struct OutArg {
+  void* user;
+  void* dev;
+  size_t bytes;
+  bool host;
+  OutArg(void* u, size_t b, Raw& buf) : user(u), bytes(b) {
+    host = !is_device_ptr(u);
+    if (host) {
+      buf.ensure(b);
+      dev = buf.p;
+    } else {
+      dev = u;
+    }
+  }
+  void finish(cudaStream_t st) {
+    if (host) {
+      CK(cudaMemcpyAsync(user, dev, bytes, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+    }
+  }
+};
 
 int fail(const std::exception& e, int code) {
   g_err = e.what();
   return code;
 }
 
+template <typename F>
+void with_prec(tomo_op* op, F&& f) {
+  if (op->f64)
+    f(double{});
+  else
+    f(float{});
+}
+
 }  // namespace
 }  // namespace tomo_b200
 
 #define TOMO_TRY try {
-#define TOMO_CATCH                                                      \
-  return TOMO_OK;                                                       \
-  }                                                                     \
-  catch (const tomo_b200::ConfigError& e) { return fail(e, TOMO_ERR_CONFIG); }     \
+#define TOMO_CATCH                                                                   \
+  return TOMO_OK;                                                                    \
+  }                                                                                  \
+  catch (const tomo_b200::ConfigError& e) { return fail(e, TOMO_ERR_CONFIG); }       \
   catch (const tomo_b200::NumericalError& e) { return fail(e, TOMO_ERR_NUMERICAL); } \
-  catch (const tomo_b200::CudaError& e) { return fail(e, TOMO_ERR_CUDA); }         \
-  catch (const std::bad_alloc& e) { return fail(e, TOMO_ERR_CUDA); }               \
+  catch (const tomo_b200::CudaError& e) { return fail(e, TOMO_ERR_CUDA); }           \
+  catch (const std::bad_alloc& e) { return fail(e, TOMO_ERR_CUDA); }                 \
   catch (const std::exception& e) { return fail(e, TOMO_ERR_CONFIG); }
 
 static cudaStream_t S_(void* s) { return static_cast<cudaStream_t>(s); }
@@ -840,6 +871,7 @@ int tomo_op_create(const tomo_geom_desc* geom, const tomo_op_desc* desc, tomo_op
   if (dd.max_batch < 1) dd.max_batch = 1;
   if (dd.backend != TOMO_BACKEND_DIRECT && dd.backend != TOMO_BACKEND_SURROGATE)
     throw ConfigError("unknown backend (the Gram 'fused' backend is not built on the GPU)");
+  if (dd.precision != TOMO_F32 && dd.precision != TOMO_F64) throw ConfigError("unknown precision");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
     cudaGetLastError();
@@ -850,10 +882,16 @@ int tomo_op_create(const tomo_geom_desc* geom, const tomo_op_desc* desc, tomo_op
   op->g = make_geom(geom, &dd);
   op->desc = dd;
   op->device = dd.device;
+  op->f64 = dd.precision == TOMO_F64;
+  op->rsz = op->f64 ? 8 : 4;
   DeviceGuard dg(op->device);
-  build_tables(op.get());
-  op->ensure_batch(dd.max_batch);
-  if (dd.backend == TOMO_BACKEND_SURROGATE) build_stencil(op.get(), 0);
+  tomo_op* o = op.get();
+  with_prec(o, [&](auto tag) {
+    using R = decltype(tag);
+    build_tables<R>(o);
+    o->ensure_batch(dd.max_batch);
+    if (dd.backend == TOMO_BACKEND_SURROGATE) build_stencil<R>(o, 0);
+  });
   CK(cudaDeviceSynchronize());
   *out = op.release();
   TOMO_CATCH
@@ -878,9 +916,10 @@ int tomo_op_get_info(const tomo_op* op, tomo_op_info* info) {
   info->nnz = op->nnz;
   info->wt_rows = op->wt_rows;
   info->wt_slots = op->wt_slots;
-  info->bytes_w = static_cast<int64_t>(op->Ppad) * op->nq * 32;
-  info->bytes_wt = op->wt_slots * 8 + (static_cast<int64_t>(op->g.m) * op->g.m / 32 + 1) * 4;
+  info->bytes_w = static_cast<int64_t>(op->Ppad) * op->nq * 32 * (16 + 4 * static_cast<int64_t>(op->rsz)) / 32;
+  info->bytes_wt = op->wt_slots * (op->f64 ? 16 : 8) + (static_cast<int64_t>(op->g.m) * op->g.m / 32 + 1) * 4;
   info->surrogate_r = op->rad;
+  info->precision = op->f64 ? TOMO_F64 : TOMO_F32;
   std::memcpy(info->stencil, op->stencil64, sizeof(info->stencil));
   TOMO_CATCH
 }
@@ -890,54 +929,54 @@ int tomo_apply_normal(tomo_op* op, const void* in, void* out, int batch, void* s
   check_op(op, batch);
   DeviceGuard dg(op->device);
   const cudaStream_t st = S_(stream);
-  const size_t cnt = static_cast<size_t>(batch) * op->L();
-  const float2* din = stage_in<float2>(in, cnt, op->sc.cin, st);
-  const bool host_out = !is_device_ptr(out);
-  float2* dout = host_out ? (op->sc.cout.ensure(cnt), op->sc.cout.p) : static_cast<float2*>(out);
-  if (surrogate(op)) {
-    // T acts on real and imaginary parts independently (sparse.cpp:27-42)
-    op->sc.fin.ensure(cnt * 2);
-    op->sc.fout.ensure(cnt * 2);
-    float* re = op->sc.fin.p;
-    float* im = op->sc.fin.p + cnt;
-    CK(cudaMemcpy2DAsync(re, 4, din, 8, 4, cnt, cudaMemcpyDeviceToDevice, st));
-    CK(cudaMemcpy2DAsync(im, 4, reinterpret_cast<const float*>(din) + 1, 8, 4, cnt, cudaMemcpyDeviceToDevice, st));
-    const SysParams sp = sysp(1.0, 0.0, 0.0, 0.0);
-    for (int part = 0; part < 2; ++part)
-      launch_stencil(op->g.n, batch, op->rad, op->desc.euclidean, op->coef, 2, op->sc.fin.p + part * cnt, nullptr,
-                     nullptr, op->sc.fout.p + part * cnt, nullptr, nullptr, sp, 0, op->red(), st);
-    CK(cudaMemcpy2DAsync(dout, 8, op->sc.fout.p, 4, 4, cnt, cudaMemcpyDeviceToDevice, st));
-    CK(cudaMemcpy2DAsync(reinterpret_cast<float*>(dout) + 1, 8, op->sc.fout.p + cnt, 4, 4, cnt,
-                         cudaMemcpyDeviceToDevice, st));
-  } else {
-    normal_direct(op, batch, din, true, dout, st);
-  }
-  if (host_out) {
-    CK(cudaMemcpyAsync(out, dout, sizeof(float2) * cnt, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-  }
+  with_prec(op, [&](auto tag) {
+    using R = decltype(tag);
+    const size_t cnt = static_cast<size_t>(batch) * op->L();
+    const void* din = stage_in(in, cnt * sizeof(cplx<R>), op->sc.cin, st);
+    OutArg o(out, cnt * sizeof(cplx<R>), op->sc.cout);
+    if (op->surrogate()) {
+      // T acts on real and imaginary parts independently (sparse.cpp:27-42)
+      op->sc.fin.ensure(cnt * 2 * sizeof(R));
+      op->sc.fout.ensure(cnt * 2 * sizeof(R));
+      R* re = op->sc.fin.as<R>();
+      R* im = re + cnt;
+      CK(cudaMemcpy2DAsync(re, sizeof(R), din, 2 * sizeof(R), sizeof(R), cnt, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpy2DAsync(im, sizeof(R), static_cast<const R*>(din) + 1, 2 * sizeof(R), sizeof(R), cnt,
+                           cudaMemcpyDeviceToDevice, st));
+      const SysParams sp = sysp(1.0, 0.0, 0.0, 0.0);
+      for (int part = 0; part < 2; ++part)
+        launch_stencil<R>(op->g.n, batch, op->rad, op->coef, 2, re + part * cnt, nullptr, nullptr,
+                          op->sc.fout.as<R>() + part * cnt, nullptr, nullptr, sp, 0, op->red(), st);
+      CK(cudaMemcpy2DAsync(o.dev, 2 * sizeof(R), op->sc.fout.p, sizeof(R), sizeof(R), cnt, cudaMemcpyDeviceToDevice,
+                           st));
+      CK(cudaMemcpy2DAsync(static_cast<R*>(o.dev) + 1, 2 * sizeof(R), op->sc.fout.as<R>() + cnt, sizeof(R), sizeof(R),
+                           cnt, cudaMemcpyDeviceToDevice, st));
+    } else {
+      normal_direct<R>(op, batch, din, true, o.dev, st);
+    }
+    o.finish(st);
+  });
   TOMO_CATCH
 }
 
-int tomo_apply_normal_real(tomo_op* op, const float* in, float* out, int batch, void* stream) {
+int tomo_apply_normal_real(tomo_op* op, const void* in, void* out, int batch, void* stream) {
   TOMO_TRY
   check_op(op, batch);
   DeviceGuard dg(op->device);
   const cudaStream_t st = S_(stream);
-  const size_t cnt = static_cast<size_t>(batch) * op->L();
-  const float* din = stage_in<float>(in, cnt, op->sc.fin, st);
-  const bool host_out = !is_device_ptr(out);
-  float* dout = host_out ? (op->sc.fout.ensure(cnt), op->sc.fout.p) : out;
-  if (surrogate(op)) {
-    launch_stencil(op->g.n, batch, op->rad, op->desc.euclidean, op->coef, 2, din, nullptr, nullptr, dout, nullptr,
-                   nullptr, sysp(1.0, 0.0, 0.0, 0.0), 0, op->red(), st);
-  } else {
-    normal_direct(op, batch, din, false, dout, st);
-  }
-  if (host_out) {
-    CK(cudaMemcpyAsync(out, dout, sizeof(float) * cnt, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-  }
+  with_prec(op, [&](auto tag) {
+    using R = decltype(tag);
+    const size_t cnt = static_cast<size_t>(batch) * op->L();
+    const void* din = stage_in(in, cnt * sizeof(R), op->sc.fin, st);
+    OutArg o(out, cnt * sizeof(R), op->sc.fout);
+    if (op->surrogate()) {
+      launch_stencil<R>(op->g.n, batch, op->rad, op->coef, 2, static_cast<const R*>(din), nullptr, nullptr,
+                        static_cast<R*>(o.dev), nullptr, nullptr, sysp(1.0, 0.0, 0.0, 0.0), 0, op->red(), st);
+    } else {
+      normal_direct<R>(op, batch, din, false, o.dev, st);
+    }
+    o.finish(st);
+  });
   TOMO_CATCH
 }
 
@@ -946,17 +985,16 @@ int tomo_forward(tomo_op* op, const void* image, void* samples, int batch, void*
   check_op(op, batch);
   DeviceGuard dg(op->device);
   const cudaStream_t st = S_(stream);
-  const size_t cnt = static_cast<size_t>(batch) * op->L();
-  const size_t scnt = static_cast<size_t>(batch) * op->g.P;
-  const float2* din = stage_in<float2>(image, cnt, op->sc.cin, st);
-  const bool host_out = !is_device_ptr(samples);
-  float2* dout = host_out ? (op->sc.cout.ensure(scnt), op->sc.cout.p) : static_cast<float2*>(samples);
-  PUpd pu{};
-  type2(op, batch, din, true, pu, dout, nullptr, st);
-  if (host_out) {
-    CK(cudaMemcpyAsync(samples, dout, sizeof(float2) * scnt, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-  }
+  with_prec(op, [&](auto tag) {
+    using R = decltype(tag);
+    const size_t cnt = static_cast<size_t>(batch) * op->L();
+    const size_t scnt = static_cast<size_t>(batch) * op->g.P;
+    const void* din = stage_in(image, cnt * sizeof(cplx<R>), op->sc.cin, st);
+    OutArg o(samples, scnt * sizeof(cplx<R>), op->sc.cout);
+    PUpd<R> pu{};
+    type2<R>(op, batch, din, true, pu, static_cast<cplx<R>*>(o.dev), nullptr, st);
+    o.finish(st);
+  });
   TOMO_CATCH
 }
 
@@ -965,19 +1003,18 @@ int tomo_adjoint(tomo_op* op, const void* samples, void* image, int batch, void*
   check_op(op, batch);
   DeviceGuard dg(op->device);
   const cudaStream_t st = S_(stream);
-  const size_t cnt = static_cast<size_t>(batch) * op->L();
-  const size_t scnt = static_cast<size_t>(batch) * op->g.P;
-  const float2* din = stage_in<float2>(samples, scnt, op->sc.cin, st);
-  const bool host_out = !is_device_ptr(image);
-  float2* dout = host_out ? (op->sc.cout.ensure(cnt), op->sc.cout.p) : static_cast<float2*>(image);
-  PbEpi e = plain_epi(PB_COMPLEX, 1.0f);
-  e.out_c = dout;
-  type1(op, batch, din, e, nullptr, st);
-  allreduce(op, reinterpret_cast<float*>(dout), cnt * 2, st);
-  if (host_out) {
-    CK(cudaMemcpyAsync(image, dout, sizeof(float2) * cnt, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-  }
+  with_prec(op, [&](auto tag) {
+    using R = decltype(tag);
+    const size_t cnt = static_cast<size_t>(batch) * op->L();
+    const size_t scnt = static_cast<size_t>(batch) * op->g.P;
+    const void* din = stage_in(samples, scnt * sizeof(cplx<R>), op->sc.cin, st);
+    OutArg o(image, cnt * sizeof(cplx<R>), op->sc.cout);
+    PbEpi<R> e = plain_epi<R>(PB_COMPLEX, 1.0);
+    e.out_c = static_cast<cplx<R>*>(o.dev);
+    type1<R>(op, batch, static_cast<const cplx<R>*>(din), e, nullptr, st);
+    allreduce<R>(op, static_cast<R*>(o.dev), cnt * 2, st);
+    o.finish(st);
+  });
   TOMO_CATCH
 }
 
@@ -986,17 +1023,16 @@ int tomo_spmv_w(tomo_op* op, const void* grid, void* samples, int batch, void* s
   check_op(op, batch);
   DeviceGuard dg(op->device);
   const cudaStream_t st = S_(stream);
-  const size_t gcnt = static_cast<size_t>(batch) * op->g.m * op->g.m;
-  const size_t scnt = static_cast<size_t>(batch) * op->g.P;
-  const float2* din = stage_in<float2>(grid, gcnt, op->sc.cin, st);
-  const bool host_out = !is_device_ptr(samples);
-  float2* dout = host_out ? (op->sc.cout.ensure(scnt), op->sc.cout.p) : static_cast<float2*>(samples);
-  OpDev d = op->dev(batch);
-  launch_w(d, batch, din, dout, nullptr, st);
-  if (host_out) {
-    CK(cudaMemcpyAsync(samples, dout, sizeof(float2) * scnt, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-  }
+  with_prec(op, [&](auto tag) {
+    using R = decltype(tag);
+    const size_t gcnt = static_cast<size_t>(batch) * op->g.m * op->g.m;
+    const size_t scnt = static_cast<size_t>(batch) * op->g.P;
+    const void* din = stage_in(grid, gcnt * sizeof(cplx<R>), op->sc.cin, st);
+    OutArg o(samples, scnt * sizeof(cplx<R>), op->sc.cout);
+    OpDev<R> d = op->dev<R>(batch);
+    launch_w<R>(d, batch, static_cast<const cplx<R>*>(din), static_cast<cplx<R>*>(o.dev), nullptr, st);
+    o.finish(st);
+  });
   TOMO_CATCH
 }
 
@@ -1005,40 +1041,38 @@ int tomo_spmv_wt(tomo_op* op, const void* samples, void* grid, int batch, void* 
   check_op(op, batch);
   DeviceGuard dg(op->device);
   const cudaStream_t st = S_(stream);
-  const size_t gcnt = static_cast<size_t>(batch) * op->g.m * op->g.m;
-  const size_t scnt = static_cast<size_t>(batch) * op->g.P;
-  const float2* din = stage_in<float2>(samples, scnt, op->sc.cin, st);
-  const bool host_out = !is_device_ptr(grid);
-  float2* dout = host_out ? (op->sc.cout.ensure(gcnt), op->sc.cout.p) : static_cast<float2*>(grid);
-  OpDev d = op->dev(batch);
-  launch_wt_grid(d, batch, din, dout, st);
-  if (host_out) {
-    CK(cudaMemcpyAsync(grid, dout, sizeof(float2) * gcnt, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-  }
+  with_prec(op, [&](auto tag) {
+    using R = decltype(tag);
+    const size_t gcnt = static_cast<size_t>(batch) * op->g.m * op->g.m;
+    const size_t scnt = static_cast<size_t>(batch) * op->g.P;
+    const void* din = stage_in(samples, scnt * sizeof(cplx<R>), op->sc.cin, st);
+    OutArg o(grid, gcnt * sizeof(cplx<R>), op->sc.cout);
+    OpDev<R> d = op->dev<R>(batch);
+    launch_wt_grid<R>(d, batch, static_cast<const cplx<R>*>(din), static_cast<cplx<R>*>(o.dev), st);
+    o.finish(st);
+  });
   TOMO_CATCH
 }
 
-int tomo_backproject(tomo_op* op, double alpha, int weighted, const void* slice_data, float* out, int batch,
+int tomo_backproject(tomo_op* op, double alpha, int weighted, const void* slice_data, void* out, int batch,
                      void* stream) {
   TOMO_TRY
   check_op(op, batch);
   DeviceGuard dg(op->device);
   const cudaStream_t st = S_(stream);
-  const size_t cnt = static_cast<size_t>(batch) * op->L();
-  const size_t scnt = static_cast<size_t>(batch) * op->g.P;
-  const float2* din = stage_in<float2>(slice_data, scnt, op->sc.cin, st);
-  const bool host_out = !is_device_ptr(out);
-  float* dout = host_out ? (op->sc.fout.ensure(cnt), op->sc.fout.p) : out;
-  backproject(op, batch, alpha, weighted != 0, din, dout, st);
-  if (host_out) {
-    CK(cudaMemcpyAsync(out, dout, sizeof(float) * cnt, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-  }
+  with_prec(op, [&](auto tag) {
+    using R = decltype(tag);
+    const size_t cnt = static_cast<size_t>(batch) * op->L();
+    const size_t scnt = static_cast<size_t>(batch) * op->g.P;
+    const void* din = stage_in(slice_data, scnt * sizeof(cplx<R>), op->sc.cin, st);
+    OutArg o(out, cnt * sizeof(R), op->sc.fout);
+    backproject<R>(op, batch, alpha, weighted != 0, static_cast<const cplx<R>*>(din), static_cast<R*>(o.dev), st);
+    o.finish(st);
+  });
   TOMO_CATCH
 }
 
-int tomo_cg(tomo_op* op, const tomo_system* sys, const float* rhs, const float* x0, float* x, int steps,
+int tomo_cg(tomo_op* op, const tomo_system* sys, const void* rhs, const void* x0, void* x, int steps,
             double rel_tol, int batch, tomo_cg_stats* stats, void* stream) {
   TOMO_TRY
   check_op(op, batch);
@@ -1047,33 +1081,33 @@ int tomo_cg(tomo_op* op, const tomo_system* sys, const float* rhs, const float* 
   DeviceGuard dg(op->device);
   op->ensure_batch(batch);
   const cudaStream_t st = S_(stream);
-  const int64_t L = op->L();
-  const size_t cnt = static_cast<size_t>(batch) * L;
-  Scratch& S = op->sc;
-  const float* drhs = stage_in<float>(rhs, cnt, S.rhs, st);
-  const float* dx0 = nullptr;
-  dx0 = x0 ? stage_in<float>(x0, cnt, S.mu0, st) : S.zero.p;
-  const bool host_out = !is_device_ptr(x);
-  float* dx = host_out ? S.x.p : x;
-  const SysParams sp = sysp(sys->alpha, sys->lambda, sys->shift, rel_tol);
-  CK(cudaMemsetAsync(S.sc.p, 0, sizeof(SliceScalars) * batch, st));
-  cg_run(op, batch, sp, drhs, dx0, dx, steps, st);
-  std::vector<SliceScalars> hs(batch);
-  CK(cudaMemcpyAsync(hs.data(), S.sc.p, sizeof(SliceScalars) * batch, cudaMemcpyDeviceToHost, st));
-  if (host_out) CK(cudaMemcpyAsync(x, dx, sizeof(float) * cnt, cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  for (int b = 0; b < batch; ++b) {
-    if (hs[b].nonfinite) throw NumericalError("cg_solve diverged (non-finite iterate)");
-    if (stats) {
-      stats[b].steps_run = hs[b].steps_run;
-      stats[b].min_ritz = std::isfinite(hs[b].min_ritz) ? hs[b].min_ritz : 0.0;
-      stats[b].final_rs = hs[b].rr[hs[b].steps_run & 1];
+  with_prec(op, [&](auto tag) {
+    using R = decltype(tag);
+    const size_t cnt = static_cast<size_t>(batch) * op->L();
+    Scratch& S = op->sc;
+    const R* drhs = static_cast<const R*>(stage_in(rhs, cnt * sizeof(R), S.fin, st));
+    const R* dx0 = x0 ? static_cast<const R*>(stage_in(x0, cnt * sizeof(R), S.mu1, st)) : S.zero.as<R>();
+    OutArg o(x, cnt * sizeof(R), S.fout);
+    CK(cudaMemsetAsync(S.sc.p, 0, sizeof(SliceScalars) * batch, st));
+    cg_run<R>(op, batch, sysp(sys->alpha, sys->lambda, sys->shift, rel_tol), drhs, dx0, static_cast<R*>(o.dev),
+              steps, st);
+    std::vector<SliceScalars> hs(batch);
+    CK(cudaMemcpyAsync(hs.data(), S.sc.p, sizeof(SliceScalars) * batch, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    o.finish(st);
+    for (int b = 0; b < batch; ++b) {
+      if (hs[b].nonfinite) throw NumericalError("cg_solve diverged (non-finite iterate)");
+      if (stats) {
+        stats[b].steps_run = hs[b].steps_run;
+        stats[b].min_ritz = std::isfinite(hs[b].min_ritz) ? hs[b].min_ritz : 0.0;
+        stats[b].final_rs = hs[b].rr[hs[b].steps_run & 1];
+      }
     }
-  }
+  });
   TOMO_CATCH
 }
 
-int tomo_split_bregman(tomo_op* op, const tomo_sb_config* cfg, const void* slice_data, float* mu, int batch,
+int tomo_split_bregman(tomo_op* op, const tomo_sb_config* cfg, const void* slice_data, void* mu, int batch,
                        double* update_l1, tomo_sb_trace* trace, void* stream) {
   TOMO_TRY
   check_op(op, batch);
@@ -1083,163 +1117,172 @@ int tomo_split_bregman(tomo_op* op, const tomo_sb_config* cfg, const void* slice
   if (cfg->max_iters < 1) throw ConfigError("SolverConfig: max_bregman_iters >= 1");
   if (cfg->cg_steps < 1) throw ConfigError("SolverConfig: cg_steps_per_update >= 1");
   if (cfg->update_tol_rel < 0.0) throw ConfigError("SolverConfig: update_tol_rel >= 0");
+  if (cfg->max_iters > kMaxLoggedIters) throw ConfigError("split_bregman_tv: max_bregman_iters > 8192 not supported");
   DeviceGuard dg(op->device);
   op->ensure_batch(batch);
   const cudaStream_t st = S_(stream);
-  const int n = op->g.n;
-  const int64_t L = op->L();
-  const size_t cnt = static_cast<size_t>(batch) * L;
-  const size_t scnt = static_cast<size_t>(batch) * op->g.P;
-  Scratch& S = op->sc;
-  const bool sur = surrogate(op);
-
-  // make_subproblem (solver.cpp:164-215): sigma, then the leak probe (:236-247)
-  double sigma = 0.0;
-  if (sur) sigma = cfg->sigma_override >= 0.0 ? cfg->sigma_override : surrogate_sigma(op, cfg->alpha, cfg->lambda, st);
-  double leak = 0.0;
-  if (!sur) {
-    leak = leak_probe(op, st);
-    if (leak > 0.1) throw NumericalError("split_bregman_tv: conjugation symmetry broken");
-  }
-  const float2* din = stage_in<float2>(slice_data, scnt, S.cin, st);
-  if (cfg->max_iters > kMaxLoggedIters) throw ConfigError("split_bregman_tv: max_bregman_iters > 8192 not supported");
-  backproject(op, batch, cfg->alpha, sur, din, S.fid.p, st);
-  CK(cudaMemcpyAsync(S.rhs.p, S.fid.p, sizeof(float) * cnt, cudaMemcpyDeviceToDevice, st));
-  for (auto* b : {&S.mu0, &S.bx0, &S.by0}) CK(cudaMemsetAsync(b->p, 0, sizeof(float) * cnt, st));
-  // per-slice scalars: zero, then the stopping tolerance
-  std::vector<SliceScalars> init(batch);
-  std::memset(init.data(), 0, sizeof(SliceScalars) * batch);
-  for (auto& s : init) s.sb_tol = cfg->update_tol_rel;
-  CK(cudaMemcpyAsync(S.sc.p, init.data(), sizeof(SliceScalars) * batch, cudaMemcpyHostToDevice, st));
-  const SysParams sp = sysp(cfg->alpha, cfg->lambda, sigma, 0.0);
-  const std::string key = fmtkey("sb", batch, {cfg->alpha, cfg->lambda, sigma, double(cfg->max_iters),
-                                               double(cfg->cg_steps), double(cfg->warm_start)});
-  run_graph(op, key, st, [&](cudaStream_t cs) {
-    float* mu_cur = S.mu0.p;
-    float* mu_nxt = S.mu1.p;
-    float *bxo = S.bx0.p, *bxn = S.bx1.p, *byo = S.by0.p, *byn = S.by1.p;
-    for (int it = 0; it < cfg->max_iters; ++it) {
-      cg_run(op, batch, sp, S.rhs.p, cfg->warm_start ? mu_cur : S.zero.p, mu_nxt, cfg->cg_steps, cs);
-      launch_sb_post(n, batch, mu_nxt, mu_cur, bxo, byo, bxn, byn, S.fid.p, S.rhs.p, static_cast<float>(cfg->lambda),
-                     op->red(), cs);
-      CK(cudaMemcpy2DAsync(S.upd_log.p + static_cast<size_t>(it) * batch, sizeof(double), &S.sc.p[0].upd,
-                           sizeof(SliceScalars), sizeof(double), batch, cudaMemcpyDeviceToDevice, cs));
-      std::swap(mu_cur, mu_nxt);
-      std::swap(bxo, bxn);
-      std::swap(byo, byn);
+  with_prec(op, [&](auto tag) {
+    using R = decltype(tag);
+    const int n = op->g.n;
+    const size_t cnt = static_cast<size_t>(batch) * op->L();
+    const size_t scnt = static_cast<size_t>(batch) * op->g.P;
+    Scratch& S = op->sc;
+    const bool sur = op->surrogate();
+    // make_subproblem (solver.cpp:164-215): sigma, then the leak probe (:236-247)
+    double sigma = 0.0;
+    if (sur) sigma = cfg->sigma_override >= 0.0 ? cfg->sigma_override : surrogate_sigma<R>(op, cfg->alpha, cfg->lambda, st);
+    double leak = 0.0;
+    if (!sur) {
+      leak = leak_probe<R>(op, st);
+      if (leak > 0.1) throw NumericalError("split_bregman_tv: conjugation symmetry broken");
     }
-    // final iterate lives in mu_cur; normalise its location to S.mu0
-    if (mu_cur != S.mu0.p)
-      CK(cudaMemcpyAsync(S.mu0.p, mu_cur, sizeof(float) * cnt, cudaMemcpyDeviceToDevice, cs));
+    const auto* din = static_cast<const cplx<R>*>(stage_in(slice_data, scnt * sizeof(cplx<R>), S.cin, st));
+    backproject<R>(op, batch, cfg->alpha, sur, din, S.fid.as<R>(), st);
+    CK(cudaMemcpyAsync(S.rhs.p, S.fid.p, sizeof(R) * cnt, cudaMemcpyDeviceToDevice, st));
+    for (auto* b : {&S.mu0, &S.bx0, &S.by0}) CK(cudaMemsetAsync(b->p, 0, sizeof(R) * cnt, st));
+    std::vector<SliceScalars> init(batch);
+    std::memset(init.data(), 0, sizeof(SliceScalars) * batch);
+    for (auto& s : init) s.sb_tol = cfg->update_tol_rel;
+    CK(cudaMemcpyAsync(S.sc.p, init.data(), sizeof(SliceScalars) * batch, cudaMemcpyHostToDevice, st));
+    const SysParams sp = sysp(cfg->alpha, cfg->lambda, sigma, 0.0);
+    const std::string key = fmtkey("sb", batch, {cfg->alpha, cfg->lambda, sigma, double(cfg->max_iters),
+                                                 double(cfg->cg_steps), double(cfg->warm_start)});
+    run_graph(op, key, st, [&](cudaStream_t cs) {
+      R* mu_cur = S.mu0.as<R>();
+      R* mu_nxt = S.mu1.as<R>();
+      R *bxo = S.bx0.as<R>(), *bxn = S.bx1.as<R>(), *byo = S.by0.as<R>(), *byn = S.by1.as<R>();
+      for (int it = 0; it < cfg->max_iters; ++it) {
+        cg_run<R>(op, batch, sp, S.rhs.as<R>(), cfg->warm_start ? mu_cur : S.zero.as<R>(), mu_nxt, cfg->cg_steps, cs);
+        launch_sb_post<R>(n, batch, mu_nxt, mu_cur, bxo, byo, bxn, byn, S.fid.as<R>(), S.rhs.as<R>(), cfg->lambda,
+                          op->red(), cs);
+        CK(cudaMemcpy2DAsync(S.upd_log.as<double>() + static_cast<size_t>(it) * batch, sizeof(double),
+                             &op->scal()[0].upd, sizeof(SliceScalars), sizeof(double), batch,
+                             cudaMemcpyDeviceToDevice, cs));
+        std::swap(mu_cur, mu_nxt);
+        std::swap(bxo, bxn);
+        std::swap(byo, byn);
+      }
+      // final iterate lives in mu_cur; normalise its location to S.mu0
+      if (mu_cur != S.mu0.as<R>()) CK(cudaMemcpyAsync(S.mu0.p, mu_cur, sizeof(R) * cnt, cudaMemcpyDeviceToDevice, cs));
+    });
+    std::vector<SliceScalars> hs(batch);
+    CK(cudaMemcpyAsync(hs.data(), S.sc.p, sizeof(SliceScalars) * batch, cudaMemcpyDeviceToHost, st));
+    std::vector<double> log(static_cast<size_t>(batch) * cfg->max_iters);
+    CK(cudaMemcpyAsync(log.data(), S.upd_log.p, sizeof(double) * log.size(), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(mu, S.mu0.p, sizeof(R) * cnt, is_device_ptr(mu) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                       st));
+    CK(cudaStreamSynchronize(st));
+    for (int b = 0; b < batch; ++b) {
+      if (hs[b].nonfinite)
+        throw NumericalError(std::string("split_bregman_tv: non-finite iterate with backend ") +
+                             (sur ? "surrogate" : "direct"));
+      const int iters = hs[b].sb_iters;
+      if (update_l1)
+        for (int it = 0; it < cfg->max_iters; ++it)
+          update_l1[static_cast<size_t>(b) * cfg->max_iters + it] =
+              it < iters ? log[static_cast<size_t>(it) * batch + b] : 0.0;
+      if (trace) {
+        trace[b].iterations = iters;
+        trace[b].first_update_l1 = hs[b].first_upd;
+        trace[b].sigma = sigma;
+        trace[b].min_ritz = std::isfinite(hs[b].min_ritz) ? hs[b].min_ritz : 0.0;
+        trace[b].imag_leakage = leak;
+        trace[b].stopped_on_tolerance = hs[b].frozen;
+      }
+    }
   });
-  std::vector<SliceScalars> hs(batch);
-  CK(cudaMemcpyAsync(hs.data(), S.sc.p, sizeof(SliceScalars) * batch, cudaMemcpyDeviceToHost, st));
-  std::vector<double> log(static_cast<size_t>(batch) * cfg->max_iters);
-  CK(cudaMemcpyAsync(log.data(), S.upd_log.p, sizeof(double) * log.size(), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(mu, S.mu0.p, sizeof(float) * cnt, is_device_ptr(mu) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  for (int b = 0; b < batch; ++b) {
-    if (hs[b].nonfinite)
-      throw NumericalError(std::string("split_bregman_tv: non-finite iterate with backend ") + (sur ? "surrogate" : "direct"));
-    const int iters = hs[b].sb_iters;
-    if (update_l1)
-      for (int it = 0; it < cfg->max_iters; ++it)
-        update_l1[static_cast<size_t>(b) * cfg->max_iters + it] = it < iters ? log[static_cast<size_t>(it) * batch + b] : 0.0;
-    if (trace) {
-      trace[b].iterations = iters;
-      trace[b].first_update_l1 = hs[b].first_upd;
-      trace[b].sigma = sigma;
-      trace[b].min_ritz = std::isfinite(hs[b].min_ritz) ? hs[b].min_ritz : 0.0;
-      trace[b].imag_leakage = leak;
-      trace[b].stopped_on_tolerance = hs[b].frozen;
-    }
-  }
   TOMO_CATCH
 }
 
-int tomo_tikhonov(tomo_op* op, double alpha, const void* slice_data, float* mu, int steps, double rel_tol, int batch,
+int tomo_tikhonov(tomo_op* op, double alpha, const void* slice_data, void* mu, int steps, double rel_tol, int batch,
                   void* stream) {
   TOMO_TRY
   check_op(op, batch);
   if (steps < 1) throw ConfigError("cg_solve: steps must be >= 1");
-  if (surrogate(op)) throw ConfigError("tomo_tikhonov: direct backend only");
+  if (op->surrogate()) throw ConfigError("tomo_tikhonov: direct backend only");
   DeviceGuard dg(op->device);
   op->ensure_batch(batch);
   const cudaStream_t st = S_(stream);
-  const size_t cnt = static_cast<size_t>(batch) * op->L();
-  const size_t scnt = static_cast<size_t>(batch) * op->g.P;
-  Scratch& S = op->sc;
-  const float2* din = stage_in<float2>(slice_data, scnt, S.cin, st);
-  backproject(op, batch, alpha, false, din, S.fid.p, st);
-  CK(cudaMemsetAsync(S.sc.p, 0, sizeof(SliceScalars) * batch, st));
-  const SysParams sp = sysp(alpha, 0.0, 1.0, rel_tol);
-  const std::string key = fmtkey("tik", batch, {alpha, double(steps), rel_tol});
-  run_graph(op, key, st, [&](cudaStream_t cs) { cg_run(op, batch, sp, S.fid.p, S.zero.p, S.x.p, steps, cs); });
-  std::vector<SliceScalars> hs(batch);
-  CK(cudaMemcpyAsync(hs.data(), S.sc.p, sizeof(SliceScalars) * batch, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(mu, S.x.p, sizeof(float) * cnt, is_device_ptr(mu) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  for (int b = 0; b < batch; ++b)
-    if (hs[b].nonfinite) throw NumericalError("tikhonov_solve: cg diverged (non-finite iterate)");
+  with_prec(op, [&](auto tag) {
+    using R = decltype(tag);
+    const size_t cnt = static_cast<size_t>(batch) * op->L();
+    const size_t scnt = static_cast<size_t>(batch) * op->g.P;
+    Scratch& S = op->sc;
+    const auto* din = static_cast<const cplx<R>*>(stage_in(slice_data, scnt * sizeof(cplx<R>), S.cin, st));
+    backproject<R>(op, batch, alpha, false, din, S.fid.as<R>(), st);
+    CK(cudaMemsetAsync(S.sc.p, 0, sizeof(SliceScalars) * batch, st));
+    const SysParams sp = sysp(alpha, 0.0, 1.0, rel_tol);
+    const std::string key = fmtkey("tik", batch, {alpha, double(steps), rel_tol});
+    run_graph(op, key, st,
+              [&](cudaStream_t cs) { cg_run<R>(op, batch, sp, S.fid.as<R>(), S.zero.as<R>(), S.x.as<R>(), steps, cs); });
+    std::vector<SliceScalars> hs(batch);
+    CK(cudaMemcpyAsync(hs.data(), S.sc.p, sizeof(SliceScalars) * batch, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(mu, S.x.p, sizeof(R) * cnt, is_device_ptr(mu) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                       st));
+    CK(cudaStreamSynchronize(st));
+    for (int b = 0; b < batch; ++b)
+      if (hs[b].nonfinite) throw NumericalError("tikhonov_solve: cg diverged (non-finite iterate)");
+  });
   TOMO_CATCH
 }
 
-int tomo_chambolle_pock(tomo_op* op, const tomo_cp_config* cfg, const void* slice_data, float* mu, int batch,
+int tomo_chambolle_pock(tomo_op* op, const tomo_cp_config* cfg, const void* slice_data, void* mu, int batch,
                         void* stream) {
   TOMO_TRY
   check_op(op, batch);
   if (!cfg || cfg->iters < 1 || cfg->cg_steps < 1) throw ConfigError("chambolle_pock: bad config");
-  if (surrogate(op)) throw ConfigError("chambolle_pock: direct backend only");
+  if (op->surrogate()) throw ConfigError("chambolle_pock: direct backend only");
   DeviceGuard dg(op->device);
   op->ensure_batch(batch);
   const cudaStream_t st = S_(stream);
-  const int n = op->g.n;
-  const size_t cnt = static_cast<size_t>(batch) * op->L();
-  const size_t scnt = static_cast<size_t>(batch) * op->g.P;
-  Scratch& S = op->sc;
-  const float2* din = stage_in<float2>(slice_data, scnt, S.cin, st);
-  backproject(op, batch, cfg->alpha, false, din, S.fid.p, st);
-  for (auto* b : {&S.mu0, &S.mu1, &S.bx0, &S.by0}) CK(cudaMemsetAsync(b->p, 0, sizeof(float) * cnt, st));
-  CK(cudaMemsetAsync(S.sc.p, 0, sizeof(SliceScalars) * batch, st));
-  const SysParams sp = sysp(cfg->tau_cp * cfg->alpha, 0.0, 1.0, 0.0);
-  const std::string key = fmtkey("cp", batch, {cfg->alpha, cfg->lambda, cfg->tau_cp, cfg->sigma_cp, cfg->theta,
-                                               double(cfg->iters), double(cfg->cg_steps)});
-  // the captured loop rotates (u^{k-1}, u^k, u^{k+1}) buffers; replay the rotation to find u^K
-  float* final_u = S.mu0.p;
-  {
-    float *up = S.mu1.p, *uc = S.mu0.p, *un = S.u2.p;
-    for (int k = 0; k < cfg->iters; ++k) {
-      float* t = up;
-      up = uc;
-      uc = un;
-      un = t;
+  with_prec(op, [&](auto tag) {
+    using R = decltype(tag);
+    const int n = op->g.n;
+    const size_t cnt = static_cast<size_t>(batch) * op->L();
+    const size_t scnt = static_cast<size_t>(batch) * op->g.P;
+    Scratch& S = op->sc;
+    const auto* din = static_cast<const cplx<R>*>(stage_in(slice_data, scnt * sizeof(cplx<R>), S.cin, st));
+    backproject<R>(op, batch, cfg->alpha, false, din, S.fid.as<R>(), st);
+    for (auto* b : {&S.mu0, &S.mu1, &S.bx0, &S.by0}) CK(cudaMemsetAsync(b->p, 0, sizeof(R) * cnt, st));
+    CK(cudaMemsetAsync(S.sc.p, 0, sizeof(SliceScalars) * batch, st));
+    const SysParams sp = sysp(cfg->tau_cp * cfg->alpha, 0.0, 1.0, 0.0);
+    const std::string key = fmtkey("cp", batch, {cfg->alpha, cfg->lambda, cfg->tau_cp, cfg->sigma_cp, cfg->theta,
+                                                 double(cfg->iters), double(cfg->cg_steps)});
+    // the captured loop rotates (u^{k-1}, u^k, u^{k+1}) buffers; replay the rotation to find u^K
+    R* final_u = nullptr;
+    {
+      R *up = S.mu1.as<R>(), *uc = S.mu0.as<R>(), *un = S.u2.as<R>();
+      for (int k = 0; k < cfg->iters; ++k) {
+        R* t = up;
+        up = uc;
+        uc = un;
+        un = t;
+      }
+      final_u = uc;
     }
-    final_u = uc;
-  }
-  run_graph(op, key, st, [&](cudaStream_t cs) {
-    float* up = S.mu1.p;
-    float* uc = S.mu0.p;
-    float* un = S.u2.p;
-    float *yxo = S.bx0.p, *yxn = S.bx1.p, *yyo = S.by0.p, *yyn = S.by1.p;
-    for (int k = 0; k < cfg->iters; ++k) {
-      launch_cp_dual(n, batch, uc, up, yxo, yyo, yxn, yyn, S.fid.p, S.rhs.p, static_cast<float>(cfg->tau_cp),
-                     static_cast<float>(cfg->sigma_cp), static_cast<float>(cfg->theta), static_cast<float>(cfg->lambda),
-                     cs);
-      cg_run(op, batch, sp, S.rhs.p, uc, un, cfg->cg_steps, cs);
-      float* t = up;
-      up = uc;
-      uc = un;
-      un = t;
-      std::swap(yxo, yxn);
-      std::swap(yyo, yyn);
-    }
+    run_graph(op, key, st, [&](cudaStream_t cs) {
+      R *up = S.mu1.as<R>(), *uc = S.mu0.as<R>(), *un = S.u2.as<R>();
+      R *yxo = S.bx0.as<R>(), *yxn = S.bx1.as<R>(), *yyo = S.by0.as<R>(), *yyn = S.by1.as<R>();
+      for (int k = 0; k < cfg->iters; ++k) {
+        launch_cp_dual<R>(n, batch, uc, up, yxo, yyo, yxn, yyn, S.fid.as<R>(), S.rhs.as<R>(), cfg->tau_cp,
+                          cfg->sigma_cp, cfg->theta, cfg->lambda, cs);
+        cg_run<R>(op, batch, sp, S.rhs.as<R>(), uc, un, cfg->cg_steps, cs);
+        R* t = up;
+        up = uc;
+        uc = un;
+        un = t;
+        std::swap(yxo, yxn);
+        std::swap(yyo, yyn);
+      }
+    });
+    std::vector<SliceScalars> hs(batch);
+    CK(cudaMemcpyAsync(hs.data(), S.sc.p, sizeof(SliceScalars) * batch, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(mu, final_u, sizeof(R) * cnt, is_device_ptr(mu) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                       st));
+    CK(cudaStreamSynchronize(st));
+    for (int b = 0; b < batch; ++b)
+      if (hs[b].nonfinite) throw NumericalError("chambolle_pock: non-finite iterate");
   });
-  std::vector<SliceScalars> hs(batch);
-  CK(cudaMemcpyAsync(hs.data(), S.sc.p, sizeof(SliceScalars) * batch, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(mu, final_u, sizeof(float) * cnt, is_device_ptr(mu) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  for (int b = 0; b < batch; ++b)
-    if (hs[b].nonfinite) throw NumericalError("chambolle_pock: non-finite iterate");
   TOMO_CATCH
 }
 
@@ -1248,7 +1291,7 @@ int tomo_op_set_allreduce(tomo_op* op, tomo_allreduce_fn fn, void* user) {
   if (!op) throw ConfigError("null op");
   op->ar_fn = fn;
   op->ar_user = user;
-  op->graphs.clear();
+  op->clear_graphs();
   TOMO_CATCH
 }
 
@@ -1273,33 +1316,44 @@ int tomo_op_attach_nccl(tomo_op* op, const char id[128], int nranks, int rank) {
   if (r != ncclSuccess) throw CudaError(std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
   if (op->comm) ncclCommDestroy(op->comm);
   op->comm = comm;
-  for (auto& kv : op->graphs)
-    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
-  op->graphs.clear();
+  op->clear_graphs();
   TOMO_CATCH
 }
 
-int tomo_grad(int n, const float* u, float* gx, float* gy, int batch, void* stream) {
+int tomo_grad(int n, int precision, const void* u, void* gx, void* gy, int batch, void* stream) {
   TOMO_TRY
   if (n < 2 || batch < 1) throw ConfigError("grad: size mismatch");
   if (!is_device_ptr(u) || !is_device_ptr(gx) || !is_device_ptr(gy)) throw ConfigError("grad: device pointers required");
-  launch_grad(n, batch, u, gx, gy, S_(stream));
+  if (precision == TOMO_F64)
+    launch_grad<double>(n, batch, static_cast<const double*>(u), static_cast<double*>(gx), static_cast<double*>(gy),
+                        S_(stream));
+  else
+    launch_grad<float>(n, batch, static_cast<const float*>(u), static_cast<float*>(gx), static_cast<float*>(gy),
+                       S_(stream));
   TOMO_CATCH
 }
 
-int tomo_grad_adjoint(int n, const float* gx, const float* gy, float* out, int batch, void* stream) {
+int tomo_grad_adjoint(int n, int precision, const void* gx, const void* gy, void* out, int batch, void* stream) {
   TOMO_TRY
   if (n < 2 || batch < 1) throw ConfigError("grad_adjoint: size mismatch");
   if (!is_device_ptr(out) || !is_device_ptr(gx) || !is_device_ptr(gy))
     throw ConfigError("grad_adjoint: device pointers required");
-  launch_grad_adjoint(n, batch, gx, gy, out, S_(stream));
+  if (precision == TOMO_F64)
+    launch_grad_adjoint<double>(n, batch, static_cast<const double*>(gx), static_cast<const double*>(gy),
+                                static_cast<double*>(out), S_(stream));
+  else
+    launch_grad_adjoint<float>(n, batch, static_cast<const float*>(gx), static_cast<const float*>(gy),
+                               static_cast<float*>(out), S_(stream));
   TOMO_CATCH
 }
 
-int tomo_shrink(int64_t len, const float* x, double gamma, float* out, void* stream) {
+int tomo_shrink(int64_t len, int precision, const void* x, double gamma, void* out, void* stream) {
   TOMO_TRY
   if (!is_device_ptr(x) || !is_device_ptr(out)) throw ConfigError("shrink: device pointers required");
-  launch_shrink(len, x, static_cast<float>(gamma), out, S_(stream));
+  if (precision == TOMO_F64)
+    launch_shrink<double>(len, static_cast<const double*>(x), gamma, static_cast<double*>(out), S_(stream));
+  else
+    launch_shrink<float>(len, static_cast<const float*>(x), gamma, static_cast<float*>(out), S_(stream));
   TOMO_CATCH
 }
 
@@ -1360,20 +1414,135 @@ int tomo_random_ellipses(int n, int count, uint64_t seed, float* img) {
   TOMO_CATCH
 }
 
-int tomo_fft_rows(int m, int rows, const void* in, void* out, int inverse, void* stream) {
+int tomo_fft_rows(int m, int rows, int precision, const void* in, void* out, int inverse, void* stream) {
   TOMO_TRY
   if (!is_device_ptr(in) || !is_device_ptr(out)) throw ConfigError("fft_rows: device pointers required");
   if (m < 32 || m > 8192 || (m & (m - 1))) throw ConfigError("fft_rows: m must be a power of two in [32, 8192]");
-  std::vector<float2> tw(m);
-  for (int k = 0; k < m; ++k) {
-    const double ang = -2.0 * M_PI * k / m;
-    tw[k] = make_float2(static_cast<float>(std::cos(ang)), static_cast<float>(std::sin(ang)));
-  }
-  DevBuf<float2> dtw;
-  dtw.upload(tw, S_(stream));
-  launch_fft_rows_test(m, rows, dtw.p, static_cast<const float2*>(in), static_cast<float2*>(out), inverse != 0,
-                       S_(stream));
-  CK(cudaStreamSynchronize(S_(stream)));
+  auto run = [&](auto tag) {
+    using R = decltype(tag);
+    std::vector<cplx<R>> tw(m);
+    for (int k = 0; k < m; ++k) {
+      const double ang = -2.0 * M_PI * k / m;
+      tw[k].x = static_cast<R>(std::cos(ang));
+      tw[k].y = static_cast<R>(std::sin(ang));
+    }
+    Raw dtw;
+    dtw.upload(tw);
+    launch_fft_rows_test<R>(m, rows, dtw.as<cplx<R>>(), static_cast<const cplx<R>*>(in), static_cast<cplx<R>*>(out),
+                            inverse != 0, S_(stream));
+    CK(cudaStreamSynchronize(S_(stream)));
+  };
+  if (precision == TOMO_F64)
+    run(double{});
+  else
+    run(float{});
+  TOMO_CATCH
+}
+
+int tomo_profile_stages(tomo_op* op, int batch, int reps, double* ms, double* bytes, void* stream) {
+  TOMO_TRY
+  check_op(op, batch);
+  if (!ms || !bytes || reps < 1) throw ConfigError("profile: bad arguments");
+  DeviceGuard dg(op->device);
+  op->ensure_batch(batch);
+  const cudaStream_t st = S_(stream);
+  with_prec(op, [&](auto tag) {
+    using R = decltype(tag);
+    const int n = op->g.n, m = op->g.m;
+    const size_t cnt = static_cast<size_t>(batch) * op->L();
+    Scratch& S = op->sc;
+    // random-ish state so every kernel does its full work
+    std::vector<R> h(cnt);
+    std::mt19937 rng(5);
+    std::normal_distribution<double> nd;
+    for (auto& v : h) v = static_cast<R>(nd(rng));
+    for (auto* b : {&S.r, &S.p0, &S.p1, &S.x, &S.ap, &S.mu0, &S.mu1, &S.bx0, &S.by0, &S.fid, &S.rhs})
+      CK(cudaMemcpyAsync(b->p, h.data(), sizeof(R) * cnt, cudaMemcpyHostToDevice, st));
+    std::vector<SliceScalars> init(batch);
+    std::memset(init.data(), 0, sizeof(SliceScalars) * batch);
+    for (auto& sc : init) {
+      sc.rr[0] = sc.rr[1] = 1.0;
+      sc.pap = sc.pp = 1.0;
+      sc.first_upd = 1e300;
+    }
+    const SysParams sp = sysp(1.0, 1.0, 0.0, 0.0);
+    Reduce red = op->red();
+    OpDev<R> d = op->dev<R>(batch);
+    std::vector<cudaEvent_t> ev(TOMO_NUM_STAGES + 1);
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    double acc[TOMO_NUM_STAGES] = {0};
+    const bool sur = op->surrogate();
+    for (int rep = 0; rep < reps + 1; ++rep) {  // first rep is warm-up
+      CK(cudaMemcpyAsync(S.sc.p, init.data(), sizeof(SliceScalars) * batch, cudaMemcpyHostToDevice, st));
+      for (int k = 0; k <= TOMO_NUM_STAGES; ++k) {
+        if (k > 0) {
+          const int s = k - 1;
+          if (!sur) {
+            if (s == 0) {
+              PUpd<R> pu{};
+              pu.enabled = 1;
+              pu.r = S.r.as<R>();
+              pu.p = S.p0.as<R>();
+              pu.step = 1;
+              pu.red = red;
+              launch_t2_rows<R>(d, batch, S.p0.p, false, pu, st);
+            } else if (s == 1) {
+              launch_t2_cols<R>(d, batch, op->scal(), st);
+            } else if (s == 2) {
+              launch_w<R>(d, batch, d.g, d.s, op->scal(), st);
+            } else if (s == 3) {
+              launch_wt_rows<R>(d, batch, op->scal(), st);
+            } else if (s == 4) {
+              PbEpi<R> e = plain_epi<R>(PB_CG_STEP, 1.0);
+              e.p = S.p0.as<R>();
+              e.ap = S.ap.as<R>();
+              e.sys = sp;
+              e.step = 1;
+              e.red = red;
+              launch_t1_rows<R>(d, batch, e, st);
+            }
+          } else if (s == 7) {
+            launch_stencil<R>(n, batch, op->rad, op->coef, 0, S.p0.as<R>(), S.r.as<R>(), S.p1.as<R>(), S.ap.as<R>(),
+                              nullptr, nullptr, sp, 1, red, st);
+          }
+          if (s == 5) launch_cg_update<R>(n, batch, S.p0.as<R>(), S.ap.as<R>(), S.x.as<R>(), S.r.as<R>(), sp, 1, red, st);
+          if (s == 6)
+            launch_sb_post<R>(n, batch, S.mu1.as<R>(), S.mu0.as<R>(), S.bx0.as<R>(), S.by0.as<R>(), S.bx1.as<R>(),
+                              S.by1.as<R>(), S.fid.as<R>(), S.rhs.as<R>(), 1.0, red, st);
+        }
+        CK(cudaEventRecord(ev[k], st));
+      }
+      CK(cudaEventSynchronize(ev[TOMO_NUM_STAGES]));
+      if (rep == 0) continue;
+      for (int k = 0; k < TOMO_NUM_STAGES; ++k) {
+        float t = 0.f;
+        CK(cudaEventElapsedTime(&t, ev[k], ev[k + 1]));
+        acc[k] += t;
+      }
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    const double B = batch, nn = static_cast<double>(n) * n, mn = static_cast<double>(m) * n,
+                 mm = static_cast<double>(m) * m, P = static_cast<double>(op->g.P), rs = sizeof(R), cs = 2 * sizeof(R);
+    const double wbytes = static_cast<double>(op->Ppad) * op->nq * 32.0 * (16.0 + 4.0 * rs) / 32.0;
+    const double wtbytes = static_cast<double>(op->wt_slots) * sizeof(WtEnt<R>) + (mm / 32.0 + 1) * 4.0;
+    double by[TOMO_NUM_STAGES] = {0};
+    if (!sur) {
+      by[0] = B * (3 * rs * nn + cs * mn);                 // read p, r; write p; write H
+      by[1] = B * (cs * mn + cs * mm);                     // read H, write g
+      by[2] = wbytes + B * (cs * op->wt_rows + cs * P);    // W stream, touched grid nodes, samples
+      by[3] = wtbytes + B * (cs * P + cs * mn);            // W^T stream, samples, write K
+      by[4] = B * (cs * mn + 2 * rs * nn);                 // read K, p; write Ap
+    } else {
+      by[7] = B * 4 * rs * nn;  // read r, p; write p, Ap
+    }
+    by[5] = B * 6 * rs * nn;  // read x, r, p, Ap; write x, r
+    by[6] = B * 8 * rs * nn;  // read mu_new, mu_old, bx, by, fid; write bx, by, rhs
+    for (int k = 0; k < TOMO_NUM_STAGES; ++k) {
+      const bool on = sur ? (k >= 5) : (k <= 6);
+      ms[k] = on ? acc[k] / reps : 0.0;
+      bytes[k] = on ? by[k] : 0.0;
+    }
+  });
   TOMO_CATCH
 }
 

@@ -78,22 +78,35 @@ def _ptr(x):
     return x.ctypes.data_as(C.c_void_p)
 
 
-def _as_input(x, complex_: bool):
-    """Contiguous float32 / complex64 view of x (torch tensor or array-like)."""
+def _np_dtype(complex_: bool, f64: bool):
+    if complex_:
+        return np.complex128 if f64 else np.complex64
+    return np.float64 if f64 else np.float32
+
+
+def _torch_dtype(complex_: bool, f64: bool):
+    torch = _torch()
+    if complex_:
+        return torch.complex128 if f64 else torch.complex64
+    return torch.float64 if f64 else torch.float32
+
+
+def _as_input(x, complex_: bool, f64: bool = False):
+    """Contiguous view of x in the op's element type (torch tensor or array-like)."""
     if _is_torch(x):
-        torch = _torch()
-        want = torch.complex64 if complex_ else torch.float32
+        want = _torch_dtype(complex_, f64)
         if x.dtype != want:
             x = x.to(want)
         return x.contiguous()
-    return np.ascontiguousarray(x, dtype=np.complex64 if complex_ else np.float32)
+    return np.ascontiguousarray(x, dtype=_np_dtype(complex_, f64))
 
 
-def _empty_like_kind(x, shape, complex_: bool):
+def _empty_like_kind(x, shape, complex_: bool, f64: bool = False):
     if _is_torch(x):
         torch = _torch()
-        return torch.empty(shape, dtype=torch.complex64 if complex_ else torch.float32, device=x.device)
-    return np.empty(shape, dtype=np.complex64 if complex_ else np.float32)
+        pin = (not x.is_cuda) and x.is_pinned()
+        return torch.empty(shape, dtype=_torch_dtype(complex_, f64), device=x.device, pin_memory=pin)
+    return np.empty(shape, dtype=_np_dtype(complex_, f64))
 
 
 @dataclass
@@ -189,15 +202,20 @@ class NormalBackend:
     """
 
     def __init__(self, geom: Geometry, kind: str = "direct", surrogate_r: int = 1, euclidean: bool = False,
-                 device: int = 0, angle_block: tuple[int, int] | None = None, max_batch: int = 1):
+                 device: int = 0, angle_block: tuple[int, int] | None = None, max_batch: int = 1,
+                 precision: str = "f32"):
         if kind not in ("direct", "surrogate"):
             raise ConfigError(f"unknown backend: {kind}")
+        if precision not in ("f32", "f64"):
+            raise ConfigError(f"unknown precision: {precision}")
         self.geom = geom
         self.kind = kind
         self.device = device
+        self.precision = precision
+        self.f64 = precision == "f64"
         ab = angle_block or (0, 0)
         desc = _lib.OpDesc(_lib.BACKEND_DIRECT if kind == "direct" else _lib.BACKEND_SURROGATE, surrogate_r,
-                           int(euclidean), device, ab[0], ab[1], max_batch)
+                           int(euclidean), device, ab[0], ab[1], max_batch, _lib.F64 if self.f64 else _lib.F32)
         gd = geom._desc()
         h = C.c_void_p()
         _check(lib().tomo_op_create(C.byref(gd), C.byref(desc), C.byref(h)))
@@ -236,9 +254,9 @@ class NormalBackend:
         return size // per_item
 
     def _unary(self, fn, x, in_complex, out_complex, in_items, out_shape_of):
-        x = _as_input(x, in_complex)
+        x = _as_input(x, in_complex, self.f64)
         B = self._batch(x, in_items)
-        out = _empty_like_kind(x, out_shape_of(x, B), out_complex)
+        out = _empty_like_kind(x, out_shape_of(x, B), out_complex, self.f64)
         _check(fn(self._h, _ptr(x), _ptr(out), B, _stream_ptr(x)))
         return out
 
@@ -282,21 +300,21 @@ class NormalBackend:
         """make_subproblem backprojection (solver.cpp:200-213)."""
         if weighted is None:
             weighted = self.kind == "surrogate"
-        f = _as_input(slice_data, True)
+        f = _as_input(slice_data, True, self.f64)
         B = self._batch(f, self.info.P)
         n = self.geom.n
-        out = _empty_like_kind(f, (B, n, n), False)
+        out = _empty_like_kind(f, (B, n, n), False, self.f64)
         _check(lib().tomo_backproject(self._h, float(alpha), int(weighted), _ptr(f), _ptr(out), B, _stream_ptr(f)))
         return out
 
     # ---------------------------------------------------------------- solvers
     def cg(self, rhs, x0=None, alpha=1.0, lambda_=1.0, shift=0.0, steps=5, rel_tol=0.0):
         """cg_solve (solver.cpp:56-95) on alpha*B + lambda*K'K + shift*I; returns (x, [CgStats])."""
-        b = _as_input(rhs, False)
+        b = _as_input(rhs, False, self.f64)
         n2 = self.geom.n ** 2
         B = self._batch(b, n2)
-        x0c = _as_input(x0, False) if x0 is not None else None
-        x = _empty_like_kind(b, self._img_shape(b, B), False)
+        x0c = _as_input(x0, False, self.f64) if x0 is not None else None
+        x = _empty_like_kind(b, self._img_shape(b, B), False, self.f64)
         sysd = _lib.System(alpha, lambda_, shift)
         st = (_lib.CgStats * B)()
         _check(lib().tomo_cg(self._h, C.byref(sysd), _ptr(b), _ptr(x0c), _ptr(x), steps, rel_tol, B, st,
@@ -305,10 +323,10 @@ class NormalBackend:
 
     def split_bregman(self, slice_data, config: SolverConfig):
         """split_bregman_tv (solver.cpp:219-307) on a batch of slices; returns (mu, [SolveTrace])."""
-        f = _as_input(slice_data, True)
+        f = _as_input(slice_data, True, self.f64)
         B = self._batch(f, self.info.P)
         n = self.geom.n
-        mu = _empty_like_kind(f, (B, n, n), False)
+        mu = _empty_like_kind(f, (B, n, n), False, self.f64)
         cfg = _lib.SbConfig(config.alpha, config.lambda_, config.max_bregman_iters, config.cg_steps_per_update,
                             config.update_tol_rel, int(config.warm_start),
                             -1.0 if config.sigma_override is None else float(config.sigma_override))
@@ -326,31 +344,42 @@ class NormalBackend:
 
     def tikhonov(self, slice_data, alpha=1.0, steps=20, rel_tol=0.0):
         """Config-1 KKT solve: (alpha N + I) mu = alpha Re(F_NU f), fixed steps (solver.cpp:309-337)."""
-        f = _as_input(slice_data, True)
+        f = _as_input(slice_data, True, self.f64)
         B = self._batch(f, self.info.P)
         n = self.geom.n
-        mu = _empty_like_kind(f, (B, n, n), False)
+        mu = _empty_like_kind(f, (B, n, n), False, self.f64)
         _check(lib().tomo_tikhonov(self._h, float(alpha), _ptr(f), _ptr(mu), steps, rel_tol, B, _stream_ptr(f)))
         return mu
 
     def chambolle_pock(self, slice_data, alpha=1.0, lambda_=1.0, tau_cp=0.35, sigma_cp=0.35, theta=1.0,
                        iters=10, cg_steps=15):
         """Chambolle-Pock anisotropic TV with CG primal prox (extension of PAPER.md:40-48)."""
-        f = _as_input(slice_data, True)
+        f = _as_input(slice_data, True, self.f64)
         B = self._batch(f, self.info.P)
         n = self.geom.n
-        mu = _empty_like_kind(f, (B, n, n), False)
+        mu = _empty_like_kind(f, (B, n, n), False, self.f64)
         cfg = _lib.CpConfig(alpha, lambda_, tau_cp, sigma_cp, theta, iters, cg_steps)
         _check(lib().tomo_chambolle_pock(self._h, C.byref(cfg), _ptr(f), _ptr(mu), B, _stream_ptr(f)))
         return mu
+
+    def profile_stages(self, batch=1, reps=20):
+        """Per-kernel device time (ms, CUDA events on the current stream) and algorithmic bytes
+        of one hot-path solver step; {name: (ms, bytes)} for the stages this backend runs."""
+        torch = _torch()
+        ms = np.zeros(_lib.NUM_STAGES)
+        by = np.zeros(_lib.NUM_STAGES)
+        stream = C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+        _check(lib().tomo_profile_stages(self._h, batch, reps, ms.ctypes.data_as(C.c_void_p),
+                                         by.ctypes.data_as(C.c_void_p), stream))
+        return {name: (float(ms[i]), float(by[i])) for i, name in enumerate(_lib.STAGE_NAMES) if by[i] > 0}
 
     # ---------------------------------------------------------------- multi-GPU
     def attach_nccl(self, unique_id: bytes, nranks: int, rank: int):
         _check(lib().tomo_op_attach_nccl(self._h, unique_id, nranks, rank))
 
     def set_allreduce(self, fn):
-        """fn(buf_ptr:int, count:int, stream_ptr:int) -> None, summing float32 in place."""
-        def cb(buf, count, stream, user):
+        """fn(buf_ptr:int, count:int, stream_ptr:int) -> None, summing the op's element type in place."""
+        def cb(buf, count, precision, stream, user):
             try:
                 fn(buf, count, stream)
                 return 0
@@ -399,32 +428,40 @@ def radial_density_weights(geom: Geometry) -> np.ndarray:
     return np.tile(w, geom.n_angles)
 
 
-def grad(u):
-    """grad (solver.cpp:12-25) on a CUDA tensor (.., n, n)."""
+def _prec_of(x):
     torch = _torch()
-    u = u.contiguous().float()
+    if x.dtype == torch.float64:
+        return _lib.F64, x.contiguous()
+    return _lib.F32, x.contiguous().float()
+
+
+def grad(u):
+    """grad (solver.cpp:12-25) on a CUDA tensor (.., n, n), float32 or float64."""
+    torch = _torch()
+    prec, u = _prec_of(u)
     n = u.shape[-1]
     B = u.numel() // (n * n)
     gx, gy = torch.empty_like(u), torch.empty_like(u)
-    _check(lib().tomo_grad(n, _ptr(u), _ptr(gx), _ptr(gy), B, _stream_ptr(u)))
+    _check(lib().tomo_grad(n, prec, _ptr(u), _ptr(gx), _ptr(gy), B, _stream_ptr(u)))
     return gx, gy
 
 
 def grad_adjoint(gx, gy):
     torch = _torch()
-    gx, gy = gx.contiguous().float(), gy.contiguous().float()
+    prec, gx = _prec_of(gx)
+    gy = gy.contiguous().to(gx.dtype)
     n = gx.shape[-1]
     B = gx.numel() // (n * n)
     out = torch.empty_like(gx)
-    _check(lib().tomo_grad_adjoint(n, _ptr(gx), _ptr(gy), _ptr(out), B, _stream_ptr(gx)))
+    _check(lib().tomo_grad_adjoint(n, prec, _ptr(gx), _ptr(gy), _ptr(out), B, _stream_ptr(gx)))
     return out
 
 
 def shrink(x, gamma: float):
     torch = _torch()
-    x = x.contiguous().float()
+    prec, x = _prec_of(x)
     out = torch.empty_like(x)
-    _check(lib().tomo_shrink(x.numel(), _ptr(x), float(gamma), _ptr(out), _stream_ptr(x)))
+    _check(lib().tomo_shrink(x.numel(), prec, _ptr(x), float(gamma), _ptr(out), _stream_ptr(x)))
     return out
 
 
@@ -447,8 +484,10 @@ def kernel_launches() -> int:
 def fft_rows(x, inverse=False):
     """Test hook: batched length-m FFT rows through the in-CTA Stockham kernel (unscaled)."""
     torch = _torch()
-    x = x.contiguous().to(torch.complex64)
+    f64 = x.dtype == torch.complex128
+    x = x.contiguous().to(torch.complex128 if f64 else torch.complex64)
     rows, m = x.shape
     out = torch.empty_like(x)
-    _check(lib().tomo_fft_rows(m, rows, _ptr(x), _ptr(out), int(inverse), _stream_ptr(x)))
+    _check(lib().tomo_fft_rows(m, rows, _lib.F64 if f64 else _lib.F32, _ptr(x), _ptr(out), int(inverse),
+                               _stream_ptr(x)))
     return out

@@ -27,8 +27,18 @@ def pgeom(T, og: O.Geometry):
                       win_hi=og.win_hi, tau=og.tau)
 
 
-def cuda(x, complex_=False):
-    return torch.from_numpy(np.ascontiguousarray(x, np.complex64 if complex_ else np.float32)).cuda()
+def cuda(x, complex_=False, f64=False):
+    if f64:
+        dt = np.complex128 if complex_ else np.float64
+    else:
+        dt = np.complex64 if complex_ else np.float32
+    return torch.from_numpy(np.ascontiguousarray(x, dt)).cuda()
+
+
+# fp32 operator parity is the north star's 1e-5; the fp64 path (used by the W-backend
+# solvers) must agree with the fp64 oracle to rounding.
+OP_TOL_F64 = 1e-11
+PRECS = ["f32", "f64"]
 
 
 RNG = np.random.default_rng(2024)
@@ -43,29 +53,38 @@ GEOMS = {
 }
 
 
+@pytest.mark.parametrize("prec", PRECS)
 @pytest.mark.parametrize("m", [32, 64, 128, 256, 512, 1024, 2048, 4096, 8192])
-def test_fft_rows(T, m):
+def test_fft_rows(T, m, prec):
+    f64 = prec == "f64"
+    tol = 1e-13 if f64 else 2e-6
     x = RNG.standard_normal((3, m)) + 1j * RNG.standard_normal((3, m))
-    out = T.tomo.fft_rows(cuda(x, True)).cpu().numpy()
-    assert rel(out, np.fft.fft(x, axis=1)) < 2e-6
-    outi = T.tomo.fft_rows(cuda(x, True), inverse=True).cpu().numpy()
-    assert rel(outi, np.fft.ifft(x, axis=1) * m) < 2e-6
+    out = T.tomo.fft_rows(cuda(x, True, f64)).cpu().numpy()
+    assert rel(out, np.fft.fft(x, axis=1)) < tol
+    outi = T.tomo.fft_rows(cuda(x, True, f64), inverse=True).cpu().numpy()
+    assert rel(outi, np.fft.ifft(x, axis=1) * m) < tol
 
 
+@pytest.mark.parametrize("prec", PRECS)
 @pytest.mark.parametrize("name", list(GEOMS))
-def test_forward_adjoint_normal(T, name):
+def test_forward_adjoint_normal(T, name, prec):
+    f64 = prec == "f64"
+    tol = OP_TOL_F64 if f64 else OP_TOL
     og = O.Geometry(**GEOMS[name])
-    op = T.make_direct_backend(pgeom(T, og))
+    op = T.make_direct_backend(pgeom(T, og), precision=prec)
     n = og.n
     u = RNG.standard_normal((n, n)) + 1j * RNG.standard_normal((n, n))
     s = RNG.standard_normal(og.P) + 1j * RNG.standard_normal(og.P)
-    u32 = u.astype(np.complex64)
-    s32 = s.astype(np.complex64)
-    assert rel(op.forward(cuda(u32, True)).cpu().numpy().ravel(), O.type2(og, u32)) < OP_TOL
-    assert rel(op.adjoint(cuda(s32, True)).cpu().numpy().ravel(), O.type1(og, s32).ravel()) < OP_TOL
-    assert rel(op.apply_normal(cuda(u32, True)).cpu().numpy().ravel(), O.apply_normal(og, u32).ravel()) < OP_TOL
-    ur = RNG.standard_normal((n, n)).astype(np.float32)
-    assert rel(op.apply_normal_real(cuda(ur)).cpu().numpy().ravel(), O.apply_normal_real(og, ur).ravel()) < OP_TOL
+    if not f64:  # same input bytes to both sides
+        u = u.astype(np.complex64)
+        s = s.astype(np.complex64)
+    assert rel(op.forward(cuda(u, True, f64)).cpu().numpy().ravel(), O.type2(og, u)) < tol
+    assert rel(op.adjoint(cuda(s, True, f64)).cpu().numpy().ravel(), O.type1(og, s).ravel()) < tol
+    assert rel(op.apply_normal(cuda(u, True, f64)).cpu().numpy().ravel(), O.apply_normal(og, u).ravel()) < tol
+    ur = RNG.standard_normal((n, n))
+    if not f64:
+        ur = ur.astype(np.float32)
+    assert rel(op.apply_normal_real(cuda(ur, False, f64)).cpu().numpy().ravel(), O.apply_normal_real(og, ur).ravel()) < tol
 
 
 def test_spmv_pair_matches_interpolate_spread(T):
@@ -108,13 +127,17 @@ def gold_geom(T, d):
     return T.Geometry(n=int(d["n"]), n_angles=int(d["n_angles"]), win_lo=-msp, win_hi=msp, tau=float(d["tau"]))
 
 
-def test_golden_operator(T, gold):
+@pytest.mark.parametrize("prec", PRECS)
+def test_golden_operator(T, gold, prec):
     """CUDA path vs outputs of the reference itself (tests/golden, built from /root/reference)."""
-    op = T.make_direct_backend(gold_geom(T, gold))
-    assert rel(op.forward(cuda(gold["u"], True)).cpu().numpy().ravel(), gold["type2_u"]) < OP_TOL
-    assert rel(op.adjoint(cuda(gold["s"], True)).cpu().numpy().ravel(), gold["type1_s"].ravel()) < OP_TOL
-    assert rel(op.apply_normal(cuda(gold["u"], True)).cpu().numpy().ravel(), gold["normal_u"].ravel()) < OP_TOL
-    assert rel(op.apply_normal_real(cuda(gold["ur"])).cpu().numpy().ravel(), gold["normal_real_ur"].ravel()) < OP_TOL
+    f64 = prec == "f64"
+    tol = OP_TOL_F64 if f64 else OP_TOL
+    op = T.make_direct_backend(gold_geom(T, gold), precision=prec)
+    assert rel(op.forward(cuda(gold["u"], True, f64)).cpu().numpy().ravel(), gold["type2_u"]) < tol
+    assert rel(op.adjoint(cuda(gold["s"], True, f64)).cpu().numpy().ravel(), gold["type1_s"].ravel()) < tol
+    assert rel(op.apply_normal(cuda(gold["u"], True, f64)).cpu().numpy().ravel(), gold["normal_u"].ravel()) < tol
+    assert rel(op.apply_normal_real(cuda(gold["ur"], False, f64)).cpu().numpy().ravel(),
+               gold["normal_real_ur"].ravel()) < tol
 
 
 def test_golden_surrogate(T, gold):
@@ -126,18 +149,18 @@ def test_golden_surrogate(T, gold):
 
 
 def test_golden_cg(T, gold):
-    op = T.make_direct_backend(gold_geom(T, gold))
-    x, st = op.cg(cuda(gold["cg_rhs"]), alpha=10.0, lambda_=1.0, steps=5)
-    assert rel(x.cpu().numpy().ravel(), gold["cg_x"].ravel()) < 1e-4
+    op = T.make_direct_backend(gold_geom(T, gold), precision="f64")
+    x, st = op.cg(cuda(gold["cg_rhs"], False, True), alpha=10.0, lambda_=1.0, steps=5)
+    assert rel(x.cpu().numpy().ravel(), gold["cg_x"].ravel()) < 1e-8
     assert abs(st[0].min_ritz - float(gold["cg_min_ritz"])) < 1e-4 * abs(float(gold["cg_min_ritz"]))
     assert st[0].steps_run == 5
 
 
 def test_golden_split_bregman(T, gold):
     g = gold_geom(T, gold)
-    op = T.make_direct_backend(g)
+    op = T.make_direct_backend(g, precision="f64")
     cfg = T.SolverConfig(alpha=10.0, lambda_=1.0, max_bregman_iters=5, cg_steps_per_update=5, update_tol_rel=0.0)
-    mu, tr = op.split_bregman(cuda(gold["data"], True), cfg)
+    mu, tr = op.split_bregman(cuda(gold["data"], True, True), cfg)
     assert rel(mu.cpu().numpy().ravel(), gold["sb_direct_mu"].ravel()) < REC_TOL
     assert rel(tr[0].update_l1, gold["sb_direct_upd"]) < REC_TOL
     assert abs(tr[0].imag_leakage - float(gold["sb_direct_leak"])) < 1e-3 * max(float(gold["sb_direct_leak"]), 1e-6) + 1e-6
@@ -149,8 +172,8 @@ def test_golden_split_bregman(T, gold):
 
 
 def test_golden_tikhonov(T, gold):
-    op = T.make_direct_backend(gold_geom(T, gold))
-    mu = op.tikhonov(cuda(gold["data"], True), alpha=1.0, steps=20)
+    op = T.make_direct_backend(gold_geom(T, gold), precision="f64")
+    mu = op.tikhonov(cuda(gold["data"], True, True), alpha=1.0, steps=20)
     assert rel(mu.cpu().numpy().ravel(), gold["tikhonov_mu"].ravel()) < REC_TOL
 
 
@@ -162,9 +185,9 @@ def test_sb_extension_geometry_and_batch(T):
         ph = O.random_ellipses(n, 10, seed)
         f, _ = O.synthesize(og, ph, 0.01, seed)
         fs.append(f.astype(np.complex64))
-    op = T.make_direct_backend(pgeom(T, og), max_batch=2)
+    op = T.make_direct_backend(pgeom(T, og), max_batch=2, precision="f64")
     cfg = T.SolverConfig(alpha=10.0, lambda_=1.0, max_bregman_iters=6, cg_steps_per_update=4, update_tol_rel=0.0)
-    mu, tr = op.split_bregman(cuda(np.stack(fs), True), cfg)
+    mu, tr = op.split_bregman(cuda(np.stack(fs), True, True), cfg)
     for b in range(2):
         ref, upd, _ = O.split_bregman(og, fs[b], backend=0, alpha=10.0, lam=1.0, max_iters=6, cg_steps=4)
         assert rel(mu[b].cpu().numpy(), ref) < REC_TOL
@@ -175,10 +198,10 @@ def test_sb_tolerance_stop(T):
     og = O.Geometry(**GEOMS["ref_msp6"])
     ph = O.shepp_logan(og.n)
     f, _ = O.synthesize(og, ph, 0.0, 0)
-    op = T.make_direct_backend(pgeom(T, og))
+    op = T.make_direct_backend(pgeom(T, og), precision="f64")
     cfg = T.SolverConfig(alpha=1.0, lambda_=1.0, max_bregman_iters=40, cg_steps_per_update=5, update_tol_rel=0.05)
-    mu, tr = op.split_bregman(cuda(f, True), cfg)
-    ref, upd, otr = O.split_bregman(og, f.astype(np.complex64), backend=0, alpha=1.0, lam=1.0, max_iters=40,
+    mu, tr = op.split_bregman(cuda(f, True, True), cfg)
+    ref, upd, otr = O.split_bregman(og, f, backend=0, alpha=1.0, lam=1.0, max_iters=40,
                                     cg_steps=5, update_tol_rel=0.05)
     assert tr[0].stopping_reason == "tolerance" and otr.stopped_on_tolerance == 1
     assert tr[0].iterations == otr.iterations
@@ -208,11 +231,10 @@ def test_chambolle_pock_vs_oracle(T):
     og = O.Geometry(**GEOMS["R4_gl_tau"])
     ph = O.random_ellipses(og.n, 6, 11)
     f, _ = O.synthesize(og, ph, 0.01, 11)
-    op = T.make_direct_backend(pgeom(T, og))
+    op = T.make_direct_backend(pgeom(T, og), precision="f64")
     kw = dict(alpha=1e-2, lambda_=1e-2, tau_cp=0.35, sigma_cp=0.35, theta=1.0, iters=4, cg_steps=6)
-    mu = op.chambolle_pock(cuda(f, True), **kw)
-    ref = O.chambolle_pock(og, f.astype(np.complex64), alpha=1e-2, lam=1e-2, tau_cp=0.35, sigma_cp=0.35, theta=1.0,
-                           iters=4, cg_steps=6)
+    mu = op.chambolle_pock(cuda(f, True, True), **kw)
+    ref = O.chambolle_pock(og, f, alpha=1e-2, lam=1e-2, tau_cp=0.35, sigma_cp=0.35, theta=1.0, iters=4, cg_steps=6)
     assert rel(mu.cpu().numpy(), ref) < REC_TOL
 
 
@@ -230,15 +252,19 @@ def test_angle_shards_sum_to_full(T):
     assert rel(tot, full.apply_normal_real(cuda(u)).cpu().numpy()) < 1e-6
 
 
-def test_grad_shrink_ops(T):
+@pytest.mark.parametrize("prec", PRECS)
+def test_grad_shrink_ops(T, prec):
+    f64 = prec == "f64"
     n = 33
-    u = RNG.standard_normal((n, n)).astype(np.float32)
-    gx, gy = T.grad(cuda(u))
+    u = RNG.standard_normal((n, n))
+    if not f64:
+        u = u.astype(np.float32)
+    gx, gy = T.grad(cuda(u, False, f64))
     ogx, ogy = O.grad(u.astype(np.float64))
     assert np.allclose(gx.cpu().numpy(), ogx, atol=1e-6) and np.allclose(gy.cpu().numpy(), ogy, atol=1e-6)
     adj = T.grad_adjoint(gx, gy).cpu().numpy()
     assert np.allclose(adj, O.grad_adjoint(ogx, ogy), atol=1e-5)
-    sh = T.shrink(cuda(u), 0.5).cpu().numpy()
+    sh = T.shrink(cuda(u, False, f64), 0.5).cpu().numpy()
     assert np.allclose(sh, O.shrink(u.astype(np.float64), 0.5), atol=1e-6)
 
 
