@@ -32,6 +32,8 @@ struct RefSetup {
   std::shared_ptr<const SliceTransform> transform;
 };
 
+thread_local int g_nb = 0;  // radial samples per angle for the next setup (0 -> n)
+
 RefSetup make_setup(int n, int n_angles, int m_sp, double tau) {
   AngleSet set;
   set.subsample_d = 1;
@@ -39,7 +41,27 @@ RefSetup make_setup(int n, int n_angles, int m_sp, double tau) {
   for (int a = 0; a < n_angles; ++a) set.angles[a] = a * M_PI / n_angles;
   RefSetup s;
   s.params = tau > 0 ? make_params(m_sp, tau, n) : make_params(m_sp, static_cast<double>(m_sp) / (double(n) * n), n);
-  s.grid = slice_points(set, n);
+  const int nb = g_nb > 0 ? g_nb : n;
+  if (nb == n) {
+    s.grid = slice_points(set, n);
+  } else {
+    // Extension D1 (n_b != n radial samples): the same angle-major lattice as slice_points
+    // (fourier_slice.cpp:22-41) with spacing 2*pi/n_b, fed through the reference's own
+    // FrequencyPointSet::make and SliceTransform.
+    Eigen::MatrixXd coords(static_cast<Eigen::Index>(n_angles) * nb, 2);
+    Eigen::Index row = 0;
+    for (int a = 0; a < n_angles; ++a) {
+      const double c = std::cos(set.angles[a]), sn = std::sin(set.angles[a]);
+      for (int t = 0; t < nb; ++t, ++row) {
+        const double k_r = (2.0 * M_PI / nb) * (t - nb / 2);
+        coords(row, 0) = k_r * c;
+        coords(row, 1) = k_r * sn;
+      }
+    }
+    s.grid.angle_set = set;
+    s.grid.n = n;
+    s.grid.points = FrequencyPointSet::make(2, std::move(coords));
+  }
   s.transform = std::make_shared<const SliceTransform>(s.grid, s.params);
   return s;
 }
@@ -74,6 +96,9 @@ int code_of(const std::exception& e) {
 extern "C" {
 
 const char* ref_last_error(void) { return g_err.c_str(); }
+
+// Radial samples per angle for subsequent calls on this thread (0 -> n, the reference).
+void ref_set_nb(int nb) { g_nb = nb; }
 
 int ref_points(int n, int A, int m_sp, double tau, double* coords) {
   REF_TRY

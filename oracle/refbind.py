@@ -45,6 +45,7 @@ def lib():
         _LIB.ref_tikhonov_identity.argtypes = [C.c_int, C.c_int, C.c_int, d, d, C.c_void_p, C.c_int,
                                                C.c_void_p]
         _LIB.ref_shepp_logan.argtypes = [C.c_int, C.c_void_p]
+        _LIB.ref_set_nb.argtypes = [C.c_int]
         _LIB.ref_synthesize.argtypes = [C.c_int, C.c_int, C.c_int, d, C.c_void_p, d, C.c_uint64, C.c_void_p]
     return _LIB
 
@@ -59,13 +60,17 @@ def _p(a):
 
 
 class Ref:
-    """Reference geometry: n_b = n, R = 2, window [-m_sp, m_sp], theta_a = a*pi/A."""
+    """Reference geometry: R = 2, window [-m_sp, m_sp], theta_a = a*pi/A; n_b radial samples
+    (default n, the reference; other values go through the reference's FrequencyPointSet /
+    SliceTransform with the slice_points lattice at spacing 2*pi/n_b)."""
 
-    def __init__(self, n, n_angles, m_sp, tau=None):
+    def __init__(self, n, n_angles, m_sp, tau=None, n_b=0):
         self.n, self.A, self.m_sp = n, n_angles, m_sp
+        self.n_b = n_b or n
         self.tau = tau if tau is not None else m_sp / float(n * n)
-        self.P = n * n_angles
+        self.P = self.n_b * n_angles
         self._a = (n, n_angles, m_sp, self.tau)
+        lib().ref_set_nb(self.n_b)
 
     def points(self):
         out = np.empty((self.P, 2))
