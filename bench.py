@@ -289,11 +289,11 @@ class Workload:
         if k in ("sb", "c1"):
             steps = c.get("cg", 10)
             iters = c.get("iters", 1)
-            counts = {"t2_rows": iters * (steps + 1), "t2_cols": iters * (steps + 1), "w_spmv": iters * (steps + 1),
-                      "wt_rows": iters * (steps + 1), "t1_rows": iters * (steps + 1), "cg_update": iters * steps,
-                      "sb_post": iters}
+            a = iters * (steps + 1)
+            counts = {"t2_rows": a, "t2_cols": a, "w_spmv": a, "wt_spread": a, "t1_cols": a, "t1_rows": a,
+                      "cg_update": iters * steps, "sb_post": iters}
         elif k == "apply":
-            counts = {"t2_rows": 1, "t2_cols": 1, "w_spmv": 1, "wt_rows": 1, "t1_rows": 1}
+            counts = {"t2_rows": 1, "t2_cols": 1, "w_spmv": 1, "wt_spread": 1, "t1_cols": 1, "t1_rows": 1}
         else:  # surrogate
             counts = {"stencil": c["iters"] * (c["cg"] + 1), "cg_update": c["iters"] * c["cg"], "sb_post": c["iters"]}
         share = {s: counts.get(s, 0) * prof[s][0] for s in prof}

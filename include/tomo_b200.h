@@ -197,11 +197,11 @@ int tomo_fft_rows(int m, int rows, int precision, const void* in, void* out, int
  * returns, per stage, the mean device time (ms) and the algorithmic HBM bytes one launch
  * moves. Stage ids:
  *   0 t2_rows (P1: p-update + deapod + pad + row iFFT)   1 t2_cols (P2: column iFFT)
- *   2 w (W SELL-32 SpMV)   3 wt_rows (W^T SpMV + first type-1 FFT pass)
- *   4 t1_rows (PB: FFT + crop + deapod + CG epilogue)   5 cg_update   6 sb_post
- *   7 stencil (surrogate T + K'K + CG dots)
+ *   2 w (W SELL-32 SpMV)   3 wt_spread (W^T task SpMV + split-block fix-up)
+ *   4 t1_cols (PA: grid-row FFT, pruned)   5 t1_rows (PB: FFT + crop + deapod + CG epilogue)
+ *   6 cg_update   7 sb_post   8 stencil (surrogate T + K'K + CG dots)
  * Stages that do not apply to the backend report 0. Returns TOMO_OK. */
-#define TOMO_NUM_STAGES 8
+#define TOMO_NUM_STAGES 9
 int tomo_profile_stages(tomo_op* op, int batch, int reps, double* ms, double* bytes, void* stream);
 
 /* Number of library kernels launched since load (for the bench's gpu_launches claim). */

@@ -23,8 +23,8 @@ BACKEND_DIRECT = 0
 BACKEND_SURROGATE = 2
 F32 = 0
 F64 = 1
-NUM_STAGES = 8
-STAGE_NAMES = ["t2_rows", "t2_cols", "w_spmv", "wt_rows", "t1_rows", "cg_update", "sb_post", "stencil"]
+NUM_STAGES = 9
+STAGE_NAMES = ["t2_rows", "t2_cols", "w_spmv", "wt_spread", "t1_cols", "t1_rows", "cg_update", "sb_post", "stencil"]
 
 
 class GeomDesc(C.Structure):

@@ -1,11 +1,14 @@
-// fft.cuh — in-CTA Stockham FFT over shared memory (sm_100a).
+// fft.cuh — in-CTA Stockham FFT rows (sm_100a).
 //
-// Replaces the reference's per-row Eigen/kissfft calls (proj/src/fft.cpp:26-50). One CTA
-// transforms `rows` rows of length M (power of two, 32 <= M <= 8192) that already sit in
-// shared memory with the pad16() layout and row stride padded_len(M). Each row is served
-// by M/16 threads; passes are radix-16 (registers) with a final radix-2/4/8 pass, one
-// smem exchange per pass (Stockham autosort, natural-order output). Twiddles come from a
-// per-length table e^{-2 pi i k / M} built on the host in fp64.
+// Replaces the reference's per-row Eigen/kissfft calls (proj/src/fft.cpp:26-50). A CTA
+// transforms `rpc` rows of length M (power of two, 32 <= M <= 8192); each row is served by
+// M/16 threads. Passes are radix-16 in registers with a final radix-2/4/8 pass (Stockham
+// autosort, natural-order output). The FIRST pass loads its 16 inputs per thread straight
+// from global memory through a caller-supplied loader (coalesced: thread j reads j + r*M/16)
+// and the LAST pass hands its outputs straight to a caller-supplied storer (coalesced for the
+// natural-order row stores); only the middle exchanges go through shared memory (pad16
+// layout, conflict-free). Twiddles w^1, w^2, w^4, w^8 come from a per-length fp64-built
+// table e^{-2 pi i k/M}; the other powers are products of those (<= 3 roundings deep).
 //
 // Only the forward (e^{-i}) transform is implemented; inverse transforms conjugate on load
 // and on store (ifft(x) = conj(fft(conj(x))), unscaled; the 1/m factors are folded into
@@ -104,36 +107,71 @@ struct FftShape {
                            : (M >= 512) ? 9 : (M >= 256) ? 8 : (M >= 128) ? 7 : (M >= 64) ? 6 : 5;
   static constexpr int N16 = LOG / 4;          // number of radix-16 passes
   static constexpr int RL = 1 << (LOG % 4);    // final radix (1 = none)
+  static constexpr int NP = N16 + (RL > 1 ? 1 : 0);
   static constexpr int T = M / 16;             // threads per row
-  static constexpr int STRIDE = padded_len(M); // smem row stride (float2)
+  static constexpr int STRIDE = padded_len(M); // smem row stride (elements)
   static_assert((1 << LOG) == M, "M must be a power of two in [32, 8192]");
+  static_assert(NP >= 2, "at least two passes");
 };
 
-// One Stockham pass of radix R with sub-transform size Ns over a row in smem.
-// Thread `t` (0..T-1) of the row handles butterflies j = t, t+T, ... (M/R of them).
-// Every thread of the CTA executes both barriers; `active` gates the work only.
-template <int M, int R, typename C2>
-TOMO_DEV void stockham_pass(C2* row, const C2* __restrict__ tw, int Ns, int t, bool active) {
+// v[r] *= W^{r * base} for r = 1..R-1, W = e^{-2 pi i / M}: four table loads, the rest by
+// products (w3 = w1 w2, w5 = w4 w1, ..., w15 = w8 w7).
+template <int R, typename C2>
+TOMO_DEV void twiddle(C2* v, const C2* __restrict__ tw, int base) {
+  const C2 w1 = __ldg(&tw[base]);
+  v[1] = cmul(v[1], w1);
+  if constexpr (R >= 4) {
+    const C2 w2 = __ldg(&tw[2 * base]);
+    const C2 w3 = cmul(w1, w2);
+    v[2] = cmul(v[2], w2);
+    v[3] = cmul(v[3], w3);
+    if constexpr (R >= 8) {
+      const C2 w4 = __ldg(&tw[4 * base]);
+      const C2 w5 = cmul(w4, w1), w6 = cmul(w4, w2), w7 = cmul(w4, w3);
+      v[4] = cmul(v[4], w4);
+      v[5] = cmul(v[5], w5);
+      v[6] = cmul(v[6], w6);
+      v[7] = cmul(v[7], w7);
+      if constexpr (R >= 16) {
+        const C2 w8 = __ldg(&tw[8 * base]);
+        v[8] = cmul(v[8], w8);
+        v[9] = cmul(v[9], cmul(w8, w1));
+        v[10] = cmul(v[10], cmul(w8, w2));
+        v[11] = cmul(v[11], cmul(w8, w3));
+        v[12] = cmul(v[12], cmul(w8, w4));
+        v[13] = cmul(v[13], cmul(w8, w5));
+        v[14] = cmul(v[14], cmul(w8, w6));
+        v[15] = cmul(v[15], cmul(w8, w7));
+      }
+    }
+  }
+}
+
+// One Stockham pass (radix R, sub-transform size Ns) of the row owned by this thread group.
+// FIRST: inputs come from load(i) (global), otherwise from the smem row. LAST: outputs go to
+// store(k, value), otherwise back into the smem row. Every thread of the CTA must call each
+// pass (barriers inside); `active` gates the work. STORE_SMEM_LAST: the storer writes the smem
+// row, so a barrier separates the last reads from those writes.
+template <int M, int R, bool FIRST, bool LAST, bool STORE_SMEM_LAST, typename C2, typename Load, typename Store>
+TOMO_DEV void fft_pass(C2* row, const C2* __restrict__ tw, int Ns, int t, bool active, Load& load, Store& store) {
   constexpr int T = M / 16;
-  constexpr int NB = M / R;        // butterflies per pass
-  constexpr int PER = NB / T;      // butterflies per thread (16/R)
+  constexpr int NB = M / R;    // butterflies per pass
+  constexpr int PER = NB / T;  // butterflies per thread (16/R)
   C2 v[PER][R];
   if (active) {
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
       const int j = t + q * T;
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[q][r] = row[pad16(j + r * NB)];
-      if (Ns > 1) {
+      for (int r = 0; r < R; ++r) v[q][r] = FIRST ? load(j + r * NB) : row[pad16(j + r * NB)];
+      if (!FIRST) {
         const int jm = j & (Ns - 1);
-        const int step = (M / (Ns * R)) * jm;  // twiddle index increment per r
-#pragma unroll
-        for (int r = 1; r < R; ++r) v[q][r] = cmul(v[q][r], __ldg(&tw[r * step]));
+        if (jm) twiddle<R, C2>(v[q], tw, (M / (Ns * R)) * jm);
       }
       Dft<R, C2>::run(v[q]);
     }
   }
-  __syncthreads();
+  if (!FIRST && (!LAST || STORE_SMEM_LAST)) __syncthreads();
   if (active) {
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
@@ -141,26 +179,39 @@ TOMO_DEV void stockham_pass(C2* row, const C2* __restrict__ tw, int Ns, int t, b
       const int jm = j & (Ns - 1);
       const int base = (j - jm) * R + jm;
 #pragma unroll
-      for (int r = 0; r < R; ++r) row[pad16(base + r * Ns)] = v[q][r];
+      for (int r = 0; r < R; ++r) {
+        if (LAST)
+          store(base + r * Ns, v[q][r]);
+        else
+          row[pad16(base + r * Ns)] = v[q][r];
+      }
     }
   }
-  __syncthreads();
+  if (!LAST || STORE_SMEM_LAST) __syncthreads();
 }
 
-// Forward FFT of one row per thread group, in place in smem. All threads of the CTA must
-// call it (it contains barriers); `t` = thread index within the row (0..M/16-1), and
-// threads without a row pass active = false.
-template <int M, typename C2>
-TOMO_DEV void fft_row_smem(C2* row, const C2* __restrict__ tw, int t, bool active) {
+// Forward FFT of one row per thread group: load(i) -> ... -> store(k, X[k]).
+template <int M, bool STORE_SMEM, typename C2, typename Load, typename Store>
+TOMO_DEV void fft_row(C2* row, const C2* __restrict__ tw, int t, bool active, Load&& load, Store&& store) {
   using S = FftShape<M>;
-  __syncthreads();
-  int Ns = 1;
+  fft_pass<M, 16, true, false, false, C2>(row, tw, 1, t, active, load, store);
+  if constexpr (S::RL > 1) {
+    int Ns = 16;
 #pragma unroll
-  for (int p = 0; p < S::N16; ++p) {
-    stockham_pass<M, 16, C2>(row, tw, Ns, t, active);
-    Ns *= 16;
+    for (int p = 1; p < S::N16; ++p) {
+      fft_pass<M, 16, false, false, false, C2>(row, tw, Ns, t, active, load, store);
+      Ns *= 16;
+    }
+    fft_pass<M, S::RL, false, true, STORE_SMEM, C2>(row, tw, Ns, t, active, load, store);
+  } else {
+    int Ns = 16;
+#pragma unroll
+    for (int p = 1; p < S::N16 - 1; ++p) {
+      fft_pass<M, 16, false, false, false, C2>(row, tw, Ns, t, active, load, store);
+      Ns *= 16;
+    }
+    fft_pass<M, 16, false, true, STORE_SMEM, C2>(row, tw, Ns, t, active, load, store);
   }
-  if constexpr (S::RL > 1) stockham_pass<M, S::RL, C2>(row, tw, Ns, t, active);
 }
 
 }  // namespace tomo_b200

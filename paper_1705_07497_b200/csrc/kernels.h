@@ -44,13 +44,25 @@ struct OpDev {
   const cplx<R>* tw;               // m   : e^{-2 pi i k/m}
   const int4* w_cols;              // SELL-32 ELL of W: [(Ppad/32) * nq * 32] int4
   const Quad<R>* w_vals;           //                   [(Ppad/32) * nq * 32]
-  const uint32_t* wt_chunk;        // G32+1 offsets (units of 32 entries)
-  const WtEnt<R>* wt_ent;          // {sample j, weight}
+  // W^T: nodes of each grid row sorted by entry count (SELL-32-sigma, sigma = one grid row);
+  // the 32-node blocks are processed as a balanced list of warp tasks of <= kWtMaxChunks
+  // chunks; blocks longer than that are split and their partial sums combined by a fix-up.
+  const WtEnt<R>* wt_ent;          // chunk-major: entry (chunk c, lane l) at [c*32 + l]
+  const int4* wt_tasks;            // {block, chunk0, nchunks, slot (-1: direct)}
+  int n_tasks;
+  const uint16_t* wt_perm;         // [G32*32] sorted position -> ix of the block's row
+  const int4* wt_heavy;            // {block, slot0, nslots, 0}
+  int n_heavy;
+  int n_slots;
+  cplx<R>* wt_part;                // B x n_slots x 32 partial sums of split blocks
+  cplx<R>* Gt;                     // B x m x m  spread grid [iy][ix]; untouched nodes stay 0
   cplx<R>* H;                      // B x m x n  (type-2 row pass output, [iy][t1])
   cplx<R>* g;                      // B x m x m  (oversampled spatial grid, [iy][ix])
   cplx<R>* s;                      // B x P      (slice samples)
   cplx<R>* K;                      // B x n x m  (type-1 row pass output, [t1][iy])
 };
+
+constexpr int kWtMaxChunks = 24;
 
 // Per-slice scalar state of the device-resident CG / split-Bregman loops. All reductions
 // land here through the last-block-reduces pattern (deterministic order).
@@ -126,6 +138,13 @@ void launch_w(const OpDev<R>& d, int B, const cplx<R>* grid, cplx<R>* samples, c
               cudaStream_t st);
 template <typename R>
 void launch_wt_rows(const OpDev<R>& d, int B, const SliceScalars* skip, cudaStream_t st);
+// W^T SpMV alone: samples -> spread grid (task kernel + split-block fix-up); `grid` must hold
+// zeros at untouched nodes (they are never written).
+template <typename R>
+void launch_wt_spread(const OpDev<R>& d, int B, const cplx<R>* samples, cplx<R>* grid, const SliceScalars* skip,
+                      cudaStream_t st);
+template <typename R>
+void launch_t1_cols_only(const OpDev<R>& d, int B, const SliceScalars* skip, cudaStream_t st);
 template <typename R>
 void launch_t1_rows(const OpDev<R>& d, int B, const PbEpi<R>& e, cudaStream_t st);
 template <typename R>

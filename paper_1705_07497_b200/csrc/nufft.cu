@@ -2,9 +2,9 @@
 //
 //   type-2 (F_NU^*, proj/src/nufft.cpp:261-286):  P1 deapod+pad+row iFFT  ->  P2 column iFFT
 //                                                  -> W  (SELL-32 ELL SpMV, interpolate :160-202)
-//   type-1 (F_NU,   proj/src/nufft.cpp:236-259):  W^T (SELL-32 SpMV over the precomputed
-//                                                  transpose, spread :119-158) fused into the
-//                                                  first FFT pass -> PB row FFT + crop + deapod
+//   type-1 (F_NU,   proj/src/nufft.cpp:236-259):  W^T (SpMV over the precomputed, count-sorted
+//                                                  transpose, spread :119-158) -> PA grid-row
+//                                                  FFT -> PB image-row FFT + crop + deapod
 //
 // The 2-D transforms (fft.cpp:26-50) are split into a pass over the n non-zero image rows and
 // a pass over the m grid rows; zero padding and cropping (coeff_bin, nufft.cpp:232) are
@@ -67,9 +67,17 @@ __device__ __forceinline__ WtEnt<double> ldg(const WtEnt<double>* p) {
   return WtEnt<double>{v.x, 0, __hiloint2double(v.w, v.z)};
 }
 
-// ---------------------------------------------------------------- P1: image rows
+struct NoStore {
+  template <typename C2>
+  TOMO_DEV void operator()(int, C2) const {}
+};
+
+// ---------------------------------------------------------------- P1: image rows (t1)
+// deapodise + pad + inverse FFT along t2; the CG p-update (p = r + beta p) is fused into the
+// load; output transposed to H[iy][t1] through smem.
 template <int M, typename R>
-__global__ void k_t2_rows(OpDev<R> d, const void* __restrict__ in, int in_complex, PUpd<R> pu, int rpc) {
+__global__ void __launch_bounds__(1024) k_t2_rows(OpDev<R> d, const void* __restrict__ in, int in_complex,
+                                                  PUpd<R> pu, int rpc) {
   using S = FftShape<M>;
   using C2 = cplx<R>;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -80,48 +88,47 @@ __global__ void k_t2_rows(OpDev<R> d, const void* __restrict__ in, int in_comple
   if (!pu.enabled && pu.red.sc && pu.red.sc[b].frozen) return;
   const int rr = threadIdx.x / S::T, t = threadIdx.x % S::T;
   const int n = d.n;
-  const int t1 = blockIdx.x * rpc + rr;
+  const int t10 = blockIdx.x * rpc;
+  const int t1 = t10 + rr;
   const bool active = rr < rpc && t1 < n;
   C2* row = sm + rr * S::STRIDE;
-  if (active) {
-    const R a1 = d.apod[t1];
-    const size_t base = (static_cast<size_t>(b) * n + t1) * n;
-    const R bt = static_cast<R>(beta);
-    for (int i = t; i < M; i += S::T) {
-      const int t2 = (i + n / 2) & (M - 1);
-      C2 v = czero<C2>();
-      if (t2 < n) {
-        const R sc = a1 * d.apod[t2];
-        if (in_complex) {
-          v = reinterpret_cast<const C2*>(in)[base + t2];
-        } else if (pu.enabled) {
-          R pv = pu.p[base + t2];
-          if (pu.step > 0) {
-            pv = pu.r[base + t2] + bt * pv;
-            pu.p[base + t2] = pv;
-          }
-          v.x = pv;
-        } else {
-          v.x = reinterpret_cast<const R*>(in)[base + t2];
+  const size_t base = (static_cast<size_t>(b) * n + (active ? t1 : 0)) * n;
+  const R a1 = active ? d.apod[t1] : R(0);
+  const R bt = static_cast<R>(beta);
+  auto load = [&](int i) -> C2 {
+    const int t2 = (i + n / 2) & (M - 1);
+    C2 v = czero<C2>();
+    if (t2 < n) {
+      const R sc = a1 * __ldg(&d.apod[t2]);
+      if (in_complex) {
+        v = reinterpret_cast<const C2*>(in)[base + t2];
+      } else if (pu.enabled) {
+        R pv = pu.p[base + t2];
+        if (pu.step > 0) {
+          pv = pu.r[base + t2] + bt * pv;
+          pu.p[base + t2] = pv;
         }
-        v = cconj(cscale(v, sc));  // inverse transform: conj in, conj out
+        v.x = pv;
+      } else {
+        v.x = reinterpret_cast<const R*>(in)[base + t2];
       }
-      row[pad16(i)] = v;
+      v = cconj(cscale(v, sc));  // inverse transform: conj in, conj out
     }
-  }
-  fft_row_smem<M, C2>(row, d.tw, t, active);
+    return v;
+  };
+  auto store = [&](int k, C2 v) { row[pad16(k)] = cconj(v); };
+  fft_row<M, true, C2>(row, d.tw, t, active, load, store);
   // transposed store H[b][k][t1]: rpc consecutive t1 per k
-  const int t10 = blockIdx.x * rpc;
   C2* H = d.H + static_cast<size_t>(b) * M * n;
   for (int idx = threadIdx.x; idx < M * rpc; idx += blockDim.x) {
     const int k = idx / rpc, q = idx - k * rpc;
-    if (t10 + q < n) H[static_cast<size_t>(k) * n + t10 + q] = cconj(sm[q * S::STRIDE + pad16(k)]);
+    if (t10 + q < n) H[static_cast<size_t>(k) * n + t10 + q] = sm[q * S::STRIDE + pad16(k)];
   }
 }
 
 // ---------------------------------------------------------------- P2: grid rows (iy)
 template <int M, typename R>
-__global__ void k_t2_cols(OpDev<R> d, int rpc, const SliceScalars* skip) {
+__global__ void __launch_bounds__(1024) k_t2_cols(OpDev<R> d, int rpc, const SliceScalars* skip) {
   using S = FftShape<M>;
   using C2 = cplx<R>;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -133,24 +140,20 @@ __global__ void k_t2_cols(OpDev<R> d, int rpc, const SliceScalars* skip) {
   const int iy = blockIdx.x * rpc + rr;
   const bool active = rr < rpc;
   C2* row = sm + rr * S::STRIDE;
-  if (active) {
-    const C2* H = d.H + (static_cast<size_t>(b) * M + iy) * n;
-    for (int i = t; i < M; i += S::T) {
-      const int t1 = (i + n / 2) & (M - 1);
-      row[pad16(i)] = t1 < n ? cconj(H[t1]) : czero<C2>();
-    }
-  }
-  fft_row_smem<M, C2>(row, d.tw, t, active);
-  if (active) {
-    C2* g = d.g + (static_cast<size_t>(b) * M + iy) * M;
-    for (int i = t; i < M; i += S::T) g[i] = cconj(row[pad16(i)]);
-  }
+  const C2* H = d.H + (static_cast<size_t>(b) * M + (active ? iy : 0)) * n;
+  C2* g = d.g + (static_cast<size_t>(b) * M + (active ? iy : 0)) * M;
+  auto load = [&](int i) -> C2 {
+    const int t1 = (i + n / 2) & (M - 1);
+    return t1 < n ? cconj(H[t1]) : czero<C2>();
+  };
+  auto store = [&](int k, C2 v) { g[k] = cconj(v); };
+  fft_row<M, false, C2>(row, d.tw, t, active, load, store);
 }
 
 // ---------------------------------------------------------------- W: SELL-32 ELL SpMV
 // One thread per slice sample (row of W); entries streamed as int4 column / value quads,
-// coalesced across the warp (lane = row within the 32-row slice). The batch of slices
-// shares the matrix stream (SpMM over BT slices per pass).
+// coalesced across the warp (lane = row within the 32-row slice), four quads prefetched per
+// step so 16 grid gathers are in flight. The batch of slices shares the matrix stream.
 template <int BT, typename R>
 __global__ void __launch_bounds__(256) k_w(OpDev<R> d, int B, const cplx<R>* __restrict__ grid,
                                             cplx<R>* __restrict__ out, const SliceScalars* skip) {
@@ -159,22 +162,35 @@ __global__ void __launch_bounds__(256) k_w(OpDev<R> d, int B, const cplx<R>* __r
   if (j >= d.Ppad) return;
   const int blk = j >> 5, lane = j & 31;
   const size_t G = static_cast<size_t>(d.m) * d.m;
+  const int4* cp = d.w_cols + static_cast<size_t>(blk) * d.nq * 32 + lane;
+  const Quad<R>* vp = d.w_vals + static_cast<size_t>(blk) * d.nq * 32 + lane;
   for (int b0 = 0; b0 < B; b0 += BT) {
     C2 acc[BT];
 #pragma unroll
     for (int q = 0; q < BT; ++q) acc[q] = czero<C2>();
-    const int4* cp = d.w_cols + static_cast<size_t>(blk) * d.nq * 32 + lane;
-    const Quad<R>* vp = d.w_vals + static_cast<size_t>(blk) * d.nq * 32 + lane;
-    for (int q4 = 0; q4 < d.nq; ++q4) {
-      const int4 c = __ldg(cp + q4 * 32);
-      const Quad<R> v = ldg(vp + q4 * 32);
+    for (int q0 = 0; q0 < d.nq; q0 += 4) {
+      int4 c[4];
+      Quad<R> v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (q0 + u < d.nq) {
+          c[u] = __ldg(cp + (q0 + u) * 32);
+          v[u] = ldg(vp + (q0 + u) * 32);
+        } else {
+          c[u] = make_int4(0, 0, 0, 0);
+          v[u] = Quad<R>{{R(0), R(0), R(0), R(0)}};
+        }
+      }
 #pragma unroll
       for (int q = 0; q < BT; ++q) {
         if (b0 + q < B) {
           const C2* gb = grid + G * (b0 + q);
-          const C2 g0 = gb[c.x], g1 = gb[c.y], g2 = gb[c.z], g3 = gb[c.w];
-          acc[q].x += v.v[0] * g0.x + v.v[1] * g1.x + v.v[2] * g2.x + v.v[3] * g3.x;
-          acc[q].y += v.v[0] * g0.y + v.v[1] * g1.y + v.v[2] * g2.y + v.v[3] * g3.y;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const C2 g0 = gb[c[u].x], g1 = gb[c[u].y], g2 = gb[c[u].z], g3 = gb[c[u].w];
+            acc[q].x += v[u].v[0] * g0.x + v[u].v[1] * g1.x + v[u].v[2] * g2.x + v[u].v[3] * g3.x;
+            acc[q].y += v[u].v[0] * g0.y + v[u].v[1] * g1.y + v[u].v[2] * g2.y + v[u].v[3] * g3.y;
+          }
         }
       }
     }
@@ -187,34 +203,76 @@ __global__ void __launch_bounds__(256) k_w(OpDev<R> d, int B, const cplx<R>* __r
   }
 }
 
-// W^T SpMV of one 32-node SELL block: lane's node value.
+// ---------------------------------------------------------------- W^T: balanced task SpMV
+// One warp per task {block, chunk0, nchunks, slot}: lane l accumulates node (block, l) over
+// the task's chunks (coalesced 32-entry chunks, 4 in flight), then writes either the grid node
+// (iy*m + perm) or, for a split block, its partial slot.
 template <typename R>
-__device__ __forceinline__ cplx<R> wt_node(const OpDev<R>& d, const cplx<R>* __restrict__ s, int gb, int lane) {
+__global__ void __launch_bounds__(256) k_wt_tasks(OpDev<R> d, int B, const cplx<R>* __restrict__ s_all,
+                                                   cplx<R>* __restrict__ grid, const SliceScalars* skip) {
   using C2 = cplx<R>;
-  const uint32_t c0 = __ldg(&d.wt_chunk[gb]), c1 = __ldg(&d.wt_chunk[gb + 1]);
-  C2 a0 = czero<C2>(), a1 = czero<C2>();
+  const int task = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (task >= d.n_tasks) return;
+  const int4 tk = __ldg(&d.wt_tasks[task]);
+  const int blk = tk.x, c0 = tk.y, nc = tk.z, slot = tk.w;
+  const int bpr = d.m / 32;  // blocks per grid row
+  const int iy = blk / bpr;
+  const int ix = __ldg(&d.wt_perm[static_cast<size_t>(blk) * 32 + lane]);
+  const size_t G = static_cast<size_t>(d.m) * d.m;
   const WtEnt<R>* e = d.wt_ent + static_cast<size_t>(c0) * 32 + lane;
-  uint32_t c = c0;
-  for (; c + 1 < c1; c += 2, e += 64) {
-    const WtEnt<R> x0 = ldg(e), x1 = ldg(e + 32);
-    const C2 s0 = __ldg(&s[x0.j]), s1 = __ldg(&s[x1.j]);
-    a0.x += x0.w * s0.x;
-    a0.y += x0.w * s0.y;
-    a1.x += x1.w * s1.x;
-    a1.y += x1.w * s1.y;
+  for (int b = 0; b < B; ++b) {
+    if (skip && (skip[b].done || skip[b].frozen)) continue;
+    const C2* s = s_all + static_cast<size_t>(b) * d.P;
+    C2 a0 = czero<C2>(), a1 = czero<C2>();
+    int c = 0;
+    for (; c + 4 <= nc; c += 4) {
+      const WtEnt<R> x0 = ldg(e + (c + 0) * 32), x1 = ldg(e + (c + 1) * 32);
+      const WtEnt<R> x2 = ldg(e + (c + 2) * 32), x3 = ldg(e + (c + 3) * 32);
+      const C2 s0 = __ldg(&s[x0.j]), s1 = __ldg(&s[x1.j]), s2 = __ldg(&s[x2.j]), s3 = __ldg(&s[x3.j]);
+      a0.x += x0.w * s0.x + x2.w * s2.x;
+      a0.y += x0.w * s0.y + x2.w * s2.y;
+      a1.x += x1.w * s1.x + x3.w * s3.x;
+      a1.y += x1.w * s1.y + x3.w * s3.y;
+    }
+    for (; c < nc; ++c) {
+      const WtEnt<R> x0 = ldg(e + c * 32);
+      const C2 s0 = __ldg(&s[x0.j]);
+      a0.x += x0.w * s0.x;
+      a0.y += x0.w * s0.y;
+    }
+    const C2 v = cadd(a0, a1);
+    if (slot < 0)
+      grid[G * b + static_cast<size_t>(iy) * d.m + ix] = v;
+    else
+      d.wt_part[(static_cast<size_t>(b) * d.n_slots + slot) * 32 + lane] = v;
   }
-  if (c < c1) {
-    const WtEnt<R> x0 = ldg(e);
-    const C2 s0 = __ldg(&s[x0.j]);
-    a0.x += x0.w * s0.x;
-    a0.y += x0.w * s0.y;
-  }
-  return cadd(a0, a1);
 }
 
-// ---------------------------------------------------------------- W^T + first type-1 pass
+// Split blocks: node value = sum of the block's partial slots in fixed order.
+template <typename R>
+__global__ void k_wt_fixup(OpDev<R> d, int B, cplx<R>* __restrict__ grid, const SliceScalars* skip) {
+  using C2 = cplx<R>;
+  const int h = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (h >= d.n_heavy) return;
+  const int4 hv = __ldg(&d.wt_heavy[h]);
+  const int blk = hv.x, slot0 = hv.y, ns = hv.z;
+  const int iy = blk / (d.m / 32);
+  const int ix = __ldg(&d.wt_perm[static_cast<size_t>(blk) * 32 + lane]);
+  const size_t G = static_cast<size_t>(d.m) * d.m;
+  for (int b = 0; b < B; ++b) {
+    if (skip && (skip[b].done || skip[b].frozen)) continue;
+    C2 acc = czero<C2>();
+    for (int k = 0; k < ns; ++k) acc = cadd(acc, d.wt_part[(static_cast<size_t>(b) * d.n_slots + slot0 + k) * 32 + lane]);
+    grid[G * b + static_cast<size_t>(iy) * d.m + ix] = acc;
+  }
+}
+
+// ---------------------------------------------------------------- PA: grid rows (iy), type 1
+// forward FFT along ix of the spread grid row, pruned to the n bins, transposed to K[t1][iy].
 template <int M, typename R>
-__global__ void k_wt_rows(OpDev<R> d, int rpc, const SliceScalars* skip) {
+__global__ void __launch_bounds__(1024) k_t1_cols(OpDev<R> d, int rpc, const SliceScalars* skip) {
   using S = FftShape<M>;
   using C2 = cplx<R>;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -223,24 +281,20 @@ __global__ void k_wt_rows(OpDev<R> d, int rpc, const SliceScalars* skip) {
   if (skip && (skip[b].done || skip[b].frozen)) return;
   const int n = d.n;
   const int iy0 = blockIdx.x * rpc;
-  const C2* s = d.s + static_cast<size_t>(b) * d.P;
-  // W^T rows of the CTA's grid rows: SELL blocks [iy0*M/32, (iy0+rpc)*M/32)
-  const int nblocks = rpc * (M / 32);
-  const int gb0 = iy0 * (M / 32);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  for (int q = warp; q < nblocks; q += nwarps) {
-    const C2 v = wt_node<R>(d, s, gb0 + q, lane);
-    const int local = q * 32 + lane;  // node index within the CTA's rows
-    const int rr = local / M, ix = local - rr * M;
-    sm[rr * S::STRIDE + pad16(ix)] = v;
-  }
   const int rr = threadIdx.x / S::T, t = threadIdx.x % S::T;
-  fft_row_smem<M, C2>(sm + rr * S::STRIDE, d.tw, t, rr < rpc);
-  // pruned transposed store K[b][t1][iy0 + q] = X[bin(t1)]
+  const bool active = rr < rpc;
+  C2* row = sm + rr * S::STRIDE;
+  const C2* Gr = d.Gt + (static_cast<size_t>(b) * M + iy0 + (active ? rr : 0)) * M;
+  auto load = [&](int i) -> C2 { return Gr[i]; };
+  auto store = [&](int k, C2 v) {
+    const int t1 = (k + n / 2) & (M - 1);  // inverse of bin_of
+    if (t1 < n) row[pad16(t1)] = v;
+  };
+  fft_row<M, true, C2>(row, d.tw, t, active, load, store);
   C2* K = d.K + static_cast<size_t>(b) * n * M;
   for (int idx = threadIdx.x; idx < n * rpc; idx += blockDim.x) {
     const int t1 = idx / rpc, q = idx - t1 * rpc;
-    K[static_cast<size_t>(t1) * M + iy0 + q] = sm[q * S::STRIDE + pad16(bin_of(t1, n, M))];
+    K[static_cast<size_t>(t1) * M + iy0 + q] = sm[q * S::STRIDE + pad16(t1)];
   }
 }
 
@@ -257,8 +311,10 @@ __device__ __forceinline__ R ktk_at(const R* __restrict__ p, int n, int i, int j
 }
 
 // ---------------------------------------------------------------- PB: image rows (t1)
+// forward FFT along iy, crop to the n bins, deapodise, then the epilogue: complex / real
+// output or the CG system apply alpha*Re(N p) + lambda K'K p + shift p with the dots.
 template <int M, typename R>
-__global__ void k_t1_rows(OpDev<R> d, PbEpi<R> e, int rpc) {
+__global__ void __launch_bounds__(1024) k_t1_rows(OpDev<R> d, PbEpi<R> e, int rpc) {
   using S = FftShape<M>;
   using C2 = cplx<R>;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -272,46 +328,43 @@ __global__ void k_t1_rows(OpDev<R> d, PbEpi<R> e, int rpc) {
   const int t1 = blockIdx.x * rpc + rr;
   const bool active = rr < rpc && t1 < n;
   C2* row = sm + rr * S::STRIDE;
-  if (active) {
-    const C2* K = d.K + (static_cast<size_t>(b) * n + t1) * M;
-    for (int i = t; i < M; i += S::T) row[pad16(i)] = K[i];
-  }
-  fft_row_smem<M, C2>(row, d.tw, t, active);
+  const C2* Kr = d.K + (static_cast<size_t>(b) * n + (active ? t1 : 0)) * M;
+  const R a1 = active ? d.apod[t1] * e.scale : R(0);
+  const size_t base = (static_cast<size_t>(b) * n + (active ? t1 : 0)) * n;
+  const R lam = static_cast<R>(e.sys.lambda), shift = static_cast<R>(e.sys.shift);
+  const R* p = e.p ? e.p + static_cast<size_t>(b) * n * n : nullptr;
   double acc0 = 0.0, acc1 = 0.0;
-  if (active) {
-    const R a1 = d.apod[t1] * e.scale;
-    const size_t base = (static_cast<size_t>(b) * n + t1) * n;
-    const R lam = static_cast<R>(e.sys.lambda), shift = static_cast<R>(e.sys.shift);
-    for (int t2 = t; t2 < n; t2 += S::T) {
-      const C2 X = row[pad16(bin_of(t2, n, M))];
-      const R sc = a1 * d.apod[t2];
-      const size_t o = base + t2;
-      if (e.mode == PB_COMPLEX) {
-        e.out_c[o] = cscale(X, sc);
-      } else if (e.mode == PB_REAL) {
-        e.out_r[o] = X.x * sc;
-      } else {
-        const R* p = e.p + static_cast<size_t>(b) * n * n;
-        const R pv = p[static_cast<size_t>(t1) * n + t2];
-        R ax = X.x * sc;
-        if (lam != R(0)) ax += lam * ktk_at<R>(p, n, t1, t2, pv);
-        ax += shift * pv;
-        if (e.mode == PB_CG_STEP) {
-          e.ap[o] = ax;
-          acc0 += static_cast<double>(pv) * ax;
-          acc1 += static_cast<double>(pv) * pv;
-        } else {  // PB_CG_INIT: r = b - A x0, p = r, x = x0
-          const R bv = e.b[o];
-          const R rv = bv - ax;
-          e.ap[o] = rv;
-          e.p_out[o] = rv;
-          e.x_out[o] = pv;
-          acc0 += static_cast<double>(rv) * rv;
-          acc1 += static_cast<double>(bv) * bv;
-        }
+  auto load = [&](int i) -> C2 { return Kr[i]; };
+  auto store = [&](int k, C2 X) {
+    const int t2 = (k + n / 2) & (M - 1);
+    if (t2 >= n) return;
+    const R sc = a1 * __ldg(&d.apod[t2]);
+    const size_t o = base + t2;
+    if (e.mode == PB_COMPLEX) {
+      e.out_c[o] = cscale(X, sc);
+    } else if (e.mode == PB_REAL) {
+      e.out_r[o] = X.x * sc;
+    } else {
+      const R pv = p[static_cast<size_t>(t1) * n + t2];
+      R ax = X.x * sc;
+      if (lam != R(0)) ax += lam * ktk_at<R>(p, n, t1, t2, pv);
+      ax += shift * pv;
+      if (e.mode == PB_CG_STEP) {
+        e.ap[o] = ax;
+        acc0 += static_cast<double>(pv) * ax;
+        acc1 += static_cast<double>(pv) * pv;
+      } else {  // PB_CG_INIT: r = b - A x0, p = r, x = x0
+        const R bv = e.b[o];
+        const R rv = bv - ax;
+        e.ap[o] = rv;
+        e.p_out[o] = rv;
+        e.x_out[o] = pv;
+        acc0 += static_cast<double>(rv) * rv;
+        acc1 += static_cast<double>(bv) * bv;
       }
     }
-  }
+  };
+  fft_row<M, false, C2>(row, d.tw, t, active, load, store);
   if (e.mode >= PB_CG_STEP) {
     double t0s, t1s;
     SliceScalars& sc = e.red.sc[b];
@@ -330,17 +383,6 @@ __global__ void k_t1_rows(OpDev<R> d, PbEpi<R> e, int rpc) {
       }
     }
   }
-}
-
-// ---------------------------------------------------------------- standalone W^T (tests)
-template <typename R>
-__global__ void k_wt_grid(OpDev<R> d, int B, const cplx<R>* __restrict__ s, cplx<R>* __restrict__ grid) {
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (gw >= d.G32) return;
-  const size_t G = static_cast<size_t>(d.m) * d.m;
-  for (int b = 0; b < B; ++b)
-    grid[G * b + static_cast<size_t>(gw) * 32 + lane] = wt_node<R>(d, s + static_cast<size_t>(b) * d.P, gw, lane);
 }
 
 // Radial density weights |k_r| (DC: 1/4), normal_ops.cpp:208-219, applied to samples.
@@ -362,25 +404,23 @@ __global__ void k_fft_rows_test(const cplx<R>* tw, const cplx<R>* in, cplx<R>* o
   C2* sm = reinterpret_cast<C2*>(smraw);
   const int r = blockIdx.x;
   const int t = threadIdx.x;
-  for (int i = t; i < M; i += S::T) {
-    C2 v = in[static_cast<size_t>(r) * M + i];
-    sm[pad16(i)] = inverse ? cconj(v) : v;
-  }
-  fft_row_smem<M, C2>(sm, tw, t, true);
-  for (int i = t; i < M; i += S::T) {
-    C2 v = sm[pad16(i)];
-    out[static_cast<size_t>(r) * M + i] = inverse ? cconj(v) : v;
-  }
+  const C2* src = in + static_cast<size_t>(r) * M;
+  C2* dst = out + static_cast<size_t>(r) * M;
+  auto load = [&](int i) -> C2 { return inverse ? cconj(src[i]) : src[i]; };
+  auto store = [&](int k, C2 v) { dst[k] = inverse ? cconj(v) : v; };
+  fft_row<M, false, C2>(sm, tw, t, true, load, store);
 }
 
 // ---------------------------------------------------------------- dispatch helpers
-// rows-per-CTA: enough threads per CTA, bounded smem, and at least ~2 waves of CTAs.
-int choose_rpc(int m, int rows_per_slice, int B, size_t elem) {
+// rows-per-CTA: transposed stores need >= 32 B per row segment (rpc >= 32 / sizeof(C2)),
+// enough threads per CTA, bounded smem, and as many CTAs as possible above that.
+int choose_rpc(int m, int rows_per_slice, int B, size_t elem, bool transposed) {
   const int T = m / 16;
-  int rpc = std::max(1, 256 / T);
-  while (rpc > 1 && (rpc * T > 1024 || static_cast<size_t>(rpc) * padded_len(m) * elem > 100 * 1024)) rpc >>= 1;
-  while (rpc > 1 && static_cast<int64_t>((rows_per_slice + rpc - 1) / rpc) * B < 2 * 148) rpc >>= 1;
-  return rpc;
+  const int min_rpc = transposed ? std::max(1, static_cast<int>(32 / elem)) : 1;
+  int rpc = std::max(min_rpc, std::max(1, 128 / T));
+  while (rpc > 1 && (rpc * T > 1024 || static_cast<size_t>(rpc) * padded_len(m) * elem > 110 * 1024)) rpc >>= 1;
+  while (rpc > min_rpc && rpc * T > 256 && static_cast<int64_t>((rows_per_slice + rpc - 1) / rpc) * B < 2 * 148) rpc >>= 1;
+  return std::max(rpc, 1);
 }
 
 template <typename F>
@@ -419,7 +459,7 @@ void launch_t2_rows(const OpDev<R>& d, int B, const void* in, bool in_complex, c
   dispatch_m(d.m, [&](auto MC) {
     constexpr int M = decltype(MC)::value;
     using S = FftShape<M>;
-    const int rpc = choose_rpc(M, d.n, B, sizeof(cplx<R>));
+    const int rpc = choose_rpc(M, d.n, B, sizeof(cplx<R>), true);
     const size_t smem = static_cast<size_t>(rpc) * S::STRIDE * sizeof(cplx<R>);
     set_smem(k_t2_rows<M, R>, smem);
     dim3 grid((d.n + rpc - 1) / rpc, B);
@@ -433,7 +473,7 @@ void launch_t2_cols(const OpDev<R>& d, int B, const SliceScalars* skip, cudaStre
   dispatch_m(d.m, [&](auto MC) {
     constexpr int M = decltype(MC)::value;
     using S = FftShape<M>;
-    const int rpc = choose_rpc(M, M, B, sizeof(cplx<R>));
+    const int rpc = choose_rpc(M, M, B, sizeof(cplx<R>), false);
     const size_t smem = static_cast<size_t>(rpc) * S::STRIDE * sizeof(cplx<R>);
     set_smem(k_t2_cols<M, R>, smem);
     dim3 grid(M / rpc, B);
@@ -457,15 +497,37 @@ void launch_w(const OpDev<R>& d, int B, const cplx<R>* grid, cplx<R>* samples, c
 }
 
 template <typename R>
+void launch_wt_spread(const OpDev<R>& d, int B, const cplx<R>* samples, cplx<R>* grid, const SliceScalars* skip,
+                      cudaStream_t st) {
+  const int threads = 256;
+  if (d.n_tasks > 0) {
+    const int blocks = (d.n_tasks * 32 + threads - 1) / threads;
+    k_wt_tasks<R><<<blocks, threads, 0, st>>>(d, B, samples, grid, skip);
+    note_launch();
+  }
+  if (d.n_heavy > 0) {
+    const int blocks = (d.n_heavy * 32 + threads - 1) / threads;
+    k_wt_fixup<R><<<blocks, threads, 0, st>>>(d, B, grid, skip);
+    note_launch();
+  }
+}
+
+template <typename R>
 void launch_wt_rows(const OpDev<R>& d, int B, const SliceScalars* skip, cudaStream_t st) {
+  launch_wt_spread<R>(d, B, d.s, d.Gt, skip, st);
+  launch_t1_cols_only<R>(d, B, skip, st);
+}
+
+template <typename R>
+void launch_t1_cols_only(const OpDev<R>& d, int B, const SliceScalars* skip, cudaStream_t st) {
   dispatch_m(d.m, [&](auto MC) {
     constexpr int M = decltype(MC)::value;
     using S = FftShape<M>;
-    const int rpc = choose_rpc(M, M, B, sizeof(cplx<R>));
+    const int rpc = choose_rpc(M, M, B, sizeof(cplx<R>), true);
     const size_t smem = static_cast<size_t>(rpc) * S::STRIDE * sizeof(cplx<R>);
-    set_smem(k_wt_rows<M, R>, smem);
+    set_smem(k_t1_cols<M, R>, smem);
     dim3 grid(M / rpc, B);
-    k_wt_rows<M, R><<<grid, std::max(32, rpc * S::T), smem, st>>>(d, rpc, skip);
+    k_t1_cols<M, R><<<grid, rpc * S::T, smem, st>>>(d, rpc, skip);
     note_launch();
   });
 }
@@ -475,23 +537,21 @@ void launch_t1_rows(const OpDev<R>& d, int B, const PbEpi<R>& e, cudaStream_t st
   dispatch_m(d.m, [&](auto MC) {
     constexpr int M = decltype(MC)::value;
     using S = FftShape<M>;
-    int rpc = choose_rpc(M, d.n, B, sizeof(cplx<R>));
+    int rpc = choose_rpc(M, d.n, B, sizeof(cplx<R>), false);
+    while ((rpc * S::T) % 32) rpc <<= 1;  // whole warps for the block reduction
     while (rpc > 1 && (d.n + rpc - 1) / rpc > MAX_PART_BLOCKS) rpc <<= 1;
     const size_t smem = static_cast<size_t>(rpc) * S::STRIDE * sizeof(cplx<R>);
     set_smem(k_t1_rows<M, R>, smem);
     dim3 grid((d.n + rpc - 1) / rpc, B);
-    const int threads = std::max(32, rpc * S::T);
-    k_t1_rows<M, R><<<grid, threads, smem, st>>>(d, e, rpc);
+    k_t1_rows<M, R><<<grid, rpc * S::T, smem, st>>>(d, e, rpc);
     note_launch();
   });
 }
 
 template <typename R>
 void launch_wt_grid(const OpDev<R>& d, int B, const cplx<R>* samples, cplx<R>* grid, cudaStream_t st) {
-  const int threads = 256;
-  const int blocks = (d.G32 * 32 + threads - 1) / threads;
-  k_wt_grid<R><<<blocks, threads, 0, st>>>(d, B, samples, grid);
-  note_launch();
+  cudaMemsetAsync(grid, 0, sizeof(cplx<R>) * static_cast<size_t>(B) * d.m * d.m, st);
+  launch_wt_spread<R>(d, B, samples, grid, nullptr, st);
 }
 
 template <typename R>
@@ -519,7 +579,10 @@ void launch_fft_rows_test(int m, int rows, const cplx<R>* tw, const cplx<R>* in,
   template void launch_t2_rows<R>(const OpDev<R>&, int, const void*, bool, const PUpd<R>&, cudaStream_t);   \
   template void launch_t2_cols<R>(const OpDev<R>&, int, const SliceScalars*, cudaStream_t);                 \
   template void launch_w<R>(const OpDev<R>&, int, const cplx<R>*, cplx<R>*, const SliceScalars*, cudaStream_t); \
+  template void launch_wt_spread<R>(const OpDev<R>&, int, const cplx<R>*, cplx<R>*, const SliceScalars*,    \
+                                    cudaStream_t);                                                          \
   template void launch_wt_rows<R>(const OpDev<R>&, int, const SliceScalars*, cudaStream_t);                 \
+  template void launch_t1_cols_only<R>(const OpDev<R>&, int, const SliceScalars*, cudaStream_t);            \
   template void launch_t1_rows<R>(const OpDev<R>&, int, const PbEpi<R>&, cudaStream_t);                     \
   template void launch_wt_grid<R>(const OpDev<R>&, int, const cplx<R>*, cplx<R>*, cudaStream_t);            \
   template void launch_weight_samples<R>(cplx<R>*, int, int, int, cudaStream_t);                            \

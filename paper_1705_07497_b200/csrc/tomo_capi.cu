@@ -221,7 +221,7 @@ constexpr int kMaxLoggedIters = 8192;
 // Device scratch of an op, sized for `cap` slices (element type = op precision).
 struct Scratch {
   int cap = 0;
-  Raw H, g, s, K;                 // complex
+  Raw H, g, s, K, Gt, part_wt;    // complex
   Raw cin, cout, fin, fout;       // staging for host pointers / temporaries
   Raw r, p0, p1, ap, x, rhs, fid, mu0, mu1, bx0, bx1, by0, by1, nred, zero, u2;  // real vectors
   Raw upd_log, sc, part;
@@ -244,7 +244,8 @@ struct tomo_op {
   size_t rsz = 4;  // sizeof(R)
   int64_t nnz = 0, wt_rows = 0, wt_slots = 0;
   int nq = 0, Ppad = 0;
-  Raw apod, tw, wcols, wvals, wtchunk, wtent;
+  int n_tasks = 0, n_heavy = 0, n_slots = 0;
+  Raw apod, tw, wcols, wvals, wtent, wttasks, wtperm, wtheavy;
   Scratch sc;
   // surrogate
   int rad = 0;
@@ -287,8 +288,15 @@ struct tomo_op {
     d.tw = tw.as<cplx<R>>();
     d.w_cols = wcols.as<int4>();
     d.w_vals = wvals.as<Quad<R>>();
-    d.wt_chunk = wtchunk.as<uint32_t>();
     d.wt_ent = wtent.as<WtEnt<R>>();
+    d.wt_tasks = wttasks.as<int4>();
+    d.n_tasks = n_tasks;
+    d.wt_perm = wtperm.as<uint16_t>();
+    d.wt_heavy = wtheavy.as<int4>();
+    d.n_heavy = n_heavy;
+    d.n_slots = n_slots;
+    d.wt_part = sc.part_wt.as<cplx<R>>();
+    d.Gt = sc.Gt.as<cplx<R>>();
     d.H = sc.H.as<cplx<R>>();
     d.g = sc.g.as<cplx<R>>();
     d.s = sc.s.as<cplx<R>>();
@@ -301,6 +309,9 @@ struct tomo_op {
     const size_t m = g.m, n = g.n, cz = 2 * rsz;
     sc.H.ensure(B * m * n * cz);
     sc.g.ensure(B * m * m * cz);
+    sc.Gt.ensure(B * m * m * cz);
+    CK(cudaMemset(sc.Gt.p, 0, B * m * m * cz));  // untouched spread-grid nodes stay zero
+    sc.part_wt.ensure(static_cast<size_t>(B) * std::max(n_slots, 1) * 32 * cz);
     sc.s.ensure(B * static_cast<size_t>(g.P) * cz);
     sc.K.ensure(B * n * m * cz);
     sc.sc.ensure(sizeof(SliceScalars) * B);
@@ -373,6 +384,9 @@ void build_tables(tomo_op* op) {
     }
   }
 
+  // W^T: per grid row, nodes sorted by entry count (descending, stable in ix); 32 sorted nodes
+  // form a block of L = max count chunks; entries chunk-major within the block; blocks with
+  // L > kWtMaxChunks are split into several tasks whose partials a fix-up kernel sums.
   const int64_t G = static_cast<int64_t>(m) * m;
   std::vector<int64_t> off(G + 1, 0);
   for (int64_t i = 0; i < G; ++i) off[i + 1] = off[i] + cnt[i];
@@ -391,27 +405,35 @@ void build_tables(tomo_op* op) {
     }
   }
   const int64_t G32 = G / 32;
-  std::vector<uint32_t> chunk(G32 + 1, 0);
+  const int bpr = m / 32;
+  std::vector<uint16_t> perm(G);
+  std::vector<int> blockL(G32);
+  std::vector<int> order(m);
   int64_t touched = 0;
-  for (int64_t bk = 0; bk < G32; ++bk) {
-    int Lb = 0;
-    for (int l = 0; l < 32; ++l) {
-      const int c = cnt[bk * 32 + l];
-      Lb = std::max(Lb, c);
-      touched += c > 0;
+  for (int iy = 0; iy < m; ++iy) {
+    const int* crow = cnt.data() + static_cast<int64_t>(iy) * m;
+    for (int ix = 0; ix < m; ++ix) {
+      order[ix] = ix;
+      touched += crow[ix] > 0;
     }
-    if (static_cast<uint64_t>(chunk[bk]) + Lb > 0xffffffffull / 32) throw ConfigError("W^T too large");
-    chunk[bk + 1] = chunk[bk] + Lb;
+    std::stable_sort(order.begin(), order.end(), [crow](int a, int b) { return crow[a] > crow[b]; });
+    for (int k = 0; k < m; ++k) perm[static_cast<int64_t>(iy) * m + k] = static_cast<uint16_t>(order[k]);
+    for (int kb = 0; kb < bpr; ++kb) blockL[static_cast<int64_t>(iy) * bpr + kb] = crow[order[kb * 32]];
   }
+  std::vector<int64_t> chunk0(G32 + 1, 0);
+  for (int64_t bk = 0; bk < G32; ++bk) chunk0[bk + 1] = chunk0[bk] + blockL[bk];
+  if (chunk0[G32] > (int64_t(1) << 31) - 1) throw ConfigError("W^T too large");
   op->wt_rows = touched;
-  op->wt_slots = static_cast<int64_t>(chunk[G32]) * 32;
+  op->wt_slots = chunk0[G32] * 32;
   std::vector<WtEnt<R>> ent(std::max<int64_t>(op->wt_slots, 1));
   for (int64_t bk = 0; bk < G32; ++bk) {
-    const int Lb = static_cast<int>(chunk[bk + 1] - chunk[bk]);
+    const int Lb = blockL[bk];
+    if (!Lb) continue;
+    const int iy = static_cast<int>(bk / bpr);
     for (int l = 0; l < 32; ++l) {
-      const int64_t node = bk * 32 + l;
+      const int64_t node = static_cast<int64_t>(iy) * m + perm[bk * 32 + l];
       const int c = cnt[node];
-      int lastj = c > 0 ? tj[off[node]] : 0;
+      int lastj = c > 0 ? tj[off[node]] : tj[off[static_cast<int64_t>(iy) * m + perm[bk * 32]]];
       for (int k = 0; k < Lb; ++k) {
         WtEnt<R> e{};
         if (k < c) {
@@ -422,10 +444,32 @@ void build_tables(tomo_op* op) {
           e.j = lastj;  // padding: re-read a sample already in cache, weight 0
           e.w = R(0);
         }
-        ent[(static_cast<size_t>(chunk[bk]) + k) * 32 + l] = e;
+        ent[(static_cast<size_t>(chunk0[bk]) + k) * 32 + l] = e;
       }
     }
   }
+  std::vector<int4> tasks, heavy;
+  int slots = 0;
+  for (int64_t bk = 0; bk < G32; ++bk) {
+    const int Lb = blockL[bk];
+    if (!Lb) continue;
+    if (Lb <= kWtMaxChunks) {
+      tasks.push_back(make_int4(static_cast<int>(bk), static_cast<int>(chunk0[bk]), Lb, -1));
+    } else {
+      const int ns = (Lb + kWtMaxChunks - 1) / kWtMaxChunks;
+      heavy.push_back(make_int4(static_cast<int>(bk), slots, ns, 0));
+      for (int k = 0; k < ns; ++k) {
+        const int c0 = k * kWtMaxChunks;
+        tasks.push_back(make_int4(static_cast<int>(bk), static_cast<int>(chunk0[bk]) + c0,
+                                  std::min(kWtMaxChunks, Lb - c0), slots++));
+      }
+    }
+  }
+  // longest tasks first (they are launched first and overlap the rest)
+  std::stable_sort(tasks.begin(), tasks.end(), [](const int4& a, const int4& b) { return a.z > b.z; });
+  op->n_tasks = static_cast<int>(tasks.size());
+  op->n_heavy = static_cast<int>(heavy.size());
+  op->n_slots = slots;
 
   // deapodisation a[t]/m (nufft.cpp:204-227 with the 1/m per-axis FFT scale folded in)
   std::vector<R> apod(g.n);
@@ -442,8 +486,10 @@ void build_tables(tomo_op* op) {
   }
   op->wcols.upload(cols);
   op->wvals.upload(vals);
-  op->wtchunk.upload(chunk);
   op->wtent.upload(ent);
+  op->wttasks.upload(tasks.empty() ? std::vector<int4>(1) : tasks);
+  op->wtperm.upload(perm);
+  op->wtheavy.upload(heavy.empty() ? std::vector<int4>(1) : heavy);
   op->apod.upload(apod);
   op->tw.upload(tw);
 }
@@ -917,7 +963,8 @@ int tomo_op_get_info(const tomo_op* op, tomo_op_info* info) {
   info->wt_rows = op->wt_rows;
   info->wt_slots = op->wt_slots;
   info->bytes_w = static_cast<int64_t>(op->Ppad) * op->nq * 32 * (16 + 4 * static_cast<int64_t>(op->rsz)) / 32;
-  info->bytes_wt = op->wt_slots * (op->f64 ? 16 : 8) + (static_cast<int64_t>(op->g.m) * op->g.m / 32 + 1) * 4;
+  info->bytes_wt = op->wt_slots * (op->f64 ? 16 : 8) + static_cast<int64_t>(op->n_tasks) * 16 +
+                   static_cast<int64_t>(op->g.m) * op->g.m * 2;
   info->surrogate_r = op->rad;
   info->precision = op->f64 ? TOMO_F64 : TOMO_F32;
   std::memcpy(info->stencil, op->stencil64, sizeof(info->stencil));
@@ -1491,8 +1538,10 @@ int tomo_profile_stages(tomo_op* op, int batch, int reps, double* ms, double* by
             } else if (s == 2) {
               launch_w<R>(d, batch, d.g, d.s, op->scal(), st);
             } else if (s == 3) {
-              launch_wt_rows<R>(d, batch, op->scal(), st);
+              launch_wt_spread<R>(d, batch, d.s, d.Gt, op->scal(), st);
             } else if (s == 4) {
+              launch_t1_cols_only<R>(d, batch, op->scal(), st);
+            } else if (s == 5) {
               PbEpi<R> e = plain_epi<R>(PB_CG_STEP, 1.0);
               e.p = S.p0.as<R>();
               e.ap = S.ap.as<R>();
@@ -1501,12 +1550,12 @@ int tomo_profile_stages(tomo_op* op, int batch, int reps, double* ms, double* by
               e.red = red;
               launch_t1_rows<R>(d, batch, e, st);
             }
-          } else if (s == 7) {
+          } else if (s == 8) {
             launch_stencil<R>(n, batch, op->rad, op->coef, 0, S.p0.as<R>(), S.r.as<R>(), S.p1.as<R>(), S.ap.as<R>(),
                               nullptr, nullptr, sp, 1, red, st);
           }
-          if (s == 5) launch_cg_update<R>(n, batch, S.p0.as<R>(), S.ap.as<R>(), S.x.as<R>(), S.r.as<R>(), sp, 1, red, st);
-          if (s == 6)
+          if (s == 6) launch_cg_update<R>(n, batch, S.p0.as<R>(), S.ap.as<R>(), S.x.as<R>(), S.r.as<R>(), sp, 1, red, st);
+          if (s == 7)
             launch_sb_post<R>(n, batch, S.mu1.as<R>(), S.mu0.as<R>(), S.bx0.as<R>(), S.by0.as<R>(), S.bx1.as<R>(),
                               S.by1.as<R>(), S.fid.as<R>(), S.rhs.as<R>(), 1.0, red, st);
         }
@@ -1524,21 +1573,23 @@ int tomo_profile_stages(tomo_op* op, int batch, int reps, double* ms, double* by
     const double B = batch, nn = static_cast<double>(n) * n, mn = static_cast<double>(m) * n,
                  mm = static_cast<double>(m) * m, P = static_cast<double>(op->g.P), rs = sizeof(R), cs = 2 * sizeof(R);
     const double wbytes = static_cast<double>(op->Ppad) * op->nq * 32.0 * (16.0 + 4.0 * rs) / 32.0;
-    const double wtbytes = static_cast<double>(op->wt_slots) * sizeof(WtEnt<R>) + (mm / 32.0 + 1) * 4.0;
+    const double wtbytes = static_cast<double>(op->wt_slots) * sizeof(WtEnt<R>) + op->n_tasks * 16.0 +
+                           static_cast<double>(op->wt_rows) * 2.0;
     double by[TOMO_NUM_STAGES] = {0};
     if (!sur) {
       by[0] = B * (3 * rs * nn + cs * mn);                 // read p, r; write p; write H
       by[1] = B * (cs * mn + cs * mm);                     // read H, write g
       by[2] = wbytes + B * (cs * op->wt_rows + cs * P);    // W stream, touched grid nodes, samples
-      by[3] = wtbytes + B * (cs * P + cs * mn);            // W^T stream, samples, write K
-      by[4] = B * (cs * mn + 2 * rs * nn);                 // read K, p; write Ap
+      by[3] = wtbytes + B * (cs * P + cs * op->wt_rows);   // W^T stream, samples, write touched nodes
+      by[4] = B * (cs * mm + cs * mn);                     // read spread grid, write K
+      by[5] = B * (cs * mn + 2 * rs * nn);                 // read K, p; write Ap
     } else {
-      by[7] = B * 4 * rs * nn;  // read r, p; write p, Ap
+      by[8] = B * 4 * rs * nn;  // read r, p; write p, Ap
     }
-    by[5] = B * 6 * rs * nn;  // read x, r, p, Ap; write x, r
-    by[6] = B * 8 * rs * nn;  // read mu_new, mu_old, bx, by, fid; write bx, by, rhs
+    by[6] = B * 6 * rs * nn;  // read x, r, p, Ap; write x, r
+    by[7] = B * 8 * rs * nn;  // read mu_new, mu_old, bx, by, fid; write bx, by, rhs
     for (int k = 0; k < TOMO_NUM_STAGES; ++k) {
-      const bool on = sur ? (k >= 5) : (k <= 6);
+      const bool on = sur ? (k >= 6) : (k <= 7);
       ms[k] = on ? acc[k] / reps : 0.0;
       bytes[k] = on ? by[k] : 0.0;
     }
