@@ -27,6 +27,10 @@ namespace {
 
 __device__ __forceinline__ int bin_of(int t, int n, int M) { return (t - n / 2 + M) & (M - 1); }
 
+// FFT-row kernels: at most 512 threads per CTA so ptxas may give each thread up to 128
+// registers (a radix-16 fp64 butterfly holds 64 registers of data alone).
+constexpr int kFftThreads = 512;
+
 // beta for the fused CG p-update (solver.cpp:84): rr[k] / rr[k-1]; returns false when the
 // slice's CG is finished (done flag or rs == 0, solver.cpp:70).
 __device__ __forceinline__ bool cg_step_live(const Reduce& red, int b, int step, double& beta) {
@@ -76,7 +80,7 @@ struct NoStore {
 // deapodise + pad + inverse FFT along t2; the CG p-update (p = r + beta p) is fused into the
 // load; output transposed to H[iy][t1] through smem.
 template <int M, typename R>
-__global__ void __launch_bounds__(1024) k_t2_rows(OpDev<R> d, const void* __restrict__ in, int in_complex,
+__global__ void __launch_bounds__(kFftThreads) k_t2_rows(OpDev<R> d, const void* __restrict__ in, int in_complex,
                                                   PUpd<R> pu, int rpc) {
   using S = FftShape<M>;
   using C2 = cplx<R>;
@@ -128,7 +132,7 @@ __global__ void __launch_bounds__(1024) k_t2_rows(OpDev<R> d, const void* __rest
 
 // ---------------------------------------------------------------- P2: grid rows (iy)
 template <int M, typename R>
-__global__ void __launch_bounds__(1024) k_t2_cols(OpDev<R> d, int rpc, const SliceScalars* skip) {
+__global__ void __launch_bounds__(kFftThreads) k_t2_cols(OpDev<R> d, int rpc, const SliceScalars* skip) {
   using S = FftShape<M>;
   using C2 = cplx<R>;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -272,7 +276,7 @@ __global__ void k_wt_fixup(OpDev<R> d, int B, cplx<R>* __restrict__ grid, const 
 // ---------------------------------------------------------------- PA: grid rows (iy), type 1
 // forward FFT along ix of the spread grid row, pruned to the n bins, transposed to K[t1][iy].
 template <int M, typename R>
-__global__ void __launch_bounds__(1024) k_t1_cols(OpDev<R> d, int rpc, const SliceScalars* skip) {
+__global__ void __launch_bounds__(kFftThreads) k_t1_cols(OpDev<R> d, int rpc, const SliceScalars* skip) {
   using S = FftShape<M>;
   using C2 = cplx<R>;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -314,7 +318,7 @@ __device__ __forceinline__ R ktk_at(const R* __restrict__ p, int n, int i, int j
 // forward FFT along iy, crop to the n bins, deapodise, then the epilogue: complex / real
 // output or the CG system apply alpha*Re(N p) + lambda K'K p + shift p with the dots.
 template <int M, typename R>
-__global__ void __launch_bounds__(1024) k_t1_rows(OpDev<R> d, PbEpi<R> e, int rpc) {
+__global__ void __launch_bounds__(kFftThreads) k_t1_rows(OpDev<R> d, PbEpi<R> e, int rpc) {
   using S = FftShape<M>;
   using C2 = cplx<R>;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -418,7 +422,7 @@ int choose_rpc(int m, int rows_per_slice, int B, size_t elem, bool transposed) {
   const int T = m / 16;
   const int min_rpc = transposed ? std::max(1, static_cast<int>(32 / elem)) : 1;
   int rpc = std::max(min_rpc, std::max(1, 128 / T));
-  while (rpc > 1 && (rpc * T > 1024 || static_cast<size_t>(rpc) * padded_len(m) * elem > 110 * 1024)) rpc >>= 1;
+  while (rpc > 1 && (rpc * T > kFftThreads || static_cast<size_t>(rpc) * padded_len(m) * elem > 110 * 1024)) rpc >>= 1;
   while (rpc > min_rpc && rpc * T > 256 && static_cast<int64_t>((rows_per_slice + rpc - 1) / rpc) * B < 2 * 148) rpc >>= 1;
   return std::max(rpc, 1);
 }

@@ -1515,61 +1515,66 @@ int tomo_profile_stages(tomo_op* op, int batch, int reps, double* ms, double* by
     const SysParams sp = sysp(1.0, 1.0, 0.0, 0.0);
     Reduce red = op->red();
     OpDev<R> d = op->dev<R>(batch);
-    std::vector<cudaEvent_t> ev(TOMO_NUM_STAGES + 1);
-    for (auto& e : ev) CK(cudaEventCreate(&e));
     double acc[TOMO_NUM_STAGES] = {0};
     const bool sur = op->surrogate();
-    for (int rep = 0; rep < reps + 1; ++rep) {  // first rep is warm-up
-      CK(cudaMemcpyAsync(S.sc.p, init.data(), sizeof(SliceScalars) * batch, cudaMemcpyHostToDevice, st));
-      for (int k = 0; k <= TOMO_NUM_STAGES; ++k) {
-        if (k > 0) {
-          const int s = k - 1;
-          if (!sur) {
-            if (s == 0) {
-              PUpd<R> pu{};
-              pu.enabled = 1;
-              pu.r = S.r.as<R>();
-              pu.p = S.p0.as<R>();
-              pu.step = 1;
-              pu.red = red;
-              launch_t2_rows<R>(d, batch, S.p0.p, false, pu, st);
-            } else if (s == 1) {
-              launch_t2_cols<R>(d, batch, op->scal(), st);
-            } else if (s == 2) {
-              launch_w<R>(d, batch, d.g, d.s, op->scal(), st);
-            } else if (s == 3) {
-              launch_wt_spread<R>(d, batch, d.s, d.Gt, op->scal(), st);
-            } else if (s == 4) {
-              launch_t1_cols_only<R>(d, batch, op->scal(), st);
-            } else if (s == 5) {
-              PbEpi<R> e = plain_epi<R>(PB_CG_STEP, 1.0);
-              e.p = S.p0.as<R>();
-              e.ap = S.ap.as<R>();
-              e.sys = sp;
-              e.step = 1;
-              e.red = red;
-              launch_t1_rows<R>(d, batch, e, st);
-            }
-          } else if (s == 8) {
-            launch_stencil<R>(n, batch, op->rad, op->coef, 0, S.p0.as<R>(), S.r.as<R>(), S.p1.as<R>(), S.ap.as<R>(),
-                              nullptr, nullptr, sp, 1, red, st);
-          }
-          if (s == 6) launch_cg_update<R>(n, batch, S.p0.as<R>(), S.ap.as<R>(), S.x.as<R>(), S.r.as<R>(), sp, 1, red, st);
-          if (s == 7)
-            launch_sb_post<R>(n, batch, S.mu1.as<R>(), S.mu0.as<R>(), S.bx0.as<R>(), S.by0.as<R>(), S.bx1.as<R>(),
-                              S.by1.as<R>(), S.fid.as<R>(), S.rhs.as<R>(), 1.0, red, st);
+    auto launch_stage = [&](int s, cudaStream_t cs) {
+      if (!sur) {
+        if (s == 0) {
+          PUpd<R> pu{};
+          pu.enabled = 1;
+          pu.r = S.r.as<R>();
+          pu.p = S.p0.as<R>();
+          pu.step = 1;
+          pu.red = red;
+          launch_t2_rows<R>(d, batch, S.p0.p, false, pu, cs);
+        } else if (s == 1) {
+          launch_t2_cols<R>(d, batch, op->scal(), cs);
+        } else if (s == 2) {
+          launch_w<R>(d, batch, d.g, d.s, op->scal(), cs);
+        } else if (s == 3) {
+          launch_wt_spread<R>(d, batch, d.s, d.Gt, op->scal(), cs);
+        } else if (s == 4) {
+          launch_t1_cols_only<R>(d, batch, op->scal(), cs);
+        } else if (s == 5) {
+          PbEpi<R> e = plain_epi<R>(PB_CG_STEP, 1.0);
+          e.p = S.p0.as<R>();
+          e.ap = S.ap.as<R>();
+          e.sys = sp;
+          e.step = 1;
+          e.red = red;
+          launch_t1_rows<R>(d, batch, e, cs);
         }
-        CK(cudaEventRecord(ev[k], st));
+      } else if (s == 8) {
+        launch_stencil<R>(n, batch, op->rad, op->coef, 0, S.p0.as<R>(), S.r.as<R>(), S.p1.as<R>(), S.ap.as<R>(),
+                          nullptr, nullptr, sp, 1, red, cs);
       }
-      CK(cudaEventSynchronize(ev[TOMO_NUM_STAGES]));
-      if (rep == 0) continue;
-      for (int k = 0; k < TOMO_NUM_STAGES; ++k) {
-        float t = 0.f;
-        CK(cudaEventElapsedTime(&t, ev[k], ev[k + 1]));
-        acc[k] += t;
-      }
+      if (s == 6) launch_cg_update<R>(n, batch, S.p0.as<R>(), S.ap.as<R>(), S.x.as<R>(), S.r.as<R>(), sp, 1, red, cs);
+      if (s == 7)
+        launch_sb_post<R>(n, batch, S.mu1.as<R>(), S.mu0.as<R>(), S.bx0.as<R>(), S.by0.as<R>(), S.bx1.as<R>(),
+                          S.by1.as<R>(), S.fid.as<R>(), S.rhs.as<R>(), 1.0, red, cs);
+    };
+    CK(cudaMemcpyAsync(S.sc.p, init.data(), sizeof(SliceScalars) * batch, cudaMemcpyHostToDevice, st));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    for (int s = 0; s < TOMO_NUM_STAGES; ++s) {
+      const bool on = sur ? (s >= 6) : (s <= 7);
+      if (!on) continue;
+      // each stage timed as a CUDA graph of `reps` back-to-back launches (no host launch gaps)
+      const std::string key = fmtkey("prof", batch, {double(s), double(reps)});
+      run_graph(op, key, st, [&](cudaStream_t cs) {
+        for (int r = 0; r < reps; ++r) launch_stage(s, cs);
+      });  // warm-up launch + instantiation
+      CK(cudaEventRecord(e0, st));
+      run_graph(op, key, st, [&](cudaStream_t) {});
+      CK(cudaEventRecord(e1, st));
+      CK(cudaEventSynchronize(e1));
+      float t = 0.f;
+      CK(cudaEventElapsedTime(&t, e0, e1));
+      acc[s] = t;
     }
-    for (auto& e : ev) cudaEventDestroy(e);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
     const double B = batch, nn = static_cast<double>(n) * n, mn = static_cast<double>(m) * n,
                  mm = static_cast<double>(m) * m, P = static_cast<double>(op->g.P), rs = sizeof(R), cs = 2 * sizeof(R);
     const double wbytes = static_cast<double>(op->Ppad) * op->nq * 32.0 * (16.0 + 4.0 * rs) / 32.0;
