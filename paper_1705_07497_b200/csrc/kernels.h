@@ -52,6 +52,8 @@ struct OpDev {
   int n_tasks;
   const uint16_t* wt_perm;         // [G32*32] sorted position -> ix of the block's row
   const int4* wt_heavy;            // {block, slot0, nslots, 0}
+  const int* wt_slot_heavy;        // slot -> heavy block index
+  unsigned* wt_heavy_cnt;          // B x n_heavy task tickets (zero between launches)
   int n_heavy;
   int n_slots;
   cplx<R>* wt_part;                // B x n_slots x 32 partial sums of split blocks

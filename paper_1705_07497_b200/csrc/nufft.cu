@@ -246,10 +246,28 @@ __global__ void __launch_bounds__(256) k_wt_tasks(OpDev<R> d, int B, const cplx<
       a0.y += x0.w * s0.y;
     }
     const C2 v = cadd(a0, a1);
-    if (slot < 0)
+    if (slot < 0) {
       grid[G * b + static_cast<size_t>(iy) * d.m + ix] = v;
-    else
-      d.wt_part[(static_cast<size_t>(b) * d.n_slots + slot) * 32 + lane] = v;
+    } else {
+      // split block: publish the partial; the warp that finishes the block's last task sums
+      // all of its partials in slot order (deterministic) and writes the node values
+      C2* part = d.wt_part + static_cast<size_t>(b) * d.n_slots * 32;
+      part[static_cast<size_t>(slot) * 32 + lane] = v;
+      __threadfence();
+      const int h = __ldg(&d.wt_slot_heavy[slot]);
+      unsigned* cnt = d.wt_heavy_cnt + static_cast<size_t>(b) * d.n_heavy + h;
+      unsigned ticket = 0;
+      if (lane == 0) ticket = atomicAdd(cnt, 1u);
+      ticket = __shfl_sync(0xffffffffu, ticket, 0);
+      const int4 hv = __ldg(&d.wt_heavy[h]);
+      if (ticket == static_cast<unsigned>(hv.z - 1)) {
+        __threadfence();
+        C2 acc = czero<C2>();
+        for (int k = 0; k < hv.z; ++k) acc = cadd(acc, __ldcg(&part[static_cast<size_t>(hv.y + k) * 32 + lane]));
+        grid[G * b + static_cast<size_t>(iy) * d.m + ix] = acc;
+        if (lane == 0) *cnt = 0u;
+      }
+    }
   }
 }
 
@@ -507,11 +525,6 @@ void launch_wt_spread(const OpDev<R>& d, int B, const cplx<R>* samples, cplx<R>*
   if (d.n_tasks > 0) {
     const int blocks = (d.n_tasks * 32 + threads - 1) / threads;
     k_wt_tasks<R><<<blocks, threads, 0, st>>>(d, B, samples, grid, skip);
-    note_launch();
-  }
-  if (d.n_heavy > 0) {
-    const int blocks = (d.n_heavy * 32 + threads - 1) / threads;
-    k_wt_fixup<R><<<blocks, threads, 0, st>>>(d, B, grid, skip);
     note_launch();
   }
 }

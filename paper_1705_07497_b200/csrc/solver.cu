@@ -23,10 +23,12 @@ namespace {
 constexpr int kVecThreads = 256;
 
 int vec_blocks(int64_t L, int B) {
-  // ~4 elements per thread; fewer blocks when the batch already fills the GPU
-  const int64_t per_block = static_cast<int64_t>(kVecThreads) * 4;
-  int64_t nb = (L + per_block - 1) / per_block;
-  if (nb * B > 8 * 148) nb = std::max<int64_t>(1, (8 * 148 + B - 1) / B);
+  // One element per thread (all loads of the pass in flight at once: these kernels are
+  // latency-bound at solver sizes), up to 4096 blocks per slice, then more per thread.
+  (void)B;
+  const int64_t ept = std::max<int64_t>(1, (L + kVecThreads * 4096LL - 1) / (kVecThreads * 4096LL));
+  const int64_t per_block = static_cast<int64_t>(kVecThreads) * ept;
+  const int64_t nb = (L + per_block - 1) / per_block;
   return static_cast<int>(std::min<int64_t>(std::max<int64_t>(nb, 1), MAX_PART_BLOCKS));
 }
 

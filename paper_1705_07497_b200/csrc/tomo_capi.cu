@@ -222,6 +222,7 @@ constexpr int kMaxLoggedIters = 8192;
 struct Scratch {
   int cap = 0;
   Raw H, g, s, K, Gt, part_wt;    // complex
+  Raw heavy_cnt;
   Raw cin, cout, fin, fout;       // staging for host pointers / temporaries
   Raw r, p0, p1, ap, x, rhs, fid, mu0, mu1, bx0, bx1, by0, by1, nred, zero, u2;  // real vectors
   Raw upd_log, sc, part;
@@ -245,7 +246,7 @@ struct tomo_op {
   int64_t nnz = 0, wt_rows = 0, wt_slots = 0;
   int nq = 0, Ppad = 0;
   int n_tasks = 0, n_heavy = 0, n_slots = 0;
-  Raw apod, tw, wcols, wvals, wtent, wttasks, wtperm, wtheavy;
+  Raw apod, tw, wcols, wvals, wtent, wttasks, wtperm, wtheavy, wtslotheavy;
   Scratch sc;
   // surrogate
   int rad = 0;
@@ -293,6 +294,8 @@ struct tomo_op {
     d.n_tasks = n_tasks;
     d.wt_perm = wtperm.as<uint16_t>();
     d.wt_heavy = wtheavy.as<int4>();
+    d.wt_slot_heavy = wtslotheavy.as<int>();
+    d.wt_heavy_cnt = sc.heavy_cnt.as<unsigned>();
     d.n_heavy = n_heavy;
     d.n_slots = n_slots;
     d.wt_part = sc.part_wt.as<cplx<R>>();
@@ -312,6 +315,8 @@ struct tomo_op {
     sc.Gt.ensure(B * m * m * cz);
     CK(cudaMemset(sc.Gt.p, 0, B * m * m * cz));  // untouched spread-grid nodes stay zero
     sc.part_wt.ensure(static_cast<size_t>(B) * std::max(n_slots, 1) * 32 * cz);
+    sc.heavy_cnt.ensure(sizeof(unsigned) * static_cast<size_t>(B) * std::max(n_heavy, 1));
+    CK(cudaMemset(sc.heavy_cnt.p, 0, sizeof(unsigned) * static_cast<size_t>(B) * std::max(n_heavy, 1)));
     sc.s.ensure(B * static_cast<size_t>(g.P) * cz);
     sc.K.ensure(B * n * m * cz);
     sc.sc.ensure(sizeof(SliceScalars) * B);
@@ -449,6 +454,7 @@ void build_tables(tomo_op* op) {
     }
   }
   std::vector<int4> tasks, heavy;
+  std::vector<int> slot_heavy;
   int slots = 0;
   for (int64_t bk = 0; bk < G32; ++bk) {
     const int Lb = blockL[bk];
@@ -458,6 +464,7 @@ void build_tables(tomo_op* op) {
     } else {
       const int ns = (Lb + kWtMaxChunks - 1) / kWtMaxChunks;
       heavy.push_back(make_int4(static_cast<int>(bk), slots, ns, 0));
+      for (int k = 0; k < ns; ++k) slot_heavy.push_back(static_cast<int>(heavy.size()) - 1);
       for (int k = 0; k < ns; ++k) {
         const int c0 = k * kWtMaxChunks;
         tasks.push_back(make_int4(static_cast<int>(bk), static_cast<int>(chunk0[bk]) + c0,
@@ -490,6 +497,7 @@ void build_tables(tomo_op* op) {
   op->wttasks.upload(tasks.empty() ? std::vector<int4>(1) : tasks);
   op->wtperm.upload(perm);
   op->wtheavy.upload(heavy.empty() ? std::vector<int4>(1) : heavy);
+  op->wtslotheavy.upload(slot_heavy.empty() ? std::vector<int>(1) : slot_heavy);
   op->apod.upload(apod);
   op->tw.upload(tw);
 }
