@@ -44,6 +44,13 @@ struct OpDev {
   const cplx<R>* tw;               // m   : e^{-2 pi i k/m}
   const int4* w_cols;              // SELL-32 ELL of W: [(Ppad/32) * nq * 32] int4
   const Quad<R>* w_vals;           //                   [(Ppad/32) * nq * 32]
+  // Separable ("rank-1 block") storage of the same W: row j's w x w block is
+  // wx_j[a] * wy_j[b] at nodes ((iy0+b) mod m, (ix0+a) mod m) (nufft.cpp:185-200).
+  const int* w_base;               // [Ppad] ix0 | iy0 << 16
+  const R* w_x;                    // [w][Ppad]
+  const R* w_y;                    // [w][Ppad]
+  int w;                           // window width
+  int w_sep;                       // 1: use the separable storage for W, 0: the SELL-32 ELL
   // W^T: nodes of each grid row sorted by entry count (SELL-32-sigma, sigma = one grid row);
   // the 32-node blocks are processed as a balanced list of warp tasks of <= kWtMaxChunks
   // chunks; blocks longer than that are split and their partial sums combined by a fix-up.

@@ -80,7 +80,7 @@ struct NoStore {
 // deapodise + pad + inverse FFT along t2; the CG p-update (p = r + beta p) is fused into the
 // load; output transposed to H[iy][t1] through smem.
 template <int M, typename R>
-__global__ void __launch_bounds__(kFftThreads) k_t2_rows(OpDev<R> d, const void* __restrict__ in, int in_complex,
+__global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? 2 : 1) k_t2_rows(OpDev<R> d, const void* __restrict__ in, int in_complex,
                                                   PUpd<R> pu, int rpc) {
   using S = FftShape<M>;
   using C2 = cplx<R>;
@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(kFftThreads) k_t2_rows(OpDev<R> d, const void*
 
 // ---------------------------------------------------------------- P2: grid rows (iy)
 template <int M, typename R>
-__global__ void __launch_bounds__(kFftThreads) k_t2_cols(OpDev<R> d, int rpc, const SliceScalars* skip) {
+__global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? 2 : 1) k_t2_cols(OpDev<R> d, int rpc, const SliceScalars* skip) {
   using S = FftShape<M>;
   using C2 = cplx<R>;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -204,6 +204,67 @@ __global__ void __launch_bounds__(256) k_w(OpDev<R> d, int B, const cplx<R>* __r
         if (b0 + q < B && !(skip && (skip[b0 + q].done || skip[b0 + q].frozen)))
           out[static_cast<size_t>(b0 + q) * d.P + j] = acc[q];
     }
+  }
+}
+
+// ---------------------------------------------------------------- W, separable storage
+// Same matrix as k_w, stored as its rank-1 blocks: per row j the base node (ix0, iy0) and the
+// two window factor vectors (SoA, coalesced): 4 + 2w*sizeof(R) bytes per row instead of
+// w^2*(4 + sizeof(R)). The inner loop walks a grid row (b fixed, ix0+a consecutive).
+template <int BT, typename R>
+__global__ void __launch_bounds__(256) k_w_sep(OpDev<R> d, int B, const cplx<R>* __restrict__ grid,
+                                                cplx<R>* __restrict__ out, const SliceScalars* skip) {
+  using C2 = cplx<R>;
+  constexpr int WMAX = 16;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= d.P) return;
+  const int m = d.m, w = d.w;
+  const int base = __ldg(&d.w_base[j]);
+  const int ix0 = base & 0xffff, iy0 = base >> 16;
+  R wx[WMAX], wy[WMAX];
+  int ix[WMAX];
+#pragma unroll
+  for (int a = 0; a < WMAX; ++a) {
+    if (a < w) {
+      wx[a] = __ldg(&d.w_x[static_cast<size_t>(a) * d.Ppad + j]);
+      wy[a] = __ldg(&d.w_y[static_cast<size_t>(a) * d.Ppad + j]);
+      const int t = ix0 + a;
+      ix[a] = t >= m ? t - m : t;
+    }
+  }
+  const size_t G = static_cast<size_t>(m) * m;
+  for (int b0 = 0; b0 < B; b0 += BT) {
+    C2 acc[BT];
+#pragma unroll
+    for (int q = 0; q < BT; ++q) acc[q] = czero<C2>();
+#pragma unroll
+    for (int bb = 0; bb < WMAX; ++bb) {
+      if (bb < w) {
+        const int t = iy0 + bb;
+        const size_t rowoff = static_cast<size_t>(t >= m ? t - m : t) * m;
+#pragma unroll
+        for (int q = 0; q < BT; ++q) {
+          if (b0 + q < B) {
+            const C2* row = grid + G * (b0 + q) + rowoff;
+            C2 ra = czero<C2>();
+#pragma unroll
+            for (int a = 0; a < WMAX; ++a) {
+              if (a < w) {
+                const C2 gv = row[ix[a]];
+                ra.x += wx[a] * gv.x;
+                ra.y += wx[a] * gv.y;
+              }
+            }
+            acc[q].x += wy[bb] * ra.x;
+            acc[q].y += wy[bb] * ra.y;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < BT; ++q)
+      if (b0 + q < B && !(skip && (skip[b0 + q].done || skip[b0 + q].frozen)))
+        out[static_cast<size_t>(b0 + q) * d.P + j] = acc[q];
   }
 }
 
@@ -294,7 +355,7 @@ __global__ void k_wt_fixup(OpDev<R> d, int B, cplx<R>* __restrict__ grid, const 
 // ---------------------------------------------------------------- PA: grid rows (iy), type 1
 // forward FFT along ix of the spread grid row, pruned to the n bins, transposed to K[t1][iy].
 template <int M, typename R>
-__global__ void __launch_bounds__(kFftThreads) k_t1_cols(OpDev<R> d, int rpc, const SliceScalars* skip) {
+__global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? 2 : 1) k_t1_cols(OpDev<R> d, int rpc, const SliceScalars* skip) {
   using S = FftShape<M>;
   using C2 = cplx<R>;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -336,7 +397,7 @@ __device__ __forceinline__ R ktk_at(const R* __restrict__ p, int n, int i, int j
 // forward FFT along iy, crop to the n bins, deapodise, then the epilogue: complex / real
 // output or the CG system apply alpha*Re(N p) + lambda K'K p + shift p with the dots.
 template <int M, typename R>
-__global__ void __launch_bounds__(kFftThreads) k_t1_rows(OpDev<R> d, PbEpi<R> e, int rpc) {
+__global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? 2 : 1) k_t1_rows(OpDev<R> d, PbEpi<R> e, int rpc) {
   using S = FftShape<M>;
   using C2 = cplx<R>;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -509,12 +570,18 @@ void launch_w(const OpDev<R>& d, int B, const cplx<R>* grid, cplx<R>* samples, c
               cudaStream_t st) {
   const int threads = 256;
   const int blocks = (d.Ppad + threads - 1) / threads;
-  if (B >= 4)
+  if (d.w_sep) {
+    if (B >= 2)
+      k_w_sep<2, R><<<blocks, threads, 0, st>>>(d, B, grid, samples, skip);
+    else
+      k_w_sep<1, R><<<blocks, threads, 0, st>>>(d, B, grid, samples, skip);
+  } else if (B >= 4) {
     k_w<4, R><<<blocks, threads, 0, st>>>(d, B, grid, samples, skip);
-  else if (B >= 2)
+  } else if (B >= 2) {
     k_w<2, R><<<blocks, threads, 0, st>>>(d, B, grid, samples, skip);
-  else
+  } else {
     k_w<1, R><<<blocks, threads, 0, st>>>(d, B, grid, samples, skip);
+  }
   note_launch();
 }
 

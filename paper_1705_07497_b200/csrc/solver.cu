@@ -22,13 +22,24 @@ namespace {
 
 constexpr int kVecThreads = 256;
 
+template <typename R>
+struct Vec16;
+template <>
+struct Vec16<float> {
+  using T = float4;
+};
+template <>
+struct Vec16<double> {
+  using T = double2;
+};
+
 int vec_blocks(int64_t L, int B) {
-  // One element per thread (all loads of the pass in flight at once: these kernels are
-  // latency-bound at solver sizes), up to 4096 blocks per slice, then more per thread.
-  (void)B;
-  const int64_t ept = std::max<int64_t>(1, (L + kVecThreads * 4096LL - 1) / (kVecThreads * 4096LL));
-  const int64_t per_block = static_cast<int64_t>(kVecThreads) * ept;
-  const int64_t nb = (L + per_block - 1) / per_block;
+  // ~4 elements per thread, but keep the per-slice block count (and so the cost of the
+  // last-block reduction) bounded when a batch of slices already fills the GPU.
+  const int64_t per_block = static_cast<int64_t>(kVecThreads) * 4;
+  int64_t nb = (L + per_block - 1) / per_block;
+  const int64_t cap = std::max<int64_t>(8, 16 * 148 / std::max(B, 1));
+  nb = std::min(nb, cap);
   return static_cast<int>(std::min<int64_t>(std::max<int64_t>(nb, 1), MAX_PART_BLOCKS));
 }
 
@@ -62,13 +73,29 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_update(int64_t L, const R* _
   const size_t off = static_cast<size_t>(b) * L;
   double rr = 0.0;
   bool fin = true;
-  for (int64_t i = gtid(); i < L; i += gstride()) {
-    const R xv = x[off + i] + alpha * p[off + i];
-    const R rv = r[off + i] - alpha * ap[off + i];
-    x[off + i] = xv;
-    r[off + i] = rv;
-    fin = fin && finite_r(xv);
-    rr += static_cast<double>(rv) * rv;
+  // 16-byte vectors (float4 / double2), two per iteration: 8 independent loads in flight
+  using V = typename Vec16<R>::T;
+  constexpr int VW = 16 / sizeof(R);
+  const int64_t nv = L / VW;  // L = n^2 with n even: multiple of 4
+  const V* p4 = reinterpret_cast<const V*>(p + off);
+  const V* ap4 = reinterpret_cast<const V*>(ap + off);
+  V* x4 = reinterpret_cast<V*>(x + off);
+  V* r4 = reinterpret_cast<V*>(r + off);
+  for (int64_t i = gtid(); i < nv; i += gstride()) {
+    V pv = p4[i], av = ap4[i], xv = x4[i], rv = r4[i];
+    R* pe = reinterpret_cast<R*>(&pv);
+    R* ae = reinterpret_cast<R*>(&av);
+    R* xe = reinterpret_cast<R*>(&xv);
+    R* re = reinterpret_cast<R*>(&rv);
+#pragma unroll
+    for (int k = 0; k < VW; ++k) {
+      xe[k] += alpha * pe[k];
+      re[k] -= alpha * ae[k];
+      fin = fin && finite_r(xe[k]);
+      rr += static_cast<double>(re[k]) * re[k];
+    }
+    x4[i] = xv;
+    r4[i] = rv;
   }
   if (!fin) sc.nonfinite = 1;
   double t0, t1;

@@ -16,6 +16,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -246,7 +247,8 @@ struct tomo_op {
   int64_t nnz = 0, wt_rows = 0, wt_slots = 0;
   int nq = 0, Ppad = 0;
   int n_tasks = 0, n_heavy = 0, n_slots = 0;
-  Raw apod, tw, wcols, wvals, wtent, wttasks, wtperm, wtheavy, wtslotheavy;
+  Raw apod, tw, wcols, wvals, wbase, wxs, wys, wtent, wttasks, wtperm, wtheavy, wtslotheavy;
+  int w_sep = 1;  // W storage used by the interpolation kernel (TOMO_W_FORMAT=ell selects SELL-32)
   Scratch sc;
   // surrogate
   int rad = 0;
@@ -289,6 +291,11 @@ struct tomo_op {
     d.tw = tw.as<cplx<R>>();
     d.w_cols = wcols.as<int4>();
     d.w_vals = wvals.as<Quad<R>>();
+    d.w_base = wbase.as<int>();
+    d.w_x = wxs.as<R>();
+    d.w_y = wys.as<R>();
+    d.w = g.w;
+    d.w_sep = w_sep;
     d.wt_ent = wtent.as<WtEnt<R>>();
     d.wt_tasks = wttasks.as<int4>();
     d.n_tasks = n_tasks;
@@ -491,6 +498,22 @@ void build_tables(tomo_op* op) {
     tw[k].x = static_cast<R>(std::cos(ang));
     tw[k].y = static_cast<R>(std::sin(ang));
   }
+  // separable storage of the same rows: base node + the two factor vectors (SoA)
+  std::vector<int> wbase(op->Ppad, 0);
+  std::vector<R> wxs(static_cast<size_t>(w) * op->Ppad, R(0)), wys(static_cast<size_t>(w) * op->Ppad, R(0));
+  for (int64_t j = 0; j < g.P; ++j) {
+    const int ix0 = wrapi(pl.mjx[j] + g.lo, m), iy0 = wrapi(pl.mjy[j] + g.lo, m);
+    wbase[j] = ix0 | (iy0 << 16);
+    for (int a = 0; a < w; ++a) {
+      wxs[static_cast<size_t>(a) * op->Ppad + j] = static_cast<R>(pl.wx[j * w + a]);
+      wys[static_cast<size_t>(a) * op->Ppad + j] = static_cast<R>(pl.wy[j * w + a]);
+    }
+  }
+  const char* fmt = std::getenv("TOMO_W_FORMAT");
+  op->w_sep = (fmt && std::string(fmt) == "ell") ? 0 : 1;
+  op->wbase.upload(wbase);
+  op->wxs.upload(wxs);
+  op->wys.upload(wys);
   op->wcols.upload(cols);
   op->wvals.upload(vals);
   op->wtent.upload(ent);
@@ -1585,7 +1608,8 @@ int tomo_profile_stages(tomo_op* op, int batch, int reps, double* ms, double* by
     cudaEventDestroy(e1);
     const double B = batch, nn = static_cast<double>(n) * n, mn = static_cast<double>(m) * n,
                  mm = static_cast<double>(m) * m, P = static_cast<double>(op->g.P), rs = sizeof(R), cs = 2 * sizeof(R);
-    const double wbytes = static_cast<double>(op->Ppad) * op->nq * 32.0 * (16.0 + 4.0 * rs) / 32.0;
+    const double wbytes = op->w_sep ? static_cast<double>(op->g.P) * (4.0 + 2.0 * op->g.w * rs)
+                                    : static_cast<double>(op->Ppad) * op->nq * 32.0 * (16.0 + 4.0 * rs) / 32.0;
     const double wtbytes = static_cast<double>(op->wt_slots) * sizeof(WtEnt<R>) + op->n_tasks * 16.0 +
                            static_cast<double>(op->wt_rows) * 2.0;
     double by[TOMO_NUM_STAGES] = {0};
