@@ -1534,8 +1534,10 @@ int tomo_profile_stages(tomo_op* op, int batch, int reps, double* ms, double* by
     std::mt19937 rng(5);
     std::normal_distribution<double> nd;
     for (auto& v : h) v = static_cast<R>(nd(rng));
-    for (auto* b : {&S.r, &S.p0, &S.p1, &S.x, &S.ap, &S.mu0, &S.mu1, &S.bx0, &S.by0, &S.fid, &S.rhs})
+    for (auto* b : {&S.r, &S.p0, &S.p1, &S.x, &S.ap, &S.mu0, &S.bx0, &S.by0, &S.fid, &S.rhs})
       CK(cudaMemcpyAsync(b->p, h.data(), sizeof(R) * cnt, cudaMemcpyHostToDevice, st));
+    for (auto& v : h) v = static_cast<R>(nd(rng));  // mu_new != mu_old: the update is non-zero
+    CK(cudaMemcpyAsync(S.mu1.p, h.data(), sizeof(R) * cnt, cudaMemcpyHostToDevice, st));
     std::vector<SliceScalars> init(batch);
     std::memset(init.data(), 0, sizeof(SliceScalars) * batch);
     for (auto& sc : init) {
@@ -1593,9 +1595,11 @@ int tomo_profile_stages(tomo_op* op, int batch, int reps, double* ms, double* by
       if (!on) continue;
       // each stage timed as a CUDA graph of `reps` back-to-back launches (no host launch gaps)
       const std::string key = fmtkey("prof", batch, {double(s), double(reps)});
+      CK(cudaMemcpyAsync(S.sc.p, init.data(), sizeof(SliceScalars) * batch, cudaMemcpyHostToDevice, st));
       run_graph(op, key, st, [&](cudaStream_t cs) {
         for (int r = 0; r < reps; ++r) launch_stage(s, cs);
       });  // warm-up launch + instantiation
+      CK(cudaMemcpyAsync(S.sc.p, init.data(), sizeof(SliceScalars) * batch, cudaMemcpyHostToDevice, st));
       CK(cudaEventRecord(e0, st));
       run_graph(op, key, st, [&](cudaStream_t) {});
       CK(cudaEventRecord(e1, st));
