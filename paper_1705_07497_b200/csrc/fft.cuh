@@ -101,15 +101,20 @@ struct Dft<16, C2> {
   }
 };
 
-template <int M>
+// Row of length M served by T = M/RB threads: passes of radix RB (16, 8 or 4) and a final
+// smaller radix RL. A smaller base radix gives more threads per row and fewer registers per
+// thread (more warps for small, latency-bound problems) at the cost of one more smem pass.
+template <int M, int RB = 16>
 struct FftShape {
   static constexpr int LOG = (M >= 8192) ? 13 : (M >= 4096) ? 12 : (M >= 2048) ? 11 : (M >= 1024) ? 10
                            : (M >= 512) ? 9 : (M >= 256) ? 8 : (M >= 128) ? 7 : (M >= 64) ? 6 : 5;
-  static constexpr int N16 = LOG / 4;          // number of radix-16 passes
-  static constexpr int RL = 1 << (LOG % 4);    // final radix (1 = none)
-  static constexpr int NP = N16 + (RL > 1 ? 1 : 0);
-  static constexpr int T = M / 16;             // threads per row
-  static constexpr int STRIDE = padded_len(M); // smem row stride (elements)
+  static constexpr int LB = RB == 16 ? 4 : RB == 8 ? 3 : 2;  // log2(RB)
+  static constexpr int NB = LOG / LB;                          // number of radix-RB passes
+  static constexpr int RL = 1 << (LOG % LB);                   // final radix (1 = none)
+  static constexpr int NP = NB + (RL > 1 ? 1 : 0);
+  static constexpr int T = M / RB;                             // threads per row
+  static constexpr int STRIDE = padded_len(M);                 // smem row stride (elements)
+  static_assert(RB == 16 || RB == 8 || RB == 4, "base radix");
   static_assert((1 << LOG) == M, "M must be a power of two in [32, 8192]");
   static_assert(NP >= 2, "at least two passes");
 };
@@ -152,11 +157,12 @@ TOMO_DEV void twiddle(C2* v, const C2* __restrict__ tw, int base) {
 // store(k, value), otherwise back into the smem row. Every thread of the CTA must call each
 // pass (barriers inside); `active` gates the work. STORE_SMEM_LAST: the storer writes the smem
 // row, so a barrier separates the last reads from those writes.
-template <int M, int R, bool FIRST, bool LAST, bool STORE_SMEM_LAST, typename C2, typename Load, typename Store>
+template <int M, int RB, int R, bool FIRST, bool LAST, bool STORE_SMEM_LAST, typename C2, typename Load,
+          typename Store>
 TOMO_DEV void fft_pass(C2* row, const C2* __restrict__ tw, int Ns, int t, bool active, Load& load, Store& store) {
-  constexpr int T = M / 16;
+  constexpr int T = M / RB;
   constexpr int NB = M / R;    // butterflies per pass
-  constexpr int PER = NB / T;  // butterflies per thread (16/R)
+  constexpr int PER = NB / T;  // butterflies per thread (RB/R)
   C2 v[PER][R];
   if (active) {
 #pragma unroll
@@ -191,26 +197,26 @@ TOMO_DEV void fft_pass(C2* row, const C2* __restrict__ tw, int Ns, int t, bool a
 }
 
 // Forward FFT of one row per thread group: load(i) -> ... -> store(k, X[k]).
-template <int M, bool STORE_SMEM, typename C2, typename Load, typename Store>
+template <int M, int RB, bool STORE_SMEM, typename C2, typename Load, typename Store>
 TOMO_DEV void fft_row(C2* row, const C2* __restrict__ tw, int t, bool active, Load&& load, Store&& store) {
-  using S = FftShape<M>;
-  fft_pass<M, 16, true, false, false, C2>(row, tw, 1, t, active, load, store);
+  using S = FftShape<M, RB>;
+  fft_pass<M, RB, RB, true, false, false, C2>(row, tw, 1, t, active, load, store);
   if constexpr (S::RL > 1) {
-    int Ns = 16;
+    int Ns = RB;
 #pragma unroll
-    for (int p = 1; p < S::N16; ++p) {
-      fft_pass<M, 16, false, false, false, C2>(row, tw, Ns, t, active, load, store);
-      Ns *= 16;
+    for (int p = 1; p < S::NB; ++p) {
+      fft_pass<M, RB, RB, false, false, false, C2>(row, tw, Ns, t, active, load, store);
+      Ns *= RB;
     }
-    fft_pass<M, S::RL, false, true, STORE_SMEM, C2>(row, tw, Ns, t, active, load, store);
+    fft_pass<M, RB, S::RL, false, true, STORE_SMEM, C2>(row, tw, Ns, t, active, load, store);
   } else {
-    int Ns = 16;
+    int Ns = RB;
 #pragma unroll
-    for (int p = 1; p < S::N16 - 1; ++p) {
-      fft_pass<M, 16, false, false, false, C2>(row, tw, Ns, t, active, load, store);
-      Ns *= 16;
+    for (int p = 1; p < S::NB - 1; ++p) {
+      fft_pass<M, RB, RB, false, false, false, C2>(row, tw, Ns, t, active, load, store);
+      Ns *= RB;
     }
-    fft_pass<M, 16, false, true, STORE_SMEM, C2>(row, tw, Ns, t, active, load, store);
+    fft_pass<M, RB, RB, false, true, STORE_SMEM, C2>(row, tw, Ns, t, active, load, store);
   }
 }
 

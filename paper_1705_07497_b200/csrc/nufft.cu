@@ -79,10 +79,10 @@ struct NoStore {
 // ---------------------------------------------------------------- P1: image rows (t1)
 // deapodise + pad + inverse FFT along t2; the CG p-update (p = r + beta p) is fused into the
 // load; output transposed to H[iy][t1] through smem.
-template <int M, typename R>
+template <int M, int RB, typename R>
 __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? 2 : 1) k_t2_rows(OpDev<R> d, const void* __restrict__ in, int in_complex,
                                                   PUpd<R> pu, int rpc) {
-  using S = FftShape<M>;
+  using S = FftShape<M, RB>;
   using C2 = cplx<R>;
   extern __shared__ __align__(16) unsigned char smraw[];
   C2* sm = reinterpret_cast<C2*>(smraw);
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? 2 : 1) k_t2_rows
     return v;
   };
   auto store = [&](int k, C2 v) { row[pad16(k)] = cconj(v); };
-  fft_row<M, true, C2>(row, d.tw, t, active, load, store);
+  fft_row<M, RB, true, C2>(row, d.tw, t, active, load, store);
   // transposed store H[b][k][t1]: rpc consecutive t1 per k
   C2* H = d.H + static_cast<size_t>(b) * M * n;
   for (int idx = threadIdx.x; idx < M * rpc; idx += blockDim.x) {
@@ -131,9 +131,9 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? 2 : 1) k_t2_rows
 }
 
 // ---------------------------------------------------------------- P2: grid rows (iy)
-template <int M, typename R>
+template <int M, int RB, typename R>
 __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? 2 : 1) k_t2_cols(OpDev<R> d, int rpc, const SliceScalars* skip) {
-  using S = FftShape<M>;
+  using S = FftShape<M, RB>;
   using C2 = cplx<R>;
   extern __shared__ __align__(16) unsigned char smraw[];
   C2* sm = reinterpret_cast<C2*>(smraw);
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? 2 : 1) k_t2_cols
     return t1 < n ? cconj(H[t1]) : czero<C2>();
   };
   auto store = [&](int k, C2 v) { g[k] = cconj(v); };
-  fft_row<M, false, C2>(row, d.tw, t, active, load, store);
+  fft_row<M, RB, false, C2>(row, d.tw, t, active, load, store);
 }
 
 // ---------------------------------------------------------------- W: SELL-32 ELL SpMV
@@ -211,11 +211,10 @@ __global__ void __launch_bounds__(256) k_w(OpDev<R> d, int B, const cplx<R>* __r
 // Same matrix as k_w, stored as its rank-1 blocks: per row j the base node (ix0, iy0) and the
 // two window factor vectors (SoA, coalesced): 4 + 2w*sizeof(R) bytes per row instead of
 // w^2*(4 + sizeof(R)). The inner loop walks a grid row (b fixed, ix0+a consecutive).
-template <int BT, typename R>
+template <int BT, int WMAX, typename R>
 __global__ void __launch_bounds__(256) k_w_sep(OpDev<R> d, int B, const cplx<R>* __restrict__ grid,
                                                 cplx<R>* __restrict__ out, const SliceScalars* skip) {
   using C2 = cplx<R>;
-  constexpr int WMAX = 16;
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= d.P) return;
   const int m = d.m, w = d.w;
@@ -354,9 +353,9 @@ __global__ void k_wt_fixup(OpDev<R> d, int B, cplx<R>* __restrict__ grid, const 
 
 // ---------------------------------------------------------------- PA: grid rows (iy), type 1
 // forward FFT along ix of the spread grid row, pruned to the n bins, transposed to K[t1][iy].
-template <int M, typename R>
+template <int M, int RB, typename R>
 __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? 2 : 1) k_t1_cols(OpDev<R> d, int rpc, const SliceScalars* skip) {
-  using S = FftShape<M>;
+  using S = FftShape<M, RB>;
   using C2 = cplx<R>;
   extern __shared__ __align__(16) unsigned char smraw[];
   C2* sm = reinterpret_cast<C2*>(smraw);
@@ -373,7 +372,7 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? 2 : 1) k_t1_cols
     const int t1 = (k + n / 2) & (M - 1);  // inverse of bin_of
     if (t1 < n) row[pad16(t1)] = v;
   };
-  fft_row<M, true, C2>(row, d.tw, t, active, load, store);
+  fft_row<M, RB, true, C2>(row, d.tw, t, active, load, store);
   C2* K = d.K + static_cast<size_t>(b) * n * M;
   for (int idx = threadIdx.x; idx < n * rpc; idx += blockDim.x) {
     const int t1 = idx / rpc, q = idx - t1 * rpc;
@@ -396,9 +395,9 @@ __device__ __forceinline__ R ktk_at(const R* __restrict__ p, int n, int i, int j
 // ---------------------------------------------------------------- PB: image rows (t1)
 // forward FFT along iy, crop to the n bins, deapodise, then the epilogue: complex / real
 // output or the CG system apply alpha*Re(N p) + lambda K'K p + shift p with the dots.
-template <int M, typename R>
+template <int M, int RB, typename R>
 __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? 2 : 1) k_t1_rows(OpDev<R> d, PbEpi<R> e, int rpc) {
-  using S = FftShape<M>;
+  using S = FftShape<M, RB>;
   using C2 = cplx<R>;
   extern __shared__ __align__(16) unsigned char smraw[];
   C2* sm = reinterpret_cast<C2*>(smraw);
@@ -447,7 +446,7 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? 2 : 1) k_t1_rows
       }
     }
   };
-  fft_row<M, false, C2>(row, d.tw, t, active, load, store);
+  fft_row<M, RB, false, C2>(row, d.tw, t, active, load, store);
   if (e.mode >= PB_CG_STEP) {
     double t0s, t1s;
     SliceScalars& sc = e.red.sc[b];
@@ -479,9 +478,9 @@ __global__ void k_weight_samples(cplx<R>* s, int B, int P, int nb) {
   s[i] = cscale(s[i], w);
 }
 
-template <int M, typename R>
+template <int M, int RB, typename R>
 __global__ void k_fft_rows_test(const cplx<R>* tw, const cplx<R>* in, cplx<R>* out, int rows, int inverse) {
-  using S = FftShape<M>;
+  using S = FftShape<M, RB>;
   using C2 = cplx<R>;
   extern __shared__ __align__(16) unsigned char smraw[];
   C2* sm = reinterpret_cast<C2*>(smraw);
@@ -491,19 +490,28 @@ __global__ void k_fft_rows_test(const cplx<R>* tw, const cplx<R>* in, cplx<R>* o
   C2* dst = out + static_cast<size_t>(r) * M;
   auto load = [&](int i) -> C2 { return inverse ? cconj(src[i]) : src[i]; };
   auto store = [&](int k, C2 v) { dst[k] = inverse ? cconj(v) : v; };
-  fft_row<M, false, C2>(sm, tw, t, true, load, store);
+  fft_row<M, RB, false, C2>(sm, tw, t, true, load, store);
 }
 
 // ---------------------------------------------------------------- dispatch helpers
 // rows-per-CTA: transposed stores need >= 32 B per row segment (rpc >= 32 / sizeof(C2)),
 // enough threads per CTA, bounded smem, and as many CTAs as possible above that.
-int choose_rpc(int m, int rows_per_slice, int B, size_t elem, bool transposed) {
-  const int T = m / 16;
+int choose_rpc(int T, int m, int rows_per_slice, int B, size_t elem, bool transposed) {
   const int min_rpc = transposed ? std::max(1, static_cast<int>(32 / elem)) : 1;
   int rpc = std::max(min_rpc, std::max(1, 128 / T));
   while (rpc > 1 && (rpc * T > kFftThreads || static_cast<size_t>(rpc) * padded_len(m) * elem > 110 * 1024)) rpc >>= 1;
   while (rpc > min_rpc && rpc * T > 256 && static_cast<int64_t>((rows_per_slice + rpc - 1) / rpc) * B < 2 * 148) rpc >>= 1;
   return std::max(rpc, 1);
+}
+
+// Base radix for a batch of `rows` rows of length m: radix-16 (fewest smem passes) when the
+// rows alone give enough threads to fill the GPU, else radix 8 or 4 (more threads per row,
+// fewer registers per thread) -- small solver problems are latency-bound, not flop-bound.
+int choose_rb(int m, int64_t rows, size_t elem) {
+  const int64_t want = (elem >= 16 ? 2 : 1) * 148LL * 2048;
+  if (rows * (m / 16) >= want) return 16;
+  if (rows * (m / 8) >= want / 2 || m < 64) return 8;
+  return 4;
 }
 
 template <typename F>
@@ -520,6 +528,17 @@ void dispatch_m(int m, F&& f) {
     case 8192: f(std::integral_constant<int, 8192>{}); break;
     default: throw std::runtime_error("grid side m must be a power of two in [32, 8192], got " + std::to_string(m));
   }
+}
+
+template <typename F>
+void dispatch_m_rb(int m, int rb, F&& f) {
+  dispatch_m(m, [&](auto MC) {
+    switch (rb) {
+      case 16: f(MC, std::integral_constant<int, 16>{}); break;
+      case 8: f(MC, std::integral_constant<int, 8>{}); break;
+      default: f(MC, std::integral_constant<int, 4>{}); break;
+    }
+  });
 }
 
 template <typename K>
@@ -539,28 +558,28 @@ void set_smem(K kernel, size_t bytes) {
 
 template <typename R>
 void launch_t2_rows(const OpDev<R>& d, int B, const void* in, bool in_complex, const PUpd<R>& pu, cudaStream_t st) {
-  dispatch_m(d.m, [&](auto MC) {
-    constexpr int M = decltype(MC)::value;
-    using S = FftShape<M>;
-    const int rpc = choose_rpc(M, d.n, B, sizeof(cplx<R>), true);
+  dispatch_m_rb(d.m, choose_rb(d.m, static_cast<int64_t>(d.n) * B, sizeof(cplx<R>)), [&](auto MC, auto RC) {
+    constexpr int M = decltype(MC)::value, RB = decltype(RC)::value;
+    using S = FftShape<M, RB>;
+    const int rpc = choose_rpc(S::T, M, d.n, B, sizeof(cplx<R>), true);
     const size_t smem = static_cast<size_t>(rpc) * S::STRIDE * sizeof(cplx<R>);
-    set_smem(k_t2_rows<M, R>, smem);
+    set_smem(k_t2_rows<M, RB, R>, smem);
     dim3 grid((d.n + rpc - 1) / rpc, B);
-    k_t2_rows<M, R><<<grid, rpc * S::T, smem, st>>>(d, in, in_complex ? 1 : 0, pu, rpc);
+    k_t2_rows<M, RB, R><<<grid, rpc * S::T, smem, st>>>(d, in, in_complex ? 1 : 0, pu, rpc);
     note_launch();
   });
 }
 
 template <typename R>
 void launch_t2_cols(const OpDev<R>& d, int B, const SliceScalars* skip, cudaStream_t st) {
-  dispatch_m(d.m, [&](auto MC) {
-    constexpr int M = decltype(MC)::value;
-    using S = FftShape<M>;
-    const int rpc = choose_rpc(M, M, B, sizeof(cplx<R>), false);
+  dispatch_m_rb(d.m, choose_rb(d.m, static_cast<int64_t>(d.m) * B, sizeof(cplx<R>)), [&](auto MC, auto RC) {
+    constexpr int M = decltype(MC)::value, RB = decltype(RC)::value;
+    using S = FftShape<M, RB>;
+    const int rpc = choose_rpc(S::T, M, M, B, sizeof(cplx<R>), false);
     const size_t smem = static_cast<size_t>(rpc) * S::STRIDE * sizeof(cplx<R>);
-    set_smem(k_t2_cols<M, R>, smem);
+    set_smem(k_t2_cols<M, RB, R>, smem);
     dim3 grid(M / rpc, B);
-    k_t2_cols<M, R><<<grid, rpc * S::T, smem, st>>>(d, rpc, skip);
+    k_t2_cols<M, RB, R><<<grid, rpc * S::T, smem, st>>>(d, rpc, skip);
     note_launch();
   });
 }
@@ -571,10 +590,20 @@ void launch_w(const OpDev<R>& d, int B, const cplx<R>* grid, cplx<R>* samples, c
   const int threads = 256;
   const int blocks = (d.Ppad + threads - 1) / threads;
   if (d.w_sep) {
-    if (B >= 2)
-      k_w_sep<2, R><<<blocks, threads, 0, st>>>(d, B, grid, samples, skip);
+    // compile-time window bound: registers scale with it (6/7 are the configs' windows)
+    auto go = [&](auto WC) {
+      constexpr int WM = decltype(WC)::value;
+      if (B >= 2)
+        k_w_sep<2, WM, R><<<blocks, threads, 0, st>>>(d, B, grid, samples, skip);
+      else
+        k_w_sep<1, WM, R><<<blocks, threads, 0, st>>>(d, B, grid, samples, skip);
+    };
+    if (d.w <= 6)
+      go(std::integral_constant<int, 6>{});
+    else if (d.w <= 8)
+      go(std::integral_constant<int, 8>{});
     else
-      k_w_sep<1, R><<<blocks, threads, 0, st>>>(d, B, grid, samples, skip);
+      go(std::integral_constant<int, 16>{});
   } else if (B >= 4) {
     k_w<4, R><<<blocks, threads, 0, st>>>(d, B, grid, samples, skip);
   } else if (B >= 2) {
@@ -604,30 +633,30 @@ void launch_wt_rows(const OpDev<R>& d, int B, const SliceScalars* skip, cudaStre
 
 template <typename R>
 void launch_t1_cols_only(const OpDev<R>& d, int B, const SliceScalars* skip, cudaStream_t st) {
-  dispatch_m(d.m, [&](auto MC) {
-    constexpr int M = decltype(MC)::value;
-    using S = FftShape<M>;
-    const int rpc = choose_rpc(M, M, B, sizeof(cplx<R>), true);
+  dispatch_m_rb(d.m, choose_rb(d.m, static_cast<int64_t>(d.m) * B, sizeof(cplx<R>)), [&](auto MC, auto RC) {
+    constexpr int M = decltype(MC)::value, RB = decltype(RC)::value;
+    using S = FftShape<M, RB>;
+    const int rpc = choose_rpc(S::T, M, M, B, sizeof(cplx<R>), true);
     const size_t smem = static_cast<size_t>(rpc) * S::STRIDE * sizeof(cplx<R>);
-    set_smem(k_t1_cols<M, R>, smem);
+    set_smem(k_t1_cols<M, RB, R>, smem);
     dim3 grid(M / rpc, B);
-    k_t1_cols<M, R><<<grid, rpc * S::T, smem, st>>>(d, rpc, skip);
+    k_t1_cols<M, RB, R><<<grid, rpc * S::T, smem, st>>>(d, rpc, skip);
     note_launch();
   });
 }
 
 template <typename R>
 void launch_t1_rows(const OpDev<R>& d, int B, const PbEpi<R>& e, cudaStream_t st) {
-  dispatch_m(d.m, [&](auto MC) {
-    constexpr int M = decltype(MC)::value;
-    using S = FftShape<M>;
-    int rpc = choose_rpc(M, d.n, B, sizeof(cplx<R>), false);
+  dispatch_m_rb(d.m, choose_rb(d.m, static_cast<int64_t>(d.n) * B, sizeof(cplx<R>)), [&](auto MC, auto RC) {
+    constexpr int M = decltype(MC)::value, RB = decltype(RC)::value;
+    using S = FftShape<M, RB>;
+    int rpc = choose_rpc(S::T, M, d.n, B, sizeof(cplx<R>), false);
     while ((rpc * S::T) % 32) rpc <<= 1;  // whole warps for the block reduction
     while (rpc > 1 && (d.n + rpc - 1) / rpc > MAX_PART_BLOCKS) rpc <<= 1;
     const size_t smem = static_cast<size_t>(rpc) * S::STRIDE * sizeof(cplx<R>);
-    set_smem(k_t1_rows<M, R>, smem);
+    set_smem(k_t1_rows<M, RB, R>, smem);
     dim3 grid((d.n + rpc - 1) / rpc, B);
-    k_t1_rows<M, R><<<grid, rpc * S::T, smem, st>>>(d, e, rpc);
+    k_t1_rows<M, RB, R><<<grid, rpc * S::T, smem, st>>>(d, e, rpc);
     note_launch();
   });
 }
@@ -649,12 +678,12 @@ void launch_weight_samples(cplx<R>* s, int B, int P, int nb, cudaStream_t st) {
 template <typename R>
 void launch_fft_rows_test(int m, int rows, const cplx<R>* tw, const cplx<R>* in, cplx<R>* out, bool inverse,
                           cudaStream_t st) {
-  dispatch_m(m, [&](auto MC) {
-    constexpr int M = decltype(MC)::value;
-    using S = FftShape<M>;
+  dispatch_m_rb(m, choose_rb(m, rows, sizeof(cplx<R>)), [&](auto MC, auto RC) {
+    constexpr int M = decltype(MC)::value, RB = decltype(RC)::value;
+    using S = FftShape<M, RB>;
     const size_t smem = S::STRIDE * sizeof(cplx<R>);
-    set_smem(k_fft_rows_test<M, R>, smem);
-    k_fft_rows_test<M, R><<<rows, S::T, smem, st>>>(tw, in, out, rows, inverse ? 1 : 0);
+    set_smem(k_fft_rows_test<M, RB, R>, smem);
+    k_fft_rows_test<M, RB, R><<<rows, S::T, smem, st>>>(tw, in, out, rows, inverse ? 1 : 0);
     note_launch();
   });
 }
