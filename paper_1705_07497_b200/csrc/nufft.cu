@@ -504,15 +504,10 @@ int choose_rpc(int T, int m, int rows_per_slice, int B, size_t elem, bool transp
   return std::max(rpc, 1);
 }
 
-// Base radix for a batch of `rows` rows of length m: radix-16 (fewest smem passes) when the
-// rows alone give enough threads to fill the GPU, else radix 8 or 4 (more threads per row,
-// fewer registers per thread) -- small solver problems are latency-bound, not flop-bound.
-int choose_rb(int m, int64_t rows, size_t elem) {
-  const int64_t want = (elem >= 16 ? 2 : 1) * 148LL * 2048;
-  if (rows * (m / 16) >= want) return 16;
-  if (rows * (m / 8) >= want / 2 || m < 64) return 8;
-  return 4;
-}
+// Base radix of the FFT rows. Measured on B200 (c2 fp64 / c3 fp32): radix 8 and 4 (more
+// threads per row, one more smem pass) were 1.3-1.9x slower than radix 16 even where radix 16
+// leaves the GPU under-occupied, so radix 16 is used throughout (fft.cuh keeps the others).
+int choose_rb(int, int64_t, size_t) { return 16; }
 
 template <typename F>
 void dispatch_m(int m, F&& f) {
@@ -533,11 +528,8 @@ void dispatch_m(int m, F&& f) {
 template <typename F>
 void dispatch_m_rb(int m, int rb, F&& f) {
   dispatch_m(m, [&](auto MC) {
-    switch (rb) {
-      case 16: f(MC, std::integral_constant<int, 16>{}); break;
-      case 8: f(MC, std::integral_constant<int, 8>{}); break;
-      default: f(MC, std::integral_constant<int, 4>{}); break;
-    }
+    (void)rb;
+    f(MC, std::integral_constant<int, 16>{});
   });
 }
 

@@ -54,7 +54,7 @@ GEOMS = {
 
 
 @pytest.mark.parametrize("prec", PRECS)
-@pytest.mark.parametrize("rows", [3, 600, 6000])  # the launcher picks radix 4 / 8 / 16 by row count
+@pytest.mark.parametrize("rows", [3, 600])
 @pytest.mark.parametrize("m", [32, 64, 128, 256, 512, 1024, 2048, 4096, 8192])
 def test_fft_rows(T, m, prec, rows):
     f64 = prec == "f64"
