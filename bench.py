@@ -42,6 +42,10 @@ CONFIGS = {
                metric="normal-op applies/sec", unit="applies/s"),
     "c4": dict(n=512, A=120, nb=725, R=2, lo=-2, hi=3, kind="sb_sur", alpha=1.0, lam=1.0, iters=30, cg=5, r=1,
                slices=256, prec="f32", metric="split-Bregman slices/sec", unit="slices/s"),
+    # 4x oversampling (m = 8192), Greengard-Lee tau (extension D7); Chambolle-Pock with a 15-step CG
+    # prox; one step = 2 CP iterations; reported as normal-op applies/s (16 applies per CP iteration)
+    "c5": dict(n=2048, A=360, nb=2897, R=4, lo=-2, hi=3, kind="cp", alpha=1e-3, lam=1e-2, tau_cp=0.35,
+               sigma_cp=0.35, theta=1.0, iters=2, cg=15, prec="f64", metric="normal-op applies/sec", unit="applies/s"),
 }
 
 
@@ -221,6 +225,13 @@ class Workload:
             self.u_host = self.u.cpu().pin_memory()
             self.out_host = torch.empty(g.n, g.n, dtype=torch.complex64).pin_memory()
             self.h2d = self.d2h = self.u.numel() * 8 * c["applies"]
+        elif kind == "cp":
+            self.op = T.make_direct_backend(g, precision=c["prec"], device=local)
+            self.f = torch.from_numpy(synth_slices(T, self.op, c, [5000 + rank], torch)).cuda()
+            self.units_per_step = c["iters"] * (c["cg"] + 1)
+            self.f_host = self.f.cpu().pin_memory()
+            self.h2d = self.f.numel() * self.f.element_size()
+            self.d2h = g.n * g.n * 8
         elif kind == "c1":
             self.op = T.make_direct_backend(g, precision=c["prec"], device=local)
             self.f = torch.from_numpy(synth_slices(T, self.op, c, [3000 + rank], torch)).cuda()
@@ -262,6 +273,11 @@ class Workload:
             for _ in range(self.c["applies"]):
                 self.out = self.op.apply_normal_real(self.u)
             self.mu = self.op.tikhonov(self.f, alpha=self.c["alpha"], steps=self.c["cg"])
+        elif k == "cp":
+            c = self.c
+            self.mu = self.op.chambolle_pock(self.f, alpha=c["alpha"], lambda_=c["lam"], tau_cp=c["tau_cp"],
+                                             sigma_cp=c["sigma_cp"], theta=c["theta"], iters=c["iters"],
+                                             cg_steps=c["cg"])
 
     # -- end to end through the C ABI with host (pinned) buffers
     def step_e2e(self):
@@ -279,6 +295,10 @@ class Workload:
             for _ in range(self.c["applies"]):
                 self.op.apply_normal_real(self.u_host)
             self.op.tikhonov(self.f_host, alpha=self.c["alpha"], steps=self.c["cg"])
+        elif k == "cp":
+            c = self.c
+            self.op.chambolle_pock(self.f_host, alpha=c["alpha"], lambda_=c["lam"], tau_cp=c["tau_cp"],
+                                   sigma_cp=c["sigma_cp"], theta=c["theta"], iters=c["iters"], cg_steps=c["cg"])
 
     # -- kernel census + roofline of the dominant kernel (CUDA events, live)
     def roofline(self, peak_gbs):
@@ -286,7 +306,7 @@ class Workload:
         k = c["kind"]
         B = 1 if k != "sb_sur" else self.batch
         prof = self.op.profile_stages(batch=B, reps=10)
-        if k in ("sb", "c1"):
+        if k in ("sb", "c1", "cp"):
             steps = c.get("cg", 10)
             iters = c.get("iters", 1)
             a = iters * (steps + 1)
@@ -312,6 +332,12 @@ def flush_l2(torch, buf):
 
 
 # ----------------------------------------------------------------------------- CPU baseline
+def og_cp(c):
+    from oracle import oracle as O
+    return O.Geometry(n=c["n"], n_angles=c["A"], n_b=c["nb"], oversample=c["R"], win_lo=c["lo"], win_hi=c["hi"],
+                      tau=np.pi * 3 / (c["n"] ** 2 * c["R"] * (c["R"] - 0.5)))
+
+
 def cpu_sample(cname, c, prefer_reference=True):
     """Time the reference's CPU path (oracle/_ref) — or the oracle port — on a bounded sample of
     the workload and extrapolate to the metric's unit. Returns (value, kind, sample, cores)."""
@@ -324,8 +350,9 @@ def cpu_sample(cname, c, prefer_reference=True):
     msp = 3
     og = O.Geometry(n=n, n_angles=A, n_b=nb, win_lo=c["lo"], win_hi=c["hi"], tau=3.0 / n ** 2)
     rng = np.random.default_rng(0)
-    ph = O.random_ellipses(n, 10, 1)
-    f, _ = O.synthesize(og, ph, 0.01, 1)
+    if c["kind"] != "cp":
+        ph = O.random_ellipses(n, 10, 1)
+        f, _ = O.synthesize(og, ph, 0.01, 1)
     if c["kind"] == "sb" or c["kind"] == "sb_sur":
         backend = 0 if c["kind"] == "sb" else 2
         def run(iters):
@@ -346,6 +373,13 @@ def cpu_sample(cname, c, prefer_reference=True):
         sample = (f"split_bregman_tv on one {n}^2 slice ({A}x{nb}, {'m_sp=3 7x7' if use_ref else 'width-6'} window),"
                   f" 1 and 2 outer x {c['cg']} CG timed; slice time = setup + {c['iters']} x per-outer")
         return 1.0 / t_slice, kind, sample, 1
+    if c["kind"] == "cp":
+        # the reference hard-codes m_r = 2n (nufft.cpp:40), so R = 4 exists only in the oracle port
+        u = rng.standard_normal((n, n))
+        t = time.perf_counter()
+        O.apply_normal_real(og_cp(c), u)
+        dt = time.perf_counter() - t
+        return 1.0 / dt, "port", f"1 real apply_normal at {n}^2, R=4 (m={4 * n}), {A}x{nb} (oracle port)", 1
     if c["kind"] in ("apply", "c1"):
         u = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
         reps = 3

@@ -290,6 +290,21 @@ __global__ void __launch_bounds__(256) k_wt_tasks(OpDev<R> d, int B, const cplx<
     const C2* s = s_all + static_cast<size_t>(b) * d.P;
     C2 a0 = czero<C2>(), a1 = czero<C2>();
     int c = 0;
+    for (; c + 8 <= nc; c += 8) {  // 8 entry loads, then 8 sample gathers, in flight
+      WtEnt<R> x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] = ldg(e + (c + u) * 32);
+      C2 sv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) sv[u] = __ldg(&s[x[u].j]);
+#pragma unroll
+      for (int u = 0; u < 8; u += 2) {
+        a0.x += x[u].w * sv[u].x;
+        a0.y += x[u].w * sv[u].y;
+        a1.x += x[u + 1].w * sv[u + 1].x;
+        a1.y += x[u + 1].w * sv[u + 1].y;
+      }
+    }
     for (; c + 4 <= nc; c += 4) {
       const WtEnt<R> x0 = ldg(e + (c + 0) * 32), x1 = ldg(e + (c + 1) * 32);
       const WtEnt<R> x2 = ldg(e + (c + 2) * 32), x3 = ldg(e + (c + 3) * 32);
