@@ -196,6 +196,43 @@ TOMO_DEV void fft_pass(C2* row, const C2* __restrict__ tw, int Ns, int t, bool a
   if (!LAST || STORE_SMEM_LAST) __syncthreads();
 }
 
+// Forward FFT whose first-pass inputs were loaded earlier into registers: pre[r] holds the
+// element at position t + r*M/RB (what load(t + r*M/RB) would return). Lets a persistent
+// kernel prefetch the next row while the current one is transformed.
+template <int M, int RB, bool STORE_SMEM, typename C2, typename Store>
+TOMO_DEV void fft_row_pre(C2* row, const C2* __restrict__ tw, int t, bool active, const C2 (&pre)[RB],
+                          Store&& store) {
+  using S = FftShape<M, RB>;
+  static_assert(S::T * RB == M, "one first-pass butterfly per thread");
+  if (active) {
+    C2 v[RB];
+#pragma unroll
+    for (int r = 0; r < RB; ++r) v[r] = pre[r];
+    Dft<RB, C2>::run(v);
+#pragma unroll
+    for (int r = 0; r < RB; ++r) row[pad16(t * RB + r)] = v[r];  // Stockham output of the Ns = 1 pass
+  }
+  __syncthreads();
+  auto noload = [](int) { return C2{}; };
+  if constexpr (S::RL > 1) {
+    int Ns = RB;
+#pragma unroll
+    for (int p = 1; p < S::NB; ++p) {
+      fft_pass<M, RB, RB, false, false, false, C2>(row, tw, Ns, t, active, noload, store);
+      Ns *= RB;
+    }
+    fft_pass<M, RB, S::RL, false, true, STORE_SMEM, C2>(row, tw, Ns, t, active, noload, store);
+  } else {
+    int Ns = RB;
+#pragma unroll
+    for (int p = 1; p < S::NB - 1; ++p) {
+      fft_pass<M, RB, RB, false, false, false, C2>(row, tw, Ns, t, active, noload, store);
+      Ns *= RB;
+    }
+    fft_pass<M, RB, RB, false, true, STORE_SMEM, C2>(row, tw, Ns, t, active, noload, store);
+  }
+}
+
 // Forward FFT of one row per thread group: load(i) -> ... -> store(k, X[k]).
 template <int M, int RB, bool STORE_SMEM, typename C2, typename Load, typename Store>
 TOMO_DEV void fft_row(C2* row, const C2* __restrict__ tw, int t, bool active, Load&& load, Store&& store) {

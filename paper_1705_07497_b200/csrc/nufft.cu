@@ -21,6 +21,8 @@
 #include "fft.cuh"
 #include "kernels.h"
 
+#include <cuda_pipeline.h>
+
 namespace tomo_b200 {
 
 namespace {
@@ -30,6 +32,7 @@ __device__ __forceinline__ int bin_of(int t, int n, int M) { return (t - n / 2 +
 // FFT-row kernels: at most 512 threads per CTA so ptxas may give each thread up to 128
 // registers (a radix-16 fp64 butterfly holds 64 registers of data alone).
 constexpr int kFftThreads = 512;
+constexpr size_t kMaxSmem = 220 * 1024;  // dynamic smem a persistent FFT CTA may use
 
 // beta for the fused CG p-update (solver.cpp:84): rr[k] / rr[k-1]; returns false when the
 // slice's CG is finished (done flag or rs == 0, solver.cpp:70).
@@ -290,22 +293,7 @@ __global__ void __launch_bounds__(256) k_wt_tasks(OpDev<R> d, int B, const cplx<
     const C2* s = s_all + static_cast<size_t>(b) * d.P;
     C2 a0 = czero<C2>(), a1 = czero<C2>();
     int c = 0;
-    for (; c + 8 <= nc; c += 8) {  // 8 entry loads, then 8 sample gathers, in flight
-      WtEnt<R> x[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) x[u] = ldg(e + (c + u) * 32);
-      C2 sv[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) sv[u] = __ldg(&s[x[u].j]);
-#pragma unroll
-      for (int u = 0; u < 8; u += 2) {
-        a0.x += x[u].w * sv[u].x;
-        a0.y += x[u].w * sv[u].y;
-        a1.x += x[u + 1].w * sv[u + 1].x;
-        a1.y += x[u + 1].w * sv[u + 1].y;
-      }
-    }
-    for (; c + 4 <= nc; c += 4) {
+    for (; c + 4 <= nc; c += 4) {  // (an 8-deep variant measured slower: occupancy)
       const WtEnt<R> x0 = ldg(e + (c + 0) * 32), x1 = ldg(e + (c + 1) * 32);
       const WtEnt<R> x2 = ldg(e + (c + 2) * 32), x3 = ldg(e + (c + 3) * 32);
       const C2 s0 = __ldg(&s[x0.j]), s1 = __ldg(&s[x1.j]), s2 = __ldg(&s[x2.j]), s3 = __ldg(&s[x3.j]);
@@ -482,6 +470,190 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? 2 : 1) k_t1_rows
   }
 }
 
+// ================================================================ persistent FFT-row kernels
+// Grid (CTAs per slice, B). Each CTA walks its slice's rows g = blockIdx.x, blockIdx.x +
+// gridDim.x, ... (rpc rows per step). The next step's input rows are copied global -> smem
+// with cp.async (LDGSTS) right after the current step's first pass has consumed the staging
+// buffer, so the copy overlaps the remaining FFT passes and the stores (one staging buffer,
+// no extra registers).
+
+template <typename C2>
+TOMO_DEV void async_copy(C2* dst_smem, const C2* src) {
+  __pipeline_memcpy_async(dst_smem, src, sizeof(C2));
+}
+
+// P2: inverse FFT along ix of H rows (t1 at the n bins), natural store g[iy][ix].
+template <int M, int RB, typename R>
+__global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? 2 : 1)
+k_t2_cols_p(OpDev<R> d, const SliceScalars* skip) {
+  using S = FftShape<M, RB>;
+  using C2 = cplx<R>;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  C2* row = reinterpret_cast<C2*>(smraw);
+  C2* stage = row + S::STRIDE;  // n entries (compact t1)
+  const int b = blockIdx.y;
+  if (skip && (skip[b].done || skip[b].frozen)) return;  // CTA-uniform
+  const int n = d.n, t = threadIdx.x;
+  const C2* Hb = d.H + static_cast<size_t>(b) * M * n;
+  C2* gb = d.g + static_cast<size_t>(b) * M * M;
+  auto issue = [&](int iy) {
+    const C2* H = Hb + static_cast<size_t>(iy) * n;
+    for (int k = t; k < n; k += S::T) async_copy(&stage[k], &H[k]);
+  };
+  int iy = blockIdx.x;
+  if (iy < M) issue(iy);
+  __pipeline_commit();
+  for (; iy < M; iy += gridDim.x) {
+    __pipeline_wait_prior(0);
+    __syncthreads();
+    C2 pre[RB];
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      const int t1 = (t + r * S::T + n / 2) & (M - 1);
+      pre[r] = t1 < n ? cconj(stage[t1]) : czero<C2>();
+    }
+    __syncthreads();  // staging consumed by every thread
+    if (iy + static_cast<int>(gridDim.x) < M) issue(iy + gridDim.x);
+    __pipeline_commit();
+    C2* gout = gb + static_cast<size_t>(iy) * M;
+    fft_row_pre<M, RB, false, C2>(row, d.tw, t, true, pre, [&](int k, C2 v) { gout[k] = cconj(v); });
+  }
+  __pipeline_wait_prior(0);
+}
+
+// PA: forward FFT of rpc spread-grid rows, pruned to the n bins, transposed store K[t1][iy].
+template <int M, int RB, typename R>
+__global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? 2 : 1)
+k_t1_cols_p(OpDev<R> d, int rpc, const SliceScalars* skip) {
+  using S = FftShape<M, RB>;
+  using C2 = cplx<R>;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  C2* sm = reinterpret_cast<C2*>(smraw);
+  C2* stage = sm + static_cast<size_t>(rpc) * S::STRIDE;  // rpc x M
+  const int b = blockIdx.y;
+  if (skip && (skip[b].done || skip[b].frozen)) return;
+  const int n = d.n;
+  const int rr = threadIdx.x / S::T, t = threadIdx.x % S::T;
+  C2* row = sm + rr * S::STRIDE;
+  const int steps = M / rpc;
+  const C2* Gb = d.Gt + static_cast<size_t>(b) * M * M;
+  C2* K = d.K + static_cast<size_t>(b) * n * M;
+  auto issue = [&](int st) {
+    const C2* Gr = Gb + static_cast<size_t>(st) * rpc * M;  // rpc consecutive rows
+    for (int k = threadIdx.x; k < rpc * M; k += blockDim.x) async_copy(&stage[k], &Gr[k]);
+  };
+  int st = blockIdx.x;
+  if (st < steps) issue(st);
+  __pipeline_commit();
+  for (; st < steps; st += gridDim.x) {
+    __pipeline_wait_prior(0);
+    __syncthreads();
+    C2 pre[RB];
+#pragma unroll
+    for (int r = 0; r < RB; ++r) pre[r] = stage[rr * M + t + r * S::T];
+    __syncthreads();
+    if (st + static_cast<int>(gridDim.x) < steps) issue(st + gridDim.x);
+    __pipeline_commit();
+    const int iy0 = st * rpc;
+    fft_row_pre<M, RB, true, C2>(row, d.tw, t, true, pre, [&](int k, C2 v) {
+      const int t1 = (k + n / 2) & (M - 1);  // inverse of bin_of
+      if (t1 < n) row[pad16(t1)] = v;
+    });
+    for (int idx = threadIdx.x; idx < n * rpc; idx += blockDim.x) {
+      const int t1 = idx / rpc, q = idx - t1 * rpc;
+      K[static_cast<size_t>(t1) * M + iy0 + q] = sm[q * S::STRIDE + pad16(t1)];
+    }
+  }
+  __pipeline_wait_prior(0);
+}
+
+// PB: forward FFT along iy of K rows, crop + deapodise + epilogue (as k_t1_rows); the CG dots
+// are accumulated over all rows of the CTA and reduced once per CTA.
+template <int M, int RB, typename R>
+__global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? 2 : 1)
+k_t1_rows_p(OpDev<R> d, PbEpi<R> e) {
+  using S = FftShape<M, RB>;
+  using C2 = cplx<R>;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  C2* row = reinterpret_cast<C2*>(smraw);
+  C2* stage = row + S::STRIDE;  // M entries
+  __shared__ double red_scratch[32];
+  const int b = blockIdx.y;
+  if (e.mode == PB_CG_STEP && (e.red.sc[b].done || e.red.sc[b].frozen)) return;
+  if (e.mode == PB_CG_INIT && e.red.sc[b].frozen) return;
+  const int n = d.n, t = threadIdx.x;
+  const C2* Kb = d.K + static_cast<size_t>(b) * n * M;
+  auto issue = [&](int t1) {
+    const C2* Kr = Kb + static_cast<size_t>(t1) * M;
+    for (int k = t; k < M; k += S::T) async_copy(&stage[k], &Kr[k]);
+  };
+  const R lam = static_cast<R>(e.sys.lambda), shift = static_cast<R>(e.sys.shift);
+  const R* p = e.p ? e.p + static_cast<size_t>(b) * n * n : nullptr;
+  double acc0 = 0.0, acc1 = 0.0;
+  int t1 = blockIdx.x;
+  if (t1 < n) issue(t1);
+  __pipeline_commit();
+  for (; t1 < n; t1 += gridDim.x) {
+    __pipeline_wait_prior(0);
+    __syncthreads();
+    C2 pre[RB];
+#pragma unroll
+    for (int r = 0; r < RB; ++r) pre[r] = stage[t + r * S::T];
+    __syncthreads();
+    if (t1 + static_cast<int>(gridDim.x) < n) issue(t1 + gridDim.x);
+    __pipeline_commit();
+    const R a1 = d.apod[t1] * e.scale;
+    const size_t base = (static_cast<size_t>(b) * n + t1) * n;
+    fft_row_pre<M, RB, false, C2>(row, d.tw, t, true, pre, [&](int k, C2 X) {
+      const int t2 = (k + n / 2) & (M - 1);
+      if (t2 >= n) return;
+      const R sc = a1 * __ldg(&d.apod[t2]);
+      const size_t o = base + t2;
+      if (e.mode == PB_COMPLEX) {
+        e.out_c[o] = cscale(X, sc);
+      } else if (e.mode == PB_REAL) {
+        e.out_r[o] = X.x * sc;
+      } else {
+        const R pv = p[static_cast<size_t>(t1) * n + t2];
+        R ax = X.x * sc;
+        if (lam != R(0)) ax += lam * ktk_at<R>(p, n, t1, t2, pv);
+        ax += shift * pv;
+        if (e.mode == PB_CG_STEP) {
+          e.ap[o] = ax;
+          acc0 += static_cast<double>(pv) * ax;
+          acc1 += static_cast<double>(pv) * pv;
+        } else {  // PB_CG_INIT: r = b - A x0, p = r, x = x0
+          const R bv = e.b[o];
+          const R rv = bv - ax;
+          e.ap[o] = rv;
+          e.p_out[o] = rv;
+          e.x_out[o] = pv;
+          acc0 += static_cast<double>(rv) * rv;
+          acc1 += static_cast<double>(bv) * bv;
+        }
+      }
+    });
+  }
+  __pipeline_wait_prior(0);
+  if (e.mode < PB_CG_STEP) return;
+  double t0s, t1s;
+  SliceScalars& sc = e.red.sc[b];
+  double* part = e.red.part + static_cast<size_t>(b) * MAX_PART_BLOCKS * 2;
+  if (reduce2_last(acc0, acc1, part, gridDim.x, blockIdx.x, &sc.counter[0], red_scratch, t0s, t1s) &&
+      threadIdx.x == 0) {
+    if (e.mode == PB_CG_STEP) {
+      sc.pap = t0s;
+      sc.pp = t1s;
+    } else {
+      sc.rr[0] = t0s;
+      sc.bb = t1s;
+      sc.done = 0;
+      sc.steps_run = 0;
+      sc.min_ritz = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+    }
+  }
+}
+
 // Radial density weights |k_r| (DC: 1/4), normal_ops.cpp:208-219, applied to samples.
 template <typename R>
 __global__ void k_weight_samples(cplx<R>* s, int B, int P, int nb) {
@@ -577,16 +749,38 @@ void launch_t2_rows(const OpDev<R>& d, int B, const void* in, bool in_complex, c
   });
 }
 
+template <typename K>
+int persistent_ctas(K kernel, int threads, size_t smem, int rows_per_slice, int B) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> occ_cache;
+  int occ = 0;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = occ_cache.find(reinterpret_cast<const void*>(kernel));
+    if (it != occ_cache.end()) {
+      occ = it->second;
+    } else {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem);
+      occ_cache[reinterpret_cast<const void*>(kernel)] = occ;
+    }
+  }
+  int sms = 148;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t slots = static_cast<int64_t>(std::max(occ, 1)) * sms;
+  const int64_t per_slice = std::max<int64_t>(1, slots / std::max(B, 1));
+  return static_cast<int>(std::min<int64_t>(rows_per_slice, per_slice));
+}
+
 template <typename R>
 void launch_t2_cols(const OpDev<R>& d, int B, const SliceScalars* skip, cudaStream_t st) {
   dispatch_m_rb(d.m, choose_rb(d.m, static_cast<int64_t>(d.m) * B, sizeof(cplx<R>)), [&](auto MC, auto RC) {
     constexpr int M = decltype(MC)::value, RB = decltype(RC)::value;
     using S = FftShape<M, RB>;
-    const int rpc = choose_rpc(S::T, M, M, B, sizeof(cplx<R>), false);
-    const size_t smem = static_cast<size_t>(rpc) * S::STRIDE * sizeof(cplx<R>);
-    set_smem(k_t2_cols<M, RB, R>, smem);
-    dim3 grid(M / rpc, B);
-    k_t2_cols<M, RB, R><<<grid, rpc * S::T, smem, st>>>(d, rpc, skip);
+    const size_t smem = (static_cast<size_t>(S::STRIDE) + d.n) * sizeof(cplx<R>);
+    set_smem(k_t2_cols_p<M, RB, R>, smem);
+    const int ctas = persistent_ctas(k_t2_cols_p<M, RB, R>, S::T, smem, M, B);
+    k_t2_cols_p<M, RB, R><<<dim3(ctas, B), S::T, smem, st>>>(d, skip);
     note_launch();
   });
 }
@@ -643,11 +837,22 @@ void launch_t1_cols_only(const OpDev<R>& d, int B, const SliceScalars* skip, cud
   dispatch_m_rb(d.m, choose_rb(d.m, static_cast<int64_t>(d.m) * B, sizeof(cplx<R>)), [&](auto MC, auto RC) {
     constexpr int M = decltype(MC)::value, RB = decltype(RC)::value;
     using S = FftShape<M, RB>;
-    const int rpc = choose_rpc(S::T, M, M, B, sizeof(cplx<R>), true);
-    const size_t smem = static_cast<size_t>(rpc) * S::STRIDE * sizeof(cplx<R>);
-    set_smem(k_t1_cols<M, RB, R>, smem);
-    dim3 grid(M / rpc, B);
-    k_t1_cols<M, RB, R><<<grid, rpc * S::T, smem, st>>>(d, rpc, skip);
+    // transposed K stores need >= 32 B per row segment; staging holds rpc full rows
+    int rpc = std::max(1, static_cast<int>(32 / sizeof(cplx<R>)));
+    while (rpc > 1 && (rpc * S::T > kFftThreads ||
+                       static_cast<size_t>(rpc) * (S::STRIDE + M) * sizeof(cplx<R>) > 200 * 1024))
+      rpc >>= 1;
+    const size_t smem = static_cast<size_t>(rpc) * (S::STRIDE + M) * sizeof(cplx<R>);
+    if (smem <= kMaxSmem) {
+      set_smem(k_t1_cols_p<M, RB, R>, smem);
+      const int ctas = persistent_ctas(k_t1_cols_p<M, RB, R>, rpc * S::T, smem, M / rpc, B);
+      k_t1_cols_p<M, RB, R><<<dim3(ctas, B), rpc * S::T, smem, st>>>(d, rpc, skip);
+    } else {  // row + staging do not fit (fp64, m = 8192): one-shot CTAs
+      const int rpc1 = choose_rpc(S::T, M, M, B, sizeof(cplx<R>), true);
+      const size_t smem1 = static_cast<size_t>(rpc1) * S::STRIDE * sizeof(cplx<R>);
+      set_smem(k_t1_cols<M, RB, R>, smem1);
+      k_t1_cols<M, RB, R><<<dim3(M / rpc1, B), rpc1 * S::T, smem1, st>>>(d, rpc1, skip);
+    }
     note_launch();
   });
 }
@@ -657,13 +862,21 @@ void launch_t1_rows(const OpDev<R>& d, int B, const PbEpi<R>& e, cudaStream_t st
   dispatch_m_rb(d.m, choose_rb(d.m, static_cast<int64_t>(d.n) * B, sizeof(cplx<R>)), [&](auto MC, auto RC) {
     constexpr int M = decltype(MC)::value, RB = decltype(RC)::value;
     using S = FftShape<M, RB>;
-    int rpc = choose_rpc(S::T, M, d.n, B, sizeof(cplx<R>), false);
-    while ((rpc * S::T) % 32) rpc <<= 1;  // whole warps for the block reduction
-    while (rpc > 1 && (d.n + rpc - 1) / rpc > MAX_PART_BLOCKS) rpc <<= 1;
-    const size_t smem = static_cast<size_t>(rpc) * S::STRIDE * sizeof(cplx<R>);
-    set_smem(k_t1_rows<M, RB, R>, smem);
-    dim3 grid((d.n + rpc - 1) / rpc, B);
-    k_t1_rows<M, RB, R><<<grid, rpc * S::T, smem, st>>>(d, e, rpc);
+    constexpr size_t smem_p = (static_cast<size_t>(S::STRIDE) + M) * sizeof(cplx<R>);
+    if constexpr (S::T % 32 == 0 && smem_p <= kMaxSmem) {
+      const size_t smem = smem_p;
+      set_smem(k_t1_rows_p<M, RB, R>, smem);
+      const int ctas = std::min(MAX_PART_BLOCKS, persistent_ctas(k_t1_rows_p<M, RB, R>, S::T, smem, d.n, B));
+      k_t1_rows_p<M, RB, R><<<dim3(ctas, B), S::T, smem, st>>>(d, e);
+    } else {  // rows shorter than 512: whole warps need several rows per CTA
+      int rpc = choose_rpc(S::T, M, d.n, B, sizeof(cplx<R>), false);
+      while ((rpc * S::T) % 32) rpc <<= 1;
+      while (rpc > 1 && (d.n + rpc - 1) / rpc > MAX_PART_BLOCKS) rpc <<= 1;
+      const size_t smem = static_cast<size_t>(rpc) * S::STRIDE * sizeof(cplx<R>);
+      set_smem(k_t1_rows<M, RB, R>, smem);
+      dim3 grid((d.n + rpc - 1) / rpc, B);
+      k_t1_rows<M, RB, R><<<grid, rpc * S::T, smem, st>>>(d, e, rpc);
+    }
     note_launch();
   });
 }
