@@ -33,6 +33,9 @@ __device__ __forceinline__ int bin_of(int t, int n, int M) { return (t - n / 2 +
 // registers (a radix-16 fp64 butterfly holds 64 registers of data alone).
 constexpr int kFftThreads = 512;
 constexpr size_t kMaxSmem = 220 * 1024;  // dynamic smem a persistent FFT CTA may use
+// Persistent prefetching FFT-row kernels measured faster only for the longest rows (c5,
+// m = 8192); below that the one-shot kernels (more CTAs in flight) win.
+constexpr int kPersistMinM = 4096;
 
 // beta for the fused CG p-update (solver.cpp:84): rr[k] / rr[k-1]; returns false when the
 // slice's CG is finished (done flag or rs == 0, solver.cpp:70).
@@ -777,10 +780,17 @@ void launch_t2_cols(const OpDev<R>& d, int B, const SliceScalars* skip, cudaStre
   dispatch_m_rb(d.m, choose_rb(d.m, static_cast<int64_t>(d.m) * B, sizeof(cplx<R>)), [&](auto MC, auto RC) {
     constexpr int M = decltype(MC)::value, RB = decltype(RC)::value;
     using S = FftShape<M, RB>;
-    const size_t smem = (static_cast<size_t>(S::STRIDE) + d.n) * sizeof(cplx<R>);
-    set_smem(k_t2_cols_p<M, RB, R>, smem);
-    const int ctas = persistent_ctas(k_t2_cols_p<M, RB, R>, S::T, smem, M, B);
-    k_t2_cols_p<M, RB, R><<<dim3(ctas, B), S::T, smem, st>>>(d, skip);
+    if (M >= kPersistMinM) {
+      const size_t smem = (static_cast<size_t>(S::STRIDE) + d.n) * sizeof(cplx<R>);
+      set_smem(k_t2_cols_p<M, RB, R>, smem);
+      const int ctas = persistent_ctas(k_t2_cols_p<M, RB, R>, S::T, smem, M, B);
+      k_t2_cols_p<M, RB, R><<<dim3(ctas, B), S::T, smem, st>>>(d, skip);
+    } else {
+      const int rpc = choose_rpc(S::T, M, M, B, sizeof(cplx<R>), false);
+      const size_t smem = static_cast<size_t>(rpc) * S::STRIDE * sizeof(cplx<R>);
+      set_smem(k_t2_cols<M, RB, R>, smem);
+      k_t2_cols<M, RB, R><<<dim3(M / rpc, B), rpc * S::T, smem, st>>>(d, rpc, skip);
+    }
     note_launch();
   });
 }
@@ -843,7 +853,7 @@ void launch_t1_cols_only(const OpDev<R>& d, int B, const SliceScalars* skip, cud
                        static_cast<size_t>(rpc) * (S::STRIDE + M) * sizeof(cplx<R>) > 200 * 1024))
       rpc >>= 1;
     const size_t smem = static_cast<size_t>(rpc) * (S::STRIDE + M) * sizeof(cplx<R>);
-    if (smem <= kMaxSmem) {
+    if (smem <= kMaxSmem && M >= kPersistMinM) {
       set_smem(k_t1_cols_p<M, RB, R>, smem);
       const int ctas = persistent_ctas(k_t1_cols_p<M, RB, R>, rpc * S::T, smem, M / rpc, B);
       k_t1_cols_p<M, RB, R><<<dim3(ctas, B), rpc * S::T, smem, st>>>(d, rpc, skip);
@@ -863,7 +873,7 @@ void launch_t1_rows(const OpDev<R>& d, int B, const PbEpi<R>& e, cudaStream_t st
     constexpr int M = decltype(MC)::value, RB = decltype(RC)::value;
     using S = FftShape<M, RB>;
     constexpr size_t smem_p = (static_cast<size_t>(S::STRIDE) + M) * sizeof(cplx<R>);
-    if constexpr (S::T % 32 == 0 && smem_p <= kMaxSmem) {
+    if constexpr (S::T % 32 == 0 && smem_p <= kMaxSmem && M >= kPersistMinM) {
       const size_t smem = smem_p;
       set_smem(k_t1_rows_p<M, RB, R>, smem);
       const int ctas = std::min(MAX_PART_BLOCKS, persistent_ctas(k_t1_rows_p<M, RB, R>, S::T, smem, d.n, B));
