@@ -296,9 +296,23 @@ __global__ void __launch_bounds__(256) k_wt_tasks(OpDev<R> d, int B, const cplx<
     const C2* s = s_all + static_cast<size_t>(b) * d.P;
     C2 a0 = czero<C2>(), a1 = czero<C2>();
     int c = 0;
-    for (; c + 4 <= nc; c += 4) {  // (an 8-deep variant measured slower: occupancy)
-      const WtEnt<R> x0 = ldg(e + (c + 0) * 32), x1 = ldg(e + (c + 1) * 32);
-      const WtEnt<R> x2 = ldg(e + (c + 2) * 32), x3 = ldg(e + (c + 3) * 32);
+    // software-pipelined: the entry loads of group c+4 are in flight while group c's samples
+    // are gathered (an 8-deep unrolled variant measured slower: occupancy)
+    WtEnt<R> n0{}, n1{}, n2{}, n3{};
+    if (nc >= 4) {
+      n0 = ldg(e + 0 * 32);
+      n1 = ldg(e + 1 * 32);
+      n2 = ldg(e + 2 * 32);
+      n3 = ldg(e + 3 * 32);
+    }
+    for (; c + 4 <= nc; c += 4) {
+      const WtEnt<R> x0 = n0, x1 = n1, x2 = n2, x3 = n3;
+      if (c + 8 <= nc) {
+        n0 = ldg(e + (c + 4) * 32);
+        n1 = ldg(e + (c + 5) * 32);
+        n2 = ldg(e + (c + 6) * 32);
+        n3 = ldg(e + (c + 7) * 32);
+      }
       const C2 s0 = __ldg(&s[x0.j]), s1 = __ldg(&s[x1.j]), s2 = __ldg(&s[x2.j]), s3 = __ldg(&s[x3.j]);
       a0.x += x0.w * s0.x + x2.w * s2.x;
       a0.y += x0.w * s0.y + x2.w * s2.y;

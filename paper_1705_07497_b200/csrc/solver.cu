@@ -113,7 +113,10 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_update(int64_t L, const R* _
 
 // ------------------------------------------------------------------ surrogate stencil
 // Tile of 32x32 outputs, 256 threads (32 x 8, 4 rows each). Halo H = max(rad, 1).
-constexpr int kTile = 32;
+// 64x64 outputs per CTA (256 threads = 64 columns x 4, 16 rows each): the halo and the
+// per-CTA dot reduction are amortised over 4096 pixels.
+constexpr int kTile = 64;
+constexpr int kTileRows = 4;  // thread rows
 
 template <int RAD, typename R>
 __global__ void __launch_bounds__(256) k_stencil(int n, StencilCoef coef, int mode, const R* __restrict__ in,
@@ -154,12 +157,12 @@ __global__ void __launch_bounds__(256) k_stencil(int n, StencilCoef coef, int mo
     q[li][lj] = v;
   }
   __syncthreads();
-  const int tj = threadIdx.x & 31, ti = threadIdx.x >> 5;
+  const int tj = threadIdx.x % kTile, ti = threadIdx.x / kTile;
   const R alpha = static_cast<R>(sys.alpha), lam = static_cast<R>(sys.lambda), shift = static_cast<R>(sys.shift);
   double acc0 = 0.0, acc1 = 0.0;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int li = ti + 8 * k + HALO, lj = tj + HALO;
+#pragma unroll 4
+  for (int k = 0; k < kTile / kTileRows; ++k) {
+    const int li = ti + kTileRows * k + HALO, lj = tj + HALO;
     const int gi = i0 + li, gj = j0 + lj;
     if (gi >= n || gj >= n) continue;
     const R c = q[li][lj];

@@ -19,6 +19,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
+#include <tuple>
 #include <memory>
 #include <random>
 #include <stdexcept>
@@ -1496,19 +1498,31 @@ int tomo_fft_rows(int m, int rows, int precision, const void* in, void* out, int
   TOMO_TRY
   if (!is_device_ptr(in) || !is_device_ptr(out)) throw ConfigError("fft_rows: device pointers required");
   if (m < 32 || m > 8192 || (m & (m - 1))) throw ConfigError("fft_rows: m must be a power of two in [32, 8192]");
+  // twiddle tables cached per (device, m, precision): the call is a single kernel launch
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int>, std::unique_ptr<Raw>> tables;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
   auto run = [&](auto tag) {
     using R = decltype(tag);
-    std::vector<cplx<R>> tw(m);
-    for (int k = 0; k < m; ++k) {
-      const double ang = -2.0 * M_PI * k / m;
-      tw[k].x = static_cast<R>(std::cos(ang));
-      tw[k].y = static_cast<R>(std::sin(ang));
+    const cplx<R>* twp = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      auto& slot = tables[std::make_tuple(dev, m, precision)];
+      if (!slot) {
+        std::vector<cplx<R>> tw(m);
+        for (int k = 0; k < m; ++k) {
+          const double ang = -2.0 * M_PI * k / m;
+          tw[k].x = static_cast<R>(std::cos(ang));
+          tw[k].y = static_cast<R>(std::sin(ang));
+        }
+        slot = std::make_unique<Raw>();
+        slot->upload(tw);
+      }
+      twp = slot->as<cplx<R>>();
     }
-    Raw dtw;
-    dtw.upload(tw);
-    launch_fft_rows_test<R>(m, rows, dtw.as<cplx<R>>(), static_cast<const cplx<R>*>(in), static_cast<cplx<R>*>(out),
-                            inverse != 0, S_(stream));
-    CK(cudaStreamSynchronize(S_(stream)));
+    launch_fft_rows_test<R>(m, rows, twp, static_cast<const cplx<R>*>(in), static_cast<cplx<R>*>(out), inverse != 0,
+                            S_(stream));
   };
   if (precision == TOMO_F64)
     run(double{});
