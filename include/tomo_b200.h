@@ -45,6 +45,7 @@ extern "C" {
 
 /* backends — tomo::BackendKind (proj/include/tomo/normal_ops.hpp:10) */
 #define TOMO_BACKEND_DIRECT 0    /* W / W^T sparse interpolation pair (the GPU form of "direct") */
+#define TOMO_BACKEND_FUSED 1     /* Gram W^T W on the oversampled grid (make_fused_backend) */
 #define TOMO_BACKEND_SURROGATE 2 /* truncated translated stencil T */
 
 /* Geometry: SliceGrid + NufftParams (fourier_slice.hpp:24-28, nufft.hpp:16-21) with the
@@ -70,6 +71,8 @@ typedef struct tomo_op_desc {
   int angle_end;
   int max_batch;    /* slices per call the scratch is sized for (>= 1) */
   int precision;    /* TOMO_F32 | TOMO_F64 */
+  int64_t mem_cap_bytes; /* fused backend: refuse Gram builds whose estimate exceeds this
+                          * (build_btb, normal_ops.cpp:81-84); 0 -> kDefaultBtbMemCap = 8 GiB */
 } tomo_op_desc;
 
 typedef struct tomo_op tomo_op;
@@ -85,14 +88,19 @@ typedef struct tomo_op_info {
   double stencil[81];   /* surrogate stencil (2r+1)^2, fp64 host copy */
   int surrogate_r;
   int precision;
+  int backend;
+  int64_t gram_nnz;     /* fused backend: non-zeros of W^T W (= build_btb's CSR nnz) */
+  int64_t gram_slots;   /* fused backend: task-SpMV slots incl. padding */
+  int64_t bytes_gram;   /* fused backend: device bytes of the Gram tables */
 } tomo_op_info;
 
 const char* tomo_last_error(void);
 
-/* make_direct_backend / make_surrogate_backend (normal_ops.hpp:35-39) over a
- * SliceTransform(SliceGrid, NufftParams) (fourier_slice.hpp:39). Builds W (SELL-32 ELL),
- * its transpose, deapodisation and FFT tables on `device`; for the surrogate also the
- * stencil (build_surrogate, normal_ops.hpp:60). */
+/* make_direct_backend / make_fused_backend / make_surrogate_backend (normal_ops.hpp:35-39)
+ * over a SliceTransform(SliceGrid, NufftParams) (fourier_slice.hpp:39). Builds W (SELL-32
+ * ELL), its transpose, deapodisation and FFT tables on `device`; for the fused backend also
+ * the Gram W^T W (build_btb, normal_ops.hpp:47); for the surrogate also the stencil
+ * (build_surrogate, normal_ops.hpp:60). */
 int tomo_op_create(const tomo_geom_desc* geom, const tomo_op_desc* desc, tomo_op** out);
 void tomo_op_destroy(tomo_op* op);
 int tomo_op_get_info(const tomo_op* op, tomo_op_info* info);

@@ -103,7 +103,8 @@ struct SolveTrace {
 // in fp64), W/W^T ("direct") or surrogate stencil.
 class NormalBackend {
  public:
-  NormalBackend(const Geometry& g, int backend, int surrogate_r = 1, int device = 0, int max_batch = 1)
+  NormalBackend(const Geometry& g, int backend, int surrogate_r = 1, int device = 0, int max_batch = 1,
+                int64_t mem_cap_bytes = 0)
       : geom_(g) {
     tomo_geom_desc gd = g.desc();
     tomo_op_desc od{};
@@ -112,6 +113,7 @@ class NormalBackend {
     od.device = device;
     od.max_batch = max_batch;
     od.precision = TOMO_F64;
+    od.mem_cap_bytes = mem_cap_bytes;
     tomo_op* op = nullptr;
     check(tomo_op_create(&gd, &od, &op));
     op_.reset(op);
@@ -132,9 +134,13 @@ class NormalBackend {
   std::unique_ptr<tomo_op, Del> op_;
 };
 
-// make_direct_backend / make_surrogate_backend (normal_ops.hpp:35-39)
+// make_direct_backend / make_fused_backend / make_surrogate_backend (normal_ops.hpp:35-39)
 inline NormalBackend make_direct_backend(const Geometry& g, int device = 0) {
   return NormalBackend(g, TOMO_BACKEND_DIRECT, 1, device);
+}
+inline NormalBackend make_fused_backend(const Geometry& g, int64_t mem_cap_bytes = int64_t(8) << 30,
+                                        int device = 0) {
+  return NormalBackend(g, TOMO_BACKEND_FUSED, 1, device, 1, mem_cap_bytes);
 }
 inline NormalBackend make_surrogate_backend(const Geometry& g, int radius_r = 1, int device = 0) {
   return NormalBackend(g, TOMO_BACKEND_SURROGATE, radius_r, device);

@@ -20,6 +20,7 @@ TOMO_ERR_IO = 4
 TOMO_ERR_CUDA = 5
 
 BACKEND_DIRECT = 0
+BACKEND_FUSED = 1
 BACKEND_SURROGATE = 2
 F32 = 0
 F64 = 1
@@ -35,14 +36,17 @@ class GeomDesc(C.Structure):
 
 class OpDesc(C.Structure):
     _fields_ = [("backend", C.c_int), ("surrogate_r", C.c_int), ("euclidean", C.c_int), ("device", C.c_int),
-                ("angle_begin", C.c_int), ("angle_end", C.c_int), ("max_batch", C.c_int), ("precision", C.c_int)]
+                ("angle_begin", C.c_int), ("angle_end", C.c_int), ("max_batch", C.c_int), ("precision", C.c_int),
+                ("mem_cap_bytes", C.c_int64)]
 
 
 class OpInfo(C.Structure):
     _fields_ = [("n", C.c_int), ("m", C.c_int), ("n_b", C.c_int), ("n_angles_local", C.c_int),
                 ("window", C.c_int), ("P", C.c_int64), ("nnz", C.c_int64), ("wt_rows", C.c_int64),
                 ("wt_slots", C.c_int64), ("bytes_w", C.c_int64), ("bytes_wt", C.c_int64),
-                ("stencil", C.c_double * 81), ("surrogate_r", C.c_int), ("precision", C.c_int)]
+                ("stencil", C.c_double * 81), ("surrogate_r", C.c_int), ("precision", C.c_int),
+                ("backend", C.c_int), ("gram_nnz", C.c_int64), ("gram_slots", C.c_int64),
+                ("bytes_gram", C.c_int64)]
 
 
 class System(C.Structure):

@@ -27,6 +27,22 @@ struct alignas(16) WtEnt<double> {
   double w;
 };
 
+// A sparse operator on the grid's row-sorted 32-node blocks, applied as a balanced list of warp
+// tasks (used for W^T, input = samples, and for the Gram W^T W, input = the grid).
+template <typename R>
+struct TaskSpmv {
+  const WtEnt<R>* ent;      // chunk-major: entry (chunk c, lane l) at [c*32 + l]; .j = input index
+  const int4* tasks;        // {block, chunk0, nchunks, slot (-1: direct)}
+  int n_tasks;
+  const uint16_t* perm;     // [blocks*32] sorted position -> ix of the block's grid row
+  const int4* heavy;        // {block, slot0, nslots, 0}
+  const int* slot_heavy;    // slot -> heavy block index
+  unsigned* heavy_cnt;      // B x n_heavy task tickets (zero between launches)
+  int n_heavy;
+  int n_slots;
+  cplx<R>* part;            // B x n_slots x 32 partial sums of split blocks
+};
+
 // Four W values of one SELL-32 slot quad (16 B fp32 / 32 B fp64).
 template <typename R>
 struct alignas(4 * sizeof(R)) Quad {
@@ -69,6 +85,12 @@ struct OpDev {
   cplx<R>* g;                      // B x m x m  (oversampled spatial grid, [iy][ix])
   cplx<R>* s;                      // B x P      (slice samples)
   cplx<R>* K;                      // B x n x m  (type-1 row pass output, [t1][iy])
+  TaskSpmv<R> gram;                // fused backend: W^T W on the grid (n_tasks == 0 if not built)
+
+  TaskSpmv<R> wt_view() const {
+    return TaskSpmv<R>{wt_ent, wt_tasks, n_tasks, wt_perm, wt_heavy, wt_slot_heavy, wt_heavy_cnt, n_heavy, n_slots,
+                       wt_part};
+  }
 };
 
 constexpr int kWtMaxChunks = 24;
@@ -154,6 +176,10 @@ void launch_wt_spread(const OpDev<R>& d, int B, const cplx<R>* samples, cplx<R>*
                       cudaStream_t st);
 template <typename R>
 void launch_t1_cols_only(const OpDev<R>& d, int B, const SliceScalars* skip, cudaStream_t st);
+// Fused (Gram) backend: grid_out = (W^T W) grid_in on the oversampled grid.
+template <typename R>
+void launch_gram(const OpDev<R>& d, int B, const cplx<R>* grid_in, cplx<R>* grid_out, const SliceScalars* skip,
+                 cudaStream_t st);
 template <typename R>
 void launch_t1_rows(const OpDev<R>& d, int B, const PbEpi<R>& e, cudaStream_t st);
 template <typename R>

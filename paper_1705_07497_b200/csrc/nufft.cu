@@ -273,46 +273,37 @@ __global__ void __launch_bounds__(256) k_w_sep(OpDev<R> d, int B, const cplx<R>*
   }
 }
 
-// ---------------------------------------------------------------- W^T: balanced task SpMV
+// ---------------------------------------------------------------- W^T / Gram: balanced task SpMV
+// The same kernel applies W^T (input = slice samples, stride P) and, for the fused backend, the
+// Gram operator W^T W (input = the grid, stride m^2; grid_in must not alias grid).
 // One warp per task {block, chunk0, nchunks, slot}: lane l accumulates node (block, l) over
 // the task's chunks (coalesced 32-entry chunks, 4 in flight), then writes either the grid node
 // (iy*m + perm) or, for a split block, its partial slot.
 template <typename R>
-__global__ void __launch_bounds__(256) k_wt_tasks(OpDev<R> d, int B, const cplx<R>* __restrict__ s_all,
-                                                   cplx<R>* __restrict__ grid, const SliceScalars* skip) {
+__global__ void __launch_bounds__(256) k_task_spmv(TaskSpmv<R> ts, int m, int B, const cplx<R>* __restrict__ s_all,
+                                                    size_t in_stride, cplx<R>* __restrict__ grid,
+                                                    const SliceScalars* skip) {
   using C2 = cplx<R>;
   const int task = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (task >= d.n_tasks) return;
-  const int4 tk = __ldg(&d.wt_tasks[task]);
+  if (task >= ts.n_tasks) return;
+  const int4 tk = __ldg(&ts.tasks[task]);
   const int blk = tk.x, c0 = tk.y, nc = tk.z, slot = tk.w;
-  const int bpr = d.m / 32;  // blocks per grid row
+  const int bpr = m / 32;  // blocks per grid row
   const int iy = blk / bpr;
-  const int ix = __ldg(&d.wt_perm[static_cast<size_t>(blk) * 32 + lane]);
-  const size_t G = static_cast<size_t>(d.m) * d.m;
-  const WtEnt<R>* e = d.wt_ent + static_cast<size_t>(c0) * 32 + lane;
+  const int ix = __ldg(&ts.perm[static_cast<size_t>(blk) * 32 + lane]);
+  const size_t G = static_cast<size_t>(m) * m;
+  const WtEnt<R>* e = ts.ent + static_cast<size_t>(c0) * 32 + lane;
   for (int b = 0; b < B; ++b) {
     if (skip && (skip[b].done || skip[b].frozen)) continue;
-    const C2* s = s_all + static_cast<size_t>(b) * d.P;
+    const C2* s = s_all + static_cast<size_t>(b) * in_stride;
     C2 a0 = czero<C2>(), a1 = czero<C2>();
     int c = 0;
-    // software-pipelined: the entry loads of group c+4 are in flight while group c's samples
-    // are gathered (an 8-deep unrolled variant measured slower: occupancy)
-    WtEnt<R> n0{}, n1{}, n2{}, n3{};
-    if (nc >= 4) {
-      n0 = ldg(e + 0 * 32);
-      n1 = ldg(e + 1 * 32);
-      n2 = ldg(e + 2 * 32);
-      n3 = ldg(e + 3 * 32);
-    }
+    // four chunks per step (8-deep unrolling and software-pipelined entry loads were both
+    // measured slower on B200: occupancy)
     for (; c + 4 <= nc; c += 4) {
-      const WtEnt<R> x0 = n0, x1 = n1, x2 = n2, x3 = n3;
-      if (c + 8 <= nc) {
-        n0 = ldg(e + (c + 4) * 32);
-        n1 = ldg(e + (c + 5) * 32);
-        n2 = ldg(e + (c + 6) * 32);
-        n3 = ldg(e + (c + 7) * 32);
-      }
+      const WtEnt<R> x0 = ldg(e + (c + 0) * 32), x1 = ldg(e + (c + 1) * 32);
+      const WtEnt<R> x2 = ldg(e + (c + 2) * 32), x3 = ldg(e + (c + 3) * 32);
       const C2 s0 = __ldg(&s[x0.j]), s1 = __ldg(&s[x1.j]), s2 = __ldg(&s[x2.j]), s3 = __ldg(&s[x3.j]);
       a0.x += x0.w * s0.x + x2.w * s2.x;
       a0.y += x0.w * s0.y + x2.w * s2.y;
@@ -327,47 +318,27 @@ __global__ void __launch_bounds__(256) k_wt_tasks(OpDev<R> d, int B, const cplx<
     }
     const C2 v = cadd(a0, a1);
     if (slot < 0) {
-      grid[G * b + static_cast<size_t>(iy) * d.m + ix] = v;
+      grid[G * b + static_cast<size_t>(iy) * m + ix] = v;
     } else {
       // split block: publish the partial; the warp that finishes the block's last task sums
       // all of its partials in slot order (deterministic) and writes the node values
-      C2* part = d.wt_part + static_cast<size_t>(b) * d.n_slots * 32;
+      C2* part = ts.part + static_cast<size_t>(b) * ts.n_slots * 32;
       part[static_cast<size_t>(slot) * 32 + lane] = v;
       __threadfence();
-      const int h = __ldg(&d.wt_slot_heavy[slot]);
-      unsigned* cnt = d.wt_heavy_cnt + static_cast<size_t>(b) * d.n_heavy + h;
+      const int h = __ldg(&ts.slot_heavy[slot]);
+      unsigned* cnt = ts.heavy_cnt + static_cast<size_t>(b) * ts.n_heavy + h;
       unsigned ticket = 0;
       if (lane == 0) ticket = atomicAdd(cnt, 1u);
       ticket = __shfl_sync(0xffffffffu, ticket, 0);
-      const int4 hv = __ldg(&d.wt_heavy[h]);
+      const int4 hv = __ldg(&ts.heavy[h]);
       if (ticket == static_cast<unsigned>(hv.z - 1)) {
         __threadfence();
         C2 acc = czero<C2>();
         for (int k = 0; k < hv.z; ++k) acc = cadd(acc, __ldcg(&part[static_cast<size_t>(hv.y + k) * 32 + lane]));
-        grid[G * b + static_cast<size_t>(iy) * d.m + ix] = acc;
+        grid[G * b + static_cast<size_t>(iy) * m + ix] = acc;
         if (lane == 0) *cnt = 0u;
       }
     }
-  }
-}
-
-// Split blocks: node value = sum of the block's partial slots in fixed order.
-template <typename R>
-__global__ void k_wt_fixup(OpDev<R> d, int B, cplx<R>* __restrict__ grid, const SliceScalars* skip) {
-  using C2 = cplx<R>;
-  const int h = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (h >= d.n_heavy) return;
-  const int4 hv = __ldg(&d.wt_heavy[h]);
-  const int blk = hv.x, slot0 = hv.y, ns = hv.z;
-  const int iy = blk / (d.m / 32);
-  const int ix = __ldg(&d.wt_perm[static_cast<size_t>(blk) * 32 + lane]);
-  const size_t G = static_cast<size_t>(d.m) * d.m;
-  for (int b = 0; b < B; ++b) {
-    if (skip && (skip[b].done || skip[b].frozen)) continue;
-    C2 acc = czero<C2>();
-    for (int k = 0; k < ns; ++k) acc = cadd(acc, d.wt_part[(static_cast<size_t>(b) * d.n_slots + slot0 + k) * 32 + lane]);
-    grid[G * b + static_cast<size_t>(iy) * d.m + ix] = acc;
   }
 }
 
@@ -843,9 +814,22 @@ template <typename R>
 void launch_wt_spread(const OpDev<R>& d, int B, const cplx<R>* samples, cplx<R>* grid, const SliceScalars* skip,
                       cudaStream_t st) {
   const int threads = 256;
-  if (d.n_tasks > 0) {
-    const int blocks = (d.n_tasks * 32 + threads - 1) / threads;
-    k_wt_tasks<R><<<blocks, threads, 0, st>>>(d, B, samples, grid, skip);
+  const TaskSpmv<R> ts = d.wt_view();
+  if (ts.n_tasks > 0) {
+    const int blocks = (ts.n_tasks * 32 + threads - 1) / threads;
+    k_task_spmv<R><<<blocks, threads, 0, st>>>(ts, d.m, B, samples, static_cast<size_t>(d.P), grid, skip);
+    note_launch();
+  }
+}
+
+template <typename R>
+void launch_gram(const OpDev<R>& d, int B, const cplx<R>* grid_in, cplx<R>* grid_out, const SliceScalars* skip,
+                 cudaStream_t st) {
+  const int threads = 256;
+  if (d.gram.n_tasks > 0) {
+    const int blocks = (d.gram.n_tasks * 32 + threads - 1) / threads;
+    k_task_spmv<R><<<blocks, threads, 0, st>>>(d.gram, d.m, B, grid_in, static_cast<size_t>(d.m) * d.m, grid_out,
+                                               skip);
     note_launch();
   }
 }
@@ -940,6 +924,7 @@ void launch_fft_rows_test(int m, int rows, const cplx<R>* tw, const cplx<R>* in,
                                     cudaStream_t);                                                          \
   template void launch_wt_rows<R>(const OpDev<R>&, int, const SliceScalars*, cudaStream_t);                 \
   template void launch_t1_cols_only<R>(const OpDev<R>&, int, const SliceScalars*, cudaStream_t);            \
+  template void launch_gram<R>(const OpDev<R>&, int, const cplx<R>*, cplx<R>*, const SliceScalars*, cudaStream_t); \
   template void launch_t1_rows<R>(const OpDev<R>&, int, const PbEpi<R>&, cudaStream_t);                     \
   template void launch_wt_grid<R>(const OpDev<R>&, int, const cplx<R>*, cplx<R>*, cudaStream_t);            \
   template void launch_weight_samples<R>(cplx<R>*, int, int, int, cudaStream_t);                            \

@@ -224,11 +224,18 @@ constexpr int kMaxLoggedIters = 8192;
 // Device scratch of an op, sized for `cap` slices (element type = op precision).
 struct Scratch {
   int cap = 0;
-  Raw H, g, s, K, Gt, part_wt;    // complex
-  Raw heavy_cnt;
+  Raw H, g, s, K, Gt, part_wt, part_gram;  // complex
+  Raw heavy_cnt, heavy_cnt_gram;
   Raw cin, cout, fin, fout;       // staging for host pointers / temporaries
   Raw r, p0, p1, ap, x, rhs, fid, mu0, mu1, bx0, bx1, by0, by1, nred, zero, u2;  // real vectors
   Raw upd_log, sc, part;
+};
+
+// Device tables of one task-SpMV operator (the fused backend's Gram; see TaskSpmv).
+struct TaskSet {
+  Raw ent, tasks, perm, heavy, slot_heavy;
+  int n_tasks = 0, n_heavy = 0, n_slots = 0;
+  int64_t slots = 0, nnz = 0, bytes = 0;
 };
 
 struct GraphEntry {
@@ -250,6 +257,7 @@ struct tomo_op {
   int nq = 0, Ppad = 0;
   int n_tasks = 0, n_heavy = 0, n_slots = 0;
   Raw apod, tw, wcols, wvals, wbase, wxs, wys, wtent, wttasks, wtperm, wtheavy, wtslotheavy;
+  TaskSet gram;  // fused backend only
   int w_sep = 1;  // W storage used by the interpolation kernel (TOMO_W_FORMAT=ell selects SELL-32)
   Scratch sc;
   // surrogate
@@ -276,6 +284,7 @@ struct tomo_op {
 
   bool sharded() const { return g.a0 != 0 || g.a1 != g.A; }
   bool surrogate() const { return desc.backend == TOMO_BACKEND_SURROGATE; }
+  bool fused() const { return desc.backend == TOMO_BACKEND_FUSED; }
   int64_t L() const { return static_cast<int64_t>(g.n) * g.n; }
 
   template <typename R>
@@ -313,6 +322,9 @@ struct tomo_op {
     d.g = sc.g.as<cplx<R>>();
     d.s = sc.s.as<cplx<R>>();
     d.K = sc.K.as<cplx<R>>();
+    d.gram = TaskSpmv<R>{gram.ent.as<WtEnt<R>>(), gram.tasks.as<int4>(), gram.n_tasks, gram.perm.as<uint16_t>(),
+                         gram.heavy.as<int4>(), gram.slot_heavy.as<int>(), sc.heavy_cnt_gram.as<unsigned>(),
+                         gram.n_heavy, gram.n_slots, sc.part_gram.as<cplx<R>>()};
     return d;
   }
 
@@ -326,6 +338,12 @@ struct tomo_op {
     sc.part_wt.ensure(static_cast<size_t>(B) * std::max(n_slots, 1) * 32 * cz);
     sc.heavy_cnt.ensure(sizeof(unsigned) * static_cast<size_t>(B) * std::max(n_heavy, 1));
     CK(cudaMemset(sc.heavy_cnt.p, 0, sizeof(unsigned) * static_cast<size_t>(B) * std::max(n_heavy, 1)));
+    if (fused()) {
+      sc.part_gram.ensure(static_cast<size_t>(B) * std::max(gram.n_slots, 1) * 32 * cz);
+      const size_t hb = sizeof(unsigned) * static_cast<size_t>(B) * std::max(gram.n_heavy, 1);
+      sc.heavy_cnt_gram.ensure(hb);
+      CK(cudaMemset(sc.heavy_cnt_gram.p, 0, hb));
+    }
     sc.s.ensure(B * static_cast<size_t>(g.P) * cz);
     sc.K.ensure(B * n * m * cz);
     sc.sc.ensure(sizeof(SliceScalars) * B);
@@ -353,6 +371,202 @@ namespace {
 // wx[a]*wy[b], nufft.cpp:185-200), W^T as SELL-32 over consecutive grid nodes (entries sorted
 // by sample index: the exact transpose of the same products, spread nufft.cpp:142-157).
 // ------------------------------------------------------------------------------------------
+// Task tables of a sparse operator on the grid (W^T, or the Gram for the fused backend), built
+// one grid row at a time: per row the nodes are sorted by entry count (descending, stable in
+// ix); 32 sorted nodes form a block of L = max count chunks (entries chunk-major, padded with
+// weight-0 re-reads of a sample already in cache); blocks with L > max_chunks are split into
+// several warp tasks whose partial sums the last task of the block combines.
+template <typename R>
+struct TaskBuilder {
+  int m, max_chunks;
+  std::vector<WtEnt<R>> ent;
+  std::vector<int4> tasks, heavy;
+  std::vector<int> slot_heavy;
+  std::vector<uint16_t> perm;
+  std::vector<int> order;
+  int slots = 0;
+  int64_t chunks = 0, touched = 0;
+
+  TaskBuilder(int m_, int max_chunks_, int64_t nnz_hint)
+      : m(m_), max_chunks(max_chunks_), perm(static_cast<size_t>(m_) * m_), order(m_) {
+    ent.reserve(static_cast<size_t>(nnz_hint * 1.1) + 32);
+  }
+
+  // grid row iy: node ix holds entries [off[ix], off[ix+1]) of (col, val)
+  void add_row(int iy, const int64_t* off, const int32_t* col, const R* val) {
+    const int bpr = m / 32;
+    for (int ix = 0; ix < m; ++ix) {
+      order[ix] = ix;
+      touched += off[ix + 1] > off[ix];
+    }
+    std::stable_sort(order.begin(), order.end(),
+                     [off](int a, int b) { return off[a + 1] - off[a] > off[b + 1] - off[b]; });
+    for (int k = 0; k < m; ++k) perm[static_cast<int64_t>(iy) * m + k] = static_cast<uint16_t>(order[k]);
+    for (int kb = 0; kb < bpr; ++kb) {
+      const int first = order[kb * 32];
+      const int Lb = static_cast<int>(off[first + 1] - off[first]);
+      if (!Lb) continue;
+      const int64_t c0 = chunks;
+      chunks += Lb;
+      if (chunks > (int64_t(1) << 31) - 1) throw ConfigError("sparse operator too large for 32-bit chunk indices");
+      ent.resize(static_cast<size_t>(chunks) * 32);
+      for (int l = 0; l < 32; ++l) {
+        const int ix = order[kb * 32 + l];
+        const int c = static_cast<int>(off[ix + 1] - off[ix]);
+        int lastj = c > 0 ? col[off[ix]] : col[off[first]];
+        for (int k = 0; k < Lb; ++k) {
+          WtEnt<R> e{};
+          if (k < c) {
+            lastj = col[off[ix] + k];
+            e.j = lastj;
+            e.w = val[off[ix] + k];
+          } else {
+            e.j = lastj;  // padding: re-read an input already in cache, weight 0
+            e.w = R(0);
+          }
+          ent[(static_cast<size_t>(c0) + k) * 32 + l] = e;
+        }
+      }
+      const int bk = iy * bpr + kb;
+      if (Lb <= max_chunks) {
+        tasks.push_back(make_int4(bk, static_cast<int>(c0), Lb, -1));
+      } else {
+        const int ns = (Lb + max_chunks - 1) / max_chunks;
+        heavy.push_back(make_int4(bk, slots, ns, 0));
+        for (int k = 0; k < ns; ++k) slot_heavy.push_back(static_cast<int>(heavy.size()) - 1);
+        for (int k = 0; k < ns; ++k) {
+          const int cc = k * max_chunks;
+          tasks.push_back(make_int4(bk, static_cast<int>(c0) + cc, std::min(max_chunks, Lb - cc), slots++));
+        }
+      }
+    }
+  }
+
+  void finish() {
+    // longest tasks first (they are launched first and overlap the rest)
+    std::stable_sort(tasks.begin(), tasks.end(), [](const int4& a, const int4& b) { return a.z > b.z; });
+    if (ent.empty()) ent.resize(1);
+  }
+
+  void upload(Raw& dent, Raw& dtasks, Raw& dperm, Raw& dheavy, Raw& dslot) const {
+    dent.upload(ent);
+    dtasks.upload(tasks.empty() ? std::vector<int4>(1) : tasks);
+    dperm.upload(perm);
+    dheavy.upload(heavy.empty() ? std::vector<int4>(1) : heavy);
+    dslot.upload(slot_heavy.empty() ? std::vector<int>(1) : slot_heavy);
+  }
+};
+
+// Gram W^T W of the spreading operator on the (transposed) grid, build_btb
+// (normal_ops.cpp:53-173): entry (u, v) = sum_j W[j][u] W[j][v]; row u reaches the nodes within
+// w-1 per axis (band 2w-1). Accumulated in fp64 with a dense band per node over blocks of grid
+// rows, samples in ascending order and the reference's product association
+// (wx[a]wx[a2]) * (wy[b]wy[b2]), exact zeros dropped; emitted straight into task tables.
+template <typename R>
+void build_gram(tomo_op* op, const Plan& pl) {
+  const Geom& g = op->g;
+  const int m = g.m, w = g.w, band = 2 * w - 1, band2 = band * band;
+  const int64_t cap = op->desc.mem_cap_bytes > 0 ? op->desc.mem_cap_bytes : (int64_t(8) << 30);
+  const int64_t est = op->wt_rows * static_cast<int64_t>(band2) * 16;
+  if (est > cap)
+    throw ConfigError("build_btb: estimated " + std::to_string(est >> 20) +
+                      " MiB exceeds cap; raise the cap or use a smaller m_sp");
+  const int64_t lines_budget = std::max<int64_t>(1, (int64_t(128) << 20) / (static_cast<int64_t>(m) * band2 * 8));
+  const int lines = static_cast<int>(std::min<int64_t>(lines_budget, m));
+  // samples bucketed by the first grid row of their window (ascending j within a bucket)
+  std::vector<int> iy0(g.P), ix0(g.P);
+  std::vector<int64_t> boff(m + 1, 0);
+  for (int64_t j = 0; j < g.P; ++j) {
+    iy0[j] = wrapi(pl.mjy[j] + g.lo, m);
+    ix0[j] = wrapi(pl.mjx[j] + g.lo, m);
+    boff[iy0[j] + 1]++;
+  }
+  for (int r = 0; r < m; ++r) boff[r + 1] += boff[r];
+  std::vector<int> bucket(g.P);
+  {
+    std::vector<int64_t> fp(boff.begin(), boff.end() - 1);
+    for (int64_t j = 0; j < g.P; ++j) bucket[fp[iy0[j]]++] = static_cast<int>(j);
+  }
+  std::vector<double> acc(static_cast<size_t>(lines) * m * band2);
+  std::vector<double> px(static_cast<size_t>(w) * w), py(static_cast<size_t>(w) * w);
+  std::vector<int> list;
+  std::vector<int64_t> roff(m + 1);
+  std::vector<int32_t> rcol;
+  std::vector<R> rval;
+  rcol.reserve(static_cast<size_t>(m) * band2);
+  rval.reserve(static_cast<size_t>(m) * band2);
+  TaskBuilder<R> tb(m, 128, op->wt_rows * band2);
+  int64_t nnz = 0;
+  for (int y0 = 0; y0 < m; y0 += lines) {
+    const int y1 = std::min(m, y0 + lines);
+    std::fill(acc.begin(), acc.begin() + static_cast<size_t>(y1 - y0) * m * band2, 0.0);
+    // samples whose window rows iy0..iy0+w-1 (mod m) meet [y0, y1)
+    list.clear();
+    if (y1 - y0 + w - 1 >= m) {
+      for (int64_t j = 0; j < g.P; ++j) list.push_back(static_cast<int>(j));
+    } else {
+      for (int r = y0 - w + 1; r < y1; ++r) {
+        const int rr = wrapi(r, m);
+        for (int64_t k = boff[rr]; k < boff[rr + 1]; ++k) list.push_back(bucket[k]);
+      }
+      std::sort(list.begin(), list.end());
+    }
+    for (int j : list) {
+      const double* wxj = pl.wx.data() + static_cast<size_t>(j) * w;
+      const double* wyj = pl.wy.data() + static_cast<size_t>(j) * w;
+      for (int a = 0; a < w; ++a)
+        for (int a2 = 0; a2 < w; ++a2) px[a * w + a2] = wxj[a] * wxj[a2];
+      for (int b = 0; b < w; ++b)
+        for (int b2 = 0; b2 < w; ++b2) py[b * w + b2] = wyj[b] * wyj[b2];
+      for (int b = 0; b < w; ++b) {
+        const int iy = wrapi(iy0[j] + b, m);
+        if (iy < y0 || iy >= y1) continue;
+        for (int a = 0; a < w; ++a) {
+          const int ix = wrapi(ix0[j] + a, m);
+          double* cell = acc.data() + (static_cast<size_t>(iy - y0) * m + ix) * band2;
+          for (int b2 = 0; b2 < w; ++b2) {
+            const double vy = py[b * w + b2];
+            double* dst = cell + static_cast<size_t>(b2 - b + w - 1) * band + (w - 1 - a);
+            const double* pxa = px.data() + a * w;
+            for (int a2 = 0; a2 < w; ++a2) dst[a2] += pxa[a2] * vy;
+          }
+        }
+      }
+    }
+    for (int iy = y0; iy < y1; ++iy) {
+      rcol.clear();
+      rval.clear();
+      roff[0] = 0;
+      for (int ix = 0; ix < m; ++ix) {
+        const double* cell = acc.data() + (static_cast<size_t>(iy - y0) * m + ix) * band2;
+        for (int dy = 0; dy < band; ++dy) {
+          const int cy = wrapi(iy + dy - (w - 1), m);
+          for (int dx = 0; dx < band; ++dx) {
+            const double v = cell[dy * band + dx];
+            if (v != 0.0) {
+              rcol.push_back(cy * m + wrapi(ix + dx - (w - 1), m));
+              rval.push_back(static_cast<R>(v));
+            }
+          }
+        }
+        roff[ix + 1] = static_cast<int64_t>(rcol.size());
+      }
+      nnz += static_cast<int64_t>(rcol.size());
+      tb.add_row(iy, roff.data(), rcol.data(), rval.data());
+    }
+  }
+  tb.finish();
+  TaskSet& ts = op->gram;
+  ts.n_tasks = static_cast<int>(tb.tasks.size());
+  ts.n_heavy = static_cast<int>(tb.heavy.size());
+  ts.n_slots = tb.slots;
+  ts.slots = tb.chunks * 32;
+  ts.nnz = nnz;
+  ts.bytes = ts.slots * static_cast<int64_t>(sizeof(WtEnt<R>)) + static_cast<int64_t>(ts.n_tasks) * 16 +
+             static_cast<int64_t>(m) * m * 2;
+  tb.upload(ts.ent, ts.tasks, ts.perm, ts.heavy, ts.slot_heavy);
+}
+
 template <typename R>
 void build_tables(tomo_op* op) {
   const Geom& g = op->g;
@@ -418,74 +632,14 @@ void build_tables(tomo_op* op) {
       tv[k] = vals[o].v[c];
     }
   }
-  const int64_t G32 = G / 32;
-  const int bpr = m / 32;
-  std::vector<uint16_t> perm(G);
-  std::vector<int> blockL(G32);
-  std::vector<int> order(m);
-  int64_t touched = 0;
-  for (int iy = 0; iy < m; ++iy) {
-    const int* crow = cnt.data() + static_cast<int64_t>(iy) * m;
-    for (int ix = 0; ix < m; ++ix) {
-      order[ix] = ix;
-      touched += crow[ix] > 0;
-    }
-    std::stable_sort(order.begin(), order.end(), [crow](int a, int b) { return crow[a] > crow[b]; });
-    for (int k = 0; k < m; ++k) perm[static_cast<int64_t>(iy) * m + k] = static_cast<uint16_t>(order[k]);
-    for (int kb = 0; kb < bpr; ++kb) blockL[static_cast<int64_t>(iy) * bpr + kb] = crow[order[kb * 32]];
-  }
-  std::vector<int64_t> chunk0(G32 + 1, 0);
-  for (int64_t bk = 0; bk < G32; ++bk) chunk0[bk + 1] = chunk0[bk] + blockL[bk];
-  if (chunk0[G32] > (int64_t(1) << 31) - 1) throw ConfigError("W^T too large");
-  op->wt_rows = touched;
-  op->wt_slots = chunk0[G32] * 32;
-  std::vector<WtEnt<R>> ent(std::max<int64_t>(op->wt_slots, 1));
-  for (int64_t bk = 0; bk < G32; ++bk) {
-    const int Lb = blockL[bk];
-    if (!Lb) continue;
-    const int iy = static_cast<int>(bk / bpr);
-    for (int l = 0; l < 32; ++l) {
-      const int64_t node = static_cast<int64_t>(iy) * m + perm[bk * 32 + l];
-      const int c = cnt[node];
-      int lastj = c > 0 ? tj[off[node]] : tj[off[static_cast<int64_t>(iy) * m + perm[bk * 32]]];
-      for (int k = 0; k < Lb; ++k) {
-        WtEnt<R> e{};
-        if (k < c) {
-          lastj = tj[off[node] + k];
-          e.j = lastj;
-          e.w = tv[off[node] + k];
-        } else {
-          e.j = lastj;  // padding: re-read a sample already in cache, weight 0
-          e.w = R(0);
-        }
-        ent[(static_cast<size_t>(chunk0[bk]) + k) * 32 + l] = e;
-      }
-    }
-  }
-  std::vector<int4> tasks, heavy;
-  std::vector<int> slot_heavy;
-  int slots = 0;
-  for (int64_t bk = 0; bk < G32; ++bk) {
-    const int Lb = blockL[bk];
-    if (!Lb) continue;
-    if (Lb <= kWtMaxChunks) {
-      tasks.push_back(make_int4(static_cast<int>(bk), static_cast<int>(chunk0[bk]), Lb, -1));
-    } else {
-      const int ns = (Lb + kWtMaxChunks - 1) / kWtMaxChunks;
-      heavy.push_back(make_int4(static_cast<int>(bk), slots, ns, 0));
-      for (int k = 0; k < ns; ++k) slot_heavy.push_back(static_cast<int>(heavy.size()) - 1);
-      for (int k = 0; k < ns; ++k) {
-        const int c0 = k * kWtMaxChunks;
-        tasks.push_back(make_int4(static_cast<int>(bk), static_cast<int>(chunk0[bk]) + c0,
-                                  std::min(kWtMaxChunks, Lb - c0), slots++));
-      }
-    }
-  }
-  // longest tasks first (they are launched first and overlap the rest)
-  std::stable_sort(tasks.begin(), tasks.end(), [](const int4& a, const int4& b) { return a.z > b.z; });
-  op->n_tasks = static_cast<int>(tasks.size());
-  op->n_heavy = static_cast<int>(heavy.size());
-  op->n_slots = slots;
+  TaskBuilder<R> tb(m, kWtMaxChunks, off[G]);
+  for (int iy = 0; iy < m; ++iy) tb.add_row(iy, off.data() + static_cast<int64_t>(iy) * m, tj.data(), tv.data());
+  tb.finish();
+  op->wt_rows = tb.touched;
+  op->wt_slots = tb.chunks * 32;
+  op->n_tasks = static_cast<int>(tb.tasks.size());
+  op->n_heavy = static_cast<int>(tb.heavy.size());
+  op->n_slots = tb.slots;
 
   // deapodisation a[t]/m (nufft.cpp:204-227 with the 1/m per-axis FFT scale folded in)
   std::vector<R> apod(g.n);
@@ -518,13 +672,10 @@ void build_tables(tomo_op* op) {
   op->wys.upload(wys);
   op->wcols.upload(cols);
   op->wvals.upload(vals);
-  op->wtent.upload(ent);
-  op->wttasks.upload(tasks.empty() ? std::vector<int4>(1) : tasks);
-  op->wtperm.upload(perm);
-  op->wtheavy.upload(heavy.empty() ? std::vector<int4>(1) : heavy);
-  op->wtslotheavy.upload(slot_heavy.empty() ? std::vector<int>(1) : slot_heavy);
+  tb.upload(op->wtent, op->wttasks, op->wtperm, op->wtheavy, op->wtslotheavy);
   op->apod.upload(apod);
   op->tw.upload(tw);
+  if (op->fused()) build_gram<R>(op, pl);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -570,17 +721,37 @@ PbEpi<R> plain_epi(int mode, double scale) {
   return e;
 }
 
-// Re(N u) (or N u complex) for the W/W^T backend, incl. the cross-rank sum when sharded.
+// One normal-operator apply N = F_NU F_NU^* through the five-kernel pipeline:
+// P1 (p-update, deapod, pad, row iFFT) -> P2 (column iFFT) -> [W then W^T | Gram W^T W]
+// -> PA (pruned column FFT) -> PB (row FFT, crop, deapod, epilogue `e`).
+// Direct: apply_normal_direct (normal_ops.cpp:28-30); fused: apply_normal_fused (:175-206).
+template <typename R>
+void normal_core(tomo_op* op, int B, const void* in, bool complex_in, const PUpd<R>& pu, const PbEpi<R>& e,
+                 const SliceScalars* skip, cudaStream_t st) {
+  OpDev<R> d = op->dev<R>(B);
+  launch_t2_rows<R>(d, B, in, complex_in, pu, st);
+  launch_t2_cols<R>(d, B, skip, st);
+  if (op->fused()) {
+    launch_gram<R>(d, B, d.g, d.Gt, skip, st);
+  } else {
+    launch_w<R>(d, B, d.g, d.s, skip, st);
+    launch_wt_spread<R>(d, B, d.s, d.Gt, skip, st);
+  }
+  launch_t1_cols_only<R>(d, B, skip, st);
+  launch_t1_rows<R>(d, B, e, st);
+}
+
+// Re(N u) (or N u complex) for the W/W^T and Gram backends, incl. the cross-rank sum when
+// sharded.
 template <typename R>
 void normal_direct(tomo_op* op, int B, const void* in, bool cplx_io, void* out, cudaStream_t st) {
   PUpd<R> pu{};
-  type2<R>(op, B, in, cplx_io, pu, nullptr, nullptr, st);
   PbEpi<R> e = plain_epi<R>(cplx_io ? PB_COMPLEX : PB_REAL, 1.0);
   if (cplx_io)
     e.out_c = static_cast<cplx<R>*>(out);
   else
     e.out_r = static_cast<R*>(out);
-  type1<R>(op, B, nullptr, e, nullptr, st);
+  normal_core<R>(op, B, in, cplx_io, pu, e, nullptr, st);
   allreduce<R>(op, static_cast<R*>(out), static_cast<size_t>(B) * op->L() * (cplx_io ? 2 : 1), st);
 }
 
@@ -613,13 +784,12 @@ void cg_run(tomo_op* op, int B, const SysParams& s, const R* rhs, const R* x0, R
     }
     return;
   }
-  // W / W^T backend: init r = b - A x0, p = r, x = x0
+  // W / W^T (or Gram) backend: init r = b - A x0, p = r, x = x0
   const bool shard = op->sharded();
   R* nred = S.nred.as<R>();
   {
     PUpd<R> pu{};
     pu.red = red;
-    type2<R>(op, B, x0, false, pu, nullptr, nullptr, st);
     if (!shard) {
       PbEpi<R> e = plain_epi<R>(PB_CG_INIT, s.alpha);
       e.p = x0;
@@ -630,11 +800,11 @@ void cg_run(tomo_op* op, int B, const SysParams& s, const R* rhs, const R* x0, R
       e.sys = s;
       e.step = 0;
       e.red = red;
-      type1<R>(op, B, nullptr, e, nullptr, st);
+      normal_core<R>(op, B, x0, false, pu, e, nullptr, st);
     } else {
       PbEpi<R> e = plain_epi<R>(PB_REAL, s.alpha);
       e.out_r = nred;
-      type1<R>(op, B, nullptr, e, nullptr, st);
+      normal_core<R>(op, B, x0, false, pu, e, nullptr, st);
       allreduce<R>(op, nred, static_cast<size_t>(B) * L, st);
       launch_cg_epilogue<R>(n, B, 1, nred, x0, rhs, r, p0, x, s, 0, red, st);
     }
@@ -646,7 +816,6 @@ void cg_run(tomo_op* op, int B, const SysParams& s, const R* rhs, const R* x0, R
     pu.p = p0;
     pu.step = k;
     pu.red = red;
-    type2<R>(op, B, p0, false, pu, nullptr, skip, st);
     if (!shard) {
       PbEpi<R> e = plain_epi<R>(PB_CG_STEP, s.alpha);
       e.p = p0;
@@ -654,11 +823,11 @@ void cg_run(tomo_op* op, int B, const SysParams& s, const R* rhs, const R* x0, R
       e.sys = s;
       e.step = k;
       e.red = red;
-      type1<R>(op, B, nullptr, e, skip, st);
+      normal_core<R>(op, B, p0, false, pu, e, skip, st);
     } else {
       PbEpi<R> e = plain_epi<R>(PB_REAL, s.alpha);
       e.out_r = nred;
-      type1<R>(op, B, nullptr, e, skip, st);
+      normal_core<R>(op, B, p0, false, pu, e, skip, st);
       allreduce<R>(op, nred, static_cast<size_t>(B) * L, st);
       launch_cg_epilogue<R>(n, B, 0, nred, p0, nullptr, ap, nullptr, nullptr, s, k, red, st);
     }
@@ -948,8 +1117,8 @@ int tomo_op_create(const tomo_geom_desc* geom, const tomo_op_desc* desc, tomo_op
   tomo_op_desc dd{};
   if (desc) dd = *desc;
   if (dd.max_batch < 1) dd.max_batch = 1;
-  if (dd.backend != TOMO_BACKEND_DIRECT && dd.backend != TOMO_BACKEND_SURROGATE)
-    throw ConfigError("unknown backend (the Gram 'fused' backend is not built on the GPU)");
+  if (dd.backend != TOMO_BACKEND_DIRECT && dd.backend != TOMO_BACKEND_FUSED && dd.backend != TOMO_BACKEND_SURROGATE)
+    throw ConfigError("unknown backend");
   if (dd.precision != TOMO_F32 && dd.precision != TOMO_F64) throw ConfigError("unknown precision");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
@@ -1000,6 +1169,10 @@ int tomo_op_get_info(const tomo_op* op, tomo_op_info* info) {
                    static_cast<int64_t>(op->g.m) * op->g.m * 2;
   info->surrogate_r = op->rad;
   info->precision = op->f64 ? TOMO_F64 : TOMO_F32;
+  info->backend = op->desc.backend;
+  info->gram_nnz = op->gram.nnz;
+  info->gram_slots = op->gram.slots;
+  info->bytes_gram = op->gram.bytes;
   std::memcpy(info->stencil, op->stencil64, sizeof(info->stencil));
   TOMO_CATCH
 }
@@ -1577,7 +1750,10 @@ int tomo_profile_stages(tomo_op* op, int batch, int reps, double* ms, double* by
         } else if (s == 1) {
           launch_t2_cols<R>(d, batch, op->scal(), cs);
         } else if (s == 2) {
-          launch_w<R>(d, batch, d.g, d.s, op->scal(), cs);
+          if (op->fused())
+            launch_gram<R>(d, batch, d.g, d.Gt, op->scal(), cs);
+          else
+            launch_w<R>(d, batch, d.g, d.s, op->scal(), cs);
         } else if (s == 3) {
           launch_wt_spread<R>(d, batch, d.s, d.Gt, op->scal(), cs);
         } else if (s == 4) {
@@ -1604,8 +1780,9 @@ int tomo_profile_stages(tomo_op* op, int batch, int reps, double* ms, double* by
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
+    auto stage_on = [&](int s) { return sur ? (s >= 6) : (s <= 7 && !(op->fused() && s == 3)); };
     for (int s = 0; s < TOMO_NUM_STAGES; ++s) {
-      const bool on = sur ? (s >= 6) : (s <= 7);
+      const bool on = stage_on(s);
       if (!on) continue;
       // each stage timed as a CUDA graph of `reps` back-to-back launches (no host launch gaps)
       const std::string key = fmtkey("prof", batch, {double(s), double(reps)});
@@ -1634,7 +1811,9 @@ int tomo_profile_stages(tomo_op* op, int batch, int reps, double* ms, double* by
     if (!sur) {
       by[0] = B * (3 * rs * nn + cs * mn);                 // read p, r; write p; write H
       by[1] = B * (cs * mn + cs * mm);                     // read H, write g
-      by[2] = wbytes + B * (cs * op->wt_rows + cs * P);    // W stream, touched grid nodes, samples
+      by[2] = op->fused()  // Gram stream, read + write touched nodes | W stream, touched nodes, samples
+                  ? static_cast<double>(op->gram.bytes) + B * (2 * cs * op->wt_rows)
+                  : wbytes + B * (cs * op->wt_rows + cs * P);
       by[3] = wtbytes + B * (cs * P + cs * op->wt_rows);   // W^T stream, samples, write touched nodes
       by[4] = B * (cs * mm + cs * mn);                     // read spread grid, write K
       by[5] = B * (cs * mn + 2 * rs * nn);                 // read K, p; write Ap
@@ -1644,7 +1823,7 @@ int tomo_profile_stages(tomo_op* op, int batch, int reps, double* ms, double* by
     by[6] = B * 6 * rs * nn;  // read x, r, p, Ap; write x, r
     by[7] = B * 8 * rs * nn;  // read mu_new, mu_old, bx, by, fid; write bx, by, rhs
     for (int k = 0; k < TOMO_NUM_STAGES; ++k) {
-      const bool on = sur ? (k >= 6) : (k <= 7);
+      const bool on = stage_on(k);
       ms[k] = on ? acc[k] / reps : 0.0;
       bytes[k] = on ? by[k] : 0.0;
     }

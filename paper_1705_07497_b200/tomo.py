@@ -2,7 +2,7 @@
 B200 C ABI (include/tomo_b200.h).
 
 Names follow the reference: ``SliceTransform``-style geometry, ``make_direct_backend`` /
-``make_surrogate_backend`` (normal_ops.hpp:35-39), ``apply_normal`` / ``apply_normal_real``
+``make_fused_backend`` / ``make_surrogate_backend`` (normal_ops.hpp:35-39), ``apply_normal`` / ``apply_normal_real``
 (normal_ops.hpp:65-69), ``cg_solve`` (solver.hpp:43), ``split_bregman_tv`` (solver.hpp:83),
 ``tikhonov_solve`` (solver.hpp:91), ``grad`` / ``grad_adjoint`` / ``shrink`` (solver.hpp:19-24).
 Errors are raised as the reference's exception classes (errors.hpp:9-30).
@@ -198,13 +198,17 @@ class NormalBackend:
     """Device-resident normal operator (tomo::NormalBackend, normal_ops.hpp:23-31).
 
     kind "direct": N = F_NU F_NU^* through the precomputed W (SELL-32 ELL) and W^T tables and
-    the pruned in-CTA FFT passes; kind "surrogate": the translated stencil T.
+    the pruned in-CTA FFT passes; kind "fused": the same FFT passes around one SpMV with the
+    Gram W^T W (build_btb / apply_normal_fused, normal_ops.cpp:53-206); kind "surrogate": the
+    translated stencil T.
     """
+
+    _KINDS = {"direct": _lib.BACKEND_DIRECT, "fused": _lib.BACKEND_FUSED, "surrogate": _lib.BACKEND_SURROGATE}
 
     def __init__(self, geom: Geometry, kind: str = "direct", surrogate_r: int = 1, euclidean: bool = False,
                  device: int = 0, angle_block: tuple[int, int] | None = None, max_batch: int = 1,
-                 precision: str = "f32"):
-        if kind not in ("direct", "surrogate"):
+                 precision: str = "f32", mem_cap_bytes: int = 0):
+        if kind not in self._KINDS:
             raise ConfigError(f"unknown backend: {kind}")
         if precision not in ("f32", "f64"):
             raise ConfigError(f"unknown precision: {precision}")
@@ -214,8 +218,8 @@ class NormalBackend:
         self.precision = precision
         self.f64 = precision == "f64"
         ab = angle_block or (0, 0)
-        desc = _lib.OpDesc(_lib.BACKEND_DIRECT if kind == "direct" else _lib.BACKEND_SURROGATE, surrogate_r,
-                           int(euclidean), device, ab[0], ab[1], max_batch, _lib.F64 if self.f64 else _lib.F32)
+        desc = _lib.OpDesc(self._KINDS[kind], surrogate_r, int(euclidean), device, ab[0], ab[1], max_batch,
+                           _lib.F64 if self.f64 else _lib.F32, int(mem_cap_bytes))
         gd = geom._desc()
         h = C.c_void_p()
         _check(lib().tomo_op_create(C.byref(gd), C.byref(desc), C.byref(h)))
@@ -398,6 +402,11 @@ def nccl_unique_id() -> bytes:
 # ---------------------------------------------------------------- reference-named functions
 def make_direct_backend(geom: Geometry, **kw) -> NormalBackend:
     return NormalBackend(geom, "direct", **kw)
+
+
+def make_fused_backend(geom: Geometry, mem_cap_bytes: int = 8 << 30, **kw) -> NormalBackend:
+    """make_fused_backend (normal_ops.hpp:37): Gram W^T W, refused above `mem_cap_bytes`."""
+    return NormalBackend(geom, "fused", mem_cap_bytes=mem_cap_bytes, **kw)
 
 
 def make_surrogate_backend(geom: Geometry, radius_r: int = 1, euclidean: bool = False, **kw) -> NormalBackend:

@@ -1,5 +1,5 @@
 // Drives libtomo_b200 through the reference-shaped C++ wrapper (include/tomo_b200.hpp):
-// geometry -> make_direct_backend -> apply_normal / split_bregman_tv, exactly as a caller of
+// geometry -> make_direct_backend / make_fused_backend -> apply_normal / split_bregman_tv, exactly as a caller of
 // the reference library (proj/include/tomo/normal_ops.hpp, solver.hpp) would. Writes the
 // results as raw doubles for tests/test_cpp_wrapper.py to compare with the oracle.
 #include <cmath>
@@ -28,6 +28,9 @@ int main(int argc, char** argv) {
   std::ofstream os(argv[1], std::ios::binary);
   os.write(reinterpret_cast<const char*>(nu.data()), sizeof(Complex) * nu.size());
   os.write(reinterpret_cast<const char*>(mu.data()), sizeof(double) * mu.size());
+  NormalBackend fused = make_fused_backend(g);
+  std::vector<Complex> nf = apply_normal(fused, u);
+  os.write(reinterpret_cast<const char*>(nf.data()), sizeof(Complex) * nf.size());
   bool threw = false;
   try {
     Geometry bad = Geometry::preset(30, 4, 6);  // m = 60: not a power of two

@@ -32,12 +32,15 @@ def test_cpp_wrapper_matches_oracle(tmp_path):
     assert res.returncode == 0, res.stdout + res.stderr
     raw = np.fromfile(out, dtype=np.float64)
     nu = raw[:2 * 1024].view(np.complex128)
-    mu = raw[2 * 1024:]
+    mu = raw[2 * 1024:3 * 1024]
+    nf = raw[3 * 1024:].view(np.complex128)
     g = O.Geometry(n=32, n_angles=25, win_lo=-6, win_hi=6)
     i = np.arange(1024)
     u = np.sin(0.37 * i) + 1j * np.cos(0.11 * i)
     ref = O.apply_normal(g, u).ravel()
     assert np.linalg.norm(nu - ref) / np.linalg.norm(ref) < 1e-11
+    reff = O.apply_normal_fused(g, u).ravel()
+    assert np.linalg.norm(nf - reff) / np.linalg.norm(reff) < 1e-11
     f = O.type2(g, u)
     mref, _, _ = O.split_bregman(g, f, backend=0, alpha=10.0, lam=1.0, max_iters=4, cg_steps=5)
     assert np.linalg.norm(mu - mref.ravel()) / np.linalg.norm(mref) < 1e-3
