@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #define TOMO_DEV __device__ __forceinline__
 
 namespace tomo_b200 {
@@ -156,5 +158,19 @@ TOMO_DEV bool reduce2_last(double v0, double v1, double* part, int nblk, int blk
 
 template <typename R>
 TOMO_DEV bool finite_r(R v) { return isfinite(v); }
+
+// Host: launch `kern` on `st` through cudaLaunchKernelEx (status returned for CK_LAUNCH).
+// Programmatic dependent launch was measured here (griddepcontrol.wait at kernel entry,
+// programmatic stream serialisation on every launch) and gave no gain inside the solver graphs.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(std::forward<Args>(args))...);
+}
 
 }  // namespace tomo_b200

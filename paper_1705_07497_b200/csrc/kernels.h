@@ -11,6 +11,9 @@ namespace tomo_b200 {
 
 // Launch accounting + error check after every kernel launch (defined in tomo_capi.cu).
 void note_launch();
+// Error check of a cudaLaunchKernelEx status (throws CudaError).
+void check_launch(cudaError_t e);
+#define CK_LAUNCH(x) ::tomo_b200::check_launch(x)
 
 // W^T entry: sample index + weight. fp32: 8 B {j, w}; fp64: 16 B {j, pad, w}.
 template <typename R>

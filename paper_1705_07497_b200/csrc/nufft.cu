@@ -12,6 +12,7 @@
 // is kept transposed ([iy][ix]) so every pass reads and writes contiguous rows; W's column
 // indices are built for that layout. All kernels are templated on the real type R.
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -279,7 +280,7 @@ __global__ void __launch_bounds__(256) k_w_sep(OpDev<R> d, int B, const cplx<R>*
 // One warp per task {block, chunk0, nchunks, slot}: lane l accumulates node (block, l) over
 // the task's chunks (coalesced 32-entry chunks, 4 in flight), then writes either the grid node
 // (iy*m + perm) or, for a split block, its partial slot.
-template <typename R>
+template <int GRP, typename R>
 __global__ void __launch_bounds__(256) k_task_spmv(TaskSpmv<R> ts, int m, int B, const cplx<R>* __restrict__ s_all,
                                                     size_t in_stride, cplx<R>* __restrict__ grid,
                                                     const SliceScalars* skip) {
@@ -298,23 +299,28 @@ __global__ void __launch_bounds__(256) k_task_spmv(TaskSpmv<R> ts, int m, int B,
     if (skip && (skip[b].done || skip[b].frozen)) continue;
     const C2* s = s_all + static_cast<size_t>(b) * in_stride;
     C2 a0 = czero<C2>(), a1 = czero<C2>();
-    int c = 0;
-    // four chunks per step (8-deep unrolling and software-pipelined entry loads were both
-    // measured slower on B200: occupancy)
-    for (; c + 4 <= nc; c += 4) {
-      const WtEnt<R> x0 = ldg(e + (c + 0) * 32), x1 = ldg(e + (c + 1) * 32);
-      const WtEnt<R> x2 = ldg(e + (c + 2) * 32), x3 = ldg(e + (c + 3) * 32);
-      const C2 s0 = __ldg(&s[x0.j]), s1 = __ldg(&s[x1.j]), s2 = __ldg(&s[x2.j]), s3 = __ldg(&s[x3.j]);
-      a0.x += x0.w * s0.x + x2.w * s2.x;
-      a0.y += x0.w * s0.y + x2.w * s2.y;
-      a1.x += x1.w * s1.x + x3.w * s3.x;
-      a1.y += x1.w * s1.y + x3.w * s3.y;
-    }
-    for (; c < nc; ++c) {
-      const WtEnt<R> x0 = ldg(e + c * 32);
-      const C2 s0 = __ldg(&s[x0.j]);
-      a0.x += x0.w * s0.x;
-      a0.y += x0.w * s0.y;
+    // groups of GRP chunks with predicated tails (all loads of a group in flight at once)
+    for (int c = 0; c < nc; c += GRP) {
+      WtEnt<R> q[GRP];
+      C2 v[GRP];
+#pragma unroll
+      for (int k = 0; k < GRP; ++k) {
+        if (c + k < nc) {
+          q[k] = ldg(e + (c + k) * 32);
+        } else {
+          q[k].j = 0;
+          q[k].w = R(0);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < GRP; ++k) v[k] = c + k < nc ? __ldg(&s[q[k].j]) : czero<C2>();
+#pragma unroll
+      for (int k = 0; k < GRP; k += 2) {
+        a0.x += q[k].w * v[k].x;
+        a0.y += q[k].w * v[k].y;
+        a1.x += q[k + 1].w * v[k + 1].x;
+        a1.y += q[k + 1].w * v[k + 1].y;
+      }
     }
     const C2 v = cadd(a0, a1);
     if (slot < 0) {
@@ -732,7 +738,7 @@ void launch_t2_rows(const OpDev<R>& d, int B, const void* in, bool in_complex, c
     const size_t smem = static_cast<size_t>(rpc) * S::STRIDE * sizeof(cplx<R>);
     set_smem(k_t2_rows<M, RB, R>, smem);
     dim3 grid((d.n + rpc - 1) / rpc, B);
-    k_t2_rows<M, RB, R><<<grid, rpc * S::T, smem, st>>>(d, in, in_complex ? 1 : 0, pu, rpc);
+    CK_LAUNCH(launch_k(k_t2_rows<M, RB, R>, grid, rpc * S::T, smem, st, d, in, in_complex ? 1 : 0, pu, rpc));
     note_launch();
   });
 }
@@ -769,12 +775,12 @@ void launch_t2_cols(const OpDev<R>& d, int B, const SliceScalars* skip, cudaStre
       const size_t smem = (static_cast<size_t>(S::STRIDE) + d.n) * sizeof(cplx<R>);
       set_smem(k_t2_cols_p<M, RB, R>, smem);
       const int ctas = persistent_ctas(k_t2_cols_p<M, RB, R>, S::T, smem, M, B);
-      k_t2_cols_p<M, RB, R><<<dim3(ctas, B), S::T, smem, st>>>(d, skip);
+      CK_LAUNCH(launch_k(k_t2_cols_p<M, RB, R>, dim3(ctas, B), S::T, smem, st, d, skip));
     } else {
       const int rpc = choose_rpc(S::T, M, M, B, sizeof(cplx<R>), false);
       const size_t smem = static_cast<size_t>(rpc) * S::STRIDE * sizeof(cplx<R>);
       set_smem(k_t2_cols<M, RB, R>, smem);
-      k_t2_cols<M, RB, R><<<dim3(M / rpc, B), rpc * S::T, smem, st>>>(d, rpc, skip);
+      CK_LAUNCH(launch_k(k_t2_cols<M, RB, R>, dim3(M / rpc, B), rpc * S::T, smem, st, d, rpc, skip));
     }
     note_launch();
   });
@@ -790,9 +796,9 @@ void launch_w(const OpDev<R>& d, int B, const cplx<R>* grid, cplx<R>* samples, c
     auto go = [&](auto WC) {
       constexpr int WM = decltype(WC)::value;
       if (B >= 2)
-        k_w_sep<2, WM, R><<<blocks, threads, 0, st>>>(d, B, grid, samples, skip);
+        CK_LAUNCH(launch_k(k_w_sep<2, WM, R>, blocks, threads, 0, st, d, B, grid, samples, skip));
       else
-        k_w_sep<1, WM, R><<<blocks, threads, 0, st>>>(d, B, grid, samples, skip);
+        CK_LAUNCH(launch_k(k_w_sep<1, WM, R>, blocks, threads, 0, st, d, B, grid, samples, skip));
     };
     if (d.w <= 6)
       go(std::integral_constant<int, 6>{});
@@ -801,37 +807,37 @@ void launch_w(const OpDev<R>& d, int B, const cplx<R>* grid, cplx<R>* samples, c
     else
       go(std::integral_constant<int, 16>{});
   } else if (B >= 4) {
-    k_w<4, R><<<blocks, threads, 0, st>>>(d, B, grid, samples, skip);
+    CK_LAUNCH(launch_k(k_w<4, R>, blocks, threads, 0, st, d, B, grid, samples, skip));
   } else if (B >= 2) {
-    k_w<2, R><<<blocks, threads, 0, st>>>(d, B, grid, samples, skip);
+    CK_LAUNCH(launch_k(k_w<2, R>, blocks, threads, 0, st, d, B, grid, samples, skip));
   } else {
-    k_w<1, R><<<blocks, threads, 0, st>>>(d, B, grid, samples, skip);
+    CK_LAUNCH(launch_k(k_w<1, R>, blocks, threads, 0, st, d, B, grid, samples, skip));
   }
+  note_launch();
+}
+
+template <typename R>
+void launch_task_spmv(const TaskSpmv<R>& ts, int m, int B, const cplx<R>* x, size_t in_stride, cplx<R>* grid,
+                      const SliceScalars* skip, cudaStream_t st) {
+  if (ts.n_tasks <= 0) return;
+  const int threads = 256;
+  const int blocks = (ts.n_tasks * 32 + threads - 1) / threads;
+  // group depth measured on B200: fp32 6 (32 registers, full occupancy), fp64 4
+  constexpr int GRP = sizeof(R) == 4 ? 6 : 4;
+  CK_LAUNCH(launch_k(k_task_spmv<GRP, R>, blocks, threads, 0, st, ts, m, B, x, in_stride, grid, skip));
   note_launch();
 }
 
 template <typename R>
 void launch_wt_spread(const OpDev<R>& d, int B, const cplx<R>* samples, cplx<R>* grid, const SliceScalars* skip,
                       cudaStream_t st) {
-  const int threads = 256;
-  const TaskSpmv<R> ts = d.wt_view();
-  if (ts.n_tasks > 0) {
-    const int blocks = (ts.n_tasks * 32 + threads - 1) / threads;
-    k_task_spmv<R><<<blocks, threads, 0, st>>>(ts, d.m, B, samples, static_cast<size_t>(d.P), grid, skip);
-    note_launch();
-  }
+  launch_task_spmv<R>(d.wt_view(), d.m, B, samples, static_cast<size_t>(d.P), grid, skip, st);
 }
 
 template <typename R>
 void launch_gram(const OpDev<R>& d, int B, const cplx<R>* grid_in, cplx<R>* grid_out, const SliceScalars* skip,
                  cudaStream_t st) {
-  const int threads = 256;
-  if (d.gram.n_tasks > 0) {
-    const int blocks = (d.gram.n_tasks * 32 + threads - 1) / threads;
-    k_task_spmv<R><<<blocks, threads, 0, st>>>(d.gram, d.m, B, grid_in, static_cast<size_t>(d.m) * d.m, grid_out,
-                                               skip);
-    note_launch();
-  }
+  launch_task_spmv<R>(d.gram, d.m, B, grid_in, static_cast<size_t>(d.m) * d.m, grid_out, skip, st);
 }
 
 template <typename R>
@@ -854,12 +860,12 @@ void launch_t1_cols_only(const OpDev<R>& d, int B, const SliceScalars* skip, cud
     if (smem <= kMaxSmem && M >= kPersistMinM) {
       set_smem(k_t1_cols_p<M, RB, R>, smem);
       const int ctas = persistent_ctas(k_t1_cols_p<M, RB, R>, rpc * S::T, smem, M / rpc, B);
-      k_t1_cols_p<M, RB, R><<<dim3(ctas, B), rpc * S::T, smem, st>>>(d, rpc, skip);
+      CK_LAUNCH(launch_k(k_t1_cols_p<M, RB, R>, dim3(ctas, B), rpc * S::T, smem, st, d, rpc, skip));
     } else {  // row + staging do not fit (fp64, m = 8192): one-shot CTAs
       const int rpc1 = choose_rpc(S::T, M, M, B, sizeof(cplx<R>), true);
       const size_t smem1 = static_cast<size_t>(rpc1) * S::STRIDE * sizeof(cplx<R>);
       set_smem(k_t1_cols<M, RB, R>, smem1);
-      k_t1_cols<M, RB, R><<<dim3(M / rpc1, B), rpc1 * S::T, smem1, st>>>(d, rpc1, skip);
+      CK_LAUNCH(launch_k(k_t1_cols<M, RB, R>, dim3(M / rpc1, B), rpc1 * S::T, smem1, st, d, rpc1, skip));
     }
     note_launch();
   });
@@ -875,7 +881,7 @@ void launch_t1_rows(const OpDev<R>& d, int B, const PbEpi<R>& e, cudaStream_t st
       const size_t smem = smem_p;
       set_smem(k_t1_rows_p<M, RB, R>, smem);
       const int ctas = std::min(MAX_PART_BLOCKS, persistent_ctas(k_t1_rows_p<M, RB, R>, S::T, smem, d.n, B));
-      k_t1_rows_p<M, RB, R><<<dim3(ctas, B), S::T, smem, st>>>(d, e);
+      CK_LAUNCH(launch_k(k_t1_rows_p<M, RB, R>, dim3(ctas, B), S::T, smem, st, d, e));
     } else {  // rows shorter than 512: whole warps need several rows per CTA
       int rpc = choose_rpc(S::T, M, d.n, B, sizeof(cplx<R>), false);
       while ((rpc * S::T) % 32) rpc <<= 1;
@@ -883,7 +889,7 @@ void launch_t1_rows(const OpDev<R>& d, int B, const PbEpi<R>& e, cudaStream_t st
       const size_t smem = static_cast<size_t>(rpc) * S::STRIDE * sizeof(cplx<R>);
       set_smem(k_t1_rows<M, RB, R>, smem);
       dim3 grid((d.n + rpc - 1) / rpc, B);
-      k_t1_rows<M, RB, R><<<grid, rpc * S::T, smem, st>>>(d, e, rpc);
+      CK_LAUNCH(launch_k(k_t1_rows<M, RB, R>, grid, rpc * S::T, smem, st, d, e, rpc));
     }
     note_launch();
   });
@@ -899,7 +905,7 @@ template <typename R>
 void launch_weight_samples(cplx<R>* s, int B, int P, int nb, cudaStream_t st) {
   // angle blocks hold whole angles: t = j % nb is unchanged by a shard offset
   const int64_t total = static_cast<int64_t>(B) * P;
-  k_weight_samples<R><<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(s, B, P, nb);
+  CK_LAUNCH(launch_k(k_weight_samples<R>, static_cast<unsigned>((total + 255) / 256), 256, 0, st, s, B, P, nb));
   note_launch();
 }
 
@@ -911,7 +917,7 @@ void launch_fft_rows_test(int m, int rows, const cplx<R>* tw, const cplx<R>* in,
     using S = FftShape<M, RB>;
     const size_t smem = S::STRIDE * sizeof(cplx<R>);
     set_smem(k_fft_rows_test<M, RB, R>, smem);
-    k_fft_rows_test<M, RB, R><<<rows, S::T, smem, st>>>(tw, in, out, rows, inverse ? 1 : 0);
+    CK_LAUNCH(launch_k(k_fft_rows_test<M, RB, R>, rows, S::T, smem, st, tw, in, out, rows, inverse ? 1 : 0));
     note_launch();
   });
 }

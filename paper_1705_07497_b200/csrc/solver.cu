@@ -464,7 +464,7 @@ template <typename R>
 void launch_cg_update(int n, int B, const R* p, const R* ap, R* x, R* r, const SysParams& sys, int step,
                       const Reduce& red, cudaStream_t st) {
   const int64_t L = static_cast<int64_t>(n) * n;
-  k_cg_update<R><<<dim3(vec_blocks(L, B), B), kVecThreads, 0, st>>>(L, p, ap, x, r, sys, step, red);
+  CK_LAUNCH(launch_k(k_cg_update<R>, dim3(vec_blocks(L, B), B), kVecThreads, 0, st, L, p, ap, x, r, sys, step, red));
   note_launch();
 }
 
@@ -474,10 +474,10 @@ void launch_stencil(int n, int B, int rad, const StencilCoef& coef, int mode, co
                     cudaStream_t st) {
   dim3 grid((n + kTile - 1) / kTile, (n + kTile - 1) / kTile, B);
   switch (rad) {
-    case 1: k_stencil<1, R><<<grid, 256, 0, st>>>(n, coef, mode, in, r_in, p_out, ap_out, b, x_out, sys, step, red); break;
-    case 2: k_stencil<2, R><<<grid, 256, 0, st>>>(n, coef, mode, in, r_in, p_out, ap_out, b, x_out, sys, step, red); break;
-    case 3: k_stencil<3, R><<<grid, 256, 0, st>>>(n, coef, mode, in, r_in, p_out, ap_out, b, x_out, sys, step, red); break;
-    default: k_stencil<4, R><<<grid, 256, 0, st>>>(n, coef, mode, in, r_in, p_out, ap_out, b, x_out, sys, step, red); break;
+    case 1: CK_LAUNCH(launch_k(k_stencil<1, R>, grid, 256, 0, st, n, coef, mode, in, r_in, p_out, ap_out, b, x_out, sys, step, red)); break;
+    case 2: CK_LAUNCH(launch_k(k_stencil<2, R>, grid, 256, 0, st, n, coef, mode, in, r_in, p_out, ap_out, b, x_out, sys, step, red)); break;
+    case 3: CK_LAUNCH(launch_k(k_stencil<3, R>, grid, 256, 0, st, n, coef, mode, in, r_in, p_out, ap_out, b, x_out, sys, step, red)); break;
+    default: CK_LAUNCH(launch_k(k_stencil<4, R>, grid, 256, 0, st, n, coef, mode, in, r_in, p_out, ap_out, b, x_out, sys, step, red)); break;
   }
   note_launch();
 }
@@ -486,8 +486,8 @@ template <typename R>
 void launch_cg_epilogue(int n, int B, int mode, const R* nred, const R* p, const R* b, R* ap, R* p_out, R* x_out,
                         const SysParams& sys, int step, const Reduce& red, cudaStream_t st) {
   const int64_t L = static_cast<int64_t>(n) * n;
-  k_cg_epilogue<R><<<dim3(vec_blocks(L, B), B), kVecThreads, 0, st>>>(n, mode, nred, p, b, ap, p_out, x_out, sys, step,
-                                                                      red);
+  CK_LAUNCH(launch_k(k_cg_epilogue<R>, dim3(vec_blocks(L, B), B), kVecThreads, 0, st, n, mode, nred, p, b, ap, p_out, x_out, sys, step,
+                                                                      red));
   note_launch();
 }
 
@@ -495,8 +495,8 @@ template <typename R>
 void launch_sb_post(int n, int B, R* mu_new, const R* mu_old, const R* bx_old, const R* by_old, R* bx_new, R* by_new,
                     const R* fid, R* rhs, double lambda, const Reduce& red, cudaStream_t st) {
   const int64_t L = static_cast<int64_t>(n) * n;
-  k_sb_post<R><<<dim3(vec_blocks(L, B), B), kVecThreads, 0, st>>>(n, mu_new, mu_old, bx_old, by_old, bx_new, by_new,
-                                                                  fid, rhs, lambda, red);
+  CK_LAUNCH(launch_k(k_sb_post<R>, dim3(vec_blocks(L, B), B), kVecThreads, 0, st, n, mu_new, mu_old, bx_old, by_old, bx_new, by_new,
+                                                                  fid, rhs, lambda, red));
   note_launch();
 }
 
@@ -505,47 +505,47 @@ void launch_cp_dual(int n, int B, const R* u_cur, const R* u_prev, const R* yx_o
                     R* yy_new, const R* bp, R* rhs, double tau, double sigma, double theta, double lambda,
                     cudaStream_t st) {
   const int64_t L = static_cast<int64_t>(n) * n;
-  k_cp_dual<R><<<dim3(vec_blocks(L, B), B), kVecThreads, 0, st>>>(n, u_cur, u_prev, yx_old, yy_old, yx_new, yy_new, bp,
-                                                                  rhs, R(tau), R(sigma), R(theta), R(lambda));
+  CK_LAUNCH(launch_k(k_cp_dual<R>, dim3(vec_blocks(L, B), B), kVecThreads, 0, st, n, u_cur, u_prev, yx_old, yy_old, yx_new, yy_new, bp,
+                                                                  rhs, R(tau), R(sigma), R(theta), R(lambda)));
   note_launch();
 }
 
 template <typename R>
 void launch_axpby(int64_t len, double a, const R* x, double b, const R* y, R* out, cudaStream_t st) {
-  k_axpby<R><<<blocks_for(len, 256), 256, 0, st>>>(len, R(a), x, R(b), y, out);
+  CK_LAUNCH(launch_k(k_axpby<R>, blocks_for(len, 256), 256, 0, st, len, R(a), x, R(b), y, out));
   note_launch();
 }
 
 template <typename R>
 void launch_dot(int n, int B, const R* x, const R* y, const Reduce& red, cudaStream_t st) {
   const int64_t L = static_cast<int64_t>(n) * n;
-  k_dot<R><<<dim3(vec_blocks(L, B), B), kVecThreads, 0, st>>>(L, x, y, red);
+  CK_LAUNCH(launch_k(k_dot<R>, dim3(vec_blocks(L, B), B), kVecThreads, 0, st, L, x, y, red));
   note_launch();
 }
 
 template <typename R>
 void launch_leak(int64_t len, const cplx<R>* v, const Reduce& red, cudaStream_t st) {
-  k_leak<R><<<vec_blocks(len, 1), kVecThreads, 0, st>>>(len, v, red);
+  CK_LAUNCH(launch_k(k_leak<R>, vec_blocks(len, 1), kVecThreads, 0, st, len, v, red));
   note_launch();
 }
 
 template <typename R>
 void launch_grad(int n, int B, const R* u, R* gx, R* gy, cudaStream_t st) {
   const int64_t L = static_cast<int64_t>(n) * n;
-  k_grad<R><<<dim3(vec_blocks(L, B), B), kVecThreads, 0, st>>>(n, u, gx, gy);
+  CK_LAUNCH(launch_k(k_grad<R>, dim3(vec_blocks(L, B), B), kVecThreads, 0, st, n, u, gx, gy));
   note_launch();
 }
 
 template <typename R>
 void launch_grad_adjoint(int n, int B, const R* gx, const R* gy, R* out, cudaStream_t st) {
   const int64_t L = static_cast<int64_t>(n) * n;
-  k_grad_adjoint<R><<<dim3(vec_blocks(L, B), B), kVecThreads, 0, st>>>(n, gx, gy, out);
+  CK_LAUNCH(launch_k(k_grad_adjoint<R>, dim3(vec_blocks(L, B), B), kVecThreads, 0, st, n, gx, gy, out));
   note_launch();
 }
 
 template <typename R>
 void launch_shrink(int64_t len, const R* x, double gamma, R* out, cudaStream_t st) {
-  k_shrink<R><<<blocks_for(len, 256), 256, 0, st>>>(len, x, R(gamma), out);
+  CK_LAUNCH(launch_k(k_shrink<R>, blocks_for(len, 256), 256, 0, st, len, x, R(gamma), out));
   note_launch();
 }
 

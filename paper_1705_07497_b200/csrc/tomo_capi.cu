@@ -46,6 +46,13 @@ thread_local std::string g_err;
 std::atomic<int64_t> g_launches{0};
 thread_local int64_t* g_capture_count = nullptr;
 
+void check_launch(cudaError_t e) {
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw CudaError(std::string("kernel launch failed: ") + cudaGetErrorString(e));
+  }
+}
+
 void note_launch() {
   if (g_capture_count)
     ++*g_capture_count;
@@ -495,7 +502,7 @@ void build_gram(tomo_op* op, const Plan& pl) {
   std::vector<R> rval;
   rcol.reserve(static_cast<size_t>(m) * band2);
   rval.reserve(static_cast<size_t>(m) * band2);
-  TaskBuilder<R> tb(m, 128, op->wt_rows * band2);
+  TaskBuilder<R> tb(m, kWtMaxChunks, op->wt_rows * band2);
   int64_t nnz = 0;
   for (int y0 = 0; y0 < m; y0 += lines) {
     const int y1 = std::min(m, y0 + lines);
