@@ -274,6 +274,41 @@ __global__ void __launch_bounds__(256) k_w_sep(OpDev<R> d, int B, const cplx<R>*
   }
 }
 
+// Wide windows (w > 8, e.g. the digits12 preset's 25 taps): the same separable product with the
+// factor vectors read in the loops (L1-resident per thread) instead of held in registers.
+template <typename R>
+__global__ void __launch_bounds__(256) k_w_sep_wide(OpDev<R> d, int B, const cplx<R>* __restrict__ grid,
+                                                     cplx<R>* __restrict__ out, const SliceScalars* skip) {
+  using C2 = cplx<R>;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= d.P) return;
+  const int m = d.m, w = d.w;
+  const int base = __ldg(&d.w_base[j]);
+  const int ix0 = base & 0xffff, iy0 = base >> 16;
+  const size_t G = static_cast<size_t>(m) * m;
+  for (int b = 0; b < B; ++b) {
+    if (skip && (skip[b].done || skip[b].frozen)) continue;
+    const C2* gb = grid + G * b;
+    C2 acc = czero<C2>();
+    for (int bb = 0; bb < w; ++bb) {
+      const int t = iy0 + bb;
+      const C2* row = gb + static_cast<size_t>(t >= m ? t - m : t) * m;
+      C2 ra = czero<C2>();
+      for (int a = 0; a < w; ++a) {
+        const int u = ix0 + a;
+        const R wx = __ldg(&d.w_x[static_cast<size_t>(a) * d.Ppad + j]);
+        const C2 gv = row[u >= m ? u - m : u];
+        ra.x += wx * gv.x;
+        ra.y += wx * gv.y;
+      }
+      const R wy = __ldg(&d.w_y[static_cast<size_t>(bb) * d.Ppad + j]);
+      acc.x += wy * ra.x;
+      acc.y += wy * ra.y;
+    }
+    out[static_cast<size_t>(b) * d.P + j] = acc;
+  }
+}
+
 // ---------------------------------------------------------------- W^T / Gram: balanced task SpMV
 // The same kernel applies W^T (input = slice samples, stride P) and, for the fused backend, the
 // Gram operator W^T W (input = the grid, stride m^2; grid_in must not alias grid).
@@ -805,7 +840,7 @@ void launch_w(const OpDev<R>& d, int B, const cplx<R>* grid, cplx<R>* samples, c
     else if (d.w <= 8)
       go(std::integral_constant<int, 8>{});
     else
-      go(std::integral_constant<int, 16>{});
+      CK_LAUNCH(launch_k(k_w_sep_wide<R>, blocks, threads, 0, st, d, B, grid, samples, skip));
   } else if (B >= 4) {
     CK_LAUNCH(launch_k(k_w<4, R>, blocks, threads, 0, st, d, B, grid, samples, skip));
   } else if (B >= 2) {

@@ -155,7 +155,8 @@ Geom make_geom(const tomo_geom_desc* d, const tomo_op_desc* od) {
   if (!(g.tau > 0.0)) throw ConfigError("make_params: tau must be positive");
   g.m = g.R * g.n;
   g.w = g.hi - g.lo + 1;
-  if (g.w > 16) throw ConfigError("spreading window too wide for the GPU tables (max 16)");
+  if (g.w > 64) throw ConfigError("spreading window too wide (max 64 taps per axis)");
+  if (g.w > g.R * g.n) throw ConfigError("spreading window wider than the oversampled grid");
   if (g.m < 32 || g.m > 8192 || (g.m & (g.m - 1)) != 0)
     throw ConfigError("grid side m = R*n must be a power of two in [32, 8192]");
   g.angles.resize(g.A);
@@ -677,8 +678,10 @@ void build_tables(tomo_op* op) {
   op->wbase.upload(wbase);
   op->wxs.upload(wxs);
   op->wys.upload(wys);
-  op->wcols.upload(cols);
-  op->wvals.upload(vals);
+  if (!op->w_sep) {  // the SELL-32 ELL form is uploaded only when selected (TOMO_W_FORMAT=ell)
+    op->wcols.upload(cols);
+    op->wvals.upload(vals);
+  }
   tb.upload(op->wtent, op->wttasks, op->wtperm, op->wtheavy, op->wtslotheavy);
   op->apod.upload(apod);
   op->tw.upload(tw);
@@ -1171,7 +1174,8 @@ int tomo_op_get_info(const tomo_op* op, tomo_op_info* info) {
   info->nnz = op->nnz;
   info->wt_rows = op->wt_rows;
   info->wt_slots = op->wt_slots;
-  info->bytes_w = static_cast<int64_t>(op->Ppad) * op->nq * 32 * (16 + 4 * static_cast<int64_t>(op->rsz)) / 32;
+  info->bytes_w = op->w_sep ? static_cast<int64_t>(op->Ppad) * (4 + 2 * op->g.w * static_cast<int64_t>(op->rsz))
+                            : static_cast<int64_t>(op->Ppad) * op->nq * 32 * (16 + 4 * static_cast<int64_t>(op->rsz)) / 32;
   info->bytes_wt = op->wt_slots * (op->f64 ? 16 : 8) + static_cast<int64_t>(op->n_tasks) * 16 +
                    static_cast<int64_t>(op->g.m) * op->g.m * 2;
   info->surrogate_r = op->rad;

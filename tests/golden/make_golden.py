@@ -21,6 +21,7 @@ CASES = {
     "n32_msp6": (32, 25, 6),   # digits6 preset (proj/src/nufft.cpp:26-34)
     "n32_msp3": (32, 25, 3),   # the 7x7 window used as the literal-reference parity config
     "n64_msp2": (64, 50, 2),   # digits2 preset
+    "n32_msp12": (32, 25, 12),  # digits12 preset: 25-tap window, Gram band 49 wraps on m = 64
 }
 
 
@@ -65,5 +66,7 @@ def make(name, n, A, m_sp):
 if __name__ == "__main__":
     if not refbind.available():
         sys.exit("oracle/_ref/libtomo_ref.so missing: run `make -C oracle ref` first")
+    only = sys.argv[1:]
     for k, v in CASES.items():
-        make(k, *v)
+        if not only or k in only:
+            make(k, *v)

@@ -46,6 +46,7 @@ RNG = np.random.default_rng(2024)
 GEOMS = {
     "ref_msp6": dict(n=32, n_angles=25, win_lo=-6, win_hi=6),
     "ref_msp3": dict(n=32, n_angles=25, win_lo=-3, win_hi=3),
+    "ref_msp12": dict(n=32, n_angles=25, win_lo=-12, win_hi=12),  # digits12: 25 taps (wide W kernel)
     "width6_odd_nb": dict(n=64, n_angles=30, n_b=65, win_lo=-2, win_hi=3, tau=3 / 64 ** 2),
     "R4_gl_tau": dict(n=32, n_angles=20, n_b=33, oversample=4, win_lo=-3, win_hi=3,
                       tau=np.pi * 3 / (32 ** 2 * 4 * 3.5)),
