@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(256) k_w(OpDev<R> d, int B, const cplx<R>* __r
 // Same matrix as k_w, stored as its rank-1 blocks: per row j the base node (ix0, iy0) and the
 // two window factor vectors (SoA, coalesced): 4 + 2w*sizeof(R) bytes per row instead of
 // w^2*(4 + sizeof(R)). The inner loop walks a grid row (b fixed, ix0+a consecutive).
-template <int BT, int WMAX, typename R>
+template <int BT, int WMAX, int RU, typename R>
 __global__ void __launch_bounds__(256) k_w_sep(OpDev<R> d, int B, const cplx<R>* __restrict__ grid,
                                                 cplx<R>* __restrict__ out, const SliceScalars* skip) {
   using C2 = cplx<R>;
@@ -227,13 +227,12 @@ __global__ void __launch_bounds__(256) k_w_sep(OpDev<R> d, int B, const cplx<R>*
   const int m = d.m, w = d.w;
   const int base = __ldg(&d.w_base[j]);
   const int ix0 = base & 0xffff, iy0 = base >> 16;
-  R wx[WMAX], wy[WMAX];
+  R wx[WMAX];
   int ix[WMAX];
 #pragma unroll
   for (int a = 0; a < WMAX; ++a) {
     if (a < w) {
       wx[a] = __ldg(&d.w_x[static_cast<size_t>(a) * d.Ppad + j]);
-      wy[a] = __ldg(&d.w_y[static_cast<size_t>(a) * d.Ppad + j]);
       const int t = ix0 + a;
       ix[a] = t >= m ? t - m : t;
     }
@@ -243,26 +242,32 @@ __global__ void __launch_bounds__(256) k_w_sep(OpDev<R> d, int B, const cplx<R>*
     C2 acc[BT];
 #pragma unroll
     for (int q = 0; q < BT; ++q) acc[q] = czero<C2>();
+    // RU grid rows per step: RU*w gathers in flight per thread (registers vs. occupancy)
+#pragma unroll 1
+    for (int bb0 = 0; bb0 < w; bb0 += RU) {
 #pragma unroll
-    for (int bb = 0; bb < WMAX; ++bb) {
-      if (bb < w) {
-        const int t = iy0 + bb;
-        const size_t rowoff = static_cast<size_t>(t >= m ? t - m : t) * m;
+      for (int k = 0; k < RU; ++k) {
+        const int bb = bb0 + k;
+        if (bb < w) {
+          const R wyv = __ldg(&d.w_y[static_cast<size_t>(bb) * d.Ppad + j]);
+          const int t = iy0 + bb;
+          const size_t rowoff = static_cast<size_t>(t >= m ? t - m : t) * m;
 #pragma unroll
-        for (int q = 0; q < BT; ++q) {
-          if (b0 + q < B) {
-            const C2* row = grid + G * (b0 + q) + rowoff;
-            C2 ra = czero<C2>();
+          for (int q = 0; q < BT; ++q) {
+            if (b0 + q < B) {
+              const C2* row = grid + G * (b0 + q) + rowoff;
+              C2 ra = czero<C2>();
 #pragma unroll
-            for (int a = 0; a < WMAX; ++a) {
-              if (a < w) {
-                const C2 gv = row[ix[a]];
-                ra.x += wx[a] * gv.x;
-                ra.y += wx[a] * gv.y;
+              for (int a = 0; a < WMAX; ++a) {
+                if (a < w) {
+                  const C2 gv = row[ix[a]];
+                  ra.x += wx[a] * gv.x;
+                  ra.y += wx[a] * gv.y;
+                }
               }
+              acc[q].x += wyv * ra.x;
+              acc[q].y += wyv * ra.y;
             }
-            acc[q].x += wy[bb] * ra.x;
-            acc[q].y += wy[bb] * ra.y;
           }
         }
       }
@@ -828,12 +833,14 @@ void launch_w(const OpDev<R>& d, int B, const cplx<R>* grid, cplx<R>* samples, c
   const int blocks = (d.Ppad + threads - 1) / threads;
   if (d.w_sep) {
     // compile-time window bound: registers scale with it (6/7 are the configs' windows)
+    // one grid row (w gathers) per step: rows-in-flight 1, 2, 3 and w measured equal on B200
+    // (c2 8.8-9.2 us, c3 16-19 us); 1 needs the fewest registers
     auto go = [&](auto WC) {
       constexpr int WM = decltype(WC)::value;
       if (B >= 2)
-        CK_LAUNCH(launch_k(k_w_sep<2, WM, R>, blocks, threads, 0, st, d, B, grid, samples, skip));
+        CK_LAUNCH(launch_k(k_w_sep<2, WM, 1, R>, blocks, threads, 0, st, d, B, grid, samples, skip));
       else
-        CK_LAUNCH(launch_k(k_w_sep<1, WM, R>, blocks, threads, 0, st, d, B, grid, samples, skip));
+        CK_LAUNCH(launch_k(k_w_sep<1, WM, 1, R>, blocks, threads, 0, st, d, B, grid, samples, skip));
     };
     if (d.w <= 6)
       go(std::integral_constant<int, 6>{});
