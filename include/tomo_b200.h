@@ -105,6 +105,27 @@ int tomo_op_create(const tomo_geom_desc* geom, const tomo_op_desc* desc, tomo_op
 void tomo_op_destroy(tomo_op* op);
 int tomo_op_get_info(const tomo_op* op, tomo_op_info* info);
 
+/* ---- the reference's on-disk operators, TOMOSPM1 (save_sparse / load_sparse,
+ * proj/src/sparse.cpp:68-141; cache keying bench.cpp:62-114) ---- */
+typedef struct tomo_tspm_meta {
+  int64_t rows, cols, nnz;
+  int symmetric;
+  int n, m_sp;          /* provenance trailer (SparseOperator::Meta, sparse.hpp:20-28) */
+  double tau;
+  int angle_count, d, r; /* r = 0: Gram B*B (fused); r >= 1: surrogate T */
+} tomo_tspm_meta;
+/* load_sparse + SparseOperator::validate of `path` (no GPU needed). */
+int tomo_tspm_info(const char* path, tomo_tspm_meta* info);
+/* make_fused_backend / make_surrogate_backend with the sparse operator read from a TOMOSPM1
+ * file (bench.cpp:78-114 load_or_build_sparse): desc->backend TOMO_BACKEND_FUSED takes a Gram,
+ * TOMO_BACKEND_SURROGATE a surrogate T (radius and truncation from the file). The trailer must
+ * match the geometry (meta_matches, bench.cpp:78-84) -> TOMO_ERR_CONFIG otherwise; unreadable
+ * or truncated files -> TOMO_ERR_IO. */
+int tomo_op_create_tspm(const tomo_geom_desc* geom, const tomo_op_desc* desc, const char* path, tomo_op** out);
+/* save_sparse of the op's Gram (fused) or surrogate T in the reference's layout, with the
+ * trailer {n, m_sp, tau, angle_count, d = angle_subsample_d, r}. */
+int tomo_op_save_tspm(const tomo_op* op, const char* path, int angle_subsample_d);
+
 /* apply_normal (normal_ops.hpp:65): complex n^2 -> complex n^2, batch slices. */
 int tomo_apply_normal(tomo_op* op, const void* in, void* out, int batch, void* stream);
 /* apply_normal_real (normal_ops.hpp:69): Re(N u) for real u (surrogate: T u). */

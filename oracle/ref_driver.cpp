@@ -20,6 +20,7 @@
 #include "tomo/normal_ops.hpp"
 #include "tomo/nufft.hpp"
 #include "tomo/solver.hpp"
+#include "tomo/sparse.hpp"
 
 using namespace tomo;
 
@@ -307,6 +308,28 @@ int ref_synthesize(int n, int A, int m_sp, double tau, const double* phantom, do
   Vector v(Eigen::Index(n) * n);
   for (Eigen::Index i = 0; i < v.size(); ++i) v[i] = phantom[i];
   put(synthesize_data(Image(n, v), s.grid, s.params, sigma, seed), samples);
+  REF_CATCH
+}
+
+// The reference's own on-disk operators (TOMOSPM1, sparse.cpp:68-106): the Gram of
+// make_fused_backend and the surrogate T of build_surrogate, written by save_sparse.
+int ref_save_btb(int n, int A, int m_sp, double tau, const char* path) {
+  REF_TRY
+  auto s = make_setup(n, A, m_sp, tau);
+  NormalBackend b = make_fused_backend(s.transform);
+  save_sparse(*b.btb, path);
+  REF_CATCH
+}
+
+int ref_save_surrogate(int n, int A, int m_sp, double tau, int r, int euclidean, const char* path) {
+  REF_TRY
+  auto s = make_setup(n, A, m_sp, tau);
+  NormalBackend fused = make_direct_backend(s.transform);
+  fused.kind = BackendKind::fused;
+  SurrogateConfig cfg;
+  cfg.radius_r = r;
+  cfg.euclidean = euclidean != 0;
+  save_sparse(build_surrogate(fused, cfg), path);
   REF_CATCH
 }
 

@@ -46,6 +46,8 @@ def lib():
                                                C.c_void_p]
         _LIB.ref_shepp_logan.argtypes = [C.c_int, C.c_void_p]
         _LIB.ref_set_nb.argtypes = [C.c_int]
+        _LIB.ref_save_btb.argtypes = [C.c_int, C.c_int, C.c_int, d, C.c_char_p]
+        _LIB.ref_save_surrogate.argtypes = [C.c_int, C.c_int, C.c_int, d, C.c_int, C.c_int, C.c_char_p]
         _LIB.ref_synthesize.argtypes = [C.c_int, C.c_int, C.c_int, d, C.c_void_p, d, C.c_uint64, C.c_void_p]
     return _LIB
 
@@ -117,6 +119,14 @@ class Ref:
 
     def btb_nnz(self):
         return int(lib().ref_btb_nnz(*self._a))
+
+    def save_btb(self, path):
+        """make_fused_backend + save_sparse: the reference's TOMOSPM1 Gram file."""
+        _check(lib().ref_save_btb(*self._a, str(path).encode()))
+
+    def save_surrogate(self, path, r, euclidean=False):
+        """build_surrogate + save_sparse: the reference's TOMOSPM1 surrogate T file."""
+        _check(lib().ref_save_surrogate(*self._a, r, int(euclidean), str(path).encode()))
 
     def surrogate_stencil(self, r):
         out = np.zeros((2 * r + 1, 2 * r + 1))

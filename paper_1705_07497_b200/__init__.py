@@ -7,12 +7,12 @@ this package is the Python mirror of the reference's operator/solver API.
 from .tomo import (  # noqa: F401
     CgStats, ConfigError, CudaError, Error, Geometry, IoError, NormalBackend, NumericalError, SolveTrace,
     SolverConfig, apply_normal, apply_normal_real, generate_shepp_logan, grad, grad_adjoint, kernel_launches,
-    make_direct_backend, make_fused_backend, make_surrogate_backend, nccl_unique_id, radial_density_weights, random_ellipses, shrink,
+    make_direct_backend, make_fused_backend, make_surrogate_backend, nccl_unique_id, load_sparse_info, radial_density_weights, random_ellipses, shrink,
     split_bregman_tv, tikhonov_solve,
 )
 
 __all__ = [
-    "Geometry", "NormalBackend", "SolverConfig", "SolveTrace", "CgStats", "make_direct_backend", "make_fused_backend",
+    "Geometry", "NormalBackend", "SolverConfig", "SolveTrace", "CgStats", "make_direct_backend", "make_fused_backend", "load_sparse_info",
     "make_surrogate_backend", "apply_normal", "apply_normal_real", "split_bregman_tv", "tikhonov_solve",
     "grad", "grad_adjoint", "shrink", "generate_shepp_logan", "random_ellipses", "radial_density_weights",
     "nccl_unique_id", "kernel_launches", "Error", "ConfigError", "NumericalError", "IoError", "CudaError",

@@ -72,6 +72,12 @@ class CpConfig(C.Structure):
                 ("sigma_cp", C.c_double), ("theta", C.c_double), ("iters", C.c_int), ("cg_steps", C.c_int)]
 
 
+class TspmMeta(C.Structure):
+    _fields_ = [("rows", C.c_int64), ("cols", C.c_int64), ("nnz", C.c_int64), ("symmetric", C.c_int),
+                ("n", C.c_int), ("m_sp", C.c_int), ("tau", C.c_double), ("angle_count", C.c_int),
+                ("d", C.c_int), ("r", C.c_int)]
+
+
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p, C.c_void_p)
 
 VP = C.c_void_p
@@ -82,6 +88,9 @@ EXPORTS = {
     "tomo_op_create": (C.c_int, [C.POINTER(GeomDesc), C.POINTER(OpDesc), C.POINTER(VP)]),
     "tomo_op_destroy": (None, [VP]),
     "tomo_op_get_info": (C.c_int, [VP, C.POINTER(OpInfo)]),
+    "tomo_tspm_info": (C.c_int, [C.c_char_p, C.POINTER(TspmMeta)]),
+    "tomo_op_create_tspm": (C.c_int, [C.POINTER(GeomDesc), C.POINTER(OpDesc), C.c_char_p, C.POINTER(VP)]),
+    "tomo_op_save_tspm": (C.c_int, [VP, C.c_char_p, C.c_int]),
     "tomo_apply_normal": (C.c_int, [VP, VP, VP, C.c_int, VP]),
     "tomo_apply_normal_real": (C.c_int, [VP, VP, VP, C.c_int, VP]),
     "tomo_forward": (C.c_int, [VP, VP, VP, C.c_int, VP]),

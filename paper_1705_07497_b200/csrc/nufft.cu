@@ -722,6 +722,7 @@ int choose_rpc(int T, int m, int rows_per_slice, int B, size_t elem, bool transp
   int rpc = std::max(min_rpc, std::max(1, 128 / T));
   while (rpc > 1 && (rpc * T > kFftThreads || static_cast<size_t>(rpc) * padded_len(m) * elem > 110 * 1024)) rpc >>= 1;
   while (rpc > min_rpc && rpc * T > 256 && static_cast<int64_t>((rows_per_slice + rpc - 1) / rpc) * B < 2 * 148) rpc >>= 1;
+  while (rpc > 1 && rpc > rows_per_slice) rpc >>= 1;  // small grids (m = 32): never more rows than exist
   return std::max(rpc, 1);
 }
 

@@ -29,6 +29,7 @@
 
 #include "../../include/tomo_b200.h"
 #include "kernels.h"
+#include "tspm.h"
 
 namespace tomo_b200 {
 
@@ -41,6 +42,10 @@ struct NumericalError : std::runtime_error {
 struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+struct IoError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+using TspmIO = Tspm<IoError, ConfigError>;
 
 thread_local std::string g_err;
 std::atomic<int64_t> g_launches{0};
@@ -266,6 +271,7 @@ struct tomo_op {
   int n_tasks = 0, n_heavy = 0, n_slots = 0;
   Raw apod, tw, wcols, wvals, wbase, wxs, wys, wtent, wttasks, wtperm, wtheavy, wtslotheavy;
   TaskSet gram;  // fused backend only
+  const TspmFile* src = nullptr;  // during tomo_op_create_tspm: the loaded Gram / surrogate T
   int w_sep = 1;  // W storage used by the interpolation kernel (TOMO_W_FORMAT=ell selects SELL-32)
   Scratch sc;
   // surrogate
@@ -469,16 +475,11 @@ struct TaskBuilder {
 // (normal_ops.cpp:53-173): entry (u, v) = sum_j W[j][u] W[j][v]; row u reaches the nodes within
 // w-1 per axis (band 2w-1). Accumulated in fp64 with a dense band per node over blocks of grid
 // rows, samples in ascending order and the reference's product association
-// (wx[a]wx[a2]) * (wy[b]wy[b2]), exact zeros dropped; emitted straight into task tables.
-template <typename R>
-void build_gram(tomo_op* op, const Plan& pl) {
-  const Geom& g = op->g;
+// (wx[a]wx[a2]) * (wy[b]wy[b2]), exact zeros dropped. Emits one grid row iy at a time:
+// sink(iy, roff[m+1], col (node iy'*m+ix'), val) with node ix's entries at [roff[ix], roff[ix+1]).
+template <typename Sink>
+void gram_rows(const Geom& g, const Plan& pl, Sink&& sink) {
   const int m = g.m, w = g.w, band = 2 * w - 1, band2 = band * band;
-  const int64_t cap = op->desc.mem_cap_bytes > 0 ? op->desc.mem_cap_bytes : (int64_t(8) << 30);
-  const int64_t est = op->wt_rows * static_cast<int64_t>(band2) * 16;
-  if (est > cap)
-    throw ConfigError("build_btb: estimated " + std::to_string(est >> 20) +
-                      " MiB exceeds cap; raise the cap or use a smaller m_sp");
   const int64_t lines_budget = std::max<int64_t>(1, (int64_t(128) << 20) / (static_cast<int64_t>(m) * band2 * 8));
   const int lines = static_cast<int>(std::min<int64_t>(lines_budget, m));
   // samples bucketed by the first grid row of their window (ascending j within a bucket)
@@ -500,11 +501,9 @@ void build_gram(tomo_op* op, const Plan& pl) {
   std::vector<int> list;
   std::vector<int64_t> roff(m + 1);
   std::vector<int32_t> rcol;
-  std::vector<R> rval;
+  std::vector<double> rval;
   rcol.reserve(static_cast<size_t>(m) * band2);
   rval.reserve(static_cast<size_t>(m) * band2);
-  TaskBuilder<R> tb(m, kWtMaxChunks, op->wt_rows * band2);
-  int64_t nnz = 0;
   for (int y0 = 0; y0 < m; y0 += lines) {
     const int y1 = std::min(m, y0 + lines);
     std::fill(acc.begin(), acc.begin() + static_cast<size_t>(y1 - y0) * m * band2, 0.0);
@@ -553,16 +552,19 @@ void build_gram(tomo_op* op, const Plan& pl) {
             const double v = cell[dy * band + dx];
             if (v != 0.0) {
               rcol.push_back(cy * m + wrapi(ix + dx - (w - 1), m));
-              rval.push_back(static_cast<R>(v));
+              rval.push_back(v);
             }
           }
         }
         roff[ix + 1] = static_cast<int64_t>(rcol.size());
       }
-      nnz += static_cast<int64_t>(rcol.size());
-      tb.add_row(iy, roff.data(), rcol.data(), rval.data());
+      sink(iy, roff.data(), rcol.data(), rval.data());
     }
   }
+}
+
+template <typename R>
+void gram_upload(tomo_op* op, TaskBuilder<R>& tb, int64_t nnz) {
   tb.finish();
   TaskSet& ts = op->gram;
   ts.n_tasks = static_cast<int>(tb.tasks.size());
@@ -571,8 +573,110 @@ void build_gram(tomo_op* op, const Plan& pl) {
   ts.slots = tb.chunks * 32;
   ts.nnz = nnz;
   ts.bytes = ts.slots * static_cast<int64_t>(sizeof(WtEnt<R>)) + static_cast<int64_t>(ts.n_tasks) * 16 +
-             static_cast<int64_t>(m) * m * 2;
+             static_cast<int64_t>(op->g.m) * op->g.m * 2;
   tb.upload(ts.ent, ts.tasks, ts.perm, ts.heavy, ts.slot_heavy);
+}
+
+template <typename R>
+void build_gram(tomo_op* op, const Plan& pl) {
+  const Geom& g = op->g;
+  const int m = g.m, band = 2 * g.w - 1, band2 = band * band;
+  const int64_t cap = op->desc.mem_cap_bytes > 0 ? op->desc.mem_cap_bytes : (int64_t(8) << 30);
+  const int64_t est = op->wt_rows * static_cast<int64_t>(band2) * 16;
+  if (est > cap)
+    throw ConfigError("build_btb: estimated " + std::to_string(est >> 20) +
+                      " MiB exceeds cap; raise the cap or use a smaller m_sp");
+  TaskBuilder<R> tb(m, kWtMaxChunks, op->wt_rows * band2);
+  std::vector<R> rv;
+  int64_t nnz = 0;
+  gram_rows(g, pl, [&](int iy, const int64_t* roff, const int32_t* rcol, const double* rval) {
+    rv.assign(rval, rval + roff[m]);
+    tb.add_row(iy, roff, rcol, rv.data());
+    nnz += roff[m];
+  });
+  gram_upload<R>(op, tb, nnz);
+}
+
+// Reference cache provenance (bench.cpp:78-84 meta_matches): n, m_sp, tau, angle count, r.
+void check_tspm_meta(const tomo_op* op, const TspmFile& t, bool gram) {
+  const Geom& g = op->g;
+  if (g.lo != -g.hi) throw ConfigError("TOMOSPM1: the reference format needs a symmetric window [-m_sp, m_sp]");
+  if (g.nb != g.n || g.R != 2) throw ConfigError("TOMOSPM1: the reference format has n_b = n and R = 2");
+  if (op->sharded()) throw ConfigError("TOMOSPM1: operators are whole-geometry (not angle shards)");
+  const TspmMeta& mt = t.meta;
+  if (mt.n != g.n || mt.m_sp != g.hi || mt.tau != g.tau || mt.angle_count != g.A || (gram ? mt.r != 0 : mt.r < 1))
+    throw ConfigError("TOMOSPM1: cache metadata mismatch (n, m_sp, tau, angle count or r)");
+  const int64_t side = gram ? static_cast<int64_t>(g.m) * g.m : static_cast<int64_t>(g.n) * g.n;
+  if (t.rows != side || t.cols != side) throw ConfigError("TOMOSPM1: operator size does not match the geometry");
+}
+
+// Gram from a reference cache file: row tx*m+ty of the reference layout is node ty*m+tx here.
+template <typename R>
+void gram_from_tspm(tomo_op* op, const TspmFile& t) {
+  check_tspm_meta(op, t, true);
+  const int m = op->g.m;
+  TaskBuilder<R> tb(m, kWtMaxChunks, t.nnz());
+  std::vector<int64_t> roff(m + 1);
+  std::vector<int32_t> rcol;
+  std::vector<R> rval;
+  for (int iy = 0; iy < m; ++iy) {
+    rcol.clear();
+    rval.clear();
+    roff[0] = 0;
+    for (int ix = 0; ix < m; ++ix) {
+      const int64_t r = static_cast<int64_t>(ix) * m + iy;
+      for (int64_t k = t.off[r]; k < t.off[r + 1]; ++k) {
+        const int c = t.col[k];
+        rcol.push_back((c % m) * m + c / m);
+        rval.push_back(static_cast<R>(t.val[k]));
+      }
+      roff[ix + 1] = static_cast<int64_t>(rcol.size());
+    }
+    tb.add_row(iy, roff.data(), rcol.data(), rval.data());
+  }
+  gram_upload<R>(op, tb, t.nnz());
+}
+
+// The Gram in the reference's CSR layout (row tx*m+ty, columns ascending), fp64, for save_sparse.
+TspmFile gram_to_tspm(const tomo_op* op) {
+  const Geom& g = op->g;
+  const int m = g.m;
+  const int64_t G = static_cast<int64_t>(m) * m;
+  const Plan pl = make_plan(g);
+  // node lists in this layout (iy-major), then re-emitted ix-major with sorted columns
+  std::vector<int64_t> noff(G + 1, 0);
+  std::vector<int32_t> col;
+  std::vector<double> val;
+  gram_rows(g, pl, [&](int iy, const int64_t* roff, const int32_t* rcol, const double* rval) {
+    const int64_t base = static_cast<int64_t>(col.size());
+    for (int ix = 0; ix < m; ++ix) noff[static_cast<int64_t>(iy) * m + ix + 1] = base + roff[ix + 1];
+    for (int64_t k = 0; k < roff[m]; ++k) {
+      const int c = rcol[k];
+      col.push_back((c % m) * m + c / m);
+      val.push_back(rval[k]);
+    }
+  });
+  TspmFile t;
+  t.rows = t.cols = G;
+  t.symmetric = true;
+  t.off.reserve(G + 1);
+  t.off.push_back(0);
+  t.col.reserve(col.size());
+  t.val.reserve(val.size());
+  std::vector<std::pair<int32_t, double>> row;
+  for (int tx = 0; tx < m; ++tx)
+    for (int ty = 0; ty < m; ++ty) {
+      const int64_t node = static_cast<int64_t>(ty) * m + tx;
+      row.clear();
+      for (int64_t k = noff[node]; k < noff[node + 1]; ++k) row.emplace_back(col[k], val[k]);
+      std::sort(row.begin(), row.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+      for (const auto& e : row) {
+        t.col.push_back(e.first);
+        t.val.push_back(e.second);
+      }
+      t.off.push_back(static_cast<int64_t>(t.val.size()));
+    }
+  return t;
 }
 
 template <typename R>
@@ -685,7 +789,12 @@ void build_tables(tomo_op* op) {
   tb.upload(op->wtent, op->wttasks, op->wtperm, op->wtheavy, op->wtslotheavy);
   op->apod.upload(apod);
   op->tw.upload(tw);
-  if (op->fused()) build_gram<R>(op, pl);
+  if (op->fused()) {
+    if (op->src)
+      gram_from_tspm<R>(op, *op->src);
+    else
+      build_gram<R>(op, pl);
+  }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1027,6 +1136,82 @@ void build_stencil(tomo_op* op, cudaStream_t st) {
     }
 }
 
+// Surrogate T from a reference cache file (build_surrogate's CSR, normal_ops.cpp:266-281): the
+// stencil is read off the centre pixel's row, its support tells Chebyshev from Euclidean
+// truncation, and every row must be exactly the clipped translation of it.
+void stencil_from_tspm(tomo_op* op, const TspmFile& t) {
+  check_tspm_meta(op, t, false);
+  const int n = op->g.n, r = t.meta.r;
+  if (r > 4 || r >= n / 2) throw ConfigError("build_surrogate: radius out of range (GPU supports 1..4)");
+  const int side = 2 * r + 1;
+  double st[81] = {0};
+  bool present[81] = {false};
+  const int64_t c = static_cast<int64_t>(n / 2) * n + n / 2;
+  for (int64_t k = t.off[c]; k < t.off[c + 1]; ++k) {
+    const int di = t.col[k] / n - n / 2, dj = t.col[k] % n - n / 2;
+    if (di < -r || di > r || dj < -r || dj > r) throw ConfigError("TOMOSPM1: surrogate entry outside radius r");
+    st[(di + r) * side + (dj + r)] = t.val[k];
+    present[(di + r) * side + (dj + r)] = true;
+  }
+  bool euclid = false;
+  for (int di = -r; di <= r; ++di)
+    for (int dj = -r; dj <= r; ++dj)
+      if (!present[(di + r) * side + (dj + r)]) euclid = true;
+  for (int di = -r; di <= r; ++di)
+    for (int dj = -r; dj <= r; ++dj)
+      if (present[(di + r) * side + (dj + r)] != (!euclid || di * di + dj * dj <= r * r))
+        throw ConfigError("TOMOSPM1: surrogate support is neither Chebyshev nor Euclidean");
+  int64_t k = 0;
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      const int64_t row = static_cast<int64_t>(i) * n + j;
+      if (t.off[row] != k) throw ConfigError("TOMOSPM1: surrogate T is not a translated stencil");
+      for (int di = -r; di <= r; ++di) {
+        const int ii = i + di;
+        if (ii < 0 || ii >= n) continue;
+        for (int dj = -r; dj <= r; ++dj) {
+          const int jj = j + dj;
+          if (jj < 0 || jj >= n || !present[(di + r) * side + (dj + r)]) continue;
+          if (k >= t.nnz() || t.col[k] != ii * n + jj || t.val[k] != st[(di + r) * side + (dj + r)])
+            throw ConfigError("TOMOSPM1: surrogate T is not a translated stencil");
+          ++k;
+        }
+      }
+    }
+  if (k != t.nnz()) throw ConfigError("TOMOSPM1: surrogate T is not a translated stencil");
+  op->rad = r;
+  op->desc.surrogate_r = r;
+  op->desc.euclidean = euclid ? 1 : 0;
+  for (int q = 0; q < 81; ++q) op->stencil64[q] = q < side * side ? st[q] : 0.0;
+  for (int q = 0; q < side * side; ++q) op->coef.c[q] = st[q];
+}
+
+// build_surrogate's CSR from the op's stencil (same loop order, so same bytes as save_sparse).
+TspmFile surrogate_to_tspm(const tomo_op* op) {
+  const int n = op->g.n, r = op->rad, side = 2 * r + 1;
+  const bool euclid = op->desc.euclidean != 0;
+  TspmFile t;
+  t.rows = t.cols = static_cast<int64_t>(n) * n;
+  t.symmetric = true;
+  t.off.push_back(0);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      for (int di = -r; di <= r; ++di) {
+        const int ii = i + di;
+        if (ii < 0 || ii >= n) continue;
+        for (int dj = -r; dj <= r; ++dj) {
+          const int jj = j + dj;
+          if (jj < 0 || jj >= n) continue;
+          if (euclid && di * di + dj * dj > r * r) continue;
+          t.col.push_back(ii * n + jj);
+          t.val.push_back(op->stencil64[(di + r) * side + (dj + r)]);
+        }
+      }
+      t.off.push_back(static_cast<int64_t>(t.val.size()));
+    }
+  return t;
+}
+
 template <typename R>
 double leak_probe(tomo_op* op, cudaStream_t st) {
   if (op->leak >= 0.0) return op->leak;
@@ -1105,6 +1290,7 @@ void with_prec(tomo_op* op, F&& f) {
   catch (const tomo_b200::ConfigError& e) { return fail(e, TOMO_ERR_CONFIG); }       \
   catch (const tomo_b200::NumericalError& e) { return fail(e, TOMO_ERR_NUMERICAL); } \
   catch (const tomo_b200::CudaError& e) { return fail(e, TOMO_ERR_CUDA); }           \
+  catch (const tomo_b200::IoError& e) { return fail(e, TOMO_ERR_IO); }               \
   catch (const std::bad_alloc& e) { return fail(e, TOMO_ERR_CUDA); }                 \
   catch (const std::exception& e) { return fail(e, TOMO_ERR_CONFIG); }
 
@@ -1120,10 +1306,10 @@ extern "C" {
 const char* tomo_last_error(void) { return g_err.c_str(); }
 int64_t tomo_kernel_launches(void) { return g_launches.load(); }
 
-int tomo_op_create(const tomo_geom_desc* geom, const tomo_op_desc* desc, tomo_op** out) {
-  TOMO_TRY
-  if (!out) throw ConfigError("tomo_op_create: null out");
-  *out = nullptr;
+}  // extern "C"
+
+namespace {
+tomo_op* create_op(const tomo_geom_desc* geom, const tomo_op_desc* desc, const TspmFile* src) {
   tomo_op_desc dd{};
   if (desc) dd = *desc;
   if (dd.max_batch < 1) dd.max_batch = 1;
@@ -1142,16 +1328,86 @@ int tomo_op_create(const tomo_geom_desc* geom, const tomo_op_desc* desc, tomo_op
   op->device = dd.device;
   op->f64 = dd.precision == TOMO_F64;
   op->rsz = op->f64 ? 8 : 4;
+  op->src = src;
   DeviceGuard dg(op->device);
   tomo_op* o = op.get();
   with_prec(o, [&](auto tag) {
     using R = decltype(tag);
     build_tables<R>(o);
     o->ensure_batch(dd.max_batch);
-    if (dd.backend == TOMO_BACKEND_SURROGATE) build_stencil<R>(o, 0);
+    if (dd.backend == TOMO_BACKEND_SURROGATE) {
+      if (src)
+        stencil_from_tspm(o, *src);
+      else
+        build_stencil<R>(o, 0);
+    }
   });
   CK(cudaDeviceSynchronize());
-  *out = op.release();
+  op->src = nullptr;
+  return op.release();
+}
+}  // namespace
+
+extern "C" {
+
+int tomo_op_create(const tomo_geom_desc* geom, const tomo_op_desc* desc, tomo_op** out) {
+  TOMO_TRY
+  if (!out) throw ConfigError("tomo_op_create: null out");
+  *out = nullptr;
+  *out = create_op(geom, desc, nullptr);
+  TOMO_CATCH
+}
+
+int tomo_tspm_info(const char* path, tomo_tspm_meta* info) {
+  TOMO_TRY
+  if (!path || !info) throw ConfigError("tomo_tspm_info: null argument");
+  const TspmFile t = TspmIO::read(path, true);
+  std::memset(info, 0, sizeof(*info));
+  info->rows = t.rows;
+  info->cols = t.cols;
+  info->nnz = t.nnz();
+  info->symmetric = t.symmetric ? 1 : 0;
+  info->n = t.meta.n;
+  info->m_sp = t.meta.m_sp;
+  info->tau = t.meta.tau;
+  info->angle_count = t.meta.angle_count;
+  info->d = t.meta.d;
+  info->r = t.meta.r;
+  TOMO_CATCH
+}
+
+int tomo_op_create_tspm(const tomo_geom_desc* geom, const tomo_op_desc* desc, const char* path, tomo_op** out) {
+  TOMO_TRY
+  if (!out || !path) throw ConfigError("tomo_op_create_tspm: null argument");
+  *out = nullptr;
+  if (!desc || (desc->backend != TOMO_BACKEND_FUSED && desc->backend != TOMO_BACKEND_SURROGATE))
+    throw ConfigError("tomo_op_create_tspm: backend must be fused (Gram) or surrogate (T)");
+  const TspmFile t = TspmIO::read(path, true);
+  *out = create_op(geom, desc, &t);
+  TOMO_CATCH
+}
+
+int tomo_op_save_tspm(const tomo_op* op, const char* path, int angle_subsample_d) {
+  TOMO_TRY
+  if (!op || !path) throw ConfigError("tomo_op_save_tspm: null argument");
+  const Geom& g = op->g;
+  TspmFile t;
+  if (op->desc.backend == TOMO_BACKEND_FUSED) {
+    t = gram_to_tspm(op);
+  } else if (op->desc.backend == TOMO_BACKEND_SURROGATE) {
+    t = surrogate_to_tspm(op);
+  } else {
+    throw ConfigError("tomo_op_save_tspm: the direct backend has no sparse operator to save");
+  }
+  if (g.lo != -g.hi) throw ConfigError("TOMOSPM1: the reference format needs a symmetric window [-m_sp, m_sp]");
+  if (op->sharded()) throw ConfigError("TOMOSPM1: operators are whole-geometry (not angle shards)");
+  t.meta.n = g.n;
+  t.meta.m_sp = g.hi;
+  t.meta.tau = g.tau;
+  t.meta.angle_count = g.A;
+  t.meta.d = angle_subsample_d;
+  t.meta.r = op->desc.backend == TOMO_BACKEND_FUSED ? 0 : op->rad;
+  TspmIO::write(t, path);
   TOMO_CATCH
 }
 

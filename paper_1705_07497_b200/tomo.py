@@ -14,6 +14,7 @@ and back (synchronous). Results come back in the kind that was passed in.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import math
 from dataclasses import dataclass, field
 
@@ -207,7 +208,7 @@ class NormalBackend:
 
     def __init__(self, geom: Geometry, kind: str = "direct", surrogate_r: int = 1, euclidean: bool = False,
                  device: int = 0, angle_block: tuple[int, int] | None = None, max_batch: int = 1,
-                 precision: str = "f32", mem_cap_bytes: int = 0):
+                 precision: str = "f32", mem_cap_bytes: int = 0, tspm: str | None = None):
         if kind not in self._KINDS:
             raise ConfigError(f"unknown backend: {kind}")
         if precision not in ("f32", "f64"):
@@ -222,7 +223,10 @@ class NormalBackend:
                            _lib.F64 if self.f64 else _lib.F32, int(mem_cap_bytes))
         gd = geom._desc()
         h = C.c_void_p()
-        _check(lib().tomo_op_create(C.byref(gd), C.byref(desc), C.byref(h)))
+        if tspm is not None:  # load_or_build_sparse's cached operator (bench.cpp:78-114)
+            _check(lib().tomo_op_create_tspm(C.byref(gd), C.byref(desc), os.fsencode(tspm), C.byref(h)))
+        else:
+            _check(lib().tomo_op_create(C.byref(gd), C.byref(desc), C.byref(h)))
         self._h = h
         self._allreduce_cb = None
 
@@ -377,6 +381,11 @@ class NormalBackend:
                                          by.ctypes.data_as(C.c_void_p), stream))
         return {name: (float(ms[i]), float(by[i])) for i, name in enumerate(_lib.STAGE_NAMES) if by[i] > 0}
 
+    # ---------------------------------------------------------------- on-disk operators
+    def save_sparse(self, path, angle_subsample_d: int = 1):
+        """save_sparse (sparse.cpp:68-106) of the Gram (fused) or surrogate T, TOMOSPM1."""
+        _check(lib().tomo_op_save_tspm(self._h, os.fsencode(path), int(angle_subsample_d)))
+
     # ---------------------------------------------------------------- multi-GPU
     def attach_nccl(self, unique_id: bytes, nranks: int, rank: int):
         _check(lib().tomo_op_attach_nccl(self._h, unique_id, nranks, rank))
@@ -391,6 +400,13 @@ class NormalBackend:
                 return 1
         self._allreduce_cb = _lib.ALLREDUCE_FN(cb)
         _check(lib().tomo_op_set_allreduce(self._h, self._allreduce_cb, None))
+
+
+def load_sparse_info(path) -> dict:
+    """load_sparse (sparse.cpp:108-141) + validate: header and provenance trailer of a TOMOSPM1 file."""
+    m = _lib.TspmMeta()
+    _check(lib().tomo_tspm_info(os.fsencode(path), C.byref(m)))
+    return {k: getattr(m, k) for k, _ in m._fields_}
 
 
 def nccl_unique_id() -> bytes:

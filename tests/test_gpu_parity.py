@@ -50,6 +50,7 @@ GEOMS = {
     "width6_odd_nb": dict(n=64, n_angles=30, n_b=65, win_lo=-2, win_hi=3, tau=3 / 64 ** 2),
     "R4_gl_tau": dict(n=32, n_angles=20, n_b=33, oversample=4, win_lo=-3, win_hi=3,
                       tau=np.pi * 3 / (32 ** 2 * 4 * 3.5)),
+    "n16_m32": dict(n=16, n_angles=10, win_lo=-2, win_hi=2),  # smallest grid (m = 32)
     "n128": dict(n=128, n_angles=50, n_b=129, win_lo=-2, win_hi=3, tau=3 / 128 ** 2),
 }
 
