@@ -193,6 +193,28 @@ template <typename R>
 void launch_fft_rows_test(int m, int rows, const cplx<R>* tw, const cplx<R>* in, cplx<R>* out, bool inverse,
                           cudaStream_t st);
 
+// ---- operator construction on the device (opbuild.cu) ----
+struct BuildArgs {
+  int m, nb, lo, hi, w;
+  int64_t P, Ppad;
+  double tau;
+};
+struct GpuBuildSizes {
+  int64_t chunks = 0;   // W^T chunks (slots / 32)
+  int n_tasks = 0, n_slots = 0, n_heavy = 0;
+  int64_t touched = 0;  // non-empty W^T rows
+};
+struct GpuBuild;
+// plan + separable W (written to base/wx/wy) + W^T structure; returns the table sizes
+template <typename R>
+GpuBuild* gpu_build_begin(const BuildArgs& a, const double* h_cs, const double* h_e3, int* base, R* wx, R* wy,
+                          cudaStream_t st, GpuBuildSizes* sizes);
+// W^T entries / tasks / perm / heavy tables into caller-allocated buffers
+template <typename R>
+void gpu_build_finish(GpuBuild* b, WtEnt<R>* ent, int4* tasks, uint16_t* perm, int4* heavy, int* slot_heavy,
+                      cudaStream_t st);
+void gpu_build_free(GpuBuild* b);
+
 // ---- launchers (solver.cu) ----
 struct StencilCoef {
   double c[81];             // (2r+1)^2 row-major, r <= 4

@@ -1,0 +1,377 @@
+// opbuild.cu — operator construction on the GPU: plan_spreading
+// (proj/src/nufft.cpp:71-101, weights :56-69) and the W / W^T tables of tomo_capi.cu's host
+// build_tables, produced on the device so that setup no longer dominates at large sizes.
+//
+//   k_plan        one thread per slice sample: nearest grid index, e1/e2 recurrence (fp64, the
+//                 host formula with the products rounded exactly as on the host), the separable
+//                 W storage (base node + factor vectors) and the (node, sample) pairs of W^T
+//   radix sorts   (node, sample) pairs -> W^T rows in ascending sample order (= the host fill);
+//                 nodes of every grid row by (count desc, ix) (= the host stable_sort)
+//   k_blocks ...  32-node blocks, chunk offsets, warp tasks (split above kWtMaxChunks), the
+//                 stable longest-first task order, and the chunk-major entry stream
+//
+// The result is the same table layout (and, up to 1-ulp differences of exp(), the same values)
+// as the host build; tests/test_gpu_build.py compares the two.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <memory>
+#include <stdexcept>
+#include <vector>
+#include <string>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace tomo_b200 {
+
+namespace {
+
+#define BK(x)                                                                   \
+  do {                                                                          \
+    const cudaError_t e_ = (x);                                                 \
+    if (e_ != cudaSuccess) throw std::runtime_error(std::string("opbuild: ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  explicit DBuf(size_t count) { alloc(count); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() {
+    if (p) cudaFree(p);
+  }
+  void alloc(size_t count) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = count;
+    BK(cudaMalloc(&p, sizeof(T) * std::max<size_t>(count, 1)));
+  }
+};
+
+__device__ __forceinline__ int wrapd(int i, int m) { return i < 0 ? i + m : (i >= m ? i - m : i); }
+
+__device__ __forceinline__ double reduce_2pi(double v) {
+  const double two_pi = 2.0 * M_PI;
+  double r = fmod(v, two_pi);
+  if (r < 0.0) r += two_pi;
+  if (r >= two_pi) r = 0.0;
+  return r;
+}
+
+// plan + separable W + W^T pairs; j in [0, Ppad)
+template <typename R>
+__global__ void k_plan(BuildArgs a, const double* __restrict__ cs, const double* __restrict__ e3, int* base,
+                       R* wxr, R* wyr, unsigned long long* keys, R* vals, int* cnt) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= a.Ppad) return;
+  const int w = a.w;
+  if (j >= a.P) {
+    base[j] = 0;
+    for (int q = 0; q < w; ++q) {
+      wxr[static_cast<size_t>(q) * a.Ppad + j] = R(0);
+      wyr[static_cast<size_t>(q) * a.Ppad + j] = R(0);
+    }
+    return;
+  }
+  const int al = static_cast<int>(j / a.nb), t = static_cast<int>(j % a.nb);
+  const double c = cs[2 * al], s = cs[2 * al + 1];
+  const double big_m = a.m / 2.0, h = M_PI / big_m;
+  const double k_r = (2.0 * M_PI / a.nb) * (t - a.nb / 2);
+  const double xy[2] = {reduce_2pi(__dmul_rn(k_r, c)), reduce_2pi(__dmul_rn(k_r, s))};
+  const int reach = max(a.hi, -a.lo);
+  double wd[2][64];
+  int i0[2];
+  for (int dd = 0; dd < 2; ++dd) {
+    int mj = static_cast<int>(floor(xy[dd] / h));
+    if (mj >= a.m) mj = a.m - 1;
+    const double xi = __dsub_rn(xy[dd], __dmul_rn(h, static_cast<double>(mj)));  // no FMA contraction
+    const double f1 = exp(-__dmul_rn(xi, xi) / (4.0 * a.tau));
+    const double f2 = exp(__dmul_rn(xi, M_PI) / (big_m * 2.0 * a.tau));
+    const double f2inv = 1.0 / f2;
+    double* wv = wd[dd];
+    wv[-a.lo] = f1;
+    double p = f1, q = f1;
+    for (int l = 1; l <= reach; ++l) {
+      p = __dmul_rn(p, f2);
+      q = __dmul_rn(q, f2inv);
+      if (l <= a.hi) wv[l - a.lo] = __dmul_rn(p, e3[l - a.lo]);
+      if (-l >= a.lo) wv[-l - a.lo] = __dmul_rn(q, e3[-l - a.lo]);
+    }
+    i0[dd] = wrapd(mj + a.lo, a.m);
+  }
+  base[j] = i0[0] | (i0[1] << 16);
+  for (int q = 0; q < w; ++q) {
+    wxr[static_cast<size_t>(q) * a.Ppad + j] = static_cast<R>(wd[0][q]);
+    wyr[static_cast<size_t>(q) * a.Ppad + j] = static_cast<R>(wd[1][q]);
+  }
+  // W^T pairs: entry (a, b) of row j -> node ((iy0+b) mod m, (ix0+a) mod m), value wx[a]wy[b]
+  const size_t e0 = static_cast<size_t>(j) * w * w;
+  for (int qa = 0; qa < w; ++qa) {
+    const int ix = wrapd(i0[0] + qa, a.m);
+    for (int qb = 0; qb < w; ++qb) {
+      const int iy = wrapd(i0[1] + qb, a.m);
+      const int node = iy * a.m + ix;
+      keys[e0 + qa * w + qb] = (static_cast<unsigned long long>(node) << 32) | static_cast<unsigned long long>(j);
+      vals[e0 + qa * w + qb] = static_cast<R>(__dmul_rn(wd[0][qa], wd[1][qb]));
+      atomicAdd(&cnt[node], 1);
+    }
+  }
+}
+
+// per node: key (iy, count descending, ix) for the per-row stable order; touched-node count
+__global__ void k_node_keys(int m, int maxc, const int* __restrict__ cnt, unsigned long long* keys,
+                            unsigned long long* touched) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t G = static_cast<int64_t>(m) * m;
+  if (i >= G) return;
+  const int iy = static_cast<int>(i / m), ix = static_cast<int>(i % m);
+  const int c = cnt[i];
+  keys[i] = (static_cast<unsigned long long>(iy) << 32) | (static_cast<unsigned long long>(maxc - c) << 16) |
+            static_cast<unsigned long long>(ix);
+  if (c > 0) atomicAdd(touched, 1ull);
+}
+
+// per 32-node block: perm, chunk count L, task / slot / heavy counts
+__global__ void k_blocks(int m, int maxch, const unsigned long long* __restrict__ sorted, const int* __restrict__ cnt,
+                         uint16_t* perm, int* L, int* ntask, int* nslot, int* nheavy) {
+  const int64_t bk = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const int64_t G32 = static_cast<int64_t>(m) * m / 32;
+  if (bk >= G32) return;
+  const int ix = static_cast<int>(sorted[bk * 32 + lane] & 0xFFFFull);
+  perm[bk * 32 + lane] = static_cast<uint16_t>(ix);
+  if (lane == 0) {
+    const int iy = static_cast<int>((bk * 32) / m);
+    const int l = cnt[static_cast<int64_t>(iy) * m + ix];
+    L[bk] = l;
+    const int nt = l == 0 ? 0 : (l <= maxch ? 1 : (l + maxch - 1) / maxch);
+    ntask[bk] = nt;
+    nslot[bk] = l > maxch ? nt : 0;
+    nheavy[bk] = l > maxch ? 1 : 0;
+  }
+}
+
+__global__ void k_tasks(int64_t G32, int maxch, const int* __restrict__ L, const int64_t* __restrict__ chunk0,
+                        const int* __restrict__ toff, const int* __restrict__ soff, const int* __restrict__ hoff,
+                        int4* tasks, int* tkey, int4* heavy, int* slot_heavy) {
+  const int64_t bk = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (bk >= G32) return;
+  const int l = L[bk];
+  if (!l) return;
+  const int c0 = static_cast<int>(chunk0[bk]);
+  if (l <= maxch) {
+    tasks[toff[bk]] = make_int4(static_cast<int>(bk), c0, l, -1);
+    tkey[toff[bk]] = maxch - l;
+    return;
+  }
+  const int ns = (l + maxch - 1) / maxch, s0 = soff[bk], h = hoff[bk];
+  heavy[h] = make_int4(static_cast<int>(bk), s0, ns, 0);
+  for (int k = 0; k < ns; ++k) {
+    const int nc = min(maxch, l - k * maxch);
+    tasks[toff[bk] + k] = make_int4(static_cast<int>(bk), c0 + k * maxch, nc, s0 + k);
+    tkey[toff[bk] + k] = maxch - nc;
+    slot_heavy[s0 + k] = h;
+  }
+}
+
+template <typename R>
+__global__ void k_gather_tasks(int n, const int* __restrict__ idx, const int4* __restrict__ in, int4* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = in[idx[i]];
+}
+
+// chunk-major entries: block bk, lane l, chunk k < L; padding re-reads the last sample
+template <typename R>
+__global__ void k_entries(int m, const uint16_t* __restrict__ perm, const int* __restrict__ L,
+                          const int64_t* __restrict__ chunk0, const int* __restrict__ cnt, const int* __restrict__ off,
+                          const unsigned long long* __restrict__ skeys, const R* __restrict__ svals, WtEnt<R>* ent) {
+  const int64_t bk = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const int64_t G32 = static_cast<int64_t>(m) * m / 32;
+  if (bk >= G32) return;
+  const int l = L[bk];
+  if (!l) return;
+  const int64_t row = (bk * 32) / m * m;
+  const int64_t node = row + perm[bk * 32 + lane];
+  const int64_t first = row + perm[bk * 32];
+  const int c = cnt[node];
+  const int o = off[node];
+  int lastj = static_cast<int>((c > 0 ? skeys[o] : skeys[off[first]]) & 0xFFFFFFFFull);
+  for (int k = 0; k < l; ++k) {
+    WtEnt<R> e{};
+    if (k < c) {
+      lastj = static_cast<int>(skeys[o + k] & 0xFFFFFFFFull);
+      e.j = lastj;
+      e.w = svals[o + k];
+    } else {
+      e.j = lastj;
+      e.w = R(0);
+    }
+    ent[(static_cast<size_t>(chunk0[bk]) + k) * 32 + lane] = e;
+  }
+}
+
+int bits_for(uint64_t v) {
+  int b = 1;
+  while ((uint64_t(1) << b) <= v && b < 64) ++b;
+  return b;
+}
+
+}  // namespace
+
+struct GpuBuild {
+  BuildArgs a{};
+  int64_t nnz = 0, G = 0, G32 = 0;
+  DBuf<unsigned long long> skeys;
+  DBuf<int> cnt, off, L, ntask, nslot, nheavy, toff, soff, hoff, tkey, tkey2, tidx, tidx2;
+  DBuf<int64_t> chunk0;
+  DBuf<int4> tasks_raw;
+  DBuf<unsigned char> vals_sorted;  // R values, type-erased
+  DBuf<uint16_t> perm;
+  GpuBuildSizes sz{};
+};
+
+template <typename R>
+GpuBuild* gpu_build_begin(const BuildArgs& a, const double* h_cs, const double* h_e3, int* base, R* wx, R* wy,
+                          cudaStream_t st, GpuBuildSizes* sizes) {
+  auto b = std::make_unique<GpuBuild>();
+  b->a = a;
+  const int m = a.m, w = a.w;
+  b->nnz = a.P * w * w;
+  b->G = static_cast<int64_t>(m) * m;
+  b->G32 = b->G / 32;
+  if (b->nnz >= (int64_t(1) << 31)) throw std::runtime_error("opbuild: W^T too large for 32-bit offsets");
+  const int n_ang = static_cast<int>(a.P / a.nb);
+  DBuf<double> cs(2 * static_cast<size_t>(n_ang)), e3(w);
+  BK(cudaMemcpyAsync(cs.p, h_cs, sizeof(double) * 2 * n_ang, cudaMemcpyHostToDevice, st));
+  BK(cudaMemcpyAsync(e3.p, h_e3, sizeof(double) * w, cudaMemcpyHostToDevice, st));
+  DBuf<unsigned long long> keys(b->nnz);
+  DBuf<R> vals(b->nnz);
+  b->skeys.alloc(b->nnz);
+  b->vals_sorted.alloc(sizeof(R) * b->nnz);
+  b->cnt.alloc(b->G);
+  BK(cudaMemsetAsync(b->cnt.p, 0, sizeof(int) * b->G, st));
+  k_plan<R><<<static_cast<unsigned>((a.Ppad + 127) / 128), 128, 0, st>>>(a, cs.p, e3.p, base, wx, wy, keys.p, vals.p,
+                                                                        b->cnt.p);
+  BK(cudaGetLastError());
+  // W^T rows: sort the (node, sample) pairs; ascending sample order within a node = the host fill
+  const int key_bits = 32 + bits_for(static_cast<uint64_t>(b->G));
+  size_t tmp_bytes = 0;
+  BK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys.p, b->skeys.p, vals.p,
+                                     reinterpret_cast<R*>(b->vals_sorted.p), static_cast<int>(b->nnz), 0, key_bits,
+                                     st));
+  DBuf<unsigned char> tmp(tmp_bytes);
+  BK(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, keys.p, b->skeys.p, vals.p,
+                                     reinterpret_cast<R*>(b->vals_sorted.p), static_cast<int>(b->nnz), 0, key_bits,
+                                     st));
+  b->off.alloc(b->G);
+  tmp_bytes = 0;
+  BK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, b->cnt.p, b->off.p, static_cast<int>(b->G), st));
+  tmp.alloc(tmp_bytes);
+  BK(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, b->cnt.p, b->off.p, static_cast<int>(b->G), st));
+  // per-row node order: (count desc, ix asc) = the host's stable_sort by count
+  const int maxc = 65535;
+  DBuf<unsigned long long> nkeys(b->G), nsorted(b->G), touched(1);
+  BK(cudaMemsetAsync(touched.p, 0, sizeof(unsigned long long), st));
+  k_node_keys<<<static_cast<unsigned>((b->G + 255) / 256), 256, 0, st>>>(m, maxc, b->cnt.p, nkeys.p, touched.p);
+  BK(cudaGetLastError());
+  tmp_bytes = 0;
+  const int nbits = 32 + bits_for(static_cast<uint64_t>(m));
+  BK(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, nkeys.p, nsorted.p, static_cast<int>(b->G), 0, nbits, st));
+  tmp.alloc(tmp_bytes);
+  BK(cub::DeviceRadixSort::SortKeys(tmp.p, tmp_bytes, nkeys.p, nsorted.p, static_cast<int>(b->G), 0, nbits, st));
+  // blocks
+  b->perm.alloc(b->G);
+  b->L.alloc(b->G32);
+  b->ntask.alloc(b->G32);
+  b->nslot.alloc(b->G32);
+  b->nheavy.alloc(b->G32);
+  k_blocks<<<static_cast<unsigned>((b->G32 + 7) / 8), 256, 0, st>>>(m, kWtMaxChunks, nsorted.p, b->cnt.p, b->perm.p,
+                                                                   b->L.p, b->ntask.p, b->nslot.p, b->nheavy.p);
+  BK(cudaGetLastError());
+  b->chunk0.alloc(b->G32 + 1);
+  b->toff.alloc(b->G32 + 1);
+  b->soff.alloc(b->G32 + 1);
+  b->hoff.alloc(b->G32 + 1);
+  auto scan = [&](const int* in, auto* out) {
+    size_t tb = 0;
+    BK(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, static_cast<int>(b->G32), st));
+    DBuf<unsigned char> t2(tb);
+    BK(cub::DeviceScan::ExclusiveSum(t2.p, tb, in, out, static_cast<int>(b->G32), st));
+  };
+  scan(b->L.p, b->chunk0.p);
+  scan(b->ntask.p, b->toff.p);
+  scan(b->nslot.p, b->soff.p);
+  scan(b->nheavy.p, b->hoff.p);
+  // totals = last exclusive sum + last count
+  int64_t c_last = 0;
+  int l_last = 0, t_last = 0, nt_last = 0, s_last = 0, ns_last = 0, h_last = 0, nh_last = 0;
+  unsigned long long tch = 0;
+  BK(cudaMemcpyAsync(&c_last, b->chunk0.p + b->G32 - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  BK(cudaMemcpyAsync(&l_last, b->L.p + b->G32 - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  BK(cudaMemcpyAsync(&t_last, b->toff.p + b->G32 - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  BK(cudaMemcpyAsync(&nt_last, b->ntask.p + b->G32 - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  BK(cudaMemcpyAsync(&s_last, b->soff.p + b->G32 - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  BK(cudaMemcpyAsync(&ns_last, b->nslot.p + b->G32 - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  BK(cudaMemcpyAsync(&h_last, b->hoff.p + b->G32 - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  BK(cudaMemcpyAsync(&nh_last, b->nheavy.p + b->G32 - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  BK(cudaMemcpyAsync(&tch, touched.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  BK(cudaStreamSynchronize(st));
+  b->sz.chunks = c_last + l_last;
+  b->sz.n_tasks = t_last + nt_last;
+  b->sz.n_slots = s_last + ns_last;
+  b->sz.n_heavy = h_last + nh_last;
+  b->sz.touched = static_cast<int64_t>(tch);
+  if (b->sz.chunks > (int64_t(1) << 31) - 1) throw std::runtime_error("opbuild: W^T too large");
+  *sizes = b->sz;
+  return b.release();
+}
+
+template <typename R>
+void gpu_build_finish(GpuBuild* b, WtEnt<R>* ent, int4* tasks, uint16_t* perm, int4* heavy, int* slot_heavy,
+                      cudaStream_t st) {
+  const int m = b->a.m;
+  const int nt = b->sz.n_tasks;
+  DBuf<int4> traw(nt);
+  DBuf<int> tkey(nt), tkey2(nt), tidx(nt), tidx2(nt);
+  k_tasks<<<static_cast<unsigned>((b->G32 + 255) / 256), 256, 0, st>>>(
+      b->G32, kWtMaxChunks, b->L.p, b->chunk0.p, b->toff.p, b->soff.p, b->hoff.p, traw.p, tkey.p, heavy, slot_heavy);
+  BK(cudaGetLastError());
+  if (nt > 0) {
+    // longest tasks first, stable (LSD radix sort) = the host's stable_sort by nchunks desc
+    std::vector<int> iota(nt);
+    for (int i = 0; i < nt; ++i) iota[i] = i;
+    BK(cudaMemcpyAsync(tidx.p, iota.data(), sizeof(int) * nt, cudaMemcpyHostToDevice, st));
+    size_t tb = 0;
+    BK(cub::DeviceRadixSort::SortPairs(nullptr, tb, tkey.p, tkey2.p, tidx.p, tidx2.p, nt, 0,
+                                       bits_for(kWtMaxChunks), st));
+    DBuf<unsigned char> t2(tb);
+    BK(cub::DeviceRadixSort::SortPairs(t2.p, tb, tkey.p, tkey2.p, tidx.p, tidx2.p, nt, 0, bits_for(kWtMaxChunks),
+                                       st));
+    k_gather_tasks<R><<<(nt + 255) / 256, 256, 0, st>>>(nt, tidx2.p, traw.p, tasks);
+    BK(cudaGetLastError());
+    BK(cudaStreamSynchronize(st));  // iota must outlive the copy
+  }
+  BK(cudaMemcpyAsync(perm, b->perm.p, sizeof(uint16_t) * b->G, cudaMemcpyDeviceToDevice, st));
+  k_entries<R><<<static_cast<unsigned>((b->G32 + 7) / 8), 256, 0, st>>>(
+      m, b->perm.p, b->L.p, b->chunk0.p, b->cnt.p, b->off.p, b->skeys.p,
+      reinterpret_cast<const R*>(b->vals_sorted.p), ent);
+  BK(cudaGetLastError());
+  BK(cudaStreamSynchronize(st));
+}
+
+void gpu_build_free(GpuBuild* b) { delete b; }
+
+#define TOMO_INST_BUILD(R)                                                                                     \
+  template GpuBuild* gpu_build_begin<R>(const BuildArgs&, const double*, const double*, int*, R*, R*,         \
+                                        cudaStream_t, GpuBuildSizes*);                                        \
+  template void gpu_build_finish<R>(GpuBuild*, WtEnt<R>*, int4*, uint16_t*, int4*, int*, cudaStream_t);
+
+TOMO_INST_BUILD(float)
+TOMO_INST_BUILD(double)
+
+}  // namespace tomo_b200

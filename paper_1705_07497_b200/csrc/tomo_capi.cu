@@ -679,16 +679,14 @@ TspmFile gram_to_tspm(const tomo_op* op) {
   return t;
 }
 
+// Host build of W (separable + SELL-32 ELL) and W^T (fp64 plan, the reference's recurrence).
 template <typename R>
-void build_tables(tomo_op* op) {
+void build_w_host(tomo_op* op) {
   const Geom& g = op->g;
   const Plan pl = make_plan(g);
   const int w = g.w, w2 = w * w;
-  const int w2pad = (w2 + 3) / 4 * 4;
-  op->nq = w2pad / 4;
-  op->Ppad = static_cast<int>((g.P + 31) / 32 * 32);
+  const int w2pad = op->nq * 4;
   const int m = g.m;
-  op->nnz = g.P * w2;
 
   std::vector<int4> cols(static_cast<size_t>(op->Ppad) * op->nq);
   std::vector<Quad<R>> vals(cols.size());
@@ -753,6 +751,78 @@ void build_tables(tomo_op* op) {
   op->n_heavy = static_cast<int>(tb.heavy.size());
   op->n_slots = tb.slots;
 
+  // separable storage of the same rows: base node + the two factor vectors (SoA)
+  std::vector<int> wbase(op->Ppad, 0);
+  std::vector<R> wxs(static_cast<size_t>(w) * op->Ppad, R(0)), wys(static_cast<size_t>(w) * op->Ppad, R(0));
+  for (int64_t j = 0; j < g.P; ++j) {
+    const int ix0 = wrapi(pl.mjx[j] + g.lo, m), iy0 = wrapi(pl.mjy[j] + g.lo, m);
+    wbase[j] = ix0 | (iy0 << 16);
+    for (int a = 0; a < w; ++a) {
+      wxs[static_cast<size_t>(a) * op->Ppad + j] = static_cast<R>(pl.wx[j * w + a]);
+      wys[static_cast<size_t>(a) * op->Ppad + j] = static_cast<R>(pl.wy[j * w + a]);
+    }
+  }
+  op->wbase.upload(wbase);
+  op->wxs.upload(wxs);
+  op->wys.upload(wys);
+  if (!op->w_sep) {  // the SELL-32 ELL form is uploaded only when selected (TOMO_W_FORMAT=ell)
+    op->wcols.upload(cols);
+    op->wvals.upload(vals);
+  }
+  tb.upload(op->wtent, op->wttasks, op->wtperm, op->wtheavy, op->wtslotheavy);
+}
+
+// Device build of the separable W and of W^T (opbuild.cu): same tables as build_w_host.
+template <typename R>
+void build_w_gpu(tomo_op* op) {
+  const Geom& g = op->g;
+  const int w = g.w, m = g.m;
+  BuildArgs a{m, g.nb, g.lo, g.hi, w, g.P, op->Ppad, g.tau};
+  std::vector<double> cs;
+  for (int k = g.a0; k < g.a1; ++k) {
+    cs.push_back(std::cos(g.angles[k]));
+    cs.push_back(std::sin(g.angles[k]));
+  }
+  const double big_m = m / 2.0;
+  std::vector<double> e3(w);
+  for (int l = g.lo; l <= g.hi; ++l) e3[l - g.lo] = std::exp(-(M_PI * l / big_m) * (M_PI * l / big_m) / (4.0 * g.tau));
+  op->wbase.ensure(sizeof(int) * op->Ppad);
+  op->wxs.ensure(sizeof(R) * w * op->Ppad);
+  op->wys.ensure(sizeof(R) * w * op->Ppad);
+  GpuBuildSizes sz{};
+  std::unique_ptr<GpuBuild, void (*)(GpuBuild*)> b(
+      gpu_build_begin<R>(a, cs.data(), e3.data(), op->wbase.as<int>(), op->wxs.as<R>(), op->wys.as<R>(), 0, &sz),
+      gpu_build_free);
+  op->wt_rows = sz.touched;
+  op->wt_slots = sz.chunks * 32;
+  op->n_tasks = sz.n_tasks;
+  op->n_heavy = sz.n_heavy;
+  op->n_slots = sz.n_slots;
+  op->wtent.ensure(sizeof(WtEnt<R>) * std::max<int64_t>(op->wt_slots, 1));
+  op->wttasks.ensure(sizeof(int4) * std::max(sz.n_tasks, 1));
+  op->wtperm.ensure(sizeof(uint16_t) * static_cast<size_t>(m) * m);
+  op->wtheavy.ensure(sizeof(int4) * std::max(sz.n_heavy, 1));
+  op->wtslotheavy.ensure(sizeof(int) * std::max(sz.n_slots, 1));
+  gpu_build_finish<R>(b.get(), op->wtent.as<WtEnt<R>>(), op->wttasks.as<int4>(), op->wtperm.as<uint16_t>(),
+                      op->wtheavy.as<int4>(), op->wtslotheavy.as<int>(), 0);
+}
+
+template <typename R>
+void build_tables(tomo_op* op) {
+  const Geom& g = op->g;
+  const int w = g.w, m = g.m;
+  op->nq = (w * w + 3) / 4;
+  op->Ppad = static_cast<int>((g.P + 31) / 32 * 32);
+  op->nnz = g.P * w * w;
+  const char* fmt = std::getenv("TOMO_W_FORMAT");
+  op->w_sep = (fmt && std::string(fmt) == "ell") ? 0 : 1;
+  // W / W^T are built on the device unless the SELL-32 ELL form of W is requested (host) or
+  // TOMO_BUILD=host asks for the host build (kept as the reference for tests/test_gpu_build.py)
+  const char* bld = std::getenv("TOMO_BUILD");
+  if (op->w_sep && !(bld && std::string(bld) == "host"))
+    build_w_gpu<R>(op);
+  else
+    build_w_host<R>(op);
   // deapodisation a[t]/m (nufft.cpp:204-227 with the 1/m per-axis FFT scale folded in)
   std::vector<R> apod(g.n);
   const double root = std::sqrt(M_PI / g.tau);
@@ -766,34 +836,13 @@ void build_tables(tomo_op* op) {
     tw[k].x = static_cast<R>(std::cos(ang));
     tw[k].y = static_cast<R>(std::sin(ang));
   }
-  // separable storage of the same rows: base node + the two factor vectors (SoA)
-  std::vector<int> wbase(op->Ppad, 0);
-  std::vector<R> wxs(static_cast<size_t>(w) * op->Ppad, R(0)), wys(static_cast<size_t>(w) * op->Ppad, R(0));
-  for (int64_t j = 0; j < g.P; ++j) {
-    const int ix0 = wrapi(pl.mjx[j] + g.lo, m), iy0 = wrapi(pl.mjy[j] + g.lo, m);
-    wbase[j] = ix0 | (iy0 << 16);
-    for (int a = 0; a < w; ++a) {
-      wxs[static_cast<size_t>(a) * op->Ppad + j] = static_cast<R>(pl.wx[j * w + a]);
-      wys[static_cast<size_t>(a) * op->Ppad + j] = static_cast<R>(pl.wy[j * w + a]);
-    }
-  }
-  const char* fmt = std::getenv("TOMO_W_FORMAT");
-  op->w_sep = (fmt && std::string(fmt) == "ell") ? 0 : 1;
-  op->wbase.upload(wbase);
-  op->wxs.upload(wxs);
-  op->wys.upload(wys);
-  if (!op->w_sep) {  // the SELL-32 ELL form is uploaded only when selected (TOMO_W_FORMAT=ell)
-    op->wcols.upload(cols);
-    op->wvals.upload(vals);
-  }
-  tb.upload(op->wtent, op->wttasks, op->wtperm, op->wtheavy, op->wtslotheavy);
   op->apod.upload(apod);
   op->tw.upload(tw);
   if (op->fused()) {
     if (op->src)
       gram_from_tspm<R>(op, *op->src);
     else
-      build_gram<R>(op, pl);
+      build_gram<R>(op, make_plan(g));
   }
 }
 
