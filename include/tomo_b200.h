@@ -183,6 +183,14 @@ typedef struct tomo_sb_trace { /* SolveTrace (solver.hpp:67-80), per slice */
  * max_iters (or NULL); trace: host, batch entries (or NULL). Synchronizes `stream`. */
 int tomo_split_bregman(tomo_op* op, const tomo_sb_config* cfg, const void* slice_data, void* mu, int batch,
                        double* update_l1, tomo_sb_trace* trace, void* stream);
+/* The same solve with the reference's full per-iteration trace (SolveTrace, solver.hpp:67-80;
+ * record_reference, solver.cpp:291-294): update_l1 and rel_l1_err (batch x max_iters, host;
+ * rel_l1_err needs `reference`, batch x n^2 of the op's element type, else NULL), t_total_s and
+ * t_cg_s (max_iters, host; CUDA-event times from the start of the Bregman loop, the CG part
+ * accumulated like t_cg). One CG graph and one update graph per iteration. */
+int tomo_split_bregman_record(tomo_op* op, const tomo_sb_config* cfg, const void* slice_data, void* mu, int batch,
+                              const void* reference, double* update_l1, double* rel_l1_err, double* t_total_s,
+                              double* t_cg_s, tomo_sb_trace* trace, void* stream);
 
 /* ---- tikhonov_solve with K = identity (solver.cpp:309-337) at a fixed step count:
  * cg_solve(alpha N + I, alpha Re(F_NU f), 0, steps, rel_tol). */

@@ -100,6 +100,7 @@ EXPORTS = {
     "tomo_backproject": (C.c_int, [VP, C.c_double, C.c_int, VP, VP, C.c_int, VP]),
     "tomo_cg": (C.c_int, [VP, C.POINTER(System), VP, VP, VP, C.c_int, C.c_double, C.c_int, VP, VP]),
     "tomo_split_bregman": (C.c_int, [VP, C.POINTER(SbConfig), VP, VP, C.c_int, VP, VP, VP]),
+    "tomo_split_bregman_record": (C.c_int, [VP, C.POINTER(SbConfig), VP, VP, C.c_int, VP, VP, VP, VP, VP, VP, VP]),
     "tomo_tikhonov": (C.c_int, [VP, C.c_double, VP, VP, C.c_int, C.c_double, C.c_int, VP]),
     "tomo_chambolle_pock": (C.c_int, [VP, C.POINTER(CpConfig), VP, VP, C.c_int, VP]),
     "tomo_op_set_allreduce": (C.c_int, [VP, ALLREDUCE_FN, VP]),

@@ -115,7 +115,7 @@ struct SliceScalars {
   int steps_run;
   int frozen;         // split Bregman stopped on tolerance: later iterations pass through
   int sb_iters;       // split Bregman iterations run
-  int pad_;
+  int logged;         // iterations already appended to the recorded log (k_sb_log)
   unsigned counter[4];
 };
 
@@ -244,6 +244,9 @@ template <typename R>
 void launch_dot(int n, int B, const R* x, const R* y, const Reduce& red, cudaStream_t st);
 template <typename R>
 void launch_leak(int64_t len, const cplx<R>* v, const Reduce& red, cudaStream_t st);
+template <typename R>
+void launch_sb_log(int n, int B, const R* mu, const R* ref, double* upd_log, double* rel_log, const Reduce& red,
+                   cudaStream_t st);
 template <typename R>
 void launch_grad(int n, int B, const R* u, R* gx, R* gy, cudaStream_t st);
 template <typename R>

@@ -405,6 +405,37 @@ __global__ void __launch_bounds__(kVecThreads) k_dot(int64_t L, const R* __restr
     red.sc[b].dot = t0;
 }
 
+// Per-iteration split-Bregman log for the recorded (host-timed) driver: ||mu - ref||_1 and
+// ||ref||_1 (relative_l1_error, image.cpp:69-76) reduced in fixed order; the last block appends
+// update_l1 / rel_l1 at the slice's iteration count if an iteration ran since the last log.
+template <typename R>
+__global__ void __launch_bounds__(kVecThreads) k_sb_log(int64_t L, int B, const R* __restrict__ mu,
+                                                        const R* __restrict__ ref, double* upd_log, double* rel_log,
+                                                        Reduce red) {
+  __shared__ double scratch[32];
+  const int b = blockIdx.y;
+  const size_t off = static_cast<size_t>(b) * L;
+  double num = 0.0, den = 0.0;
+  if (ref)
+    for (int64_t i = gtid(); i < L; i += gstride()) {
+      const double r = ref[off + i];
+      num += fabs(static_cast<double>(mu[off + i]) - r);
+      den += fabs(r);
+    }
+  double t0, t1;
+  double* part = red.part + static_cast<size_t>(b) * MAX_PART_BLOCKS * 2;
+  if (reduce2_last(num, den, part, gridDim.x, blockIdx.x, &red.sc[b].counter[3], scratch, t0, t1) &&
+      threadIdx.x == 0) {
+    SliceScalars& sc = red.sc[b];
+    if (sc.sb_iters > sc.logged) {
+      const size_t it = static_cast<size_t>(sc.sb_iters - 1);
+      upd_log[it * B + b] = sc.upd;
+      if (rel_log) rel_log[it * B + b] = t1 > 0.0 ? t0 / t1 : 0.0;
+      sc.logged = sc.sb_iters;
+    }
+  }
+}
+
 template <typename R>
 __global__ void __launch_bounds__(kVecThreads) k_leak(int64_t len, const cplx<R>* __restrict__ v, Reduce red) {
   __shared__ double scratch[32];
@@ -524,6 +555,15 @@ void launch_dot(int n, int B, const R* x, const R* y, const Reduce& red, cudaStr
 }
 
 template <typename R>
+void launch_sb_log(int n, int B, const R* mu, const R* ref, double* upd_log, double* rel_log, const Reduce& red,
+                   cudaStream_t st) {
+  const int64_t L = static_cast<int64_t>(n) * n;
+  CK_LAUNCH(launch_k(k_sb_log<R>, dim3(vec_blocks(L, B), B), kVecThreads, 0, st, L, B, mu, ref, upd_log, rel_log,
+                     red));
+  note_launch();
+}
+
+template <typename R>
 void launch_leak(int64_t len, const cplx<R>* v, const Reduce& red, cudaStream_t st) {
   CK_LAUNCH(launch_k(k_leak<R>, vec_blocks(len, 1), kVecThreads, 0, st, len, v, red));
   note_launch();
@@ -550,6 +590,7 @@ void launch_shrink(int64_t len, const R* x, double gamma, R* out, cudaStream_t s
 }
 
 #define TOMO_INST_SOLVER(R)                                                                                        \
+  template void launch_sb_log<R>(int, int, const R*, const R*, double*, double*, const Reduce&, cudaStream_t); \
   template void launch_cg_update<R>(int, int, const R*, const R*, R*, R*, const SysParams&, int, const Reduce&,     \
                                     cudaStream_t);                                                                 \
   template void launch_stencil<R>(int, int, int, const StencilCoef&, int, const R*, const R*, R*, R*, const R*, R*, \

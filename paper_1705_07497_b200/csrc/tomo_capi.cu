@@ -241,7 +241,7 @@ struct Scratch {
   Raw heavy_cnt, heavy_cnt_gram;
   Raw cin, cout, fin, fout;       // staging for host pointers / temporaries
   Raw r, p0, p1, ap, x, rhs, fid, mu0, mu1, bx0, bx1, by0, by1, nred, zero, u2;  // real vectors
-  Raw upd_log, sc, part;
+  Raw upd_log, rel_log, sc, part;
 };
 
 // Device tables of one task-SpMV operator (the fused backend's Gram; see TaskSpmv).
@@ -1676,9 +1676,16 @@ int tomo_cg(tomo_op* op, const tomo_system* sys, const void* rhs, const void* x0
   TOMO_CATCH
 }
 
-int tomo_split_bregman(tomo_op* op, const tomo_sb_config* cfg, const void* slice_data, void* mu, int batch,
-                       double* update_l1, tomo_sb_trace* trace, void* stream) {
-  TOMO_TRY
+}  // extern "C"
+
+namespace {
+// split_bregman_tv (solver.cpp:219-307) for `batch` slices. Default: the whole Bregman loop is
+// one CUDA graph. `record`: one graph launch for the CG and one for the Bregman update per
+// iteration with CUDA events between them, giving the reference's per-iteration trace
+// (t_total_s, t_cg_s; rel_l1_err against `reference` when given, update_l1).
+void sb_impl(tomo_op* op, const tomo_sb_config* cfg, const void* slice_data, void* mu, int batch,
+             const void* reference, double* update_l1, double* rel_l1_err, double* t_total_s, double* t_cg_s,
+             tomo_sb_trace* trace, cudaStream_t st, bool record) {
   check_op(op, batch);
   if (!cfg) throw ConfigError("null config");
   if (!(cfg->alpha > 0.0)) throw ConfigError("SolverConfig: alpha must be positive");
@@ -1689,7 +1696,6 @@ int tomo_split_bregman(tomo_op* op, const tomo_sb_config* cfg, const void* slice
   if (cfg->max_iters > kMaxLoggedIters) throw ConfigError("split_bregman_tv: max_bregman_iters > 8192 not supported");
   DeviceGuard dg(op->device);
   op->ensure_batch(batch);
-  const cudaStream_t st = S_(stream);
   with_prec(op, [&](auto tag) {
     using R = decltype(tag);
     const int n = op->g.n;
@@ -1714,44 +1720,90 @@ int tomo_split_bregman(tomo_op* op, const tomo_sb_config* cfg, const void* slice
     for (auto& s : init) s.sb_tol = cfg->update_tol_rel;
     CK(cudaMemcpyAsync(S.sc.p, init.data(), sizeof(SliceScalars) * batch, cudaMemcpyHostToDevice, st));
     const SysParams sp = sysp(cfg->alpha, cfg->lambda, sigma, 0.0);
-    const std::string key = fmtkey("sb", batch, {cfg->alpha, cfg->lambda, sigma, double(cfg->max_iters),
-                                                 double(cfg->cg_steps), double(cfg->warm_start)});
-    run_graph(op, key, st, [&](cudaStream_t cs) {
-      R* mu_cur = S.mu0.as<R>();
-      R* mu_nxt = S.mu1.as<R>();
-      R *bxo = S.bx0.as<R>(), *bxn = S.bx1.as<R>(), *byo = S.by0.as<R>(), *byn = S.by1.as<R>();
-      for (int it = 0; it < cfg->max_iters; ++it) {
-        cg_run<R>(op, batch, sp, S.rhs.as<R>(), cfg->warm_start ? mu_cur : S.zero.as<R>(), mu_nxt, cfg->cg_steps, cs);
-        launch_sb_post<R>(n, batch, mu_nxt, mu_cur, bxo, byo, bxn, byn, S.fid.as<R>(), S.rhs.as<R>(), cfg->lambda,
-                          op->red(), cs);
-        CK(cudaMemcpy2DAsync(S.upd_log.as<double>() + static_cast<size_t>(it) * batch, sizeof(double),
-                             &op->scal()[0].upd, sizeof(SliceScalars), sizeof(double), batch,
-                             cudaMemcpyDeviceToDevice, cs));
-        std::swap(mu_cur, mu_nxt);
-        std::swap(bxo, bxn);
-        std::swap(byo, byn);
+    const int iters = cfg->max_iters;
+    R* mus[2] = {S.mu0.as<R>(), S.mu1.as<R>()};
+    R* bxs[2] = {S.bx0.as<R>(), S.bx1.as<R>()};
+    R* bys[2] = {S.by0.as<R>(), S.by1.as<R>()};
+    std::vector<cudaEvent_t> ev;
+    if (!record) {
+      const std::string key = fmtkey("sb", batch, {cfg->alpha, cfg->lambda, sigma, double(iters), double(cfg->cg_steps),
+                                                   double(cfg->warm_start)});
+      run_graph(op, key, st, [&](cudaStream_t cs) {
+        for (int it = 0; it < iters; ++it) {
+          const int p = it & 1;
+          cg_run<R>(op, batch, sp, S.rhs.as<R>(), cfg->warm_start ? mus[p] : S.zero.as<R>(), mus[p ^ 1],
+                    cfg->cg_steps, cs);
+          launch_sb_post<R>(n, batch, mus[p ^ 1], mus[p], bxs[p], bys[p], bxs[p ^ 1], bys[p ^ 1], S.fid.as<R>(),
+                            S.rhs.as<R>(), cfg->lambda, op->red(), cs);
+          CK(cudaMemcpy2DAsync(S.upd_log.as<double>() + static_cast<size_t>(it) * batch, sizeof(double),
+                               &op->scal()[0].upd, sizeof(SliceScalars), sizeof(double), batch,
+                               cudaMemcpyDeviceToDevice, cs));
+        }
+        // final iterate lives in mus[iters & 1]; normalise its location to S.mu0
+        if (iters & 1) CK(cudaMemcpyAsync(S.mu0.p, S.mu1.p, sizeof(R) * cnt, cudaMemcpyDeviceToDevice, cs));
+      });
+    } else {
+      const R* dref = nullptr;
+      if (reference) dref = static_cast<const R*>(stage_in(reference, cnt * sizeof(R), S.u2, st));
+      S.rel_log.ensure(sizeof(double) * static_cast<size_t>(batch) * iters);
+      ev.resize(3 * static_cast<size_t>(iters) + 1);
+      for (auto& e : ev) CK(cudaEventCreate(&e));
+      CK(cudaEventRecord(ev[0], st));
+      for (int it = 0; it < iters; ++it) {
+        const int p = it & 1;
+        run_graph(op, fmtkey("sbr_cg", batch, {cfg->alpha, cfg->lambda, sigma, double(cfg->cg_steps),
+                                               double(cfg->warm_start), double(p)}),
+                  st, [&](cudaStream_t cs) {
+                    cg_run<R>(op, batch, sp, S.rhs.as<R>(), cfg->warm_start ? mus[p] : S.zero.as<R>(), mus[p ^ 1],
+                              cfg->cg_steps, cs);
+                  });
+        CK(cudaEventRecord(ev[3 * it + 1], st));
+        run_graph(op, fmtkey("sbr_post", batch, {cfg->lambda, double(p), dref ? 1.0 : 0.0}), st, [&](cudaStream_t cs) {
+          launch_sb_post<R>(n, batch, mus[p ^ 1], mus[p], bxs[p], bys[p], bxs[p ^ 1], bys[p ^ 1], S.fid.as<R>(),
+                            S.rhs.as<R>(), cfg->lambda, op->red(), cs);
+          launch_sb_log<R>(n, batch, mus[p ^ 1], dref, S.upd_log.as<double>(),
+                           dref ? S.rel_log.as<double>() : nullptr, op->red(), cs);
+        });
+        CK(cudaEventRecord(ev[3 * it + 2], st));
+        if (it + 1 < iters) CK(cudaEventRecord(ev[3 * it + 3], st));
       }
-      // final iterate lives in mu_cur; normalise its location to S.mu0
-      if (mu_cur != S.mu0.as<R>()) CK(cudaMemcpyAsync(S.mu0.p, mu_cur, sizeof(R) * cnt, cudaMemcpyDeviceToDevice, cs));
-    });
+      if (iters & 1) CK(cudaMemcpyAsync(S.mu0.p, S.mu1.p, sizeof(R) * cnt, cudaMemcpyDeviceToDevice, st));
+    }
     std::vector<SliceScalars> hs(batch);
     CK(cudaMemcpyAsync(hs.data(), S.sc.p, sizeof(SliceScalars) * batch, cudaMemcpyDeviceToHost, st));
-    std::vector<double> log(static_cast<size_t>(batch) * cfg->max_iters);
+    std::vector<double> log(static_cast<size_t>(batch) * iters), rlog;
     CK(cudaMemcpyAsync(log.data(), S.upd_log.p, sizeof(double) * log.size(), cudaMemcpyDeviceToHost, st));
+    if (record && reference) {
+      rlog.resize(log.size());
+      CK(cudaMemcpyAsync(rlog.data(), S.rel_log.p, sizeof(double) * rlog.size(), cudaMemcpyDeviceToHost, st));
+    }
     CK(cudaMemcpyAsync(mu, S.mu0.p, sizeof(R) * cnt, is_device_ptr(mu) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
                        st));
     CK(cudaStreamSynchronize(st));
+    if (record) {
+      double cg_acc = 0.0;
+      for (int it = 0; it < iters; ++it) {
+        float t_it = 0.f, t_c = 0.f;
+        CK(cudaEventElapsedTime(&t_it, ev[0], ev[3 * it + 2]));
+        CK(cudaEventElapsedTime(&t_c, it == 0 ? ev[0] : ev[3 * it], ev[3 * it + 1]));
+        cg_acc += t_c * 1e-3;
+        if (t_total_s) t_total_s[it] = t_it * 1e-3;
+        if (t_cg_s) t_cg_s[it] = cg_acc;
+      }
+      for (auto& e : ev) cudaEventDestroy(e);
+    }
     for (int b = 0; b < batch; ++b) {
       if (hs[b].nonfinite)
         throw NumericalError(std::string("split_bregman_tv: non-finite iterate with backend ") +
-                             (sur ? "surrogate" : "direct"));
-      const int iters = hs[b].sb_iters;
-      if (update_l1)
-        for (int it = 0; it < cfg->max_iters; ++it)
-          update_l1[static_cast<size_t>(b) * cfg->max_iters + it] =
-              it < iters ? log[static_cast<size_t>(it) * batch + b] : 0.0;
+                             (sur ? "surrogate" : (op->fused() ? "fused" : "direct")));
+      const int ran = hs[b].sb_iters;
+      for (int it = 0; it < iters; ++it) {
+        const size_t o = static_cast<size_t>(b) * iters + it, l = static_cast<size_t>(it) * batch + b;
+        if (update_l1) update_l1[o] = it < ran ? log[l] : 0.0;
+        if (rel_l1_err && !rlog.empty()) rel_l1_err[o] = it < ran ? rlog[l] : 0.0;
+      }
       if (trace) {
-        trace[b].iterations = iters;
+        trace[b].iterations = ran;
         trace[b].first_update_l1 = hs[b].first_upd;
         trace[b].sigma = sigma;
         trace[b].min_ritz = std::isfinite(hs[b].min_ritz) ? hs[b].min_ritz : 0.0;
@@ -1760,6 +1812,24 @@ int tomo_split_bregman(tomo_op* op, const tomo_sb_config* cfg, const void* slice
       }
     }
   });
+}
+}  // namespace
+
+extern "C" {
+
+int tomo_split_bregman(tomo_op* op, const tomo_sb_config* cfg, const void* slice_data, void* mu, int batch,
+                       double* update_l1, tomo_sb_trace* trace, void* stream) {
+  TOMO_TRY
+  sb_impl(op, cfg, slice_data, mu, batch, nullptr, update_l1, nullptr, nullptr, nullptr, trace, S_(stream), false);
+  TOMO_CATCH
+}
+
+int tomo_split_bregman_record(tomo_op* op, const tomo_sb_config* cfg, const void* slice_data, void* mu, int batch,
+                              const void* reference, double* update_l1, double* rel_l1_err, double* t_total_s,
+                              double* t_cg_s, tomo_sb_trace* trace, void* stream) {
+  TOMO_TRY
+  sb_impl(op, cfg, slice_data, mu, batch, reference, update_l1, rel_l1_err, t_total_s, t_cg_s, trace, S_(stream),
+          true);
   TOMO_CATCH
 }
 

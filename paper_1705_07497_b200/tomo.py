@@ -186,6 +186,19 @@ class SolveTrace:
     stabilization_shift: float = 0.0
     min_ritz: float = 0.0
     imag_leakage: float = 0.0
+    rel_l1_err: np.ndarray = field(default_factory=lambda: np.zeros(0))  # with record_reference
+    t_total_s: np.ndarray = field(default_factory=lambda: np.zeros(0))   # recorded solves only
+    t_cg_s: np.ndarray = field(default_factory=lambda: np.zeros(0))
+
+    def write_csv(self, path):
+        """SolveTrace::write_csv (solver.cpp:140-150)."""
+        with open(path, "w") as f:
+            f.write("iter,update_l1,rel_l1_err,t_total_s,t_cg_s\n")
+            for i, u in enumerate(self.update_l1):
+                rel = f"{self.rel_l1_err[i]:.6g}" if i < len(self.rel_l1_err) else ""
+                tt = self.t_total_s[i] if i < len(self.t_total_s) else 0.0
+                tc = self.t_cg_s[i] if i < len(self.t_cg_s) else 0.0
+                f.write(f"{i + 1},{u:.6g},{rel},{tt:.6g},{tc:.6g}\n")
 
 
 @dataclass
@@ -348,6 +361,43 @@ class NormalBackend:
             traces.append(SolveTrace(upd.reshape(B, -1)[b, : t.iterations].copy(), t.iterations,
                                      "tolerance" if t.stopped_on_tolerance else "max_iterations",
                                      t.first_update_l1, t.sigma, t.min_ritz, t.imag_leakage))
+        return mu, traces
+
+    def split_bregman_record(self, slice_data, config: SolverConfig, reference=None):
+        """split_bregman_tv with the reference's per-iteration trace: t_total_s / t_cg_s (CUDA
+        events, one graph launch per CG and per update) and, given the phantom(s) as
+        `reference` (record_reference, solver.cpp:291-294), rel_l1_err per iteration."""
+        f = _as_input(slice_data, True, self.f64)
+        B = self._batch(f, self.info.P)
+        n = self.geom.n
+        mu = _empty_like_kind(f, (B, n, n), False, self.f64)
+        ref = None
+        if reference is not None:
+            ref = _as_input(reference, False, self.f64)
+            size = ref.size if isinstance(ref, np.ndarray) else ref.numel()
+            if size != B * n * n:
+                raise ConfigError("split_bregman_record: reference must hold batch x n^2 values")
+        cfg = _lib.SbConfig(config.alpha, config.lambda_, config.max_bregman_iters, config.cg_steps_per_update,
+                            config.update_tol_rel, int(config.warm_start),
+                            -1.0 if config.sigma_override is None else float(config.sigma_override))
+        K = config.max_bregman_iters
+        upd, rel = np.zeros(B * K), np.zeros(B * K)
+        tt, tc = np.zeros(K), np.zeros(K)
+        tr = (_lib.SbTrace * B)()
+        vp = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+        _check(lib().tomo_split_bregman_record(self._h, C.byref(cfg), _ptr(f), _ptr(mu), B,
+                                               _ptr(ref) if ref is not None else None, vp(upd),
+                                               vp(rel) if ref is not None else None, vp(tt), vp(tc), tr,
+                                               _stream_ptr(f)))
+        traces = []
+        for b in range(B):
+            t = tr[b]
+            k = t.iterations
+            traces.append(SolveTrace(upd.reshape(B, K)[b, :k].copy(), k,
+                                     "tolerance" if t.stopped_on_tolerance else "max_iterations",
+                                     t.first_update_l1, t.sigma, t.min_ritz, t.imag_leakage,
+                                     rel.reshape(B, K)[b, :k].copy() if ref is not None else np.zeros(0),
+                                     tt[:k].copy(), tc[:k].copy()))
         return mu, traces
 
     def tikhonov(self, slice_data, alpha=1.0, steps=20, rel_tol=0.0):

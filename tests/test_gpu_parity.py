@@ -302,3 +302,28 @@ def test_full_size_properties(T):
     # linearity
     w = op.apply_normal(u + 2 * v)
     assert (torch.linalg.norm(w - (nu + 2 * nv)) / torch.linalg.norm(w)).item() < 1e-5
+
+
+def test_sb_recorded_trace_vs_oracle(T):
+    """Recorded split Bregman (per-iteration graphs + events): same iterate as the one-graph
+    solve, update_l1 per iteration, rel_l1_err against the phantom (record_reference), and
+    monotone t_total_s >= t_cg_s."""
+    og = O.Geometry(**GEOMS["ref_msp3"])
+    ph = O.shepp_logan(og.n)
+    f, _ = O.synthesize(og, ph, 0.0, 0)
+    op = T.make_direct_backend(pgeom(T, og), precision="f64")
+    cfg = T.SolverConfig(alpha=10.0, lambda_=1.0, max_bregman_iters=6, cg_steps_per_update=4, update_tol_rel=0.0)
+    mu0, tr0 = op.split_bregman(cuda(f, True, True), cfg)
+    mu, tr = op.split_bregman_record(cuda(f, True, True), cfg, reference=cuda(ph, False, True))
+    assert np.array_equal(mu.cpu().numpy(), mu0.cpu().numpy())
+    t = tr[0]
+    assert t.iterations == 6 and np.allclose(t.update_l1, tr0[0].update_l1, rtol=0, atol=0)
+    ref_mu, ref_upd, _ = O.split_bregman(og, f, backend=0, alpha=10.0, lam=1.0, max_iters=6, cg_steps=4)
+    assert rel(t.update_l1, ref_upd) < REC_TOL
+    assert abs(t.rel_l1_err[-1] - O.rel_l1(mu[0].cpu().numpy(), ph)) < 1e-12
+    assert np.all(np.diff(t.t_total_s) > 0) and np.all(t.t_cg_s <= t.t_total_s) and np.all(np.diff(t.t_cg_s) > 0)
+    # tolerance stop: logs stop at the stopping iteration
+    cfg.update_tol_rel = 0.5
+    cfg.max_bregman_iters = 40
+    _, tr = op.split_bregman_record(cuda(f, True, True), cfg, reference=cuda(ph, False, True))
+    assert tr[0].stopping_reason == "tolerance" and len(tr[0].rel_l1_err) == tr[0].iterations < 40
