@@ -18,6 +18,19 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompil
          "-Xptxas", "-warn-spills"]
 
 
+def _nccl_dir():
+    """The NCCL torch itself loads (the nvidia-nccl wheel): linking the same libnccl.so.2 keeps one
+    NCCL per process whichever of torch / libtomo_b200 is loaded first."""
+    try:
+        import nvidia.nccl
+        d = nvidia.nccl.__path__[0]
+        if os.path.exists(os.path.join(d, "lib", "libnccl.so.2")):
+            return d
+    except ImportError:
+        pass
+    return None
+
+
 def _stale(target: str, deps) -> bool:
     if not os.path.exists(target):
         return True
@@ -37,7 +50,9 @@ def build(verbose: bool = False, jobs: int = 3) -> str:
     for src in SOURCES:
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
         objs.append(obj)
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        nccl = _nccl_dir()
+        inc = ["-I", os.path.join(nccl, "include")] if nccl else []
+        cmd = [NVCC, *ARCH, *FLAGS, *inc, "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd), flush=True)
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
@@ -53,7 +68,13 @@ def build(verbose: bool = False, jobs: int = 3) -> str:
         for src, text in failed:
             sys.stderr.write(f"---- nvcc failed on {src}\n{text}\n")
         raise RuntimeError("nvcc build of libtomo_b200 failed")
-    link = [NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-lnccl", "-lcudart"]
+    nccl = _nccl_dir()
+    if nccl:
+        lib = os.path.join(nccl, "lib")
+        nccl_link = ["-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath," + lib]
+    else:
+        nccl_link = ["-lnccl"]
+    link = [NVCC, *ARCH, "-shared", "-o", OUT, *objs, *nccl_link, "-lcudart"]
     if verbose:
         print(" ".join(link), flush=True)
     subprocess.check_call(link)

@@ -59,3 +59,13 @@ def test_no_gpu_fails_loudly():
     import paper_1705_07497_b200 as T
     with pytest.raises(T.CudaError):
         T.make_direct_backend(T.Geometry(n=32, n_angles=8))
+
+
+def test_library_then_torch_share_one_nccl():
+    """libtomo_b200 links the NCCL torch loads (nvidia-nccl wheel), so loading the library before
+    `import torch` must not leave torch resolving NCCL symbols against an older system NCCL."""
+    import subprocess
+    import sys
+    code = "import paper_1705_07497_b200 as T; T.tomo.lib(); import torch; print('ok')"
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
