@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtomo_b200.so")
+LIB_PATH = os.path.join(_HERE, os.environ.get("TOMO_LIB_NAME", "libtomo_b200.so"))  # variant builds for A/B runs
 _LIB = None
 
 TOMO_OK = 0

@@ -10,7 +10,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OUT = os.path.join(HERE, "libtomo_b200.so")
+OUT = os.path.join(HERE, os.environ.get("TOMO_LIB_NAME", "libtomo_b200.so"))  # variant builds for A/B runs
 SOURCES = ["nufft.cu", "solver.cu", "opbuild.cu", "tomo_capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -43,7 +43,7 @@ def build(verbose: bool = False, jobs: int = 3) -> str:
     deps.append(os.path.join(os.path.dirname(HERE), "include", "tomo_b200.h"))
     if not _stale(OUT, deps):
         return OUT
-    objdir = os.path.join(HERE, "_build")
+    objdir = os.path.join(HERE, "_build" + os.environ.get("TOMO_LIB_NAME", "").replace(".so", ""))
     os.makedirs(objdir, exist_ok=True)
     procs = []
     objs = []
@@ -52,7 +52,8 @@ def build(verbose: bool = False, jobs: int = 3) -> str:
         objs.append(obj)
         nccl = _nccl_dir()
         inc = ["-I", os.path.join(nccl, "include")] if nccl else []
-        cmd = [NVCC, *ARCH, *FLAGS, *inc, "-c", os.path.join(CSRC, src), "-o", obj]
+        defs = os.environ.get("TOMO_NVCC_DEFS", "").split()
+        cmd = [NVCC, *ARCH, *FLAGS, *defs, *inc, "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd), flush=True)
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))

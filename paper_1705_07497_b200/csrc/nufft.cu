@@ -33,6 +33,12 @@ __device__ __forceinline__ int bin_of(int t, int n, int M) { return (t - n / 2 +
 // FFT-row kernels: at most 512 threads per CTA so ptxas may give each thread up to 128
 // registers (a radix-16 fp64 butterfly holds 64 registers of data alone).
 constexpr int kFftThreads = 512;
+#ifndef TOMO_FFT_MINB_F32
+#define TOMO_FFT_MINB_F32 2
+#endif
+#ifndef TOMO_FFT_MINB_F64
+#define TOMO_FFT_MINB_F64 1
+#endif
 constexpr size_t kMaxSmem = 220 * 1024;  // dynamic smem a persistent FFT CTA may use
 // Persistent prefetching FFT-row kernels measured faster only for the longest rows (c5,
 // m = 8192); below that the one-shot kernels (more CTAs in flight) win.
@@ -87,7 +93,7 @@ struct NoStore {
 // deapodise + pad + inverse FFT along t2; the CG p-update (p = r + beta p) is fused into the
 // load; output transposed to H[iy][t1] through smem.
 template <int M, int RB, typename R>
-__global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? 2 : 1) k_t2_rows(OpDev<R> d, const void* __restrict__ in, int in_complex,
+__global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F32 : TOMO_FFT_MINB_F64) k_t2_rows(OpDev<R> d, const void* __restrict__ in, int in_complex,
                                                   PUpd<R> pu, int rpc) {
   using S = FftShape<M, RB>;
   using C2 = cplx<R>;
@@ -139,7 +145,7 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? 2 : 1) k_t2_rows
 
 // ---------------------------------------------------------------- P2: grid rows (iy)
 template <int M, int RB, typename R>
-__global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? 2 : 1) k_t2_cols(OpDev<R> d, int rpc, const SliceScalars* skip) {
+__global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F32 : TOMO_FFT_MINB_F64) k_t2_cols(OpDev<R> d, int rpc, const SliceScalars* skip) {
   using S = FftShape<M, RB>;
   using C2 = cplx<R>;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -391,7 +397,7 @@ __global__ void __launch_bounds__(256) k_task_spmv(TaskSpmv<R> ts, int m, int B,
 // ---------------------------------------------------------------- PA: grid rows (iy), type 1
 // forward FFT along ix of the spread grid row, pruned to the n bins, transposed to K[t1][iy].
 template <int M, int RB, typename R>
-__global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? 2 : 1) k_t1_cols(OpDev<R> d, int rpc, const SliceScalars* skip) {
+__global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F32 : TOMO_FFT_MINB_F64) k_t1_cols(OpDev<R> d, int rpc, const SliceScalars* skip) {
   using S = FftShape<M, RB>;
   using C2 = cplx<R>;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -433,7 +439,7 @@ __device__ __forceinline__ R ktk_at(const R* __restrict__ p, int n, int i, int j
 // forward FFT along iy, crop to the n bins, deapodise, then the epilogue: complex / real
 // output or the CG system apply alpha*Re(N p) + lambda K'K p + shift p with the dots.
 template <int M, int RB, typename R>
-__global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? 2 : 1) k_t1_rows(OpDev<R> d, PbEpi<R> e, int rpc) {
+__global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F32 : TOMO_FFT_MINB_F64) k_t1_rows(OpDev<R> d, PbEpi<R> e, int rpc) {
   using S = FftShape<M, RB>;
   using C2 = cplx<R>;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -518,7 +524,7 @@ TOMO_DEV void async_copy(C2* dst_smem, const C2* src) {
 
 // P2: inverse FFT along ix of H rows (t1 at the n bins), natural store g[iy][ix].
 template <int M, int RB, typename R>
-__global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? 2 : 1)
+__global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F32 : TOMO_FFT_MINB_F64)
 k_t2_cols_p(OpDev<R> d, const SliceScalars* skip) {
   using S = FftShape<M, RB>;
   using C2 = cplx<R>;
@@ -557,7 +563,7 @@ k_t2_cols_p(OpDev<R> d, const SliceScalars* skip) {
 
 // PA: forward FFT of rpc spread-grid rows, pruned to the n bins, transposed store K[t1][iy].
 template <int M, int RB, typename R>
-__global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? 2 : 1)
+__global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F32 : TOMO_FFT_MINB_F64)
 k_t1_cols_p(OpDev<R> d, int rpc, const SliceScalars* skip) {
   using S = FftShape<M, RB>;
   using C2 = cplx<R>;
@@ -604,7 +610,7 @@ k_t1_cols_p(OpDev<R> d, int rpc, const SliceScalars* skip) {
 // PB: forward FFT along iy of K rows, crop + deapodise + epilogue (as k_t1_rows); the CG dots
 // are accumulated over all rows of the CTA and reduced once per CTA.
 template <int M, int RB, typename R>
-__global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? 2 : 1)
+__global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F32 : TOMO_FFT_MINB_F64)
 k_t1_rows_p(OpDev<R> d, PbEpi<R> e) {
   using S = FftShape<M, RB>;
   using C2 = cplx<R>;
