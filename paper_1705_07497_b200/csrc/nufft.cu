@@ -771,6 +771,30 @@ void dispatch_m_rb(int m, int rb, F&& f) {
   });
 }
 
+// The n-row passes (P1, PB) run on n of the m rows only. For fp64 rows up to m = 2048 that
+// leaves the GPU short of warps (126-register threads, ~7 warps/SM at c2), and radix-8 rows
+// (twice the threads per row, one more smem pass) measured faster: c2 t2_rows 10.5 -> 9.9 us,
+// t1_rows 11.7 -> 10.7 us. fp32 (c3: 17 -> 23 us) and m = 8192 keep radix 16.
+// TOMO_ROW_RB=8|16 overrides (A/B runs).
+int row_rb(int m, size_t elem) {
+  static const int forced = [] {
+    const char* v = std::getenv("TOMO_ROW_RB");
+    return v ? std::atoi(v) : 0;
+  }();
+  if (forced == 8 || forced == 16) return forced;
+  return elem == 16 && m <= 2048 ? 8 : 16;
+}
+
+template <typename F>
+void dispatch_m_rows(int m, size_t elem, F&& f) {
+  dispatch_m(m, [&](auto MC) {
+    if (row_rb(m, elem) == 8 && decltype(MC)::value / 8 <= kFftThreads)
+      f(MC, std::integral_constant<int, 8>{});
+    else
+      f(MC, std::integral_constant<int, 16>{});
+  });
+}
+
 template <typename K>
 void set_smem(K kernel, size_t bytes) {
   // Opt in to > 48 KB dynamic smem once per kernel (and per larger size).
@@ -788,7 +812,7 @@ void set_smem(K kernel, size_t bytes) {
 
 template <typename R>
 void launch_t2_rows(const OpDev<R>& d, int B, const void* in, bool in_complex, const PUpd<R>& pu, cudaStream_t st) {
-  dispatch_m_rb(d.m, choose_rb(d.m, static_cast<int64_t>(d.n) * B, sizeof(cplx<R>)), [&](auto MC, auto RC) {
+  dispatch_m_rows(d.m, sizeof(cplx<R>), [&](auto MC, auto RC) {
     constexpr int M = decltype(MC)::value, RB = decltype(RC)::value;
     using S = FftShape<M, RB>;
     const int rpc = choose_rpc(S::T, M, d.n, B, sizeof(cplx<R>), true);
@@ -932,7 +956,7 @@ void launch_t1_cols_only(const OpDev<R>& d, int B, const SliceScalars* skip, cud
 
 template <typename R>
 void launch_t1_rows(const OpDev<R>& d, int B, const PbEpi<R>& e, cudaStream_t st) {
-  dispatch_m_rb(d.m, choose_rb(d.m, static_cast<int64_t>(d.n) * B, sizeof(cplx<R>)), [&](auto MC, auto RC) {
+  dispatch_m_rows(d.m, sizeof(cplx<R>), [&](auto MC, auto RC) {
     constexpr int M = decltype(MC)::value, RB = decltype(RC)::value;
     using S = FftShape<M, RB>;
     constexpr size_t smem_p = (static_cast<size_t>(S::STRIDE) + M) * sizeof(cplx<R>);
