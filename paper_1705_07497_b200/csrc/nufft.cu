@@ -795,6 +795,31 @@ void dispatch_m_rows(int m, size_t elem, F&& f) {
   });
 }
 
+// Grid-row passes (P2, PA): radix 16 unless TOMO_COL_RB=8 (A/B runs; one-shot kernels only).
+int col_rb(int m, size_t elem) {
+  static const int forced = [] {
+    const char* v = std::getenv("TOMO_COL_RB");
+    return v ? std::atoi(v) : 0;
+  }();
+  (void)m;
+  (void)elem;
+  return forced == 8 ? 8 : 16;
+}
+
+template <typename F>
+void dispatch_m_cols(int m, size_t elem, F&& f) {
+  dispatch_m(m, [&](auto MC) {
+    constexpr int M = decltype(MC)::value;
+    if constexpr (M < kPersistMinM) {
+      if (col_rb(m, elem) == 8) {
+        f(MC, std::integral_constant<int, 8>{});
+        return;
+      }
+    }
+    f(MC, std::integral_constant<int, 16>{});
+  });
+}
+
 template <typename K>
 void set_smem(K kernel, size_t bytes) {
   // Opt in to > 48 KB dynamic smem once per kernel (and per larger size).
@@ -849,10 +874,10 @@ int persistent_ctas(K kernel, int threads, size_t smem, int rows_per_slice, int 
 
 template <typename R>
 void launch_t2_cols(const OpDev<R>& d, int B, const SliceScalars* skip, cudaStream_t st) {
-  dispatch_m_rb(d.m, choose_rb(d.m, static_cast<int64_t>(d.m) * B, sizeof(cplx<R>)), [&](auto MC, auto RC) {
+  dispatch_m_cols(d.m, sizeof(cplx<R>), [&](auto MC, auto RC) {
     constexpr int M = decltype(MC)::value, RB = decltype(RC)::value;
     using S = FftShape<M, RB>;
-    if (M >= kPersistMinM) {
+    if constexpr (M >= kPersistMinM) {
       const size_t smem = (static_cast<size_t>(S::STRIDE) + d.n) * sizeof(cplx<R>);
       set_smem(k_t2_cols_p<M, RB, R>, smem);
       const int ctas = persistent_ctas(k_t2_cols_p<M, RB, R>, S::T, smem, M, B);
@@ -931,25 +956,29 @@ void launch_wt_rows(const OpDev<R>& d, int B, const SliceScalars* skip, cudaStre
 
 template <typename R>
 void launch_t1_cols_only(const OpDev<R>& d, int B, const SliceScalars* skip, cudaStream_t st) {
-  dispatch_m_rb(d.m, choose_rb(d.m, static_cast<int64_t>(d.m) * B, sizeof(cplx<R>)), [&](auto MC, auto RC) {
+  dispatch_m_cols(d.m, sizeof(cplx<R>), [&](auto MC, auto RC) {
     constexpr int M = decltype(MC)::value, RB = decltype(RC)::value;
     using S = FftShape<M, RB>;
-    // transposed K stores need >= 32 B per row segment; staging holds rpc full rows
-    int rpc = std::max(1, static_cast<int>(32 / sizeof(cplx<R>)));
-    while (rpc > 1 && (rpc * S::T > kFftThreads ||
-                       static_cast<size_t>(rpc) * (S::STRIDE + M) * sizeof(cplx<R>) > 200 * 1024))
-      rpc >>= 1;
-    const size_t smem = static_cast<size_t>(rpc) * (S::STRIDE + M) * sizeof(cplx<R>);
-    if (smem <= kMaxSmem && M >= kPersistMinM) {
-      set_smem(k_t1_cols_p<M, RB, R>, smem);
-      const int ctas = persistent_ctas(k_t1_cols_p<M, RB, R>, rpc * S::T, smem, M / rpc, B);
-      CK_LAUNCH(launch_k(k_t1_cols_p<M, RB, R>, dim3(ctas, B), rpc * S::T, smem, st, d, rpc, skip));
-    } else {  // row + staging do not fit (fp64, m = 8192): one-shot CTAs
-      const int rpc1 = choose_rpc(S::T, M, M, B, sizeof(cplx<R>), true);
-      const size_t smem1 = static_cast<size_t>(rpc1) * S::STRIDE * sizeof(cplx<R>);
-      set_smem(k_t1_cols<M, RB, R>, smem1);
-      CK_LAUNCH(launch_k(k_t1_cols<M, RB, R>, dim3(M / rpc1, B), rpc1 * S::T, smem1, st, d, rpc1, skip));
+    if constexpr (M >= kPersistMinM) {
+      // transposed K stores need >= 32 B per row segment; staging holds rpc full rows
+      int rpc = std::max(1, static_cast<int>(32 / sizeof(cplx<R>)));
+      while (rpc > 1 && (rpc * S::T > kFftThreads ||
+                         static_cast<size_t>(rpc) * (S::STRIDE + M) * sizeof(cplx<R>) > 200 * 1024))
+        rpc >>= 1;
+      const size_t smem = static_cast<size_t>(rpc) * (S::STRIDE + M) * sizeof(cplx<R>);
+      if (smem <= kMaxSmem) {
+        set_smem(k_t1_cols_p<M, RB, R>, smem);
+        const int ctas = persistent_ctas(k_t1_cols_p<M, RB, R>, rpc * S::T, smem, M / rpc, B);
+        CK_LAUNCH(launch_k(k_t1_cols_p<M, RB, R>, dim3(ctas, B), rpc * S::T, smem, st, d, rpc, skip));
+        note_launch();
+        return;
+      }
     }
+    // one-shot CTAs (also when row + staging do not fit: fp64, m = 8192)
+    const int rpc1 = choose_rpc(S::T, M, M, B, sizeof(cplx<R>), true);
+    const size_t smem1 = static_cast<size_t>(rpc1) * S::STRIDE * sizeof(cplx<R>);
+    set_smem(k_t1_cols<M, RB, R>, smem1);
+    CK_LAUNCH(launch_k(k_t1_cols<M, RB, R>, dim3(M / rpc1, B), rpc1 * S::T, smem1, st, d, rpc1, skip));
     note_launch();
   });
 }
