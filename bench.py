@@ -354,6 +354,10 @@ def cpu_sample(cname, c, prefer_reference=True):
     from oracle import oracle as O
     from oracle import refbind
     use_ref = prefer_reference and refbind.available()
+    # the reference's surrogate weights assume n_b = n (radial_density_weights, normal_ops.cpp:208-219):
+    # with n_b != n only the oracle port runs the surrogate split Bregman
+    if c["kind"] == "sb_sur" and c["nb"] != c["n"]:
+        use_ref = False
     kind = "reference" if use_ref else "port"
     n, A, nb = c["n"], c["A"], c["nb"]
     # the reference window is symmetric [-m_sp, m_sp]; the width-6 [-2,3] config maps to m_sp=3

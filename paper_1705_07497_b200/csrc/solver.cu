@@ -145,6 +145,8 @@ __global__ void __launch_bounds__(256) k_stencil(int n, StencilCoef coef, int mo
   for (int k = threadIdx.x; k < SIDE * SIDE; k += blockDim.x) cf[k] = static_cast<R>(coef.c[k]);
   const size_t off = static_cast<size_t>(b) * n * n;
   const int i0 = blockIdx.y * kTile - HALO, j0 = blockIdx.x * kTile - HALO;
+  // the halo tile: W*W/256 ~ 17 loads per thread, issued 6 at a time (unrolled: independent loads)
+#pragma unroll 6
   for (int idx = threadIdx.x; idx < W * W; idx += blockDim.x) {
     const int li = idx / W, lj = idx - li * W;
     const int gi = i0 + li, gj = j0 + lj;
@@ -157,25 +159,41 @@ __global__ void __launch_bounds__(256) k_stencil(int n, StencilCoef coef, int mo
     q[li][lj] = v;
   }
   __syncthreads();
+  // each thread: one column, kTile / kTileRows consecutive rows, the (2RAD+1)^2 neighbourhood in
+  // a register window that slides down one row per output (2RAD+1 smem reads per output)
+  constexpr int RPT = kTile / kTileRows;
   const int tj = threadIdx.x % kTile, ti = threadIdx.x / kTile;
   const R alpha = static_cast<R>(sys.alpha), lam = static_cast<R>(sys.lambda), shift = static_cast<R>(sys.shift);
   double acc0 = 0.0, acc1 = 0.0;
-#pragma unroll 4
-  for (int k = 0; k < kTile / kTileRows; ++k) {
-    const int li = ti + kTileRows * k + HALO, lj = tj + HALO;
-    const int gi = i0 + li, gj = j0 + lj;
+  const int lj = tj + HALO, r0 = ti * RPT + HALO;
+  const int gj = j0 + lj;
+  R win[SIDE][SIDE];
+#pragma unroll
+  for (int k = 0; k < SIDE - 1; ++k)
+#pragma unroll
+    for (int dj = 0; dj < SIDE; ++dj) win[k + 1][dj] = q[r0 - RAD + k][lj - RAD + dj];
+#pragma unroll
+  for (int k = 0; k < RPT; ++k) {
+    const int li = r0 + k;
+#pragma unroll
+    for (int a = 0; a < SIDE - 1; ++a)
+#pragma unroll
+      for (int dj = 0; dj < SIDE; ++dj) win[a][dj] = win[a + 1][dj];
+#pragma unroll
+    for (int dj = 0; dj < SIDE; ++dj) win[SIDE - 1][dj] = q[li + RAD][lj - RAD + dj];
+    const int gi = i0 + li;
     if (gi >= n || gj >= n) continue;
-    const R c = q[li][lj];
+    const R c = win[RAD][RAD];
     R tq = 0;
 #pragma unroll
-    for (int di = -RAD; di <= RAD; ++di)
+    for (int di = 0; di < SIDE; ++di)
 #pragma unroll
-      for (int dj = -RAD; dj <= RAD; ++dj) tq += cf[(di + RAD) * SIDE + (dj + RAD)] * q[li + di][lj + dj];
+      for (int dj = 0; dj < SIDE; ++dj) tq += cf[di * SIDE + dj] * win[di][dj];
     R kk = 0;
-    if (gj >= 1) kk += c - q[li][lj - 1];
-    if (gj <= n - 2) kk -= q[li][lj + 1] - c;
-    if (gi >= 1) kk += c - q[li - 1][lj];
-    if (gi <= n - 2) kk -= q[li + 1][lj] - c;
+    if (gj >= 1) kk += c - win[RAD][RAD - 1];
+    if (gj <= n - 2) kk -= win[RAD][RAD + 1] - c;
+    if (gi >= 1) kk += c - win[RAD - 1][RAD];
+    if (gi <= n - 2) kk -= win[RAD + 1][RAD] - c;
     const R ax = alpha * tq + lam * kk + shift * c;
     const size_t o = off + static_cast<size_t>(gi) * n + gj;
     if (mode == 0) {
@@ -243,7 +261,7 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_epilogue(int n, int mode, co
   const R lam = static_cast<R>(sys.lambda), shift = static_cast<R>(sys.shift);
   double acc0 = 0.0, acc1 = 0.0;
   for (int64_t i = gtid(); i < L; i += gstride()) {
-    const int ii = static_cast<int>(i / n), jj = static_cast<int>(i - static_cast<int64_t>(ii) * n);
+    const int ii = static_cast<int>(i) / n, jj = static_cast<int>(i) - ii * n;
     const R pv = pb[i];
     R ax = nred[off + i];
     if (lam != R(0)) ax += lam * ktk_g(pb, n, ii, jj);
@@ -316,7 +334,7 @@ __global__ void __launch_bounds__(kVecThreads) k_sb_post(int n, R* __restrict__ 
   double upd = 0.0;
   bool fin = true;
   for (int64_t i = gtid(); i < L; i += gstride()) {
-    const int ii = static_cast<int>(i / n), jj = static_cast<int>(i - static_cast<int64_t>(ii) * n);
+    const int ii = static_cast<int>(i) / n, jj = static_cast<int>(i) - ii * n;  // 32-bit: L < 2^31
     const R c = mu[i];
     fin = fin && finite_r(c);
     upd += fabs(static_cast<double>(c) - static_cast<double>(mu_old[off + i]));
@@ -367,7 +385,7 @@ __global__ void __launch_bounds__(kVecThreads) k_cp_dual(int n, const R* __restr
   auto ubar = [&](int64_t k) { return uc[k] + theta * (uc[k] - up[k]); };
   auto clampl = [&](R v) { return fmin(lambda, fmax(-lambda, v)); };
   for (int64_t i = gtid(); i < L; i += gstride()) {
-    const int ii = static_cast<int>(i / n), jj = static_cast<int>(i - static_cast<int64_t>(ii) * n);
+    const int ii = static_cast<int>(i) / n, jj = static_cast<int>(i) - ii * n;
     const R c = ubar(i);
     const R gx = jj < n - 1 ? ubar(i + 1) - c : R(0);
     const R gy = ii < n - 1 ? ubar(i + n) - c : R(0);
