@@ -185,6 +185,7 @@ class Workload:
         import paper_1705_07497_b200 as T
         self.T, self.c, self.torch = T, c, torch
         self.replayed_launches = 0  # kernels launched by torch-graph replays (not seen by the C ABI counter)
+        self.sharded = False  # c5 at N > 1: one slice, angle-block sharded (strong scaling)
         self.name = cfg_name
         g = make_geom(T, c)
         self.geom = g
@@ -232,8 +233,22 @@ class Workload:
             self.out_host = torch.empty(self.batch, g.n, g.n, dtype=torch.complex64).pin_memory()
             self.h2d = self.d2h = self.u.numel() * 8 * self.calls
         elif kind == "cp":
-            self.op = T.make_direct_backend(g, precision=c["prec"], device=local)
-            self.f = torch.from_numpy(synth_slices(T, self.op, c, [5000 + rank], torch)).cuda()
+            if world > 1:
+                # one large slice sharded by angle blocks: every rank owns the W rows
+                # of its block; each adjoint is summed across ranks by an NCCL all-reduce inside
+                # the library; the CP/CG state is replicated. Same data on every N: synthesised with
+                # the whole operator, then each rank keeps its block's samples.
+                from paper_1705_07497_b200.distributed import angle_blocks, make_sharded_backend
+                full = T.make_direct_backend(g, precision=c["prec"], device=local)
+                f_all = synth_slices(T, full, c, [5000], torch)
+                del full
+                a0, a1 = angle_blocks(c["A"], world)[rank]
+                self.op = make_sharded_backend(g, rank, world, local, precision=c["prec"])
+                self.f = torch.from_numpy(np.ascontiguousarray(f_all[:, a0 * c["nb"]:a1 * c["nb"]])).cuda()
+                self.sharded = True
+            else:
+                self.op = T.make_direct_backend(g, precision=c["prec"], device=local)
+                self.f = torch.from_numpy(synth_slices(T, self.op, c, [5000 + rank], torch)).cuda()
             self.units_per_step = c["iters"] * (c["cg"] + 1)
             self.f_host = self.f.cpu().pin_memory()
             self.h2d = self.f.numel() * self.f.element_size()
@@ -475,7 +490,8 @@ def main():
     barrier(world)
     launches = T.kernel_launches() - launches0 + (wl.replayed_launches - replayed0)
     t_max = allreduce_max(total_ms, world)
-    units = allreduce_sum(float(wl.units_per_step * args.steps), world)
+    # sharded c5: all ranks work on the same applies (one slice) -> count them once
+    units = float(wl.units_per_step * args.steps) if wl.sharded else allreduce_sum(float(wl.units_per_step * args.steps), world)
     launches = int(allreduce_sum(float(launches), world))
     value = units / (t_max * 1e-3)
 
@@ -497,7 +513,7 @@ def main():
         e2e_ms += max(e0.elapsed_time(e1), (time.perf_counter() - t0) * 1e3)
     e2e_steps = max(1, min(args.steps, 3))
     e2e_max = allreduce_max(e2e_ms, world)
-    e2e_units = allreduce_sum(float(wl.units_per_step * e2e_steps), world)
+    e2e_units = float(wl.units_per_step * e2e_steps) if wl.sharded else allreduce_sum(float(wl.units_per_step * e2e_steps), world)
     e2e_value = e2e_units / (e2e_max * 1e-3)
 
     top, roof = wl.roofline(peak)
@@ -521,14 +537,14 @@ def main():
         line = {
             "metric": c["metric"], "value": value, "unit": c["unit"], "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
-            "scaling": "strong" if c["kind"] == "sb_sur" else "weak", "vs_baseline": None,
+            "scaling": "strong" if (c["kind"] == "sb_sur" or wl.sharded) else "weak", "vs_baseline": None,
             "dtype": c["prec"], "data": "synthetic (seeded random ellipses, 1% complex Gaussian noise; c3 random normal)",
             "config": {"workload": args.config, "n": c["n"], "angles": c["A"], "n_b": c["nb"], "oversample": c["R"],
                        "window": [c["lo"], c["hi"]], "m": info.m, "P": int(info.P), "nnz_W": int(info.nnz),
                        "wt_rows": int(info.wt_rows), "wt_slots": int(info.wt_slots), "precision": c["prec"],
                        "l2": "flushed between timed steps (256 MiB write)",
                        **{k: c[k] for k in ("alpha", "lam", "iters", "cg", "applies", "slices", "r") if k in c},
-                       "parallelism": f"{'slice-sharded' if c['kind'] == 'sb_sur' else 'replicas'} x{world}"},
+                       "parallelism": f"{'slice-sharded' if c['kind'] == 'sb_sur' else ('angle-sharded' if wl.sharded else 'replicas')} x{world}"},
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": c["unit"], "h2d_bytes_per_step": int(wl.h2d),
