@@ -205,7 +205,7 @@ class Workload:
             lo = rank * per_rank
             hi = min(c["slices"], lo + per_rank)
             self.nslices = max(0, hi - lo)
-            self.batch = min(64, max(1, self.nslices))
+            self.batch = min(int(c.get("batch", 64)), max(1, self.nslices))
             self.op = T.make_surrogate_backend(g, radius_r=c["r"], max_batch=self.batch, device=local)
             fs = synth_slices(T, self.op, c, list(range(2000 + lo, 2000 + hi)), torch)
             self.f = torch.from_numpy(fs).cuda()

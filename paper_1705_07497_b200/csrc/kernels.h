@@ -205,6 +205,7 @@ struct GpuBuildSizes {
   int64_t touched = 0;  // non-empty W^T rows
 };
 struct GpuBuild;
+bool wt_row_order(int m);  // W^T warp-task order (opbuild.cu)
 // plan + separable W (written to base/wx/wy) + W^T structure; returns the table sizes
 template <typename R>
 GpuBuild* gpu_build_begin(const BuildArgs& a, const double* h_cs, const double* h_e3, int* base, R* wx, R* wy,

@@ -458,7 +458,8 @@ struct TaskBuilder {
 
   void finish() {
     // longest tasks first (they are launched first and overlap the rest)
-    std::stable_sort(tasks.begin(), tasks.end(), [](const int4& a, const int4& b) { return a.z > b.z; });
+    if (!wt_row_order(m))
+      std::stable_sort(tasks.begin(), tasks.end(), [](const int4& a, const int4& b) { return a.z > b.z; });
     if (ent.empty()) ent.resize(1);
   }
 
