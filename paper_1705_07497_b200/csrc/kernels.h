@@ -68,6 +68,8 @@ struct OpDev {
   const int* w_base;               // [Ppad] ix0 | iy0 << 16
   const R* w_x;                    // [w][Ppad]
   const R* w_y;                    // [w][Ppad]
+  const int* w_perm;               // [P] table position -> sample index: the separable tables are
+                                   // stored in grid-tile order (spatial locality of the gathers)
   int w;                           // window width
   int w_sep;                       // 1: use the separable storage for W, 0: the SELL-32 ELL
   // W^T: nodes of each grid row sorted by entry count (SELL-32-sigma, sigma = one grid row);
@@ -215,6 +217,10 @@ template <typename R>
 void gpu_build_finish(GpuBuild* b, WtEnt<R>* ent, int4* tasks, uint16_t* perm, int4* heavy, int* slot_heavy,
                       cudaStream_t st);
 void gpu_build_free(GpuBuild* b);
+// Re-order the separable W tables (base, wx, wy; [Ppad] / [w][Ppad]) by 16x16 grid tile of the
+// window base; perm[t] = sample stored at position t.
+template <typename R>
+void gpu_sort_w_tables(int m, int64_t P, int64_t Ppad, int w, int* base, R* wx, R* wy, int* perm, cudaStream_t st);
 
 // ---- launchers (solver.cu) ----
 struct StencilCoef {

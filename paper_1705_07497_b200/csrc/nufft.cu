@@ -238,19 +238,20 @@ template <int BT, int WMAX, int RU, typename R>
 __global__ void __launch_bounds__(256) k_w_sep(OpDev<R> d, int B, const cplx<R>* __restrict__ grid,
                                                 cplx<R>* __restrict__ out, const SliceScalars* skip) {
   using C2 = cplx<R>;
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= d.P) return;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;  // table position
+  if (t >= d.P) return;
+  const int j = d.w_perm ? __ldg(&d.w_perm[t]) : t;    // sample
   const int m = d.m, w = d.w;
-  const int base = __ldg(&d.w_base[j]);
+  const int base = __ldg(&d.w_base[t]);
   const int ix0 = base & 0xffff, iy0 = base >> 16;
   R wx[WMAX];
   int ix[WMAX];
 #pragma unroll
   for (int a = 0; a < WMAX; ++a) {
     if (a < w) {
-      wx[a] = __ldg(&d.w_x[static_cast<size_t>(a) * d.Ppad + j]);
-      const int t = ix0 + a;
-      ix[a] = t >= m ? t - m : t;
+      wx[a] = __ldg(&d.w_x[static_cast<size_t>(a) * d.Ppad + t]);
+      const int u = ix0 + a;
+      ix[a] = u >= m ? u - m : u;
     }
   }
   const size_t G = static_cast<size_t>(m) * m;
@@ -265,9 +266,9 @@ __global__ void __launch_bounds__(256) k_w_sep(OpDev<R> d, int B, const cplx<R>*
       for (int k = 0; k < RU; ++k) {
         const int bb = bb0 + k;
         if (bb < w) {
-          const R wyv = __ldg(&d.w_y[static_cast<size_t>(bb) * d.Ppad + j]);
-          const int t = iy0 + bb;
-          const size_t rowoff = static_cast<size_t>(t >= m ? t - m : t) * m;
+          const R wyv = __ldg(&d.w_y[static_cast<size_t>(bb) * d.Ppad + t]);
+          const int u = iy0 + bb;
+          const size_t rowoff = static_cast<size_t>(u >= m ? u - m : u) * m;
 #pragma unroll
           for (int q = 0; q < BT; ++q) {
             if (b0 + q < B) {
@@ -301,10 +302,11 @@ template <typename R>
 __global__ void __launch_bounds__(256) k_w_sep_wide(OpDev<R> d, int B, const cplx<R>* __restrict__ grid,
                                                      cplx<R>* __restrict__ out, const SliceScalars* skip) {
   using C2 = cplx<R>;
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= d.P) return;
+  const int tp = blockIdx.x * blockDim.x + threadIdx.x;  // table position
+  if (tp >= d.P) return;
+  const int j = d.w_perm ? __ldg(&d.w_perm[tp]) : tp;   // sample
   const int m = d.m, w = d.w;
-  const int base = __ldg(&d.w_base[j]);
+  const int base = __ldg(&d.w_base[tp]);
   const int ix0 = base & 0xffff, iy0 = base >> 16;
   const size_t G = static_cast<size_t>(m) * m;
   for (int b = 0; b < B; ++b) {
@@ -317,12 +319,12 @@ __global__ void __launch_bounds__(256) k_w_sep_wide(OpDev<R> d, int B, const cpl
       C2 ra = czero<C2>();
       for (int a = 0; a < w; ++a) {
         const int u = ix0 + a;
-        const R wx = __ldg(&d.w_x[static_cast<size_t>(a) * d.Ppad + j]);
+        const R wx = __ldg(&d.w_x[static_cast<size_t>(a) * d.Ppad + tp]);
         const C2 gv = row[u >= m ? u - m : u];
         ra.x += wx * gv.x;
         ra.y += wx * gv.y;
       }
-      const R wy = __ldg(&d.w_y[static_cast<size_t>(bb) * d.Ppad + j]);
+      const R wy = __ldg(&d.w_y[static_cast<size_t>(bb) * d.Ppad + tp]);
       acc.x += wy * ra.x;
       acc.y += wy * ra.y;
     }

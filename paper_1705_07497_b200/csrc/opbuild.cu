@@ -383,10 +383,64 @@ void gpu_build_finish(GpuBuild* b, WtEnt<R>* ent, int4* tasks, uint16_t* perm, i
 
 void gpu_build_free(GpuBuild* b) { delete b; }
 
+namespace {
+__global__ void k_tile_keys(int64_t P, int m, const int* __restrict__ base, unsigned long long* keys, int* idx) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= P) return;
+  const int b = base[j];
+  const int ix0 = b & 0xffff, iy0 = b >> 16;
+  const unsigned long long tile = static_cast<unsigned long long>(iy0 / 16) * (m / 16) + ix0 / 16;
+  keys[j] = (tile << 32) | static_cast<unsigned long long>(j);
+  idx[j] = static_cast<int>(j);
+}
+
+template <typename R>
+__global__ void k_gather_w(int64_t P, int64_t Ppad, int w, const int* __restrict__ perm, const int* __restrict__ base_in,
+                           const R* __restrict__ wx_in, const R* __restrict__ wy_in, int* base_out, R* wx_out,
+                           R* wy_out) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= P) return;
+  const int j = perm[t];
+  base_out[t] = base_in[j];
+  for (int a = 0; a < w; ++a) {
+    wx_out[a * Ppad + t] = wx_in[a * Ppad + j];
+    wy_out[a * Ppad + t] = wy_in[a * Ppad + j];
+  }
+}
+}  // namespace
+
+template <typename R>
+void gpu_sort_w_tables(int m, int64_t P, int64_t Ppad, int w, int* base, R* wx, R* wy, int* perm, cudaStream_t st) {
+  if (P <= 0) return;
+  DBuf<unsigned long long> keys(P), skeys(P);
+  DBuf<int> idx(P);
+  const unsigned grid = static_cast<unsigned>((P + 255) / 256);
+  k_tile_keys<<<grid, 256, 0, st>>>(P, m, base, keys.p, idx.p);
+  BK(cudaGetLastError());
+  const int tiles = (m / 16) * (m / 16);
+  const int key_bits = 32 + bits_for(static_cast<uint64_t>(tiles));
+  size_t tb = 0;
+  BK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.p, skeys.p, idx.p, perm, static_cast<int>(P), 0, key_bits, st));
+  DBuf<unsigned char> tmp(tb);
+  BK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.p, skeys.p, idx.p, perm, static_cast<int>(P), 0, key_bits, st));
+  DBuf<int> b2(Ppad);
+  DBuf<R> x2(static_cast<size_t>(w) * Ppad), y2(static_cast<size_t>(w) * Ppad);
+  BK(cudaMemcpyAsync(b2.p, base, sizeof(int) * Ppad, cudaMemcpyDeviceToDevice, st));  // padding rows
+  BK(cudaMemcpyAsync(x2.p, wx, sizeof(R) * w * Ppad, cudaMemcpyDeviceToDevice, st));
+  BK(cudaMemcpyAsync(y2.p, wy, sizeof(R) * w * Ppad, cudaMemcpyDeviceToDevice, st));
+  k_gather_w<R><<<grid, 256, 0, st>>>(P, Ppad, w, perm, base, wx, wy, b2.p, x2.p, y2.p);
+  BK(cudaGetLastError());
+  BK(cudaMemcpyAsync(base, b2.p, sizeof(int) * Ppad, cudaMemcpyDeviceToDevice, st));
+  BK(cudaMemcpyAsync(wx, x2.p, sizeof(R) * w * Ppad, cudaMemcpyDeviceToDevice, st));
+  BK(cudaMemcpyAsync(wy, y2.p, sizeof(R) * w * Ppad, cudaMemcpyDeviceToDevice, st));
+  BK(cudaStreamSynchronize(st));
+}
+
 #define TOMO_INST_BUILD(R)                                                                                     \
   template GpuBuild* gpu_build_begin<R>(const BuildArgs&, const double*, const double*, int*, R*, R*,         \
                                         cudaStream_t, GpuBuildSizes*);                                        \
-  template void gpu_build_finish<R>(GpuBuild*, WtEnt<R>*, int4*, uint16_t*, int4*, int*, cudaStream_t);
+  template void gpu_build_finish<R>(GpuBuild*, WtEnt<R>*, int4*, uint16_t*, int4*, int*, cudaStream_t); \
+  template void gpu_sort_w_tables<R>(int, int64_t, int64_t, int, int*, R*, R*, int*, cudaStream_t);
 
 TOMO_INST_BUILD(float)
 TOMO_INST_BUILD(double)

@@ -270,6 +270,8 @@ struct tomo_op {
   int nq = 0, Ppad = 0;
   int n_tasks = 0, n_heavy = 0, n_slots = 0;
   Raw apod, tw, wcols, wvals, wbase, wxs, wys, wtent, wttasks, wtperm, wtheavy, wtslotheavy;
+  Raw wperm;           // separable-W table position -> sample (grid-tile order)
+  bool w_sorted = false;
   TaskSet gram;  // fused backend only
   const TspmFile* src = nullptr;  // during tomo_op_create_tspm: the loaded Gram / surrogate T
   int w_sep = 1;  // W storage used by the interpolation kernel (TOMO_W_FORMAT=ell selects SELL-32)
@@ -319,6 +321,7 @@ struct tomo_op {
     d.w_base = wbase.as<int>();
     d.w_x = wxs.as<R>();
     d.w_y = wys.as<R>();
+    d.w_perm = w_sorted ? wperm.as<int>() : nullptr;
     d.w = g.w;
     d.w_sep = w_sep;
     d.wt_ent = wtent.as<WtEnt<R>>();
@@ -824,6 +827,14 @@ void build_tables(tomo_op* op) {
     build_w_gpu<R>(op);
   else
     build_w_host<R>(op);
+  // separable W in 16x16 grid-tile order: concurrently running warps gather from nearby nodes
+  const char* word = std::getenv("TOMO_W_ORDER");
+  op->w_sorted = op->w_sep && !(word && std::string(word) == "angle");
+  if (op->w_sorted) {
+    op->wperm.ensure(sizeof(int) * std::max<int64_t>(g.P, 1));
+    gpu_sort_w_tables<R>(m, g.P, op->Ppad, w, op->wbase.as<int>(), op->wxs.as<R>(), op->wys.as<R>(),
+                         op->wperm.as<int>(), 0);
+  }
   // deapodisation a[t]/m (nufft.cpp:204-227 with the 1/m per-axis FFT scale folded in)
   std::vector<R> apod(g.n);
   const double root = std::sqrt(M_PI / g.tau);
