@@ -69,7 +69,11 @@ struct OpDev {
   const R* w_x;                    // [w][Ppad]
   const R* w_y;                    // [w][Ppad]
   const int* w_perm;               // [P] table position -> sample index: the separable tables are
-                                   // stored in grid-tile order (spatial locality of the gathers)
+                                   // stored in grid-tile order (spatial locality of the gathers).
+                                   // With w_perm set, the op's internal sample vectors (W output,
+                                   // W^T input, W^T entry indices) use positions; the reference
+                                   // order only at the API boundary (forward/adjoint).
+  int w_out_pos;                   // W writes sample t at position t (1) or at w_perm[t] (0)
   int w;                           // window width
   int w_sep;                       // 1: use the separable storage for W, 0: the SELL-32 ELL
   // W^T: nodes of each grid row sorted by entry count (SELL-32-sigma, sigma = one grid row);
@@ -190,7 +194,10 @@ void launch_t1_rows(const OpDev<R>& d, int B, const PbEpi<R>& e, cudaStream_t st
 template <typename R>
 void launch_wt_grid(const OpDev<R>& d, int B, const cplx<R>* samples, cplx<R>* grid, cudaStream_t st);
 template <typename R>
-void launch_weight_samples(cplx<R>* s, int B, int P, int nb, cudaStream_t st);
+void launch_weight_samples(cplx<R>* s, int B, int P, int nb, const int* perm, cudaStream_t st);
+// out[b][t] = in[b][perm[t]] (reference sample order -> the op's position order)
+template <typename R>
+void launch_gather_samples(const cplx<R>* in, cplx<R>* out, const int* perm, int B, int P, cudaStream_t st);
 template <typename R>
 void launch_fft_rows_test(int m, int rows, const cplx<R>* tw, const cplx<R>* in, cplx<R>* out, bool inverse,
                           cudaStream_t st);
@@ -220,7 +227,8 @@ void gpu_build_free(GpuBuild* b);
 // Re-order the separable W tables (base, wx, wy; [Ppad] / [w][Ppad]) by 16x16 grid tile of the
 // window base; perm[t] = sample stored at position t.
 template <typename R>
-void gpu_sort_w_tables(int m, int64_t P, int64_t Ppad, int w, int* base, R* wx, R* wy, int* perm, cudaStream_t st);
+void gpu_sort_w_tables(int m, int64_t P, int64_t Ppad, int w, int* base, R* wx, R* wy, int* perm, WtEnt<R>* ent,
+                       int64_t n_ent, cudaStream_t st);
 
 // ---- launchers (solver.cu) ----
 struct StencilCoef {

@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(256) k_w_sep(OpDev<R> d, int B, const cplx<R>*
   using C2 = cplx<R>;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;  // table position
   if (t >= d.P) return;
-  const int j = d.w_perm ? __ldg(&d.w_perm[t]) : t;    // sample
+  const int j = d.w_perm && !d.w_out_pos ? __ldg(&d.w_perm[t]) : t;  // output index
   const int m = d.m, w = d.w;
   const int base = __ldg(&d.w_base[t]);
   const int ix0 = base & 0xffff, iy0 = base >> 16;
@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(256) k_w_sep_wide(OpDev<R> d, int B, const cpl
   using C2 = cplx<R>;
   const int tp = blockIdx.x * blockDim.x + threadIdx.x;  // table position
   if (tp >= d.P) return;
-  const int j = d.w_perm ? __ldg(&d.w_perm[tp]) : tp;   // sample
+  const int j = d.w_perm && !d.w_out_pos ? __ldg(&d.w_perm[tp]) : tp;  // output index
   const int m = d.m, w = d.w;
   const int base = __ldg(&d.w_base[tp]);
   const int ix0 = base & 0xffff, iy0 = base >> 16;
@@ -708,13 +708,23 @@ k_t1_rows_p(OpDev<R> d, PbEpi<R> e) {
 
 // Radial density weights |k_r| (DC: 1/4), normal_ops.cpp:208-219, applied to samples.
 template <typename R>
-__global__ void k_weight_samples(cplx<R>* s, int B, int P, int nb) {
+__global__ void k_weight_samples(cplx<R>* s, int B, int P, int nb, const int* __restrict__ perm) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= static_cast<int64_t>(B) * P) return;
-  const int j = static_cast<int>(i % P);
+  const int t = static_cast<int>(i % P);
+  const int j = perm ? perm[t] : t;  // reference sample index
   const int kr = (j % nb) - nb / 2;
   const R w = kr == 0 ? R(0.25) : static_cast<R>(kr < 0 ? -kr : kr);
   s[i] = cscale(s[i], w);
+}
+
+template <typename R>
+__global__ void k_gather_samples(const cplx<R>* __restrict__ in, cplx<R>* __restrict__ out, const int* __restrict__ perm,
+                                 int B, int P) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= static_cast<int64_t>(B) * P) return;
+  const int64_t b = i / P, t = i - b * P;
+  out[i] = in[b * P + (perm ? perm[t] : t)];
 }
 
 template <int M, int RB, typename R>
@@ -1016,10 +1026,17 @@ void launch_wt_grid(const OpDev<R>& d, int B, const cplx<R>* samples, cplx<R>* g
 }
 
 template <typename R>
-void launch_weight_samples(cplx<R>* s, int B, int P, int nb, cudaStream_t st) {
+void launch_weight_samples(cplx<R>* s, int B, int P, int nb, const int* perm, cudaStream_t st) {
   // angle blocks hold whole angles: t = j % nb is unchanged by a shard offset
   const int64_t total = static_cast<int64_t>(B) * P;
-  CK_LAUNCH(launch_k(k_weight_samples<R>, static_cast<unsigned>((total + 255) / 256), 256, 0, st, s, B, P, nb));
+  CK_LAUNCH(launch_k(k_weight_samples<R>, static_cast<unsigned>((total + 255) / 256), 256, 0, st, s, B, P, nb, perm));
+  note_launch();
+}
+
+template <typename R>
+void launch_gather_samples(const cplx<R>* in, cplx<R>* out, const int* perm, int B, int P, cudaStream_t st) {
+  const int64_t total = static_cast<int64_t>(B) * P;
+  CK_LAUNCH(launch_k(k_gather_samples<R>, static_cast<unsigned>((total + 255) / 256), 256, 0, st, in, out, perm, B, P));
   note_launch();
 }
 
@@ -1047,7 +1064,8 @@ void launch_fft_rows_test(int m, int rows, const cplx<R>* tw, const cplx<R>* in,
   template void launch_gram<R>(const OpDev<R>&, int, const cplx<R>*, cplx<R>*, const SliceScalars*, cudaStream_t); \
   template void launch_t1_rows<R>(const OpDev<R>&, int, const PbEpi<R>&, cudaStream_t);                     \
   template void launch_wt_grid<R>(const OpDev<R>&, int, const cplx<R>*, cplx<R>*, cudaStream_t);            \
-  template void launch_weight_samples<R>(cplx<R>*, int, int, int, cudaStream_t);                            \
+  template void launch_weight_samples<R>(cplx<R>*, int, int, int, const int*, cudaStream_t);               \
+  template void launch_gather_samples<R>(const cplx<R>*, cplx<R>*, const int*, int, int, cudaStream_t);     \
   template void launch_fft_rows_test<R>(int, int, const cplx<R>*, const cplx<R>*, cplx<R>*, bool, cudaStream_t);
 
 TOMO_INST_NUFFT(float)

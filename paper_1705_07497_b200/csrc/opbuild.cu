@@ -407,10 +407,21 @@ __global__ void k_gather_w(int64_t P, int64_t Ppad, int w, const int* __restrict
     wy_out[a * Ppad + t] = wy_in[a * Ppad + j];
   }
 }
+__global__ void k_inverse(int64_t P, const int* __restrict__ perm, int* pos) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t < P) pos[perm[t]] = static_cast<int>(t);
+}
+
+template <typename R>
+__global__ void k_remap_ent(int64_t n, const int* __restrict__ pos, WtEnt<R>* ent) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) ent[i].j = pos[ent[i].j];
+}
 }  // namespace
 
 template <typename R>
-void gpu_sort_w_tables(int m, int64_t P, int64_t Ppad, int w, int* base, R* wx, R* wy, int* perm, cudaStream_t st) {
+void gpu_sort_w_tables(int m, int64_t P, int64_t Ppad, int w, int* base, R* wx, R* wy, int* perm, WtEnt<R>* ent,
+                       int64_t n_ent, cudaStream_t st) {
   if (P <= 0) return;
   DBuf<unsigned long long> keys(P), skeys(P);
   DBuf<int> idx(P);
@@ -433,6 +444,12 @@ void gpu_sort_w_tables(int m, int64_t P, int64_t Ppad, int w, int* base, R* wx, 
   BK(cudaMemcpyAsync(base, b2.p, sizeof(int) * Ppad, cudaMemcpyDeviceToDevice, st));
   BK(cudaMemcpyAsync(wx, x2.p, sizeof(R) * w * Ppad, cudaMemcpyDeviceToDevice, st));
   BK(cudaMemcpyAsync(wy, y2.p, sizeof(R) * w * Ppad, cudaMemcpyDeviceToDevice, st));
+  if (ent && n_ent > 0) {  // W^T entries index samples by position from now on
+    DBuf<int> pos(P);
+    k_inverse<<<grid, 256, 0, st>>>(P, perm, pos.p);
+    k_remap_ent<R><<<static_cast<unsigned>((n_ent + 255) / 256), 256, 0, st>>>(n_ent, pos.p, ent);
+    BK(cudaGetLastError());
+  }
   BK(cudaStreamSynchronize(st));
 }
 
@@ -440,7 +457,7 @@ void gpu_sort_w_tables(int m, int64_t P, int64_t Ppad, int w, int* base, R* wx, 
   template GpuBuild* gpu_build_begin<R>(const BuildArgs&, const double*, const double*, int*, R*, R*,         \
                                         cudaStream_t, GpuBuildSizes*);                                        \
   template void gpu_build_finish<R>(GpuBuild*, WtEnt<R>*, int4*, uint16_t*, int4*, int*, cudaStream_t); \
-  template void gpu_sort_w_tables<R>(int, int64_t, int64_t, int, int*, R*, R*, int*, cudaStream_t);
+  template void gpu_sort_w_tables<R>(int, int64_t, int64_t, int, int*, R*, R*, int*, WtEnt<R>*, int64_t, cudaStream_t);
 
 TOMO_INST_BUILD(float)
 TOMO_INST_BUILD(double)

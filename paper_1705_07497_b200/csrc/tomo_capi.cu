@@ -322,6 +322,7 @@ struct tomo_op {
     d.w_x = wxs.as<R>();
     d.w_y = wys.as<R>();
     d.w_perm = w_sorted ? wperm.as<int>() : nullptr;
+    d.w_out_pos = w_sorted ? 1 : 0;
     d.w = g.w;
     d.w_sep = w_sep;
     d.wt_ent = wtent.as<WtEnt<R>>();
@@ -833,7 +834,7 @@ void build_tables(tomo_op* op) {
   if (op->w_sorted) {
     op->wperm.ensure(sizeof(int) * std::max<int64_t>(g.P, 1));
     gpu_sort_w_tables<R>(m, g.P, op->Ppad, w, op->wbase.as<int>(), op->wxs.as<R>(), op->wys.as<R>(),
-                         op->wperm.as<int>(), 0);
+                         op->wperm.as<int>(), op->wtent.as<WtEnt<R>>(), op->wt_slots, 0);
   }
   // deapodisation a[t]/m (nufft.cpp:204-227 with the 1/m per-axis FFT scale folded in)
   std::vector<R> apod(g.n);
@@ -876,19 +877,33 @@ void allreduce(tomo_op* op, R* buf, size_t count, cudaStream_t st) {
   }
 }
 
+// F_NU^* into d.s (the op's internal sample order) or, with ext_out, into an external buffer in
+// the reference's sample order.
 template <typename R>
-void type2(tomo_op* op, int B, const void* in, bool complex_in, const PUpd<R>& pu, cplx<R>* samples_out,
+void type2(tomo_op* op, int B, const void* in, bool complex_in, const PUpd<R>& pu, cplx<R>* ext_out,
            const SliceScalars* skip, cudaStream_t st) {
   OpDev<R> d = op->dev<R>(B);
   launch_t2_rows<R>(d, B, in, complex_in, pu, st);
   launch_t2_cols<R>(d, B, skip, st);
-  launch_w<R>(d, B, d.g, samples_out ? samples_out : d.s, skip, st);
+  if (ext_out) d.w_out_pos = 0;
+  launch_w<R>(d, B, d.g, ext_out ? ext_out : d.s, skip, st);
 }
 
+// External samples (reference order) -> d.s in the op's internal order.
 template <typename R>
-void type1(tomo_op* op, int B, const cplx<R>* samples, const PbEpi<R>& e, const SliceScalars* skip, cudaStream_t st) {
+cplx<R>* samples_in(tomo_op* op, int B, const cplx<R>* ext, cudaStream_t st) {
   OpDev<R> d = op->dev<R>(B);
-  if (samples) d.s = const_cast<cplx<R>*>(samples);
+  if (op->w_sorted)
+    launch_gather_samples<R>(ext, d.s, d.w_perm, B, static_cast<int>(op->g.P), st);
+  else if (ext != d.s)
+    CK(cudaMemcpyAsync(d.s, ext, sizeof(cplx<R>) * B * op->g.P, cudaMemcpyDeviceToDevice, st));
+  return d.s;
+}
+
+// F_NU of the samples in d.s (internal order).
+template <typename R>
+void type1(tomo_op* op, int B, const PbEpi<R>& e, const SliceScalars* skip, cudaStream_t st) {
+  OpDev<R> d = op->dev<R>(B);
   launch_wt_rows<R>(d, B, skip, st);
   launch_t1_rows<R>(d, B, e, st);
 }
@@ -1018,16 +1033,14 @@ void cg_run(tomo_op* op, int B, const SysParams& s, const R* rhs, const R* x0, R
 // Back-projection alpha*Re(F_NU f) (solver.cpp:200-213), optionally density weighted.
 template <typename R>
 void backproject(tomo_op* op, int B, double alpha, bool weighted, const cplx<R>* f, R* out, cudaStream_t st) {
-  const cplx<R>* src = f;
+  cplx<R>* s = samples_in<R>(op, B, f, st);
   if (weighted) {
     OpDev<R> d = op->dev<R>(B);
-    CK(cudaMemcpyAsync(d.s, f, sizeof(cplx<R>) * B * op->g.P, cudaMemcpyDeviceToDevice, st));
-    launch_weight_samples<R>(d.s, B, static_cast<int>(op->g.P), op->g.nb, st);
-    src = d.s;
+    launch_weight_samples<R>(s, B, static_cast<int>(op->g.P), op->g.nb, d.w_perm, st);
   }
   PbEpi<R> e = plain_epi<R>(PB_REAL, alpha);
   e.out_r = out;
-  type1<R>(op, B, src, e, nullptr, st);
+  type1<R>(op, B, e, nullptr, st);
   allreduce<R>(op, out, static_cast<size_t>(B) * op->L(), st);
 }
 
@@ -1177,11 +1190,11 @@ void build_stencil(tomo_op* op, cudaStream_t st) {
   CK(cudaMemcpyAsync(S.cin.p, delta.data(), sizeof(cplx<R>) * L, cudaMemcpyHostToDevice, st));
   OpDev<R> d = op->dev<R>(1);
   PUpd<R> pu{};
-  type2<R>(op, 1, S.cin.p, true, pu, d.s, nullptr, st);
-  launch_weight_samples<R>(d.s, 1, static_cast<int>(op->g.P), op->g.nb, st);
+  type2<R>(op, 1, S.cin.p, true, pu, nullptr, nullptr, st);
+  launch_weight_samples<R>(d.s, 1, static_cast<int>(op->g.P), op->g.nb, d.w_perm, st);
   PbEpi<R> e = plain_epi<R>(PB_REAL, 1.0);
   e.out_r = S.fout.as<R>();
-  type1<R>(op, 1, d.s, e, nullptr, st);
+  type1<R>(op, 1, e, nullptr, st);
   std::vector<R> resp(L);
   CK(cudaMemcpyAsync(resp.data(), S.fout.p, sizeof(R) * L, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -1592,7 +1605,8 @@ int tomo_adjoint(tomo_op* op, const void* samples, void* image, int batch, void*
     OutArg o(image, cnt * sizeof(cplx<R>), op->sc.cout);
     PbEpi<R> e = plain_epi<R>(PB_COMPLEX, 1.0);
     e.out_c = static_cast<cplx<R>*>(o.dev);
-    type1<R>(op, batch, static_cast<const cplx<R>*>(din), e, nullptr, st);
+    samples_in<R>(op, batch, static_cast<const cplx<R>*>(din), st);
+    type1<R>(op, batch, e, nullptr, st);
     allreduce<R>(op, static_cast<R*>(o.dev), cnt * 2, st);
     o.finish(st);
   });
@@ -1611,6 +1625,7 @@ int tomo_spmv_w(tomo_op* op, const void* grid, void* samples, int batch, void* s
     const void* din = stage_in(grid, gcnt * sizeof(cplx<R>), op->sc.cin, st);
     OutArg o(samples, scnt * sizeof(cplx<R>), op->sc.cout);
     OpDev<R> d = op->dev<R>(batch);
+    d.w_out_pos = 0;  // reference sample order at the API
     launch_w<R>(d, batch, static_cast<const cplx<R>*>(din), static_cast<cplx<R>*>(o.dev), nullptr, st);
     o.finish(st);
   });
@@ -1629,7 +1644,8 @@ int tomo_spmv_wt(tomo_op* op, const void* samples, void* grid, int batch, void* 
     const void* din = stage_in(samples, scnt * sizeof(cplx<R>), op->sc.cin, st);
     OutArg o(grid, gcnt * sizeof(cplx<R>), op->sc.cout);
     OpDev<R> d = op->dev<R>(batch);
-    launch_wt_grid<R>(d, batch, static_cast<const cplx<R>*>(din), static_cast<cplx<R>*>(o.dev), st);
+    launch_wt_grid<R>(d, batch, samples_in<R>(op, batch, static_cast<const cplx<R>*>(din), st),
+                      static_cast<cplx<R>*>(o.dev), st);
     o.finish(st);
   });
   TOMO_CATCH
