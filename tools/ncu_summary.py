@@ -70,6 +70,31 @@ def summarise(raw_csv, cfg, tag):
     return "\n".join(md) + "\n", {k: int(sum(v) / len(v)) for k, v in traffic.items()}
 
 
+def launches(csv_path, md_path, title):
+    """Per-stage share of a `--metrics gpu__time_duration.sum` launch list."""
+    from collections import Counter
+    rows = [r for r in csv.reader(open(csv_path)) if len(r) > 5]
+    h = rows[0]
+    ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    tot, cnt = Counter(), Counter()
+    for r in rows[1:]:
+        st = stage_of(r[ki])
+        if not st:
+            continue
+        v = num(r[vi])
+        v = v / 1000 if r[ui] in ("ns", "nsecond") else v
+        tot[st] += v
+        cnt[st] += 1
+    T = sum(tot.values()) or 1
+    lines = [f"# {title}", "",
+             "Consecutive launches inside the timed solve (`tools/profile.sh`). Cold-cache, serialised per-launch",
+             "times: compare the SHARE of the step with bench.py's live `stage_share_of_step`.", "",
+             "| stage | launches | mean µs | share |", "|---|---|---|---|"]
+    for st in sorted(tot, key=lambda k: -tot[k]):
+        lines.append(f"| {st} | {cnt[st]} | {tot[st] / cnt[st]:.2f} | {tot[st] / T:.3f} |")
+    open(md_path, "w").write("\n".join(lines) + "\n")
+
+
 if __name__ == "__main__":
     tag = sys.argv[1]
     src = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "gpurun_out")
@@ -84,3 +109,9 @@ if __name__ == "__main__":
         tj[cfg] = traffic
         print(cfg, traffic)
     json.dump(tj, open(tj_path, "w"), indent=1)
+    lc = os.path.join(src, f"{tag}_launches_c2.csv")
+    if os.path.exists(lc):
+        import shutil
+        shutil.copy(lc, os.path.join(ROOT, "profiles", f"{tag}_launches_c2.csv"))
+        launches(lc, os.path.join(ROOT, "profiles", f"{tag}_launches_c2_summary.md"),
+                 "Launch list of the default bench (c2) — `ncu --metrics gpu__time_duration.sum --clock-control none`")

@@ -13,7 +13,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"$K" -s 600 -
     --log-file $OUT/${TAG}_launches_c2.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline > $OUT/${TAG}_launches_c2.log 2>&1
 # one full capture of each kernel of one solver step per config
 for c in c2 c3 c4 c5; do
-  case $c in c4) skip=200; cnt=3;; c5) skip=40; cnt=9;; *) skip=60; cnt=7;; esac
+  case $c in c4) skip=800; cnt=3;; c5) skip=40; cnt=9;; *) skip=60; cnt=7;; esac
   KK=$K; [ $c = c4 ] && KK='k_stencil|k_cg_update|k_sb_post'
   timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"$KK" -s $skip -c $cnt \
       -o $REP/${TAG}_full_$c python bench.py --config $c --steps 1 --warmup 1 --no-cpu-baseline \
