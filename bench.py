@@ -229,9 +229,11 @@ class Workload:
             self.calls = c["applies"] // self.batch
             self.chunk = max(d for d in range(1, 51) if self.calls % d == 0)
             self.graph = None
-            self.u_host = self.u.cpu().pin_memory()
-            self.out_host = torch.empty(self.batch, g.n, g.n, dtype=torch.complex64).pin_memory()
-            self.h2d = self.d2h = self.u.numel() * 8 * self.calls
+            # end to end: host batches of up to 50 pinned slices per call; the library streams them
+            # (host->device of slice i+1 and device->host of slice i-1 overlap the apply of slice i)
+            self.e2e_batch = max(d for d in range(1, 51) if c["applies"] % d == 0)
+            self.u_host = self.u[0].expand(self.e2e_batch, g.n, g.n).contiguous().cpu().pin_memory()
+            self.h2d = self.d2h = g.n * g.n * 8 * c["applies"]
         elif kind == "cp":
             if world > 1:
                 # one large slice sharded by angle blocks: every rank owns the W rows
@@ -261,9 +263,10 @@ class Workload:
             self.out = torch.empty_like(self.u)
             self.units_per_step = c["applies"] + c["cg"] + 1
             self.f_host = self.f.cpu().pin_memory()
-            self.u_host = self.u.cpu().pin_memory()
-            self.h2d = self.f.numel() * 16 + self.u.numel() * 8
-            self.d2h = g.n * g.n * 8 * 2
+            # end to end: the 100 applies as one host batch (streamed through the library)
+            self.u_host = self.u.expand(c["applies"], g.n, g.n).contiguous().cpu().pin_memory()
+            self.h2d = self.f.numel() * 16 + self.u_host.numel() * 8
+            self.d2h = g.n * g.n * 8 * (c["applies"] + 1)
         else:
             raise SystemExit(f"unknown workload kind {kind}")
 
@@ -314,11 +317,10 @@ class Workload:
             for i in range(0, self.nslices, self.batch):
                 self.op.split_bregman(self.f_host[i:i + self.batch], self.cfg)
         elif k == "apply":
-            for _ in range(self.calls):
+            for _ in range(self.c["applies"] // self.e2e_batch):
                 self.op.apply_normal(self.u_host)
         elif k == "c1":
-            for _ in range(self.c["applies"]):
-                self.op.apply_normal_real(self.u_host)
+            self.op.apply_normal_real(self.u_host)
             self.op.tikhonov(self.f_host, alpha=self.c["alpha"], steps=self.c["cg"])
         elif k == "cp":
             c = self.c

@@ -288,9 +288,19 @@ struct tomo_op {
   ncclComm_t comm = nullptr;
   std::map<std::string, GraphEntry> graphs;
 
+  // host-buffer pipeline (host_pipeline): copy streams, events, double-buffered staging
+  cudaStream_t pipe_in = nullptr, pipe_out = nullptr;
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
+  Raw pin_buf[2], pout_buf[2];
+
   ~tomo_op() {
     clear_graphs();
     if (comm) ncclCommDestroy(comm);
+    for (int k = 0; k < 2; ++k)
+      for (cudaEvent_t e : {ev_in[k], ev_comp[k], ev_out[k]})
+        if (e) cudaEventDestroy(e);
+    if (pipe_in) cudaStreamDestroy(pipe_in);
+    if (pipe_out) cudaStreamDestroy(pipe_out);
   }
   void clear_graphs() {
     for (auto& kv : graphs)
@@ -1341,6 +1351,52 @@ struct OutArg {
   }
 };
 
+// Host input and host output, several slices: stream the batch in chunks, host->device copy of
+// chunk c+1 and device->host copy of chunk c-1 on their own streams while chunk c computes on
+// `st` (double-buffered staging; the op's scratch is used by one chunk at a time). Pinned host
+// buffers make the copies asynchronous; pageable ones still give the right answer.
+template <typename F>
+bool host_pipeline(tomo_op* op, int batch, const void* in, size_t in_per, void* out, size_t out_per, cudaStream_t st,
+                   F&& compute) {
+  if (batch < 2 || !in || !out || is_device_ptr(in) || is_device_ptr(out)) return false;
+  const int chunk = std::max(1, std::min(std::max(1, op->desc.max_batch), (batch + 1) / 2));
+  if (!op->pipe_in) {
+    CK(cudaStreamCreateWithFlags(&op->pipe_in, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&op->pipe_out, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+      CK(cudaEventCreateWithFlags(&op->ev_in[k], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&op->ev_comp[k], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&op->ev_out[k], cudaEventDisableTiming));
+    }
+  }
+  for (int k = 0; k < 2; ++k) {
+    op->pin_buf[k].ensure(in_per * chunk);
+    op->pout_buf[k].ensure(out_per * chunk);
+  }
+  CK(cudaEventRecord(op->ev_comp[0], st));  // staging free: nothing in flight yet
+  CK(cudaEventRecord(op->ev_comp[1], st));
+  CK(cudaEventRecord(op->ev_out[0], st));
+  CK(cudaEventRecord(op->ev_out[1], st));
+  const auto* src = static_cast<const unsigned char*>(in);
+  auto* dst = static_cast<unsigned char*>(out);
+  for (int c0 = 0, c = 0; c0 < batch; c0 += chunk, ++c) {
+    const int nb = std::min(chunk, batch - c0), k = c & 1;
+    CK(cudaStreamWaitEvent(op->pipe_in, op->ev_comp[k], 0));  // chunk c-2 no longer reads pin_buf[k]
+    CK(cudaMemcpyAsync(op->pin_buf[k].p, src + in_per * c0, in_per * nb, cudaMemcpyHostToDevice, op->pipe_in));
+    CK(cudaEventRecord(op->ev_in[k], op->pipe_in));
+    CK(cudaStreamWaitEvent(st, op->ev_in[k], 0));
+    CK(cudaStreamWaitEvent(st, op->ev_out[k], 0));  // chunk c-2 copied out of pout_buf[k]
+    compute(nb, op->pin_buf[k].p, op->pout_buf[k].p);
+    CK(cudaEventRecord(op->ev_comp[k], st));
+    CK(cudaStreamWaitEvent(op->pipe_out, op->ev_comp[k], 0));
+    CK(cudaMemcpyAsync(dst + out_per * c0, op->pout_buf[k].p, out_per * nb, cudaMemcpyDeviceToHost, op->pipe_out));
+    CK(cudaEventRecord(op->ev_out[k], op->pipe_out));
+  }
+  CK(cudaStreamSynchronize(op->pipe_out));
+  CK(cudaStreamSynchronize(st));
+  return true;
+}
+
 int fail(const std::exception& e, int code) {
   g_err = e.what();
   return code;
@@ -1525,6 +1581,10 @@ int tomo_apply_normal(tomo_op* op, const void* in, void* out, int batch, void* s
   const cudaStream_t st = S_(stream);
   with_prec(op, [&](auto tag) {
     using R = decltype(tag);
+    if (!op->surrogate() &&
+        host_pipeline(op, batch, in, op->L() * sizeof(cplx<R>), out, op->L() * sizeof(cplx<R>), st,
+                      [&](int nb, const void* din, void* dout) { normal_direct<R>(op, nb, din, true, dout, st); }))
+      return;
     const size_t cnt = static_cast<size_t>(batch) * op->L();
     const void* din = stage_in(in, cnt * sizeof(cplx<R>), op->sc.cin, st);
     OutArg o(out, cnt * sizeof(cplx<R>), op->sc.cout);
@@ -1560,6 +1620,10 @@ int tomo_apply_normal_real(tomo_op* op, const void* in, void* out, int batch, vo
   const cudaStream_t st = S_(stream);
   with_prec(op, [&](auto tag) {
     using R = decltype(tag);
+    if (!op->surrogate() &&
+        host_pipeline(op, batch, in, op->L() * sizeof(R), out, op->L() * sizeof(R), st,
+                      [&](int nb, const void* din, void* dout) { normal_direct<R>(op, nb, din, false, dout, st); }))
+      return;
     const size_t cnt = static_cast<size_t>(batch) * op->L();
     const void* din = stage_in(in, cnt * sizeof(R), op->sc.fin, st);
     OutArg o(out, cnt * sizeof(R), op->sc.fout);
@@ -1583,9 +1647,14 @@ int tomo_forward(tomo_op* op, const void* image, void* samples, int batch, void*
     using R = decltype(tag);
     const size_t cnt = static_cast<size_t>(batch) * op->L();
     const size_t scnt = static_cast<size_t>(batch) * op->g.P;
+    PUpd<R> pu{};
+    if (host_pipeline(op, batch, image, op->L() * sizeof(cplx<R>), samples, op->g.P * sizeof(cplx<R>), st,
+                      [&](int nb, const void* din, void* dout) {
+                        type2<R>(op, nb, din, true, pu, static_cast<cplx<R>*>(dout), nullptr, st);
+                      }))
+      return;
     const void* din = stage_in(image, cnt * sizeof(cplx<R>), op->sc.cin, st);
     OutArg o(samples, scnt * sizeof(cplx<R>), op->sc.cout);
-    PUpd<R> pu{};
     type2<R>(op, batch, din, true, pu, static_cast<cplx<R>*>(o.dev), nullptr, st);
     o.finish(st);
   });
@@ -1601,13 +1670,18 @@ int tomo_adjoint(tomo_op* op, const void* samples, void* image, int batch, void*
     using R = decltype(tag);
     const size_t cnt = static_cast<size_t>(batch) * op->L();
     const size_t scnt = static_cast<size_t>(batch) * op->g.P;
+    auto adj = [&](int nb, const void* din, void* dout) {
+      PbEpi<R> e = plain_epi<R>(PB_COMPLEX, 1.0);
+      e.out_c = static_cast<cplx<R>*>(dout);
+      samples_in<R>(op, nb, static_cast<const cplx<R>*>(din), st);
+      type1<R>(op, nb, e, nullptr, st);
+      allreduce<R>(op, static_cast<R*>(dout), static_cast<size_t>(nb) * op->L() * 2, st);
+    };
+    if (host_pipeline(op, batch, samples, op->g.P * sizeof(cplx<R>), image, op->L() * sizeof(cplx<R>), st, adj))
+      return;
     const void* din = stage_in(samples, scnt * sizeof(cplx<R>), op->sc.cin, st);
     OutArg o(image, cnt * sizeof(cplx<R>), op->sc.cout);
-    PbEpi<R> e = plain_epi<R>(PB_COMPLEX, 1.0);
-    e.out_c = static_cast<cplx<R>*>(o.dev);
-    samples_in<R>(op, batch, static_cast<const cplx<R>*>(din), st);
-    type1<R>(op, batch, e, nullptr, st);
-    allreduce<R>(op, static_cast<R*>(o.dev), cnt * 2, st);
+    adj(batch, din, o.dev);
     o.finish(st);
   });
   TOMO_CATCH

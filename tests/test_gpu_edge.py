@@ -83,3 +83,24 @@ def test_empty_batch_is_a_config_error(T):
     buf = cuda(np.zeros((og.n, og.n)), True)
     rc = _lib.lib().tomo_apply_normal(op._h, C.c_void_p(buf.data_ptr()), C.c_void_p(buf.data_ptr()), 0, None)
     assert rc == _lib.TOMO_ERR_CONFIG and b"batch" in _lib.lib().tomo_last_error()
+
+
+def test_host_batches_are_streamed(T):
+    """Host input + host output with several slices go through the chunked host<->device
+    pipeline (tomo_capi.cu host_pipeline); results equal the device-resident path."""
+    og = O.Geometry(**GEOMS["width6_odd_nb"])
+    rng = np.random.default_rng(21)
+    for prec in ("f32", "f64"):
+        f64 = prec == "f64"
+        op = T.make_direct_backend(pgeom(T, og), precision=prec, max_batch=2)
+        u = rng.standard_normal((7, og.n, og.n)) + 1j * rng.standard_normal((7, og.n, og.n))
+        dev = cuda(u, True, f64)
+        pinned = dev.cpu().pin_memory()
+        for fn in (op.apply_normal, op.forward):
+            want = fn(dev).cpu().numpy()
+            got = fn(pinned)
+            assert got.is_pinned() and np.array_equal(got.numpy(), want)
+        s = op.forward(dev)
+        assert np.array_equal(op.adjoint(s.cpu().pin_memory()).numpy(), op.adjoint(s).cpu().numpy())
+        ur = dev.real.contiguous()
+        assert np.array_equal(op.apply_normal_real(ur.cpu().pin_memory()).numpy(), op.apply_normal_real(ur).cpu().numpy())
