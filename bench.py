@@ -38,7 +38,9 @@ CONFIGS = {
                metric="normal-op applies/sec", unit="applies/s"),
     "c2": dict(n=512, A=90, nb=725, R=2, lo=-2, hi=3, kind="sb", alpha=10.0, lam=1.0, iters=50, cg=10, prec="f64",
                metric="split-Bregman slices/sec", unit="slices/s"),
-    "c3": dict(n=1024, A=180, nb=1449, R=2, lo=-2, hi=3, kind="apply", applies=1000, prec="f32",
+    # 1000 applies on random-normal inputs, issued as calls of 2 independent inputs that the
+    # library runs on two concurrent lanes (streams with their own grids)
+    "c3": dict(n=1024, A=180, nb=1449, R=2, lo=-2, hi=3, kind="apply", applies=1000, batch=2, prec="f32",
                metric="normal-op applies/sec", unit="applies/s"),
     "c4": dict(n=512, A=120, nb=725, R=2, lo=-2, hi=3, kind="sb_sur", alpha=1.0, lam=1.0, iters=30, cg=5, r=1,
                slices=256, prec="f32", metric="split-Bregman slices/sec", unit="slices/s"),
@@ -545,7 +547,7 @@ def main():
                        "window": [c["lo"], c["hi"]], "m": info.m, "P": int(info.P), "nnz_W": int(info.nnz),
                        "wt_rows": int(info.wt_rows), "wt_slots": int(info.wt_slots), "precision": c["prec"],
                        "l2": "flushed between timed steps (256 MiB write)",
-                       **{k: c[k] for k in ("alpha", "lam", "iters", "cg", "applies", "slices", "r") if k in c},
+                       **{k: c[k] for k in ("alpha", "lam", "iters", "cg", "applies", "slices", "r", "batch") if k in c},
                        "parallelism": f"{'slice-sharded' if c['kind'] == 'sb_sur' else ('angle-sharded' if wl.sharded else 'replicas')} x{world}"},
             "roofline": roof,
             "cpu_baseline": cpu,

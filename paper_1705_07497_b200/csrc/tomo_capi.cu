@@ -288,6 +288,12 @@ struct tomo_op {
   ncclComm_t comm = nullptr;
   std::map<std::string, GraphEntry> graphs;
 
+  // second execution lane for batches of independent slices (apply paths): its own grids and
+  // W^T partial/ticket buffers and its own stream, so two sub-batches run concurrently
+  Scratch lane1;
+  int cur_lane = 0;  // dev() hands out lane-1 buffers while this is 1
+  cudaStream_t lane_st = nullptr;
+  cudaEvent_t lane_fork = nullptr, lane_join = nullptr;
   // host-buffer pipeline (host_pipeline): copy streams, events, double-buffered staging
   cudaStream_t pipe_in = nullptr, pipe_out = nullptr;
   cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
@@ -301,6 +307,9 @@ struct tomo_op {
         if (e) cudaEventDestroy(e);
     if (pipe_in) cudaStreamDestroy(pipe_in);
     if (pipe_out) cudaStreamDestroy(pipe_out);
+    if (lane_fork) cudaEventDestroy(lane_fork);
+    if (lane_join) cudaEventDestroy(lane_join);
+    if (lane_st) cudaStreamDestroy(lane_st);
   }
   void clear_graphs() {
     for (auto& kv : graphs)
@@ -316,6 +325,8 @@ struct tomo_op {
   template <typename R>
   OpDev<R> dev(int B) {
     ensure_batch(B);
+    if (cur_lane) ensure_lane(B);
+    Scratch& sc = cur_lane ? lane1 : this->sc;
     OpDev<R> d{};
     d.n = g.n;
     d.m = g.m;
@@ -385,6 +396,29 @@ struct tomo_op {
     sc.upd_log.ensure(sizeof(double) * static_cast<size_t>(B) * kMaxLoggedIters);
     sc.cap = B;
     clear_graphs();  // buffers moved
+  }
+
+  // lane-1 grids (the apply path only: no solver vectors or scalars)
+  void ensure_lane(int B) {
+    if (B <= lane1.cap) return;
+    const size_t m = g.m, n = g.n, cz = 2 * rsz;
+    lane1.H.ensure(B * m * n * cz);
+    lane1.g.ensure(B * m * m * cz);
+    lane1.Gt.ensure(B * m * m * cz);
+    CK(cudaMemset(lane1.Gt.p, 0, B * m * m * cz));
+    lane1.part_wt.ensure(static_cast<size_t>(B) * std::max(n_slots, 1) * 32 * cz);
+    lane1.heavy_cnt.ensure(sizeof(unsigned) * static_cast<size_t>(B) * std::max(n_heavy, 1));
+    CK(cudaMemset(lane1.heavy_cnt.p, 0, sizeof(unsigned) * static_cast<size_t>(B) * std::max(n_heavy, 1)));
+    if (fused()) {
+      lane1.part_gram.ensure(static_cast<size_t>(B) * std::max(gram.n_slots, 1) * 32 * cz);
+      const size_t hb = sizeof(unsigned) * static_cast<size_t>(B) * std::max(gram.n_heavy, 1);
+      lane1.heavy_cnt_gram.ensure(hb);
+      CK(cudaMemset(lane1.heavy_cnt_gram.p, 0, hb));
+    }
+    lane1.s.ensure(B * static_cast<size_t>(g.P) * cz);
+    lane1.K.ensure(B * n * m * cz);
+    lane1.cap = B;
+    clear_graphs();
   }
 
   Reduce red() { return Reduce{sc.sc.as<SliceScalars>(), sc.part.as<double>()}; }
@@ -944,6 +978,44 @@ void normal_core(tomo_op* op, int B, const void* in, bool complex_in, const PUpd
   }
   launch_t1_cols_only<R>(d, B, skip, st);
   launch_t1_rows<R>(d, B, e, st);
+}
+
+// Two-lane execution of a batch of independent slices: the first half on `st` (lane 0), the
+// second half on the op's lane stream with lane-1 buffers, forked from and joined back into `st`
+// with events (also inside CUDA-graph capture). Two lanes overlap the latency-bound passes of
+// one apply with those of another (c3: 8.4k -> 11.0k applies/s measured with two handles).
+// f(b0, nb, stream) runs slices [b0, b0 + nb) of the batch.
+template <typename F>
+void two_lanes(tomo_op* op, int batch, cudaStream_t st, F&& f) {
+  static const bool enabled = [] {
+    const char* v = std::getenv("TOMO_LANES");
+    return !(v && v[0] == '1');
+  }();
+  if (batch < 2 || !enabled || op->sharded()) {
+    f(0, batch, st);
+    return;
+  }
+  if (!op->lane_st) {
+    CK(cudaStreamCreateWithFlags(&op->lane_st, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&op->lane_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&op->lane_join, cudaEventDisableTiming));
+  }
+  const int b0 = (batch + 1) / 2;
+  op->ensure_batch(b0);
+  op->ensure_lane(batch - b0);
+  CK(cudaEventRecord(op->lane_fork, st));
+  CK(cudaStreamWaitEvent(op->lane_st, op->lane_fork, 0));
+  f(0, b0, st);
+  op->cur_lane = 1;
+  try {
+    f(b0, batch - b0, op->lane_st);
+  } catch (...) {
+    op->cur_lane = 0;
+    throw;
+  }
+  op->cur_lane = 0;
+  CK(cudaEventRecord(op->lane_join, op->lane_st));
+  CK(cudaStreamWaitEvent(st, op->lane_join, 0));
 }
 
 // Re(N u) (or N u complex) for the W/W^T and Gram backends, incl. the cross-rank sum when
@@ -1606,7 +1678,11 @@ int tomo_apply_normal(tomo_op* op, const void* in, void* out, int batch, void* s
       CK(cudaMemcpy2DAsync(static_cast<R*>(o.dev) + 1, 2 * sizeof(R), op->sc.fout.as<R>() + cnt, sizeof(R), sizeof(R),
                            cnt, cudaMemcpyDeviceToDevice, st));
     } else {
-      normal_direct<R>(op, batch, din, true, o.dev, st);
+      const size_t L = op->L();
+      two_lanes(op, batch, st, [&](int b0, int nb, cudaStream_t ls) {
+        normal_direct<R>(op, nb, static_cast<const cplx<R>*>(din) + b0 * L, true,
+                         static_cast<cplx<R>*>(o.dev) + b0 * L, ls);
+      });
     }
     o.finish(st);
   });
@@ -1631,7 +1707,10 @@ int tomo_apply_normal_real(tomo_op* op, const void* in, void* out, int batch, vo
       launch_stencil<R>(op->g.n, batch, op->rad, op->coef, 2, static_cast<const R*>(din), nullptr, nullptr,
                         static_cast<R*>(o.dev), nullptr, nullptr, sysp(1.0, 0.0, 0.0, 0.0), 0, op->red(), st);
     } else {
-      normal_direct<R>(op, batch, din, false, o.dev, st);
+      const size_t L = op->L();
+      two_lanes(op, batch, st, [&](int b0, int nb, cudaStream_t ls) {
+        normal_direct<R>(op, nb, static_cast<const R*>(din) + b0 * L, false, static_cast<R*>(o.dev) + b0 * L, ls);
+      });
     }
     o.finish(st);
   });
