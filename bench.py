@@ -333,7 +333,8 @@ class Workload:
     def roofline(self, peak_gbs):
         c = self.c
         k = c["kind"]
-        B = self.batch if k in ("sb_sur", "apply") else 1
+        # the kernels as launched: c4 batches; c3 calls of `batch` inputs run as two lanes of batch/2
+        B = self.batch if k == "sb_sur" else ((self.batch + 1) // 2 if k == "apply" else 1)
         prof = self.op.profile_stages(batch=B, reps=10)
         if k in ("sb", "c1", "cp"):
             steps = c.get("cg", 10)
