@@ -145,18 +145,64 @@ __global__ void __launch_bounds__(256) k_stencil(int n, StencilCoef coef, int mo
   for (int k = threadIdx.x; k < SIDE * SIDE; k += blockDim.x) cf[k] = static_cast<R>(coef.c[k]);
   const size_t off = static_cast<size_t>(b) * n * n;
   const int i0 = blockIdx.y * kTile - HALO, j0 = blockIdx.x * kTile - HALO;
-  // the halo tile: W*W/256 ~ 17 loads per thread, issued 6 at a time (unrolled: independent loads)
-#pragma unroll 6
-  for (int idx = threadIdx.x; idx < W * W; idx += blockDim.x) {
-    const int li = idx / W, lj = idx - li * W;
-    const int gi = i0 + li, gj = j0 + lj;
-    R v = 0;
-    if (gi >= 0 && gi < n && gj >= 0 && gj < n) {
-      const size_t o = off + static_cast<size_t>(gi) * n + gj;
-      v = in[o];
-      if (mode == 0 && step > 0) v = r_in[o] + beta * v;
+  // the halo tile. n % (16/sizeof R) == 0: the kTile interior columns of each row with 16-byte
+  // vector loads (aligned: they start at a multiple of kTile), the 2*HALO halo columns scalar;
+  // otherwise every element scalar.
+  auto put = [&](int li, int lj, R v, R rv) {
+    q[li][lj] = (mode == 0 && step > 0) ? rv + beta * v : v;
+  };
+  constexpr int VW = 16 / sizeof(R);
+  if (n % VW == 0) {
+    using V = typename Vec16<R>::T;
+    constexpr int VPR = kTile / VW;  // vectors per interior row
+#pragma unroll 4
+    for (int idx = threadIdx.x; idx < W * VPR; idx += blockDim.x) {
+      const int li = idx / VPR, vq = idx - li * VPR;
+      const int gi = i0 + li, gj = j0 + HALO + vq * VW;
+      R v[VW], rv[VW];
+#pragma unroll
+      for (int e = 0; e < VW; ++e) v[e] = rv[e] = R(0);
+      if (gi >= 0 && gi < n && gj < n) {
+        const size_t o = off + static_cast<size_t>(gi) * n + gj;
+        const V a = *reinterpret_cast<const V*>(in + o);
+        const R* ae = reinterpret_cast<const R*>(&a);
+#pragma unroll
+        for (int e = 0; e < VW; ++e) v[e] = ae[e];
+        if (mode == 0 && step > 0) {
+          const V rr = *reinterpret_cast<const V*>(r_in + o);
+          const R* re = reinterpret_cast<const R*>(&rr);
+#pragma unroll
+          for (int e = 0; e < VW; ++e) rv[e] = re[e];
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < VW; ++e) put(li, HALO + vq * VW + e, v[e], rv[e]);
     }
-    q[li][lj] = v;
+    for (int idx = threadIdx.x; idx < W * 2 * HALO; idx += blockDim.x) {
+      const int li = idx / (2 * HALO), h = idx - li * (2 * HALO);
+      const int lj = h < HALO ? h : kTile + h;
+      const int gi = i0 + li, gj = j0 + lj;
+      R v = 0, rv = 0;
+      if (gi >= 0 && gi < n && gj >= 0 && gj < n) {
+        const size_t o = off + static_cast<size_t>(gi) * n + gj;
+        v = in[o];
+        if (mode == 0 && step > 0) rv = r_in[o];
+      }
+      put(li, lj, v, rv);
+    }
+  } else {
+#pragma unroll 6
+    for (int idx = threadIdx.x; idx < W * W; idx += blockDim.x) {
+      const int li = idx / W, lj = idx - li * W;
+      const int gi = i0 + li, gj = j0 + lj;
+      R v = 0, rv = 0;
+      if (gi >= 0 && gi < n && gj >= 0 && gj < n) {
+        const size_t o = off + static_cast<size_t>(gi) * n + gj;
+        v = in[o];
+        if (mode == 0 && step > 0) rv = r_in[o];
+      }
+      put(li, lj, v, rv);
+    }
   }
   __syncthreads();
   // each thread: one column, kTile / kTileRows consecutive rows, the (2RAD+1)^2 neighbourhood in
