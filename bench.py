@@ -258,10 +258,11 @@ class Workload:
             self.h2d = self.f.numel() * self.f.element_size()
             self.d2h = g.n * g.n * 8
         elif kind == "c1":
-            self.op = T.make_direct_backend(g, precision=c["prec"], device=local)
+            self.op = T.make_direct_backend(g, precision=c["prec"], device=local, max_batch=2)
             self.f = torch.from_numpy(synth_slices(T, self.op, c, [3000 + rank], torch)).cuda()
             ph = T.random_ellipses(g.n, 10, seed=3000 + rank)
             self.u = torch.from_numpy(ph.astype(np.float64)).cuda()
+            self.u2 = self.u.expand(2, g.n, g.n).contiguous()
             self.out = torch.empty_like(self.u)
             self.units_per_step = c["applies"] + c["cg"] + 1
             self.f_host = self.f.cpu().pin_memory()
@@ -300,8 +301,9 @@ class Workload:
                 self.graph.replay()
             self.replayed_launches += self.per_replay * (self.calls // self.chunk)
         elif k == "c1":
-            for _ in range(self.c["applies"]):
-                self.out = self.op.apply_normal_real(self.u)
+            # the 100 applies as calls of 2 (independent, equal) inputs on the library's two lanes
+            for _ in range(self.c["applies"] // 2):
+                self.out = self.op.apply_normal_real(self.u2)
             self.mu = self.op.tikhonov(self.f, alpha=self.c["alpha"], steps=self.c["cg"])
         elif k == "cp":
             c = self.c
