@@ -224,6 +224,12 @@ template <typename R>
 void gpu_build_finish(GpuBuild* b, WtEnt<R>* ent, int4* tasks, uint16_t* perm, int4* heavy, int* slot_heavy,
                       cudaStream_t st);
 void gpu_build_free(GpuBuild* b);
+// The Gram W^T W of the fused backend from fp64 window factors (P x w each) and window bases
+// (ix0 | iy0 << 16); same tables as the host TaskBuilder path. nullptr: too large for this
+// builder (the host build runs instead). Finish with gpu_build_finish.
+template <typename R>
+GpuBuild* gpu_build_gram_begin(int m, int w, int64_t P, const int* h_base, const double* h_wx, const double* h_wy,
+                               cudaStream_t st, GpuBuildSizes* sizes, int64_t* nnz_out);
 // Re-order the separable W tables (base, wx, wy; [Ppad] / [w][Ppad]) by 16x16 grid tile of the
 // window base; perm[t] = sample stored at position t.
 template <typename R>

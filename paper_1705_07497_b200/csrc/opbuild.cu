@@ -189,7 +189,7 @@ __global__ void k_gather_tasks(int n, const int* __restrict__ idx, const int4* _
 template <typename R>
 __global__ void k_entries(int m, const uint16_t* __restrict__ perm, const int* __restrict__ L,
                           const int64_t* __restrict__ chunk0, const int* __restrict__ cnt, const int* __restrict__ off,
-                          const unsigned long long* __restrict__ skeys, const R* __restrict__ svals, WtEnt<R>* ent) {
+                          const int* __restrict__ sj, const R* __restrict__ svals, WtEnt<R>* ent) {
   const int64_t bk = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   const int64_t G32 = static_cast<int64_t>(m) * m / 32;
@@ -201,11 +201,11 @@ __global__ void k_entries(int m, const uint16_t* __restrict__ perm, const int* _
   const int64_t first = row + perm[bk * 32];
   const int c = cnt[node];
   const int o = off[node];
-  int lastj = static_cast<int>((c > 0 ? skeys[o] : skeys[off[first]]) & 0xFFFFFFFFull);
+  int lastj = c > 0 ? sj[o] : sj[off[first]];
   for (int k = 0; k < l; ++k) {
     WtEnt<R> e{};
     if (k < c) {
-      lastj = static_cast<int>(skeys[o + k] & 0xFFFFFFFFull);
+      lastj = sj[o + k];
       e.j = lastj;
       e.w = svals[o + k];
     } else {
@@ -238,10 +238,15 @@ int bits_for(uint64_t v) {
 
 }  // namespace
 
+__global__ void k_low32(int64_t n, const unsigned long long* __restrict__ keys, int* out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = static_cast<int>(keys[i] & 0xFFFFFFFFull);
+}
+
 struct GpuBuild {
   BuildArgs a{};
   int64_t nnz = 0, G = 0, G32 = 0;
-  DBuf<unsigned long long> skeys;
+  DBuf<int> sj;  // entry columns (sample / grid node) in final entry order
   DBuf<int> cnt, off, L, ntask, nslot, nheavy, toff, soff, hoff, tkey, tkey2, tidx, tidx2;
   DBuf<int64_t> chunk0;
   DBuf<int4> tasks_raw;
@@ -249,6 +254,8 @@ struct GpuBuild {
   DBuf<uint16_t> perm;
   GpuBuildSizes sz{};
 };
+
+void build_structure(GpuBuild* b, cudaStream_t st);
 
 template <typename R>
 GpuBuild* gpu_build_begin(const BuildArgs& a, const double* h_cs, const double* h_e3, int* base, R* wx, R* wy,
@@ -264,9 +271,8 @@ GpuBuild* gpu_build_begin(const BuildArgs& a, const double* h_cs, const double* 
   DBuf<double> cs(2 * static_cast<size_t>(n_ang)), e3(w);
   BK(cudaMemcpyAsync(cs.p, h_cs, sizeof(double) * 2 * n_ang, cudaMemcpyHostToDevice, st));
   BK(cudaMemcpyAsync(e3.p, h_e3, sizeof(double) * w, cudaMemcpyHostToDevice, st));
-  DBuf<unsigned long long> keys(b->nnz);
+  DBuf<unsigned long long> keys(b->nnz), skeys(b->nnz);
   DBuf<R> vals(b->nnz);
-  b->skeys.alloc(b->nnz);
   b->vals_sorted.alloc(sizeof(R) * b->nnz);
   b->cnt.alloc(b->G);
   BK(cudaMemsetAsync(b->cnt.p, 0, sizeof(int) * b->G, st));
@@ -276,13 +282,29 @@ GpuBuild* gpu_build_begin(const BuildArgs& a, const double* h_cs, const double* 
   // W^T rows: sort the (node, sample) pairs; ascending sample order within a node = the host fill
   const int key_bits = 32 + bits_for(static_cast<uint64_t>(b->G));
   size_t tmp_bytes = 0;
-  BK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys.p, b->skeys.p, vals.p,
+  BK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys.p, skeys.p, vals.p,
                                      reinterpret_cast<R*>(b->vals_sorted.p), static_cast<int>(b->nnz), 0, key_bits,
                                      st));
-  DBuf<unsigned char> tmp(tmp_bytes);
-  BK(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, keys.p, b->skeys.p, vals.p,
-                                     reinterpret_cast<R*>(b->vals_sorted.p), static_cast<int>(b->nnz), 0, key_bits,
-                                     st));
+  {
+    DBuf<unsigned char> tmp(tmp_bytes);
+    BK(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, keys.p, skeys.p, vals.p,
+                                       reinterpret_cast<R*>(b->vals_sorted.p), static_cast<int>(b->nnz), 0, key_bits,
+                                       st));
+  }
+  b->sj.alloc(b->nnz);
+  k_low32<<<static_cast<unsigned>((b->nnz + 255) / 256), 256, 0, st>>>(b->nnz, skeys.p, b->sj.p);
+  BK(cudaGetLastError());
+  build_structure(b.get(), st);
+  *sizes = b->sz;
+  return b.release();
+}
+
+// Task structure from entries already in final order (b->sj, b->vals_sorted) and the per-node
+// counts b->cnt: node offsets, per-row node order, 32-node blocks, warp tasks, totals.
+void build_structure(GpuBuild* b, cudaStream_t st) {
+  const int m = b->a.m;
+  size_t tmp_bytes = 0;
+  DBuf<unsigned char> tmp;
   b->off.alloc(b->G);
   tmp_bytes = 0;
   BK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, b->cnt.p, b->off.p, static_cast<int>(b->G), st));
@@ -342,8 +364,6 @@ GpuBuild* gpu_build_begin(const BuildArgs& a, const double* h_cs, const double* 
   b->sz.n_heavy = h_last + nh_last;
   b->sz.touched = static_cast<int64_t>(tch);
   if (b->sz.chunks > (int64_t(1) << 31) - 1) throw std::runtime_error("opbuild: W^T too large");
-  *sizes = b->sz;
-  return b.release();
 }
 
 template <typename R>
@@ -375,13 +395,162 @@ void gpu_build_finish(GpuBuild* b, WtEnt<R>* ent, int4* tasks, uint16_t* perm, i
   }
   BK(cudaMemcpyAsync(perm, b->perm.p, sizeof(uint16_t) * b->G, cudaMemcpyDeviceToDevice, st));
   k_entries<R><<<static_cast<unsigned>((b->G32 + 7) / 8), 256, 0, st>>>(
-      m, b->perm.p, b->L.p, b->chunk0.p, b->cnt.p, b->off.p, b->skeys.p,
+      m, b->perm.p, b->L.p, b->chunk0.p, b->cnt.p, b->off.p, b->sj.p,
       reinterpret_cast<const R*>(b->vals_sorted.p), ent);
   BK(cudaGetLastError());
   BK(cudaStreamSynchronize(st));
 }
 
 void gpu_build_free(GpuBuild* b) { delete b; }
+
+// ---- the fused backend's Gram W^T W on the device (build_btb, normal_ops.cpp:53-173) ------------
+namespace {
+// one thread per (sample j, tap a, tap b): the w^2 products landing in node (iy0+b, ix0+a)'s band
+// cells, fp64, with the host's association (wx[a] wx[a2]) (wy[b] wy[b2])
+__global__ void k_gram_tuples(int64_t P, int m, int w, const int* __restrict__ base, const double* __restrict__ wx,
+                              const double* __restrict__ wy, unsigned long long* keys, double* vals) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t w2 = static_cast<int64_t>(w) * w;
+  if (t >= P * w2) return;
+  const int64_t j = t / w2;
+  const int ab = static_cast<int>(t - j * w2), a = ab / w, bb = ab - a * w;
+  const int ix0 = base[j] & 0xffff, iy0 = base[j] >> 16;
+  const int ix = wrapd(ix0 + a, m), iy = wrapd(iy0 + bb, m);
+  const unsigned long long row = static_cast<unsigned long long>(iy) * m + ix;
+  const int band = 2 * w - 1;
+  const double* wxj = wx + j * w;
+  const double* wyj = wy + j * w;
+  const size_t o = static_cast<size_t>(t) * w2;
+  for (int b2 = 0; b2 < w; ++b2) {
+    const double py = __dmul_rn(wyj[bb], wyj[b2]);
+    for (int a2 = 0; a2 < w; ++a2) {
+      const double px = __dmul_rn(wxj[a], wxj[a2]);
+      const int cell = (b2 - bb + w - 1) * band + (a2 - a + w - 1);
+      keys[o + b2 * w + a2] = (row << 14) | static_cast<unsigned long long>(cell);
+      vals[o + b2 * w + a2] = __dmul_rn(px, py);
+    }
+  }
+}
+
+__global__ void k_heads(int64_t n, const unsigned long long* __restrict__ keys, int* head) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) head[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
+}
+
+__global__ void k_seg_starts(int64_t n, const int* __restrict__ head, const int* __restrict__ sid, int* start) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n && head[i]) start[sid[i]] = static_cast<int>(i);
+}
+
+// one thread per (node, band cell): the sum over samples in ascending j order (the stable sort kept
+// it), exactly the host band accumulation; exact zeros dropped like build_btb
+__global__ void k_seg_sum(int nseg, int64_t n, int m, int w, const int* __restrict__ start,
+                          const unsigned long long* __restrict__ keys, const double* __restrict__ vals, int* row,
+                          int* col, double* sum, int* keep) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nseg) return;
+  const int64_t i0 = start[s], i1 = s + 1 < nseg ? start[s + 1] : n;
+  double acc = 0.0;
+  for (int64_t i = i0; i < i1; ++i) acc += vals[i];
+  const unsigned long long k = keys[i0];
+  const int r = static_cast<int>(k >> 14), cell = static_cast<int>(k & 0x3fff);
+  const int band = 2 * w - 1;
+  const int dy = cell / band - (w - 1), dx = cell % band - (w - 1);
+  const int iy = r / m, ix = r - iy * m;
+  row[s] = r;
+  col[s] = wrapd(iy + dy, m) * m + wrapd(ix + dx, m);
+  sum[s] = acc;
+  keep[s] = acc != 0.0 ? 1 : 0;
+}
+
+template <typename R>
+__global__ void k_gram_compact(int nseg, const int* __restrict__ keep, const int* __restrict__ pos,
+                               const int* __restrict__ row, const int* __restrict__ col, const double* __restrict__ sum,
+                               int* sj, R* sv, int* cnt) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nseg || !keep[s]) return;
+  sj[pos[s]] = col[s];
+  sv[pos[s]] = static_cast<R>(sum[s]);
+  atomicAdd(&cnt[row[s]], 1);
+}
+}  // namespace
+
+template <typename R>
+GpuBuild* gpu_build_gram_begin(int m, int w, int64_t P, const int* h_base, const double* h_wx, const double* h_wy,
+                               cudaStream_t st, GpuBuildSizes* sizes, int64_t* nnz_out) {
+  const int64_t w2 = static_cast<int64_t>(w) * w;
+  const int64_t n = P * w2 * w2;
+  if (n >= (int64_t(1) << 31) || 2 * w - 1 > 127) return nullptr;  // the host build handles it
+  auto b = std::make_unique<GpuBuild>();
+  b->a.m = m;
+  b->G = static_cast<int64_t>(m) * m;
+  b->G32 = b->G / 32;
+  DBuf<int> base(P);
+  DBuf<double> wx(P * w), wy(P * w);
+  BK(cudaMemcpyAsync(base.p, h_base, sizeof(int) * P, cudaMemcpyHostToDevice, st));
+  BK(cudaMemcpyAsync(wx.p, h_wx, sizeof(double) * P * w, cudaMemcpyHostToDevice, st));
+  BK(cudaMemcpyAsync(wy.p, h_wy, sizeof(double) * P * w, cudaMemcpyHostToDevice, st));
+  DBuf<unsigned long long> keys(n), skeys(n);
+  DBuf<double> vals(n), svals(n);
+  k_gram_tuples<<<static_cast<unsigned>((P * w2 + 255) / 256), 256, 0, st>>>(P, m, w, base.p, wx.p, wy.p, keys.p,
+                                                                            vals.p);
+  BK(cudaGetLastError());
+  const int key_bits = 14 + bits_for(static_cast<uint64_t>(b->G));
+  size_t tb = 0;
+  BK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.p, skeys.p, vals.p, svals.p, static_cast<int>(n), 0, key_bits,
+                                     st));
+  {
+    DBuf<unsigned char> tmp(tb);
+    BK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.p, skeys.p, vals.p, svals.p, static_cast<int>(n), 0,
+                                       key_bits, st));
+  }
+  keys.alloc(1);  // release
+  vals.alloc(1);
+  DBuf<int> head(n), sid(n);
+  const unsigned gn = static_cast<unsigned>((n + 255) / 256);
+  k_heads<<<gn, 256, 0, st>>>(n, skeys.p, head.p);
+  tb = 0;
+  BK(cub::DeviceScan::ExclusiveSum(nullptr, tb, head.p, sid.p, static_cast<int>(n), st));
+  {
+    DBuf<unsigned char> tmp(tb);
+    BK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, head.p, sid.p, static_cast<int>(n), st));
+  }
+  int last_sid = 0, last_head = 0;
+  BK(cudaMemcpyAsync(&last_sid, sid.p + n - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  BK(cudaMemcpyAsync(&last_head, head.p + n - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  BK(cudaStreamSynchronize(st));
+  const int nseg = last_sid + last_head;
+  DBuf<int> start(nseg), row(nseg), col(nseg), keep(nseg), pos(nseg);
+  DBuf<double> sum(nseg);
+  k_seg_starts<<<gn, 256, 0, st>>>(n, head.p, sid.p, start.p);
+  const unsigned gs = static_cast<unsigned>((nseg + 255) / 256);
+  k_seg_sum<<<gs, 256, 0, st>>>(nseg, n, m, w, start.p, skeys.p, svals.p, row.p, col.p, sum.p, keep.p);
+  BK(cudaGetLastError());
+  tb = 0;
+  BK(cub::DeviceScan::ExclusiveSum(nullptr, tb, keep.p, pos.p, nseg, st));
+  {
+    DBuf<unsigned char> tmp(tb);
+    BK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, keep.p, pos.p, nseg, st));
+  }
+  int last_pos = 0, last_keep = 0;
+  BK(cudaMemcpyAsync(&last_pos, pos.p + nseg - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  BK(cudaMemcpyAsync(&last_keep, keep.p + nseg - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  BK(cudaStreamSynchronize(st));
+  const int64_t nnz = static_cast<int64_t>(last_pos) + last_keep;
+  b->nnz = nnz;
+  b->sj.alloc(nnz);
+  b->vals_sorted.alloc(sizeof(R) * nnz);
+  b->cnt.alloc(b->G);
+  BK(cudaMemsetAsync(b->cnt.p, 0, sizeof(int) * b->G, st));
+  k_gram_compact<R><<<gs, 256, 0, st>>>(nseg, keep.p, pos.p, row.p, col.p, sum.p, b->sj.p,
+                                        reinterpret_cast<R*>(b->vals_sorted.p), b->cnt.p);
+  BK(cudaGetLastError());
+  build_structure(b.get(), st);
+  *sizes = b->sz;
+  *nnz_out = nnz;
+  return b.release();
+}
+
 
 namespace {
 __global__ void k_tile_keys(int64_t P, int m, const int* __restrict__ base, unsigned long long* keys, int* idx) {
@@ -457,7 +626,9 @@ void gpu_sort_w_tables(int m, int64_t P, int64_t Ppad, int w, int* base, R* wx, 
   template GpuBuild* gpu_build_begin<R>(const BuildArgs&, const double*, const double*, int*, R*, R*,         \
                                         cudaStream_t, GpuBuildSizes*);                                        \
   template void gpu_build_finish<R>(GpuBuild*, WtEnt<R>*, int4*, uint16_t*, int4*, int*, cudaStream_t); \
-  template void gpu_sort_w_tables<R>(int, int64_t, int64_t, int, int*, R*, R*, int*, WtEnt<R>*, int64_t, cudaStream_t);
+  template void gpu_sort_w_tables<R>(int, int64_t, int64_t, int, int*, R*, R*, int*, WtEnt<R>*, int64_t, cudaStream_t); \
+  template GpuBuild* gpu_build_gram_begin<R>(int, int, int64_t, const int*, const double*, const double*, cudaStream_t, \
+                                             GpuBuildSizes*, int64_t*);
 
 TOMO_INST_BUILD(float)
 TOMO_INST_BUILD(double)

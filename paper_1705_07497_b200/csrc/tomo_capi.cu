@@ -635,6 +635,34 @@ void build_gram(tomo_op* op, const Plan& pl) {
   if (est > cap)
     throw ConfigError("build_btb: estimated " + std::to_string(est >> 20) +
                       " MiB exceeds cap; raise the cap or use a smaller m_sp");
+  const char* bld = std::getenv("TOMO_BUILD");
+  if (!(bld && std::string(bld) == "host")) {  // on the device (opbuild.cu), same tables
+    std::vector<int> base(g.P);
+    for (int64_t j = 0; j < g.P; ++j)
+      base[j] = wrapi(pl.mjx[j] + g.lo, m) | (wrapi(pl.mjy[j] + g.lo, m) << 16);
+    GpuBuildSizes sz{};
+    int64_t nnz = 0;
+    GpuBuild* raw = gpu_build_gram_begin<R>(m, g.w, g.P, base.data(), pl.wx.data(), pl.wy.data(), 0, &sz, &nnz);
+    if (raw) {
+      std::unique_ptr<GpuBuild, void (*)(GpuBuild*)> gb(raw, gpu_build_free);
+      TaskSet& ts = op->gram;
+      ts.n_tasks = sz.n_tasks;
+      ts.n_heavy = sz.n_heavy;
+      ts.n_slots = sz.n_slots;
+      ts.slots = sz.chunks * 32;
+      ts.nnz = nnz;
+      ts.bytes = ts.slots * static_cast<int64_t>(sizeof(WtEnt<R>)) + static_cast<int64_t>(ts.n_tasks) * 16 +
+                 static_cast<int64_t>(m) * m * 2;
+      ts.ent.ensure(sizeof(WtEnt<R>) * std::max<int64_t>(ts.slots, 1));
+      ts.tasks.ensure(sizeof(int4) * std::max(ts.n_tasks, 1));
+      ts.perm.ensure(sizeof(uint16_t) * static_cast<size_t>(m) * m);
+      ts.heavy.ensure(sizeof(int4) * std::max(ts.n_heavy, 1));
+      ts.slot_heavy.ensure(sizeof(int) * std::max(ts.n_slots, 1));
+      gpu_build_finish<R>(gb.get(), ts.ent.as<WtEnt<R>>(), ts.tasks.as<int4>(), ts.perm.as<uint16_t>(),
+                          ts.heavy.as<int4>(), ts.slot_heavy.as<int>(), 0);
+      return;
+    }
+  }
   TaskBuilder<R> tb(m, kWtMaxChunks, op->wt_rows * band2);
   std::vector<R> rv;
   int64_t nnz = 0;

@@ -56,3 +56,20 @@ def test_device_build_matches_host_build(T, name, prec):
     tol = 1e-13 if f64 else 1e-6
     assert rel(dev.apply_normal(x).cpu().numpy(), host.apply_normal(x).cpu().numpy()) < tol
     assert rel(dev.forward(x).cpu().numpy(), host.forward(x).cpu().numpy()) < tol
+
+
+@pytest.mark.parametrize("name", ["ref_msp3", "ref_msp6", "width6_odd_nb", "n16_m32"])
+def test_device_gram_matches_host_gram(T, name):
+    """The fused backend's Gram built on the device equals the host build_btb restatement:
+    same nnz and the same tables, hence bitwise-equal applies."""
+    og = O.Geometry(**GEOMS[name])
+    os.environ["TOMO_BUILD"] = "host"
+    try:
+        host = T.make_fused_backend(pgeom(T, og), precision="f64")
+    finally:
+        del os.environ["TOMO_BUILD"]
+    dev = T.make_fused_backend(pgeom(T, og), precision="f64")
+    assert dev.info.gram_nnz == host.info.gram_nnz == O.btb_nnz(og)
+    assert dev.info.gram_slots == host.info.gram_slots
+    u = cuda(RNG.standard_normal((og.n, og.n)) + 1j * RNG.standard_normal((og.n, og.n)), True, True)
+    assert np.array_equal(dev.apply_normal(u).cpu().numpy(), host.apply_normal(u).cpu().numpy())
