@@ -104,3 +104,23 @@ def test_host_batches_are_streamed(T):
         assert np.array_equal(op.adjoint(s.cpu().pin_memory()).numpy(), op.adjoint(s).cpu().numpy())
         ur = dev.real.contiguous()
         assert np.array_equal(op.apply_normal_real(ur.cpu().pin_memory()).numpy(), op.apply_normal_real(ur).cpu().numpy())
+
+
+def test_nccl_single_rank_plumbing(T):
+    """The NCCL path of angle-block sharding (tomo_op_attach_nccl + the all-reduce after every
+    adjoint, also inside the captured solver graphs) on a one-rank communicator: a shard's
+    results equal the same shard with a no-op all-reduce hook."""
+    og = O.Geometry(**GEOMS["width6_odd_nb"])
+    g = pgeom(T, og)
+    blk = (0, og.n_angles // 2)
+    hook = T.make_direct_backend(g, precision="f64", angle_block=blk)
+    hook.set_allreduce(lambda *a: None)
+    nccl = T.make_direct_backend(g, precision="f64", angle_block=blk)
+    nccl.attach_nccl(T.nccl_unique_id(), 1, 0)
+    rng = np.random.default_rng(31)
+    u = cuda(rng.standard_normal((og.n, og.n)), False, True)
+    assert np.array_equal(nccl.apply_normal_real(u).cpu().numpy(), hook.apply_normal_real(u).cpu().numpy())
+    f = cuda(rng.standard_normal((og.n_angles // 2) * og.n_b) + 0j, True, True)
+    a = nccl.chambolle_pock(f, alpha=1e-2, lambda_=1e-2, iters=2, cg_steps=3).cpu().numpy()
+    b = hook.chambolle_pock(f, alpha=1e-2, lambda_=1e-2, iters=2, cg_steps=3).cpu().numpy()
+    assert np.array_equal(a, b)
