@@ -168,6 +168,8 @@ typedef struct tomo_sb_config { /* SolverConfig (solver.hpp:51-65) */
   double update_tol_rel;
   int warm_start;
   double sigma_override; /* < 0: surrogate sigma from Lanczos (solver.cpp:175-192) */
+  int data_feedback;     /* outer residual feedback on the data term (solver.hpp:58-61,
+                          * solver.cpp:176-187, 283-286); 0 = off (the reference default) */
 } tomo_sb_config;
 
 typedef struct tomo_sb_trace { /* SolveTrace (solver.hpp:67-80), per slice */

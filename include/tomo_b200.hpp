@@ -89,6 +89,7 @@ struct SolverConfig {
   int max_bregman_iters = 6000, cg_steps_per_update = 5;
   double update_tol_rel = 1e-8;
   bool warm_start = true;
+  bool data_feedback = false;  // solver.hpp:58-61
 };
 
 // tomo::SolveTrace subset (solver.hpp:67-80)
@@ -179,7 +180,7 @@ inline std::pair<std::vector<double>, SolveTrace> split_bregman_tv(const NormalB
                                                                    const SolverConfig& c) {
   const int n = b.geometry().n;
   tomo_sb_config cfg{c.alpha, c.lambda, c.max_bregman_iters, c.cg_steps_per_update, c.update_tol_rel,
-                     c.warm_start ? 1 : 0, -1.0};
+                     c.warm_start ? 1 : 0, -1.0, c.data_feedback ? 1 : 0};
   std::vector<double> mu(static_cast<size_t>(n) * n), upd(c.max_bregman_iters);
   tomo_sb_trace tr{};
   check(tomo_split_bregman(b.handle(), &cfg, slice_data.data(), mu.data(), 1, upd.data(), &tr, nullptr));

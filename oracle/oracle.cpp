@@ -688,7 +688,8 @@ static double tridiag_extreme(const RVec& a, const RVec& b, bool largest) {
 }
 
 // lanczos_extreme_ritz (solver.cpp:97-130).
-static double lanczos(const System& op, int64_t dim, int iters, uint64_t seed, bool largest) {
+template <typename Op>
+static double lanczos(const Op& op, int64_t dim, int iters, uint64_t seed, bool largest) {
   std::mt19937_64 rng(seed);
   std::normal_distribution<double> gauss;
   RVec v(dim);
@@ -721,6 +722,23 @@ static double surrogate_sigma(const Geometry& g, int r, bool euclid, double alph
   return 1.2 * std::max(0.0, -lanczos(base, dim, 40, 7, false));
 }
 
+// With data feedback (solver.cpp:176-187): contraction floor from the largest Ritz value of
+// alpha F W F* - 2 (alpha T + lambda K'K).
+static double surrogate_sigma_feedback(const Geometry& g, int r, bool euclid, double alpha, double lambda) {
+  orc_system s{2, r, euclid ? 1 : 0, alpha, lambda, 0.0, 0};
+  System base = make_system(g, &s);
+  const int64_t dim = static_cast<int64_t>(g.n) * g.n;
+  const RVec wts = radial_weights(g);
+  auto gap = [&g, &wts, &base, alpha](const RVec& u, RVec& out) {
+    RVec tmp;
+    base(u, tmp);
+    const RVec wn = weighted_normal_real(g, wts, u);
+    out.resize(u.size());
+    for (size_t i = 0; i < u.size(); ++i) out[i] = alpha * wn[i] - 2.0 * tmp[i];
+  };
+  return 1.2 * std::max(0.0, 0.5 * lanczos(gap, dim, 40, 7, true));
+}
+
 // backproject (solver.cpp:200-213).
 static RVec backproject(const Geometry& g, int backend, double alpha, const CVec& f) {
   CVec s = f;
@@ -746,7 +764,7 @@ static void from_cvec(const CVec& v, double* p) {
   }
 }
 
-// split_bregman_tv (solver.cpp:219-307); data feedback off (the reference default).
+// split_bregman_tv (solver.cpp:219-307), incl. the optional data feedback.
 static RVec split_bregman(const Geometry& g, const orc_sb_config* c, const CVec& f,
                           double* upd_out, orc_sb_trace* tr) {
   if (!(c->alpha > 0.0)) throw ConfigError("SolverConfig: alpha must be positive");
@@ -759,9 +777,11 @@ static RVec split_bregman(const Geometry& g, const orc_sb_config* c, const CVec&
   const int64_t dim = static_cast<int64_t>(n) * n;
   const bool surrogate = c->backend == 2;
   double sigma = 0.0;
+  const bool feedback = c->data_feedback != 0;
   if (surrogate)
     sigma = c->sigma_override >= 0.0 ? c->sigma_override
-                                     : surrogate_sigma(g, c->surrogate_r, c->euclidean != 0, c->alpha, c->lambda);
+            : feedback ? surrogate_sigma_feedback(g, c->surrogate_r, c->euclidean != 0, c->alpha, c->lambda)
+                       : surrogate_sigma(g, c->surrogate_r, c->euclidean != 0, c->alpha, c->lambda);
   orc_system sd{c->backend, c->surrogate_r, c->euclidean, c->alpha, c->lambda, sigma, 0};
   System sys = make_system(g, &sd);
 
@@ -780,7 +800,8 @@ static RVec split_bregman(const Geometry& g, const orc_sb_config* c, const CVec&
   }
 
   RVec mu(dim, 0.0), dx(dim, 0.0), dy(dim, 0.0), bx(dim, 0.0), by(dim, 0.0);
-  const RVec fid = backproject(g, c->backend, c->alpha, f);
+  CVec fk = f;  // solver.cpp:252-253
+  RVec fid = backproject(g, c->backend, c->alpha, fk);
   const double gamma = 1.0 / c->lambda;
   double min_ritz = std::numeric_limits<double>::infinity();
   double first = 0.0;
@@ -804,6 +825,13 @@ static RVec split_bregman(const Geometry& g, const orc_sb_config* c, const CVec&
       dy[i] = shrink1(gy[i] + by[i], gamma);
       bx[i] += gx[i] - dx[i];
       by[i] += gy[i] - dy[i];
+    }
+    if (feedback) {  // fk += f - F_NU^* mu_next; fidelity rhs = backproject(fk) (solver.cpp:283-286)
+      CVec cm(dim);
+      for (int64_t i = 0; i < dim; ++i) cm[i] = cd(mu_next[i], 0.0);
+      const CVec s_mu = type2(g, cm);
+      for (int64_t j = 0; j < g.P; ++j) fk[j] += f[j] - s_mu[j];
+      fid = backproject(g, c->backend, c->alpha, fk);
     }
     double upd = 0.0;
     bool finite = true;

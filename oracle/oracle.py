@@ -43,7 +43,7 @@ class SbConfig(C.Structure):
     _fields_ = [("backend", C.c_int), ("surrogate_r", C.c_int), ("euclidean", C.c_int),
                 ("alpha", C.c_double), ("lambda_", C.c_double), ("max_iters", C.c_int),
                 ("cg_steps", C.c_int), ("update_tol_rel", C.c_double), ("warm_start", C.c_int),
-                ("sigma_override", C.c_double)]
+                ("sigma_override", C.c_double), ("data_feedback", C.c_int)]
 
 
 class SbTrace(C.Structure):
@@ -364,10 +364,10 @@ def backproject(geom, backend, alpha, f):
 
 
 def split_bregman(geom, f, backend=0, alpha=1.0, lam=1.0, max_iters=10, cg_steps=5,
-                  update_tol_rel=0.0, warm_start=True, r=1, euclidean=False, sigma=None):
+                  update_tol_rel=0.0, warm_start=True, r=1, euclidean=False, sigma=None, feedback=False):
     s, ref = _g(geom)
     cfg = SbConfig(backend, r, int(euclidean), alpha, lam, max_iters, cg_steps, update_tol_rel,
-                   int(warm_start), -1.0 if sigma is None else float(sigma))
+                   int(warm_start), -1.0 if sigma is None else float(sigma), int(feedback))
     ff = _c128(f)
     mu = np.empty(geom.n * geom.n)
     upd = np.zeros(max_iters)

@@ -34,6 +34,7 @@ struct RefSetup {
 };
 
 thread_local int g_nb = 0;  // radial samples per angle for the next setup (0 -> n)
+thread_local int g_feedback = 0;  // SolverConfig::data_feedback for the next ref_split_bregman
 
 RefSetup make_setup(int n, int n_angles, int m_sp, double tau) {
   AngleSet set;
@@ -100,6 +101,8 @@ const char* ref_last_error(void) { return g_err.c_str(); }
 
 // Radial samples per angle for subsequent calls on this thread (0 -> n, the reference).
 void ref_set_nb(int nb) { g_nb = nb; }
+// SolverConfig::data_feedback (solver.hpp:58-61) for subsequent ref_split_bregman calls.
+void ref_set_feedback(int on) { g_feedback = on; }
 
 int ref_points(int n, int A, int m_sp, double tau, double* coords) {
   REF_TRY
@@ -269,6 +272,7 @@ int ref_split_bregman(int n, int A, int m_sp, double tau, int backend, int r, do
   cfg.max_bregman_iters = iters;
   cfg.cg_steps_per_update = cg_steps;
   cfg.update_tol_rel = 0.0;
+  cfg.data_feedback = g_feedback != 0;
   auto res = split_bregman_tv(b, cvec(slice_data, s.grid.points.count()), cfg);
   for (Eigen::Index i = 0; i < res.first.data.size(); ++i) mu[i] = res.first.data[i];
   if (update_l1)

@@ -46,6 +46,7 @@ def lib():
                                                C.c_void_p]
         _LIB.ref_shepp_logan.argtypes = [C.c_int, C.c_void_p]
         _LIB.ref_set_nb.argtypes = [C.c_int]
+        _LIB.ref_set_feedback.argtypes = [C.c_int]
         _LIB.ref_save_btb.argtypes = [C.c_int, C.c_int, C.c_int, d, C.c_char_p]
         _LIB.ref_save_surrogate.argtypes = [C.c_int, C.c_int, C.c_int, d, C.c_int, C.c_int, C.c_char_p]
         _LIB.ref_synthesize.argtypes = [C.c_int, C.c_int, C.c_int, d, C.c_void_p, d, C.c_uint64, C.c_void_p]
@@ -147,14 +148,18 @@ class Ref:
         _check(lib().ref_cg_sb_system(*self._a, alpha, lam, _p(rhs), _p(x0), steps, _p(x), C.byref(mr)))
         return x, mr.value
 
-    def split_bregman(self, f, backend=0, r=1, alpha=1.0, lam=1.0, iters=5, cg_steps=5):
+    def split_bregman(self, f, backend=0, r=1, alpha=1.0, lam=1.0, iters=5, cg_steps=5, feedback=False):
         f = np.ascontiguousarray(f, np.complex128)
         mu = np.empty((self.n, self.n))
         upd = np.empty(iters)
         sg = C.c_double()
         lk = C.c_double()
-        _check(lib().ref_split_bregman(*self._a, backend, r, alpha, lam, iters, cg_steps, _p(f), _p(mu),
-                                       _p(upd), C.byref(sg), C.byref(lk)))
+        lib().ref_set_feedback(int(feedback))
+        try:
+            _check(lib().ref_split_bregman(*self._a, backend, r, alpha, lam, iters, cg_steps, _p(f), _p(mu),
+                                           _p(upd), C.byref(sg), C.byref(lk)))
+        finally:
+            lib().ref_set_feedback(0)
         return mu, upd, sg.value, lk.value
 
     def tikhonov_identity(self, f, alpha=1.0, steps=20):

@@ -111,6 +111,7 @@ typedef struct {
   double update_tol_rel;
   int warm_start;
   double sigma_override; /* < 0 -> compute (Lanczos) */
+  int data_feedback;     /* SolverConfig::data_feedback (solver.cpp:176-187, 283-286) */
 } orc_sb_config;
 
 typedef struct {

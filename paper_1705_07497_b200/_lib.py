@@ -59,7 +59,8 @@ class CgStats(C.Structure):
 
 class SbConfig(C.Structure):
     _fields_ = [("alpha", C.c_double), ("lambda_", C.c_double), ("max_iters", C.c_int), ("cg_steps", C.c_int),
-                ("update_tol_rel", C.c_double), ("warm_start", C.c_int), ("sigma_override", C.c_double)]
+                ("update_tol_rel", C.c_double), ("warm_start", C.c_int), ("sigma_override", C.c_double),
+                ("data_feedback", C.c_int)]
 
 
 class SbTrace(C.Structure):

@@ -30,7 +30,7 @@ def _run_options(p):
     p.add_argument("--iters", type=int, default=c.iters, help="maximum Bregman iterations")
     p.add_argument("--cg-steps", type=int, default=c.cg_steps, help="CG steps per Bregman update")
     p.add_argument("--tol", type=float, default=c.tol, help="relative L1 update stopping threshold")
-    p.add_argument("--feedback", action="store_true", help="outer Bregman data feedback (not supported)")
+    p.add_argument("--feedback", action="store_true", help="outer Bregman data feedback")
     p.add_argument("--noise", type=float, default=c.noise, help="complex noise sigma added to the data")
     p.add_argument("--seed", type=int, default=c.seed, help="seed for all stochastic elements")
     p.add_argument("--cache-dir", default=c.cache_dir, help="precomputed operator cache directory")

@@ -198,6 +198,9 @@ void launch_weight_samples(cplx<R>* s, int B, int P, int nb, const int* perm, cu
 // out[b][t] = in[b][perm[t]] (reference sample order -> the op's position order)
 template <typename R>
 void launch_gather_samples(const cplx<R>* in, cplx<R>* out, const int* perm, int B, int P, cudaStream_t st);
+// fk += f - s, s = fk (split-Bregman data feedback)
+template <typename R>
+void launch_feedback_samples(int64_t n, cplx<R>* fk, const cplx<R>* f, cplx<R>* s, cudaStream_t st);
 template <typename R>
 void launch_fft_rows_test(int m, int rows, const cplx<R>* tw, const cplx<R>* in, cplx<R>* out, bool inverse,
                           cudaStream_t st);

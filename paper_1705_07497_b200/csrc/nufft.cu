@@ -727,6 +727,18 @@ __global__ void k_gather_samples(const cplx<R>* __restrict__ in, cplx<R>* __rest
   out[i] = in[b * P + (perm ? perm[t] : t)];
 }
 
+// split-Bregman data feedback (solver.cpp:283-286): fk += f - F_NU^* mu, and s = fk for the
+// back-projection that follows
+template <typename R>
+__global__ void k_feedback_samples(int64_t n, cplx<R>* __restrict__ fk, const cplx<R>* __restrict__ f,
+                                   cplx<R>* __restrict__ s) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const cplx<R> v = cadd(fk[i], csub(f[i], s[i]));
+  fk[i] = v;
+  s[i] = v;
+}
+
 template <int M, int RB, typename R>
 __global__ void k_fft_rows_test(const cplx<R>* tw, const cplx<R>* in, cplx<R>* out, int rows, int inverse) {
   using S = FftShape<M, RB>;
@@ -1034,6 +1046,12 @@ void launch_weight_samples(cplx<R>* s, int B, int P, int nb, const int* perm, cu
 }
 
 template <typename R>
+void launch_feedback_samples(int64_t n, cplx<R>* fk, const cplx<R>* f, cplx<R>* s, cudaStream_t st) {
+  CK_LAUNCH(launch_k(k_feedback_samples<R>, static_cast<unsigned>((n + 255) / 256), 256, 0, st, n, fk, f, s));
+  note_launch();
+}
+
+template <typename R>
 void launch_gather_samples(const cplx<R>* in, cplx<R>* out, const int* perm, int B, int P, cudaStream_t st) {
   const int64_t total = static_cast<int64_t>(B) * P;
   CK_LAUNCH(launch_k(k_gather_samples<R>, static_cast<unsigned>((total + 255) / 256), 256, 0, st, in, out, perm, B, P));
@@ -1066,6 +1084,7 @@ void launch_fft_rows_test(int m, int rows, const cplx<R>* tw, const cplx<R>* in,
   template void launch_wt_grid<R>(const OpDev<R>&, int, const cplx<R>*, cplx<R>*, cudaStream_t);            \
   template void launch_weight_samples<R>(cplx<R>*, int, int, int, const int*, cudaStream_t);               \
   template void launch_gather_samples<R>(const cplx<R>*, cplx<R>*, const int*, int, int, cudaStream_t);     \
+  template void launch_feedback_samples<R>(int64_t, cplx<R>*, const cplx<R>*, cplx<R>*, cudaStream_t);      \
   template void launch_fft_rows_test<R>(int, int, const cplx<R>*, const cplx<R>*, cplx<R>*, bool, cudaStream_t);
 
 TOMO_INST_NUFFT(float)

@@ -242,6 +242,7 @@ struct Scratch {
   Raw cin, cout, fin, fout;       // staging for host pointers / temporaries
   Raw r, p0, p1, ap, x, rhs, fid, mu0, mu1, bx0, bx1, by0, by1, nred, zero, u2;  // real vectors
   Raw upd_log, rel_log, sc, part;
+  Raw fk, fint;  // split-Bregman data feedback: running data and the slice data, internal order
 };
 
 // Device tables of one task-SpMV operator (the fused backend's Gram; see TaskSpmv).
@@ -1235,9 +1236,13 @@ double device_dot(tomo_op* op, const R* x, const R* y, cudaStream_t st) {
   return v;
 }
 
+// make_subproblem's surrogate shift (solver.cpp:175-192) by 40-step Lanczos (lanczos_extreme_ritz,
+// :97-130; device applies and dots, host tridiagonal bisection). Without data feedback: the PSD
+// floor 1.2 max(0, -lambda_min(alpha T + lambda K'K)); with it: the contraction floor
+// 1.2 max(0, lambda_max(alpha F W F* - 2 (alpha T + lambda K'K)) / 2).
 template <typename R>
-double surrogate_sigma(tomo_op* op, double alpha, double lambda, cudaStream_t st) {
-  auto key = std::make_pair(alpha, lambda);
+double surrogate_sigma(tomo_op* op, double alpha, double lambda, cudaStream_t st, bool feedback = false) {
+  auto key = std::make_pair(alpha, feedback ? -lambda - 1.0 : lambda);  // lambda > 0: distinct keys
   auto it = op->sigma_cache.find(key);
   if (it != op->sigma_cache.end()) return it->second;
   const int n = op->g.n;
@@ -1258,25 +1263,44 @@ double surrogate_sigma(tomo_op* op, double alpha, double lambda, cudaStream_t st
   R* vcur = S.x.as<R>();
   R* vprev = S.p0.as<R>();
   R* w = S.ap.as<R>();
+  R* w2 = S.u2.as<R>();
   CK(cudaMemcpyAsync(vcur, vf.data(), sizeof(R) * L, cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(vprev, 0, sizeof(R) * L, st));
   const SysParams sp = sysp(alpha, lambda, 0.0, 0.0);
   std::vector<double> alphas, betas;
   double beta = 0.0, extreme = 0.0;
   for (int itr = 0; itr < 40; ++itr) {
-    launch_stencil<R>(n, 1, op->rad, op->coef, 2, vcur, nullptr, nullptr, w, nullptr, nullptr, sp, 0, op->red(), st);
+    if (!feedback) {
+      launch_stencil<R>(n, 1, op->rad, op->coef, 2, vcur, nullptr, nullptr, w, nullptr, nullptr, sp, 0, op->red(), st);
+    } else {  // w = alpha Re(F W F* v) - 2 (alpha T + lambda K'K) v
+      launch_stencil<R>(n, 1, op->rad, op->coef, 2, vcur, nullptr, nullptr, w2, nullptr, nullptr, sp, 0, op->red(), st);
+      PUpd<R> pu{};
+      type2<R>(op, 1, vcur, false, pu, nullptr, nullptr, st);
+      OpDev<R> d = op->dev<R>(1);
+      launch_weight_samples<R>(d.s, 1, static_cast<int>(op->g.P), op->g.nb, d.w_perm, st);
+      PbEpi<R> e = plain_epi<R>(PB_REAL, 1.0);
+      e.out_r = w;
+      type1<R>(op, 1, e, nullptr, st);
+      launch_axpby<R>(L, alpha, w, -2.0, w2, w, st);
+    }
     const double a = device_dot<R>(op, vcur, w, st);
     alphas.push_back(a);
     launch_axpby<R>(L, 1.0, w, -a, vcur, w, st);
     launch_axpby<R>(L, 1.0, w, -beta, vprev, w, st);
     beta = std::sqrt(device_dot<R>(op, w, w, st));
-    extreme = tridiag_min(alphas, betas);
+    if (feedback) {  // largest Ritz value: -(smallest of -T)
+      std::vector<double> neg(alphas.size());
+      for (size_t k = 0; k < alphas.size(); ++k) neg[k] = -alphas[k];
+      extreme = -tridiag_min(neg, betas);
+    } else {
+      extreme = tridiag_min(alphas, betas);
+    }
     if (beta < 1e-12) break;
     betas.push_back(beta);
     std::swap(vprev, vcur);                                    // vprev <- v
     launch_axpby<R>(L, 1.0 / beta, w, 0.0, w, vcur, st);       // v <- w / beta
   }
-  const double sigma = 1.2 * std::max(0.0, -extreme);
+  const double sigma = feedback ? 1.2 * std::max(0.0, 0.5 * extreme) : 1.2 * std::max(0.0, -extreme);
   op->sigma_cache[key] = sigma;
   return sigma;
 }
@@ -1913,15 +1937,36 @@ void sb_impl(tomo_op* op, const tomo_sb_config* cfg, const void* slice_data, voi
     Scratch& S = op->sc;
     const bool sur = op->surrogate();
     // make_subproblem (solver.cpp:164-215): sigma, then the leak probe (:236-247)
+    const bool feedback = cfg->data_feedback != 0;
     double sigma = 0.0;
-    if (sur) sigma = cfg->sigma_override >= 0.0 ? cfg->sigma_override : surrogate_sigma<R>(op, cfg->alpha, cfg->lambda, st);
+    if (sur)
+      sigma = cfg->sigma_override >= 0.0 ? cfg->sigma_override
+                                         : surrogate_sigma<R>(op, cfg->alpha, cfg->lambda, st, feedback);
     double leak = 0.0;
     if (!sur) {
       leak = leak_probe<R>(op, st);
       if (leak > 0.1) throw NumericalError("split_bregman_tv: conjugation symmetry broken");
     }
     const auto* din = static_cast<const cplx<R>*>(stage_in(slice_data, scnt * sizeof(cplx<R>), S.cin, st));
+    if (feedback) {  // fk = f (solver.cpp:252), both kept in the op's internal sample order
+      S.fk.ensure(scnt * sizeof(cplx<R>));
+      S.fint.ensure(scnt * sizeof(cplx<R>));
+      const cplx<R>* fi = samples_in<R>(op, batch, din, st);
+      CK(cudaMemcpyAsync(S.fint.p, fi, scnt * sizeof(cplx<R>), cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(S.fk.p, fi, scnt * sizeof(cplx<R>), cudaMemcpyDeviceToDevice, st));
+    }
     backproject<R>(op, batch, cfg->alpha, sur, din, S.fid.as<R>(), st);
+    // data feedback after the CG of an iteration: fk += f - F_NU^* mu_next, fid = backproject(fk)
+    auto feedback_step = [&](R* mu_next, cudaStream_t cs) {
+      PUpd<R> pu{};
+      type2<R>(op, batch, mu_next, false, pu, nullptr, nullptr, cs);
+      OpDev<R> d = op->dev<R>(batch);
+      launch_feedback_samples<R>(static_cast<int64_t>(scnt), S.fk.as<cplx<R>>(), S.fint.as<cplx<R>>(), d.s, cs);
+      if (sur) launch_weight_samples<R>(d.s, batch, static_cast<int>(op->g.P), op->g.nb, d.w_perm, cs);
+      PbEpi<R> e = plain_epi<R>(PB_REAL, cfg->alpha);
+      e.out_r = S.fid.as<R>();
+      type1<R>(op, batch, e, nullptr, cs);
+    };
     CK(cudaMemcpyAsync(S.rhs.p, S.fid.p, sizeof(R) * cnt, cudaMemcpyDeviceToDevice, st));
     for (auto* b : {&S.mu0, &S.bx0, &S.by0}) CK(cudaMemsetAsync(b->p, 0, sizeof(R) * cnt, st));
     std::vector<SliceScalars> init(batch);
@@ -1936,12 +1981,13 @@ void sb_impl(tomo_op* op, const tomo_sb_config* cfg, const void* slice_data, voi
     std::vector<cudaEvent_t> ev;
     if (!record) {
       const std::string key = fmtkey("sb", batch, {cfg->alpha, cfg->lambda, sigma, double(iters), double(cfg->cg_steps),
-                                                   double(cfg->warm_start)});
+                                                   double(cfg->warm_start), double(feedback)});
       run_graph(op, key, st, [&](cudaStream_t cs) {
         for (int it = 0; it < iters; ++it) {
           const int p = it & 1;
           cg_run<R>(op, batch, sp, S.rhs.as<R>(), cfg->warm_start ? mus[p] : S.zero.as<R>(), mus[p ^ 1],
                     cfg->cg_steps, cs);
+          if (feedback) feedback_step(mus[p ^ 1], cs);
           launch_sb_post<R>(n, batch, mus[p ^ 1], mus[p], bxs[p], bys[p], bxs[p ^ 1], bys[p ^ 1], S.fid.as<R>(),
                             S.rhs.as<R>(), cfg->lambda, op->red(), cs);
           CK(cudaMemcpy2DAsync(S.upd_log.as<double>() + static_cast<size_t>(it) * batch, sizeof(double),
@@ -1967,7 +2013,8 @@ void sb_impl(tomo_op* op, const tomo_sb_config* cfg, const void* slice_data, voi
                               cfg->cg_steps, cs);
                   });
         CK(cudaEventRecord(ev[3 * it + 1], st));
-        run_graph(op, fmtkey("sbr_post", batch, {cfg->lambda, double(p), dref ? 1.0 : 0.0}), st, [&](cudaStream_t cs) {
+        run_graph(op, fmtkey("sbr_post", batch, {cfg->lambda, double(p), dref ? 1.0 : 0.0, cfg->alpha, double(feedback)}), st, [&](cudaStream_t cs) {
+          if (feedback) feedback_step(mus[p ^ 1], cs);
           launch_sb_post<R>(n, batch, mus[p ^ 1], mus[p], bxs[p], bys[p], bxs[p ^ 1], bys[p ^ 1], S.fid.as<R>(),
                             S.rhs.as<R>(), cfg->lambda, op->red(), cs);
           launch_sb_log<R>(n, batch, mus[p ^ 1], dref, S.upd_log.as<double>(),

@@ -58,8 +58,6 @@ class RunConfig:
             raise T.ConfigError(f"unknown preset: {self.preset}")
         if self.backend not in BACKENDS:
             raise T.ConfigError(f"unknown backend: {self.backend}")
-        if self.feedback:
-            raise T.ConfigError("config: data feedback is not supported by the B200 solver")
 
     def describe(self) -> str:
         """Canonical key=value line (bench.cpp:38-47; doubles as C++ ostream prints them)."""
@@ -78,7 +76,8 @@ class RunConfig:
 
     def solver_config(self) -> T.SolverConfig:
         return T.SolverConfig(alpha=self.alpha, lambda_=self.lambda_, max_bregman_iters=self.iters,
-                              cg_steps_per_update=self.cg_steps, update_tol_rel=self.tol)
+                              cg_steps_per_update=self.cg_steps, update_tol_rel=self.tol,
+                              data_feedback=self.feedback)
 
 
 def geometry(c: RunConfig) -> T.Geometry:

@@ -164,7 +164,7 @@ class Geometry:
 
 @dataclass
 class SolverConfig:
-    """tomo::SolverConfig (solver.hpp:51-65); data feedback is not supported (reference default off)."""
+    """tomo::SolverConfig (solver.hpp:51-65)."""
 
     alpha: float = 1.0
     lambda_: float = 1.0
@@ -173,6 +173,7 @@ class SolverConfig:
     update_tol_rel: float = 1e-8
     warm_start: bool = True
     sigma_override: float | None = None
+    data_feedback: bool = False  # outer residual feedback on the data term (solver.hpp:58-61)
 
 
 @dataclass
@@ -350,7 +351,8 @@ class NormalBackend:
         mu = _empty_like_kind(f, (B, n, n), False, self.f64)
         cfg = _lib.SbConfig(config.alpha, config.lambda_, config.max_bregman_iters, config.cg_steps_per_update,
                             config.update_tol_rel, int(config.warm_start),
-                            -1.0 if config.sigma_override is None else float(config.sigma_override))
+                            -1.0 if config.sigma_override is None else float(config.sigma_override),
+                            int(config.data_feedback))
         upd = np.zeros(B * config.max_bregman_iters)
         tr = (_lib.SbTrace * B)()
         _check(lib().tomo_split_bregman(self._h, C.byref(cfg), _ptr(f), _ptr(mu), B,
@@ -379,7 +381,8 @@ class NormalBackend:
                 raise ConfigError("split_bregman_record: reference must hold batch x n^2 values")
         cfg = _lib.SbConfig(config.alpha, config.lambda_, config.max_bregman_iters, config.cg_steps_per_update,
                             config.update_tol_rel, int(config.warm_start),
-                            -1.0 if config.sigma_override is None else float(config.sigma_override))
+                            -1.0 if config.sigma_override is None else float(config.sigma_override),
+                            int(config.data_feedback))
         K = config.max_bregman_iters
         upd, rel = np.zeros(B * K), np.zeros(B * K)
         tt, tc = np.zeros(K), np.zeros(K)

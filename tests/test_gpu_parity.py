@@ -327,3 +327,26 @@ def test_sb_recorded_trace_vs_oracle(T):
     cfg.max_bregman_iters = 40
     _, tr = op.split_bregman_record(cuda(f, True, True), cfg, reference=cuda(ph, False, True))
     assert tr[0].stopping_reason == "tolerance" and len(tr[0].rel_l1_err) == tr[0].iterations < 40
+
+
+@pytest.mark.parametrize("backend", ["direct", "surrogate"])
+def test_sb_data_feedback_vs_oracle(T, backend):
+    """SolverConfig.data_feedback (solver.cpp:176-187, 283-286) on the GPU vs the oracle (pinned to
+    the reference in tests/test_oracle_pin.py), in both the one-graph and the recorded driver."""
+    og = O.Geometry(**GEOMS["ref_msp3"])
+    ph = O.shepp_logan(og.n)
+    f, _ = O.synthesize(og, ph, 0.0, 0)
+    alpha = 10.0 if backend == "direct" else 1.0
+    op = (T.make_direct_backend(pgeom(T, og), precision="f64") if backend == "direct"
+          else T.make_surrogate_backend(pgeom(T, og), radius_r=1, precision="f64"))
+    cfg = T.SolverConfig(alpha=alpha, lambda_=1.0, max_bregman_iters=4, cg_steps_per_update=4, update_tol_rel=0.0,
+                         data_feedback=True)
+    mu, tr = op.split_bregman(cuda(f, True, True), cfg)
+    mref, uref, rtr = O.split_bregman(og, f, backend=0 if backend == "direct" else 2, alpha=alpha, lam=1.0,
+                                      max_iters=4, cg_steps=4, feedback=True)
+    assert rel(mu[0].cpu().numpy(), mref) < REC_TOL
+    assert rel(tr[0].update_l1, uref) < REC_TOL
+    if backend == "surrogate":
+        assert abs(tr[0].stabilization_shift - rtr.sigma) <= 1e-3 * abs(rtr.sigma)
+    mu2, tr2 = op.split_bregman_record(cuda(f, True, True), cfg)
+    assert np.array_equal(mu2.cpu().numpy(), mu.cpu().numpy())

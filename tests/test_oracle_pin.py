@@ -39,3 +39,27 @@ def test_pin_tau_override_and_sb():
     # Shrink thresholds amplify last-bit FFT differences (1e-13 after one outer iteration,
     # ~1e-6 after four); the product bar is 1e-3.
     assert rel(mu_o, mu_r) < 1e-5
+
+
+@pytest.mark.parametrize("backend", [0, 2])
+def test_split_bregman_data_feedback_pinned(backend):
+    """SolverConfig::data_feedback (solver.cpp:176-187, 283-286): outer residual feedback on the
+    data term, and for the surrogate the feedback contraction floor sigma; oracle vs reference."""
+    if not refbind.available():
+        pytest.skip("oracle/_ref not built")
+    n, A, msp = 32, 25, 3
+    ref = refbind.Ref(n, A, msp)
+    g = O.Geometry(n=n, n_angles=A, win_lo=-msp, win_hi=msp, tau=ref.tau)
+    ph = refbind.shepp_logan(n)
+    f = ref.synthesize(ph, 0.0, 0)
+    mu_r, upd_r, sg_r, _ = ref.split_bregman(f, backend=backend, r=1, alpha=10.0 if backend == 0 else 1.0,
+                                             lam=1.0, iters=4, cg_steps=4, feedback=True)
+    mu_o, upd_o, tr = O.split_bregman(g, f, backend=backend, r=1, alpha=10.0 if backend == 0 else 1.0, lam=1.0,
+                                      max_iters=4, cg_steps=4, feedback=True)
+    assert abs(tr.sigma - sg_r) <= 1e-6 * max(abs(sg_r), 1.0)
+    assert np.linalg.norm(mu_o - mu_r) / np.linalg.norm(mu_r) < 1e-6
+    assert np.allclose(upd_o, upd_r, rtol=1e-6)
+    # feedback changes the iterates (it is not a no-op)
+    mu_n, _, _ = O.split_bregman(g, f, backend=backend, r=1, alpha=10.0 if backend == 0 else 1.0, lam=1.0,
+                                 max_iters=4, cg_steps=4)
+    assert np.linalg.norm(mu_n - mu_o) > 1e-6 * np.linalg.norm(mu_o)
