@@ -459,7 +459,6 @@ def main():
         v = statistics.median(vals)
         line = {"impl": "reference", "metric": c["metric"], "value": v, "unit": c["unit"], "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / v,  # per unit of the metric (one bounded CPU sample per step)
-               
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded random ellipses, 1% complex Gaussian noise)",
                 "config": {"workload": args.config},

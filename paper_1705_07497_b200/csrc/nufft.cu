@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(256) k_w_sep_wide(OpDev<R> d, int B, const cpl
 // One warp per task {block, chunk0, nchunks, slot}: lane l accumulates node (block, l) over
 // the task's chunks (coalesced 32-entry chunks, 4 in flight), then writes either the grid node
 // (iy*m + perm) or, for a split block, its partial slot.
-template <int GRP, typename R>
+template <int GRP, bool PIPE, typename R>
 __global__ void __launch_bounds__(256) k_task_spmv(TaskSpmv<R> ts, int m, int B, const cplx<R>* __restrict__ s_all,
                                                     size_t in_stride, cplx<R>* __restrict__ grid,
                                                     const SliceScalars* skip) {
@@ -357,6 +357,44 @@ __global__ void __launch_bounds__(256) k_task_spmv(TaskSpmv<R> ts, int m, int B,
     if (skip && (skip[b].done || skip[b].frozen)) continue;
     const C2* s = s_all + static_cast<size_t>(b) * in_stride;
     C2 a0 = czero<C2>(), a1 = czero<C2>();
+    if constexpr (PIPE) {
+    // software pipeline: the entries of group c+GRP are loaded while group c's gathers are in
+    // flight, so a group costs max(entry stream, L2 gather) latency instead of their sum
+    WtEnt<R> q[GRP];
+#pragma unroll
+    for (int k = 0; k < GRP; ++k) {
+      if (k < nc) {
+        q[k] = ldcs(e + k * 32);
+      } else {
+        q[k].j = 0;
+        q[k].w = R(0);
+      }
+    }
+    for (int c = 0; c < nc; c += GRP) {
+      C2 v[GRP];
+#pragma unroll
+      for (int k = 0; k < GRP; ++k) v[k] = c + k < nc ? __ldg(&s[q[k].j]) : czero<C2>();
+      WtEnt<R> qn[GRP];
+#pragma unroll
+      for (int k = 0; k < GRP; ++k) {
+        if (c + GRP + k < nc) {
+          qn[k] = ldcs(e + (c + GRP + k) * 32);
+        } else {
+          qn[k].j = 0;
+          qn[k].w = R(0);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < GRP; k += 2) {
+        a0.x += q[k].w * v[k].x;
+        a0.y += q[k].w * v[k].y;
+        a1.x += q[k + 1].w * v[k + 1].x;
+        a1.y += q[k + 1].w * v[k + 1].y;
+      }
+#pragma unroll
+      for (int k = 0; k < GRP; ++k) q[k] = qn[k];
+    }
+    } else {
     // groups of GRP chunks with predicated tails (all loads of a group in flight at once)
     for (int c = 0; c < nc; c += GRP) {
       WtEnt<R> q[GRP];
@@ -379,6 +417,7 @@ __global__ void __launch_bounds__(256) k_task_spmv(TaskSpmv<R> ts, int m, int B,
         a1.x += q[k + 1].w * v[k + 1].x;
         a1.y += q[k + 1].w * v[k + 1].y;
       }
+    }
     }
     const C2 v = cadd(a0, a1);
     if (slot < 0) {
@@ -800,11 +839,13 @@ void dispatch_m_rb(int m, int rb, F&& f) {
 // (twice the threads per row, one more smem pass) measured faster: c2 t2_rows 10.5 -> 9.9 us,
 // t1_rows 11.7 -> 10.7 us. fp32 (c3: 17 -> 23 us) and m = 8192 keep radix 16.
 // TOMO_ROW_RB=8|16 overrides (A/B runs).
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : dflt;
+}
+
 int row_rb(int m, size_t elem) {
-  static const int forced = [] {
-    const char* v = std::getenv("TOMO_ROW_RB");
-    return v ? std::atoi(v) : 0;
-  }();
+  static const int forced = env_int("TOMO_ROW_RB", 0);
   if (forced == 8 || forced == 16) return forced;
   return elem == 16 && m <= 2048 ? 8 : 16;
 }
@@ -954,9 +995,26 @@ void launch_task_spmv(const TaskSpmv<R>& ts, int m, int B, const cplx<R>* x, siz
   if (ts.n_tasks <= 0) return;
   const int threads = 256;
   const int blocks = (ts.n_tasks * 32 + threads - 1) / threads;
-  // group depth measured on B200: fp32 6 (32 registers, full occupancy), fp64 4
-  constexpr int GRP = sizeof(R) == 4 ? 6 : 4;
-  CK_LAUNCH(launch_k(k_task_spmv<GRP, R>, blocks, threads, 0, st, ts, m, B, x, in_stride, grid, skip));
+  // group depth and software pipelining measured on B200 (c2/c3/c5): fp32 6 chunks, not
+  // pipelined (32 registers, full occupancy); fp64 4 chunks, pipelined for m <= 2048 (c2 W^T
+  // 16.8 -> 14.8 us; c5's m = 8192 W^T got slower, 342 -> 375 us). TOMO_WT_GRP / TOMO_WT_PIPE
+  // override for A/B runs.
+  static const int env_grp = env_int("TOMO_WT_GRP", 0), env_pipe = env_int("TOMO_WT_PIPE", -1);
+  const bool pipe = env_pipe >= 0 ? env_pipe != 0 : (sizeof(R) == 8 && m <= 2048);
+  const int grp = env_grp > 0 ? env_grp : (sizeof(R) == 4 ? 6 : 4);
+  auto go = [&](auto kern) {
+    CK_LAUNCH(launch_k(kern, blocks, threads, 0, st, ts, m, B, x, in_stride, grid, skip));
+  };
+  if constexpr (sizeof(R) == 4) {
+    if (pipe && grp == 4) go(k_task_spmv<4, true, R>);
+    else if (pipe) go(k_task_spmv<6, true, R>);
+    else go(k_task_spmv<6, false, R>);
+  } else {
+    if (pipe && grp == 2) go(k_task_spmv<2, true, R>);
+    else if (pipe && grp == 6) go(k_task_spmv<6, true, R>);
+    else if (pipe) go(k_task_spmv<4, true, R>);
+    else go(k_task_spmv<4, false, R>);
+  }
   note_launch();
 }
 

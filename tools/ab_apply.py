@@ -14,5 +14,5 @@ rng = np.random.default_rng(0)
 u = rng.standard_normal((g.n, g.n))
 dt = torch.float64 if c["prec"] == "f64" else torch.float32
 out = op.apply_normal_real(torch.from_numpy(u).to(dt).cuda()).cpu().numpy()
-np.save(sys.argv[2], out)
+np.save(sys.argv[2], out[::4, ::4])  # subsample: keeps gpurun_out small
 print(sys.argv[1], float(np.linalg.norm(out)))

@@ -1,0 +1,7 @@
+# A/B of env-selected kernel variants: bash tools/ab_run.sh "<cfg>:<ENV=..,ENV=..>:<tag>" ...
+for spec in "$@"; do
+  IFS=: read c envs tag <<< "$spec"
+  env $(echo $envs | tr ',' ' ') timeout 300 python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline \
+    > gpurun_out/ab_${tag}_$c.json 2> gpurun_out/ab_${tag}_$c.err
+  echo "$c $tag rc=$?"
+done
