@@ -34,13 +34,14 @@ sys.path.insert(0, ROOT)
 HBM_FALLBACK_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback if MEASURED_PEAKS.json is absent
 
 CONFIGS = {
-    "c1": dict(n=256, A=60, nb=367, R=2, lo=-2, hi=3, kind="c1", alpha=1.0, applies=100, cg=20, prec="f64",
+    # the 100 independent applies are issued as calls of 20 inputs (run on the library's lanes)
+    "c1": dict(n=256, A=60, nb=367, R=2, lo=-2, hi=3, kind="c1", alpha=1.0, applies=100, batch=20, cg=20, prec="f64",
                metric="normal-op applies/sec", unit="applies/s"),
     "c2": dict(n=512, A=90, nb=725, R=2, lo=-2, hi=3, kind="sb", alpha=10.0, lam=1.0, iters=50, cg=10, prec="f64",
                metric="split-Bregman slices/sec", unit="slices/s"),
-    # 1000 applies on random-normal inputs, issued as calls of 2 independent inputs that the
-    # library runs on two concurrent lanes (streams with their own grids)
-    "c3": dict(n=1024, A=180, nb=1449, R=2, lo=-2, hi=3, kind="apply", applies=1000, batch=2, prec="f32",
+    # 1000 applies on random-normal inputs, issued as calls of 3 independent inputs that the
+    # library runs on three concurrent lanes (streams with their own grids)
+    "c3": dict(n=1024, A=180, nb=1449, R=2, lo=-2, hi=3, kind="apply", applies=1000, batch=3, prec="f32",
                metric="normal-op applies/sec", unit="applies/s"),
     "c4": dict(n=512, A=120, nb=725, R=2, lo=-2, hi=3, kind="sb_sur", alpha=1.0, lam=1.0, iters=30, cg=5, r=1,
                slices=256, prec="f32", metric="split-Bregman slices/sec", unit="slices/s"),
@@ -221,14 +222,13 @@ class Workload:
         elif kind == "apply":
             # `batch` independent random-normal inputs per call (1 = the reference's time_apply shape)
             self.batch = int(c.get("batch", 1))
-            if c["applies"] % self.batch:
-                raise SystemExit("applies must be a multiple of batch")
             self.op = T.make_direct_backend(g, precision=c["prec"], device=local, max_batch=self.batch)
             gen = torch.Generator(device="cuda").manual_seed(7 + rank)
             self.u = torch.randn(self.batch, g.n, g.n, dtype=torch.complex64, device="cuda", generator=gen)
             self.out = torch.empty_like(self.u)
             self.units_per_step = c["applies"]
             self.calls = c["applies"] // self.batch
+            self.rem = c["applies"] % self.batch  # a last, smaller call
             self.chunk = max(d for d in range(1, 51) if self.calls % d == 0)
             self.graph = None
             # end to end: host batches of up to 50 pinned slices per call; the library streams them
@@ -258,11 +258,12 @@ class Workload:
             self.h2d = self.f.numel() * self.f.element_size()
             self.d2h = g.n * g.n * 8
         elif kind == "c1":
-            self.op = T.make_direct_backend(g, precision=c["prec"], device=local, max_batch=2)
+            self.batch = int(c.get("batch", 2))
+            self.op = T.make_direct_backend(g, precision=c["prec"], device=local, max_batch=self.batch)
             self.f = torch.from_numpy(synth_slices(T, self.op, c, [3000 + rank], torch)).cuda()
             ph = T.random_ellipses(g.n, 10, seed=3000 + rank)
             self.u = torch.from_numpy(ph.astype(np.float64)).cuda()
-            self.u2 = self.u.expand(2, g.n, g.n).contiguous()
+            self.u2 = self.u.expand(self.batch, g.n, g.n).contiguous()
             self.out = torch.empty_like(self.u)
             self.units_per_step = c["applies"] + c["cg"] + 1
             self.f_host = self.f.cpu().pin_memory()
@@ -300,10 +301,15 @@ class Workload:
             for _ in range(self.calls // self.chunk):
                 self.graph.replay()
             self.replayed_launches += self.per_replay * (self.calls // self.chunk)
+            if self.rem:
+                self.out = self.op.apply_normal(self.u[:self.rem])
         elif k == "c1":
-            # the 100 applies as calls of 2 (independent, equal) inputs on the library's two lanes
-            for _ in range(self.c["applies"] // 2):
+            # the 100 applies as calls of `batch` (independent, equal) inputs on the library's lanes
+            na = self.c["applies"]
+            for _ in range(na // self.batch):
                 self.out = self.op.apply_normal_real(self.u2)
+            if na % self.batch:
+                self.out = self.op.apply_normal_real(self.u2[:na % self.batch])
             self.mu = self.op.tikhonov(self.f, alpha=self.c["alpha"], steps=self.c["cg"])
         elif k == "cp":
             c = self.c
@@ -335,8 +341,10 @@ class Workload:
     def roofline(self, peak_gbs):
         c = self.c
         k = c["kind"]
-        # the kernels as launched: c4 batches; c3 calls of `batch` inputs run as two lanes of batch/2
-        B = self.batch if k == "sb_sur" else ((self.batch + 1) // 2 if k == "apply" else 1)
+        # the kernels as launched: c4 batches; c1/c3 calls of `batch` inputs run on the library's
+        # lanes (TOMO_LANES, default 3) as sub-batches of ceil(batch / lanes)
+        lanes = min(max(int(os.environ.get("TOMO_LANES", "3") or 3), 1), 4)
+        B = self.batch if k == "sb_sur" else (-(-self.batch // lanes) if k in ("apply", "c1") else 1)
         prof = self.op.profile_stages(batch=B, reps=10)
         if k in ("sb", "c1", "cp"):
             steps = c.get("cg", 10)

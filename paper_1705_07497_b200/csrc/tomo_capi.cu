@@ -289,12 +289,13 @@ struct tomo_op {
   ncclComm_t comm = nullptr;
   std::map<std::string, GraphEntry> graphs;
 
-  // second execution lane for batches of independent slices (apply paths): its own grids and
-  // W^T partial/ticket buffers and its own stream, so two sub-batches run concurrently
-  Scratch lane1;
-  int cur_lane = 0;  // dev() hands out lane-1 buffers while this is 1
-  cudaStream_t lane_st = nullptr;
-  cudaEvent_t lane_fork = nullptr, lane_join = nullptr;
+  // extra execution lanes for batches of independent slices (apply paths): each has its own
+  // grids, W^T partial/ticket buffers and stream, so sub-batches run concurrently
+  static constexpr int kMaxLanes = 4;
+  Scratch lanes[kMaxLanes - 1];  // lanes 1..kMaxLanes-1 (lane 0 = sc)
+  int cur_lane = 0;              // dev() hands out lane cur_lane's buffers
+  cudaStream_t lane_st[kMaxLanes - 1] = {};
+  cudaEvent_t lane_fork = nullptr, lane_join[kMaxLanes - 1] = {};
   // host-buffer pipeline (host_pipeline): copy streams, events, double-buffered staging
   cudaStream_t pipe_in = nullptr, pipe_out = nullptr;
   cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
@@ -309,8 +310,10 @@ struct tomo_op {
     if (pipe_in) cudaStreamDestroy(pipe_in);
     if (pipe_out) cudaStreamDestroy(pipe_out);
     if (lane_fork) cudaEventDestroy(lane_fork);
-    if (lane_join) cudaEventDestroy(lane_join);
-    if (lane_st) cudaStreamDestroy(lane_st);
+    for (int k = 0; k < kMaxLanes - 1; ++k) {
+      if (lane_join[k]) cudaEventDestroy(lane_join[k]);
+      if (lane_st[k]) cudaStreamDestroy(lane_st[k]);
+    }
   }
   void clear_graphs() {
     for (auto& kv : graphs)
@@ -326,8 +329,8 @@ struct tomo_op {
   template <typename R>
   OpDev<R> dev(int B) {
     ensure_batch(B);
-    if (cur_lane) ensure_lane(B);
-    Scratch& sc = cur_lane ? lane1 : this->sc;
+    if (cur_lane) ensure_lane(cur_lane, B);
+    Scratch& sc = cur_lane ? lanes[cur_lane - 1] : this->sc;
     OpDev<R> d{};
     d.n = g.n;
     d.m = g.m;
@@ -399,26 +402,27 @@ struct tomo_op {
     clear_graphs();  // buffers moved
   }
 
-  // lane-1 grids (the apply path only: no solver vectors or scalars)
-  void ensure_lane(int B) {
-    if (B <= lane1.cap) return;
+  // grids of lane k >= 1 (the apply path only: no solver vectors or scalars)
+  void ensure_lane(int k, int B) {
+    Scratch& ln = lanes[k - 1];
+    if (B <= ln.cap) return;
     const size_t m = g.m, n = g.n, cz = 2 * rsz;
-    lane1.H.ensure(B * m * n * cz);
-    lane1.g.ensure(B * m * m * cz);
-    lane1.Gt.ensure(B * m * m * cz);
-    CK(cudaMemset(lane1.Gt.p, 0, B * m * m * cz));
-    lane1.part_wt.ensure(static_cast<size_t>(B) * std::max(n_slots, 1) * 32 * cz);
-    lane1.heavy_cnt.ensure(sizeof(unsigned) * static_cast<size_t>(B) * std::max(n_heavy, 1));
-    CK(cudaMemset(lane1.heavy_cnt.p, 0, sizeof(unsigned) * static_cast<size_t>(B) * std::max(n_heavy, 1)));
+    ln.H.ensure(B * m * n * cz);
+    ln.g.ensure(B * m * m * cz);
+    ln.Gt.ensure(B * m * m * cz);
+    CK(cudaMemset(ln.Gt.p, 0, B * m * m * cz));
+    ln.part_wt.ensure(static_cast<size_t>(B) * std::max(n_slots, 1) * 32 * cz);
+    ln.heavy_cnt.ensure(sizeof(unsigned) * static_cast<size_t>(B) * std::max(n_heavy, 1));
+    CK(cudaMemset(ln.heavy_cnt.p, 0, sizeof(unsigned) * static_cast<size_t>(B) * std::max(n_heavy, 1)));
     if (fused()) {
-      lane1.part_gram.ensure(static_cast<size_t>(B) * std::max(gram.n_slots, 1) * 32 * cz);
+      ln.part_gram.ensure(static_cast<size_t>(B) * std::max(gram.n_slots, 1) * 32 * cz);
       const size_t hb = sizeof(unsigned) * static_cast<size_t>(B) * std::max(gram.n_heavy, 1);
-      lane1.heavy_cnt_gram.ensure(hb);
-      CK(cudaMemset(lane1.heavy_cnt_gram.p, 0, hb));
+      ln.heavy_cnt_gram.ensure(hb);
+      CK(cudaMemset(ln.heavy_cnt_gram.p, 0, hb));
     }
-    lane1.s.ensure(B * static_cast<size_t>(g.P) * cz);
-    lane1.K.ensure(B * n * m * cz);
-    lane1.cap = B;
+    ln.s.ensure(B * static_cast<size_t>(g.P) * cz);
+    ln.K.ensure(B * n * m * cz);
+    ln.cap = B;
     clear_graphs();
   }
 
@@ -1009,42 +1013,57 @@ void normal_core(tomo_op* op, int B, const void* in, bool complex_in, const PUpd
   launch_t1_rows<R>(d, B, e, st);
 }
 
-// Two-lane execution of a batch of independent slices: the first half on `st` (lane 0), the
-// second half on the op's lane stream with lane-1 buffers, forked from and joined back into `st`
-// with events (also inside CUDA-graph capture). Two lanes overlap the latency-bound passes of
-// one apply with those of another (c3: 8.4k -> 11.0k applies/s measured with two handles).
-// f(b0, nb, stream) runs slices [b0, b0 + nb) of the batch.
-template <typename F>
-void two_lanes(tomo_op* op, int batch, cudaStream_t st, F&& f) {
-  static const bool enabled = [] {
-    const char* v = std::getenv("TOMO_LANES");
-    return !(v && v[0] == '1');
+// Multi-lane execution of a batch of independent slices: the batch is cut into `lanes`
+// near-equal sub-batches; sub-batch 0 runs on `st` (lane 0), sub-batch k on the op's lane-k
+// stream with lane-k buffers, forked from and joined back into `st` with events (also inside
+// CUDA-graph capture). Concurrent lanes overlap the latency-bound passes of one apply with those
+// of the others. Measured (bench, applies/s): c3 calls of 2 / 3 / 4 inputs on 2 / 3 / 4 lanes
+// 10.8k / 10.9k / 10.7k; c1 calls of 20 inputs on 2 / 4 lanes 49.1k / 53.9k, calls of 12 on 3
+// lanes 50.4k. TOMO_LANES=1..4 overrides the default (3). f(b0, nb, stream) runs slices
+// [b0, b0 + nb) of the batch.
+int lanes_cfg() {
+  static const int v = [] {
+    const char* e = std::getenv("TOMO_LANES");
+    const int k = e && *e ? std::atoi(e) : 3;
+    return std::min(std::max(k, 1), static_cast<int>(tomo_op::kMaxLanes));
   }();
-  if (batch < 2 || !enabled || op->sharded()) {
+  return v;
+}
+
+template <typename F>
+void run_lanes(tomo_op* op, int batch, cudaStream_t st, F&& f) {
+  const int nl = std::min(batch, lanes_cfg());
+  if (nl < 2 || op->sharded()) {
     f(0, batch, st);
     return;
   }
-  if (!op->lane_st) {
-    CK(cudaStreamCreateWithFlags(&op->lane_st, cudaStreamNonBlocking));
-    CK(cudaEventCreateWithFlags(&op->lane_fork, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&op->lane_join, cudaEventDisableTiming));
-  }
-  const int b0 = (batch + 1) / 2;
-  op->ensure_batch(b0);
-  op->ensure_lane(batch - b0);
+  if (!op->lane_fork) CK(cudaEventCreateWithFlags(&op->lane_fork, cudaEventDisableTiming));
+  for (int k = 1; k < nl; ++k)
+    if (!op->lane_st[k - 1]) {
+      CK(cudaStreamCreateWithFlags(&op->lane_st[k - 1], cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&op->lane_join[k - 1], cudaEventDisableTiming));
+    }
+  // sub-batch k = [bs(k), bs(k+1)): sizes differ by at most one, larger ones first
+  auto bs = [&](int k) { return k * (batch / nl) + std::min(k, batch % nl); };
+  op->ensure_batch(bs(1));
+  for (int k = 1; k < nl; ++k) op->ensure_lane(k, bs(k + 1) - bs(k));
   CK(cudaEventRecord(op->lane_fork, st));
-  CK(cudaStreamWaitEvent(op->lane_st, op->lane_fork, 0));
-  f(0, b0, st);
-  op->cur_lane = 1;
+  for (int k = 1; k < nl; ++k) CK(cudaStreamWaitEvent(op->lane_st[k - 1], op->lane_fork, 0));
+  f(0, bs(1), st);
   try {
-    f(b0, batch - b0, op->lane_st);
+    for (int k = 1; k < nl; ++k) {
+      op->cur_lane = k;
+      f(bs(k), bs(k + 1) - bs(k), op->lane_st[k - 1]);
+    }
   } catch (...) {
     op->cur_lane = 0;
     throw;
   }
   op->cur_lane = 0;
-  CK(cudaEventRecord(op->lane_join, op->lane_st));
-  CK(cudaStreamWaitEvent(st, op->lane_join, 0));
+  for (int k = 1; k < nl; ++k) {
+    CK(cudaEventRecord(op->lane_join[k - 1], op->lane_st[k - 1]));
+    CK(cudaStreamWaitEvent(st, op->lane_join[k - 1], 0));
+  }
 }
 
 // Re(N u) (or N u complex) for the W/W^T and Gram backends, incl. the cross-rank sum when
@@ -1731,7 +1750,7 @@ int tomo_apply_normal(tomo_op* op, const void* in, void* out, int batch, void* s
                            cnt, cudaMemcpyDeviceToDevice, st));
     } else {
       const size_t L = op->L();
-      two_lanes(op, batch, st, [&](int b0, int nb, cudaStream_t ls) {
+      run_lanes(op, batch, st, [&](int b0, int nb, cudaStream_t ls) {
         normal_direct<R>(op, nb, static_cast<const cplx<R>*>(din) + b0 * L, true,
                          static_cast<cplx<R>*>(o.dev) + b0 * L, ls);
       });
@@ -1760,7 +1779,7 @@ int tomo_apply_normal_real(tomo_op* op, const void* in, void* out, int batch, vo
                         static_cast<R*>(o.dev), nullptr, nullptr, sysp(1.0, 0.0, 0.0, 0.0), 0, op->red(), st);
     } else {
       const size_t L = op->L();
-      two_lanes(op, batch, st, [&](int b0, int nb, cudaStream_t ls) {
+      run_lanes(op, batch, st, [&](int b0, int nb, cudaStream_t ls) {
         normal_direct<R>(op, nb, static_cast<const R*>(din) + b0 * L, false, static_cast<R*>(o.dev) + b0 * L, ls);
       });
     }
