@@ -351,7 +351,10 @@ class Workload:
             iters = c.get("iters", 1)
             a = iters * (steps + 1)
             counts = {"t2_rows": a, "t2_cols": a, "w_spmv": a, "wt_spread": a, "t1_cols": a, "t1_rows": a,
-                      "cg_update": iters * steps, "sb_post": iters}
+                      # Chronopoulos-Gear CG (default): one update kernel per CG call, the others
+                      # are fused into the next step's first FFT pass (TOMO_CG=std: one per step)
+                      "cg_update": iters * steps if os.environ.get("TOMO_CG") == "std" else iters,
+                      "sb_post": iters}
         elif k == "apply":
             counts = {"t2_rows": 1, "t2_cols": 1, "w_spmv": 1, "wt_spread": 1, "t1_cols": 1, "t1_rows": 1}
         else:  # surrogate

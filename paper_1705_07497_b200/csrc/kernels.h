@@ -116,6 +116,7 @@ struct SliceScalars {
   double first_upd;   // split Bregman: first update (stopping rule, solver.cpp:298-303)
   double sb_tol;      // update_tol_rel
   double dot;         // scratch dot product (Lanczos)
+  double cg_alpha, cg_beta, cg_pp;  // Chronopoulos-Gear CG: alpha_k, beta_k, p.p (recurrence)
   int done;           // CG finished early (rs == 0, pAp == 0, tolerance)
   int nonfinite;      // sticky non-finite flag (-> NumericalError)
   int steps_run;
@@ -139,7 +140,9 @@ struct SysParams {
   double tol;          // relative residual tolerance (0 = off)
 };
 
-enum PbMode { PB_COMPLEX = 0, PB_REAL = 1, PB_CG_STEP = 2, PB_CG_INIT = 3 };
+// PB_CGCG: Chronopoulos-Gear step (input r_k: w = A r_k, dots r.w and r.r; the last CTA
+// derives alpha_k, beta_k and p.Ap by the recurrences, see cgcg_finalize)
+enum PbMode { PB_COMPLEX = 0, PB_REAL = 1, PB_CG_STEP = 2, PB_CG_INIT = 3, PB_CGCG = 4 };
 
 template <typename R>
 struct PbEpi {
@@ -162,10 +165,16 @@ struct PbEpi {
 template <typename R>
 struct PUpd {
   int enabled;              // 0: plain input
-  const R* r;
+  R* r;                     // cgcg: read and written in place
   R* p;                     // read and written in place
   int step;
   Reduce red;
+  // Chronopoulos-Gear (cgcg = 1, step k > 0): the vector update of step k-1 fused into the
+  // load, p = r + beta p, s = w + beta s, x += alpha p, r -= alpha s; the FFT input is the new r
+  int cgcg;
+  const R* w;               // A r of step k-1
+  R* s;                     // A p (recurrence)
+  R* x;
 };
 
 // ---- launchers (nufft.cu) ----
@@ -246,6 +255,9 @@ struct StencilCoef {
 template <typename R>
 void launch_cg_update(int n, int B, const R* p, const R* ap, R* x, R* r, const SysParams& sys, int step,
                       const Reduce& red, cudaStream_t st);
+template <typename R>
+void launch_cgcg_final(int n, int B, const R* w, R* p, R* s, R* x, R* r, const SysParams& sys, int steps,
+                       const Reduce& red, cudaStream_t st);
 // Surrogate system apply with fused p-update (mode 0: step, 1: init, 2: plain apply out=op(in)).
 template <typename R>
 void launch_stencil(int n, int B, int rad, const StencilCoef& coef, int mode, const R* in, const R* r_in, R* p_out,

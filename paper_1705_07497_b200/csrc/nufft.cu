@@ -110,8 +110,15 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F3
   extern __shared__ __align__(16) unsigned char smraw[];
   C2* sm = reinterpret_cast<C2*>(smraw);
   const int b = blockIdx.y;
-  double beta = 0.0;
-  if (pu.enabled && !cg_step_live(pu.red, b, pu.step, beta)) return;
+  double beta = 0.0, alpha = 0.0;
+  if (pu.enabled && pu.cgcg) {
+    const SliceScalars& sc = pu.red.sc[b];
+    if (sc.done || sc.frozen) return;
+    beta = sc.cg_beta;
+    alpha = sc.cg_alpha;
+  } else if (pu.enabled && !cg_step_live(pu.red, b, pu.step, beta)) {
+    return;
+  }
   if (!pu.enabled && pu.red.sc && pu.red.sc[b].frozen) return;
   const int rr = threadIdx.x / S::T, t = threadIdx.x % S::T;
   const int n = d.n;
@@ -121,7 +128,7 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F3
   C2* row = sm + rr * S::STRIDE;
   const size_t base = (static_cast<size_t>(b) * n + (active ? t1 : 0)) * n;
   const R a1 = active ? d.apod[t1] : R(0);
-  const R bt = static_cast<R>(beta);
+  const R bt = static_cast<R>(beta), al = static_cast<R>(alpha);
   auto load = [&](int i) -> C2 {
     const int t2 = (i + n / 2) & (M - 1);
     C2 v = czero<C2>();
@@ -129,6 +136,25 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F3
       const R sc = a1 * __ldg(&d.apod[t2]);
       if (in_complex) {
         v = reinterpret_cast<const C2*>(in)[base + t2];
+      } else if (pu.enabled && pu.cgcg) {
+        const size_t o = base + t2;
+        R rv = pu.r[o];
+        if (pu.step > 0) {
+          // step k-1's update; at k = 1 (beta_0 = 0) p and s are not read (p_0 = r_0, s_0 = w_0)
+          R pv = rv, sv = pu.w[o];
+          if (pu.step > 1) {
+            pv += bt * pu.p[o];
+            sv += bt * pu.s[o];
+          }
+          const R xv = pu.x[o] + al * pv;
+          rv -= al * sv;
+          pu.p[o] = pv;
+          pu.s[o] = sv;
+          pu.x[o] = xv;
+          pu.r[o] = rv;
+          if (!finite_r(xv)) pu.red.sc[b].nonfinite = 1;
+        }
+        v.x = rv;
       } else if (pu.enabled) {
         R pv = pu.p[base + t2];
         if (pu.step > 0) {
@@ -486,6 +512,40 @@ __device__ __forceinline__ R ktk_at(const R* __restrict__ p, int n, int i, int j
   return v;
 }
 
+// Chronopoulos-Gear step k from gamma = r_k.r_k and delta = r_k.(A r_k) (one reduction per
+// step instead of standard CG's two): beta_k = gamma_k / gamma_{k-1}, p.Ap = delta - beta_k
+// gamma_k / alpha_{k-1}, alpha_k = gamma_k / p.Ap, p.p = gamma_k + beta_k^2 p.p_{k-1}. The
+// reference's exits (solver.cpp:70-90) in its order: the tolerance test on rs_k (made at the
+// end of step k-1, steps_run = k-1), rs == 0 (steps_run = k), p.Ap == 0 (steps_run = k).
+__device__ __forceinline__ void cgcg_finalize(SliceScalars& sc, double delta, double gamma, const SysParams& sys,
+                                              int k) {
+  if (!isfinite(gamma)) sc.nonfinite = 1;
+  if (k > 0 && sys.tol > 0.0 && sc.bb > 0.0 && sqrt(gamma) <= sys.tol * sqrt(sc.bb)) {
+    sc.done = 1;
+    sc.steps_run = k - 1;
+    return;
+  }
+  if (gamma == 0.0) {
+    sc.done = 1;
+    sc.steps_run = k;
+    return;
+  }
+  const double beta = k > 0 ? gamma / sc.rr[(k + 1) & 1] : 0.0;
+  const double pap = k > 0 ? delta - beta * gamma / sc.cg_alpha : delta;
+  const double pp = k > 0 ? gamma + beta * beta * sc.cg_pp : gamma;
+  if (pp > 0.0) sc.min_ritz = fmin(sc.min_ritz, pap / pp);
+  if (pap == 0.0) {
+    sc.done = 1;
+    sc.steps_run = k;
+    return;
+  }
+  sc.rr[k & 1] = gamma;
+  sc.cg_beta = beta;
+  sc.cg_alpha = gamma / pap;
+  sc.cg_pp = pp;
+  sc.steps_run = k;
+}
+
 // ---------------------------------------------------------------- PB: image rows (t1)
 // forward FFT along iy, crop to the n bins, deapodise, then the epilogue: complex / real
 // output or the CG system apply alpha*Re(N p) + lambda K'K p + shift p with the dots.
@@ -497,7 +557,7 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F3
   C2* sm = reinterpret_cast<C2*>(smraw);
   __shared__ double red_scratch[32];
   const int b = blockIdx.y;
-  if (e.mode == PB_CG_STEP && (e.red.sc[b].done || e.red.sc[b].frozen)) return;
+  if ((e.mode == PB_CG_STEP || e.mode == PB_CGCG) && (e.red.sc[b].done || e.red.sc[b].frozen)) return;
   if (e.mode == PB_CG_INIT && e.red.sc[b].frozen) return;
   const int n = d.n;
   const int rr = threadIdx.x / S::T, t = threadIdx.x % S::T;
@@ -525,7 +585,7 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F3
       R ax = X.x * sc;
       if (lam != R(0)) ax += lam * ktk_at<R>(p, n, t1, t2, pv);
       ax += shift * pv;
-      if (e.mode == PB_CG_STEP) {
+      if (e.mode != PB_CG_INIT) {  // STEP: Ap, p.Ap, p.p; CGCG: w = A r, r.w, r.r
         e.ap[o] = ax;
         acc0 += static_cast<double>(pv) * ax;
         acc1 += static_cast<double>(pv) * pv;
@@ -547,7 +607,9 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F3
     double* part = e.red.part + static_cast<size_t>(b) * MAX_PART_BLOCKS * 2;
     if (reduce2_last(acc0, acc1, part, gridDim.x, blockIdx.x, &sc.counter[0], red_scratch, t0s, t1s) &&
         threadIdx.x == 0) {
-      if (e.mode == PB_CG_STEP) {
+      if (e.mode == PB_CGCG) {
+        cgcg_finalize(sc, t0s, t1s, e.sys, e.step);
+      } else if (e.mode == PB_CG_STEP) {
         sc.pap = t0s;
         sc.pp = t1s;
       } else {
@@ -670,7 +732,7 @@ k_t1_rows_p(OpDev<R> d, PbEpi<R> e) {
   C2* stage = row + S::STRIDE;  // M entries
   __shared__ double red_scratch[32];
   const int b = blockIdx.y;
-  if (e.mode == PB_CG_STEP && (e.red.sc[b].done || e.red.sc[b].frozen)) return;
+  if ((e.mode == PB_CG_STEP || e.mode == PB_CGCG) && (e.red.sc[b].done || e.red.sc[b].frozen)) return;
   if (e.mode == PB_CG_INIT && e.red.sc[b].frozen) return;
   const int n = d.n, t = threadIdx.x;
   const C2* Kb = d.K + static_cast<size_t>(b) * n * M;
@@ -709,7 +771,7 @@ k_t1_rows_p(OpDev<R> d, PbEpi<R> e) {
         R ax = X.x * sc;
         if (lam != R(0)) ax += lam * ktk_at<R>(p, n, t1, t2, pv);
         ax += shift * pv;
-        if (e.mode == PB_CG_STEP) {
+        if (e.mode != PB_CG_INIT) {  // STEP: Ap, p.Ap, p.p; CGCG: w = A r, r.w, r.r
           e.ap[o] = ax;
           acc0 += static_cast<double>(pv) * ax;
           acc1 += static_cast<double>(pv) * pv;
@@ -732,7 +794,9 @@ k_t1_rows_p(OpDev<R> d, PbEpi<R> e) {
   double* part = e.red.part + static_cast<size_t>(b) * MAX_PART_BLOCKS * 2;
   if (reduce2_last(acc0, acc1, part, gridDim.x, blockIdx.x, &sc.counter[0], red_scratch, t0s, t1s) &&
       threadIdx.x == 0) {
-    if (e.mode == PB_CG_STEP) {
+    if (e.mode == PB_CGCG) {
+      cgcg_finalize(sc, t0s, t1s, e.sys, e.step);
+    } else if (e.mode == PB_CG_STEP) {
       sc.pap = t0s;
       sc.pp = t1s;
     } else {

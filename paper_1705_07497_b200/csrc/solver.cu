@@ -111,6 +111,50 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_update(int64_t L, const R* _
   }
 }
 
+// ------------------------------------------------------------------ Chronopoulos-Gear CG: last update
+// After the last step's apply (k = steps - 1, scalars from cgcg_finalize): p = r + beta p,
+// s = w + beta s, x += alpha p, r -= alpha s, with r.r for the reference's final tolerance test
+// (solver.cpp:86-88: a break in the last step reports steps_run = steps - 1). The updates of
+// the earlier steps are fused into the next step's first FFT pass (k_t2_rows).
+template <typename R>
+__global__ void __launch_bounds__(kVecThreads) k_cgcg_final(int64_t L, const R* __restrict__ w, R* __restrict__ p,
+                                                            R* __restrict__ s, R* __restrict__ x, R* __restrict__ r,
+                                                            SysParams sys, int steps, Reduce red) {
+  __shared__ double scratch[32];
+  const int b = blockIdx.y;
+  SliceScalars& sc = red.sc[b];
+  if (sc.done || sc.frozen) return;
+  const R alpha = static_cast<R>(sc.cg_alpha), beta = static_cast<R>(sc.cg_beta);
+  const bool first = steps == 1;  // beta_0 = 0: p_0 = r_0, s_0 = w_0
+  const size_t off = static_cast<size_t>(b) * L;
+  double rr = 0.0;
+  bool fin = true;
+  for (int64_t i = gtid(); i < L; i += gstride()) {
+    const size_t o = off + i;
+    R rv = r[o];
+    R pv = rv, sv = w[o];
+    if (!first) {
+      pv += beta * p[o];
+      sv += beta * s[o];
+    }
+    const R xv = x[o] + alpha * pv;
+    rv -= alpha * sv;
+    x[o] = xv;
+    r[o] = rv;
+    fin = fin && finite_r(xv);
+    rr += static_cast<double>(rv) * rv;
+  }
+  if (!fin) sc.nonfinite = 1;
+  double t0, t1;
+  double* part = red.part + static_cast<size_t>(b) * MAX_PART_BLOCKS * 2;
+  if (reduce2_last(rr, 0.0, part, gridDim.x, blockIdx.x, &sc.counter[1], scratch, t0, t1) && threadIdx.x == 0) {
+    if (!isfinite(t0)) sc.nonfinite = 1;
+    sc.rr[steps & 1] = t0;
+    sc.steps_run = steps;
+    if (sys.tol > 0.0 && sc.bb > 0.0 && sqrt(t0) <= sys.tol * sqrt(sc.bb)) sc.steps_run = steps - 1;
+  }
+}
+
 // ------------------------------------------------------------------ surrogate stencil
 // Tile of 32x32 outputs, 256 threads (32 x 8, 4 rows each). Halo H = max(rad, 1).
 // 64x64 outputs per CTA (256 threads = 64 columns x 4, 16 rows each): the halo and the
@@ -682,6 +726,14 @@ void launch_cg_update(int n, int B, const R* p, const R* ap, R* x, R* r, const S
 }
 
 template <typename R>
+void launch_cgcg_final(int n, int B, const R* w, R* p, R* s, R* x, R* r, const SysParams& sys, int steps,
+                       const Reduce& red, cudaStream_t st) {
+  const int64_t L = static_cast<int64_t>(n) * n;
+  CK_LAUNCH(launch_k(k_cgcg_final<R>, dim3(vec_blocks(L, B), B), kVecThreads, 0, st, L, w, p, s, x, r, sys, steps, red));
+  note_launch();
+}
+
+template <typename R>
 void launch_stencil(int n, int B, int rad, const StencilCoef& coef, int mode, const R* in, const R* r_in, R* p_out,
                     R* ap_out, const R* b, R* x_out, const SysParams& sys, int step, const Reduce& red,
                     cudaStream_t st) {
@@ -777,6 +829,8 @@ void launch_shrink(int64_t len, const R* x, double gamma, R* out, cudaStream_t s
 
 #define TOMO_INST_SOLVER(R)                                                                                        \
   template void launch_sb_log<R>(int, int, const R*, const R*, double*, double*, const Reduce&, cudaStream_t); \
+  template void launch_cgcg_final<R>(int, int, const R*, R*, R*, R*, R*, const SysParams&, int, const Reduce&,     \
+                                     cudaStream_t);                                                                \
   template void launch_cg_update<R>(int, int, const R*, const R*, R*, R*, const SysParams&, int, const Reduce&,     \
                                     cudaStream_t);                                                                 \
   template void launch_stencil<R>(int, int, int, const StencilCoef&, int, const R*, const R*, R*, R*, const R*, R*, \

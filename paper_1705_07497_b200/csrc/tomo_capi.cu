@@ -1082,6 +1082,15 @@ void normal_direct(tomo_op* op, int B, const void* in, bool cplx_io, void* out, 
 
 SysParams sysp(double alpha, double lambda, double shift, double tol) { return SysParams{alpha, lambda, shift, tol}; }
 
+// Chronopoulos-Gear CG for the unsharded W/W^T and Gram backends unless TOMO_CG=std.
+bool cgcg_on() {
+  static const bool v = [] {
+    const char* e = std::getenv("TOMO_CG");
+    return !(e && std::string(e) == "std");
+  }();
+  return v;
+}
+
 // cg_solve (solver.cpp:56-95) for B slices: rhs, x0 -> x (device, B x L each).
 template <typename R>
 void cg_run(tomo_op* op, int B, const SysParams& s, const R* rhs, const R* x0, R* x, int steps, cudaStream_t st) {
@@ -1133,6 +1142,35 @@ void cg_run(tomo_op* op, int B, const SysParams& s, const R* rhs, const R* x0, R
       allreduce<R>(op, nred, static_cast<size_t>(B) * L, st);
       launch_cg_epilogue<R>(n, B, 1, nred, x0, rhs, r, p0, x, s, 0, red, st);
     }
+  }
+  if (cgcg_on() && !shard) {
+    // Chronopoulos-Gear CG: each step applies the operator to r (w = A r) with r.w and r.r in
+    // the epilogue; the vector update is fused into the next step's first FFT pass, so a step is
+    // one apply with one reduction (standard CG: an apply plus an update kernel, two
+    // reductions). Same iterates in exact arithmetic; the reference's exits and steps_run are
+    // kept (cgcg_finalize). TOMO_CG=std selects the standard two-kernel form.
+    R* s_vec = p1;
+    for (int k = 0; k < steps; ++k) {
+      PUpd<R> pu{};
+      pu.enabled = 1;
+      pu.cgcg = 1;
+      pu.r = r;
+      pu.p = p0;
+      pu.s = s_vec;
+      pu.w = ap;
+      pu.x = x;
+      pu.step = k;
+      pu.red = red;
+      PbEpi<R> e = plain_epi<R>(PB_CGCG, s.alpha);
+      e.p = r;
+      e.ap = ap;
+      e.sys = s;
+      e.step = k;
+      e.red = red;
+      normal_core<R>(op, B, r, false, pu, e, skip, st);
+    }
+    launch_cgcg_final<R>(n, B, ap, p0, s_vec, x, r, s, steps, red, st);
+    return;
   }
   for (int k = 0; k < steps; ++k) {
     PUpd<R> pu{};
@@ -2391,6 +2429,7 @@ int tomo_profile_stages(tomo_op* op, int batch, int reps, double* ms, double* by
     for (auto& sc : init) {
       sc.rr[0] = sc.rr[1] = 1.0;
       sc.pap = sc.pp = 1.0;
+      sc.cg_alpha = sc.cg_beta = 1e-3;
       sc.first_upd = 1e300;
     }
     const SysParams sp = sysp(1.0, 1.0, 0.0, 0.0);
@@ -2407,6 +2446,13 @@ int tomo_profile_stages(tomo_op* op, int batch, int reps, double* ms, double* by
           pu.p = S.p0.as<R>();
           pu.step = 1;
           pu.red = red;
+          if (cgcg_on() && !op->sharded()) {  // the fused C-G update (both recurrences live)
+            pu.cgcg = 1;
+            pu.step = 2;
+            pu.s = S.p1.as<R>();
+            pu.w = S.ap.as<R>();
+            pu.x = S.x.as<R>();
+          }
           launch_t2_rows<R>(d, batch, S.p0.p, false, pu, cs);
         } else if (s == 1) {
           launch_t2_cols<R>(d, batch, op->scal(), cs);
@@ -2432,7 +2478,13 @@ int tomo_profile_stages(tomo_op* op, int batch, int reps, double* ms, double* by
         launch_stencil<R>(n, batch, op->rad, op->coef, 0, S.p0.as<R>(), S.r.as<R>(), S.p1.as<R>(), S.ap.as<R>(),
                           nullptr, nullptr, sp, 1, red, cs);
       }
-      if (s == 6) launch_cg_update<R>(n, batch, S.p0.as<R>(), S.ap.as<R>(), S.x.as<R>(), S.r.as<R>(), sp, 1, red, cs);
+      if (s == 6) {
+        if (!sur && cgcg_on() && !op->sharded())  // C-G: one final update per CG call
+          launch_cgcg_final<R>(n, batch, S.ap.as<R>(), S.p0.as<R>(), S.p1.as<R>(), S.x.as<R>(), S.r.as<R>(), sp, 2,
+                               red, cs);
+        else
+          launch_cg_update<R>(n, batch, S.p0.as<R>(), S.ap.as<R>(), S.x.as<R>(), S.r.as<R>(), sp, 1, red, cs);
+      }
       if (s == 7)
         launch_sb_post<R>(n, batch, S.mu1.as<R>(), S.mu0.as<R>(), S.bx0.as<R>(), S.by0.as<R>(), S.bx1.as<R>(),
                           S.by1.as<R>(), S.fid.as<R>(), S.rhs.as<R>(), 1.0, red, cs);
@@ -2470,7 +2522,9 @@ int tomo_profile_stages(tomo_op* op, int batch, int reps, double* ms, double* by
                            static_cast<double>(op->wt_rows) * 2.0;
     double by[TOMO_NUM_STAGES] = {0};
     if (!sur) {
-      by[0] = B * (3 * rs * nn + cs * mn);                 // read p, r; write p; write H
+      by[0] = cgcg_on() && !op->sharded()
+                  ? B * (9 * rs * nn + cs * mn)            // C-G: read r, w, x, p, s; write p, s, x, r; write H
+                  : B * (3 * rs * nn + cs * mn);           // read p, r; write p; write H
       by[1] = B * (cs * mn + cs * mm);                     // read H, write g
       by[2] = op->fused()  // Gram stream, read + write touched nodes | W stream, touched nodes, samples
                   ? static_cast<double>(op->gram.bytes) + B * (2 * cs * op->wt_rows)
@@ -2481,7 +2535,7 @@ int tomo_profile_stages(tomo_op* op, int batch, int reps, double* ms, double* by
     } else {
       by[8] = B * 4 * rs * nn;  // read r, p; write p, Ap
     }
-    by[6] = B * 6 * rs * nn;  // read x, r, p, Ap; write x, r
+    by[6] = B * (!sur && cgcg_on() && !op->sharded() ? 7 : 6) * rs * nn;  // read x, r, p, Ap (C-G: + s); write x, r
     by[7] = B * 8 * rs * nn;  // read mu_new, mu_old, bx, by, fid; write bx, by, rhs
     for (int k = 0; k < TOMO_NUM_STAGES; ++k) {
       const bool on = stage_on(k);
