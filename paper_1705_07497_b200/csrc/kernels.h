@@ -117,6 +117,7 @@ struct SliceScalars {
   double sb_tol;      // update_tol_rel
   double dot;         // scratch dot product (Lanczos)
   double cg_alpha, cg_beta, cg_pp;  // Chronopoulos-Gear CG: alpha_k, beta_k, p.p (recurrence)
+  double rs_last;     // the last r.r computed (CgStats::final_rs)
   int done;           // CG finished early (rs == 0, pAp == 0, tolerance)
   int nonfinite;      // sticky non-finite flag (-> NumericalError)
   int steps_run;

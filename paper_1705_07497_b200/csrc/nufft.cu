@@ -520,6 +520,9 @@ __device__ __forceinline__ R ktk_at(const R* __restrict__ p, int n, int i, int j
 __device__ __forceinline__ void cgcg_finalize(SliceScalars& sc, double delta, double gamma, const SysParams& sys,
                                               int k) {
   if (!isfinite(gamma)) sc.nonfinite = 1;
+  const double gamma_prev = sc.rr[(k + 1) & 1];
+  sc.rr[k & 1] = gamma;
+  sc.rs_last = gamma;
   if (k > 0 && sys.tol > 0.0 && sc.bb > 0.0 && sqrt(gamma) <= sys.tol * sqrt(sc.bb)) {
     sc.done = 1;
     sc.steps_run = k - 1;
@@ -530,7 +533,7 @@ __device__ __forceinline__ void cgcg_finalize(SliceScalars& sc, double delta, do
     sc.steps_run = k;
     return;
   }
-  const double beta = k > 0 ? gamma / sc.rr[(k + 1) & 1] : 0.0;
+  const double beta = k > 0 ? gamma / gamma_prev : 0.0;
   const double pap = k > 0 ? delta - beta * gamma / sc.cg_alpha : delta;
   const double pp = k > 0 ? gamma + beta * beta * sc.cg_pp : gamma;
   if (pp > 0.0) sc.min_ritz = fmin(sc.min_ritz, pap / pp);
@@ -539,7 +542,6 @@ __device__ __forceinline__ void cgcg_finalize(SliceScalars& sc, double delta, do
     sc.steps_run = k;
     return;
   }
-  sc.rr[k & 1] = gamma;
   sc.cg_beta = beta;
   sc.cg_alpha = gamma / pap;
   sc.cg_pp = pp;
@@ -614,6 +616,7 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F3
         sc.pp = t1s;
       } else {
         sc.rr[0] = t0s;
+        sc.rs_last = t0s;
         sc.bb = t1s;
         sc.done = 0;
         sc.steps_run = 0;
@@ -801,6 +804,7 @@ k_t1_rows_p(OpDev<R> d, PbEpi<R> e) {
       sc.pp = t1s;
     } else {
       sc.rr[0] = t0s;
+      sc.rs_last = t0s;
       sc.bb = t1s;
       sc.done = 0;
       sc.steps_run = 0;

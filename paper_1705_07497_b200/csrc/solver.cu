@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_update(int64_t L, const R* _
   double* part = red.part + static_cast<size_t>(b) * MAX_PART_BLOCKS * 2;
   if (reduce2_last(rr, 0.0, part, gridDim.x, blockIdx.x, &sc.counter[1], scratch, t0, t1) && threadIdx.x == 0) {
     sc.rr[(step + 1) & 1] = t0;
+    sc.rs_last = t0;
     if (!isfinite(t0)) sc.nonfinite = 1;
     sc.steps_run = step + 1;
     if (sys.tol > 0.0 && sc.bb > 0.0 && sqrt(t0) <= sys.tol * sqrt(sc.bb)) {  // solver.cpp:86-88
@@ -150,6 +151,7 @@ __global__ void __launch_bounds__(kVecThreads) k_cgcg_final(int64_t L, const R* 
   if (reduce2_last(rr, 0.0, part, gridDim.x, blockIdx.x, &sc.counter[1], scratch, t0, t1) && threadIdx.x == 0) {
     if (!isfinite(t0)) sc.nonfinite = 1;
     sc.rr[steps & 1] = t0;
+    sc.rs_last = t0;
     sc.steps_run = steps;
     if (sys.tol > 0.0 && sc.bb > 0.0 && sqrt(t0) <= sys.tol * sqrt(sc.bb)) sc.steps_run = steps - 1;
   }
@@ -314,6 +316,7 @@ __global__ void __launch_bounds__(256) k_stencil(int n, StencilCoef coef, int mo
       sc.pp = t1;
     } else {
       sc.rr[0] = t0;
+      sc.rs_last = t0;
       sc.bb = t1;
       sc.done = 0;
       sc.steps_run = 0;
@@ -378,6 +381,7 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_epilogue(int n, int mode, co
       sc.pp = t1;
     } else {
       sc.rr[0] = t0;
+      sc.rs_last = t0;
       sc.bb = t1;
       sc.done = 0;
       sc.steps_run = 0;

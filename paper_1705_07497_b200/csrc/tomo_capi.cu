@@ -1959,7 +1959,7 @@ int tomo_cg(tomo_op* op, const tomo_system* sys, const void* rhs, const void* x0
       if (stats) {
         stats[b].steps_run = hs[b].steps_run;
         stats[b].min_ritz = std::isfinite(hs[b].min_ritz) ? hs[b].min_ritz : 0.0;
-        stats[b].final_rs = hs[b].rr[hs[b].steps_run & 1];
+        stats[b].final_rs = hs[b].rs_last;
       }
     }
   });

@@ -350,3 +350,29 @@ def test_sb_data_feedback_vs_oracle(T, backend):
         assert abs(tr[0].stabilization_shift - rtr.sigma) <= 1e-3 * abs(rtr.sigma)
     mu2, tr2 = op.split_bregman_record(cuda(f, True, True), cfg)
     assert np.array_equal(mu2.cpu().numpy(), mu.cpu().numpy())
+
+
+@pytest.mark.parametrize("tol", [0.0, 3e-2, 1e-3])
+def test_cg_exits_vs_oracle(T, tol):
+    """cg_solve's exits (solver.cpp:70,75,86-88) through the Chronopoulos-Gear form: the relative
+    tolerance stop, rs == 0 (zero right-hand side) and the fixed step count, per slice of a batch;
+    steps_run / final_rs / min_ritz / x against the oracle's standard CG."""
+    og = O.Geometry(**GEOMS["ref_msp3"])
+    n = og.n
+    op = T.make_direct_backend(pgeom(T, og), precision="f64")
+    # alpha N + lambda K'K + I: well conditioned, so the tolerances stop it at 5 / 10 steps
+    sysd = O.system(0, alpha=1e-3, lam=0.1, shift=1.0)
+    rhs = np.stack([RNG.standard_normal((n, n)), np.zeros((n, n)), RNG.standard_normal((n, n))])
+    x, st = op.cg(cuda(rhs, False, True), alpha=1e-3, lambda_=0.1, shift=1.0, steps=12, rel_tol=tol)
+    x = x.cpu().numpy()
+    for b in range(3):
+        xr, sr = O.cg(og, sysd, rhs[b], steps=12, rel_tol=tol)
+        assert st[b].steps_run == sr.steps_run
+        if b == 1:
+            assert sr.steps_run == 0 and not np.any(x[b])
+            continue
+        assert rel(x[b].ravel(), np.asarray(xr).ravel()) < 1e-8
+        assert abs(st[b].final_rs - sr.final_rs) <= 1e-6 * sr.final_rs
+        assert abs(st[b].min_ritz - sr.min_ritz) <= 1e-8 * abs(sr.min_ritz)
+    if tol > 0:
+        assert 0 < st[0].steps_run < 12  # the tolerance stop is exercised
