@@ -103,6 +103,9 @@ struct OpDev {
 };
 
 constexpr int kWtMaxChunks = 24;
+// chunks per W^T / Gram warp task (longer blocks are split): kWtMaxChunks unless
+// TOMO_WT_MAXCH overrides it (A/B runs; read once per process)
+int wt_max_chunks();
 
 // Per-slice scalar state of the device-resident CG / split-Bregman loops. All reductions
 // land here through the last-block-reduces pattern (deterministic order).

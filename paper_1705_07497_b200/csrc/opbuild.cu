@@ -301,6 +301,15 @@ GpuBuild* gpu_build_begin(const BuildArgs& a, const double* h_cs, const double* 
 
 // Task structure from entries already in final order (b->sj, b->vals_sorted) and the per-node
 // counts b->cnt: node offsets, per-row node order, 32-node blocks, warp tasks, totals.
+int wt_max_chunks() {
+  static const int v = [] {
+    const char* e = std::getenv("TOMO_WT_MAXCH");
+    const int k = e && *e ? std::atoi(e) : kWtMaxChunks;
+    return std::min(std::max(k, 1), 1024);
+  }();
+  return v;
+}
+
 void build_structure(GpuBuild* b, cudaStream_t st) {
   const int m = b->a.m;
   size_t tmp_bytes = 0;
@@ -327,7 +336,7 @@ void build_structure(GpuBuild* b, cudaStream_t st) {
   b->ntask.alloc(b->G32);
   b->nslot.alloc(b->G32);
   b->nheavy.alloc(b->G32);
-  k_blocks<<<static_cast<unsigned>((b->G32 + 7) / 8), 256, 0, st>>>(m, kWtMaxChunks, nsorted.p, b->cnt.p, b->perm.p,
+  k_blocks<<<static_cast<unsigned>((b->G32 + 7) / 8), 256, 0, st>>>(m, wt_max_chunks(), nsorted.p, b->cnt.p, b->perm.p,
                                                                    b->L.p, b->ntask.p, b->nslot.p, b->nheavy.p);
   BK(cudaGetLastError());
   b->chunk0.alloc(b->G32 + 1);
@@ -374,7 +383,7 @@ void gpu_build_finish(GpuBuild* b, WtEnt<R>* ent, int4* tasks, uint16_t* perm, i
   DBuf<int4> traw(nt);
   DBuf<int> tkey(nt), tkey2(nt), tidx(nt), tidx2(nt);
   k_tasks<<<static_cast<unsigned>((b->G32 + 255) / 256), 256, 0, st>>>(
-      b->G32, kWtMaxChunks, b->L.p, b->chunk0.p, b->toff.p, b->soff.p, b->hoff.p, traw.p, tkey.p, heavy, slot_heavy);
+      b->G32, wt_max_chunks(), b->L.p, b->chunk0.p, b->toff.p, b->soff.p, b->hoff.p, traw.p, tkey.p, heavy, slot_heavy);
   BK(cudaGetLastError());
   if (nt > 0 && wt_row_order(m)) {
     BK(cudaMemcpyAsync(tasks, traw.p, sizeof(int4) * nt, cudaMemcpyDeviceToDevice, st));
@@ -385,9 +394,9 @@ void gpu_build_finish(GpuBuild* b, WtEnt<R>* ent, int4* tasks, uint16_t* perm, i
     BK(cudaMemcpyAsync(tidx.p, iota.data(), sizeof(int) * nt, cudaMemcpyHostToDevice, st));
     size_t tb = 0;
     BK(cub::DeviceRadixSort::SortPairs(nullptr, tb, tkey.p, tkey2.p, tidx.p, tidx2.p, nt, 0,
-                                       bits_for(kWtMaxChunks), st));
+                                       bits_for(wt_max_chunks()), st));
     DBuf<unsigned char> t2(tb);
-    BK(cub::DeviceRadixSort::SortPairs(t2.p, tb, tkey.p, tkey2.p, tidx.p, tidx2.p, nt, 0, bits_for(kWtMaxChunks),
+    BK(cub::DeviceRadixSort::SortPairs(t2.p, tb, tkey.p, tkey2.p, tidx.p, tidx2.p, nt, 0, bits_for(wt_max_chunks()),
                                        st));
     k_gather_tasks<R><<<(nt + 255) / 256, 256, 0, st>>>(nt, tidx2.p, traw.p, tasks);
     BK(cudaGetLastError());

@@ -668,7 +668,7 @@ void build_gram(tomo_op* op, const Plan& pl) {
       return;
     }
   }
-  TaskBuilder<R> tb(m, kWtMaxChunks, op->wt_rows * band2);
+  TaskBuilder<R> tb(m, wt_max_chunks(), op->wt_rows * band2);
   std::vector<R> rv;
   int64_t nnz = 0;
   gram_rows(g, pl, [&](int iy, const int64_t* roff, const int32_t* rcol, const double* rval) {
@@ -697,7 +697,7 @@ template <typename R>
 void gram_from_tspm(tomo_op* op, const TspmFile& t) {
   check_tspm_meta(op, t, true);
   const int m = op->g.m;
-  TaskBuilder<R> tb(m, kWtMaxChunks, t.nnz());
+  TaskBuilder<R> tb(m, wt_max_chunks(), t.nnz());
   std::vector<int64_t> roff(m + 1);
   std::vector<int32_t> rcol;
   std::vector<R> rval;
@@ -824,7 +824,7 @@ void build_w_host(tomo_op* op) {
       tv[k] = vals[o].v[c];
     }
   }
-  TaskBuilder<R> tb(m, kWtMaxChunks, off[G]);
+  TaskBuilder<R> tb(m, wt_max_chunks(), off[G]);
   for (int iy = 0; iy < m; ++iy) tb.add_row(iy, off.data() + static_cast<int64_t>(iy) * m, tj.data(), tv.data());
   tb.finish();
   op->wt_rows = tb.touched;
