@@ -152,13 +152,21 @@ TOMO_DEV void twiddle(C2* v, const C2* __restrict__ tw, int base) {
   }
 }
 
+// Compile-time pruning (PR) for rows whose non-zero inputs / kept outputs are exactly the
+// first and last quarter of the row (n = M/2, the reference's 2x oversampling): bit 0 — the
+// first pass treats inputs M/4 <= i < 3M/4 as zeros (no loads, no arithmetic on them); bit 1 —
+// the last pass computes and stores only outputs k < M/4 and k >= 3M/4. Both need radix >= 4
+// for that pass (its r-th input / output then lies in the middle half iff R/4 <= r < 3R/4).
+template <int R>
+TOMO_DEV constexpr bool mid_quarter(int r) { return R >= 4 && r >= R / 4 && r < 3 * R / 4; }
+
 // One Stockham pass (radix R, sub-transform size Ns) of the row owned by this thread group.
 // FIRST: inputs come from load(i) (global), otherwise from the smem row. LAST: outputs go to
 // store(k, value), otherwise back into the smem row. Every thread of the CTA must call each
 // pass (barriers inside); `active` gates the work. STORE_SMEM_LAST: the storer writes the smem
 // row, so a barrier separates the last reads from those writes.
-template <int M, int RB, int R, bool FIRST, bool LAST, bool STORE_SMEM_LAST, typename C2, typename Load,
-          typename Store>
+template <int M, int RB, int R, bool FIRST, bool LAST, bool STORE_SMEM_LAST, typename C2, int PR = 0,
+          typename Load, typename Store>
 TOMO_DEV void fft_pass(C2* row, const C2* __restrict__ tw, int Ns, int t, bool active, Load& load, Store& store) {
   constexpr int T = M / RB;
   constexpr int NB = M / R;    // butterflies per pass
@@ -169,7 +177,12 @@ TOMO_DEV void fft_pass(C2* row, const C2* __restrict__ tw, int Ns, int t, bool a
     for (int q = 0; q < PER; ++q) {
       const int j = t + q * T;
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[q][r] = FIRST ? load(j + r * NB) : row[pad16(j + r * NB)];
+      for (int r = 0; r < R; ++r) {
+        if (FIRST && (PR & 1) && mid_quarter<R>(r))
+          v[q][r] = czero<C2>();
+        else
+          v[q][r] = FIRST ? load(j + r * NB) : row[pad16(j + r * NB)];
+      }
       if (!FIRST) {
         const int jm = j & (Ns - 1);
         if (jm) twiddle<R, C2>(v[q], tw, (M / (Ns * R)) * jm);
@@ -186,6 +199,7 @@ TOMO_DEV void fft_pass(C2* row, const C2* __restrict__ tw, int Ns, int t, bool a
       const int base = (j - jm) * R + jm;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
+        if (LAST && (PR & 2) && mid_quarter<R>(r)) continue;
         if (LAST)
           store(base + r * Ns, v[q][r]);
         else
@@ -234,10 +248,10 @@ TOMO_DEV void fft_row_pre(C2* row, const C2* __restrict__ tw, int t, bool active
 }
 
 // Forward FFT of one row per thread group: load(i) -> ... -> store(k, X[k]).
-template <int M, int RB, bool STORE_SMEM, typename C2, typename Load, typename Store>
+template <int M, int RB, bool STORE_SMEM, typename C2, int PR = 0, typename Load, typename Store>
 TOMO_DEV void fft_row(C2* row, const C2* __restrict__ tw, int t, bool active, Load&& load, Store&& store) {
   using S = FftShape<M, RB>;
-  fft_pass<M, RB, RB, true, false, false, C2>(row, tw, 1, t, active, load, store);
+  fft_pass<M, RB, RB, true, false, false, C2, PR & 1>(row, tw, 1, t, active, load, store);
   if constexpr (S::RL > 1) {
     int Ns = RB;
 #pragma unroll
@@ -245,7 +259,7 @@ TOMO_DEV void fft_row(C2* row, const C2* __restrict__ tw, int t, bool active, Lo
       fft_pass<M, RB, RB, false, false, false, C2>(row, tw, Ns, t, active, load, store);
       Ns *= RB;
     }
-    fft_pass<M, RB, S::RL, false, true, STORE_SMEM, C2>(row, tw, Ns, t, active, load, store);
+    fft_pass<M, RB, S::RL, false, true, STORE_SMEM, C2, PR & 2>(row, tw, Ns, t, active, load, store);
   } else {
     int Ns = RB;
 #pragma unroll
@@ -253,7 +267,7 @@ TOMO_DEV void fft_row(C2* row, const C2* __restrict__ tw, int t, bool active, Lo
       fft_pass<M, RB, RB, false, false, false, C2>(row, tw, Ns, t, active, load, store);
       Ns *= RB;
     }
-    fft_pass<M, RB, RB, false, true, STORE_SMEM, C2>(row, tw, Ns, t, active, load, store);
+    fft_pass<M, RB, RB, false, true, STORE_SMEM, C2, PR & 2>(row, tw, Ns, t, active, load, store);
   }
 }
 

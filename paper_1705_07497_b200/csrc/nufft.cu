@@ -94,6 +94,19 @@ __device__ __forceinline__ WtEnt<double> ldcs(const WtEnt<double>* p) {
   return WtEnt<double>{v.x, 0, __hiloint2double(v.w, v.z)};
 }
 
+// Transposed store of rpc staged rows: dst[k * ld + q] = sm[q * STRIDE + pad16(k)] for k < K,
+// q < ncols (<= rpc). Consecutive threads take consecutive q, then k, so each warp store
+// covers whole 32-byte row segments (measured: one thread per k with 16-byte vector stores
+// was slower, 2 half-sector stores per lane). rpc is a power of two: shifts, no divisions.
+template <int STRIDE, typename C2>
+TOMO_DEV void store_transposed(const C2* sm, int rpc, int ncols, int K, C2* __restrict__ dst, size_t ld) {
+  const int lg = __ffs(rpc) - 1;
+  for (int idx = threadIdx.x; idx < (K << lg); idx += blockDim.x) {
+    const int k = idx >> lg, q = idx & (rpc - 1);
+    if (q < ncols) dst[static_cast<size_t>(k) * ld + q] = sm[q * STRIDE + pad16(k)];
+  }
+}
+
 struct NoStore {
   template <typename C2>
   TOMO_DEV void operator()(int, C2) const {}
@@ -102,7 +115,7 @@ struct NoStore {
 // ---------------------------------------------------------------- P1: image rows (t1)
 // deapodise + pad + inverse FFT along t2; the CG p-update (p = r + beta p) is fused into the
 // load; output transposed to H[iy][t1] through smem.
-template <int M, int RB, typename R>
+template <int M, int RB, typename R, bool HALF = false>
 __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F32 : TOMO_FFT_MINB_F64) k_t2_rows(OpDev<R> d, const void* __restrict__ in, int in_complex,
                                                   PUpd<R> pu, int rpc) {
   using S = FftShape<M, RB>;
@@ -170,17 +183,14 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F3
     return v;
   };
   auto store = [&](int k, C2 v) { row[pad16(k)] = cconj(v); };
-  fft_row<M, RB, true, C2>(row, d.tw, t, active, load, store);
+  fft_row<M, RB, true, C2, HALF ? 1 : 0>(row, d.tw, t, active, load, store);
   // transposed store H[b][k][t1]: rpc consecutive t1 per k
   C2* H = d.H + static_cast<size_t>(b) * M * n;
-  for (int idx = threadIdx.x; idx < M * rpc; idx += blockDim.x) {
-    const int k = idx / rpc, q = idx - k * rpc;
-    if (t10 + q < n) H[static_cast<size_t>(k) * n + t10 + q] = sm[q * S::STRIDE + pad16(k)];
-  }
+  store_transposed<S::STRIDE>(sm, rpc, min(rpc, n - t10), M, H + t10, static_cast<size_t>(n));
 }
 
 // ---------------------------------------------------------------- P2: grid rows (iy)
-template <int M, int RB, typename R>
+template <int M, int RB, typename R, bool HALF = false>
 __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F32 : TOMO_FFT_MINB_F64) k_t2_cols(OpDev<R> d, int rpc, const SliceScalars* skip) {
   using S = FftShape<M, RB>;
   using C2 = cplx<R>;
@@ -200,7 +210,7 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F3
     return t1 < n ? cconj(H[t1]) : czero<C2>();
   };
   auto store = [&](int k, C2 v) { g[k] = cconj(v); };
-  fft_row<M, RB, false, C2>(row, d.tw, t, active, load, store);
+  fft_row<M, RB, false, C2, HALF ? 1 : 0>(row, d.tw, t, active, load, store);
 }
 
 // ---------------------------------------------------------------- W: SELL-32 ELL SpMV
@@ -473,7 +483,7 @@ __global__ void __launch_bounds__(256) k_task_spmv(TaskSpmv<R> ts, int m, int B,
 
 // ---------------------------------------------------------------- PA: grid rows (iy), type 1
 // forward FFT along ix of the spread grid row, pruned to the n bins, transposed to K[t1][iy].
-template <int M, int RB, typename R>
+template <int M, int RB, typename R, bool HALF = false>
 __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F32 : TOMO_FFT_MINB_F64) k_t1_cols(OpDev<R> d, int rpc, const SliceScalars* skip) {
   using S = FftShape<M, RB>;
   using C2 = cplx<R>;
@@ -492,12 +502,9 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F3
     const int t1 = (k + n / 2) & (M - 1);  // inverse of bin_of
     if (t1 < n) row[pad16(t1)] = v;
   };
-  fft_row<M, RB, true, C2>(row, d.tw, t, active, load, store);
+  fft_row<M, RB, true, C2, HALF ? 2 : 0>(row, d.tw, t, active, load, store);
   C2* K = d.K + static_cast<size_t>(b) * n * M;
-  for (int idx = threadIdx.x; idx < n * rpc; idx += blockDim.x) {
-    const int t1 = idx / rpc, q = idx - t1 * rpc;
-    K[static_cast<size_t>(t1) * M + iy0 + q] = sm[q * S::STRIDE + pad16(t1)];
-  }
+  store_transposed<S::STRIDE>(sm, rpc, rpc, n, K + iy0, static_cast<size_t>(M));
 }
 
 template <typename R>
@@ -551,7 +558,7 @@ __device__ __forceinline__ void cgcg_finalize(SliceScalars& sc, double delta, do
 // ---------------------------------------------------------------- PB: image rows (t1)
 // forward FFT along iy, crop to the n bins, deapodise, then the epilogue: complex / real
 // output or the CG system apply alpha*Re(N p) + lambda K'K p + shift p with the dots.
-template <int M, int RB, typename R>
+template <int M, int RB, typename R, bool HALF = false>
 __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F32 : TOMO_FFT_MINB_F64) k_t1_rows(OpDev<R> d, PbEpi<R> e, int rpc) {
   using S = FftShape<M, RB>;
   using C2 = cplx<R>;
@@ -602,7 +609,7 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F3
       }
     }
   };
-  fft_row<M, RB, false, C2>(row, d.tw, t, active, load, store);
+  fft_row<M, RB, false, C2, HALF ? 2 : 0>(row, d.tw, t, active, load, store);
   if (e.mode >= PB_CG_STEP) {
     double t0s, t1s;
     SliceScalars& sc = e.red.sc[b];
@@ -715,10 +722,7 @@ k_t1_cols_p(OpDev<R> d, int rpc, const SliceScalars* skip) {
       const int t1 = (k + n / 2) & (M - 1);  // inverse of bin_of
       if (t1 < n) row[pad16(t1)] = v;
     });
-    for (int idx = threadIdx.x; idx < n * rpc; idx += blockDim.x) {
-      const int t1 = idx / rpc, q = idx - t1 * rpc;
-      K[static_cast<size_t>(t1) * M + iy0 + q] = sm[q * S::STRIDE + pad16(t1)];
-    }
+    store_transposed<S::STRIDE>(sm, rpc, rpc, n, K + iy0, static_cast<size_t>(M));
   }
   __pipeline_wait_prior(0);
 }
@@ -975,9 +979,13 @@ void launch_t2_rows(const OpDev<R>& d, int B, const void* in, bool in_complex, c
     using S = FftShape<M, RB>;
     const int rpc = choose_rpc(S::T, M, d.n, B, sizeof(cplx<R>), true);
     const size_t smem = static_cast<size_t>(rpc) * S::STRIDE * sizeof(cplx<R>);
-    set_smem(k_t2_rows<M, RB, R>, smem);
     dim3 grid((d.n + rpc - 1) / rpc, B);
-    CK_LAUNCH(launch_k(k_t2_rows<M, RB, R>, grid, rpc * S::T, smem, st, d, in, in_complex ? 1 : 0, pu, rpc));
+    auto go = [&](auto kern) {
+      set_smem(kern, smem);
+      CK_LAUNCH(launch_k(kern, grid, rpc * S::T, smem, st, d, in, in_complex ? 1 : 0, pu, rpc));
+    };
+    if (2 * d.n == M) go(k_t2_rows<M, RB, R, true>);
+    else go(k_t2_rows<M, RB, R, false>);
     note_launch();
   });
 }
@@ -1018,8 +1026,12 @@ void launch_t2_cols(const OpDev<R>& d, int B, const SliceScalars* skip, cudaStre
     } else {
       const int rpc = choose_rpc(S::T, M, M, B, sizeof(cplx<R>), false);
       const size_t smem = static_cast<size_t>(rpc) * S::STRIDE * sizeof(cplx<R>);
-      set_smem(k_t2_cols<M, RB, R>, smem);
-      CK_LAUNCH(launch_k(k_t2_cols<M, RB, R>, dim3(M / rpc, B), rpc * S::T, smem, st, d, rpc, skip));
+      auto go = [&](auto kern) {
+        set_smem(kern, smem);
+        CK_LAUNCH(launch_k(kern, dim3(M / rpc, B), rpc * S::T, smem, st, d, rpc, skip));
+      };
+      if (2 * d.n == M) go(k_t2_cols<M, RB, R, true>);
+      else go(k_t2_cols<M, RB, R, false>);
     }
     note_launch();
   });
@@ -1127,8 +1139,12 @@ void launch_t1_cols_only(const OpDev<R>& d, int B, const SliceScalars* skip, cud
     // one-shot CTAs (also when row + staging do not fit: fp64, m = 8192)
     const int rpc1 = choose_rpc(S::T, M, M, B, sizeof(cplx<R>), true);
     const size_t smem1 = static_cast<size_t>(rpc1) * S::STRIDE * sizeof(cplx<R>);
-    set_smem(k_t1_cols<M, RB, R>, smem1);
-    CK_LAUNCH(launch_k(k_t1_cols<M, RB, R>, dim3(M / rpc1, B), rpc1 * S::T, smem1, st, d, rpc1, skip));
+    auto go = [&](auto kern) {
+      set_smem(kern, smem1);
+      CK_LAUNCH(launch_k(kern, dim3(M / rpc1, B), rpc1 * S::T, smem1, st, d, rpc1, skip));
+    };
+    if (2 * d.n == M) go(k_t1_cols<M, RB, R, true>);
+    else go(k_t1_cols<M, RB, R, false>);
     note_launch();
   });
 }
@@ -1149,9 +1165,13 @@ void launch_t1_rows(const OpDev<R>& d, int B, const PbEpi<R>& e, cudaStream_t st
       while ((rpc * S::T) % 32) rpc <<= 1;
       while (rpc > 1 && (d.n + rpc - 1) / rpc > MAX_PART_BLOCKS) rpc <<= 1;
       const size_t smem = static_cast<size_t>(rpc) * S::STRIDE * sizeof(cplx<R>);
-      set_smem(k_t1_rows<M, RB, R>, smem);
       dim3 grid((d.n + rpc - 1) / rpc, B);
-      CK_LAUNCH(launch_k(k_t1_rows<M, RB, R>, grid, rpc * S::T, smem, st, d, e, rpc));
+      auto go = [&](auto kern) {
+        set_smem(kern, smem);
+        CK_LAUNCH(launch_k(kern, grid, rpc * S::T, smem, st, d, e, rpc));
+      };
+      if (2 * d.n == M) go(k_t1_rows<M, RB, R, true>);
+      else go(k_t1_rows<M, RB, R, false>);
     }
     note_launch();
   });
