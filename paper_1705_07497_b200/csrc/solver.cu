@@ -164,15 +164,32 @@ __global__ void __launch_bounds__(kVecThreads) k_cgcg_final(int64_t L, const R* 
 constexpr int kTile = 64;
 constexpr int kTileRows = 4;  // thread rows
 
+// Radius 1 (the surrogate default): 8 resident CTAs per SM for fp32 (32 registers; measured
+// c4 stencil 69.0 -> 67.4 us against the unconstrained 84-register build); TOMO_STENCIL_MINB
+// overrides for A/B runs.
+#ifndef TOMO_STENCIL_MINB
+#define TOMO_STENCIL_MINB 0
+#endif
 template <int RAD, typename R>
-__global__ void __launch_bounds__(256) k_stencil(int n, StencilCoef coef, int mode, const R* __restrict__ in,
+constexpr int stencil_minb() {
+  return TOMO_STENCIL_MINB > 0 ? TOMO_STENCIL_MINB : RAD == 1 ? (sizeof(R) == 4 ? 8 : 4) : 1;
+}
+
+template <int RAD, typename R>
+__global__ void __launch_bounds__(256, stencil_minb<RAD, R>()) k_stencil(int n, StencilCoef coef, int mode, const R* __restrict__ in,
                                                  const R* __restrict__ r_in, R* __restrict__ p_out,
                                                  R* __restrict__ ap_out, const R* __restrict__ bvec,
                                                  R* __restrict__ x_out, SysParams sys, int step, Reduce red) {
   constexpr int HALO = RAD > 1 ? RAD : 1;
   constexpr int W = kTile + 2 * HALO;
   constexpr int SIDE = 2 * RAD + 1;
-  __shared__ R q[W][W + 1];
+  constexpr int VW = 16 / sizeof(R);
+  // smem tile: the interior columns start at PADL (16-byte aligned rows: vector stores), the
+  // halo columns sit just left / right of them; logical column lj lives at q[.][CO + lj]
+  constexpr int PADL = ((HALO + VW - 1) / VW) * VW;
+  constexpr int CO = PADL - HALO;
+  constexpr int QS = PADL + kTile + PADL;
+  __shared__ __align__(16) R q[W][QS];
   __shared__ R cf[SIDE * SIDE];
   __shared__ double scratch[32];
   const int b = blockIdx.z;
@@ -191,63 +208,59 @@ __global__ void __launch_bounds__(256) k_stencil(int n, StencilCoef coef, int mo
   for (int k = threadIdx.x; k < SIDE * SIDE; k += blockDim.x) cf[k] = static_cast<R>(coef.c[k]);
   const size_t off = static_cast<size_t>(b) * n * n;
   const int i0 = blockIdx.y * kTile - HALO, j0 = blockIdx.x * kTile - HALO;
-  // the halo tile. n % (16/sizeof R) == 0: the kTile interior columns of each row with 16-byte
-  // vector loads (aligned: they start at a multiple of kTile), the 2*HALO halo columns scalar;
-  // otherwise every element scalar.
-  auto put = [&](int li, int lj, R v, R rv) {
-    q[li][lj] = (mode == 0 && step > 0) ? rv + beta * v : v;
-  };
-  constexpr int VW = 16 / sizeof(R);
+  const bool upd = mode == 0 && step > 0;  // q = r + beta p (the CG p-update, solver.cpp:84)
+  // the halo tile. n % VW == 0: the kTile interior columns of each row with 16-byte vector
+  // loads and stores (aligned: they start at a multiple of kTile), the 2*HALO halo columns
+  // scalar; otherwise every element scalar.
   if (n % VW == 0) {
     using V = typename Vec16<R>::T;
-    constexpr int VPR = kTile / VW;  // vectors per interior row
-#pragma unroll 4
-    for (int idx = threadIdx.x; idx < W * VPR; idx += blockDim.x) {
-      const int li = idx / VPR, vq = idx - li * VPR;
-      const int gi = i0 + li, gj = j0 + HALO + vq * VW;
-      R v[VW], rv[VW];
+    constexpr int VPR = kTile / VW;   // vectors per interior row
+    constexpr int RPP = 256 / VPR;    // rows per pass of the 256 threads
+    const int vq = threadIdx.x % VPR, lr = threadIdx.x / VPR;
+    const int gj = j0 + HALO + vq * VW;
+#pragma unroll 3
+    for (int li = lr; li < W; li += RPP) {
+      const int gi = i0 + li;
+      V a, rr;
+      R* ae = reinterpret_cast<R*>(&a);
+      R* re = reinterpret_cast<R*>(&rr);
 #pragma unroll
-      for (int e = 0; e < VW; ++e) v[e] = rv[e] = R(0);
+      for (int e = 0; e < VW; ++e) ae[e] = re[e] = R(0);
       if (gi >= 0 && gi < n && gj < n) {
         const size_t o = off + static_cast<size_t>(gi) * n + gj;
-        const V a = *reinterpret_cast<const V*>(in + o);
-        const R* ae = reinterpret_cast<const R*>(&a);
-#pragma unroll
-        for (int e = 0; e < VW; ++e) v[e] = ae[e];
-        if (mode == 0 && step > 0) {
-          const V rr = *reinterpret_cast<const V*>(r_in + o);
-          const R* re = reinterpret_cast<const R*>(&rr);
-#pragma unroll
-          for (int e = 0; e < VW; ++e) rv[e] = re[e];
-        }
+        a = *reinterpret_cast<const V*>(in + o);
+        if (upd) rr = *reinterpret_cast<const V*>(r_in + o);
       }
+      if (upd) {
 #pragma unroll
-      for (int e = 0; e < VW; ++e) put(li, HALO + vq * VW + e, v[e], rv[e]);
+        for (int e = 0; e < VW; ++e) ae[e] = re[e] + beta * ae[e];
+      }
+      *reinterpret_cast<V*>(&q[li][PADL + vq * VW]) = a;
     }
-    for (int idx = threadIdx.x; idx < W * 2 * HALO; idx += blockDim.x) {
+    for (int idx = threadIdx.x; idx < W * 2 * HALO; idx += 256) {
       const int li = idx / (2 * HALO), h = idx - li * (2 * HALO);
       const int lj = h < HALO ? h : kTile + h;
-      const int gi = i0 + li, gj = j0 + lj;
+      const int gi = i0 + li, gj2 = j0 + lj;
       R v = 0, rv = 0;
-      if (gi >= 0 && gi < n && gj >= 0 && gj < n) {
-        const size_t o = off + static_cast<size_t>(gi) * n + gj;
+      if (gi >= 0 && gi < n && gj2 >= 0 && gj2 < n) {
+        const size_t o = off + static_cast<size_t>(gi) * n + gj2;
         v = in[o];
-        if (mode == 0 && step > 0) rv = r_in[o];
+        if (upd) rv = r_in[o];
       }
-      put(li, lj, v, rv);
+      q[li][CO + lj] = upd ? rv + beta * v : v;
     }
   } else {
 #pragma unroll 6
     for (int idx = threadIdx.x; idx < W * W; idx += blockDim.x) {
       const int li = idx / W, lj = idx - li * W;
-      const int gi = i0 + li, gj = j0 + lj;
+      const int gi = i0 + li, gj2 = j0 + lj;
       R v = 0, rv = 0;
-      if (gi >= 0 && gi < n && gj >= 0 && gj < n) {
-        const size_t o = off + static_cast<size_t>(gi) * n + gj;
+      if (gi >= 0 && gi < n && gj2 >= 0 && gj2 < n) {
+        const size_t o = off + static_cast<size_t>(gi) * n + gj2;
         v = in[o];
-        if (mode == 0 && step > 0) rv = r_in[o];
+        if (upd) rv = r_in[o];
       }
-      put(li, lj, v, rv);
+      q[li][CO + lj] = upd ? rv + beta * v : v;
     }
   }
   __syncthreads();
@@ -263,7 +276,7 @@ __global__ void __launch_bounds__(256) k_stencil(int n, StencilCoef coef, int mo
 #pragma unroll
   for (int k = 0; k < SIDE - 1; ++k)
 #pragma unroll
-    for (int dj = 0; dj < SIDE; ++dj) win[k + 1][dj] = q[r0 - RAD + k][lj - RAD + dj];
+    for (int dj = 0; dj < SIDE; ++dj) win[k + 1][dj] = q[r0 - RAD + k][CO + lj - RAD + dj];
 #pragma unroll
   for (int k = 0; k < RPT; ++k) {
     const int li = r0 + k;
@@ -272,7 +285,7 @@ __global__ void __launch_bounds__(256) k_stencil(int n, StencilCoef coef, int mo
 #pragma unroll
       for (int dj = 0; dj < SIDE; ++dj) win[a][dj] = win[a + 1][dj];
 #pragma unroll
-    for (int dj = 0; dj < SIDE; ++dj) win[SIDE - 1][dj] = q[li + RAD][lj - RAD + dj];
+    for (int dj = 0; dj < SIDE; ++dj) win[SIDE - 1][dj] = q[li + RAD][CO + lj - RAD + dj];
     const int gi = i0 + li;
     if (gi >= n || gj >= n) continue;
     const R c = win[RAD][RAD];
