@@ -451,10 +451,14 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--batch", type=int, default=0, help="c3: independent inputs per apply call (0: config)")
+    ap.add_argument("--slices", type=int, default=0,
+                    help="c4: total slices (0: config's 256); e.g. 32 on one GPU = one rank's share at N=8")
     args = ap.parse_args()
     c = dict(CONFIGS[args.config])
     if args.batch:
         c["batch"] = args.batch
+    if args.slices:
+        c["slices"] = args.slices
     world, rank, local = dist_init()
 
     if args.impl == "reference":
