@@ -16,6 +16,10 @@
 #pragma once
 #include "common.cuh"
 
+#ifndef TOMO_TW_SPLIT_M
+#define TOMO_TW_SPLIT_M 4096  // rows at least this long use split twiddle reads (A/B: 1 << 30 = never)
+#endif
+
 namespace tomo_b200 {
 
 template <int RADIX, typename C2>
@@ -119,26 +123,39 @@ struct FftShape {
   static_assert(NP >= 2, "at least two passes");
 };
 
+// Twiddle table entry W^i. SPLIT (long rows, M >= 4096: the 64-128 KB table does not stay in
+// L1 next to the CTA's row buffer): W^i = W^(i & ~63) * W^(i & 63), two reads from a 17 KB
+// L1-resident subset of the same table, one extra rounding.
+template <bool SPLIT, typename C2>
+TOMO_DEV C2 tw_at(const C2* __restrict__ tw, int i) {
+  if constexpr (SPLIT) {
+    const int lo = i & 63;  // tw[0] = 1 exactly: the product is exact for lo = 0
+    return cmul(__ldg(&tw[i - lo]), __ldg(&tw[lo]));
+  } else {
+    return __ldg(&tw[i]);
+  }
+}
+
 // v[r] *= W^{r * base} for r = 1..R-1, W = e^{-2 pi i / M}: four table loads, the rest by
 // products (w3 = w1 w2, w5 = w4 w1, ..., w15 = w8 w7).
-template <int R, typename C2>
+template <int R, typename C2, bool SPLIT = false>
 TOMO_DEV void twiddle(C2* v, const C2* __restrict__ tw, int base) {
-  const C2 w1 = __ldg(&tw[base]);
+  const C2 w1 = tw_at<SPLIT>(tw, base);
   v[1] = cmul(v[1], w1);
   if constexpr (R >= 4) {
-    const C2 w2 = __ldg(&tw[2 * base]);
+    const C2 w2 = tw_at<SPLIT>(tw, 2 * base);
     const C2 w3 = cmul(w1, w2);
     v[2] = cmul(v[2], w2);
     v[3] = cmul(v[3], w3);
     if constexpr (R >= 8) {
-      const C2 w4 = __ldg(&tw[4 * base]);
+      const C2 w4 = tw_at<SPLIT>(tw, 4 * base);
       const C2 w5 = cmul(w4, w1), w6 = cmul(w4, w2), w7 = cmul(w4, w3);
       v[4] = cmul(v[4], w4);
       v[5] = cmul(v[5], w5);
       v[6] = cmul(v[6], w6);
       v[7] = cmul(v[7], w7);
       if constexpr (R >= 16) {
-        const C2 w8 = __ldg(&tw[8 * base]);
+        const C2 w8 = tw_at<SPLIT>(tw, 8 * base);
         v[8] = cmul(v[8], w8);
         v[9] = cmul(v[9], cmul(w8, w1));
         v[10] = cmul(v[10], cmul(w8, w2));
@@ -185,7 +202,7 @@ TOMO_DEV void fft_pass(C2* row, const C2* __restrict__ tw, int Ns, int t, bool a
       }
       if (!FIRST) {
         const int jm = j & (Ns - 1);
-        if (jm) twiddle<R, C2>(v[q], tw, (M / (Ns * R)) * jm);
+        if (jm) twiddle<R, C2, (M >= TOMO_TW_SPLIT_M)>(v[q], tw, (M / (Ns * R)) * jm);
       }
       Dft<R, C2>::run(v[q]);
     }
