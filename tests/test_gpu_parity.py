@@ -54,6 +54,14 @@ GEOMS = {
     "n128": dict(n=128, n_angles=50, n_b=129, win_lo=-2, win_hi=3, tau=3 / 128 ** 2),
 }
 
+# Long rows (m = 4096): the persistent FFT-pass kernels (m >= 4096), the split twiddle reads, and
+# at R = 2 the quarter-pruned pass variants; few angles keep the oracle's W/W^T cheap.
+LARGE_GEOMS = {
+    "n2048_m4096": dict(n=2048, n_angles=8, n_b=2049, win_lo=-2, win_hi=3, tau=3 / 2048 ** 2),
+    "n1024_R4_m4096": dict(n=1024, n_angles=8, n_b=1025, oversample=4, win_lo=-2, win_hi=3,
+                           tau=np.pi * 3 / (1024 ** 2 * 4 * 3.5)),
+}
+
 
 @pytest.mark.parametrize("prec", PRECS)
 @pytest.mark.parametrize("rows", [3, 600])
@@ -88,6 +96,23 @@ def test_forward_adjoint_normal(T, name, prec):
     ur = RNG.standard_normal((n, n))
     if not f64:
         ur = ur.astype(np.float32)
+    assert rel(op.apply_normal_real(cuda(ur, False, f64)).cpu().numpy().ravel(), O.apply_normal_real(og, ur).ravel()) < tol
+
+
+@pytest.mark.parametrize("prec", PRECS)
+@pytest.mark.parametrize("name", list(LARGE_GEOMS))
+def test_long_rows_vs_oracle(T, name, prec):
+    f64 = prec == "f64"
+    tol = OP_TOL_F64 if f64 else OP_TOL
+    og = O.Geometry(**LARGE_GEOMS[name])
+    op = T.make_direct_backend(pgeom(T, og), precision=prec)
+    n = og.n
+    u = RNG.standard_normal((n, n)) + 1j * RNG.standard_normal((n, n))
+    ur = RNG.standard_normal((n, n))
+    if not f64:
+        u = u.astype(np.complex64)
+        ur = ur.astype(np.float32)
+    assert rel(op.apply_normal(cuda(u, True, f64)).cpu().numpy().ravel(), O.apply_normal(og, u).ravel()) < tol
     assert rel(op.apply_normal_real(cuda(ur, False, f64)).cpu().numpy().ravel(), O.apply_normal_real(og, ur).ravel()) < tol
 
 
