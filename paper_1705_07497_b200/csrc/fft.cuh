@@ -184,7 +184,8 @@ TOMO_DEV constexpr bool mid_quarter(int r) { return R >= 4 && r >= R / 4 && r < 
 // row, so a barrier separates the last reads from those writes.
 template <int M, int RB, int R, bool FIRST, bool LAST, bool STORE_SMEM_LAST, typename C2, int PR = 0,
           typename Load, typename Store>
-TOMO_DEV void fft_pass(C2* row, const C2* __restrict__ tw, int Ns, int t, bool active, Load& load, Store& store) {
+TOMO_DEV void fft_pass(C2* row, const C2* __restrict__ tw, int Ns, int t, bool active, Load& load, Store& store,
+                       const C2* tws = nullptr) {
   constexpr int T = M / RB;
   constexpr int NB = M / R;    // butterflies per pass
   constexpr int PER = NB / T;  // butterflies per thread (RB/R)
@@ -202,7 +203,16 @@ TOMO_DEV void fft_pass(C2* row, const C2* __restrict__ tw, int Ns, int t, bool a
       }
       if (!FIRST) {
         const int jm = j & (Ns - 1);
-        if (jm) twiddle<R, C2, (M >= TOMO_TW_SPLIT_M)>(v[q], tw, (M / (Ns * R)) * jm);
+        if (jm) {
+          if (R == RB && Ns == RB && tws) {
+            // second pass: the RB - 1 twiddles of sub-transform jm from the CTA's smem table
+            // layout [r][jm]: the lanes of a warp (consecutive jm) read consecutive entries
+#pragma unroll
+            for (int r = 1; r < R; ++r) v[q][r] = cmul(v[q][r], tws[r * RB + jm]);
+          } else {
+            twiddle<R, C2, (M >= TOMO_TW_SPLIT_M)>(v[q], tw, (M / (Ns * R)) * jm);
+          }
+        }
       }
       Dft<R, C2>::run(v[q]);
     }
@@ -227,6 +237,27 @@ TOMO_DEV void fft_pass(C2* row, const C2* __restrict__ tw, int Ns, int t, bool a
   if (!LAST || STORE_SMEM_LAST) __syncthreads();
 }
 
+// Twiddles of the second pass (Ns = RB, radix RB): entry [r][jm] = W^(r * jm * M / RB^2), the same
+// for every row of the CTA. Filled before the first pass (whose closing barrier publishes it);
+// the pass then reads its RB - 1 twiddles from smem instead of 4 table loads + 11 products.
+// TOMO_TWS=0 (A/B) keeps the table-load path.
+#ifndef TOMO_TWS
+#define TOMO_TWS 1
+#endif
+template <int M, int RB, typename C2>
+TOMO_DEV const C2* fill_tws(const C2* __restrict__ tw) {
+  if constexpr (TOMO_TWS && RB * RB <= M) {
+    __shared__ __align__(16) C2 tws[RB * RB];
+    for (int k = threadIdx.x; k < RB * RB; k += blockDim.x) {
+      const int r = k / RB, jm = k % RB;
+      tws[k] = __ldg(&tw[(M / (RB * RB)) * jm * r]);
+    }
+    return tws;
+  } else {
+    return nullptr;
+  }
+}
+
 // Forward FFT whose first-pass inputs were loaded earlier into registers: pre[r] holds the
 // element at position t + r*M/RB (what load(t + r*M/RB) would return). Lets a persistent
 // kernel prefetch the next row while the current one is transformed.
@@ -235,6 +266,7 @@ TOMO_DEV void fft_row_pre(C2* row, const C2* __restrict__ tw, int t, bool active
                           Store&& store) {
   using S = FftShape<M, RB>;
   static_assert(S::T * RB == M, "one first-pass butterfly per thread");
+  const C2* tws = fill_tws<M, RB, C2>(tw);
   if (active) {
     C2 v[RB];
 #pragma unroll
@@ -249,18 +281,18 @@ TOMO_DEV void fft_row_pre(C2* row, const C2* __restrict__ tw, int t, bool active
     int Ns = RB;
 #pragma unroll
     for (int p = 1; p < S::NB; ++p) {
-      fft_pass<M, RB, RB, false, false, false, C2>(row, tw, Ns, t, active, noload, store);
+      fft_pass<M, RB, RB, false, false, false, C2>(row, tw, Ns, t, active, noload, store, tws);
       Ns *= RB;
     }
-    fft_pass<M, RB, S::RL, false, true, STORE_SMEM, C2>(row, tw, Ns, t, active, noload, store);
+    fft_pass<M, RB, S::RL, false, true, STORE_SMEM, C2>(row, tw, Ns, t, active, noload, store, tws);
   } else {
     int Ns = RB;
 #pragma unroll
     for (int p = 1; p < S::NB - 1; ++p) {
-      fft_pass<M, RB, RB, false, false, false, C2>(row, tw, Ns, t, active, noload, store);
+      fft_pass<M, RB, RB, false, false, false, C2>(row, tw, Ns, t, active, noload, store, tws);
       Ns *= RB;
     }
-    fft_pass<M, RB, RB, false, true, STORE_SMEM, C2>(row, tw, Ns, t, active, noload, store);
+    fft_pass<M, RB, RB, false, true, STORE_SMEM, C2>(row, tw, Ns, t, active, noload, store, tws);
   }
 }
 
@@ -268,23 +300,24 @@ TOMO_DEV void fft_row_pre(C2* row, const C2* __restrict__ tw, int t, bool active
 template <int M, int RB, bool STORE_SMEM, typename C2, int PR = 0, typename Load, typename Store>
 TOMO_DEV void fft_row(C2* row, const C2* __restrict__ tw, int t, bool active, Load&& load, Store&& store) {
   using S = FftShape<M, RB>;
+  const C2* tws = fill_tws<M, RB, C2>(tw);
   fft_pass<M, RB, RB, true, false, false, C2, PR & 1>(row, tw, 1, t, active, load, store);
   if constexpr (S::RL > 1) {
     int Ns = RB;
 #pragma unroll
     for (int p = 1; p < S::NB; ++p) {
-      fft_pass<M, RB, RB, false, false, false, C2>(row, tw, Ns, t, active, load, store);
+      fft_pass<M, RB, RB, false, false, false, C2>(row, tw, Ns, t, active, load, store, tws);
       Ns *= RB;
     }
-    fft_pass<M, RB, S::RL, false, true, STORE_SMEM, C2, PR & 2>(row, tw, Ns, t, active, load, store);
+    fft_pass<M, RB, S::RL, false, true, STORE_SMEM, C2, PR & 2>(row, tw, Ns, t, active, load, store, tws);
   } else {
     int Ns = RB;
 #pragma unroll
     for (int p = 1; p < S::NB - 1; ++p) {
-      fft_pass<M, RB, RB, false, false, false, C2>(row, tw, Ns, t, active, load, store);
+      fft_pass<M, RB, RB, false, false, false, C2>(row, tw, Ns, t, active, load, store, tws);
       Ns *= RB;
     }
-    fft_pass<M, RB, RB, false, true, STORE_SMEM, C2, PR & 2>(row, tw, Ns, t, active, load, store);
+    fft_pass<M, RB, RB, false, true, STORE_SMEM, C2, PR & 2>(row, tw, Ns, t, active, load, store, tws);
   }
 }
 
