@@ -350,13 +350,13 @@ class Workload:
             steps = c.get("cg", 10)
             iters = c.get("iters", 1)
             a = iters * (steps + 1)
-            counts = {"t2_rows": a, "t2_cols": a, "w_spmv": a, "wt_spread": a, "t1_cols": a, "t1_rows": a,
+            counts = {"t2_rows": a, "t2_cols": a, "w_spmv": a, "wt_spread": a, "t1_cols": a, "wt_t1": a, "t1_rows": a,
                       # Chronopoulos-Gear CG (default): one update kernel per CG call, the others
                       # are fused into the next step's first FFT pass (TOMO_CG=std: one per step)
                       "cg_update": iters * steps if os.environ.get("TOMO_CG") == "std" else iters,
                       "sb_post": iters}
         elif k == "apply":
-            counts = {"t2_rows": 1, "t2_cols": 1, "w_spmv": 1, "wt_spread": 1, "t1_cols": 1, "t1_rows": 1}
+            counts = {"t2_rows": 1, "t2_cols": 1, "w_spmv": 1, "wt_spread": 1, "t1_cols": 1, "wt_t1": 1, "t1_rows": 1}
         else:  # surrogate
             counts = {"stencil": c["iters"] * (c["cg"] + 1), "cg_update": c["iters"] * c["cg"], "sb_post": c["iters"]}
         share = {s: counts.get(s, 0) * prof[s][0] for s in prof}

@@ -261,7 +261,7 @@ TOMO_DEV const C2* fill_tws(const C2* __restrict__ tw) {
 // Forward FFT whose first-pass inputs were loaded earlier into registers: pre[r] holds the
 // element at position t + r*M/RB (what load(t + r*M/RB) would return). Lets a persistent
 // kernel prefetch the next row while the current one is transformed.
-template <int M, int RB, bool STORE_SMEM, typename C2, typename Store>
+template <int M, int RB, bool STORE_SMEM, typename C2, int PR = 0, typename Store>
 TOMO_DEV void fft_row_pre(C2* row, const C2* __restrict__ tw, int t, bool active, const C2 (&pre)[RB],
                           Store&& store) {
   using S = FftShape<M, RB>;
@@ -284,7 +284,7 @@ TOMO_DEV void fft_row_pre(C2* row, const C2* __restrict__ tw, int t, bool active
       fft_pass<M, RB, RB, false, false, false, C2>(row, tw, Ns, t, active, noload, store, tws);
       Ns *= RB;
     }
-    fft_pass<M, RB, S::RL, false, true, STORE_SMEM, C2>(row, tw, Ns, t, active, noload, store, tws);
+    fft_pass<M, RB, S::RL, false, true, STORE_SMEM, C2, PR & 2>(row, tw, Ns, t, active, noload, store, tws);
   } else {
     int Ns = RB;
 #pragma unroll
@@ -292,7 +292,7 @@ TOMO_DEV void fft_row_pre(C2* row, const C2* __restrict__ tw, int t, bool active
       fft_pass<M, RB, RB, false, false, false, C2>(row, tw, Ns, t, active, noload, store, tws);
       Ns *= RB;
     }
-    fft_pass<M, RB, RB, false, true, STORE_SMEM, C2>(row, tw, Ns, t, active, noload, store, tws);
+    fft_pass<M, RB, RB, false, true, STORE_SMEM, C2, PR & 2>(row, tw, Ns, t, active, noload, store, tws);
   }
 }
 

@@ -89,6 +89,12 @@ struct OpDev {
   int n_heavy;
   int n_slots;
   cplx<R>* wt_part;                // B x n_slots x 32 partial sums of split blocks
+  // the same tasks grouped by grid row for the fused W^T + PA kernel (k_wt_t1): tasks of row
+  // iy at [wt_roff[iy], wt_roff[iy+1]), heavy blocks of row iy at [wt_hoff[iy], wt_hoff[iy+1])
+  const int4* wt_rtasks;           // nullptr: not built (the fused kernel is not used)
+  const int4* wt_rheavy;           // heavy blocks in block order
+  const int* wt_roff;              // [m+1]
+  const int* wt_hoff;              // [m+1]
   cplx<R>* Gt;                     // B x m x m  spread grid [iy][ix]; untouched nodes stay 0
   cplx<R>* H;                      // B x m x n  (type-2 row pass output, [iy][t1])
   cplx<R>* g;                      // B x m x m  (oversampled spatial grid, [iy][ix])
@@ -196,6 +202,11 @@ void launch_wt_rows(const OpDev<R>& d, int B, const SliceScalars* skip, cudaStre
 template <typename R>
 void launch_wt_spread(const OpDev<R>& d, int B, const cplx<R>* samples, cplx<R>* grid, const SliceScalars* skip,
                       cudaStream_t st);
+// W^T + PA fused (k_wt_t1, m < 4096, needs the row-grouped task tables); false = not taken.
+template <typename R>
+bool wt_t1_enabled(const OpDev<R>& d);
+template <typename R>
+bool launch_wt_t1(const OpDev<R>& d, int B, const SliceScalars* skip, cudaStream_t st);
 template <typename R>
 void launch_t1_cols_only(const OpDev<R>& d, int B, const SliceScalars* skip, cudaStream_t st);
 // Fused (Gram) backend: grid_out = (W^T W) grid_in on the oversampled grid.

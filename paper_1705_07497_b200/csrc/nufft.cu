@@ -507,6 +507,95 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F3
   store_transposed<S::STRIDE>(sm, rpc, rpc, n, K + iy0, static_cast<size_t>(M));
 }
 
+// W^T + PA in one kernel (grids up to m = 2048): the CTA that transforms spread-grid rows
+// iy0..iy0+rpc-1 first computes them, straight into its smem rows, from the row's W^T tasks
+// (same warp-task arithmetic and summation order as k_task_spmv, so the node values are
+// bit-identical), then runs PA's pruned forward FFT and transposed K store. The spread grid Gt
+// never goes to HBM/L2: the separate path writes and re-reads m^2 complex values per apply.
+// Split blocks publish their partials to global memory; after a barrier the CTA sums each
+// heavy block's partials in slot order (as the ticketed fix-up does) into smem.
+template <int M, int RB, typename R, bool HALF, int GRP>
+__global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F32 : TOMO_FFT_MINB_F64)
+k_wt_t1(OpDev<R> d, int rpc, const SliceScalars* skip) {
+  using S = FftShape<M, RB>;
+  using C2 = cplx<R>;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  C2* sm = reinterpret_cast<C2*>(smraw);
+  const int b = blockIdx.y;
+  if (skip && (skip[b].done || skip[b].frozen)) return;
+  const int n = d.n;
+  // CTA order 0, last, 1, last-1, ...: the heavy rows around the DC row (both ends of the
+  // wrapped grid) start in the first wave
+  const int nb = gridDim.x, bx = blockIdx.x;
+  const int iy0 = ((bx & 1) ? nb - 1 - (bx >> 1) : (bx >> 1)) * rpc;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int k = threadIdx.x; k < rpc * S::STRIDE; k += blockDim.x) sm[k] = czero<C2>();
+  __syncthreads();
+  constexpr int bpr = M / 32;
+  const C2* s = d.s + static_cast<size_t>(b) * d.P;
+  C2* part = d.wt_part + static_cast<size_t>(b) * d.n_slots * 32;
+  const int t_end = __ldg(&d.wt_roff[iy0 + rpc]);
+  for (int task = __ldg(&d.wt_roff[iy0]) + warp; task < t_end; task += nw) {
+    const int4 tk = __ldg(&d.wt_rtasks[task]);
+    const int blk = tk.x, nc = tk.z, slot = tk.w;
+    const int ix = __ldg(&d.wt_perm[static_cast<size_t>(blk) * 32 + lane]);
+    const WtEnt<R>* e = d.wt_ent + static_cast<size_t>(tk.y) * 32 + lane;
+    C2 a0 = czero<C2>(), a1 = czero<C2>();
+    for (int c = 0; c < nc; c += GRP) {
+      WtEnt<R> q[GRP];
+      C2 v[GRP];
+#pragma unroll
+      for (int k = 0; k < GRP; ++k) {
+        if (c + k < nc) {
+          q[k] = ldcs(e + (c + k) * 32);
+        } else {
+          q[k].j = 0;
+          q[k].w = R(0);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < GRP; ++k) v[k] = c + k < nc ? __ldg(&s[q[k].j]) : czero<C2>();
+#pragma unroll
+      for (int k = 0; k < GRP; k += 2) {
+        a0.x += q[k].w * v[k].x;
+        a0.y += q[k].w * v[k].y;
+        a1.x += q[k + 1].w * v[k + 1].x;
+        a1.y += q[k + 1].w * v[k + 1].y;
+      }
+    }
+    const C2 v = cadd(a0, a1);
+    if (slot < 0)
+      sm[(blk / bpr - iy0) * S::STRIDE + pad16(ix)] = v;
+    else
+      part[static_cast<size_t>(slot) * 32 + lane] = v;
+  }
+  const int h0 = __ldg(&d.wt_hoff[iy0]), h1 = __ldg(&d.wt_hoff[iy0 + rpc]);
+  if (h1 > h0) {
+    __syncthreads();  // partials of this CTA's split blocks are visible to the whole CTA
+    for (int h = h0 + warp; h < h1; h += nw) {
+      const int4 hv = __ldg(&d.wt_rheavy[h]);
+      C2 acc = czero<C2>();
+      for (int k = 0; k < hv.z; ++k) acc = cadd(acc, __ldcg(&part[static_cast<size_t>(hv.y + k) * 32 + lane]));
+      const int ix = __ldg(&d.wt_perm[static_cast<size_t>(hv.x) * 32 + lane]);
+      sm[(hv.x / bpr - iy0) * S::STRIDE + pad16(ix)] = acc;
+    }
+  }
+  __syncthreads();
+  const int rr = threadIdx.x / S::T, t = threadIdx.x % S::T;
+  const bool active = rr < rpc;
+  C2* row = sm + (active ? rr : 0) * S::STRIDE;
+  C2 pre[RB];
+#pragma unroll
+  for (int r = 0; r < RB; ++r) pre[r] = row[pad16(t + r * S::T)];
+  __syncthreads();
+  fft_row_pre<M, RB, true, C2, HALF ? 2 : 0>(row, d.tw, t, active, pre, [&](int k, C2 v) {
+    const int t1 = (k + n / 2) & (M - 1);  // inverse of bin_of
+    if (t1 < n) row[pad16(t1)] = v;
+  });
+  C2* K = d.K + static_cast<size_t>(b) * n * M;
+  store_transposed<S::STRIDE>(sm, rpc, rpc, n, K + iy0, static_cast<size_t>(M));
+}
+
 template <typename R>
 __device__ __forceinline__ R ktk_at(const R* __restrict__ p, int n, int i, int j, R c) {
   // (grad^T grad p)(i,j) with the reference's Neumann boundary (solver.cpp:12-43)
@@ -1110,8 +1199,50 @@ void launch_gram(const OpDev<R>& d, int B, const cplx<R>* grid_in, cplx<R>* grid
   launch_task_spmv<R>(d.gram, d.m, B, grid_in, static_cast<size_t>(d.m) * d.m, grid_out, skip, st);
 }
 
+// Fused W^T + PA (k_wt_t1) for m < kPersistMinM when the row-grouped task tables exist
+// (TOMO_WT_FUSE=1; default off). Returns false if not taken. Measured on B200 and rejected as
+// the default: c2 W^T + PA 14.8 + 9.1 us -> 67 us, c3 31.6 + 15.8 -> 88 us, the same at 256 /
+// 512 / 1024 threads per CTA — each CTA's gather chain (a row's tasks) and FFT run back to
+// back with 1-2 CTAs per SM, where the separate task kernel spreads the rows' tasks over
+// every warp of the GPU.
+template <typename R>
+bool wt_t1_enabled(const OpDev<R>& d) {
+  static const int env_fuse = env_int("TOMO_WT_FUSE", 0);
+  return env_fuse && d.wt_rtasks && d.m < kPersistMinM;
+}
+
+template <typename R>
+bool launch_wt_t1(const OpDev<R>& d, int B, const SliceScalars* skip, cudaStream_t st) {
+  if (!wt_t1_enabled<R>(d)) return false;
+  bool done = false;
+  dispatch_m_cols(d.m, sizeof(cplx<R>), [&](auto MC, auto RC) {
+    constexpr int M = decltype(MC)::value, RB = decltype(RC)::value;
+    using S = FftShape<M, RB>;
+    if constexpr (M < kPersistMinM) {
+      const int rpc = choose_rpc(S::T, M, M, B, sizeof(cplx<R>), true);
+      if ((rpc * S::T) % 32) return;
+      const size_t smem = static_cast<size_t>(rpc) * S::STRIDE * sizeof(cplx<R>);
+      constexpr int GRP = sizeof(R) == 4 ? 6 : 4;
+      // more warps than the FFT rows need: the W^T phase is gather-latency-bound and the heavy
+      // rows' tasks are spread over all warps of the CTA (TOMO_WT_T1_THREADS: A/B override)
+      static const int env_thr = env_int("TOMO_WT_T1_THREADS", kFftThreads);
+      const int threads = std::max(rpc * S::T, std::min(env_thr, kFftThreads) / 32 * 32);
+      auto go = [&](auto kern) {
+        set_smem(kern, smem);
+        CK_LAUNCH(launch_k(kern, dim3(M / rpc, B), threads, smem, st, d, rpc, skip));
+      };
+      if (2 * d.n == M) go(k_wt_t1<M, RB, R, true, GRP>);
+      else go(k_wt_t1<M, RB, R, false, GRP>);
+      note_launch();
+      done = true;
+    }
+  });
+  return done;
+}
+
 template <typename R>
 void launch_wt_rows(const OpDev<R>& d, int B, const SliceScalars* skip, cudaStream_t st) {
+  if (launch_wt_t1<R>(d, B, skip, st)) return;
   launch_wt_spread<R>(d, B, d.s, d.Gt, skip, st);
   launch_t1_cols_only<R>(d, B, skip, st);
 }
@@ -1224,6 +1355,8 @@ void launch_fft_rows_test(int m, int rows, const cplx<R>* tw, const cplx<R>* in,
   template void launch_wt_spread<R>(const OpDev<R>&, int, const cplx<R>*, cplx<R>*, const SliceScalars*,    \
                                     cudaStream_t);                                                          \
   template void launch_wt_rows<R>(const OpDev<R>&, int, const SliceScalars*, cudaStream_t);                 \
+  template bool wt_t1_enabled<R>(const OpDev<R>&);                                                           \
+  template bool launch_wt_t1<R>(const OpDev<R>&, int, const SliceScalars*, cudaStream_t);                   \
   template void launch_t1_cols_only<R>(const OpDev<R>&, int, const SliceScalars*, cudaStream_t);            \
   template void launch_gram<R>(const OpDev<R>&, int, const cplx<R>*, cplx<R>*, const SliceScalars*, cudaStream_t); \
   template void launch_t1_rows<R>(const OpDev<R>&, int, const PbEpi<R>&, cudaStream_t);                     \

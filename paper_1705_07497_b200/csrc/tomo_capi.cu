@@ -272,6 +272,7 @@ struct tomo_op {
   int n_tasks = 0, n_heavy = 0, n_slots = 0;
   Raw apod, tw, wcols, wvals, wbase, wxs, wys, wtent, wttasks, wtperm, wtheavy, wtslotheavy;
   Raw wperm;           // separable-W table position -> sample (grid-tile order)
+  Raw wtrtasks, wtrheavy, wtroff;  // W^T tasks / heavy blocks grouped by grid row (k_wt_t1)
   bool w_sorted = false;
   TaskSet gram;  // fused backend only
   const TspmFile* src = nullptr;  // during tomo_op_create_tspm: the loaded Gram / surrogate T
@@ -360,6 +361,10 @@ struct tomo_op {
     d.n_heavy = n_heavy;
     d.n_slots = n_slots;
     d.wt_part = sc.part_wt.as<cplx<R>>();
+    d.wt_rtasks = wtroff.p ? wtrtasks.as<int4>() : nullptr;
+    d.wt_rheavy = wtroff.p ? wtrheavy.as<int4>() : nullptr;
+    d.wt_roff = wtroff.p ? wtroff.as<int>() : nullptr;
+    d.wt_hoff = wtroff.p ? wtroff.as<int>() + (g.m + 1) : nullptr;
     d.Gt = sc.Gt.as<cplx<R>>();
     d.H = sc.H.as<cplx<R>>();
     d.g = sc.g.as<cplx<R>>();
@@ -889,6 +894,36 @@ void build_w_gpu(tomo_op* op) {
                       op->wtheavy.as<int4>(), op->wtslotheavy.as<int>(), 0);
 }
 
+// W^T tasks and heavy blocks regrouped by grid row for the fused W^T + PA kernel (k_wt_t1):
+// tasks of a row longest first (the CTA's warps take them in turn), heavy blocks in block
+// order; offsets per row. Only for m < 4096 and with TOMO_WT_FUSE=1 (A/B; the two-kernel
+// path is the default).
+void build_row_tasks(tomo_op* op) {
+  const int m = op->g.m;
+  const char* fuse = std::getenv("TOMO_WT_FUSE");
+  if (m >= 4096 || op->n_tasks <= 0 || !(fuse && std::atoi(fuse) != 0)) return;
+  std::vector<int4> tasks(op->n_tasks), heavy(op->n_heavy);
+  CK(cudaMemcpy(tasks.data(), op->wttasks.p, sizeof(int4) * tasks.size(), cudaMemcpyDeviceToHost));
+  if (op->n_heavy > 0)
+    CK(cudaMemcpy(heavy.data(), op->wtheavy.p, sizeof(int4) * heavy.size(), cudaMemcpyDeviceToHost));
+  const int bpr = m / 32;
+  std::stable_sort(tasks.begin(), tasks.end(), [&](const int4& a, const int4& b) {
+    const int ra = a.x / bpr, rb = b.x / bpr;
+    return ra != rb ? ra < rb : a.z > b.z;
+  });
+  std::stable_sort(heavy.begin(), heavy.end(), [](const int4& a, const int4& b) { return a.x < b.x; });
+  std::vector<int> off(2 * (m + 1), 0);
+  for (const int4& t : tasks) ++off[t.x / bpr + 1];
+  for (const int4& h : heavy) ++off[m + 1 + h.x / bpr + 1];
+  for (int iy = 0; iy < m; ++iy) {
+    off[iy + 1] += off[iy];
+    off[m + 1 + iy + 1] += off[m + 1 + iy];
+  }
+  op->wtrtasks.upload(tasks);
+  op->wtrheavy.upload(heavy.empty() ? std::vector<int4>(1) : heavy);
+  op->wtroff.upload(off);
+}
+
 template <typename R>
 void build_tables(tomo_op* op) {
   const Geom& g = op->g;
@@ -905,6 +940,7 @@ void build_tables(tomo_op* op) {
     build_w_gpu<R>(op);
   else
     build_w_host<R>(op);
+  build_row_tasks(op);
   // separable W in 16x16 grid-tile order: concurrently running warps gather from nearby nodes
   const char* word = std::getenv("TOMO_W_ORDER");
   op->w_sorted = op->w_sep && !(word && std::string(word) == "angle");
@@ -1005,11 +1041,11 @@ void normal_core(tomo_op* op, int B, const void* in, bool complex_in, const PUpd
   launch_t2_cols<R>(d, B, skip, st);
   if (op->fused()) {
     launch_gram<R>(d, B, d.g, d.Gt, skip, st);
+    launch_t1_cols_only<R>(d, B, skip, st);
   } else {
     launch_w<R>(d, B, d.g, d.s, skip, st);
-    launch_wt_spread<R>(d, B, d.s, d.Gt, skip, st);
+    launch_wt_rows<R>(d, B, skip, st);  // W^T + PA (one fused kernel where available)
   }
-  launch_t1_cols_only<R>(d, B, skip, st);
   launch_t1_rows<R>(d, B, e, st);
 }
 
@@ -2462,9 +2498,11 @@ int tomo_profile_stages(tomo_op* op, int batch, int reps, double* ms, double* by
           else
             launch_w<R>(d, batch, d.g, d.s, op->scal(), cs);
         } else if (s == 3) {
-          launch_wt_spread<R>(d, batch, d.s, d.Gt, op->scal(), cs);
+          // W^T; with the fused W^T + PA kernel this stage is both and stage 4 is empty
+          if (op->fused() || !launch_wt_t1<R>(d, batch, op->scal(), cs))
+            launch_wt_spread<R>(d, batch, d.s, d.Gt, op->scal(), cs);
         } else if (s == 4) {
-          launch_t1_cols_only<R>(d, batch, op->scal(), cs);
+          if (op->fused() || !wt_t1_enabled<R>(d)) launch_t1_cols_only<R>(d, batch, op->scal(), cs);
         } else if (s == 5) {
           PbEpi<R> e = plain_epi<R>(PB_CG_STEP, 1.0);
           e.p = S.p0.as<R>();
@@ -2493,7 +2531,10 @@ int tomo_profile_stages(tomo_op* op, int batch, int reps, double* ms, double* by
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
-    auto stage_on = [&](int s) { return sur ? (s >= 6) : (s <= 7 && !(op->fused() && s == 3)); };
+    const bool wt_fused = !sur && !op->fused() && wt_t1_enabled<R>(d);  // stage 3 = W^T + PA, no stage 4
+    auto stage_on = [&](int s) {
+      return sur ? (s >= 6) : (s <= 7 && !(op->fused() && s == 3) && !(wt_fused && s == 4));
+    };
     for (int s = 0; s < TOMO_NUM_STAGES; ++s) {
       const bool on = stage_on(s);
       if (!on) continue;
@@ -2529,7 +2570,8 @@ int tomo_profile_stages(tomo_op* op, int batch, int reps, double* ms, double* by
       by[2] = op->fused()  // Gram stream, read + write touched nodes | W stream, touched nodes, samples
                   ? static_cast<double>(op->gram.bytes) + B * (2 * cs * op->wt_rows)
                   : wbytes + B * (cs * op->wt_rows + cs * P);
-      by[3] = wtbytes + B * (cs * P + cs * op->wt_rows);   // W^T stream, samples, write touched nodes
+      by[3] = wt_fused ? wtbytes + B * (cs * P + cs * mn)  // W^T stream, samples, write K (grid stays on chip)
+                       : wtbytes + B * (cs * P + cs * op->wt_rows);  // W^T stream, samples, write touched nodes
       by[4] = B * (cs * mm + cs * mn);                     // read spread grid, write K
       by[5] = B * (cs * mn + 2 * rs * nn);                 // read K, p; write Ap
     } else {

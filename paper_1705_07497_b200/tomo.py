@@ -432,7 +432,10 @@ class NormalBackend:
         stream = C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
         _check(lib().tomo_profile_stages(self._h, batch, reps, ms.ctypes.data_as(C.c_void_p),
                                          by.ctypes.data_as(C.c_void_p), stream))
-        return {name: (float(ms[i]), float(by[i])) for i, name in enumerate(_lib.STAGE_NAMES) if by[i] > 0}
+        out = {name: (float(ms[i]), float(by[i])) for i, name in enumerate(_lib.STAGE_NAMES) if by[i] > 0}
+        if "wt_spread" in out and "t1_cols" not in out and "w_spmv" in out:
+            out["wt_t1"] = out.pop("wt_spread")  # the fused W^T + PA kernel (k_wt_t1)
+        return out
 
     # ---------------------------------------------------------------- on-disk operators
     def save_sparse(self, path, angle_subsample_d: int = 1):
