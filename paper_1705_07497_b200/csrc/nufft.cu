@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(256) k_w(OpDev<R> d, int B, const cplx<R>* __r
 // Same matrix as k_w, stored as its rank-1 blocks: per row j the base node (ix0, iy0) and the
 // two window factor vectors (SoA, coalesced): 4 + 2w*sizeof(R) bytes per row instead of
 // w^2*(4 + sizeof(R)). The inner loop walks a grid row (b fixed, ix0+a consecutive).
-template <int BT, int WMAX, int RU, typename R>
+template <int BT, int WMAX, int RU, typename R, bool BY = false>  // BY: slice groups across grid.y
 __global__ void __launch_bounds__(256) k_w_sep(OpDev<R> d, int B, const cplx<R>* __restrict__ grid,
                                                 cplx<R>* __restrict__ out, const SliceScalars* skip) {
   using C2 = cplx<R>;
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(256) k_w_sep(OpDev<R> d, int B, const cplx<R>*
     }
   }
   const size_t G = static_cast<size_t>(m) * m;
-  for (int b0 = 0; b0 < B; b0 += BT) {
+  for (int b0 = BY ? static_cast<int>(blockIdx.y) * BT : 0; b0 < B; b0 += (BY ? static_cast<int>(gridDim.y) : 1) * BT) {
     C2 acc[BT];
 #pragma unroll
     for (int q = 0; q < BT; ++q) acc[q] = czero<C2>();
@@ -374,7 +374,10 @@ __global__ void __launch_bounds__(256) k_w_sep_wide(OpDev<R> d, int B, const cpl
 // One warp per task {block, chunk0, nchunks, slot}: lane l accumulates node (block, l) over
 // the task's chunks (coalesced 32-entry chunks, 4 in flight), then writes either the grid node
 // (iy*m + perm) or, for a split block, its partial slot.
-template <int GRP, bool PIPE, typename R>
+// BY: slices across grid.y (batched launches with a small task grid); BY = false keeps the
+// in-warp slice loop with fp32's 32 registers (the grid.y form needs 34: 6 instead of 8 CTAs
+// per SM, c3 W^T 31.6 -> 34.6 us)
+template <int GRP, bool PIPE, typename R, bool BY = false>
 __global__ void __launch_bounds__(256) k_task_spmv(TaskSpmv<R> ts, int m, int B, const cplx<R>* __restrict__ s_all,
                                                     size_t in_stride, cplx<R>* __restrict__ grid,
                                                     const SliceScalars* skip) {
@@ -389,7 +392,7 @@ __global__ void __launch_bounds__(256) k_task_spmv(TaskSpmv<R> ts, int m, int B,
   const int ix = __ldg(&ts.perm[static_cast<size_t>(blk) * 32 + lane]);
   const size_t G = static_cast<size_t>(m) * m;
   const WtEnt<R>* e = ts.ent + static_cast<size_t>(c0) * 32 + lane;
-  for (int b = 0; b < B; ++b) {
+  for (int b = BY ? static_cast<int>(blockIdx.y) : 0; b < B; b += BY ? static_cast<int>(gridDim.y) : 1) {
     if (skip && (skip[b].done || skip[b].frozen)) continue;
     const C2* s = s_all + static_cast<size_t>(b) * in_stride;
     C2 a0 = czero<C2>(), a1 = czero<C2>();
@@ -1126,6 +1129,17 @@ void launch_t2_cols(const OpDev<R>& d, int B, const SliceScalars* skip, cudaStre
   });
 }
 
+// Batched calls (B slices per launch) of the small-grid SpMVs: slice groups go to grid.y
+// until the launch has about 8 CTAs of 256 threads per SM, instead of each thread / warp
+// looping over all B slices (c1: 86-CTA W and ~110-CTA W^T grids with B = 7 per lane).
+// TOMO_BATCH_Y=0 restores the in-thread loop (A/B runs).
+unsigned batch_ydim(int blocks, int groups) {
+  static const int env_on = env_int("TOMO_BATCH_Y", 1);
+  if (!env_on || groups <= 1) return 1u;
+  const int target = 148 * 8;
+  return static_cast<unsigned>(std::max(1, std::min(groups, (target + blocks - 1) / std::max(blocks, 1))));
+}
+
 template <typename R>
 void launch_w(const OpDev<R>& d, int B, const cplx<R>* grid, cplx<R>* samples, const SliceScalars* skip,
               cudaStream_t st) {
@@ -1137,7 +1151,10 @@ void launch_w(const OpDev<R>& d, int B, const cplx<R>* grid, cplx<R>* samples, c
     // (c2 8.8-9.2 us, c3 16-19 us); 1 needs the fewest registers
     auto go = [&](auto WC) {
       constexpr int WM = decltype(WC)::value;
-      if (B >= 2)
+      const unsigned ydim = batch_ydim(blocks, (B + 1) / 2);
+      if (B >= 2 && ydim > 1)
+        CK_LAUNCH(launch_k(k_w_sep<2, WM, 1, R, true>, dim3(blocks, ydim), threads, 0, st, d, B, grid, samples, skip));
+      else if (B >= 2)
         CK_LAUNCH(launch_k(k_w_sep<2, WM, 1, R>, blocks, threads, 0, st, d, B, grid, samples, skip));
       else
         CK_LAUNCH(launch_k(k_w_sep<1, WM, 1, R>, blocks, threads, 0, st, d, B, grid, samples, skip));
@@ -1171,18 +1188,22 @@ void launch_task_spmv(const TaskSpmv<R>& ts, int m, int B, const cplx<R>* x, siz
   static const int env_grp = env_int("TOMO_WT_GRP", 0), env_pipe = env_int("TOMO_WT_PIPE", -1);
   const bool pipe = env_pipe >= 0 ? env_pipe != 0 : (sizeof(R) == 8 && m <= 2048);
   const int grp = env_grp > 0 ? env_grp : (sizeof(R) == 4 ? 6 : 4);
-  auto go = [&](auto kern) {
-    CK_LAUNCH(launch_k(kern, blocks, threads, 0, st, ts, m, B, x, in_stride, grid, skip));
+  const unsigned ydim = batch_ydim(blocks, B);
+  auto go = [&](auto kern, auto kern_by) {
+    if (ydim > 1)
+      CK_LAUNCH(launch_k(kern_by, dim3(blocks, ydim), threads, 0, st, ts, m, B, x, in_stride, grid, skip));
+    else
+      CK_LAUNCH(launch_k(kern, blocks, threads, 0, st, ts, m, B, x, in_stride, grid, skip));
   };
   if constexpr (sizeof(R) == 4) {
-    if (pipe && grp == 4) go(k_task_spmv<4, true, R>);
-    else if (pipe) go(k_task_spmv<6, true, R>);
-    else go(k_task_spmv<6, false, R>);
+    if (pipe && grp == 4) go(k_task_spmv<4, true, R>, k_task_spmv<4, true, R, true>);
+    else if (pipe) go(k_task_spmv<6, true, R>, k_task_spmv<6, true, R, true>);
+    else go(k_task_spmv<6, false, R>, k_task_spmv<6, false, R, true>);
   } else {
-    if (pipe && grp == 2) go(k_task_spmv<2, true, R>);
-    else if (pipe && grp == 6) go(k_task_spmv<6, true, R>);
-    else if (pipe) go(k_task_spmv<4, true, R>);
-    else go(k_task_spmv<4, false, R>);
+    if (pipe && grp == 2) go(k_task_spmv<2, true, R>, k_task_spmv<2, true, R, true>);
+    else if (pipe && grp == 6) go(k_task_spmv<6, true, R>, k_task_spmv<6, true, R, true>);
+    else if (pipe) go(k_task_spmv<4, true, R>, k_task_spmv<4, true, R, true>);
+    else go(k_task_spmv<4, false, R>, k_task_spmv<4, false, R, true>);
   }
   note_launch();
 }
