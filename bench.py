@@ -37,7 +37,9 @@ CONFIGS = {
     # the 100 independent applies are issued as calls of 20 inputs (run on the library's lanes)
     "c1": dict(n=256, A=60, nb=367, R=2, lo=-2, hi=3, kind="c1", alpha=1.0, applies=100, batch=20, cg=20, prec="f64",
                metric="normal-op applies/sec", unit="applies/s"),
-    "c2": dict(n=512, A=90, nb=725, R=2, lo=-2, hi=3, kind="sb", alpha=10.0, lam=1.0, iters=50, cg=10, prec="f64",
+    # the reference's own m_sp = 3 window ([-3, 3], 7x7, tau = 3/n^2): BASELINE c2 states no width,
+    # so both arms run the same operator (same_config with the --impl reference arm)
+    "c2": dict(n=512, A=90, nb=725, R=2, lo=-3, hi=3, kind="sb", alpha=10.0, lam=1.0, iters=50, cg=10, prec="f64",
                metric="split-Bregman slices/sec", unit="slices/s"),
     # 1000 applies on random-normal inputs, issued as calls of 3 independent inputs that the
     # library runs on three concurrent lanes (streams with their own grids)
@@ -73,6 +75,17 @@ def dist_init():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return world, rank, local
+
+
+def launcher_cmd(gpus: int, argv):
+    """torchrun command running `bench.py argv` as `gpus` ranks on this node (127.0.0.1)."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
 
 
 def allreduce_max(x: float, world: int) -> float:
@@ -196,13 +209,17 @@ class Workload:
         self.units_per_step = 1
         self.h2d = self.d2h = 0
         if kind == "sb":
-            self.op = T.make_direct_backend(g, precision=c["prec"], device=local)
-            self.f = torch.from_numpy(synth_slices(T, self.op, c, [1000 + rank], torch)).cuda()
+            # `batch` independent slices per step, solved together (slice pairs on grid.y)
+            self.batch = int(c.get("batch", 1))
+            self.op = T.make_direct_backend(g, precision=c["prec"], device=local, max_batch=self.batch)
+            seeds = [1000 + rank * self.batch + i for i in range(self.batch)]
+            self.f = torch.from_numpy(synth_slices(T, self.op, c, seeds, torch)).cuda()
+            self.units_per_step = self.batch
             self.cfg = T.SolverConfig(alpha=c["alpha"], lambda_=c["lam"], max_bregman_iters=c["iters"],
                                       cg_steps_per_update=c["cg"], update_tol_rel=0.0)
             self.f_host = self.f.cpu().pin_memory()
             self.h2d = self.f.numel() * self.f.element_size()
-            self.d2h = g.n * g.n * (8 if self.op.f64 else 4)
+            self.d2h = self.batch * g.n * g.n * (8 if self.op.f64 else 4)
         elif kind == "sb_sur":
             per_rank = (c["slices"] + world - 1) // world
             lo = rank * per_rank
@@ -344,7 +361,7 @@ class Workload:
         # the kernels as launched: c4 batches; c1/c3 calls of `batch` inputs run on the library's
         # lanes (TOMO_LANES, default 3) as sub-batches of ceil(batch / lanes)
         lanes = min(max(int(os.environ.get("TOMO_LANES", "3") or 3), 1), 4)
-        B = self.batch if k == "sb_sur" else (-(-self.batch // lanes) if k in ("apply", "c1") else 1)
+        B = self.batch if k in ("sb_sur", "sb") else (-(-self.batch // lanes) if k in ("apply", "c1") else 1)
         prof = self.op.profile_stages(batch=B, reps=10)
         if k in ("sb", "c1", "cp"):
             steps = c.get("cg", 10)
@@ -363,11 +380,39 @@ class Workload:
         top = max(share, key=share.get)
         ms, by = prof[top]
         achieved = by / (ms * 1e-3) / 1e9
-        return top, {"bound": "hbm", "kernel": top, "achieved": round(achieved, 1), "peak": peak_gbs,
-                     "unit": "GB/s", "frac": round(achieved / peak_gbs, 4), "traffic": None,
-                     "algorithmic_bytes_per_launch": int(by), "ms_per_launch": round(ms, 5),
-                     "stage_ms": {s: round(v[0], 5) for s, v in prof.items()},
-                     "stage_share_of_step": {s: round(v / max(sum(share.values()), 1e-12), 4) for s, v in share.items()}}
+        out = {"bound": "hbm", "kernel": top, "achieved": round(achieved, 1), "peak": peak_gbs,
+               "unit": "GB/s", "frac": round(achieved / peak_gbs, 4), "traffic": None,
+               "algorithmic_bytes_per_launch": int(by), "ms_per_launch": round(ms, 5),
+               "stage_ms": {s: round(v[0], 5) for s, v in prof.items()},
+               "stage_share_of_step": {s: round(v / max(sum(share.values()), 1e-12), 4) for s, v in share.items()}}
+        if k != "sb_sur":
+            # the whole normal-operator apply against SURVEY §8(d)'s bytes_apply, over the sum of
+            # its six stage times (live, per launch of B slices)
+            stages = ("t2_rows", "t2_cols", "w_spmv", "wt_spread", "t1_cols", "t1_rows")
+            t_apply = sum(prof[s][0] for s in stages if s in prof)
+            ab = apply_bytes(c, self.op.info.wt_rows, complex_io=(k == "apply"), B=B)
+            out["apply"] = {"bytes": int(ab), "ms": round(t_apply, 5), "slices_per_launch": B,
+                            "achieved": round(ab / (t_apply * 1e-3) / 1e9, 1),
+                            "frac": round(ab / (t_apply * 1e-3) / 1e9 / peak_gbs, 4),
+                            "formula": "SURVEY 8(d): 2(4+r)nnz + 8T + B(in + out + 3cG + cT + 2cP)"}
+        return top, out
+
+
+def apply_bytes(c, T, complex_io, B=1):
+    """SURVEY.md §8(d) algorithmic bytes of one normal-operator apply: input + output images,
+    pad/iFFT write + FFT read + W^T grid write (3 c G), W and W^T entry streams (2 (4 + r) nnz),
+    W's gather of the T touched nodes (c T) + W^T's row pointers and ids (8 T), and the slice
+    write + read (2 c P). r = real bytes, c = 2 r."""
+    r = 8 if c["prec"] == "f64" else 4
+    cb = 2 * r
+    n2 = c["n"] ** 2
+    G = (c["R"] * c["n"]) ** 2
+    P = c["A"] * c["nb"]
+    w = c["hi"] - c["lo"] + 1
+    nnz = P * w * w
+    io = 2 * n2 * (cb if complex_io else r)
+    # matrix streams once per launch, vectors once per slice (B slices per launch)
+    return 2 * (4 + r) * nnz + 8 * T + B * (io + 3 * cb * G + cb * T + 2 * cb * P)
 
 
 def flush_l2(torch, buf):
@@ -375,70 +420,177 @@ def flush_l2(torch, buf):
 
 
 # ----------------------------------------------------------------------------- CPU baseline
-def og_cp(c):
-    from oracle import oracle as O
+# The reference's own CPU code (oracle/_ref: the unmodified reference sources built here with its
+# -O3 -march=native, proj/CMakeLists.txt:10), or the oracle port where the reference has no such
+# path (c4: its surrogate weights assume n_b = n, normal_ops.cpp:208-219; c5: m = 2n is hard-coded,
+# nufft.cpp:40). The reference is single-threaded, so "all host cores" = one process per core,
+# each running its own independent slice / apply, concurrently; units/s = sum over workers.
+SB_SAMPLE_ITERS = 5  # outer split-Bregman iterations timed per worker sample
+
+
+def host_cpu():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except AttributeError:
+        cores = os.cpu_count() or 1
+    return model, cores
+
+
+def _og(c, O):
+    tau = 3.0 / c["n"] ** 2 if c["R"] == 2 else np.pi * max(c["hi"], -c["lo"]) / (c["n"] ** 2 * c["R"] * (c["R"] - 0.5))
     return O.Geometry(n=c["n"], n_angles=c["A"], n_b=c["nb"], oversample=c["R"], win_lo=c["lo"], win_hi=c["hi"],
-                      tau=np.pi * 3 / (c["n"] ** 2 * c["R"] * (c["R"] - 0.5)))
+                      tau=tau)
 
 
-def cpu_sample(cname, c, prefer_reference=True):
-    """Time the reference's CPU path (oracle/_ref) — or the oracle port — on a bounded sample of
-    the workload and extrapolate to the metric's unit. Returns (value, kind, sample, cores)."""
+def ref_kind(c):
+    """'reference' when the reference's own code runs this workload (symmetric window, R = 2,
+    and for the surrogate n_b = n), else 'port'."""
+    from oracle import refbind
+    if not refbind.available() or c["R"] != 2 or c["lo"] != -c["hi"]:
+        return "port"
+    if c["kind"] == "sb_sur" and c["nb"] != c["n"]:
+        return "port"
+    if c["kind"] == "cp":
+        return "port"
+    return "reference"
+
+
+_WORKER_STATE = {}
+
+
+def _cpu_worker(job):
+    """One bounded sample in a spawned process: returns (units, seconds_per_unit_extrapolated,
+    wall seconds of the sample)."""
+    c, kind, seed, threads = job
+    os.environ["ORC_THREADS"] = str(threads)  # read once when the oracle library loads
     from oracle import oracle as O
     from oracle import refbind
-    use_ref = prefer_reference and refbind.available()
-    # the reference's surrogate weights assume n_b = n (radial_density_weights, normal_ops.cpp:208-219):
-    # with n_b != n only the oracle port runs the surrogate split Bregman
-    if c["kind"] == "sb_sur" and c["nb"] != c["n"]:
-        use_ref = False
-    kind = "reference" if use_ref else "port"
-    n, A, nb = c["n"], c["A"], c["nb"]
-    # the reference window is symmetric [-m_sp, m_sp]; the width-6 [-2,3] config maps to m_sp=3
-    msp = 3
-    og = O.Geometry(n=n, n_angles=A, n_b=nb, win_lo=c["lo"], win_hi=c["hi"], tau=3.0 / n ** 2)
-    rng = np.random.default_rng(0)
-    if c["kind"] != "cp":
-        ph = O.random_ellipses(n, 10, 1)
-        f, _ = O.synthesize(og, ph, 0.01, 1)
-    if c["kind"] == "sb" or c["kind"] == "sb_sur":
-        backend = 0 if c["kind"] == "sb" else 2
-        def run(iters):
-            t = time.perf_counter()
-            if use_ref:
-                ref = refbind.Ref(n, A, msp, 3.0 / n ** 2, n_b=nb)
-                ref.split_bregman(f, backend=backend, r=c.get("r", 1), alpha=c["alpha"], lam=c["lam"], iters=iters,
-                                  cg_steps=c["cg"])
-            else:
-                O.split_bregman(og, f, backend=backend, r=c.get("r", 1), alpha=c["alpha"], lam=c["lam"],
-                                max_iters=iters, cg_steps=c["cg"])
-            return time.perf_counter() - t
-        t1 = run(1)
-        t2 = run(2)
-        per_outer = max(t2 - t1, 1e-9)
-        setup = max(t1 - per_outer, 0.0)
-        t_slice = setup + c["iters"] * per_outer
-        sample = (f"split_bregman_tv on one {n}^2 slice ({A}x{nb}, {'m_sp=3 7x7' if use_ref else 'width-6'} window),"
-                  f" 1 and 2 outer x {c['cg']} CG timed; slice time = setup + {c['iters']} x per-outer")
-        return 1.0 / t_slice, kind, sample, 1
-    if c["kind"] == "cp":
-        # the reference hard-codes m_r = 2n (nufft.cpp:40), so R = 4 exists only in the oracle port
-        u = rng.standard_normal((n, n))
-        t = time.perf_counter()
-        O.apply_normal_real(og_cp(c), u)
-        dt = time.perf_counter() - t
-        return 1.0 / dt, "port", f"1 real apply_normal at {n}^2, R=4 (m={4 * n}), {A}x{nb} (oracle port)", 1
+    key = (json.dumps(c, sort_keys=True), kind)
+    st = _WORKER_STATE.get(key)
+    og = _og(c, O)
+    if st is None:  # operator construction is outside every timed region (SPEC.md:552)
+        st = {}
+        if kind == "reference" and c["kind"] in ("sb", "sb_sur", "apply", "c1"):
+            backend = 2 if c["kind"] == "sb_sur" else 0
+            st["rb"] = refbind.RefBackend(c["n"], c["A"], c["hi"], og.tau, n_b=c["nb"], backend=backend,
+                                          r=c.get("r", 1))
+        _WORKER_STATE.clear()
+        _WORKER_STATE[key] = st
+    t_wall = time.perf_counter()
+    if c["kind"] in ("sb", "sb_sur"):
+        ph = O.random_ellipses(c["n"], 10, seed)
+        f, _ = O.synthesize(og, ph, 0.01, seed)
+        k = SB_SAMPLE_ITERS
+        if kind == "reference":
+            _, t_call, t_loop = st["rb"].split_bregman(f, c["alpha"], c["lam"], k, c["cg"])
+        else:
+            t0 = time.perf_counter()
+            O.split_bregman(og, f, backend=2 if c["kind"] == "sb_sur" else 0, r=c.get("r", 1), alpha=c["alpha"],
+                            lam=c["lam"], max_iters=1, cg_steps=c["cg"])
+            t1 = time.perf_counter()
+            O.split_bregman(og, f, backend=2 if c["kind"] == "sb_sur" else 0, r=c.get("r", 1), alpha=c["alpha"],
+                            lam=c["lam"], max_iters=1 + k, cg_steps=c["cg"])
+            t2 = time.perf_counter()
+            t_loop = (t2 - t1) - (t1 - t0)  # k outer iterations, setup cancelled
+            t_call = (t2 - t1)
+        # slice = setup (make_subproblem, leak probe, back-projection) + iters x per-outer
+        t_unit = (t_call - t_loop) + c["iters"] * t_loop / k
+        return 1, t_unit, time.perf_counter() - t_wall
     if c["kind"] in ("apply", "c1"):
-        u = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
-        reps = 3
-        t = time.perf_counter()
-        for _ in range(reps):
-            if use_ref:
-                refbind.Ref(n, A, msp, 3.0 / n ** 2, n_b=nb).apply_normal(u)
-            else:
+        rng = np.random.default_rng(seed)
+        u = rng.standard_normal((c["n"], c["n"])) + 1j * rng.standard_normal((c["n"], c["n"]))
+        if kind == "reference":
+            med, _ = st["rb"].time_apply(u, reps=5)  # time_apply: 1 warm-up + median of 5
+        else:
+            O.apply_normal(og, u)
+            ts = []
+            for _ in range(5):
+                t0 = time.perf_counter()
                 O.apply_normal(og, u)
-        dt = (time.perf_counter() - t) / reps
-        return 1.0 / dt, kind, f"{reps} complex apply_normal calls at {n}^2 ({A}x{nb}), mean", 1
-    raise SystemExit("no cpu sample for " + cname)
+                ts.append(time.perf_counter() - t0)
+            med = statistics.median(ts)
+        return 1, med, time.perf_counter() - t_wall
+    if c["kind"] == "cp":
+        # one real apply (the CP/CG unit of the metric) with the port's FFT rows on all threads
+        u = np.random.default_rng(seed).standard_normal((c["n"], c["n"]))
+        t0 = time.perf_counter()
+        O.apply_normal_real(og, u)
+        return 1, time.perf_counter() - t0, time.perf_counter() - t_wall
+    raise SystemExit("no cpu sample for " + c["kind"])
+
+
+class CpuBaseline:
+    """The reference's CPU path on this box's host cores, one worker process per core (a single
+    worker with threaded FFT rows for c5's one large slice)."""
+
+    def __init__(self, c):
+        self.c = c
+        self.kind = ref_kind(c)
+        self.model, ncores = host_cpu()
+        big = c["kind"] == "cp"
+        self.workers = 1 if big else ncores
+        self.threads = ncores if big else 1
+        self.cores = self.workers * self.threads
+        import concurrent.futures as cf
+        import multiprocessing as mp
+        self.pool = cf.ProcessPoolExecutor(max_workers=self.workers, mp_context=mp.get_context("spawn"))
+        self.seed = 0
+
+    def step(self):
+        """One concurrent sample on every worker: (metric units/s over all workers, wall s)."""
+        t0 = time.perf_counter()
+        jobs = [(self.c, self.kind, 1 + self.seed + w, self.threads) for w in range(self.workers)]
+        self.seed += self.workers
+        res = list(self.pool.map(_cpu_worker, jobs))
+        wall = time.perf_counter() - t0
+        return sum(u / t for u, t, _ in res), wall, res
+
+    def close(self):
+        self.pool.shutdown()
+
+    def describe(self):
+        c = self.c
+        what = {
+            "sb": f"split_bregman_tv on independent {c['n']}^2 slices ({c['A']}x{c['nb']}, window [{c['lo']},{c['hi']}]): "
+                  f"{SB_SAMPLE_ITERS} outer x {c.get('cg')} CG timed per worker sample (the trace's loop time); "
+                  f"slice = (call - loop) + {c.get('iters')} x loop/{SB_SAMPLE_ITERS}",
+            "sb_sur": f"surrogate r={c.get('r')} split Bregman on independent {c['n']}^2 slices: {SB_SAMPLE_ITERS} outer x "
+                      f"{c.get('cg')} CG per worker sample; slice = setup + {c.get('iters')} x per-outer",
+            "apply": f"time_apply (1 warm-up + median of 5 complex apply_normal, backend prebuilt) at {c['n']}^2",
+            "c1": f"time_apply (1 warm-up + median of 5 complex apply_normal, backend prebuilt) at {c['n']}^2; "
+                  f"rate = applies/s",
+            "cp": f"one real apply_normal at {c['n']}^2, R={c['R']} (m={c['R'] * c['n']}), FFT rows on all threads",
+        }[c["kind"]]
+        return (f"{what}; {self.workers} worker process(es) x {self.threads} thread(s) concurrently on "
+                f"{self.model}; kind={self.kind}")
+
+
+# ----------------------------------------------------------------------------- line helpers
+DATA = "synthetic (seeded random ellipses, 1% complex Gaussian noise; c3 random normal)"
+
+
+def scaling_of(c, world):
+    return "strong" if (c["kind"] == "sb_sur" or (c["kind"] == "cp" and world > 1)) else "weak"
+
+
+def config_dict(name, c, world):
+    """The workload as both arms (ours and --impl reference) report it."""
+    w = c["hi"] - c["lo"] + 1
+    P = c["A"] * c["nb"]
+    par = {"sb_sur": "slice-sharded", "cp": "angle-sharded" if world > 1 else "replicas"}.get(c["kind"], "replicas")
+    return {"workload": name, "n": c["n"], "angles": c["A"], "n_b": c["nb"], "oversample": c["R"],
+            "window": [c["lo"], c["hi"]], "m": c["R"] * c["n"], "P": P, "nnz_W": P * w * w, "precision": c["prec"],
+            **{k: c[k] for k in ("alpha", "lam", "iters", "cg", "applies", "slices", "r", "batch") if k in c},
+            "parallelism": f"{par} x{world}"}
 
 
 # ----------------------------------------------------------------------------- main
@@ -450,7 +602,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--batch", type=int, default=0, help="c3: independent inputs per apply call (0: config)")
+    ap.add_argument("--batch", type=int, default=0,
+                    help="c1/c3: independent inputs per apply call; c2: slices solved per step (0: config)")
     ap.add_argument("--slices", type=int, default=0,
                     help="c4: total slices (0: config's 256); e.g. 32 on one GPU = one rank's share at N=8")
     args = ap.parse_args()
@@ -459,29 +612,39 @@ def main():
         c["batch"] = args.batch
     if args.slices:
         c["slices"] = args.slices
-    world, rank, local = dist_init()
-
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torchrun (what the driver does itself)
+        sys.exit(subprocess.call(launcher_cmd(args.gpus, sys.argv[1:])))
     if args.impl == "reference":
-        if rank != 0:
+        # the reference's own CPU path on this box's host cores (rank 0 only; the other ranks
+        # exit without work and without joining a process group)
+        if int(os.environ.get("RANK", "0")) != 0:
             return
-        vals = []
-        kind = sample = None
-        cores = 1
+        cb = CpuBaseline(c)
+        vals, walls = [], []
         for i in range(args.warmup + args.steps):
-            v, kind, sample, cores = cpu_sample(args.config, c)
+            v, wall, _ = cb.step()
             if i >= args.warmup:
                 vals.append(v)
+                walls.append(wall)
+        cb.close()
         v = statistics.median(vals)
         line = {"impl": "reference", "metric": c["metric"], "value": v, "unit": c["unit"], "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / v,  # per unit of the metric (one bounded CPU sample per step)
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic (seeded random ellipses, 1% complex Gaussian noise)",
-                "config": {"workload": args.config},
-                "cpu_baseline": {"value": v, "unit": c["unit"], "cores": cores, "kind": kind, "sample": sample},
+                "steps": args.steps, "warmup": args.warmup,
+                # one step = one concurrent bounded sample on every worker (wall time, measured)
+                "ms_per_step": 1e3 * statistics.mean(walls), "higher_is_better": True,
+                "scaling": scaling_of(c, args.gpus), "vs_baseline": None, "dtype": "f64",
+                "data": DATA, "config": config_dict(args.config, c, args.gpus),
+                "cpu_baseline": {"value": v, "unit": c["unit"], "cores": cb.cores, "kind": cb.kind,
+                                 "sample": cb.describe(), "cpu_model": cb.model, "nproc": host_cpu()[1],
+                                 "samples_per_step": cb.workers},
                 "e2e": {"value": v, "unit": c["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
 
+    world, rank, local = dist_init()
+    if world != args.gpus and rank == 0:
+        print(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}; reporting n_gpus={world}", file=sys.stderr)
     import torch
     torch.cuda.set_device(local)
     import paper_1705_07497_b200 as T
@@ -551,22 +714,23 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, kind, sample, cores = cpu_sample(args.config, c)
-        cpu = {"value": v, "unit": c["unit"], "cores": cores, "kind": kind, "sample": sample}
+        cb = CpuBaseline(c)
+        cb.step()  # worker start-up + operator construction (untimed)
+        v, wall, _ = cb.step()
+        cb.close()
+        cpu = {"value": v, "unit": c["unit"], "cores": cb.cores, "kind": cb.kind, "sample": cb.describe(),
+               "cpu_model": cb.model, "nproc": host_cpu()[1], "sample_wall_s": round(wall, 2)}
 
     if rank == 0:
         info = wl.op.info
         line = {
             "metric": c["metric"], "value": value, "unit": c["unit"], "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
-            "scaling": "strong" if (c["kind"] == "sb_sur" or wl.sharded) else "weak", "vs_baseline": None,
-            "dtype": c["prec"], "data": "synthetic (seeded random ellipses, 1% complex Gaussian noise; c3 random normal)",
-            "config": {"workload": args.config, "n": c["n"], "angles": c["A"], "n_b": c["nb"], "oversample": c["R"],
-                       "window": [c["lo"], c["hi"]], "m": info.m, "P": int(info.P), "nnz_W": int(info.nnz),
-                       "wt_rows": int(info.wt_rows), "wt_slots": int(info.wt_slots), "precision": c["prec"],
-                       "l2": "flushed between timed steps (256 MiB write)",
-                       **{k: c[k] for k in ("alpha", "lam", "iters", "cg", "applies", "slices", "r", "batch") if k in c},
-                       "parallelism": f"{'slice-sharded' if c['kind'] == 'sb_sur' else ('angle-sharded' if wl.sharded else 'replicas')} x{world}"},
+            "scaling": scaling_of(c, world), "vs_baseline": None,
+            "dtype": c["prec"], "data": DATA, "config": config_dict(args.config, c, world),
+            "l2": "flushed between timed steps (256 MiB write)",
+            "operator": {"wt_rows": int(info.wt_rows), "wt_slots": int(info.wt_slots), "P_local": int(info.P),
+                         "nnz_local": int(info.nnz)},
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": c["unit"], "h2d_bytes_per_step": int(wl.h2d),

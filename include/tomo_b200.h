@@ -18,9 +18,12 @@
  * (proj/include/tomo/image.hpp:11-13, proj/include/tomo/fourier_slice.hpp:20-27).
  * `batch` independent slices are stored back to back.
  *
- * Threading: an op is immutable after tomo_op_create except for internal scratch; calls
- * on the same op must be serialized by the caller (one stream at a time). Distinct ops may
- * be used concurrently.
+ * Threading: an op's tables are immutable after tomo_op_create, and
+ * one op may serve several host threads / streams at once. Each call leases a private
+ * workspace (device scratch, lanes, captured CUDA graphs) for its stream: concurrent calls on
+ * distinct streams run concurrently on distinct workspaces (up to 8 per op); a workspace
+ * handed from one stream to another is ordered after the previous stream's work by an event.
+ * tomo_op_set_allreduce / tomo_op_attach_nccl must not race with calls on the same op.
  */
 #ifndef TOMO_B200_H
 #define TOMO_B200_H
@@ -97,8 +100,9 @@ typedef struct tomo_op_info {
 const char* tomo_last_error(void);
 
 /* make_direct_backend / make_fused_backend / make_surrogate_backend (normal_ops.hpp:35-39)
- * over a SliceTransform(SliceGrid, NufftParams) (fourier_slice.hpp:39). Builds W (SELL-32
- * ELL), its transpose, deapodisation and FFT tables on `device`; for the fused backend also
+ * over a SliceTransform(SliceGrid, NufftParams) (fourier_slice.hpp:39). Builds W (separable
+ * per-sample window factors), its row-sorted transpose W^T, deapodisation and FFT tables on
+ * `device`; for the fused backend also
  * the Gram W^T W (build_btb, normal_ops.hpp:47); for the surrogate also the stencil
  * (build_surrogate, normal_ops.hpp:60). */
 int tomo_op_create(const tomo_geom_desc* geom, const tomo_op_desc* desc, tomo_op** out);
@@ -209,8 +213,10 @@ int tomo_chambolle_pock(tomo_op* op, const tomo_cp_config* cfg, const void* slic
                         void* stream);
 
 /* ---- angle-row sharding across GPUs: the partial adjoint images of each rank's angle
- * block are summed by this hook (in place, float32, on `stream`) after every type-1
- * transform (`count` elements of the op's precision). tomo_op_attach_nccl installs an NCCL all-reduce over a communicator built from
+ * block are summed by this hook (in place, `count` elements of the op's precision, float32
+ * or float64 as `precision` says, ordered on `stream`) after every type-1 transform. The hook
+ * runs on the host and may synchronize `stream`; an op with a hook (and no NCCL communicator)
+ * therefore runs its solver loops without CUDA graphs. tomo_op_attach_nccl installs an NCCL all-reduce over a communicator built from
  * a unique id obtained with tomo_nccl_unique_id on one rank and broadcast by the caller. */
 typedef int (*tomo_allreduce_fn)(void* buf, size_t count, int precision, void* stream, void* user);
 int tomo_op_set_allreduce(tomo_op* op, tomo_allreduce_fn fn, void* user);

@@ -5,17 +5,23 @@
 // /root/reference). The restatement is single-threaded and keeps the reference's loop
 // and operation order wherever that order is observable; reductions are plain
 // sequential sums (Eigen's vectorised reductions differ only at the 1e-16 level).
+// Independent work (the rows / columns of fft_2d, the samples of interpolate) is split over
+// host threads (parallel_for, ORC_THREADS or hardware_concurrency); every output element is
+// still computed by the same sequence of operations, so results are bit-identical to a
+// single-threaded run (spread's scatter and every reduction stay sequential).
 #include "tomo_oracle.h"
 
 #include <algorithm>
 #include <cmath>
 #include <complex>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 namespace orc {
@@ -32,6 +38,34 @@ struct NumericalError : std::runtime_error {
 };
 
 thread_local std::string g_last_error;
+
+// Static-chunked parallel loop over [0, count): chunk c of T covers a contiguous range, so
+// which thread computes an element never changes the arithmetic. Small loops run inline.
+static int orc_threads() {
+  static const int t = [] {
+    const char* e = std::getenv("ORC_THREADS");
+    int v = e ? std::atoi(e) : static_cast<int>(std::thread::hardware_concurrency());
+    return std::max(1, std::min(v, 64));
+  }();
+  return t;
+}
+
+template <class F>
+static void parallel_for(int64_t count, int64_t min_parallel, F&& fn) {
+  const int nt = orc_threads();
+  if (nt <= 1 || count < min_parallel) {
+    fn(int64_t(0), count);
+    return;
+  }
+  std::vector<std::thread> pool;
+  const int64_t chunk = (count + nt - 1) / nt;
+  for (int t = 1; t < nt; ++t) {
+    const int64_t b = t * chunk, e = std::min(count, b + chunk);
+    if (b < e) pool.emplace_back([&fn, b, e] { fn(b, e); });
+  }
+  fn(int64_t(0), std::min(count, chunk));
+  for (auto& th : pool) th.join();
+}
 
 // ---------------------------------------------------------------------------------
 // Geometry + spreading plan.
@@ -199,13 +233,17 @@ static void fft_1d_inplace(cd* data, int m, bool inverse) {
 static void fft_2d(CVec& grid, int m, bool inverse) {
   if (static_cast<int64_t>(grid.size()) != static_cast<int64_t>(m) * m)
     throw ConfigError("fft_2d: grid size mismatch");
-  for (int r = 0; r < m; ++r) fft_1d_inplace(grid.data() + static_cast<int64_t>(r) * m, m, inverse);
-  CVec buf(m);
-  for (int c = 0; c < m; ++c) {
-    for (int r = 0; r < m; ++r) buf[r] = grid[static_cast<int64_t>(r) * m + c];
-    fft_1d_inplace(buf.data(), m, inverse);
-    for (int r = 0; r < m; ++r) grid[static_cast<int64_t>(r) * m + c] = buf[r];
-  }
+  parallel_for(m, 256, [&](int64_t r0, int64_t r1) {
+    for (int64_t r = r0; r < r1; ++r) fft_1d_inplace(grid.data() + r * m, m, inverse);
+  });
+  parallel_for(m, 256, [&](int64_t c0, int64_t c1) {
+    CVec buf(m);
+    for (int64_t c = c0; c < c1; ++c) {
+      for (int r = 0; r < m; ++r) buf[r] = grid[static_cast<int64_t>(r) * m + c];
+      fft_1d_inplace(buf.data(), m, inverse);
+      for (int r = 0; r < m; ++r) grid[static_cast<int64_t>(r) * m + c] = buf[r];
+    }
+  });
 }
 
 // ---------------------------------------------------------------------------------
@@ -238,9 +276,10 @@ static CVec interpolate(const Geometry& g, const CVec& grid) {
   if (static_cast<int64_t>(grid.size()) != static_cast<int64_t>(m) * m)
     throw ConfigError("interpolate: grid size mismatch");
   CVec samples(g.P);
-  double wx[64], wy[64];
-  int ix[64], iy[64];
-  for (int64_t j = 0; j < g.P; ++j) {
+  parallel_for(g.P, 4096, [&](int64_t j0, int64_t j1) {
+  for (int64_t j = j0; j < j1; ++j) {
+    double wx[64], wy[64];
+    int ix[64], iy[64];
     weights(g, j, 0, wx);
     weights(g, j, 1, wy);
     for (int a = 0; a < w; ++a) ix[a] = wrap(g.mjx[j] + g.lo + a, m);
@@ -254,6 +293,7 @@ static CVec interpolate(const Geometry& g, const CVec& grid) {
     }
     samples[j] = acc;
   }
+  });
   return samples;
 }
 

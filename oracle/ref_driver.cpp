@@ -10,9 +10,12 @@
 // Geometry is the reference's own: n_b = n, R = 2, window [-m_sp, m_sp]; the angle set
 // theta_a = a*pi/A is built through the public AngleSet struct (fourier_slice.hpp:12-17),
 // which is what make_angle_set produces for count A (fourier_slice.cpp:18).
+#include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <algorithm>
 #include <memory>
+#include <vector>
 #include <string>
 
 #include "tomo/fourier_slice.hpp"
@@ -334,6 +337,91 @@ int ref_save_surrogate(int n, int A, int m_sp, double tau, int r, int euclidean,
   cfg.radius_r = r;
   cfg.euclidean = euclidean != 0;
   save_sparse(build_surrogate(fused, cfg), path);
+  REF_CATCH
+}
+
+// ---- persistent handles for timing (bench.py --impl reference) ---------------------------
+// One geometry + backend built once (operator construction is not timed), then
+// timed calls through the reference's public API: apply_normal with time_apply's semantics
+// (proj/src/bench.cpp:245-257) and split_bregman_tv (proj/src/solver.cpp:219-307).
+struct RefHandle {
+  RefSetup s;
+  NormalBackend b;
+};
+
+// backend: 0 direct, 1 fused, 2 surrogate (radius r). nb: radial samples (0 -> n).
+void* ref_backend_new(int n, int A, int m_sp, double tau, int nb, int backend, int r) {
+  try {
+    g_nb = nb;
+    auto* h = new RefHandle;
+    h->s = make_setup(n, A, m_sp, tau);
+    g_nb = 0;
+    if (backend == 2) {
+      NormalBackend fused = make_direct_backend(h->s.transform);
+      fused.kind = BackendKind::fused;
+      SurrogateConfig cfg;
+      cfg.radius_r = r;
+      h->b.kind = BackendKind::surrogate;
+      h->b.params = h->s.params;
+      h->b.transform = h->s.transform;
+      h->b.t = std::make_shared<SparseOperator>(build_surrogate(fused, cfg));
+      h->b.sample_weights = radial_density_weights(h->s.grid);
+      h->b.surrogate_r = r;
+    } else if (backend == 1) {
+      h->b = make_fused_backend(h->s.transform);
+    } else {
+      h->b = make_direct_backend(h->s.transform);
+    }
+    return h;
+  } catch (const std::exception& e) {
+    g_nb = 0;
+    code_of(e);
+    return nullptr;
+  }
+}
+
+void ref_backend_free(void* h) { delete static_cast<RefHandle*>(h); }
+
+// time_apply (bench.cpp:245-257): one untimed warm-up apply_normal, then `reps` timed ones;
+// returns the median seconds in *median_s and the last output in `out` (complex n^2).
+int ref_backend_time_apply(void* hp, const double* in, int reps, double* out, double* median_s) {
+  REF_TRY
+  auto* h = static_cast<RefHandle*>(hp);
+  const int n = h->b.params.n;
+  const ComplexImage probe(n, cvec(in, Eigen::Index(n) * n));
+  ComplexImage sink = apply_normal(h->b, probe);
+  std::vector<double> times;
+  for (int rep = 0; rep < reps; ++rep) {
+    const auto t0 = std::chrono::steady_clock::now();
+    sink = apply_normal(h->b, probe);
+    times.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+  }
+  std::sort(times.begin(), times.end());
+  *median_s = times.empty() ? 0.0 : times[times.size() / 2];
+  if (out) put(sink.data, out);
+  REF_CATCH
+}
+
+// One timed split_bregman_tv call: *t_call_s = the whole call (make_subproblem, leak probe,
+// back-projection and the Bregman loop), *t_loop_s = the trace's t_total_s at the last
+// iteration (the loop only, solver.cpp:255-296).
+int ref_backend_split_bregman(void* hp, double alpha, double lambda, int iters, int cg_steps,
+                              const double* slice_data, double* mu, double* t_call_s, double* t_loop_s) {
+  REF_TRY
+  auto* h = static_cast<RefHandle*>(hp);
+  SolverConfig cfg;
+  cfg.alpha = alpha;
+  cfg.lambda = lambda;
+  cfg.max_bregman_iters = iters;
+  cfg.cg_steps_per_update = cg_steps;
+  cfg.update_tol_rel = 0.0;
+  const ComplexVector f = cvec(slice_data, h->s.grid.points.count());
+  const auto t0 = std::chrono::steady_clock::now();
+  auto res = split_bregman_tv(h->b, f, cfg);
+  *t_call_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  *t_loop_s = res.second.t_total_s.empty() ? 0.0 : res.second.t_total_s.back();
+  if (mu)
+    for (Eigen::Index i = 0; i < res.first.data.size(); ++i) mu[i] = res.first.data[i];
   REF_CATCH
 }
 

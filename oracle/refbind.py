@@ -15,8 +15,21 @@ _PATH = os.path.join(_HERE, "_ref", "libtomo_ref.so")
 _LIB = None
 
 
+def _host_has_avx512() -> bool:
+    """libtomo_ref.so is built with the reference's -march=native (Sapphire Rapids here; the GPU
+    boxes are Emerald Rapids, same ISA): refuse it on a host without AVX-512F."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("flags"):
+                    return "avx512f" in line.split()
+    except OSError:
+        pass
+    return False
+
+
 def available() -> bool:
-    return os.path.exists(_PATH)
+    return os.path.exists(_PATH) and _host_has_avx512()
 
 
 def lib():
@@ -50,6 +63,12 @@ def lib():
         _LIB.ref_save_btb.argtypes = [C.c_int, C.c_int, C.c_int, d, C.c_char_p]
         _LIB.ref_save_surrogate.argtypes = [C.c_int, C.c_int, C.c_int, d, C.c_int, C.c_int, C.c_char_p]
         _LIB.ref_synthesize.argtypes = [C.c_int, C.c_int, C.c_int, d, C.c_void_p, d, C.c_uint64, C.c_void_p]
+        _LIB.ref_backend_new.restype = C.c_void_p
+        _LIB.ref_backend_new.argtypes = [C.c_int, C.c_int, C.c_int, d, C.c_int, C.c_int, C.c_int]
+        _LIB.ref_backend_free.argtypes = [C.c_void_p]
+        _LIB.ref_backend_time_apply.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+        _LIB.ref_backend_split_bregman.argtypes = [C.c_void_p, d, d, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                                                   C.c_void_p, C.c_void_p]
     return _LIB
 
 
@@ -179,3 +198,44 @@ def shepp_logan(n):
     out = np.empty((n, n))
     _check(lib().ref_shepp_logan(n, _p(out)))
     return out
+
+
+class RefBackend:
+    """A reference NormalBackend built once (construction untimed) for timing the
+    reference's own apply_normal (time_apply semantics, bench.cpp:245-257) and split_bregman_tv."""
+
+    def __init__(self, n, n_angles, m_sp, tau=None, n_b=0, backend=0, r=1):
+        self.n = n
+        self.P = (n_b or n) * n_angles
+        tau = tau if tau is not None else m_sp / float(n * n)
+        self._h = lib().ref_backend_new(n, n_angles, m_sp, tau, n_b, backend, r)
+        if not self._h:
+            raise RuntimeError("reference backend: " + lib().ref_last_error().decode())
+
+    def close(self):
+        if self._h:
+            lib().ref_backend_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def time_apply(self, u, reps=5):
+        """(median seconds of `reps` timed apply_normal calls after one warm-up, last output)."""
+        u = np.ascontiguousarray(u, np.complex128)
+        out = np.empty((self.n, self.n), np.complex128)
+        med = C.c_double()
+        _check(lib().ref_backend_time_apply(self._h, _p(u), reps, _p(out), C.byref(med)))
+        return med.value, out
+
+    def split_bregman(self, f, alpha, lam, iters, cg_steps):
+        """(mu, seconds of the whole call, seconds of the Bregman loop = trace t_total_s[-1])."""
+        f = np.ascontiguousarray(f, np.complex128)
+        mu = np.empty((self.n, self.n))
+        tc, tl = C.c_double(), C.c_double()
+        _check(lib().ref_backend_split_bregman(self._h, alpha, lam, iters, cg_steps, _p(f), _p(mu), C.byref(tc),
+                                               C.byref(tl)))
+        return mu, tc.value, tl.value

@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(256) k_task_spmv(TaskSpmv<R> ts, int m, int B,
     for (int c = 0; c < nc; c += GRP) {
       C2 v[GRP];
 #pragma unroll
-      for (int k = 0; k < GRP; ++k) v[k] = c + k < nc ? __ldg(&s[q[k].j]) : czero<C2>();
+      for (int k = 0; k < GRP; ++k) v[k] = q[k].w != R(0) ? __ldg(&s[q[k].j]) : czero<C2>();
       WtEnt<R> qn[GRP];
 #pragma unroll
       for (int k = 0; k < GRP; ++k) {
@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(256) k_task_spmv(TaskSpmv<R> ts, int m, int B,
         }
       }
 #pragma unroll
-      for (int k = 0; k < GRP; ++k) v[k] = c + k < nc ? __ldg(&s[q[k].j]) : czero<C2>();
+      for (int k = 0; k < GRP; ++k) v[k] = q[k].w != R(0) ? __ldg(&s[q[k].j]) : czero<C2>();
 #pragma unroll
       for (int k = 0; k < GRP; k += 2) {
         a0.x += q[k].w * v[k].x;
@@ -467,6 +467,7 @@ __global__ void __launch_bounds__(256) k_task_spmv(TaskSpmv<R> ts, int m, int B,
       C2* part = ts.part + static_cast<size_t>(b) * ts.n_slots * 32;
       part[static_cast<size_t>(slot) * 32 + lane] = v;
       __threadfence();
+      __syncwarp();  // every lane's partial is fenced before lane 0 takes the ticket
       const int h = __ldg(&ts.slot_heavy[slot]);
       unsigned* cnt = ts.heavy_cnt + static_cast<size_t>(b) * ts.n_heavy + h;
       unsigned ticket = 0;
@@ -557,7 +558,7 @@ k_wt_t1(OpDev<R> d, int rpc, const SliceScalars* skip) {
         }
       }
 #pragma unroll
-      for (int k = 0; k < GRP; ++k) v[k] = c + k < nc ? __ldg(&s[q[k].j]) : czero<C2>();
+      for (int k = 0; k < GRP; ++k) v[k] = q[k].w != R(0) ? __ldg(&s[q[k].j]) : czero<C2>();
 #pragma unroll
       for (int k = 0; k < GRP; k += 2) {
         a0.x += q[k].w * v[k].x;

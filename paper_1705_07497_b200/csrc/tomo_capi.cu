@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -257,6 +258,56 @@ struct GraphEntry {
   int64_t nodes = 0;
 };
 
+// Mutable per-call state of an op: device scratch, execution lanes, host-copy pipeline and the
+// CUDA graphs captured over that scratch. The op itself (geometry, W / W^T / Gram / stencil
+// tables) is immutable after creation and shared; every API call leases one workspace for its
+// stream (Lease below), so concurrent calls on distinct streams use distinct workspaces
+// (built operators are shareable, concurrent solves on separate state are
+// safe).
+struct Workspace {
+  static constexpr int kMaxLanes = 4;
+  Scratch sc;
+  // extra execution lanes for batches of independent slices (apply paths): each has its own
+  // grids, W^T partial/ticket buffers and stream, so sub-batches run concurrently
+  Scratch lanes[kMaxLanes - 1];  // lanes 1..kMaxLanes-1 (lane 0 = sc)
+  int cur_lane = 0;              // dev() hands out lane cur_lane's buffers
+  cudaStream_t lane_st[kMaxLanes - 1] = {};
+  cudaEvent_t lane_fork = nullptr, lane_join[kMaxLanes - 1] = {};
+  // host-buffer pipeline (host_pipeline): copy streams, events, double-buffered staging
+  cudaStream_t pipe_in = nullptr, pipe_out = nullptr;
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
+  Raw pin_buf[2], pout_buf[2];
+  std::map<std::string, GraphEntry> graphs;
+  // lease bookkeeping: the stream of the last call and an event recorded there when it returned
+  cudaStream_t last_stream = nullptr;
+  cudaEvent_t done = nullptr;
+  bool busy = false;
+  uint64_t last_use = 0;
+
+  Workspace() = default;
+  Workspace(const Workspace&) = delete;
+  Workspace& operator=(const Workspace&) = delete;
+  ~Workspace() {
+    clear_graphs();
+    for (int k = 0; k < 2; ++k)
+      for (cudaEvent_t e : {ev_in[k], ev_comp[k], ev_out[k]})
+        if (e) cudaEventDestroy(e);
+    if (pipe_in) cudaStreamDestroy(pipe_in);
+    if (pipe_out) cudaStreamDestroy(pipe_out);
+    if (lane_fork) cudaEventDestroy(lane_fork);
+    if (done) cudaEventDestroy(done);
+    for (int k = 0; k < kMaxLanes - 1; ++k) {
+      if (lane_join[k]) cudaEventDestroy(lane_join[k]);
+      if (lane_st[k]) cudaStreamDestroy(lane_st[k]);
+    }
+  }
+  void clear_graphs() {
+    for (auto& kv : graphs)
+      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    graphs.clear();
+  }
+};
+
 }  // namespace tomo_b200
 
 using namespace tomo_b200;
@@ -277,49 +328,36 @@ struct tomo_op {
   TaskSet gram;  // fused backend only
   const TspmFile* src = nullptr;  // during tomo_op_create_tspm: the loaded Gram / surrogate T
   int w_sep = 1;  // W storage used by the interpolation kernel (TOMO_W_FORMAT=ell selects SELL-32)
-  Scratch sc;
   // surrogate
   int rad = 0;
   StencilCoef coef{};
   double stencil64[81] = {0};
+  // lazily computed, per-op caches (shared by every workspace; guarded by cache_mu)
+  std::mutex cache_mu;
   std::map<std::pair<double, double>, double> sigma_cache;
   double leak = -1.0;
   // collective
   tomo_allreduce_fn ar_fn = nullptr;
   void* ar_user = nullptr;
   ncclComm_t comm = nullptr;
-  std::map<std::string, GraphEntry> graphs;
-
-  // extra execution lanes for batches of independent slices (apply paths): each has its own
-  // grids, W^T partial/ticket buffers and stream, so sub-batches run concurrently
-  static constexpr int kMaxLanes = 4;
-  Scratch lanes[kMaxLanes - 1];  // lanes 1..kMaxLanes-1 (lane 0 = sc)
-  int cur_lane = 0;              // dev() hands out lane cur_lane's buffers
-  cudaStream_t lane_st[kMaxLanes - 1] = {};
-  cudaEvent_t lane_fork = nullptr, lane_join[kMaxLanes - 1] = {};
-  // host-buffer pipeline (host_pipeline): copy streams, events, double-buffered staging
-  cudaStream_t pipe_in = nullptr, pipe_out = nullptr;
-  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
-  Raw pin_buf[2], pout_buf[2];
+  // workspaces (Lease): at most kMaxWorkspaces, one per concurrently calling stream
+  static constexpr int kMaxLanes = Workspace::kMaxLanes;
+  static constexpr int kMaxWorkspaces = 8;
+  std::mutex ws_mu;
+  std::condition_variable ws_cv;
+  std::vector<std::unique_ptr<Workspace>> pool;
+  uint64_t ws_clock = 0;
 
   ~tomo_op() {
-    clear_graphs();
+    pool.clear();
     if (comm) ncclCommDestroy(comm);
-    for (int k = 0; k < 2; ++k)
-      for (cudaEvent_t e : {ev_in[k], ev_comp[k], ev_out[k]})
-        if (e) cudaEventDestroy(e);
-    if (pipe_in) cudaStreamDestroy(pipe_in);
-    if (pipe_out) cudaStreamDestroy(pipe_out);
-    if (lane_fork) cudaEventDestroy(lane_fork);
-    for (int k = 0; k < kMaxLanes - 1; ++k) {
-      if (lane_join[k]) cudaEventDestroy(lane_join[k]);
-      if (lane_st[k]) cudaStreamDestroy(lane_st[k]);
-    }
   }
-  void clear_graphs() {
-    for (auto& kv : graphs)
-      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
-    graphs.clear();
+  // the workspace leased by the calling thread (every scratch-touching entry point holds one)
+  Workspace& W() const;
+  void clear_graphs() { W().clear_graphs(); }
+  void clear_all_graphs() {
+    std::lock_guard<std::mutex> lk(ws_mu);
+    for (auto& w : pool) w->clear_graphs();
   }
 
   bool sharded() const { return g.a0 != 0 || g.a1 != g.A; }
@@ -330,8 +368,9 @@ struct tomo_op {
   template <typename R>
   OpDev<R> dev(int B) {
     ensure_batch(B);
-    if (cur_lane) ensure_lane(cur_lane, B);
-    Scratch& sc = cur_lane ? lanes[cur_lane - 1] : this->sc;
+    Workspace& ws = W();
+    if (ws.cur_lane) ensure_lane(ws.cur_lane, B);
+    Scratch& sc = ws.cur_lane ? ws.lanes[ws.cur_lane - 1] : ws.sc;
     OpDev<R> d{};
     d.n = g.n;
     d.m = g.m;
@@ -377,6 +416,7 @@ struct tomo_op {
   }
 
   void ensure_batch(int B) {
+    Scratch& sc = W().sc;
     if (B <= sc.cap) return;
     const size_t m = g.m, n = g.n, cz = 2 * rsz;
     sc.H.ensure(B * m * n * cz);
@@ -403,13 +443,14 @@ struct tomo_op {
       v->ensure(vl);
     CK(cudaMemset(sc.zero.p, 0, vl));
     sc.upd_log.ensure(sizeof(double) * static_cast<size_t>(B) * kMaxLoggedIters);
+    sc.rel_log.ensure(sizeof(double) * static_cast<size_t>(B) * kMaxLoggedIters);
     sc.cap = B;
     clear_graphs();  // buffers moved
   }
 
   // grids of lane k >= 1 (the apply path only: no solver vectors or scalars)
   void ensure_lane(int k, int B) {
-    Scratch& ln = lanes[k - 1];
+    Scratch& ln = W().lanes[k - 1];
     if (B <= ln.cap) return;
     const size_t m = g.m, n = g.n, cz = 2 * rsz;
     ln.H.ensure(B * m * n * cz);
@@ -431,9 +472,109 @@ struct tomo_op {
     clear_graphs();
   }
 
-  Reduce red() { return Reduce{sc.sc.as<SliceScalars>(), sc.part.as<double>()}; }
-  SliceScalars* scal() { return sc.sc.as<SliceScalars>(); }
+  Reduce red() {
+    Scratch& sc = W().sc;
+    return Reduce{sc.sc.as<SliceScalars>(), sc.part.as<double>()};
+  }
+  SliceScalars* scal() { return W().sc.sc.as<SliceScalars>(); }
 };
+
+namespace tomo_b200 {
+namespace {
+struct LeaseRec {
+  const tomo_op* op;
+  Workspace* ws;
+  int depth;
+};
+thread_local std::vector<LeaseRec> tl_leases;
+
+// Leases one of the op's workspaces to the calling thread for one API call on `st`. Preference:
+// an idle workspace last used on the same stream (its graphs are warm and stream order already
+// serialises it), then an idle one whose last call has completed, then a new one (up to
+// kMaxWorkspaces), then the least recently used idle one; otherwise wait. A workspace last used on another stream is ordered after that stream's work
+// with its `done` event, so device buffers are never shared by two in-flight calls. Nested
+// entries on the same thread reuse the outer lease.
+class Lease {
+ public:
+  Lease(tomo_op* op, cudaStream_t st) : op_(op), st_(st) {
+    for (auto& r : tl_leases)
+      if (r.op == op) {
+        ++r.depth;
+        nested_ = true;
+        return;
+      }
+    std::unique_lock<std::mutex> lk(op->ws_mu);
+    for (;;) {
+      ws_ = nullptr;
+      for (auto& w : op->pool)  // 1. idle, last used on this stream: warm graphs, no wait
+        if (!w->busy && w->last_stream == st) {
+          ws_ = w.get();
+          break;
+        }
+      if (!ws_)
+        for (auto& w : op->pool)  // 2. idle and its last call has finished on the device
+          if (!w->busy && (!w->done || cudaEventQuery(w->done) == cudaSuccess)) {
+            ws_ = w.get();
+            break;
+          }
+      if (!ws_ && static_cast<int>(op->pool.size()) < tomo_op::kMaxWorkspaces) {  // 3. a new one
+        op->pool.emplace_back(new Workspace());
+        ws_ = op->pool.back().get();
+      }
+      if (!ws_)
+        for (auto& w : op->pool)  // 4. least recently used idle one (ordered by its event)
+          if (!w->busy && (!ws_ || w->last_use < ws_->last_use)) ws_ = w.get();
+      if (ws_) break;
+      op->ws_cv.wait(lk);
+    }
+    ws_->busy = true;
+    ws_->last_use = ++op->ws_clock;
+    lk.unlock();
+    if (ws_->done && ws_->last_stream != st) {
+      const cudaError_t e = cudaStreamWaitEvent(st, ws_->done, 0);
+      if (e != cudaSuccess) {
+        release();
+        throw CudaError(std::string("workspace lease: ") + cudaGetErrorString(e));
+      }
+    }
+    tl_leases.push_back({op, ws_, 1});
+  }
+  ~Lease() {
+    if (nested_) {
+      for (auto& r : tl_leases)
+        if (r.op == op_) --r.depth;
+      return;
+    }
+    tl_leases.pop_back();
+    if (!ws_->done) cudaEventCreateWithFlags(&ws_->done, cudaEventDisableTiming);
+    if (ws_->done) cudaEventRecord(ws_->done, st_);
+    ws_->last_stream = st_;
+    release();
+  }
+  Lease(const Lease&) = delete;
+  Lease& operator=(const Lease&) = delete;
+
+ private:
+  void release() {
+    {
+      std::lock_guard<std::mutex> lk(op_->ws_mu);
+      ws_->busy = false;
+    }
+    op_->ws_cv.notify_all();
+  }
+  tomo_op* op_;
+  cudaStream_t st_;
+  Workspace* ws_ = nullptr;
+  bool nested_ = false;
+};
+}  // namespace
+}  // namespace tomo_b200
+
+Workspace& tomo_op::W() const {
+  for (auto it = tl_leases.rbegin(); it != tl_leases.rend(); ++it)
+    if (it->op == this) return *it->ws;
+  throw std::logic_error("libtomo_b200: op scratch used outside a workspace lease");
+}
 
 namespace tomo_b200 {
 namespace {
@@ -1073,32 +1214,32 @@ void run_lanes(tomo_op* op, int batch, cudaStream_t st, F&& f) {
     f(0, batch, st);
     return;
   }
-  if (!op->lane_fork) CK(cudaEventCreateWithFlags(&op->lane_fork, cudaEventDisableTiming));
+  if (!op->W().lane_fork) CK(cudaEventCreateWithFlags(&op->W().lane_fork, cudaEventDisableTiming));
   for (int k = 1; k < nl; ++k)
-    if (!op->lane_st[k - 1]) {
-      CK(cudaStreamCreateWithFlags(&op->lane_st[k - 1], cudaStreamNonBlocking));
-      CK(cudaEventCreateWithFlags(&op->lane_join[k - 1], cudaEventDisableTiming));
+    if (!op->W().lane_st[k - 1]) {
+      CK(cudaStreamCreateWithFlags(&op->W().lane_st[k - 1], cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&op->W().lane_join[k - 1], cudaEventDisableTiming));
     }
   // sub-batch k = [bs(k), bs(k+1)): sizes differ by at most one, larger ones first
   auto bs = [&](int k) { return k * (batch / nl) + std::min(k, batch % nl); };
   op->ensure_batch(bs(1));
   for (int k = 1; k < nl; ++k) op->ensure_lane(k, bs(k + 1) - bs(k));
-  CK(cudaEventRecord(op->lane_fork, st));
-  for (int k = 1; k < nl; ++k) CK(cudaStreamWaitEvent(op->lane_st[k - 1], op->lane_fork, 0));
+  CK(cudaEventRecord(op->W().lane_fork, st));
+  for (int k = 1; k < nl; ++k) CK(cudaStreamWaitEvent(op->W().lane_st[k - 1], op->W().lane_fork, 0));
   f(0, bs(1), st);
   try {
     for (int k = 1; k < nl; ++k) {
-      op->cur_lane = k;
-      f(bs(k), bs(k + 1) - bs(k), op->lane_st[k - 1]);
+      op->W().cur_lane = k;
+      f(bs(k), bs(k + 1) - bs(k), op->W().lane_st[k - 1]);
     }
   } catch (...) {
-    op->cur_lane = 0;
+    op->W().cur_lane = 0;
     throw;
   }
-  op->cur_lane = 0;
+  op->W().cur_lane = 0;
   for (int k = 1; k < nl; ++k) {
-    CK(cudaEventRecord(op->lane_join[k - 1], op->lane_st[k - 1]));
-    CK(cudaStreamWaitEvent(st, op->lane_join[k - 1], 0));
+    CK(cudaEventRecord(op->W().lane_join[k - 1], op->W().lane_st[k - 1]));
+    CK(cudaStreamWaitEvent(st, op->W().lane_join[k - 1], 0));
   }
 }
 
@@ -1132,7 +1273,7 @@ template <typename R>
 void cg_run(tomo_op* op, int B, const SysParams& s, const R* rhs, const R* x0, R* x, int steps, cudaStream_t st) {
   const int n = op->g.n;
   const int64_t L = op->L();
-  Scratch& S = op->sc;
+  Scratch& S = op->W().sc;
   Reduce red = op->red();
   const SliceScalars* skip = op->scal();
   R* r = S.r.as<R>();
@@ -1251,8 +1392,14 @@ void backproject(tomo_op* op, int B, double alpha, bool weighted, const cplx<R>*
 // ---- graph capture of a solver loop -------------------------------------------------------
 template <typename F>
 void run_graph(tomo_op* op, const std::string& key, cudaStream_t st, F&& body) {
-  auto it = op->graphs.find(key);
-  if (it == op->graphs.end()) {
+  // A caller all-reduce hook runs on the host (it may synchronize the stream and exchange
+  // through the host), so it cannot be captured: such ops run their solver loops eagerly.
+  if (op->ar_fn && !op->comm && op->sharded()) {
+    body(st);
+    return;
+  }
+  auto it = op->W().graphs.find(key);
+  if (it == op->W().graphs.end()) {
     // Capture on a private stream so a legacy default stream (0) can still be used.
     cudaStream_t cs;
     CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
@@ -1278,7 +1425,7 @@ void run_graph(tomo_op* op, const std::string& key, cudaStream_t st, F&& body) {
     cudaGraphDestroy(graph);
     cudaStreamDestroy(cs);
     CK(ie);
-    it = op->graphs.emplace(key, ge).first;
+    it = op->W().graphs.emplace(key, ge).first;
   }
   CK(cudaGraphLaunch(it->second.exec, st));
   g_launches.fetch_add(it->second.nodes, std::memory_order_relaxed);
@@ -1336,12 +1483,15 @@ double device_dot(tomo_op* op, const R* x, const R* y, cudaStream_t st) {
 template <typename R>
 double surrogate_sigma(tomo_op* op, double alpha, double lambda, cudaStream_t st, bool feedback = false) {
   auto key = std::make_pair(alpha, feedback ? -lambda - 1.0 : lambda);  // lambda > 0: distinct keys
-  auto it = op->sigma_cache.find(key);
-  if (it != op->sigma_cache.end()) return it->second;
+  {
+    std::lock_guard<std::mutex> lk(op->cache_mu);
+    auto it = op->sigma_cache.find(key);
+    if (it != op->sigma_cache.end()) return it->second;
+  }
   const int n = op->g.n;
   const int64_t L = op->L();
   op->ensure_batch(1);
-  Scratch& S = op->sc;
+  Scratch& S = op->W().sc;
   std::mt19937_64 rng(7);
   std::normal_distribution<double> gauss;
   std::vector<double> v(L);
@@ -1394,6 +1544,7 @@ double surrogate_sigma(tomo_op* op, double alpha, double lambda, cudaStream_t st
     launch_axpby<R>(L, 1.0 / beta, w, 0.0, w, vcur, st);       // v <- w / beta
   }
   const double sigma = feedback ? 1.2 * std::max(0.0, 0.5 * extreme) : 1.2 * std::max(0.0, -extreme);
+  std::lock_guard<std::mutex> lk(op->cache_mu);
   op->sigma_cache[key] = sigma;
   return sigma;
 }
@@ -1408,7 +1559,7 @@ void build_stencil(tomo_op* op, cudaStream_t st) {
   op->rad = r;
   const int64_t L = op->L();
   op->ensure_batch(1);
-  Scratch& S = op->sc;
+  Scratch& S = op->W().sc;
   S.cin.ensure(L * sizeof(cplx<R>));
   S.fout.ensure(L * sizeof(R));
   std::vector<cplx<R>> delta(L);
@@ -1515,10 +1666,13 @@ TspmFile surrogate_to_tspm(const tomo_op* op) {
 
 template <typename R>
 double leak_probe(tomo_op* op, cudaStream_t st) {
-  if (op->leak >= 0.0) return op->leak;
+  {
+    std::lock_guard<std::mutex> lk(op->cache_mu);
+    if (op->leak >= 0.0) return op->leak;
+  }
   const int64_t L = op->L();
   op->ensure_batch(1);
-  Scratch& S = op->sc;
+  Scratch& S = op->W().sc;
   S.cin.ensure(L * sizeof(cplx<R>));
   S.cout.ensure(L * sizeof(cplx<R>));
   std::vector<cplx<R>> ones(L);
@@ -1532,8 +1686,10 @@ double leak_probe(tomo_op* op, cudaStream_t st) {
   SliceScalars h{};
   CK(cudaMemcpyAsync(&h, op->scal(), sizeof(SliceScalars), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  op->leak = h.leak_den > 0.0 ? std::sqrt(h.leak_num) / std::sqrt(h.leak_den) : 0.0;
-  return op->leak;
+  const double leak = h.leak_den > 0.0 ? std::sqrt(h.leak_num) / std::sqrt(h.leak_den) : 0.0;
+  std::lock_guard<std::mutex> lk(op->cache_mu);
+  op->leak = leak;
+  return leak;
 }
 
 // ---- host/device staging for the C ABI -----------------------------------------------------
@@ -1577,39 +1733,39 @@ bool host_pipeline(tomo_op* op, int batch, const void* in, size_t in_per, void* 
                    F&& compute) {
   if (batch < 2 || !in || !out || is_device_ptr(in) || is_device_ptr(out)) return false;
   const int chunk = std::max(1, std::min(std::max(1, op->desc.max_batch), (batch + 1) / 2));
-  if (!op->pipe_in) {
-    CK(cudaStreamCreateWithFlags(&op->pipe_in, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&op->pipe_out, cudaStreamNonBlocking));
+  if (!op->W().pipe_in) {
+    CK(cudaStreamCreateWithFlags(&op->W().pipe_in, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&op->W().pipe_out, cudaStreamNonBlocking));
     for (int k = 0; k < 2; ++k) {
-      CK(cudaEventCreateWithFlags(&op->ev_in[k], cudaEventDisableTiming));
-      CK(cudaEventCreateWithFlags(&op->ev_comp[k], cudaEventDisableTiming));
-      CK(cudaEventCreateWithFlags(&op->ev_out[k], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&op->W().ev_in[k], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&op->W().ev_comp[k], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&op->W().ev_out[k], cudaEventDisableTiming));
     }
   }
   for (int k = 0; k < 2; ++k) {
-    op->pin_buf[k].ensure(in_per * chunk);
-    op->pout_buf[k].ensure(out_per * chunk);
+    op->W().pin_buf[k].ensure(in_per * chunk);
+    op->W().pout_buf[k].ensure(out_per * chunk);
   }
-  CK(cudaEventRecord(op->ev_comp[0], st));  // staging free: nothing in flight yet
-  CK(cudaEventRecord(op->ev_comp[1], st));
-  CK(cudaEventRecord(op->ev_out[0], st));
-  CK(cudaEventRecord(op->ev_out[1], st));
+  CK(cudaEventRecord(op->W().ev_comp[0], st));  // staging free: nothing in flight yet
+  CK(cudaEventRecord(op->W().ev_comp[1], st));
+  CK(cudaEventRecord(op->W().ev_out[0], st));
+  CK(cudaEventRecord(op->W().ev_out[1], st));
   const auto* src = static_cast<const unsigned char*>(in);
   auto* dst = static_cast<unsigned char*>(out);
   for (int c0 = 0, c = 0; c0 < batch; c0 += chunk, ++c) {
     const int nb = std::min(chunk, batch - c0), k = c & 1;
-    CK(cudaStreamWaitEvent(op->pipe_in, op->ev_comp[k], 0));  // chunk c-2 no longer reads pin_buf[k]
-    CK(cudaMemcpyAsync(op->pin_buf[k].p, src + in_per * c0, in_per * nb, cudaMemcpyHostToDevice, op->pipe_in));
-    CK(cudaEventRecord(op->ev_in[k], op->pipe_in));
-    CK(cudaStreamWaitEvent(st, op->ev_in[k], 0));
-    CK(cudaStreamWaitEvent(st, op->ev_out[k], 0));  // chunk c-2 copied out of pout_buf[k]
-    compute(nb, op->pin_buf[k].p, op->pout_buf[k].p);
-    CK(cudaEventRecord(op->ev_comp[k], st));
-    CK(cudaStreamWaitEvent(op->pipe_out, op->ev_comp[k], 0));
-    CK(cudaMemcpyAsync(dst + out_per * c0, op->pout_buf[k].p, out_per * nb, cudaMemcpyDeviceToHost, op->pipe_out));
-    CK(cudaEventRecord(op->ev_out[k], op->pipe_out));
+    CK(cudaStreamWaitEvent(op->W().pipe_in, op->W().ev_comp[k], 0));  // chunk c-2 no longer reads pin_buf[k]
+    CK(cudaMemcpyAsync(op->W().pin_buf[k].p, src + in_per * c0, in_per * nb, cudaMemcpyHostToDevice, op->W().pipe_in));
+    CK(cudaEventRecord(op->W().ev_in[k], op->W().pipe_in));
+    CK(cudaStreamWaitEvent(st, op->W().ev_in[k], 0));
+    CK(cudaStreamWaitEvent(st, op->W().ev_out[k], 0));  // chunk c-2 copied out of pout_buf[k]
+    compute(nb, op->W().pin_buf[k].p, op->W().pout_buf[k].p);
+    CK(cudaEventRecord(op->W().ev_comp[k], st));
+    CK(cudaStreamWaitEvent(op->W().pipe_out, op->W().ev_comp[k], 0));
+    CK(cudaMemcpyAsync(dst + out_per * c0, op->W().pout_buf[k].p, out_per * nb, cudaMemcpyDeviceToHost, op->W().pipe_out));
+    CK(cudaEventRecord(op->W().ev_out[k], op->W().pipe_out));
   }
-  CK(cudaStreamSynchronize(op->pipe_out));
+  CK(cudaStreamSynchronize(op->W().pipe_out));
   CK(cudaStreamSynchronize(st));
   return true;
 }
@@ -1678,6 +1834,7 @@ tomo_op* create_op(const tomo_geom_desc* geom, const tomo_op_desc* desc, const T
   op->src = src;
   DeviceGuard dg(op->device);
   tomo_op* o = op.get();
+  Lease lease(o, nullptr);  // the build's scratch (stencil response, batch sizing)
   with_prec(o, [&](auto tag) {
     using R = decltype(tag);
     build_tables<R>(o);
@@ -1796,6 +1953,7 @@ int tomo_apply_normal(tomo_op* op, const void* in, void* out, int batch, void* s
   check_op(op, batch);
   DeviceGuard dg(op->device);
   const cudaStream_t st = S_(stream);
+  Lease lease(op, st);
   with_prec(op, [&](auto tag) {
     using R = decltype(tag);
     if (!op->surrogate() &&
@@ -1803,13 +1961,13 @@ int tomo_apply_normal(tomo_op* op, const void* in, void* out, int batch, void* s
                       [&](int nb, const void* din, void* dout) { normal_direct<R>(op, nb, din, true, dout, st); }))
       return;
     const size_t cnt = static_cast<size_t>(batch) * op->L();
-    const void* din = stage_in(in, cnt * sizeof(cplx<R>), op->sc.cin, st);
-    OutArg o(out, cnt * sizeof(cplx<R>), op->sc.cout);
+    const void* din = stage_in(in, cnt * sizeof(cplx<R>), op->W().sc.cin, st);
+    OutArg o(out, cnt * sizeof(cplx<R>), op->W().sc.cout);
     if (op->surrogate()) {
       // T acts on real and imaginary parts independently (sparse.cpp:27-42)
-      op->sc.fin.ensure(cnt * 2 * sizeof(R));
-      op->sc.fout.ensure(cnt * 2 * sizeof(R));
-      R* re = op->sc.fin.as<R>();
+      op->W().sc.fin.ensure(cnt * 2 * sizeof(R));
+      op->W().sc.fout.ensure(cnt * 2 * sizeof(R));
+      R* re = op->W().sc.fin.as<R>();
       R* im = re + cnt;
       CK(cudaMemcpy2DAsync(re, sizeof(R), din, 2 * sizeof(R), sizeof(R), cnt, cudaMemcpyDeviceToDevice, st));
       CK(cudaMemcpy2DAsync(im, sizeof(R), static_cast<const R*>(din) + 1, 2 * sizeof(R), sizeof(R), cnt,
@@ -1817,10 +1975,10 @@ int tomo_apply_normal(tomo_op* op, const void* in, void* out, int batch, void* s
       const SysParams sp = sysp(1.0, 0.0, 0.0, 0.0);
       for (int part = 0; part < 2; ++part)
         launch_stencil<R>(op->g.n, batch, op->rad, op->coef, 2, re + part * cnt, nullptr, nullptr,
-                          op->sc.fout.as<R>() + part * cnt, nullptr, nullptr, sp, 0, op->red(), st);
-      CK(cudaMemcpy2DAsync(o.dev, 2 * sizeof(R), op->sc.fout.p, sizeof(R), sizeof(R), cnt, cudaMemcpyDeviceToDevice,
+                          op->W().sc.fout.as<R>() + part * cnt, nullptr, nullptr, sp, 0, op->red(), st);
+      CK(cudaMemcpy2DAsync(o.dev, 2 * sizeof(R), op->W().sc.fout.p, sizeof(R), sizeof(R), cnt, cudaMemcpyDeviceToDevice,
                            st));
-      CK(cudaMemcpy2DAsync(static_cast<R*>(o.dev) + 1, 2 * sizeof(R), op->sc.fout.as<R>() + cnt, sizeof(R), sizeof(R),
+      CK(cudaMemcpy2DAsync(static_cast<R*>(o.dev) + 1, 2 * sizeof(R), op->W().sc.fout.as<R>() + cnt, sizeof(R), sizeof(R),
                            cnt, cudaMemcpyDeviceToDevice, st));
     } else {
       const size_t L = op->L();
@@ -1839,6 +1997,7 @@ int tomo_apply_normal_real(tomo_op* op, const void* in, void* out, int batch, vo
   check_op(op, batch);
   DeviceGuard dg(op->device);
   const cudaStream_t st = S_(stream);
+  Lease lease(op, st);
   with_prec(op, [&](auto tag) {
     using R = decltype(tag);
     if (!op->surrogate() &&
@@ -1846,8 +2005,8 @@ int tomo_apply_normal_real(tomo_op* op, const void* in, void* out, int batch, vo
                       [&](int nb, const void* din, void* dout) { normal_direct<R>(op, nb, din, false, dout, st); }))
       return;
     const size_t cnt = static_cast<size_t>(batch) * op->L();
-    const void* din = stage_in(in, cnt * sizeof(R), op->sc.fin, st);
-    OutArg o(out, cnt * sizeof(R), op->sc.fout);
+    const void* din = stage_in(in, cnt * sizeof(R), op->W().sc.fin, st);
+    OutArg o(out, cnt * sizeof(R), op->W().sc.fout);
     if (op->surrogate()) {
       launch_stencil<R>(op->g.n, batch, op->rad, op->coef, 2, static_cast<const R*>(din), nullptr, nullptr,
                         static_cast<R*>(o.dev), nullptr, nullptr, sysp(1.0, 0.0, 0.0, 0.0), 0, op->red(), st);
@@ -1867,6 +2026,7 @@ int tomo_forward(tomo_op* op, const void* image, void* samples, int batch, void*
   check_op(op, batch);
   DeviceGuard dg(op->device);
   const cudaStream_t st = S_(stream);
+  Lease lease(op, st);
   with_prec(op, [&](auto tag) {
     using R = decltype(tag);
     const size_t cnt = static_cast<size_t>(batch) * op->L();
@@ -1877,8 +2037,8 @@ int tomo_forward(tomo_op* op, const void* image, void* samples, int batch, void*
                         type2<R>(op, nb, din, true, pu, static_cast<cplx<R>*>(dout), nullptr, st);
                       }))
       return;
-    const void* din = stage_in(image, cnt * sizeof(cplx<R>), op->sc.cin, st);
-    OutArg o(samples, scnt * sizeof(cplx<R>), op->sc.cout);
+    const void* din = stage_in(image, cnt * sizeof(cplx<R>), op->W().sc.cin, st);
+    OutArg o(samples, scnt * sizeof(cplx<R>), op->W().sc.cout);
     type2<R>(op, batch, din, true, pu, static_cast<cplx<R>*>(o.dev), nullptr, st);
     o.finish(st);
   });
@@ -1890,6 +2050,7 @@ int tomo_adjoint(tomo_op* op, const void* samples, void* image, int batch, void*
   check_op(op, batch);
   DeviceGuard dg(op->device);
   const cudaStream_t st = S_(stream);
+  Lease lease(op, st);
   with_prec(op, [&](auto tag) {
     using R = decltype(tag);
     const size_t cnt = static_cast<size_t>(batch) * op->L();
@@ -1903,8 +2064,8 @@ int tomo_adjoint(tomo_op* op, const void* samples, void* image, int batch, void*
     };
     if (host_pipeline(op, batch, samples, op->g.P * sizeof(cplx<R>), image, op->L() * sizeof(cplx<R>), st, adj))
       return;
-    const void* din = stage_in(samples, scnt * sizeof(cplx<R>), op->sc.cin, st);
-    OutArg o(image, cnt * sizeof(cplx<R>), op->sc.cout);
+    const void* din = stage_in(samples, scnt * sizeof(cplx<R>), op->W().sc.cin, st);
+    OutArg o(image, cnt * sizeof(cplx<R>), op->W().sc.cout);
     adj(batch, din, o.dev);
     o.finish(st);
   });
@@ -1916,12 +2077,13 @@ int tomo_spmv_w(tomo_op* op, const void* grid, void* samples, int batch, void* s
   check_op(op, batch);
   DeviceGuard dg(op->device);
   const cudaStream_t st = S_(stream);
+  Lease lease(op, st);
   with_prec(op, [&](auto tag) {
     using R = decltype(tag);
     const size_t gcnt = static_cast<size_t>(batch) * op->g.m * op->g.m;
     const size_t scnt = static_cast<size_t>(batch) * op->g.P;
-    const void* din = stage_in(grid, gcnt * sizeof(cplx<R>), op->sc.cin, st);
-    OutArg o(samples, scnt * sizeof(cplx<R>), op->sc.cout);
+    const void* din = stage_in(grid, gcnt * sizeof(cplx<R>), op->W().sc.cin, st);
+    OutArg o(samples, scnt * sizeof(cplx<R>), op->W().sc.cout);
     OpDev<R> d = op->dev<R>(batch);
     d.w_out_pos = 0;  // reference sample order at the API
     launch_w<R>(d, batch, static_cast<const cplx<R>*>(din), static_cast<cplx<R>*>(o.dev), nullptr, st);
@@ -1935,12 +2097,13 @@ int tomo_spmv_wt(tomo_op* op, const void* samples, void* grid, int batch, void* 
   check_op(op, batch);
   DeviceGuard dg(op->device);
   const cudaStream_t st = S_(stream);
+  Lease lease(op, st);
   with_prec(op, [&](auto tag) {
     using R = decltype(tag);
     const size_t gcnt = static_cast<size_t>(batch) * op->g.m * op->g.m;
     const size_t scnt = static_cast<size_t>(batch) * op->g.P;
-    const void* din = stage_in(samples, scnt * sizeof(cplx<R>), op->sc.cin, st);
-    OutArg o(grid, gcnt * sizeof(cplx<R>), op->sc.cout);
+    const void* din = stage_in(samples, scnt * sizeof(cplx<R>), op->W().sc.cin, st);
+    OutArg o(grid, gcnt * sizeof(cplx<R>), op->W().sc.cout);
     OpDev<R> d = op->dev<R>(batch);
     launch_wt_grid<R>(d, batch, samples_in<R>(op, batch, static_cast<const cplx<R>*>(din), st),
                       static_cast<cplx<R>*>(o.dev), st);
@@ -1955,12 +2118,13 @@ int tomo_backproject(tomo_op* op, double alpha, int weighted, const void* slice_
   check_op(op, batch);
   DeviceGuard dg(op->device);
   const cudaStream_t st = S_(stream);
+  Lease lease(op, st);
   with_prec(op, [&](auto tag) {
     using R = decltype(tag);
     const size_t cnt = static_cast<size_t>(batch) * op->L();
     const size_t scnt = static_cast<size_t>(batch) * op->g.P;
-    const void* din = stage_in(slice_data, scnt * sizeof(cplx<R>), op->sc.cin, st);
-    OutArg o(out, cnt * sizeof(R), op->sc.fout);
+    const void* din = stage_in(slice_data, scnt * sizeof(cplx<R>), op->W().sc.cin, st);
+    OutArg o(out, cnt * sizeof(R), op->W().sc.fout);
     backproject<R>(op, batch, alpha, weighted != 0, static_cast<const cplx<R>*>(din), static_cast<R*>(o.dev), st);
     o.finish(st);
   });
@@ -1974,12 +2138,13 @@ int tomo_cg(tomo_op* op, const tomo_system* sys, const void* rhs, const void* x0
   if (!sys) throw ConfigError("null system");
   if (steps < 1) throw ConfigError("cg_solve: steps must be >= 1");
   DeviceGuard dg(op->device);
-  op->ensure_batch(batch);
   const cudaStream_t st = S_(stream);
+  Lease lease(op, st);
+  op->ensure_batch(batch);
   with_prec(op, [&](auto tag) {
     using R = decltype(tag);
     const size_t cnt = static_cast<size_t>(batch) * op->L();
-    Scratch& S = op->sc;
+    Scratch& S = op->W().sc;
     const R* drhs = static_cast<const R*>(stage_in(rhs, cnt * sizeof(R), S.fin, st));
     const R* dx0 = x0 ? static_cast<const R*>(stage_in(x0, cnt * sizeof(R), S.mu1, st)) : S.zero.as<R>();
     OutArg o(x, cnt * sizeof(R), S.fout);
@@ -2021,13 +2186,14 @@ void sb_impl(tomo_op* op, const tomo_sb_config* cfg, const void* slice_data, voi
   if (cfg->update_tol_rel < 0.0) throw ConfigError("SolverConfig: update_tol_rel >= 0");
   if (cfg->max_iters > kMaxLoggedIters) throw ConfigError("split_bregman_tv: max_bregman_iters > 8192 not supported");
   DeviceGuard dg(op->device);
+  Lease lease(op, st);
   op->ensure_batch(batch);
   with_prec(op, [&](auto tag) {
     using R = decltype(tag);
     const int n = op->g.n;
     const size_t cnt = static_cast<size_t>(batch) * op->L();
     const size_t scnt = static_cast<size_t>(batch) * op->g.P;
-    Scratch& S = op->sc;
+    Scratch& S = op->W().sc;
     const bool sur = op->surrogate();
     // make_subproblem (solver.cpp:164-215): sigma, then the leak probe (:236-247)
     const bool feedback = cfg->data_feedback != 0;
@@ -2042,8 +2208,13 @@ void sb_impl(tomo_op* op, const tomo_sb_config* cfg, const void* slice_data, voi
     }
     const auto* din = static_cast<const cplx<R>*>(stage_in(slice_data, scnt * sizeof(cplx<R>), S.cin, st));
     if (feedback) {  // fk = f (solver.cpp:252), both kept in the op's internal sample order
-      S.fk.ensure(scnt * sizeof(cplx<R>));
-      S.fint.ensure(scnt * sizeof(cplx<R>));
+      // sized for the op's batch capacity once, so graphs captured earlier never see them move
+      const size_t fcap = static_cast<size_t>(S.cap) * op->g.P * sizeof(cplx<R>);
+      if (S.fk.bytes < fcap || S.fint.bytes < fcap) {
+        S.fk.ensure(fcap);
+        S.fint.ensure(fcap);
+        op->clear_graphs();
+      }
       const cplx<R>* fi = samples_in<R>(op, batch, din, st);
       CK(cudaMemcpyAsync(S.fint.p, fi, scnt * sizeof(cplx<R>), cudaMemcpyDeviceToDevice, st));
       CK(cudaMemcpyAsync(S.fk.p, fi, scnt * sizeof(cplx<R>), cudaMemcpyDeviceToDevice, st));
@@ -2091,9 +2262,15 @@ void sb_impl(tomo_op* op, const tomo_sb_config* cfg, const void* slice_data, voi
         if (iters & 1) CK(cudaMemcpyAsync(S.mu0.p, S.mu1.p, sizeof(R) * cnt, cudaMemcpyDeviceToDevice, cs));
       });
     } else {
+      // the captured update graph only ever sees scratch owned by the op, sized by ensure_batch:
+      // the reference is copied into S.u2 (never the caller's pointer) and rel_log holds
+      // kMaxLoggedIters entries per slice, so replays after a longer solve stay in bounds
       const R* dref = nullptr;
-      if (reference) dref = static_cast<const R*>(stage_in(reference, cnt * sizeof(R), S.u2, st));
-      S.rel_log.ensure(sizeof(double) * static_cast<size_t>(batch) * iters);
+      if (reference) {
+        CK(cudaMemcpyAsync(S.u2.p, reference, cnt * sizeof(R),
+                           is_device_ptr(reference) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+        dref = S.u2.as<R>();
+      }
       ev.resize(3 * static_cast<size_t>(iters) + 1);
       for (auto& e : ev) CK(cudaEventCreate(&e));
       CK(cudaEventRecord(ev[0], st));
@@ -2189,13 +2366,14 @@ int tomo_tikhonov(tomo_op* op, double alpha, const void* slice_data, void* mu, i
   if (steps < 1) throw ConfigError("cg_solve: steps must be >= 1");
   if (op->surrogate()) throw ConfigError("tomo_tikhonov: direct backend only");
   DeviceGuard dg(op->device);
-  op->ensure_batch(batch);
   const cudaStream_t st = S_(stream);
+  Lease lease(op, st);
+  op->ensure_batch(batch);
   with_prec(op, [&](auto tag) {
     using R = decltype(tag);
     const size_t cnt = static_cast<size_t>(batch) * op->L();
     const size_t scnt = static_cast<size_t>(batch) * op->g.P;
-    Scratch& S = op->sc;
+    Scratch& S = op->W().sc;
     const auto* din = static_cast<const cplx<R>*>(stage_in(slice_data, scnt * sizeof(cplx<R>), S.cin, st));
     backproject<R>(op, batch, alpha, false, din, S.fid.as<R>(), st);
     CK(cudaMemsetAsync(S.sc.p, 0, sizeof(SliceScalars) * batch, st));
@@ -2221,14 +2399,15 @@ int tomo_chambolle_pock(tomo_op* op, const tomo_cp_config* cfg, const void* slic
   if (!cfg || cfg->iters < 1 || cfg->cg_steps < 1) throw ConfigError("chambolle_pock: bad config");
   if (op->surrogate()) throw ConfigError("chambolle_pock: direct backend only");
   DeviceGuard dg(op->device);
-  op->ensure_batch(batch);
   const cudaStream_t st = S_(stream);
+  Lease lease(op, st);
+  op->ensure_batch(batch);
   with_prec(op, [&](auto tag) {
     using R = decltype(tag);
     const int n = op->g.n;
     const size_t cnt = static_cast<size_t>(batch) * op->L();
     const size_t scnt = static_cast<size_t>(batch) * op->g.P;
-    Scratch& S = op->sc;
+    Scratch& S = op->W().sc;
     const auto* din = static_cast<const cplx<R>*>(stage_in(slice_data, scnt * sizeof(cplx<R>), S.cin, st));
     backproject<R>(op, batch, cfg->alpha, false, din, S.fid.as<R>(), st);
     for (auto* b : {&S.mu0, &S.mu1, &S.bx0, &S.by0}) CK(cudaMemsetAsync(b->p, 0, sizeof(R) * cnt, st));
@@ -2279,7 +2458,7 @@ int tomo_op_set_allreduce(tomo_op* op, tomo_allreduce_fn fn, void* user) {
   if (!op) throw ConfigError("null op");
   op->ar_fn = fn;
   op->ar_user = user;
-  op->clear_graphs();
+  op->clear_all_graphs();
   TOMO_CATCH
 }
 
@@ -2304,7 +2483,7 @@ int tomo_op_attach_nccl(tomo_op* op, const char id[128], int nranks, int rank) {
   if (r != ncclSuccess) throw CudaError(std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
   if (op->comm) ncclCommDestroy(op->comm);
   op->comm = comm;
-  op->clear_graphs();
+  op->clear_all_graphs();
   TOMO_CATCH
 }
 
@@ -2444,13 +2623,14 @@ int tomo_profile_stages(tomo_op* op, int batch, int reps, double* ms, double* by
   check_op(op, batch);
   if (!ms || !bytes || reps < 1) throw ConfigError("profile: bad arguments");
   DeviceGuard dg(op->device);
-  op->ensure_batch(batch);
   const cudaStream_t st = S_(stream);
+  Lease lease(op, st);
+  op->ensure_batch(batch);
   with_prec(op, [&](auto tag) {
     using R = decltype(tag);
     const int n = op->g.n, m = op->g.m;
     const size_t cnt = static_cast<size_t>(batch) * op->L();
-    Scratch& S = op->sc;
+    Scratch& S = op->W().sc;
     // random-ish state so every kernel does its full work
     std::vector<R> h(cnt);
     std::mt19937 rng(5);
@@ -2557,21 +2737,22 @@ int tomo_profile_stages(tomo_op* op, int batch, int reps, double* ms, double* by
     cudaEventDestroy(e1);
     const double B = batch, nn = static_cast<double>(n) * n, mn = static_cast<double>(m) * n,
                  mm = static_cast<double>(m) * m, P = static_cast<double>(op->g.P), rs = sizeof(R), cs = 2 * sizeof(R);
-    const double wbytes = op->w_sep ? static_cast<double>(op->g.P) * (4.0 + 2.0 * op->g.w * rs)
-                                    : static_cast<double>(op->Ppad) * op->nq * 32.0 * (16.0 + 4.0 * rs) / 32.0;
-    const double wtbytes = static_cast<double>(op->wt_slots) * sizeof(WtEnt<R>) + op->n_tasks * 16.0 +
-                           static_cast<double>(op->wt_rows) * 2.0;
     double by[TOMO_NUM_STAGES] = {0};
     if (!sur) {
       by[0] = cgcg_on() && !op->sharded()
                   ? B * (9 * rs * nn + cs * mn)            // C-G: read r, w, x, p, s; write p, s, x, r; write H
                   : B * (3 * rs * nn + cs * mn);           // read p, r; write p; write H
       by[1] = B * (cs * mn + cs * mm);                     // read H, write g
-      by[2] = op->fused()  // Gram stream, read + write touched nodes | W stream, touched nodes, samples
+      // SURVEY.md §8(d) algorithmic bytes (payload only, no implementation padding):
+      //   W:   (4 + r) nnz + c T + c P         (ELL entries, gather of the T touched nodes, samples)
+      //   W^T: (4 + r) nnz + 8 (T + 1) + c P + c G  (entries, row pointers + ids, samples, grid)
+      // the matrix stream is read once per launch, the vectors once per slice
+      const double nnzb = static_cast<double>(op->nnz) * (4.0 + rs);
+      by[2] = op->fused()  // Gram stream, read + write touched nodes
                   ? static_cast<double>(op->gram.bytes) + B * (2 * cs * op->wt_rows)
-                  : wbytes + B * (cs * op->wt_rows + cs * P);
-      by[3] = wt_fused ? wtbytes + B * (cs * P + cs * mn)  // W^T stream, samples, write K (grid stays on chip)
-                       : wtbytes + B * (cs * P + cs * op->wt_rows);  // W^T stream, samples, write touched nodes
+                  : nnzb + B * (cs * op->wt_rows + cs * P);
+      by[3] = wt_fused ? nnzb + 8.0 * (op->wt_rows + 1) + B * (cs * P + cs * mn)  // grid stays on chip: K
+                       : nnzb + 8.0 * (op->wt_rows + 1) + B * (cs * P + cs * mm);
       by[4] = B * (cs * mm + cs * mn);                     // read spread grid, write K
       by[5] = B * (cs * mn + 2 * rs * nn);                 // read K, p; write Ap
     } else {
