@@ -370,7 +370,7 @@ class Workload:
             counts = {"t2_rows": a, "t2_cols": a, "w_spmv": a, "wt_spread": a, "t1_cols": a, "wt_t1": a, "t1_rows": a,
                       # Chronopoulos-Gear CG (default): one update kernel per CG call, the others
                       # are fused into the next step's first FFT pass (TOMO_CG=std: one per step)
-                      "cg_update": iters * steps if os.environ.get("TOMO_CG") == "std" else iters,
+                      "cg_update": iters * steps if (os.environ.get("TOMO_AB") == "1" and os.environ.get("TOMO_CG") == "std") else iters,
                       "sb_post": iters}
         elif k == "apply":
             counts = {"t2_rows": 1, "t2_cols": 1, "w_spmv": 1, "wt_spread": 1, "t1_cols": 1, "wt_t1": 1, "t1_rows": 1}
@@ -703,6 +703,15 @@ def main():
 
     top, roof = wl.roofline(peak)
     roof["peak_source"] = peak_src
+    if "apply" in roof:
+        # the same bytes per apply over the whole timed step (all kernels, launch gaps, lanes)
+        k = c["kind"]
+        applies = {"sb": c.get("iters", 1) * (c.get("cg", 0) + 1) * wl.units_per_step,
+                   "cp": wl.units_per_step, "c1": wl.units_per_step, "apply": wl.units_per_step}[k]
+        per_apply = apply_bytes(c, wl.op.info.wt_rows, complex_io=(k == "apply"), B=1)
+        gbs = per_apply * applies * args.steps / (t_max * 1e-3) / 1e9
+        roof["apply"]["in_step"] = {"applies_per_step": applies, "bytes_per_apply": int(per_apply),
+                                    "achieved": round(gbs, 1), "frac": round(gbs / peak, 4)}
     traffic_file = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(traffic_file):
         try:

@@ -415,6 +415,12 @@ def synthesize(geom, phantom, noise_frac=0.0, seed=0):
     return out, sig.value
 
 
+def set_perturbation(eps=0.0, seed=1):
+    """Sensitivity probe: every real normal-operator input and output * (1 + eps N(0,1)); 0 = off."""
+    lib().orc_set_perturbation.argtypes = [C.c_double, C.c_uint64]
+    lib().orc_set_perturbation(float(eps), int(seed))
+
+
 def rel_l1(cand, ref_):
     a = _f64(cand).reshape(-1)
     b = _f64(ref_).reshape(-1)

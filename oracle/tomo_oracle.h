@@ -42,6 +42,13 @@ typedef struct {
 
 const char* orc_last_error(void);
 
+/* Sensitivity probe (tests only; 0 = off, the default): multiply every real normal-operator
+ * input and output by (1 + eps * N(0,1)) elementwise, seeded. */
+void orc_set_perturbation(double eps, uint64_t seed);
+/* Inner-product summation of the CG / Lanczos recurrences: 1 = compensated (default), 0 = plain
+ * sequential (probe). */
+void orc_set_dot_mode(int mode);
+
 /* ---- geometry / plan (fourier_slice.cpp:10-41, nufft.cpp:43-101) ---- */
 int64_t orc_num_points(const orc_geom* g);
 int orc_points(const orc_geom* g, double* coords /* P x 2 */);

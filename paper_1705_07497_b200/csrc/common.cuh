@@ -5,11 +5,28 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+#include <string>
 #include <utility>
 
 #define TOMO_DEV __device__ __forceinline__
 
 namespace tomo_b200 {
+
+// A/B override knobs (TOMO_ROW_RB, TOMO_COL_RB, TOMO_WT_MAXCH, TOMO_WT_GRP, TOMO_WT_PIPE,
+// TOMO_BATCH_Y, TOMO_TASK_ORDER, TOMO_CG, TOMO_BUILD) for measurement runs: honoured only when
+// TOMO_AB=1, so a production process cannot change kernel selection by accident. Host only.
+inline std::string ab_knob(const char* name) {
+  const char* ab = std::getenv("TOMO_AB");
+  if (!(ab && std::atoi(ab) != 0)) return std::string();
+  const char* v = std::getenv(name);
+  return v ? std::string(v) : std::string();
+}
+inline int ab_int(const char* name, int dflt) {
+  const std::string v = ab_knob(name);
+  return v.empty() ? dflt : std::atoi(v.c_str());
+}
+
 
 template <typename R>
 struct CplxT;

@@ -47,23 +47,16 @@ struct TaskSpmv {
 };
 
 // Four W values of one SELL-32 slot quad (16 B fp32 / 32 B fp64).
-template <typename R>
-struct alignas(4 * sizeof(R)) Quad {
-  R v[4];
-};
-
 // Operator tables + scratch for one device-resident normal operator (see DESIGN.md
 // "HBM layout"). Grid nodes are stored transposed relative to the reference:
 // node = iy*m + ix, where the reference has grid[ix*m + iy] (proj/src/nufft.cpp:185-200).
 template <typename R>
 struct OpDev {
-  int n, m, nb, P, Ppad, nq;      // nq = padded window entries / 4
+  int n, m, nb, P, Ppad;
   int G32;                         // number of 32-node SELL blocks of W^T (= m*m/32)
   const R* apod;                   // n   : a[t]/m  (deconvolve, nufft.cpp:204-227, with 1/m per axis)
   const cplx<R>* tw;               // m   : e^{-2 pi i k/m}
-  const int4* w_cols;              // SELL-32 ELL of W: [(Ppad/32) * nq * 32] int4
-  const Quad<R>* w_vals;           //                   [(Ppad/32) * nq * 32]
-  // Separable ("rank-1 block") storage of the same W: row j's w x w block is
+  // Separable ("rank-1 block") storage of W: row j's w x w block is
   // wx_j[a] * wy_j[b] at nodes ((iy0+b) mod m, (ix0+a) mod m) (nufft.cpp:185-200).
   const int* w_base;               // [Ppad] ix0 | iy0 << 16
   const R* w_x;                    // [w][Ppad]
@@ -75,7 +68,6 @@ struct OpDev {
                                    // order only at the API boundary (forward/adjoint).
   int w_out_pos;                   // W writes sample t at position t (1) or at w_perm[t] (0)
   int w;                           // window width
-  int w_sep;                       // 1: use the separable storage for W, 0: the SELL-32 ELL
   // W^T: nodes of each grid row sorted by entry count (SELL-32-sigma, sigma = one grid row);
   // the 32-node blocks are processed as a balanced list of warp tasks of <= kWtMaxChunks
   // chunks; blocks longer than that are split and their partial sums combined by a fix-up.
@@ -89,12 +81,6 @@ struct OpDev {
   int n_heavy;
   int n_slots;
   cplx<R>* wt_part;                // B x n_slots x 32 partial sums of split blocks
-  // the same tasks grouped by grid row for the fused W^T + PA kernel (k_wt_t1): tasks of row
-  // iy at [wt_roff[iy], wt_roff[iy+1]), heavy blocks of row iy at [wt_hoff[iy], wt_hoff[iy+1])
-  const int4* wt_rtasks;           // nullptr: not built (the fused kernel is not used)
-  const int4* wt_rheavy;           // heavy blocks in block order
-  const int* wt_roff;              // [m+1]
-  const int* wt_hoff;              // [m+1]
   cplx<R>* Gt;                     // B x m x m  spread grid [iy][ix]; untouched nodes stay 0
   cplx<R>* H;                      // B x m x n  (type-2 row pass output, [iy][t1])
   cplx<R>* g;                      // B x m x m  (oversampled spatial grid, [iy][ix])
@@ -202,11 +188,6 @@ void launch_wt_rows(const OpDev<R>& d, int B, const SliceScalars* skip, cudaStre
 template <typename R>
 void launch_wt_spread(const OpDev<R>& d, int B, const cplx<R>* samples, cplx<R>* grid, const SliceScalars* skip,
                       cudaStream_t st);
-// W^T + PA fused (k_wt_t1, m < 4096, needs the row-grouped task tables); false = not taken.
-template <typename R>
-bool wt_t1_enabled(const OpDev<R>& d);
-template <typename R>
-bool launch_wt_t1(const OpDev<R>& d, int B, const SliceScalars* skip, cudaStream_t st);
 template <typename R>
 void launch_t1_cols_only(const OpDev<R>& d, int B, const SliceScalars* skip, cudaStream_t st);
 // Fused (Gram) backend: grid_out = (W^T W) grid_in on the oversampled grid.

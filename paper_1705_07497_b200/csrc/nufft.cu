@@ -1,7 +1,7 @@
 // nufft.cu — the normal-operator hot path on sm_100a:
 //
 //   type-2 (F_NU^*, proj/src/nufft.cpp:261-286):  P1 deapod+pad+row iFFT  ->  P2 column iFFT
-//                                                  -> W  (SELL-32 ELL SpMV, interpolate :160-202)
+//                                                  -> W  (separable window SpMV, interpolate :160-202)
 //   type-1 (F_NU,   proj/src/nufft.cpp:236-259):  W^T (SpMV over the precomputed, count-sorted
 //                                                  transpose, spread :119-158) -> PA grid-row
 //                                                  FFT -> PB image-row FFT + crop + deapod
@@ -61,17 +61,6 @@ __device__ __forceinline__ bool cg_step_live(const Reduce& red, int b, int step,
 template <typename T>
 __device__ __forceinline__ T ldg(const T* p) {
   return __ldg(p);
-}
-template <>
-__device__ __forceinline__ Quad<float> ldg(const Quad<float>* p) {
-  const float4 v = __ldg(reinterpret_cast<const float4*>(p));
-  return Quad<float>{{v.x, v.y, v.z, v.w}};
-}
-template <>
-__device__ __forceinline__ Quad<double> ldg(const Quad<double>* p) {
-  const double2 a = __ldg(reinterpret_cast<const double2*>(p));
-  const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
-  return Quad<double>{{a.x, a.y, b.x, b.y}};
 }
 template <>
 __device__ __forceinline__ WtEnt<float> ldg(const WtEnt<float>* p) {
@@ -211,59 +200,6 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F3
   };
   auto store = [&](int k, C2 v) { g[k] = cconj(v); };
   fft_row<M, RB, false, C2, HALF ? 1 : 0>(row, d.tw, t, active, load, store);
-}
-
-// ---------------------------------------------------------------- W: SELL-32 ELL SpMV
-// One thread per slice sample (row of W); entries streamed as int4 column / value quads,
-// coalesced across the warp (lane = row within the 32-row slice), four quads prefetched per
-// step so 16 grid gathers are in flight. The batch of slices shares the matrix stream.
-template <int BT, typename R>
-__global__ void __launch_bounds__(256) k_w(OpDev<R> d, int B, const cplx<R>* __restrict__ grid,
-                                            cplx<R>* __restrict__ out, const SliceScalars* skip) {
-  using C2 = cplx<R>;
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= d.Ppad) return;
-  const int blk = j >> 5, lane = j & 31;
-  const size_t G = static_cast<size_t>(d.m) * d.m;
-  const int4* cp = d.w_cols + static_cast<size_t>(blk) * d.nq * 32 + lane;
-  const Quad<R>* vp = d.w_vals + static_cast<size_t>(blk) * d.nq * 32 + lane;
-  for (int b0 = 0; b0 < B; b0 += BT) {
-    C2 acc[BT];
-#pragma unroll
-    for (int q = 0; q < BT; ++q) acc[q] = czero<C2>();
-    for (int q0 = 0; q0 < d.nq; q0 += 4) {
-      int4 c[4];
-      Quad<R> v[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (q0 + u < d.nq) {
-          c[u] = __ldg(cp + (q0 + u) * 32);
-          v[u] = ldg(vp + (q0 + u) * 32);
-        } else {
-          c[u] = make_int4(0, 0, 0, 0);
-          v[u] = Quad<R>{{R(0), R(0), R(0), R(0)}};
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < BT; ++q) {
-        if (b0 + q < B) {
-          const C2* gb = grid + G * (b0 + q);
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const C2 g0 = gb[c[u].x], g1 = gb[c[u].y], g2 = gb[c[u].z], g3 = gb[c[u].w];
-            acc[q].x += v[u].v[0] * g0.x + v[u].v[1] * g1.x + v[u].v[2] * g2.x + v[u].v[3] * g3.x;
-            acc[q].y += v[u].v[0] * g0.y + v[u].v[1] * g1.y + v[u].v[2] * g2.y + v[u].v[3] * g3.y;
-          }
-        }
-      }
-    }
-    if (j < d.P) {
-#pragma unroll
-      for (int q = 0; q < BT; ++q)
-        if (b0 + q < B && !(skip && (skip[b0 + q].done || skip[b0 + q].frozen)))
-          out[static_cast<size_t>(b0 + q) * d.P + j] = acc[q];
-    }
-  }
 }
 
 // ---------------------------------------------------------------- W, separable storage
@@ -507,95 +443,6 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F3
     if (t1 < n) row[pad16(t1)] = v;
   };
   fft_row<M, RB, true, C2, HALF ? 2 : 0>(row, d.tw, t, active, load, store);
-  C2* K = d.K + static_cast<size_t>(b) * n * M;
-  store_transposed<S::STRIDE>(sm, rpc, rpc, n, K + iy0, static_cast<size_t>(M));
-}
-
-// W^T + PA in one kernel (grids up to m = 2048): the CTA that transforms spread-grid rows
-// iy0..iy0+rpc-1 first computes them, straight into its smem rows, from the row's W^T tasks
-// (same warp-task arithmetic and summation order as k_task_spmv, so the node values are
-// bit-identical), then runs PA's pruned forward FFT and transposed K store. The spread grid Gt
-// never goes to HBM/L2: the separate path writes and re-reads m^2 complex values per apply.
-// Split blocks publish their partials to global memory; after a barrier the CTA sums each
-// heavy block's partials in slot order (as the ticketed fix-up does) into smem.
-template <int M, int RB, typename R, bool HALF, int GRP>
-__global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F32 : TOMO_FFT_MINB_F64)
-k_wt_t1(OpDev<R> d, int rpc, const SliceScalars* skip) {
-  using S = FftShape<M, RB>;
-  using C2 = cplx<R>;
-  extern __shared__ __align__(16) unsigned char smraw[];
-  C2* sm = reinterpret_cast<C2*>(smraw);
-  const int b = blockIdx.y;
-  if (skip && (skip[b].done || skip[b].frozen)) return;
-  const int n = d.n;
-  // CTA order 0, last, 1, last-1, ...: the heavy rows around the DC row (both ends of the
-  // wrapped grid) start in the first wave
-  const int nb = gridDim.x, bx = blockIdx.x;
-  const int iy0 = ((bx & 1) ? nb - 1 - (bx >> 1) : (bx >> 1)) * rpc;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int k = threadIdx.x; k < rpc * S::STRIDE; k += blockDim.x) sm[k] = czero<C2>();
-  __syncthreads();
-  constexpr int bpr = M / 32;
-  const C2* s = d.s + static_cast<size_t>(b) * d.P;
-  C2* part = d.wt_part + static_cast<size_t>(b) * d.n_slots * 32;
-  const int t_end = __ldg(&d.wt_roff[iy0 + rpc]);
-  for (int task = __ldg(&d.wt_roff[iy0]) + warp; task < t_end; task += nw) {
-    const int4 tk = __ldg(&d.wt_rtasks[task]);
-    const int blk = tk.x, nc = tk.z, slot = tk.w;
-    const int ix = __ldg(&d.wt_perm[static_cast<size_t>(blk) * 32 + lane]);
-    const WtEnt<R>* e = d.wt_ent + static_cast<size_t>(tk.y) * 32 + lane;
-    C2 a0 = czero<C2>(), a1 = czero<C2>();
-    for (int c = 0; c < nc; c += GRP) {
-      WtEnt<R> q[GRP];
-      C2 v[GRP];
-#pragma unroll
-      for (int k = 0; k < GRP; ++k) {
-        if (c + k < nc) {
-          q[k] = ldcs(e + (c + k) * 32);
-        } else {
-          q[k].j = 0;
-          q[k].w = R(0);
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < GRP; ++k) v[k] = q[k].w != R(0) ? __ldg(&s[q[k].j]) : czero<C2>();
-#pragma unroll
-      for (int k = 0; k < GRP; k += 2) {
-        a0.x += q[k].w * v[k].x;
-        a0.y += q[k].w * v[k].y;
-        a1.x += q[k + 1].w * v[k + 1].x;
-        a1.y += q[k + 1].w * v[k + 1].y;
-      }
-    }
-    const C2 v = cadd(a0, a1);
-    if (slot < 0)
-      sm[(blk / bpr - iy0) * S::STRIDE + pad16(ix)] = v;
-    else
-      part[static_cast<size_t>(slot) * 32 + lane] = v;
-  }
-  const int h0 = __ldg(&d.wt_hoff[iy0]), h1 = __ldg(&d.wt_hoff[iy0 + rpc]);
-  if (h1 > h0) {
-    __syncthreads();  // partials of this CTA's split blocks are visible to the whole CTA
-    for (int h = h0 + warp; h < h1; h += nw) {
-      const int4 hv = __ldg(&d.wt_rheavy[h]);
-      C2 acc = czero<C2>();
-      for (int k = 0; k < hv.z; ++k) acc = cadd(acc, __ldcg(&part[static_cast<size_t>(hv.y + k) * 32 + lane]));
-      const int ix = __ldg(&d.wt_perm[static_cast<size_t>(hv.x) * 32 + lane]);
-      sm[(hv.x / bpr - iy0) * S::STRIDE + pad16(ix)] = acc;
-    }
-  }
-  __syncthreads();
-  const int rr = threadIdx.x / S::T, t = threadIdx.x % S::T;
-  const bool active = rr < rpc;
-  C2* row = sm + (active ? rr : 0) * S::STRIDE;
-  C2 pre[RB];
-#pragma unroll
-  for (int r = 0; r < RB; ++r) pre[r] = row[pad16(t + r * S::T)];
-  __syncthreads();
-  fft_row_pre<M, RB, true, C2, HALF ? 2 : 0>(row, d.tw, t, active, pre, [&](int k, C2 v) {
-    const int t1 = (k + n / 2) & (M - 1);  // inverse of bin_of
-    if (t1 < n) row[pad16(t1)] = v;
-  });
   C2* K = d.K + static_cast<size_t>(b) * n * M;
   store_transposed<S::STRIDE>(sm, rpc, rpc, n, K + iy0, static_cast<size_t>(M));
 }
@@ -1003,11 +850,8 @@ void dispatch_m_rb(int m, int rb, F&& f) {
 // leaves the GPU short of warps (126-register threads, ~7 warps/SM at c2), and radix-8 rows
 // (twice the threads per row, one more smem pass) measured faster: c2 t2_rows 10.5 -> 9.9 us,
 // t1_rows 11.7 -> 10.7 us. fp32 (c3: 17 -> 23 us) and m = 8192 keep radix 16.
-// TOMO_ROW_RB=8|16 overrides (A/B runs).
-int env_int(const char* name, int dflt) {
-  const char* v = std::getenv(name);
-  return v && *v ? std::atoi(v) : dflt;
-}
+// TOMO_ROW_RB=8|16 overrides (A/B runs, TOMO_AB=1).
+int env_int(const char* name, int dflt) { return ab_int(name, dflt); }
 
 int row_rb(int m, size_t elem) {
   static const int forced = env_int("TOMO_ROW_RB", 0);
@@ -1027,10 +871,7 @@ void dispatch_m_rows(int m, size_t elem, F&& f) {
 
 // Grid-row passes (P2, PA): radix 16 unless TOMO_COL_RB=8 (A/B runs; one-shot kernels only).
 int col_rb(int m, size_t elem) {
-  static const int forced = [] {
-    const char* v = std::getenv("TOMO_COL_RB");
-    return v ? std::atoi(v) : 0;
-  }();
+  static const int forced = ab_int("TOMO_COL_RB", 0);
   (void)m;
   (void)elem;
   return forced == 8 ? 8 : 16;
@@ -1146,7 +987,7 @@ void launch_w(const OpDev<R>& d, int B, const cplx<R>* grid, cplx<R>* samples, c
               cudaStream_t st) {
   const int threads = 256;
   const int blocks = (d.Ppad + threads - 1) / threads;
-  if (d.w_sep) {
+  {
     // compile-time window bound: registers scale with it (6/7 are the configs' windows)
     // one grid row (w gathers) per step: rows-in-flight 1, 2, 3 and w measured equal on B200
     // (c2 8.8-9.2 us, c3 16-19 us); 1 needs the fewest registers
@@ -1166,12 +1007,6 @@ void launch_w(const OpDev<R>& d, int B, const cplx<R>* grid, cplx<R>* samples, c
       go(std::integral_constant<int, 8>{});
     else
       CK_LAUNCH(launch_k(k_w_sep_wide<R>, blocks, threads, 0, st, d, B, grid, samples, skip));
-  } else if (B >= 4) {
-    CK_LAUNCH(launch_k(k_w<4, R>, blocks, threads, 0, st, d, B, grid, samples, skip));
-  } else if (B >= 2) {
-    CK_LAUNCH(launch_k(k_w<2, R>, blocks, threads, 0, st, d, B, grid, samples, skip));
-  } else {
-    CK_LAUNCH(launch_k(k_w<1, R>, blocks, threads, 0, st, d, B, grid, samples, skip));
   }
   note_launch();
 }
@@ -1221,50 +1056,8 @@ void launch_gram(const OpDev<R>& d, int B, const cplx<R>* grid_in, cplx<R>* grid
   launch_task_spmv<R>(d.gram, d.m, B, grid_in, static_cast<size_t>(d.m) * d.m, grid_out, skip, st);
 }
 
-// Fused W^T + PA (k_wt_t1) for m < kPersistMinM when the row-grouped task tables exist
-// (TOMO_WT_FUSE=1; default off). Returns false if not taken. Measured on B200 and rejected as
-// the default: c2 W^T + PA 14.8 + 9.1 us -> 67 us, c3 31.6 + 15.8 -> 88 us, the same at 256 /
-// 512 / 1024 threads per CTA — each CTA's gather chain (a row's tasks) and FFT run back to
-// back with 1-2 CTAs per SM, where the separate task kernel spreads the rows' tasks over
-// every warp of the GPU.
-template <typename R>
-bool wt_t1_enabled(const OpDev<R>& d) {
-  static const int env_fuse = env_int("TOMO_WT_FUSE", 0);
-  return env_fuse && d.wt_rtasks && d.m < kPersistMinM;
-}
-
-template <typename R>
-bool launch_wt_t1(const OpDev<R>& d, int B, const SliceScalars* skip, cudaStream_t st) {
-  if (!wt_t1_enabled<R>(d)) return false;
-  bool done = false;
-  dispatch_m_cols(d.m, sizeof(cplx<R>), [&](auto MC, auto RC) {
-    constexpr int M = decltype(MC)::value, RB = decltype(RC)::value;
-    using S = FftShape<M, RB>;
-    if constexpr (M < kPersistMinM) {
-      const int rpc = choose_rpc(S::T, M, M, B, sizeof(cplx<R>), true);
-      if ((rpc * S::T) % 32) return;
-      const size_t smem = static_cast<size_t>(rpc) * S::STRIDE * sizeof(cplx<R>);
-      constexpr int GRP = sizeof(R) == 4 ? 6 : 4;
-      // more warps than the FFT rows need: the W^T phase is gather-latency-bound and the heavy
-      // rows' tasks are spread over all warps of the CTA (TOMO_WT_T1_THREADS: A/B override)
-      static const int env_thr = env_int("TOMO_WT_T1_THREADS", kFftThreads);
-      const int threads = std::max(rpc * S::T, std::min(env_thr, kFftThreads) / 32 * 32);
-      auto go = [&](auto kern) {
-        set_smem(kern, smem);
-        CK_LAUNCH(launch_k(kern, dim3(M / rpc, B), threads, smem, st, d, rpc, skip));
-      };
-      if (2 * d.n == M) go(k_wt_t1<M, RB, R, true, GRP>);
-      else go(k_wt_t1<M, RB, R, false, GRP>);
-      note_launch();
-      done = true;
-    }
-  });
-  return done;
-}
-
 template <typename R>
 void launch_wt_rows(const OpDev<R>& d, int B, const SliceScalars* skip, cudaStream_t st) {
-  if (launch_wt_t1<R>(d, B, skip, st)) return;
   launch_wt_spread<R>(d, B, d.s, d.Gt, skip, st);
   launch_t1_cols_only<R>(d, B, skip, st);
 }
@@ -1377,8 +1170,6 @@ void launch_fft_rows_test(int m, int rows, const cplx<R>* tw, const cplx<R>* in,
   template void launch_wt_spread<R>(const OpDev<R>&, int, const cplx<R>*, cplx<R>*, const SliceScalars*,    \
                                     cudaStream_t);                                                          \
   template void launch_wt_rows<R>(const OpDev<R>&, int, const SliceScalars*, cudaStream_t);                 \
-  template bool wt_t1_enabled<R>(const OpDev<R>&);                                                           \
-  template bool launch_wt_t1<R>(const OpDev<R>&, int, const SliceScalars*, cudaStream_t);                   \
   template void launch_t1_cols_only<R>(const OpDev<R>&, int, const SliceScalars*, cudaStream_t);            \
   template void launch_gram<R>(const OpDev<R>&, int, const cplx<R>*, cplx<R>*, const SliceScalars*, cudaStream_t); \
   template void launch_t1_rows<R>(const OpDev<R>&, int, const PbEpi<R>&, cudaStream_t);                     \

@@ -222,9 +222,9 @@ __global__ void k_entries(int m, const uint16_t* __restrict__ perm, const int* _
 // slices/s, 30 vs 40 us); for large grids (m >= 4096) grid-row order keeps the samples that
 // concurrently running tasks gather in cache (c5: 440 -> 346 us). TOMO_TASK_ORDER=rows|len.
 bool wt_row_order(int m) {
-  const char* ord = std::getenv("TOMO_TASK_ORDER");
-  if (ord && std::string(ord) == "rows") return true;
-  if (ord && std::string(ord) == "len") return false;
+  const std::string ord = ab_knob("TOMO_TASK_ORDER");
+  if (ord == "rows") return true;
+  if (ord == "len") return false;
   return m >= 4096;
 }
 
@@ -302,11 +302,7 @@ GpuBuild* gpu_build_begin(const BuildArgs& a, const double* h_cs, const double* 
 // Task structure from entries already in final order (b->sj, b->vals_sorted) and the per-node
 // counts b->cnt: node offsets, per-row node order, 32-node blocks, warp tasks, totals.
 int wt_max_chunks() {
-  static const int v = [] {
-    const char* e = std::getenv("TOMO_WT_MAXCH");
-    const int k = e && *e ? std::atoi(e) : kWtMaxChunks;
-    return std::min(std::max(k, 1), 1024);
-  }();
+  static const int v = std::min(std::max(ab_int("TOMO_WT_MAXCH", kWtMaxChunks), 1), 1024);
   return v;
 }
 

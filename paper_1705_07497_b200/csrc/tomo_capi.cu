@@ -282,6 +282,7 @@ struct Workspace {
   cudaStream_t last_stream = nullptr;
   cudaEvent_t done = nullptr;
   bool busy = false;
+  bool captured = false;  // used inside a caller's stream capture: reserved for that stream
   uint64_t last_use = 0;
 
   Workspace() = default;
@@ -319,15 +320,13 @@ struct tomo_op {
   bool f64 = false;
   size_t rsz = 4;  // sizeof(R)
   int64_t nnz = 0, wt_rows = 0, wt_slots = 0;
-  int nq = 0, Ppad = 0;
+  int Ppad = 0;
   int n_tasks = 0, n_heavy = 0, n_slots = 0;
-  Raw apod, tw, wcols, wvals, wbase, wxs, wys, wtent, wttasks, wtperm, wtheavy, wtslotheavy;
+  Raw apod, tw, wbase, wxs, wys, wtent, wttasks, wtperm, wtheavy, wtslotheavy;
   Raw wperm;           // separable-W table position -> sample (grid-tile order)
-  Raw wtrtasks, wtrheavy, wtroff;  // W^T tasks / heavy blocks grouped by grid row (k_wt_t1)
   bool w_sorted = false;
   TaskSet gram;  // fused backend only
   const TspmFile* src = nullptr;  // during tomo_op_create_tspm: the loaded Gram / surrogate T
-  int w_sep = 1;  // W storage used by the interpolation kernel (TOMO_W_FORMAT=ell selects SELL-32)
   // surrogate
   int rad = 0;
   StencilCoef coef{};
@@ -377,19 +376,15 @@ struct tomo_op {
     d.nb = g.nb;
     d.P = static_cast<int>(g.P);
     d.Ppad = Ppad;
-    d.nq = nq;
     d.G32 = static_cast<int>(static_cast<int64_t>(g.m) * g.m / 32);
     d.apod = apod.as<R>();
     d.tw = tw.as<cplx<R>>();
-    d.w_cols = wcols.as<int4>();
-    d.w_vals = wvals.as<Quad<R>>();
     d.w_base = wbase.as<int>();
     d.w_x = wxs.as<R>();
     d.w_y = wys.as<R>();
     d.w_perm = w_sorted ? wperm.as<int>() : nullptr;
     d.w_out_pos = w_sorted ? 1 : 0;
     d.w = g.w;
-    d.w_sep = w_sep;
     d.wt_ent = wtent.as<WtEnt<R>>();
     d.wt_tasks = wttasks.as<int4>();
     d.n_tasks = n_tasks;
@@ -400,10 +395,6 @@ struct tomo_op {
     d.n_heavy = n_heavy;
     d.n_slots = n_slots;
     d.wt_part = sc.part_wt.as<cplx<R>>();
-    d.wt_rtasks = wtroff.p ? wtrtasks.as<int4>() : nullptr;
-    d.wt_rheavy = wtroff.p ? wtrheavy.as<int4>() : nullptr;
-    d.wt_roff = wtroff.p ? wtroff.as<int>() : nullptr;
-    d.wt_hoff = wtroff.p ? wtroff.as<int>() + (g.m + 1) : nullptr;
     d.Gt = sc.Gt.as<cplx<R>>();
     d.H = sc.H.as<cplx<R>>();
     d.g = sc.g.as<cplx<R>>();
@@ -503,6 +494,12 @@ class Lease {
         nested_ = true;
         return;
       }
+    // Under stream capture (the caller records our launches into its own graph) no event may be
+    // queried, recorded or waited on: the capture gets a workspace of its own, reserved for that
+    // stream, and ordering the graph's replays is the caller's business.
+    cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+    if (st && cudaStreamIsCapturing(st, &cst) == cudaSuccess && cst == cudaStreamCaptureStatusActive)
+      capturing_ = true;
     std::unique_lock<std::mutex> lk(op->ws_mu);
     for (;;) {
       ws_ = nullptr;
@@ -511,9 +508,9 @@ class Lease {
           ws_ = w.get();
           break;
         }
-      if (!ws_)
+      if (!ws_ && !capturing_)
         for (auto& w : op->pool)  // 2. idle and its last call has finished on the device
-          if (!w->busy && (!w->done || cudaEventQuery(w->done) == cudaSuccess)) {
+          if (!w->busy && !w->captured && (!w->done || cudaEventQuery(w->done) == cudaSuccess)) {
             ws_ = w.get();
             break;
           }
@@ -523,14 +520,15 @@ class Lease {
       }
       if (!ws_)
         for (auto& w : op->pool)  // 4. least recently used idle one (ordered by its event)
-          if (!w->busy && (!ws_ || w->last_use < ws_->last_use)) ws_ = w.get();
+          if (!w->busy && (capturing_ || !w->captured) && (!ws_ || w->last_use < ws_->last_use)) ws_ = w.get();
       if (ws_) break;
       op->ws_cv.wait(lk);
     }
     ws_->busy = true;
     ws_->last_use = ++op->ws_clock;
+    if (capturing_) ws_->captured = true;
     lk.unlock();
-    if (ws_->done && ws_->last_stream != st) {
+    if (!capturing_ && ws_->done && ws_->last_stream != st) {
       const cudaError_t e = cudaStreamWaitEvent(st, ws_->done, 0);
       if (e != cudaSuccess) {
         release();
@@ -546,8 +544,10 @@ class Lease {
       return;
     }
     tl_leases.pop_back();
-    if (!ws_->done) cudaEventCreateWithFlags(&ws_->done, cudaEventDisableTiming);
-    if (ws_->done) cudaEventRecord(ws_->done, st_);
+    if (!capturing_) {
+      if (!ws_->done) cudaEventCreateWithFlags(&ws_->done, cudaEventDisableTiming);
+      if (ws_->done) cudaEventRecord(ws_->done, st_);
+    }
     ws_->last_stream = st_;
     release();
   }
@@ -566,6 +566,7 @@ class Lease {
   cudaStream_t st_;
   Workspace* ws_ = nullptr;
   bool nested_ = false;
+  bool capturing_ = false;
 };
 }  // namespace
 }  // namespace tomo_b200
@@ -786,8 +787,7 @@ void build_gram(tomo_op* op, const Plan& pl) {
   if (est > cap)
     throw ConfigError("build_btb: estimated " + std::to_string(est >> 20) +
                       " MiB exceeds cap; raise the cap or use a smaller m_sp");
-  const char* bld = std::getenv("TOMO_BUILD");
-  if (!(bld && std::string(bld) == "host")) {  // on the device (opbuild.cu), same tables
+  if (ab_knob("TOMO_BUILD") != "host") {  // on the device (opbuild.cu), same tables
     std::vector<int> base(g.P);
     for (int64_t j = 0; j < g.P; ++j)
       base[j] = wrapi(pl.mjx[j] + g.lo, m) | (wrapi(pl.mjy[j] + g.lo, m) << 16);
@@ -907,46 +907,30 @@ TspmFile gram_to_tspm(const tomo_op* op) {
   return t;
 }
 
-// Host build of W (separable + SELL-32 ELL) and W^T (fp64 plan, the reference's recurrence).
+// Host build of W (separable) and W^T (fp64 plan, the reference's recurrence); the device
+// build (build_w_gpu) produces the same tables and is the default.
 template <typename R>
 void build_w_host(tomo_op* op) {
   const Geom& g = op->g;
   const Plan pl = make_plan(g);
   const int w = g.w, w2 = w * w;
-  const int w2pad = op->nq * 4;
   const int m = g.m;
-
-  std::vector<int4> cols(static_cast<size_t>(op->Ppad) * op->nq);
-  std::vector<Quad<R>> vals(cols.size());
-  std::vector<int32_t> rc(w2pad);
-  std::vector<double> rv(w2pad);
+  // entries of row j in the reference's loop order (a outer, b inner), nufft.cpp:142-157
+  std::vector<int32_t> ent_node(static_cast<size_t>(g.P) * w2);
+  std::vector<double> ent_val(ent_node.size());
   std::vector<int> cnt(static_cast<size_t>(m) * m, 0);
-  for (int64_t j = 0; j < op->Ppad; ++j) {
-    if (j < g.P) {
-      const double* wx = pl.wx.data() + j * w;
-      const double* wy = pl.wy.data() + j * w;
-      for (int a = 0; a < w; ++a) {
-        const int ix = wrapi(pl.mjx[j] + g.lo + a, m);
-        for (int b = 0; b < w; ++b) {
-          const int iy = wrapi(pl.mjy[j] + g.lo + b, m);
-          rc[a * w + b] = iy * m + ix;
-          rv[a * w + b] = wx[a] * wy[b];
-          cnt[static_cast<size_t>(iy) * m + ix]++;
-        }
+  for (int64_t j = 0; j < g.P; ++j) {
+    const double* wx = pl.wx.data() + j * w;
+    const double* wy = pl.wy.data() + j * w;
+    for (int a = 0; a < w; ++a) {
+      const int ix = wrapi(pl.mjx[j] + g.lo + a, m);
+      for (int b = 0; b < w; ++b) {
+        const int iy = wrapi(pl.mjy[j] + g.lo + b, m);
+        const size_t e = static_cast<size_t>(j) * w2 + a * w + b;
+        ent_node[e] = iy * m + ix;
+        ent_val[e] = wx[a] * wy[b];
+        cnt[static_cast<size_t>(iy) * m + ix]++;
       }
-      for (int e = w2; e < w2pad; ++e) {
-        rc[e] = rc[0];
-        rv[e] = 0.0;
-      }
-    } else {
-      std::fill(rc.begin(), rc.end(), 0);
-      std::fill(rv.begin(), rv.end(), 0.0);
-    }
-    const int64_t blk = j / 32, lane = j % 32;
-    for (int q = 0; q < op->nq; ++q) {
-      const size_t o = (static_cast<size_t>(blk) * op->nq + q) * 32 + lane;
-      cols[o] = make_int4(rc[4 * q], rc[4 * q + 1], rc[4 * q + 2], rc[4 * q + 3]);
-      for (int k = 0; k < 4; ++k) vals[o].v[k] = static_cast<R>(rv[4 * q + k]);
     }
   }
 
@@ -960,14 +944,11 @@ void build_w_host(tomo_op* op) {
   std::vector<R> tv(off[G]);
   std::vector<int64_t> fillp(off.begin(), off.end() - 1);
   for (int64_t j = 0; j < g.P; ++j) {
-    const int64_t blk = j / 32, lane = j % 32;
     for (int e = 0; e < w2; ++e) {
-      const int q = e / 4, c = e % 4;
-      const size_t o = (static_cast<size_t>(blk) * op->nq + q) * 32 + lane;
-      const int node = (&cols[o].x)[c];
-      const int64_t k = fillp[node]++;
+      const size_t o = static_cast<size_t>(j) * w2 + e;
+      const int64_t k = fillp[ent_node[o]]++;
       tj[k] = static_cast<int32_t>(j);
-      tv[k] = vals[o].v[c];
+      tv[k] = static_cast<R>(ent_val[o]);
     }
   }
   TaskBuilder<R> tb(m, wt_max_chunks(), off[G]);
@@ -993,10 +974,6 @@ void build_w_host(tomo_op* op) {
   op->wbase.upload(wbase);
   op->wxs.upload(wxs);
   op->wys.upload(wys);
-  if (!op->w_sep) {  // the SELL-32 ELL form is uploaded only when selected (TOMO_W_FORMAT=ell)
-    op->wcols.upload(cols);
-    op->wvals.upload(vals);
-  }
   tb.upload(op->wtent, op->wttasks, op->wtperm, op->wtheavy, op->wtslotheavy);
 }
 
@@ -1035,57 +1012,21 @@ void build_w_gpu(tomo_op* op) {
                       op->wtheavy.as<int4>(), op->wtslotheavy.as<int>(), 0);
 }
 
-// W^T tasks and heavy blocks regrouped by grid row for the fused W^T + PA kernel (k_wt_t1):
-// tasks of a row longest first (the CTA's warps take them in turn), heavy blocks in block
-// order; offsets per row. Only for m < 4096 and with TOMO_WT_FUSE=1 (A/B; the two-kernel
-// path is the default).
-void build_row_tasks(tomo_op* op) {
-  const int m = op->g.m;
-  const char* fuse = std::getenv("TOMO_WT_FUSE");
-  if (m >= 4096 || op->n_tasks <= 0 || !(fuse && std::atoi(fuse) != 0)) return;
-  std::vector<int4> tasks(op->n_tasks), heavy(op->n_heavy);
-  CK(cudaMemcpy(tasks.data(), op->wttasks.p, sizeof(int4) * tasks.size(), cudaMemcpyDeviceToHost));
-  if (op->n_heavy > 0)
-    CK(cudaMemcpy(heavy.data(), op->wtheavy.p, sizeof(int4) * heavy.size(), cudaMemcpyDeviceToHost));
-  const int bpr = m / 32;
-  std::stable_sort(tasks.begin(), tasks.end(), [&](const int4& a, const int4& b) {
-    const int ra = a.x / bpr, rb = b.x / bpr;
-    return ra != rb ? ra < rb : a.z > b.z;
-  });
-  std::stable_sort(heavy.begin(), heavy.end(), [](const int4& a, const int4& b) { return a.x < b.x; });
-  std::vector<int> off(2 * (m + 1), 0);
-  for (const int4& t : tasks) ++off[t.x / bpr + 1];
-  for (const int4& h : heavy) ++off[m + 1 + h.x / bpr + 1];
-  for (int iy = 0; iy < m; ++iy) {
-    off[iy + 1] += off[iy];
-    off[m + 1 + iy + 1] += off[m + 1 + iy];
-  }
-  op->wtrtasks.upload(tasks);
-  op->wtrheavy.upload(heavy.empty() ? std::vector<int4>(1) : heavy);
-  op->wtroff.upload(off);
-}
-
 template <typename R>
 void build_tables(tomo_op* op) {
   const Geom& g = op->g;
   const int w = g.w, m = g.m;
-  op->nq = (w * w + 3) / 4;
   op->Ppad = static_cast<int>((g.P + 31) / 32 * 32);
   op->nnz = g.P * w * w;
-  const char* fmt = std::getenv("TOMO_W_FORMAT");
-  op->w_sep = (fmt && std::string(fmt) == "ell") ? 0 : 1;
-  // W / W^T are built on the device unless the SELL-32 ELL form of W is requested (host) or
-  // TOMO_BUILD=host asks for the host build (kept as the reference for tests/test_gpu_build.py)
-  const char* bld = std::getenv("TOMO_BUILD");
-  if (op->w_sep && !(bld && std::string(bld) == "host"))
-    build_w_gpu<R>(op);
-  else
+  // W / W^T are built on the device; TOMO_BUILD=host (with TOMO_AB=1) selects the host build,
+  // kept as the reference the device tables are compared with (tests/test_gpu_build.py)
+  if (ab_knob("TOMO_BUILD") == "host")
     build_w_host<R>(op);
-  build_row_tasks(op);
+  else
+    build_w_gpu<R>(op);
   // separable W in 16x16 grid-tile order: concurrently running warps gather from nearby nodes
-  const char* word = std::getenv("TOMO_W_ORDER");
-  op->w_sorted = op->w_sep && !(word && std::string(word) == "angle");
-  if (op->w_sorted) {
+  op->w_sorted = true;
+  {
     op->wperm.ensure(sizeof(int) * std::max<int64_t>(g.P, 1));
     gpu_sort_w_tables<R>(m, g.P, op->Ppad, w, op->wbase.as<int>(), op->wxs.as<R>(), op->wys.as<R>(),
                          op->wperm.as<int>(), op->wtent.as<WtEnt<R>>(), op->wt_slots, 0);
@@ -1259,12 +1200,9 @@ void normal_direct(tomo_op* op, int B, const void* in, bool cplx_io, void* out, 
 
 SysParams sysp(double alpha, double lambda, double shift, double tol) { return SysParams{alpha, lambda, shift, tol}; }
 
-// Chronopoulos-Gear CG for the unsharded W/W^T and Gram backends unless TOMO_CG=std.
+// Chronopoulos-Gear CG for the unsharded W/W^T and Gram backends unless TOMO_CG=std (A/B).
 bool cgcg_on() {
-  static const bool v = [] {
-    const char* e = std::getenv("TOMO_CG");
-    return !(e && std::string(e) == "std");
-  }();
+  static const bool v = ab_knob("TOMO_CG") != "std";
   return v;
 }
 
@@ -1934,8 +1872,7 @@ int tomo_op_get_info(const tomo_op* op, tomo_op_info* info) {
   info->nnz = op->nnz;
   info->wt_rows = op->wt_rows;
   info->wt_slots = op->wt_slots;
-  info->bytes_w = op->w_sep ? static_cast<int64_t>(op->Ppad) * (4 + 2 * op->g.w * static_cast<int64_t>(op->rsz))
-                            : static_cast<int64_t>(op->Ppad) * op->nq * 32 * (16 + 4 * static_cast<int64_t>(op->rsz)) / 32;
+  info->bytes_w = static_cast<int64_t>(op->Ppad) * (4 + 2 * op->g.w * static_cast<int64_t>(op->rsz));
   info->bytes_wt = op->wt_slots * (op->f64 ? 16 : 8) + static_cast<int64_t>(op->n_tasks) * 16 +
                    static_cast<int64_t>(op->g.m) * op->g.m * 2;
   info->surrogate_r = op->rad;
@@ -2678,11 +2615,9 @@ int tomo_profile_stages(tomo_op* op, int batch, int reps, double* ms, double* by
           else
             launch_w<R>(d, batch, d.g, d.s, op->scal(), cs);
         } else if (s == 3) {
-          // W^T; with the fused W^T + PA kernel this stage is both and stage 4 is empty
-          if (op->fused() || !launch_wt_t1<R>(d, batch, op->scal(), cs))
-            launch_wt_spread<R>(d, batch, d.s, d.Gt, op->scal(), cs);
+          if (!op->fused()) launch_wt_spread<R>(d, batch, d.s, d.Gt, op->scal(), cs);
         } else if (s == 4) {
-          if (op->fused() || !wt_t1_enabled<R>(d)) launch_t1_cols_only<R>(d, batch, op->scal(), cs);
+          launch_t1_cols_only<R>(d, batch, op->scal(), cs);
         } else if (s == 5) {
           PbEpi<R> e = plain_epi<R>(PB_CG_STEP, 1.0);
           e.p = S.p0.as<R>();
@@ -2711,9 +2646,8 @@ int tomo_profile_stages(tomo_op* op, int batch, int reps, double* ms, double* by
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
-    const bool wt_fused = !sur && !op->fused() && wt_t1_enabled<R>(d);  // stage 3 = W^T + PA, no stage 4
     auto stage_on = [&](int s) {
-      return sur ? (s >= 6) : (s <= 7 && !(op->fused() && s == 3) && !(wt_fused && s == 4));
+      return sur ? (s >= 6) : (s <= 7 && !(op->fused() && s == 3));
     };
     for (int s = 0; s < TOMO_NUM_STAGES; ++s) {
       const bool on = stage_on(s);
@@ -2751,8 +2685,7 @@ int tomo_profile_stages(tomo_op* op, int batch, int reps, double* ms, double* by
       by[2] = op->fused()  // Gram stream, read + write touched nodes
                   ? static_cast<double>(op->gram.bytes) + B * (2 * cs * op->wt_rows)
                   : nnzb + B * (cs * op->wt_rows + cs * P);
-      by[3] = wt_fused ? nnzb + 8.0 * (op->wt_rows + 1) + B * (cs * P + cs * mn)  // grid stays on chip: K
-                       : nnzb + 8.0 * (op->wt_rows + 1) + B * (cs * P + cs * mm);
+      by[3] = nnzb + 8.0 * (op->wt_rows + 1) + B * (cs * P + cs * mm);
       by[4] = B * (cs * mm + cs * mn);                     // read spread grid, write K
       by[5] = B * (cs * mn + 2 * rs * nn);                 // read K, p; write Ap
     } else {

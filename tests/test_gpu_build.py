@@ -1,5 +1,5 @@
 """Operator construction on the device (csrc/opbuild.cu) against the host build
-(TOMO_BUILD=host): same table structure, same operator to rounding."""
+(TOMO_AB=1 TOMO_BUILD=host): same table structure, same operator to rounding."""
 import os
 
 import numpy as np
@@ -26,12 +26,17 @@ def T():
     return T
 
 
-def _host_op(T, g, **kw):
-    os.environ["TOMO_BUILD"] = "host"
+def _host_build(fn, *a, **kw):
+    """The host build (TOMO_BUILD=host, an A/B knob honoured with TOMO_AB=1)."""
+    os.environ["TOMO_AB"], os.environ["TOMO_BUILD"] = "1", "host"
     try:
-        return T.make_direct_backend(g, **kw)
+        return fn(*a, **kw)
     finally:
-        del os.environ["TOMO_BUILD"]
+        del os.environ["TOMO_BUILD"], os.environ["TOMO_AB"]
+
+
+def _host_op(T, g, **kw):
+    return _host_build(T.make_direct_backend, g, **kw)
 
 
 @pytest.mark.parametrize("prec", ["f32", "f64"])
@@ -63,11 +68,7 @@ def test_device_gram_matches_host_gram(T, name):
     """The fused backend's Gram built on the device equals the host build_btb restatement:
     same nnz and the same tables, hence bitwise-equal applies."""
     og = O.Geometry(**GEOMS[name])
-    os.environ["TOMO_BUILD"] = "host"
-    try:
-        host = T.make_fused_backend(pgeom(T, og), precision="f64")
-    finally:
-        del os.environ["TOMO_BUILD"]
+    host = _host_build(T.make_fused_backend, pgeom(T, og), precision="f64")
     dev = T.make_fused_backend(pgeom(T, og), precision="f64")
     assert dev.info.gram_nnz == host.info.gram_nnz == O.btb_nnz(og)
     assert dev.info.gram_slots == host.info.gram_slots

@@ -163,10 +163,27 @@ def test_c5_apply_and_chambolle_pock(T):
     ph, f = synth(og, 5000)
     out = op.apply_normal_real(dev(ph, np.float64)).cpu().numpy()
     record("c5", "apply_normal_real f64", rel(out, O.apply_normal_real(og, ph)), OP_TOL_F64)
-    mu = op.chambolle_pock(dev(f, np.complex128), alpha=c["alpha"], lambda_=c["lam"], tau_cp=c["tau_cp"],
-                           sigma_cp=c["sigma_cp"], theta=c["theta"], iters=1, cg_steps=c["cg"]).cpu().numpy()
+    cp = dict(alpha=c["alpha"], tau_cp=c["tau_cp"], sigma_cp=c["sigma_cp"], theta=c["theta"], iters=1)
+    fd = dev(f, np.complex128)
+    # (a) one CP iteration with a 10-step prox CG: before CG's transient (below), GPU and oracle
+    #     agree to rounding
+    mu = op.chambolle_pock(fd, lambda_=c["lam"], cg_steps=10, **cp).cpu().numpy()
+    ref = O.chambolle_pock(og, f, lam=c["lam"], cg_steps=10, **cp)
+    record("c5", "chambolle_pock 1x10 CG", rel(mu, ref), REC_TOL)
+    # (b) the config's 1 x 15: the prox system I + tau*alpha*N has kappa ~ 7e5 here, and between
+    #     CG steps 13 and 15 its Ritz values converge and CG amplifies per-apply rounding to the
+    #     1e-4 level (the GPU's two CG forms differ by 1.4e-4 from each other); DESIGN.md §5. The
+    #     bound is 1e-3 or, if larger, 3x the oracle's own spread when each of its applies is
+    #     perturbed at the rounding level of an equally exact implementation (1e-16 relative).
+    mu = op.chambolle_pock(fd, lambda_=c["lam"], cg_steps=c["cg"], **cp).cpu().numpy()
     t0 = time.perf_counter()
-    ref = O.chambolle_pock(og, f, alpha=c["alpha"], lam=c["lam"], tau_cp=c["tau_cp"], sigma_cp=c["sigma_cp"],
-                           theta=c["theta"], iters=1, cg_steps=c["cg"])
-    record("c5", f"chambolle_pock 1x{c['cg']} CG", rel(mu, ref), REC_TOL,
-           oracle_s=round(time.perf_counter() - t0, 1))
+    ref = O.chambolle_pock(og, f, lam=c["lam"], cg_steps=c["cg"], **cp)
+    t_oracle = time.perf_counter() - t0
+    try:
+        O.set_perturbation(1e-16, seed=3)
+        ref_p = O.chambolle_pock(og, f, lam=c["lam"], cg_steps=c["cg"], **cp)
+    finally:
+        O.set_perturbation(0.0)
+    spread = rel(ref_p, ref)
+    record("c5", f"chambolle_pock 1x{c['cg']} CG (bound: 3 x oracle rounding spread)", rel(mu, ref),
+           max(REC_TOL, 3.0 * spread), oracle_rounding_spread=spread, oracle_s=round(t_oracle, 1))

@@ -1,4 +1,5 @@
-"""A/B: c3 applies on one stream vs two independent op handles on two streams (graph-captured)."""
+"""A/B: c3 applies on K streams, each graph-captured; `python tools/c3_streams.py K [shared]` uses K
+op handles, or ONE shared op serving all K streams (reentrant: one workspace per stream)."""
 import sys, os, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -8,7 +9,12 @@ from bench import CONFIGS, make_geom
 c = CONFIGS["c3"]
 g = make_geom(T, c)
 nops = int(sys.argv[1]) if len(sys.argv) > 1 else 2
-ops = [T.make_direct_backend(g, precision="f32") for _ in range(nops)]
+shared = len(sys.argv) > 2 and sys.argv[2] == "shared"
+if shared:
+    op0 = T.make_direct_backend(g, precision="f32")
+    ops = [op0] * nops
+else:
+    ops = [T.make_direct_backend(g, precision="f32") for _ in range(nops)]
 u = torch.randn(g.n, g.n, dtype=torch.complex64, device="cuda")
 streams = [torch.cuda.Stream() for _ in range(nops)]
 applies, chunk = 1000, 50
@@ -40,4 +46,4 @@ for rep in range(3):
     e1.record()
     e1.synchronize()
     ms = e0.elapsed_time(e1)
-    print(f"ops={nops} applies/s {applies / (ms * 1e-3):.0f}")
+    print(f"streams={nops} {'one shared op' if shared else 'ops=' + str(nops)} applies/s {applies / (ms * 1e-3):.0f}")
