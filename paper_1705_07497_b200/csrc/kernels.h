@@ -46,7 +46,6 @@ struct TaskSpmv {
   cplx<R>* part;            // B x n_slots x 32 partial sums of split blocks
 };
 
-// Four W values of one SELL-32 slot quad (16 B fp32 / 32 B fp64).
 // Operator tables + scratch for one device-resident normal operator (see DESIGN.md
 // "HBM layout"). Grid nodes are stored transposed relative to the reference:
 // node = iy*m + ix, where the reference has grid[ix*m + iy] (proj/src/nufft.cpp:185-200).

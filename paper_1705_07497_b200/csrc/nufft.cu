@@ -985,7 +985,8 @@ unsigned batch_ydim(int blocks, int groups) {
 template <typename R>
 void launch_w(const OpDev<R>& d, int B, const cplx<R>* grid, cplx<R>* samples, const SliceScalars* skip,
               cudaStream_t st) {
-  const int threads = 256;
+  static const int env_thr = env_int("TOMO_W_THREADS", 256);
+  const int threads = env_thr == 64 || env_thr == 128 ? env_thr : 256;
   const int blocks = (d.Ppad + threads - 1) / threads;
   {
     // compile-time window bound: registers scale with it (6/7 are the configs' windows)
