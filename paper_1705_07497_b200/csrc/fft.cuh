@@ -177,20 +177,27 @@ TOMO_DEV void twiddle(C2* v, const C2* __restrict__ tw, int base) {
 template <int R>
 TOMO_DEV constexpr bool mid_quarter(int r) { return R >= 4 && r >= R / 4 && r < 3 * R / 4; }
 
-// One Stockham pass (radix R, sub-transform size Ns) of the row owned by this thread group.
+// One Stockham pass (radix R, sub-transform size NS) of the row owned by this thread group.
 // FIRST: inputs come from load(i) (global), otherwise from the smem row. LAST: outputs go to
 // store(k, value), otherwise back into the smem row. Every thread of the CTA must call each
 // pass (barriers inside); `active` gates the work. STORE_SMEM_LAST: the storer writes the smem
 // row, so a barrier separates the last reads from those writes.
-template <int M, int RB, int R, bool FIRST, bool LAST, bool STORE_SMEM_LAST, typename C2, int PR = 0,
+// NS is a compile-time constant, so whenever the padded (pad16) smem positions of a thread's
+// elements differ by compile-time amounts — reads when T and M/R are multiples of 16, writes
+// when NS is (or NS = 1 with R = 16) — they are addressed as one base pointer plus immediate
+// offsets instead of a pad16 computation per element.
+template <int M, int RB, int R, bool FIRST, bool LAST, bool STORE_SMEM_LAST, typename C2, int PR, int NS,
           typename Load, typename Store>
-TOMO_DEV void fft_pass(C2* row, const C2* __restrict__ tw, int Ns, int t, bool active, Load& load, Store& store,
+TOMO_DEV void fft_pass(C2* row, const C2* __restrict__ tw, int t, bool active, Load& load, Store& store,
                        const C2* tws = nullptr) {
   constexpr int T = M / RB;
   constexpr int NB = M / R;    // butterflies per pass
   constexpr int PER = NB / T;  // butterflies per thread (RB/R)
+  constexpr bool RD_CONST = (T % 16 == 0) && (NB % 16 == 0);
+  constexpr bool WR_CONST = (NS % 16 == 0) || (NS == 1 && R == 16);
   C2 v[PER][R];
   if (active) {
+    const C2* rd = row + pad16(t);
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
       const int j = t + q * T;
@@ -198,19 +205,23 @@ TOMO_DEV void fft_pass(C2* row, const C2* __restrict__ tw, int Ns, int t, bool a
       for (int r = 0; r < R; ++r) {
         if (FIRST && (PR & 1) && mid_quarter<R>(r))
           v[q][r] = czero<C2>();
+        else if (FIRST)
+          v[q][r] = load(j + r * NB);
+        else if constexpr (RD_CONST)
+          v[q][r] = rd[q * (T + T / 16) + r * (NB + NB / 16)];
         else
-          v[q][r] = FIRST ? load(j + r * NB) : row[pad16(j + r * NB)];
+          v[q][r] = row[pad16(j + r * NB)];
       }
       if (!FIRST) {
-        const int jm = j & (Ns - 1);
+        const int jm = j & (NS - 1);
         if (jm) {
-          if (R == RB && Ns == RB && tws) {
+          if (R == RB && NS == RB && tws) {
             // second pass: the RB - 1 twiddles of sub-transform jm from the CTA's smem table
             // layout [r][jm]: the lanes of a warp (consecutive jm) read consecutive entries
 #pragma unroll
             for (int r = 1; r < R; ++r) v[q][r] = cmul(v[q][r], tws[r * RB + jm]);
           } else {
-            twiddle<R, C2, (M >= TOMO_TW_SPLIT_M)>(v[q], tw, (M / (Ns * R)) * jm);
+            twiddle<R, C2, (M >= TOMO_TW_SPLIT_M)>(v[q], tw, (M / (NS * R)) * jm);
           }
         }
       }
@@ -222,15 +233,18 @@ TOMO_DEV void fft_pass(C2* row, const C2* __restrict__ tw, int Ns, int t, bool a
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
       const int j = t + q * T;
-      const int jm = j & (Ns - 1);
+      const int jm = j & (NS - 1);
       const int base = (j - jm) * R + jm;
+      C2* wr = row + pad16(base);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         if (LAST && (PR & 2) && mid_quarter<R>(r)) continue;
         if (LAST)
-          store(base + r * Ns, v[q][r]);
+          store(base + r * NS, v[q][r]);
+        else if constexpr (WR_CONST)
+          wr[r * (NS + NS / 16)] = v[q][r];
         else
-          row[pad16(base + r * Ns)] = v[q][r];
+          row[pad16(base + r * NS)] = v[q][r];
       }
     }
   }
@@ -258,6 +272,32 @@ TOMO_DEV const C2* fill_tws(const C2* __restrict__ tw) {
   }
 }
 
+constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
+
+// Passes P, P+1, ... of a row after the first: radix RB with sub-transform size RB^P, then the
+// last pass (radix RL, or RB when RL = 1), which hands its outputs to the storer.
+template <int M, int RB, bool STORE_SMEM, typename C2, int PR, int P, typename Store>
+TOMO_DEV void fft_rest(C2* row, const C2* __restrict__ tw, int t, bool active, Store& store, const C2* tws) {
+  using S = FftShape<M, RB>;
+  constexpr int NS = ipow(RB, P);
+  auto noload = [](int) { return C2{}; };
+  if constexpr (S::RL > 1) {
+    if constexpr (P < S::NB) {
+      fft_pass<M, RB, RB, false, false, false, C2, 0, NS>(row, tw, t, active, noload, store, tws);
+      fft_rest<M, RB, STORE_SMEM, C2, PR, P + 1>(row, tw, t, active, store, tws);
+    } else {
+      fft_pass<M, RB, S::RL, false, true, STORE_SMEM, C2, PR & 2, NS>(row, tw, t, active, noload, store, tws);
+    }
+  } else {
+    if constexpr (P < S::NB - 1) {
+      fft_pass<M, RB, RB, false, false, false, C2, 0, NS>(row, tw, t, active, noload, store, tws);
+      fft_rest<M, RB, STORE_SMEM, C2, PR, P + 1>(row, tw, t, active, store, tws);
+    } else {
+      fft_pass<M, RB, RB, false, true, STORE_SMEM, C2, PR & 2, NS>(row, tw, t, active, noload, store, tws);
+    }
+  }
+}
+
 // Forward FFT whose first-pass inputs were loaded earlier into registers: pre[r] holds the
 // element at position t + r*M/RB (what load(t + r*M/RB) would return). Lets a persistent
 // kernel prefetch the next row while the current one is transformed.
@@ -276,49 +316,15 @@ TOMO_DEV void fft_row_pre(C2* row, const C2* __restrict__ tw, int t, bool active
     for (int r = 0; r < RB; ++r) row[pad16(t * RB + r)] = v[r];  // Stockham output of the Ns = 1 pass
   }
   __syncthreads();
-  auto noload = [](int) { return C2{}; };
-  if constexpr (S::RL > 1) {
-    int Ns = RB;
-#pragma unroll
-    for (int p = 1; p < S::NB; ++p) {
-      fft_pass<M, RB, RB, false, false, false, C2>(row, tw, Ns, t, active, noload, store, tws);
-      Ns *= RB;
-    }
-    fft_pass<M, RB, S::RL, false, true, STORE_SMEM, C2, PR & 2>(row, tw, Ns, t, active, noload, store, tws);
-  } else {
-    int Ns = RB;
-#pragma unroll
-    for (int p = 1; p < S::NB - 1; ++p) {
-      fft_pass<M, RB, RB, false, false, false, C2>(row, tw, Ns, t, active, noload, store, tws);
-      Ns *= RB;
-    }
-    fft_pass<M, RB, RB, false, true, STORE_SMEM, C2, PR & 2>(row, tw, Ns, t, active, noload, store, tws);
-  }
+  fft_rest<M, RB, STORE_SMEM, C2, PR, 1>(row, tw, t, active, store, tws);
 }
 
 // Forward FFT of one row per thread group: load(i) -> ... -> store(k, X[k]).
 template <int M, int RB, bool STORE_SMEM, typename C2, int PR = 0, typename Load, typename Store>
 TOMO_DEV void fft_row(C2* row, const C2* __restrict__ tw, int t, bool active, Load&& load, Store&& store) {
-  using S = FftShape<M, RB>;
   const C2* tws = fill_tws<M, RB, C2>(tw);
-  fft_pass<M, RB, RB, true, false, false, C2, PR & 1>(row, tw, 1, t, active, load, store);
-  if constexpr (S::RL > 1) {
-    int Ns = RB;
-#pragma unroll
-    for (int p = 1; p < S::NB; ++p) {
-      fft_pass<M, RB, RB, false, false, false, C2>(row, tw, Ns, t, active, load, store, tws);
-      Ns *= RB;
-    }
-    fft_pass<M, RB, S::RL, false, true, STORE_SMEM, C2, PR & 2>(row, tw, Ns, t, active, load, store, tws);
-  } else {
-    int Ns = RB;
-#pragma unroll
-    for (int p = 1; p < S::NB - 1; ++p) {
-      fft_pass<M, RB, RB, false, false, false, C2>(row, tw, Ns, t, active, load, store, tws);
-      Ns *= RB;
-    }
-    fft_pass<M, RB, RB, false, true, STORE_SMEM, C2, PR & 2>(row, tw, Ns, t, active, load, store, tws);
-  }
+  fft_pass<M, RB, RB, true, false, false, C2, PR & 1, 1>(row, tw, t, active, load, store);
+  fft_rest<M, RB, STORE_SMEM, C2, PR, 1>(row, tw, t, active, store, tws);
 }
 
 }  // namespace tomo_b200

@@ -104,8 +104,10 @@ struct NoStore {
 // ---------------------------------------------------------------- P1: image rows (t1)
 // deapodise + pad + inverse FFT along t2; the CG p-update (p = r + beta p) is fused into the
 // load; output transposed to H[iy][t1] through smem.
-template <int M, int RB, typename R, bool HALF = false>
-__global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F32 : TOMO_FFT_MINB_F64) k_t2_rows(OpDev<R> d, const void* __restrict__ in, int in_complex,
+// IN: the input mode, a compile-time constant so the per-element load carries no mode branches:
+// 0 complex input, 1 real input, 2 standard CG p-update, 3 Chronopoulos-Gear update.
+template <int M, int RB, typename R, bool HALF = false, int IN = 0>
+__global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F32 : TOMO_FFT_MINB_F64) k_t2_rows(OpDev<R> d, const void* __restrict__ in,
                                                   PUpd<R> pu, int rpc) {
   using S = FftShape<M, RB>;
   using C2 = cplx<R>;
@@ -113,15 +115,16 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F3
   C2* sm = reinterpret_cast<C2*>(smraw);
   const int b = blockIdx.y;
   double beta = 0.0, alpha = 0.0;
-  if (pu.enabled && pu.cgcg) {
+  if constexpr (IN == 3) {
     const SliceScalars& sc = pu.red.sc[b];
     if (sc.done || sc.frozen) return;
     beta = sc.cg_beta;
     alpha = sc.cg_alpha;
-  } else if (pu.enabled && !cg_step_live(pu.red, b, pu.step, beta)) {
-    return;
+  } else if constexpr (IN == 2) {
+    if (!cg_step_live(pu.red, b, pu.step, beta)) return;
+  } else {
+    if (pu.red.sc && pu.red.sc[b].frozen) return;
   }
-  if (!pu.enabled && pu.red.sc && pu.red.sc[b].frozen) return;
   const int rr = threadIdx.x / S::T, t = threadIdx.x % S::T;
   const int n = d.n;
   const int t10 = blockIdx.x * rpc;
@@ -136,9 +139,9 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F3
     C2 v = czero<C2>();
     if (t2 < n) {
       const R sc = a1 * __ldg(&d.apod[t2]);
-      if (in_complex) {
+      if constexpr (IN == 0) {
         v = reinterpret_cast<const C2*>(in)[base + t2];
-      } else if (pu.enabled && pu.cgcg) {
+      } else if constexpr (IN == 3) {
         const size_t o = base + t2;
         R rv = pu.r[o];
         if (pu.step > 0) {
@@ -157,7 +160,7 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F3
           if (!finite_r(xv)) pu.red.sc[b].nonfinite = 1;
         }
         v.x = rv;
-      } else if (pu.enabled) {
+      } else if constexpr (IN == 2) {
         R pv = pu.p[base + t2];
         if (pu.step > 0) {
           pv = pu.r[base + t2] + bt * pv;
@@ -498,7 +501,8 @@ __device__ __forceinline__ void cgcg_finalize(SliceScalars& sc, double delta, do
 // ---------------------------------------------------------------- PB: image rows (t1)
 // forward FFT along iy, crop to the n bins, deapodise, then the epilogue: complex / real
 // output or the CG system apply alpha*Re(N p) + lambda K'K p + shift p with the dots.
-template <int M, int RB, typename R, bool HALF = false>
+// EPI: 0 complex output, 1 real output, 2 the CG modes (compile time: no per-element branches)
+template <int M, int RB, typename R, bool HALF = false, int EPI = 2>
 __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F32 : TOMO_FFT_MINB_F64) k_t1_rows(OpDev<R> d, PbEpi<R> e, int rpc) {
   using S = FftShape<M, RB>;
   using C2 = cplx<R>;
@@ -525,9 +529,9 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F3
     if (t2 >= n) return;
     const R sc = a1 * __ldg(&d.apod[t2]);
     const size_t o = base + t2;
-    if (e.mode == PB_COMPLEX) {
+    if constexpr (EPI == 0) {
       e.out_c[o] = cscale(X, sc);
-    } else if (e.mode == PB_REAL) {
+    } else if constexpr (EPI == 1) {
       e.out_r[o] = X.x * sc;
     } else {
       const R pv = p[static_cast<size_t>(t1) * n + t2];
@@ -550,7 +554,7 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F3
     }
   };
   fft_row<M, RB, false, C2, HALF ? 2 : 0>(row, d.tw, t, active, load, store);
-  if (e.mode >= PB_CG_STEP) {
+  if (EPI == 2) {
     double t0s, t1s;
     SliceScalars& sc = e.red.sc[b];
     double* part = e.red.part + static_cast<size_t>(b) * MAX_PART_BLOCKS * 2;
@@ -916,10 +920,20 @@ void launch_t2_rows(const OpDev<R>& d, int B, const void* in, bool in_complex, c
     dim3 grid((d.n + rpc - 1) / rpc, B);
     auto go = [&](auto kern) {
       set_smem(kern, smem);
-      CK_LAUNCH(launch_k(kern, grid, rpc * S::T, smem, st, d, in, in_complex ? 1 : 0, pu, rpc));
+      CK_LAUNCH(launch_k(kern, grid, rpc * S::T, smem, st, d, in, pu, rpc));
     };
-    if (2 * d.n == M) go(k_t2_rows<M, RB, R, true>);
-    else go(k_t2_rows<M, RB, R, false>);
+    const int mode = in_complex ? 0 : !pu.enabled ? 1 : pu.cgcg ? 3 : 2;
+    auto go_mode = [&](auto HC) {
+      constexpr bool H = decltype(HC)::value;
+      switch (mode) {
+        case 0: go(k_t2_rows<M, RB, R, H, 0>); break;
+        case 1: go(k_t2_rows<M, RB, R, H, 1>); break;
+        case 2: go(k_t2_rows<M, RB, R, H, 2>); break;
+        default: go(k_t2_rows<M, RB, R, H, 3>); break;
+      }
+    };
+    if (2 * d.n == M) go_mode(std::true_type{});
+    else go_mode(std::false_type{});
     note_launch();
   });
 }
@@ -1117,8 +1131,15 @@ void launch_t1_rows(const OpDev<R>& d, int B, const PbEpi<R>& e, cudaStream_t st
         set_smem(kern, smem);
         CK_LAUNCH(launch_k(kern, grid, rpc * S::T, smem, st, d, e, rpc));
       };
-      if (2 * d.n == M) go(k_t1_rows<M, RB, R, true>);
-      else go(k_t1_rows<M, RB, R, false>);
+      const int epi = e.mode == PB_COMPLEX ? 0 : e.mode == PB_REAL ? 1 : 2;
+      auto go_epi = [&](auto HC) {
+        constexpr bool H = decltype(HC)::value;
+        if (epi == 0) go(k_t1_rows<M, RB, R, H, 0>);
+        else if (epi == 1) go(k_t1_rows<M, RB, R, H, 1>);
+        else go(k_t1_rows<M, RB, R, H, 2>);
+      };
+      if (2 * d.n == M) go_epi(std::true_type{});
+      else go_epi(std::false_type{});
     }
     note_launch();
   });
