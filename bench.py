@@ -362,7 +362,7 @@ class Workload:
         # lanes (TOMO_LANES, default 3) as sub-batches of ceil(batch / lanes)
         lanes = min(max(int(os.environ.get("TOMO_LANES", "3") or 3), 1), 4)
         B = self.batch if k in ("sb_sur", "sb") else (-(-self.batch // lanes) if k in ("apply", "c1") else 1)
-        prof = self.op.profile_stages(batch=B, reps=10)
+        prof = self.op.profile_stages(batch=B, reps=10, complex_io=(k == "apply"))
         if k in ("sb", "c1", "cp"):
             steps = c.get("cg", 10)
             iters = c.get("iters", 1)

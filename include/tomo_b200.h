@@ -95,6 +95,11 @@ typedef struct tomo_op_info {
   int64_t gram_nnz;     /* fused backend: non-zeros of W^T W (= build_btb's CSR nnz) */
   int64_t gram_slots;   /* fused backend: task-SpMV slots incl. padding */
   int64_t bytes_gram;   /* fused backend: device bytes of the Gram tables */
+  /* W^T folded onto the Hermitian half grid (rows iy in [0, m/2]) for real-part outputs */
+  int64_t herm_nnz;     /* entries (= nnz + the entries of grid rows 0 and m/2, listed twice) */
+  int64_t herm_slots;   /* task-SpMV slots incl. padding */
+  int64_t herm_touched; /* touched half-grid nodes */
+  int herm_tasks;       /* warp tasks (0: not built, real inputs take the full grid) */
 } tomo_op_info;
 
 const char* tomo_last_error(void);
@@ -136,6 +141,9 @@ int tomo_apply_normal(tomo_op* op, const void* in, void* out, int batch, void* s
 int tomo_apply_normal_real(tomo_op* op, const void* in, void* out, int batch, void* stream);
 /* SliceTransform::forward (type-2, fourier_slice.hpp:43): complex image n^2 -> samples P. */
 int tomo_forward(tomo_op* op, const void* image, void* samples, int batch, void* stream);
+/* forward_transform (fourier_slice.cpp:61-64): type-2 of a REAL image n^2 -> complex samples P
+ * (the image's Hermitian spectrum: half the grid rows are transformed). */
+int tomo_forward_real(tomo_op* op, const void* image, void* samples, int batch, void* stream);
 /* SliceTransform::adjoint (type-1, fourier_slice.hpp:46): complex samples P -> image n^2. */
 int tomo_adjoint(tomo_op* op, const void* samples, void* image, int batch, void* stream);
 /* interpolate (W, nufft.hpp:66) / spread (W^T, nufft.hpp:62) alone, on the op's internal
@@ -240,14 +248,15 @@ int tomo_fft_rows(int m, int rows, int precision, const void* in, void* out, int
 /* Stage profiler (measurement, not part of the reference API): runs `reps` solver steps of
  * the op's hot path on internal scratch with CUDA events between kernels on `stream` and
  * returns, per stage, the mean device time (ms) and the algorithmic HBM bytes one launch
- * moves. Stage ids:
+ * moves. complex_io = 0: the solvers' real-image path (the
+ * Hermitian half grid where available); 1: complex applies (complex in, complex out). Stage ids:
  *   0 t2_rows (P1: p-update + deapod + pad + row iFFT)   1 t2_cols (P2: column iFFT)
  *   2 w (W SELL-32 SpMV)   3 wt_spread (W^T task SpMV + split-block fix-up)
  *   4 t1_cols (PA: grid-row FFT, pruned)   5 t1_rows (PB: FFT + crop + deapod + CG epilogue)
  *   6 cg_update   7 sb_post   8 stencil (surrogate T + K'K + CG dots)
  * Stages that do not apply to the backend report 0. Returns TOMO_OK. */
 #define TOMO_NUM_STAGES 9
-int tomo_profile_stages(tomo_op* op, int batch, int reps, double* ms, double* bytes, void* stream);
+int tomo_profile_stages(tomo_op* op, int batch, int reps, int complex_io, double* ms, double* bytes, void* stream);
 
 /* Number of library kernels launched since load (for the bench's gpu_launches claim). */
 int64_t tomo_kernel_launches(void);

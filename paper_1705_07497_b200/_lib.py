@@ -46,7 +46,8 @@ class OpInfo(C.Structure):
                 ("wt_slots", C.c_int64), ("bytes_w", C.c_int64), ("bytes_wt", C.c_int64),
                 ("stencil", C.c_double * 81), ("surrogate_r", C.c_int), ("precision", C.c_int),
                 ("backend", C.c_int), ("gram_nnz", C.c_int64), ("gram_slots", C.c_int64),
-                ("bytes_gram", C.c_int64)]
+                ("bytes_gram", C.c_int64), ("herm_nnz", C.c_int64), ("herm_slots", C.c_int64),
+                ("herm_touched", C.c_int64), ("herm_tasks", C.c_int)]
 
 
 class System(C.Structure):
@@ -95,6 +96,7 @@ EXPORTS = {
     "tomo_apply_normal": (C.c_int, [VP, VP, VP, C.c_int, VP]),
     "tomo_apply_normal_real": (C.c_int, [VP, VP, VP, C.c_int, VP]),
     "tomo_forward": (C.c_int, [VP, VP, VP, C.c_int, VP]),
+    "tomo_forward_real": (C.c_int, [VP, VP, VP, C.c_int, VP]),
     "tomo_adjoint": (C.c_int, [VP, VP, VP, C.c_int, VP]),
     "tomo_spmv_w": (C.c_int, [VP, VP, VP, C.c_int, VP]),
     "tomo_spmv_wt": (C.c_int, [VP, VP, VP, C.c_int, VP]),
@@ -113,7 +115,7 @@ EXPORTS = {
     "tomo_shepp_logan": (C.c_int, [C.c_int, VP]),
     "tomo_random_ellipses": (C.c_int, [C.c_int, C.c_int, C.c_uint64, VP]),
     "tomo_fft_rows": (C.c_int, [C.c_int, C.c_int, C.c_int, VP, VP, C.c_int, VP]),
-    "tomo_profile_stages": (C.c_int, [VP, C.c_int, C.c_int, VP, VP, VP]),
+    "tomo_profile_stages": (C.c_int, [VP, C.c_int, C.c_int, C.c_int, VP, VP, VP]),
 }
 
 

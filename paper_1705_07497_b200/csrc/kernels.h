@@ -81,11 +81,21 @@ struct OpDev {
   int n_slots;
   cplx<R>* wt_part;                // B x n_slots x 32 partial sums of split blocks
   cplx<R>* Gt;                     // B x m x m  spread grid [iy][ix]; untouched nodes stay 0
+  cplx<R>* Gth;                    // B x m x m  the folded spread grid, rows [0, m/2] (herm_out; own buffer)
   cplx<R>* H;                      // B x m x n  (type-2 row pass output, [iy][t1])
   cplx<R>* g;                      // B x m x m  (oversampled spatial grid, [iy][ix])
   cplx<R>* s;                      // B x P      (slice samples)
   cplx<R>* K;                      // B x n x m  (type-1 row pass output, [t1][iy])
   TaskSpmv<R> gram;                // fused backend: W^T W on the grid (n_tasks == 0 if not built)
+  // Real-subspace ("Hermitian") pipeline, selected per call: a real input image has a Hermitian
+  // spectrum, so type-2 keeps only grid rows iy in [0, m/2] (P1 transforms two real image rows
+  // as one complex row, P2 runs m/2 + 1 rows, W reads row -iy as the conjugate of row iy); a
+  // real-part output needs only the Hermitian part of the spread grid, so type-1 applies the
+  // folded W^T (wth) onto rows [0, m/2], PA runs m/2 + 1 rows and PB transforms two image rows
+  // per complex row (Hermitian extension on load).
+  TaskSpmv<R> wth;                 // W^T folded onto rows [0, m/2] (entry .j bit 31 = conjugate)
+  int herm_in;                     // type-2 of a real image through the half grid
+  int herm_out;                    // type-1 real-part output through the folded half grid
 
   TaskSpmv<R> wt_view() const {
     return TaskSpmv<R>{wt_ent, wt_tasks, n_tasks, wt_perm, wt_heavy, wt_slot_heavy, wt_heavy_cnt, n_heavy, n_slots,
@@ -219,6 +229,7 @@ struct GpuBuildSizes {
   int64_t chunks = 0;   // W^T chunks (slots / 32)
   int n_tasks = 0, n_slots = 0, n_heavy = 0;
   int64_t touched = 0;  // non-empty W^T rows
+  int64_t nnz = 0;      // entries
 };
 struct GpuBuild;
 bool wt_row_order(int m);  // W^T warp-task order (opbuild.cu)
@@ -239,9 +250,15 @@ GpuBuild* gpu_build_gram_begin(int m, int w, int64_t P, const int* h_base, const
                                cudaStream_t st, GpuBuildSizes* sizes, int64_t* nnz_out);
 // Re-order the separable W tables (base, wx, wy; [Ppad] / [w][Ppad]) by 16x16 grid tile of the
 // window base; perm[t] = sample stored at position t.
+// ent / ent2: W^T entry streams whose sample indices are remapped to positions (bit 31, the
+// Hermitian fold's conj flag, is kept).
 template <typename R>
 void gpu_sort_w_tables(int m, int64_t P, int64_t Ppad, int w, int* base, R* wx, R* wy, int* perm, WtEnt<R>* ent,
-                       int64_t n_ent, cudaStream_t st);
+                       int64_t n_ent, WtEnt<R>* ent2, int64_t n_ent2, cudaStream_t st);
+// Hermitian fold of a finished (unfolded) W^T build: nodes of grid rows [0, m/2], each with its own
+// entries and the conjugated entries of its mirror node (-iy, -ix). Finish with gpu_build_finish.
+template <typename R>
+GpuBuild* gpu_build_fold(const GpuBuild* src, cudaStream_t st, GpuBuildSizes* sizes);
 
 // ---- launchers (solver.cu) ----
 struct StencilCoef {

@@ -181,9 +181,100 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F3
   store_transposed<S::STRIDE>(sm, rpc, min(rpc, n - t10), M, H + t10, static_cast<size_t>(n));
 }
 
+// P1 for a real image (real input or the real CG vectors): image rows 2q and 2q+1 are
+// transformed together as the one complex row a + ib; their spectra are separated on the
+// transposed store, A[k] = (Z[k] + conj Z[-k]) / 2, B[k] = (Z[k] - conj Z[-k]) / 2i, and only
+// the rows iy in [0, m/2] of H are written (H[-iy] = conj H[iy]). IN: 1 real input, 2 standard
+// CG p-update, 3 Chronopoulos-Gear update (as k_t2_rows; applied to both rows of the pair).
+template <int M, int RB, typename R, bool HALF, int IN>
+__global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F32 : TOMO_FFT_MINB_F64)
+k_t2_rows_pk(OpDev<R> d, const void* __restrict__ in, PUpd<R> pu, int rpc) {
+  using S = FftShape<M, RB>;
+  using C2 = cplx<R>;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  C2* sm = reinterpret_cast<C2*>(smraw);
+  const int b = blockIdx.y;
+  double beta = 0.0, alpha = 0.0;
+  if constexpr (IN == 3) {
+    const SliceScalars& sc = pu.red.sc[b];
+    if (sc.done || sc.frozen) return;
+    beta = sc.cg_beta;
+    alpha = sc.cg_alpha;
+  } else if constexpr (IN == 2) {
+    if (!cg_step_live(pu.red, b, pu.step, beta)) return;
+  } else {
+    if (pu.red.sc && pu.red.sc[b].frozen) return;
+  }
+  const int rr = threadIdx.x / S::T, t = threadIdx.x % S::T;
+  const int n = d.n, npair = n >> 1;
+  const int q0 = blockIdx.x * rpc;
+  const int q = q0 + rr;
+  const bool active = rr < rpc && q < npair;
+  C2* row = sm + rr * S::STRIDE;
+  const size_t base = (static_cast<size_t>(b) * n + (active ? 2 * q : 0)) * n;  // row 2q; row 2q+1 at + n
+  const R a1a = active ? d.apod[2 * q] : R(0), a1b = active ? d.apod[2 * q + 1] : R(0);
+  const R bt = static_cast<R>(beta), al = static_cast<R>(alpha);
+  auto value = [&](size_t o) -> R {
+    if constexpr (IN == 3) {
+      R rv = pu.r[o];
+      if (pu.step > 0) {
+        R pv = rv, sv = pu.w[o];
+        if (pu.step > 1) {
+          pv += bt * pu.p[o];
+          sv += bt * pu.s[o];
+        }
+        const R xv = pu.x[o] + al * pv;
+        rv -= al * sv;
+        pu.p[o] = pv;
+        pu.s[o] = sv;
+        pu.x[o] = xv;
+        pu.r[o] = rv;
+        if (!finite_r(xv)) pu.red.sc[b].nonfinite = 1;
+      }
+      return rv;
+    } else if constexpr (IN == 2) {
+      R pv = pu.p[o];
+      if (pu.step > 0) {
+        pv = pu.r[o] + bt * pv;
+        pu.p[o] = pv;
+      }
+      return pv;
+    } else {
+      return reinterpret_cast<const R*>(in)[o];
+    }
+  };
+  auto load = [&](int i) -> C2 {
+    const int t2 = (i + n / 2) & (M - 1);
+    C2 v = czero<C2>();
+    if (t2 < n) {
+      const R ap = __ldg(&d.apod[t2]);
+      const R va = value(base + t2) * (a1a * ap);
+      const R vb = value(base + n + t2) * (a1b * ap);
+      v = mk<C2>(va, -vb);  // inverse transform: conj in, conj out
+    }
+    return v;
+  };
+  auto store = [&](int k, C2 v) { row[pad16(k)] = cconj(v); };
+  fft_row<M, RB, true, C2, HALF ? 1 : 0>(row, d.tw, t, active, load, store);
+  // separate the two spectra; transposed store H[b][k][t1] for k in [0, M/2], 2 rpc consecutive t1
+  const int ncols = 2 * max(0, min(rpc, npair - q0));
+  const int w2 = 2 * rpc, lg = __ffs(w2) - 1;
+  C2* H = d.H + static_cast<size_t>(b) * M * n + 2 * q0;
+  const R h = R(0.5);
+  for (int idx = threadIdx.x; idx < ((M / 2 + 1) << lg); idx += blockDim.x) {
+    const int k = idx >> lg, c = idx & (w2 - 1);
+    if (c < ncols) {
+      const C2* rw = sm + (c >> 1) * S::STRIDE;
+      const C2 z = rw[pad16(k)], zm = rw[pad16((M - k) & (M - 1))];
+      H[static_cast<size_t>(k) * n + c] = (c & 1) ? mk<C2>(h * (z.y + zm.y), h * (zm.x - z.x))
+                                                  : mk<C2>(h * (z.x + zm.x), h * (z.y - zm.y));
+    }
+  }
+}
+
 // ---------------------------------------------------------------- P2: grid rows (iy)
 template <int M, int RB, typename R, bool HALF = false>
-__global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F32 : TOMO_FFT_MINB_F64) k_t2_cols(OpDev<R> d, int rpc, const SliceScalars* skip) {
+__global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F32 : TOMO_FFT_MINB_F64) k_t2_cols(OpDev<R> d, int rpc, int nrows, const SliceScalars* skip) {
   using S = FftShape<M, RB>;
   using C2 = cplx<R>;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -193,7 +284,7 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F3
   const int rr = threadIdx.x / S::T, t = threadIdx.x % S::T;
   const int n = d.n;
   const int iy = blockIdx.x * rpc + rr;
-  const bool active = rr < rpc;
+  const bool active = rr < rpc && iy < nrows;  // nrows: m, or m/2 + 1 rows of a Hermitian spectrum
   C2* row = sm + rr * S::STRIDE;
   const C2* H = d.H + (static_cast<size_t>(b) * M + (active ? iy : 0)) * n;
   C2* g = d.g + (static_cast<size_t>(b) * M + (active ? iy : 0)) * M;
@@ -209,7 +300,9 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F3
 // Same matrix as k_w, stored as its rank-1 blocks: per row j the base node (ix0, iy0) and the
 // two window factor vectors (SoA, coalesced): 4 + 2w*sizeof(R) bytes per row instead of
 // w^2*(4 + sizeof(R)). The inner loop walks a grid row (b fixed, ix0+a consecutive).
-template <int BT, int WMAX, int RU, typename R, bool BY = false>  // BY: slice groups across grid.y
+// HERM: the grid holds rows iy in [0, m/2] of a Hermitian spectrum (real image); row iy > m/2 is
+// read as the conjugate of row m - iy at mirrored columns.
+template <int BT, int WMAX, int RU, typename R, bool BY = false, bool HERM = false>  // BY: slice groups across grid.y
 __global__ void __launch_bounds__(256) k_w_sep(OpDev<R> d, int B, const cplx<R>* __restrict__ grid,
                                                 cplx<R>* __restrict__ out, const SliceScalars* skip) {
   using C2 = cplx<R>;
@@ -242,8 +335,10 @@ __global__ void __launch_bounds__(256) k_w_sep(OpDev<R> d, int B, const cplx<R>*
         const int bb = bb0 + k;
         if (bb < w) {
           const R wyv = __ldg(&d.w_y[static_cast<size_t>(bb) * d.Ppad + t]);
-          const int u = iy0 + bb;
-          const size_t rowoff = static_cast<size_t>(u >= m ? u - m : u) * m;
+          const int u0 = iy0 + bb;
+          const int u = u0 >= m ? u0 - m : u0;
+          const bool mir = HERM && u > (m >> 1);
+          const size_t rowoff = static_cast<size_t>(mir ? m - u : u) * m;
 #pragma unroll
           for (int q = 0; q < BT; ++q) {
             if (b0 + q < B) {
@@ -252,11 +347,12 @@ __global__ void __launch_bounds__(256) k_w_sep(OpDev<R> d, int B, const cplx<R>*
 #pragma unroll
               for (int a = 0; a < WMAX; ++a) {
                 if (a < w) {
-                  const C2 gv = row[ix[a]];
+                  const C2 gv = row[mir ? ((m - ix[a]) & (m - 1)) : ix[a]];
                   ra.x += wx[a] * gv.x;
                   ra.y += wx[a] * gv.y;
                 }
               }
+              if (mir) ra.y = -ra.y;  // conj(sum w g) = sum w conj(g)
               acc[q].x += wyv * ra.x;
               acc[q].y += wyv * ra.y;
             }
@@ -289,16 +385,20 @@ __global__ void __launch_bounds__(256) k_w_sep_wide(OpDev<R> d, int B, const cpl
     const C2* gb = grid + G * b;
     C2 acc = czero<C2>();
     for (int bb = 0; bb < w; ++bb) {
-      const int t = iy0 + bb;
-      const C2* row = gb + static_cast<size_t>(t >= m ? t - m : t) * m;
+      const int t0 = iy0 + bb;
+      const int t = t0 >= m ? t0 - m : t0;
+      const bool mir = d.herm_in && t > (m >> 1);
+      const C2* row = gb + static_cast<size_t>(mir ? m - t : t) * m;
       C2 ra = czero<C2>();
       for (int a = 0; a < w; ++a) {
-        const int u = ix0 + a;
+        const int u0 = ix0 + a;
+        const int u = u0 >= m ? u0 - m : u0;
         const R wx = __ldg(&d.w_x[static_cast<size_t>(a) * d.Ppad + tp]);
-        const C2 gv = row[u >= m ? u - m : u];
+        const C2 gv = row[mir ? ((m - u) & (m - 1)) : u];
         ra.x += wx * gv.x;
         ra.y += wx * gv.y;
       }
+      if (mir) ra.y = -ra.y;
       const R wy = __ldg(&d.w_y[static_cast<size_t>(bb) * d.Ppad + tp]);
       acc.x += wy * ra.x;
       acc.y += wy * ra.y;
@@ -316,7 +416,19 @@ __global__ void __launch_bounds__(256) k_w_sep_wide(OpDev<R> d, int B, const cpl
 // BY: slices across grid.y (batched launches with a small task grid); BY = false keeps the
 // in-warp slice loop with fp32's 32 registers (the grid.y form needs 34: 6 instead of 8 CTAs
 // per SM, c3 W^T 31.6 -> 34.6 us)
-template <int GRP, bool PIPE, typename R, bool BY = false>
+// HERM: the Hermitian fold of W^T (entry .j bit 31 = use conj(s_j)).
+template <bool HERM, typename C2>
+__device__ __forceinline__ C2 gather_s(const C2* __restrict__ s, int j) {
+  if constexpr (HERM) {
+    C2 v = __ldg(&s[j & 0x7fffffff]);
+    if (j < 0) v.y = -v.y;
+    return v;
+  } else {
+    return __ldg(&s[j]);
+  }
+}
+
+template <int GRP, bool PIPE, typename R, bool BY = false, bool HERM = false>
 __global__ void __launch_bounds__(256) k_task_spmv(TaskSpmv<R> ts, int m, int B, const cplx<R>* __restrict__ s_all,
                                                     size_t in_stride, cplx<R>* __restrict__ grid,
                                                     const SliceScalars* skip) {
@@ -351,7 +463,7 @@ __global__ void __launch_bounds__(256) k_task_spmv(TaskSpmv<R> ts, int m, int B,
     for (int c = 0; c < nc; c += GRP) {
       C2 v[GRP];
 #pragma unroll
-      for (int k = 0; k < GRP; ++k) v[k] = q[k].w != R(0) ? __ldg(&s[q[k].j]) : czero<C2>();
+      for (int k = 0; k < GRP; ++k) v[k] = q[k].w != R(0) ? gather_s<HERM>(s, q[k].j) : czero<C2>();
       WtEnt<R> qn[GRP];
 #pragma unroll
       for (int k = 0; k < GRP; ++k) {
@@ -387,7 +499,7 @@ __global__ void __launch_bounds__(256) k_task_spmv(TaskSpmv<R> ts, int m, int B,
         }
       }
 #pragma unroll
-      for (int k = 0; k < GRP; ++k) v[k] = q[k].w != R(0) ? __ldg(&s[q[k].j]) : czero<C2>();
+      for (int k = 0; k < GRP; ++k) v[k] = q[k].w != R(0) ? gather_s<HERM>(s, q[k].j) : czero<C2>();
 #pragma unroll
       for (int k = 0; k < GRP; k += 2) {
         a0.x += q[k].w * v[k].x;
@@ -427,7 +539,7 @@ __global__ void __launch_bounds__(256) k_task_spmv(TaskSpmv<R> ts, int m, int B,
 // ---------------------------------------------------------------- PA: grid rows (iy), type 1
 // forward FFT along ix of the spread grid row, pruned to the n bins, transposed to K[t1][iy].
 template <int M, int RB, typename R, bool HALF = false>
-__global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F32 : TOMO_FFT_MINB_F64) k_t1_cols(OpDev<R> d, int rpc, const SliceScalars* skip) {
+__global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F32 : TOMO_FFT_MINB_F64) k_t1_cols(OpDev<R> d, int rpc, int nrows, const SliceScalars* skip) {
   using S = FftShape<M, RB>;
   using C2 = cplx<R>;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -437,7 +549,7 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F3
   const int n = d.n;
   const int iy0 = blockIdx.x * rpc;
   const int rr = threadIdx.x / S::T, t = threadIdx.x % S::T;
-  const bool active = rr < rpc;
+  const bool active = rr < rpc && iy0 + rr < nrows;
   C2* row = sm + rr * S::STRIDE;
   const C2* Gr = d.Gt + (static_cast<size_t>(b) * M + iy0 + (active ? rr : 0)) * M;
   auto load = [&](int i) -> C2 { return Gr[i]; };
@@ -447,7 +559,7 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F3
   };
   fft_row<M, RB, true, C2, HALF ? 2 : 0>(row, d.tw, t, active, load, store);
   C2* K = d.K + static_cast<size_t>(b) * n * M;
-  store_transposed<S::STRIDE>(sm, rpc, rpc, n, K + iy0, static_cast<size_t>(M));
+  store_transposed<S::STRIDE>(sm, rpc, min(rpc, nrows - iy0), n, K + iy0, static_cast<size_t>(M));
 }
 
 template <typename R>
@@ -577,6 +689,101 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F3
   }
 }
 
+// PB for a real-part output from a Hermitian K (rows iy in [0, m/2] stored, K[t1][-iy] =
+// conj K[t1][iy]): image rows 2q and 2q+1 as the one complex row Xa + i Xb (Hermitian extension
+// on load), whose transform is xa + i xb with both real. The folded W^T computed twice the
+// Hermitian part of the spread grid: the 1/2 is folded into the deapodisation. EPI: 1 real
+// output, 2 the CG modes (as k_t1_rows, per row of the pair).
+template <int M, int RB, typename R, bool HALF, int EPI>
+__global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F32 : TOMO_FFT_MINB_F64)
+k_t1_rows_pk(OpDev<R> d, PbEpi<R> e, int rpc) {
+  using S = FftShape<M, RB>;
+  using C2 = cplx<R>;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  C2* sm = reinterpret_cast<C2*>(smraw);
+  __shared__ double red_scratch[32];
+  const int b = blockIdx.y;
+  if ((e.mode == PB_CG_STEP || e.mode == PB_CGCG) && (e.red.sc[b].done || e.red.sc[b].frozen)) return;
+  if (e.mode == PB_CG_INIT && e.red.sc[b].frozen) return;
+  const int n = d.n, npair = n >> 1;
+  const int rr = threadIdx.x / S::T, t = threadIdx.x % S::T;
+  const int q = blockIdx.x * rpc + rr;
+  const bool active = rr < rpc && q < npair;
+  const int ta = active ? 2 * q : 0;
+  C2* row = sm + rr * S::STRIDE;
+  const C2* Ka = d.K + (static_cast<size_t>(b) * n + ta) * M;
+  const C2* Kb = Ka + M;
+  const R a1a = active ? d.apod[ta] * e.scale * R(0.5) : R(0);
+  const R a1b = active ? d.apod[ta + 1] * e.scale * R(0.5) : R(0);
+  const size_t base = (static_cast<size_t>(b) * n + ta) * n;  // row ta; row ta+1 at + n
+  const R lam = static_cast<R>(e.sys.lambda), shift = static_cast<R>(e.sys.shift);
+  const R* p = e.p ? e.p + static_cast<size_t>(b) * n * n : nullptr;
+  double acc0 = 0.0, acc1 = 0.0;
+  auto load = [&](int k) -> C2 {
+    C2 xa, xb;
+    if (k <= M / 2) {
+      xa = Ka[k];
+      xb = Kb[k];
+    } else {
+      xa = cconj(Ka[M - k]);
+      xb = cconj(Kb[M - k]);
+    }
+    return mk<C2>(xa.x - xb.y, xa.y + xb.x);  // xa + i xb
+  };
+  auto epi = [&](int t1, size_t o, int t2, R v) {
+    if constexpr (EPI == 1) {
+      e.out_r[o] = v;
+    } else {
+      const R pv = p[static_cast<size_t>(t1) * n + t2];
+      R ax = v;
+      if (lam != R(0)) ax += lam * ktk_at<R>(p, n, t1, t2, pv);
+      ax += shift * pv;
+      if (e.mode != PB_CG_INIT) {
+        e.ap[o] = ax;
+        acc0 += static_cast<double>(pv) * ax;
+        acc1 += static_cast<double>(pv) * pv;
+      } else {
+        const R bv = e.b[o];
+        const R rv = bv - ax;
+        e.ap[o] = rv;
+        e.p_out[o] = rv;
+        e.x_out[o] = pv;
+        acc0 += static_cast<double>(rv) * rv;
+        acc1 += static_cast<double>(bv) * bv;
+      }
+    }
+  };
+  auto store = [&](int k, C2 X) {
+    const int t2 = (k + n / 2) & (M - 1);
+    if (t2 >= n) return;
+    const R ap = __ldg(&d.apod[t2]);
+    epi(ta, base + t2, t2, X.x * (a1a * ap));
+    epi(ta + 1, base + n + t2, t2, X.y * (a1b * ap));
+  };
+  fft_row<M, RB, false, C2, HALF ? 2 : 0>(row, d.tw, t, active, load, store);
+  if (EPI == 2) {
+    double t0s, t1s;
+    SliceScalars& sc = e.red.sc[b];
+    double* part = e.red.part + static_cast<size_t>(b) * MAX_PART_BLOCKS * 2;
+    if (reduce2_last(acc0, acc1, part, gridDim.x, blockIdx.x, &sc.counter[0], red_scratch, t0s, t1s) &&
+        threadIdx.x == 0) {
+      if (e.mode == PB_CGCG) {
+        cgcg_finalize(sc, t0s, t1s, e.sys, e.step);
+      } else if (e.mode == PB_CG_STEP) {
+        sc.pap = t0s;
+        sc.pp = t1s;
+      } else {
+        sc.rr[0] = t0s;
+        sc.rs_last = t0s;
+        sc.bb = t1s;
+        sc.done = 0;
+        sc.steps_run = 0;
+        sc.min_ritz = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+      }
+    }
+  }
+}
+
 // ================================================================ persistent FFT-row kernels
 // Grid (CTAs per slice, B). Each CTA walks its slice's rows g = blockIdx.x, blockIdx.x +
 // gridDim.x, ... (rpc rows per step). The next step's input rows are copied global -> smem
@@ -592,7 +799,7 @@ TOMO_DEV void async_copy(C2* dst_smem, const C2* src) {
 // P2: inverse FFT along ix of H rows (t1 at the n bins), natural store g[iy][ix].
 template <int M, int RB, typename R>
 __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F32 : TOMO_FFT_MINB_F64)
-k_t2_cols_p(OpDev<R> d, const SliceScalars* skip) {
+k_t2_cols_p(OpDev<R> d, int nrows, const SliceScalars* skip) {
   using S = FftShape<M, RB>;
   using C2 = cplx<R>;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -608,9 +815,9 @@ k_t2_cols_p(OpDev<R> d, const SliceScalars* skip) {
     for (int k = t; k < n; k += S::T) async_copy(&stage[k], &H[k]);
   };
   int iy = blockIdx.x;
-  if (iy < M) issue(iy);
+  if (iy < nrows) issue(iy);
   __pipeline_commit();
-  for (; iy < M; iy += gridDim.x) {
+  for (; iy < nrows; iy += gridDim.x) {
     __pipeline_wait_prior(0);
     __syncthreads();
     C2 pre[RB];
@@ -620,7 +827,7 @@ k_t2_cols_p(OpDev<R> d, const SliceScalars* skip) {
       pre[r] = t1 < n ? cconj(stage[t1]) : czero<C2>();
     }
     __syncthreads();  // staging consumed by every thread
-    if (iy + static_cast<int>(gridDim.x) < M) issue(iy + gridDim.x);
+    if (iy + static_cast<int>(gridDim.x) < nrows) issue(iy + gridDim.x);
     __pipeline_commit();
     C2* gout = gb + static_cast<size_t>(iy) * M;
     fft_row_pre<M, RB, false, C2>(row, d.tw, t, true, pre, [&](int k, C2 v) { gout[k] = cconj(v); });
@@ -631,7 +838,7 @@ k_t2_cols_p(OpDev<R> d, const SliceScalars* skip) {
 // PA: forward FFT of rpc spread-grid rows, pruned to the n bins, transposed store K[t1][iy].
 template <int M, int RB, typename R>
 __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F32 : TOMO_FFT_MINB_F64)
-k_t1_cols_p(OpDev<R> d, int rpc, const SliceScalars* skip) {
+k_t1_cols_p(OpDev<R> d, int rpc, int nrows, const SliceScalars* skip) {
   using S = FftShape<M, RB>;
   using C2 = cplx<R>;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -642,7 +849,7 @@ k_t1_cols_p(OpDev<R> d, int rpc, const SliceScalars* skip) {
   const int n = d.n;
   const int rr = threadIdx.x / S::T, t = threadIdx.x % S::T;
   C2* row = sm + rr * S::STRIDE;
-  const int steps = M / rpc;
+  const int steps = (nrows + rpc - 1) / rpc;  // the last step's staging may cover rows >= nrows (not stored)
   const C2* Gb = d.Gt + static_cast<size_t>(b) * M * M;
   C2* K = d.K + static_cast<size_t>(b) * n * M;
   auto issue = [&](int st) {
@@ -666,7 +873,7 @@ k_t1_cols_p(OpDev<R> d, int rpc, const SliceScalars* skip) {
       const int t1 = (k + n / 2) & (M - 1);  // inverse of bin_of
       if (t1 < n) row[pad16(t1)] = v;
     });
-    store_transposed<S::STRIDE>(sm, rpc, rpc, n, K + iy0, static_cast<size_t>(M));
+    store_transposed<S::STRIDE>(sm, rpc, min(rpc, nrows - iy0), n, K + iy0, static_cast<size_t>(M));
   }
   __pipeline_wait_prior(0);
 }
@@ -912,6 +1119,33 @@ void set_smem(K kernel, size_t bytes) {
 
 template <typename R>
 void launch_t2_rows(const OpDev<R>& d, int B, const void* in, bool in_complex, const PUpd<R>& pu, cudaStream_t st) {
+  if (d.herm_in && !in_complex) {  // real image: two rows per complex transform, H rows [0, m/2]
+    dispatch_m_rows(d.m, sizeof(cplx<R>), [&](auto MC, auto RC) {
+      constexpr int M = decltype(MC)::value, RB = decltype(RC)::value;
+      using S = FftShape<M, RB>;
+      // 2 rpc t1 values per H row segment: >= 32 B segments need rpc >= 16 / sizeof(C2)
+      const int rpc = choose_rpc(S::T, M, d.n / 2, B, 2 * sizeof(cplx<R>), true);
+      const size_t smem = static_cast<size_t>(rpc) * S::STRIDE * sizeof(cplx<R>);
+      dim3 grid((d.n / 2 + rpc - 1) / rpc, B);
+      auto go = [&](auto kern) {
+        set_smem(kern, smem);
+        CK_LAUNCH(launch_k(kern, grid, rpc * S::T, smem, st, d, in, pu, rpc));
+      };
+      const int mode = !pu.enabled ? 1 : pu.cgcg ? 3 : 2;
+      auto go_mode = [&](auto HC) {
+        constexpr bool H = decltype(HC)::value;
+        switch (mode) {
+          case 1: go(k_t2_rows_pk<M, RB, R, H, 1>); break;
+          case 2: go(k_t2_rows_pk<M, RB, R, H, 2>); break;
+          default: go(k_t2_rows_pk<M, RB, R, H, 3>); break;
+        }
+      };
+      if (2 * d.n == M) go_mode(std::true_type{});
+      else go_mode(std::false_type{});
+      note_launch();
+    });
+    return;
+  }
   dispatch_m_rows(d.m, sizeof(cplx<R>), [&](auto MC, auto RC) {
     constexpr int M = decltype(MC)::value, RB = decltype(RC)::value;
     using S = FftShape<M, RB>;
@@ -966,17 +1200,18 @@ void launch_t2_cols(const OpDev<R>& d, int B, const SliceScalars* skip, cudaStre
   dispatch_m_cols(d.m, sizeof(cplx<R>), [&](auto MC, auto RC) {
     constexpr int M = decltype(MC)::value, RB = decltype(RC)::value;
     using S = FftShape<M, RB>;
+    const int nrows = d.herm_in ? M / 2 + 1 : M;  // Hermitian spectrum: rows [0, m/2]
     if constexpr (M >= kPersistMinM) {
       const size_t smem = (static_cast<size_t>(S::STRIDE) + d.n) * sizeof(cplx<R>);
       set_smem(k_t2_cols_p<M, RB, R>, smem);
-      const int ctas = persistent_ctas(k_t2_cols_p<M, RB, R>, S::T, smem, M, B);
-      CK_LAUNCH(launch_k(k_t2_cols_p<M, RB, R>, dim3(ctas, B), S::T, smem, st, d, skip));
+      const int ctas = persistent_ctas(k_t2_cols_p<M, RB, R>, S::T, smem, nrows, B);
+      CK_LAUNCH(launch_k(k_t2_cols_p<M, RB, R>, dim3(ctas, B), S::T, smem, st, d, nrows, skip));
     } else {
-      const int rpc = choose_rpc(S::T, M, M, B, sizeof(cplx<R>), false);
+      const int rpc = choose_rpc(S::T, M, nrows, B, sizeof(cplx<R>), false);
       const size_t smem = static_cast<size_t>(rpc) * S::STRIDE * sizeof(cplx<R>);
       auto go = [&](auto kern) {
         set_smem(kern, smem);
-        CK_LAUNCH(launch_k(kern, dim3(M / rpc, B), rpc * S::T, smem, st, d, rpc, skip));
+        CK_LAUNCH(launch_k(kern, dim3((nrows + rpc - 1) / rpc, B), rpc * S::T, smem, st, d, rpc, nrows, skip));
       };
       if (2 * d.n == M) go(k_t2_cols<M, RB, R, true>);
       else go(k_t2_cols<M, RB, R, false>);
@@ -1006,15 +1241,23 @@ void launch_w(const OpDev<R>& d, int B, const cplx<R>* grid, cplx<R>* samples, c
     // compile-time window bound: registers scale with it (6/7 are the configs' windows)
     // one grid row (w gathers) per step: rows-in-flight 1, 2, 3 and w measured equal on B200
     // (c2 8.8-9.2 us, c3 16-19 us); 1 needs the fewest registers
-    auto go = [&](auto WC) {
+    auto go2 = [&](auto WC, auto HC) {
       constexpr int WM = decltype(WC)::value;
+      constexpr bool HM = decltype(HC)::value;
       const unsigned ydim = batch_ydim(blocks, (B + 1) / 2);
       if (B >= 2 && ydim > 1)
-        CK_LAUNCH(launch_k(k_w_sep<2, WM, 1, R, true>, dim3(blocks, ydim), threads, 0, st, d, B, grid, samples, skip));
+        CK_LAUNCH(launch_k(k_w_sep<2, WM, 1, R, true, HM>, dim3(blocks, ydim), threads, 0, st, d, B, grid, samples,
+                           skip));
       else if (B >= 2)
-        CK_LAUNCH(launch_k(k_w_sep<2, WM, 1, R>, blocks, threads, 0, st, d, B, grid, samples, skip));
+        CK_LAUNCH(launch_k(k_w_sep<2, WM, 1, R, false, HM>, blocks, threads, 0, st, d, B, grid, samples, skip));
       else
-        CK_LAUNCH(launch_k(k_w_sep<1, WM, 1, R>, blocks, threads, 0, st, d, B, grid, samples, skip));
+        CK_LAUNCH(launch_k(k_w_sep<1, WM, 1, R, false, HM>, blocks, threads, 0, st, d, B, grid, samples, skip));
+    };
+    auto go = [&](auto WC) {
+      if (d.herm_in)
+        go2(WC, std::true_type{});
+      else
+        go2(WC, std::false_type{});
     };
     if (d.w <= 6)
       go(std::integral_constant<int, 6>{});
@@ -1028,7 +1271,7 @@ void launch_w(const OpDev<R>& d, int B, const cplx<R>* grid, cplx<R>* samples, c
 
 template <typename R>
 void launch_task_spmv(const TaskSpmv<R>& ts, int m, int B, const cplx<R>* x, size_t in_stride, cplx<R>* grid,
-                      const SliceScalars* skip, cudaStream_t st) {
+                      const SliceScalars* skip, cudaStream_t st, bool herm = false) {
   if (ts.n_tasks <= 0) return;
   const int threads = 256;
   const int blocks = (ts.n_tasks * 32 + threads - 1) / threads;
@@ -1046,6 +1289,16 @@ void launch_task_spmv(const TaskSpmv<R>& ts, int m, int B, const cplx<R>* x, siz
     else
       CK_LAUNCH(launch_k(kern, blocks, threads, 0, st, ts, m, B, x, in_stride, grid, skip));
   };
+  if (herm) {  // the folded W^T: the default group depth / pipelining only
+    if constexpr (sizeof(R) == 4) {
+      go(k_task_spmv<6, false, R, false, true>, k_task_spmv<6, false, R, true, true>);
+    } else {
+      if (pipe) go(k_task_spmv<4, true, R, false, true>, k_task_spmv<4, true, R, true, true>);
+      else go(k_task_spmv<4, false, R, false, true>, k_task_spmv<4, false, R, true, true>);
+    }
+    note_launch();
+    return;
+  }
   if constexpr (sizeof(R) == 4) {
     if (pipe && grp == 4) go(k_task_spmv<4, true, R>, k_task_spmv<4, true, R, true>);
     else if (pipe) go(k_task_spmv<6, true, R>, k_task_spmv<6, true, R, true>);
@@ -1062,7 +1315,10 @@ void launch_task_spmv(const TaskSpmv<R>& ts, int m, int B, const cplx<R>* x, siz
 template <typename R>
 void launch_wt_spread(const OpDev<R>& d, int B, const cplx<R>* samples, cplx<R>* grid, const SliceScalars* skip,
                       cudaStream_t st) {
-  launch_task_spmv<R>(d.wt_view(), d.m, B, samples, static_cast<size_t>(d.P), grid, skip, st);
+  if (d.herm_out)
+    launch_task_spmv<R>(d.wth, d.m, B, samples, static_cast<size_t>(d.P), grid, skip, st, true);
+  else
+    launch_task_spmv<R>(d.wt_view(), d.m, B, samples, static_cast<size_t>(d.P), grid, skip, st);
 }
 
 template <typename R>
@@ -1082,6 +1338,7 @@ void launch_t1_cols_only(const OpDev<R>& d, int B, const SliceScalars* skip, cud
   dispatch_m_cols(d.m, sizeof(cplx<R>), [&](auto MC, auto RC) {
     constexpr int M = decltype(MC)::value, RB = decltype(RC)::value;
     using S = FftShape<M, RB>;
+    const int nrows = d.herm_out ? M / 2 + 1 : M;  // the folded (Hermitian) grid: rows [0, m/2]
     if constexpr (M >= kPersistMinM) {
       // transposed K stores need >= 32 B per row segment; staging holds rpc full rows
       int rpc = std::max(1, static_cast<int>(32 / sizeof(cplx<R>)));
@@ -1091,18 +1348,18 @@ void launch_t1_cols_only(const OpDev<R>& d, int B, const SliceScalars* skip, cud
       const size_t smem = static_cast<size_t>(rpc) * (S::STRIDE + M) * sizeof(cplx<R>);
       if (smem <= kMaxSmem) {
         set_smem(k_t1_cols_p<M, RB, R>, smem);
-        const int ctas = persistent_ctas(k_t1_cols_p<M, RB, R>, rpc * S::T, smem, M / rpc, B);
-        CK_LAUNCH(launch_k(k_t1_cols_p<M, RB, R>, dim3(ctas, B), rpc * S::T, smem, st, d, rpc, skip));
+        const int ctas = persistent_ctas(k_t1_cols_p<M, RB, R>, rpc * S::T, smem, (nrows + rpc - 1) / rpc, B);
+        CK_LAUNCH(launch_k(k_t1_cols_p<M, RB, R>, dim3(ctas, B), rpc * S::T, smem, st, d, rpc, nrows, skip));
         note_launch();
         return;
       }
     }
     // one-shot CTAs (also when row + staging do not fit: fp64, m = 8192)
-    const int rpc1 = choose_rpc(S::T, M, M, B, sizeof(cplx<R>), true);
+    const int rpc1 = choose_rpc(S::T, M, nrows, B, sizeof(cplx<R>), true);
     const size_t smem1 = static_cast<size_t>(rpc1) * S::STRIDE * sizeof(cplx<R>);
     auto go = [&](auto kern) {
       set_smem(kern, smem1);
-      CK_LAUNCH(launch_k(kern, dim3(M / rpc1, B), rpc1 * S::T, smem1, st, d, rpc1, skip));
+      CK_LAUNCH(launch_k(kern, dim3((nrows + rpc1 - 1) / rpc1, B), rpc1 * S::T, smem1, st, d, rpc1, nrows, skip));
     };
     if (2 * d.n == M) go(k_t1_cols<M, RB, R, true>);
     else go(k_t1_cols<M, RB, R, false>);
@@ -1112,6 +1369,32 @@ void launch_t1_cols_only(const OpDev<R>& d, int B, const SliceScalars* skip, cud
 
 template <typename R>
 void launch_t1_rows(const OpDev<R>& d, int B, const PbEpi<R>& e, cudaStream_t st) {
+  if (d.herm_out) {  // real-part output from the folded grid: two image rows per complex transform
+    if (e.mode == PB_COMPLEX) throw std::runtime_error("launch_t1_rows: complex output from a folded grid");
+    dispatch_m_rows(d.m, sizeof(cplx<R>), [&](auto MC, auto RC) {
+      constexpr int M = decltype(MC)::value, RB = decltype(RC)::value;
+      using S = FftShape<M, RB>;
+      const int np = d.n / 2;
+      int rpc = choose_rpc(S::T, M, np, B, sizeof(cplx<R>), false);
+      while ((rpc * S::T) % 32) rpc <<= 1;
+      while (rpc > 1 && (np + rpc - 1) / rpc > MAX_PART_BLOCKS) rpc <<= 1;
+      const size_t smem = static_cast<size_t>(rpc) * S::STRIDE * sizeof(cplx<R>);
+      dim3 grid((np + rpc - 1) / rpc, B);
+      auto go = [&](auto kern) {
+        set_smem(kern, smem);
+        CK_LAUNCH(launch_k(kern, grid, rpc * S::T, smem, st, d, e, rpc));
+      };
+      auto go_epi = [&](auto HC) {
+        constexpr bool H = decltype(HC)::value;
+        if (e.mode == PB_REAL) go(k_t1_rows_pk<M, RB, R, H, 1>);
+        else go(k_t1_rows_pk<M, RB, R, H, 2>);
+      };
+      if (2 * d.n == M) go_epi(std::true_type{});
+      else go_epi(std::false_type{});
+      note_launch();
+    });
+    return;
+  }
   dispatch_m_rows(d.m, sizeof(cplx<R>), [&](auto MC, auto RC) {
     constexpr int M = decltype(MC)::value, RB = decltype(RC)::value;
     using S = FftShape<M, RB>;

@@ -124,10 +124,9 @@ __global__ void k_plan(BuildArgs a, const double* __restrict__ cs, const double*
 }
 
 // per node: key (iy, count descending, ix) for the per-row stable order; touched-node count
-__global__ void k_node_keys(int m, int maxc, const int* __restrict__ cnt, unsigned long long* keys,
+__global__ void k_node_keys(int m, int64_t G, int maxc, const int* __restrict__ cnt, unsigned long long* keys,
                             unsigned long long* touched) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t G = static_cast<int64_t>(m) * m;
   if (i >= G) return;
   const int iy = static_cast<int>(i / m), ix = static_cast<int>(i % m);
   const int c = cnt[i];
@@ -137,11 +136,10 @@ __global__ void k_node_keys(int m, int maxc, const int* __restrict__ cnt, unsign
 }
 
 // per 32-node block: perm, chunk count L, task / slot / heavy counts
-__global__ void k_blocks(int m, int maxch, const unsigned long long* __restrict__ sorted, const int* __restrict__ cnt,
-                         uint16_t* perm, int* L, int* ntask, int* nslot, int* nheavy) {
+__global__ void k_blocks(int m, int64_t G32, int maxch, const unsigned long long* __restrict__ sorted,
+                         const int* __restrict__ cnt, uint16_t* perm, int* L, int* ntask, int* nslot, int* nheavy) {
   const int64_t bk = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  const int64_t G32 = static_cast<int64_t>(m) * m / 32;
   if (bk >= G32) return;
   const int ix = static_cast<int>(sorted[bk * 32 + lane] & 0xFFFFull);
   perm[bk * 32 + lane] = static_cast<uint16_t>(ix);
@@ -187,12 +185,11 @@ __global__ void k_gather_tasks(int n, const int* __restrict__ idx, const int4* _
 
 // chunk-major entries: block bk, lane l, chunk k < L; padding re-reads the last sample
 template <typename R>
-__global__ void k_entries(int m, const uint16_t* __restrict__ perm, const int* __restrict__ L,
+__global__ void k_entries(int m, int64_t G32, const uint16_t* __restrict__ perm, const int* __restrict__ L,
                           const int64_t* __restrict__ chunk0, const int* __restrict__ cnt, const int* __restrict__ off,
                           const int* __restrict__ sj, const R* __restrict__ svals, WtEnt<R>* ent) {
   const int64_t bk = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  const int64_t G32 = static_cast<int64_t>(m) * m / 32;
   if (bk >= G32) return;
   const int l = L[bk];
   if (!l) return;
@@ -245,6 +242,7 @@ __global__ void k_low32(int64_t n, const unsigned long long* __restrict__ keys, 
 
 struct GpuBuild {
   BuildArgs a{};
+  int rows = 0;  // grid rows of the node set: m, or m/2 + 1 for the Hermitian fold
   int64_t nnz = 0, G = 0, G32 = 0;
   DBuf<int> sj;  // entry columns (sample / grid node) in final entry order
   DBuf<int> cnt, off, L, ntask, nslot, nheavy, toff, soff, hoff, tkey, tkey2, tidx, tidx2;
@@ -319,7 +317,7 @@ void build_structure(GpuBuild* b, cudaStream_t st) {
   const int maxc = 65535;
   DBuf<unsigned long long> nkeys(b->G), nsorted(b->G), touched(1);
   BK(cudaMemsetAsync(touched.p, 0, sizeof(unsigned long long), st));
-  k_node_keys<<<static_cast<unsigned>((b->G + 255) / 256), 256, 0, st>>>(m, maxc, b->cnt.p, nkeys.p, touched.p);
+  k_node_keys<<<static_cast<unsigned>((b->G + 255) / 256), 256, 0, st>>>(m, b->G, maxc, b->cnt.p, nkeys.p, touched.p);
   BK(cudaGetLastError());
   tmp_bytes = 0;
   const int nbits = 32 + bits_for(static_cast<uint64_t>(m));
@@ -332,7 +330,7 @@ void build_structure(GpuBuild* b, cudaStream_t st) {
   b->ntask.alloc(b->G32);
   b->nslot.alloc(b->G32);
   b->nheavy.alloc(b->G32);
-  k_blocks<<<static_cast<unsigned>((b->G32 + 7) / 8), 256, 0, st>>>(m, wt_max_chunks(), nsorted.p, b->cnt.p, b->perm.p,
+  k_blocks<<<static_cast<unsigned>((b->G32 + 7) / 8), 256, 0, st>>>(m, b->G32, wt_max_chunks(), nsorted.p, b->cnt.p, b->perm.p,
                                                                    b->L.p, b->ntask.p, b->nslot.p, b->nheavy.p);
   BK(cudaGetLastError());
   b->chunk0.alloc(b->G32 + 1);
@@ -368,6 +366,7 @@ void build_structure(GpuBuild* b, cudaStream_t st) {
   b->sz.n_slots = s_last + ns_last;
   b->sz.n_heavy = h_last + nh_last;
   b->sz.touched = static_cast<int64_t>(tch);
+  b->sz.nnz = b->nnz;
   if (b->sz.chunks > (int64_t(1) << 31) - 1) throw std::runtime_error("opbuild: W^T too large");
 }
 
@@ -400,13 +399,110 @@ void gpu_build_finish(GpuBuild* b, WtEnt<R>* ent, int4* tasks, uint16_t* perm, i
   }
   BK(cudaMemcpyAsync(perm, b->perm.p, sizeof(uint16_t) * b->G, cudaMemcpyDeviceToDevice, st));
   k_entries<R><<<static_cast<unsigned>((b->G32 + 7) / 8), 256, 0, st>>>(
-      m, b->perm.p, b->L.p, b->chunk0.p, b->cnt.p, b->off.p, b->sj.p,
+      m, b->G32, b->perm.p, b->L.p, b->chunk0.p, b->cnt.p, b->off.p, b->sj.p,
       reinterpret_cast<const R*>(b->vals_sorted.p), ent);
   BK(cudaGetLastError());
   BK(cudaStreamSynchronize(st));
 }
 
 void gpu_build_free(GpuBuild* b) { delete b; }
+
+// ---- Hermitian fold of W^T (real-subspace applies) -------------------------------------------
+// Re(F_NU s) = IFFT2 of the Hermitian part of the spread grid Gt, so a real-output type-1 needs
+// only F[node] = Gt[node] + conj(Gt[-node]) (= 2 x the Hermitian part) on the grid rows
+// iy in [0, m/2]. Entry (node (iy, ix), sample j, w) of W^T contributes w s_j to F[iy][ix] when
+// iy <= m/2 and w conj(s_j) to F[-iy][-ix] when iy >= m/2 or iy == 0 (rows 0 and m/2 are their
+// own mirror rows: both). The conj flag is bit 31 of the entry's sample index.
+namespace {
+__global__ void k_fold_count(int m, int64_t G, const int* __restrict__ cnt, int* ecnt) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= G) return;
+  const int iy = static_cast<int>(i / m);
+  ecnt[i] = cnt[i] * ((iy == 0 || iy == m / 2) ? 2 : 1);
+}
+
+template <typename R>
+__global__ void k_fold_emit(int m, int64_t G, const int* __restrict__ cnt, const int* __restrict__ off,
+                            const int* __restrict__ eoff, const int* __restrict__ sj, const R* __restrict__ vals,
+                            unsigned long long* keys, R* fvals) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= G) return;
+  const int iy = static_cast<int>(i / m), ix = static_cast<int>(i - static_cast<int64_t>(iy) * m);
+  const int c = cnt[i];
+  int o = eoff[i];
+  const unsigned long long mnode =
+      static_cast<unsigned long long>((m - iy) & (m - 1)) * m + static_cast<unsigned long long>((m - ix) & (m - 1));
+  for (int k = 0; k < c; ++k) {
+    const unsigned j = static_cast<unsigned>(sj[off[i] + k]);
+    const R v = vals[off[i] + k];
+    if (iy <= m / 2) {
+      keys[o] = (static_cast<unsigned long long>(i) << 32) | j;
+      fvals[o++] = v;
+    }
+    if (iy >= m / 2 || iy == 0) {
+      keys[o] = (mnode << 32) | 0x80000000ull | j;
+      fvals[o++] = v;
+    }
+  }
+}
+
+__global__ void k_fold_cnt(int64_t n, const unsigned long long* __restrict__ keys, int* cnt) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) atomicAdd(&cnt[keys[i] >> 32], 1);
+}
+}  // namespace
+
+template <typename R>
+GpuBuild* gpu_build_fold(const GpuBuild* src, cudaStream_t st, GpuBuildSizes* sizes) {
+  const int m = src->a.m;
+  if (src->G != static_cast<int64_t>(m) * m) throw std::runtime_error("opbuild: fold needs the unfolded W^T");
+  auto b = std::make_unique<GpuBuild>();
+  b->a = src->a;
+  b->rows = m / 2 + 1;
+  b->G = static_cast<int64_t>(b->rows) * m;
+  b->G32 = b->G / 32;
+  const unsigned gs = static_cast<unsigned>((src->G + 255) / 256);
+  DBuf<int> ecnt(src->G), eoff(src->G);
+  k_fold_count<<<gs, 256, 0, st>>>(m, src->G, src->cnt.p, ecnt.p);
+  BK(cudaGetLastError());
+  size_t tb = 0;
+  BK(cub::DeviceScan::ExclusiveSum(nullptr, tb, ecnt.p, eoff.p, static_cast<int>(src->G), st));
+  {
+    DBuf<unsigned char> tmp(tb);
+    BK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, ecnt.p, eoff.p, static_cast<int>(src->G), st));
+  }
+  int last_off = 0, last_cnt = 0;
+  BK(cudaMemcpyAsync(&last_off, eoff.p + src->G - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  BK(cudaMemcpyAsync(&last_cnt, ecnt.p + src->G - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  BK(cudaStreamSynchronize(st));
+  b->nnz = static_cast<int64_t>(last_off) + last_cnt;
+  if (b->nnz >= (int64_t(1) << 31)) throw std::runtime_error("opbuild: folded W^T too large for 32-bit offsets");
+  DBuf<unsigned long long> keys(b->nnz), skeys(b->nnz);
+  DBuf<R> vals(b->nnz);
+  k_fold_emit<R><<<gs, 256, 0, st>>>(m, src->G, src->cnt.p, src->off.p, eoff.p, src->sj.p,
+                                     reinterpret_cast<const R*>(src->vals_sorted.p), keys.p, vals.p);
+  BK(cudaGetLastError());
+  // (folded node, conj flag, sample): plain entries before conjugated ones, samples ascending
+  b->vals_sorted.alloc(sizeof(R) * b->nnz);
+  const int key_bits = 32 + bits_for(static_cast<uint64_t>(b->G));
+  tb = 0;
+  BK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.p, skeys.p, vals.p, reinterpret_cast<R*>(b->vals_sorted.p),
+                                     static_cast<int>(b->nnz), 0, key_bits, st));
+  {
+    DBuf<unsigned char> tmp(tb);
+    BK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.p, skeys.p, vals.p, reinterpret_cast<R*>(b->vals_sorted.p),
+                                       static_cast<int>(b->nnz), 0, key_bits, st));
+  }
+  b->sj.alloc(b->nnz);
+  k_low32<<<static_cast<unsigned>((b->nnz + 255) / 256), 256, 0, st>>>(b->nnz, skeys.p, b->sj.p);
+  b->cnt.alloc(b->G);
+  BK(cudaMemsetAsync(b->cnt.p, 0, sizeof(int) * b->G, st));
+  k_fold_cnt<<<static_cast<unsigned>((b->nnz + 255) / 256), 256, 0, st>>>(b->nnz, skeys.p, b->cnt.p);
+  BK(cudaGetLastError());
+  build_structure(b.get(), st);
+  *sizes = b->sz;
+  return b.release();
+}
 
 // ---- the fused backend's Gram W^T W on the device (build_btb, normal_ops.cpp:53-173) ------------
 namespace {
@@ -589,13 +685,13 @@ __global__ void k_inverse(int64_t P, const int* __restrict__ perm, int* pos) {
 template <typename R>
 __global__ void k_remap_ent(int64_t n, const int* __restrict__ pos, WtEnt<R>* ent) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) ent[i].j = pos[ent[i].j];
+  if (i < n) ent[i].j = pos[ent[i].j & 0x7fffffff] | (ent[i].j & static_cast<int>(0x80000000u));  // keeps the conj flag
 }
 }  // namespace
 
 template <typename R>
 void gpu_sort_w_tables(int m, int64_t P, int64_t Ppad, int w, int* base, R* wx, R* wy, int* perm, WtEnt<R>* ent,
-                       int64_t n_ent, cudaStream_t st) {
+                       int64_t n_ent, WtEnt<R>* ent2, int64_t n_ent2, cudaStream_t st) {
   if (P <= 0) return;
   DBuf<unsigned long long> keys(P), skeys(P);
   DBuf<int> idx(P);
@@ -622,6 +718,8 @@ void gpu_sort_w_tables(int m, int64_t P, int64_t Ppad, int w, int* base, R* wx, 
     DBuf<int> pos(P);
     k_inverse<<<grid, 256, 0, st>>>(P, perm, pos.p);
     k_remap_ent<R><<<static_cast<unsigned>((n_ent + 255) / 256), 256, 0, st>>>(n_ent, pos.p, ent);
+    if (ent2 && n_ent2 > 0)
+      k_remap_ent<R><<<static_cast<unsigned>((n_ent2 + 255) / 256), 256, 0, st>>>(n_ent2, pos.p, ent2);
     BK(cudaGetLastError());
   }
   BK(cudaStreamSynchronize(st));
@@ -631,7 +729,9 @@ void gpu_sort_w_tables(int m, int64_t P, int64_t Ppad, int w, int* base, R* wx, 
   template GpuBuild* gpu_build_begin<R>(const BuildArgs&, const double*, const double*, int*, R*, R*,         \
                                         cudaStream_t, GpuBuildSizes*);                                        \
   template void gpu_build_finish<R>(GpuBuild*, WtEnt<R>*, int4*, uint16_t*, int4*, int*, cudaStream_t); \
-  template void gpu_sort_w_tables<R>(int, int64_t, int64_t, int, int*, R*, R*, int*, WtEnt<R>*, int64_t, cudaStream_t); \
+  template void gpu_sort_w_tables<R>(int, int64_t, int64_t, int, int*, R*, R*, int*, WtEnt<R>*, int64_t, WtEnt<R>*, \
+                                     int64_t, cudaStream_t);                                                   \
+  template GpuBuild* gpu_build_fold<R>(const GpuBuild*, cudaStream_t, GpuBuildSizes*);                      \
   template GpuBuild* gpu_build_gram_begin<R>(int, int, int64_t, const int*, const double*, const double*, cudaStream_t, \
                                              GpuBuildSizes*, int64_t*);
 

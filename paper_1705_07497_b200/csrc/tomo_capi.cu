@@ -238,7 +238,7 @@ constexpr int kMaxLoggedIters = 8192;
 // Device scratch of an op, sized for `cap` slices (element type = op precision).
 struct Scratch {
   int cap = 0;
-  Raw H, g, s, K, Gt, part_wt, part_gram;  // complex
+  Raw H, g, s, K, Gt, Gth, part_wt, part_gram;  // complex (Gth: the folded half grid, own buffer)
   Raw heavy_cnt, heavy_cnt_gram;
   Raw cin, cout, fin, fout;       // staging for host pointers / temporaries
   Raw r, p0, p1, ap, x, rhs, fid, mu0, mu1, bx0, bx1, by0, by1, nred, zero, u2;  // real vectors
@@ -250,7 +250,7 @@ struct Scratch {
 struct TaskSet {
   Raw ent, tasks, perm, heavy, slot_heavy;
   int n_tasks = 0, n_heavy = 0, n_slots = 0;
-  int64_t slots = 0, nnz = 0, bytes = 0;
+  int64_t slots = 0, nnz = 0, bytes = 0, touched = 0;
 };
 
 struct GraphEntry {
@@ -326,6 +326,7 @@ struct tomo_op {
   Raw wperm;           // separable-W table position -> sample (grid-tile order)
   bool w_sorted = false;
   TaskSet gram;  // fused backend only
+  TaskSet herm;  // W^T folded onto grid rows [0, m/2] (real-subspace type-1); n_tasks == 0: not built
   const TspmFile* src = nullptr;  // during tomo_op_create_tspm: the loaded Gram / surrogate T
   // surrogate
   int rad = 0;
@@ -360,6 +361,8 @@ struct tomo_op {
   }
 
   bool sharded() const { return g.a0 != 0 || g.a1 != g.A; }
+  // real-subspace (Hermitian half-grid) pipeline available: folded W^T built, pairs of image rows
+  bool herm_ok() const { return herm.n_tasks > 0 && g.n % 2 == 0; }
   bool surrogate() const { return desc.backend == TOMO_BACKEND_SURROGATE; }
   bool fused() const { return desc.backend == TOMO_BACKEND_FUSED; }
   int64_t L() const { return static_cast<int64_t>(g.n) * g.n; }
@@ -396,6 +399,7 @@ struct tomo_op {
     d.n_slots = n_slots;
     d.wt_part = sc.part_wt.as<cplx<R>>();
     d.Gt = sc.Gt.as<cplx<R>>();
+    d.Gth = sc.Gth.as<cplx<R>>();
     d.H = sc.H.as<cplx<R>>();
     d.g = sc.g.as<cplx<R>>();
     d.s = sc.s.as<cplx<R>>();
@@ -403,8 +407,17 @@ struct tomo_op {
     d.gram = TaskSpmv<R>{gram.ent.as<WtEnt<R>>(), gram.tasks.as<int4>(), gram.n_tasks, gram.perm.as<uint16_t>(),
                          gram.heavy.as<int4>(), gram.slot_heavy.as<int>(), sc.heavy_cnt_gram.as<unsigned>(),
                          gram.n_heavy, gram.n_slots, sc.part_gram.as<cplx<R>>()};
+    // the folded W^T shares the split-block partials / tickets of W^T (never in flight together)
+    d.wth = TaskSpmv<R>{herm.ent.as<WtEnt<R>>(), herm.tasks.as<int4>(), herm.n_tasks, herm.perm.as<uint16_t>(),
+                        herm.heavy.as<int4>(), herm.slot_heavy.as<int>(), sc.heavy_cnt.as<unsigned>(),
+                        herm.n_heavy, herm.n_slots, sc.part_wt.as<cplx<R>>()};
+    d.herm_in = d.herm_out = 0;
     return d;
   }
+
+  // split-block partial slots / tickets per slice, shared by W^T and its Hermitian fold
+  size_t wt_slots_cap() const { return static_cast<size_t>(std::max({n_slots, herm.n_slots, 1})); }
+  size_t wt_heavy_cap() const { return static_cast<size_t>(std::max({n_heavy, herm.n_heavy, 1})); }
 
   void ensure_batch(int B) {
     Scratch& sc = W().sc;
@@ -414,9 +427,13 @@ struct tomo_op {
     sc.g.ensure(B * m * m * cz);
     sc.Gt.ensure(B * m * m * cz);
     CK(cudaMemset(sc.Gt.p, 0, B * m * m * cz));  // untouched spread-grid nodes stay zero
-    sc.part_wt.ensure(static_cast<size_t>(B) * std::max(n_slots, 1) * 32 * cz);
-    sc.heavy_cnt.ensure(sizeof(unsigned) * static_cast<size_t>(B) * std::max(n_heavy, 1));
-    CK(cudaMemset(sc.heavy_cnt.p, 0, sizeof(unsigned) * static_cast<size_t>(B) * std::max(n_heavy, 1)));
+    if (herm_ok()) {  // the fold touches nodes W^T does not: a grid of its own keeps both zero-clean
+      sc.Gth.ensure(B * m * m * cz);  // slice stride m^2 like Gt; rows [0, m/2] used
+      CK(cudaMemset(sc.Gth.p, 0, B * m * m * cz));
+    }
+    sc.part_wt.ensure(static_cast<size_t>(B) * wt_slots_cap() * 32 * cz);
+    sc.heavy_cnt.ensure(sizeof(unsigned) * static_cast<size_t>(B) * wt_heavy_cap());
+    CK(cudaMemset(sc.heavy_cnt.p, 0, sizeof(unsigned) * static_cast<size_t>(B) * wt_heavy_cap()));
     if (fused()) {
       sc.part_gram.ensure(static_cast<size_t>(B) * std::max(gram.n_slots, 1) * 32 * cz);
       const size_t hb = sizeof(unsigned) * static_cast<size_t>(B) * std::max(gram.n_heavy, 1);
@@ -448,9 +465,13 @@ struct tomo_op {
     ln.g.ensure(B * m * m * cz);
     ln.Gt.ensure(B * m * m * cz);
     CK(cudaMemset(ln.Gt.p, 0, B * m * m * cz));
-    ln.part_wt.ensure(static_cast<size_t>(B) * std::max(n_slots, 1) * 32 * cz);
-    ln.heavy_cnt.ensure(sizeof(unsigned) * static_cast<size_t>(B) * std::max(n_heavy, 1));
-    CK(cudaMemset(ln.heavy_cnt.p, 0, sizeof(unsigned) * static_cast<size_t>(B) * std::max(n_heavy, 1)));
+    if (herm_ok()) {
+      ln.Gth.ensure(B * m * m * cz);
+      CK(cudaMemset(ln.Gth.p, 0, B * m * m * cz));
+    }
+    ln.part_wt.ensure(static_cast<size_t>(B) * wt_slots_cap() * 32 * cz);
+    ln.heavy_cnt.ensure(sizeof(unsigned) * static_cast<size_t>(B) * wt_heavy_cap());
+    CK(cudaMemset(ln.heavy_cnt.p, 0, sizeof(unsigned) * static_cast<size_t>(B) * wt_heavy_cap()));
     if (fused()) {
       ln.part_gram.ensure(static_cast<size_t>(B) * std::max(gram.n_slots, 1) * 32 * cz);
       const size_t hb = sizeof(unsigned) * static_cast<size_t>(B) * std::max(gram.n_heavy, 1);
@@ -1010,6 +1031,24 @@ void build_w_gpu(tomo_op* op) {
   op->wtslotheavy.ensure(sizeof(int) * std::max(sz.n_slots, 1));
   gpu_build_finish<R>(b.get(), op->wtent.as<WtEnt<R>>(), op->wttasks.as<int4>(), op->wtperm.as<uint16_t>(),
                       op->wtheavy.as<int4>(), op->wtslotheavy.as<int>(), 0);
+  // the Hermitian fold of the same W^T for real-part outputs (real subspace)
+  if (ab_knob("TOMO_HERM") == "0") return;
+  GpuBuildSizes hz{};
+  std::unique_ptr<GpuBuild, void (*)(GpuBuild*)> hb(gpu_build_fold<R>(b.get(), 0, &hz), gpu_build_free);
+  TaskSet& ts = op->herm;
+  ts.nnz = hz.nnz;
+  ts.touched = hz.touched;
+  ts.n_tasks = hz.n_tasks;
+  ts.n_heavy = hz.n_heavy;
+  ts.n_slots = hz.n_slots;
+  ts.slots = hz.chunks * 32;
+  ts.ent.ensure(sizeof(WtEnt<R>) * std::max<int64_t>(ts.slots, 1));
+  ts.tasks.ensure(sizeof(int4) * std::max(ts.n_tasks, 1));
+  ts.perm.ensure(sizeof(uint16_t) * static_cast<size_t>(m / 2 + 1) * m);
+  ts.heavy.ensure(sizeof(int4) * std::max(ts.n_heavy, 1));
+  ts.slot_heavy.ensure(sizeof(int) * std::max(ts.n_slots, 1));
+  gpu_build_finish<R>(hb.get(), ts.ent.as<WtEnt<R>>(), ts.tasks.as<int4>(), ts.perm.as<uint16_t>(),
+                      ts.heavy.as<int4>(), ts.slot_heavy.as<int>(), 0);
 }
 
 template <typename R>
@@ -1029,7 +1068,8 @@ void build_tables(tomo_op* op) {
   {
     op->wperm.ensure(sizeof(int) * std::max<int64_t>(g.P, 1));
     gpu_sort_w_tables<R>(m, g.P, op->Ppad, w, op->wbase.as<int>(), op->wxs.as<R>(), op->wys.as<R>(),
-                         op->wperm.as<int>(), op->wtent.as<WtEnt<R>>(), op->wt_slots, 0);
+                         op->wperm.as<int>(), op->wtent.as<WtEnt<R>>(), op->wt_slots, op->herm.ent.as<WtEnt<R>>(),
+                         op->herm.slots, 0);
   }
   // deapodisation a[t]/m (nufft.cpp:204-227 with the 1/m per-axis FFT scale folded in)
   std::vector<R> apod(g.n);
@@ -1078,6 +1118,7 @@ template <typename R>
 void type2(tomo_op* op, int B, const void* in, bool complex_in, const PUpd<R>& pu, cplx<R>* ext_out,
            const SliceScalars* skip, cudaStream_t st) {
   OpDev<R> d = op->dev<R>(B);
+  d.herm_in = op->herm_ok() && !complex_in;
   launch_t2_rows<R>(d, B, in, complex_in, pu, st);
   launch_t2_cols<R>(d, B, skip, st);
   if (ext_out) d.w_out_pos = 0;
@@ -1099,6 +1140,8 @@ cplx<R>* samples_in(tomo_op* op, int B, const cplx<R>* ext, cudaStream_t st) {
 template <typename R>
 void type1(tomo_op* op, int B, const PbEpi<R>& e, const SliceScalars* skip, cudaStream_t st) {
   OpDev<R> d = op->dev<R>(B);
+  d.herm_out = op->herm_ok() && e.mode != PB_COMPLEX;
+  if (d.herm_out) d.Gt = d.Gth;
   launch_wt_rows<R>(d, B, skip, st);
   launch_t1_rows<R>(d, B, e, st);
 }
@@ -1119,6 +1162,11 @@ template <typename R>
 void normal_core(tomo_op* op, int B, const void* in, bool complex_in, const PUpd<R>& pu, const PbEpi<R>& e,
                  const SliceScalars* skip, cudaStream_t st) {
   OpDev<R> d = op->dev<R>(B);
+  // real image in / real part out: the Hermitian half-grid pipeline (not through the Gram, whose
+  // input is the full grid)
+  d.herm_in = op->herm_ok() && !op->fused() && !complex_in;
+  d.herm_out = op->herm_ok() && !op->fused() && e.mode != PB_COMPLEX;
+  if (d.herm_out) d.Gt = d.Gth;
   launch_t2_rows<R>(d, B, in, complex_in, pu, st);
   launch_t2_cols<R>(d, B, skip, st);
   if (op->fused()) {
@@ -1881,6 +1929,10 @@ int tomo_op_get_info(const tomo_op* op, tomo_op_info* info) {
   info->gram_nnz = op->gram.nnz;
   info->gram_slots = op->gram.slots;
   info->bytes_gram = op->gram.bytes;
+  info->herm_nnz = op->herm.nnz;
+  info->herm_slots = op->herm.slots;
+  info->herm_touched = op->herm.touched;
+  info->herm_tasks = op->herm.n_tasks;
   std::memcpy(info->stencil, op->stencil64, sizeof(info->stencil));
   TOMO_CATCH
 }
@@ -1977,6 +2029,31 @@ int tomo_forward(tomo_op* op, const void* image, void* samples, int batch, void*
     const void* din = stage_in(image, cnt * sizeof(cplx<R>), op->W().sc.cin, st);
     OutArg o(samples, scnt * sizeof(cplx<R>), op->W().sc.cout);
     type2<R>(op, batch, din, true, pu, static_cast<cplx<R>*>(o.dev), nullptr, st);
+    o.finish(st);
+  });
+  TOMO_CATCH
+}
+
+// forward_transform (fourier_slice.cpp:61-64): type-2 of a real image, through the Hermitian half grid.
+int tomo_forward_real(tomo_op* op, const void* image, void* samples, int batch, void* stream) {
+  TOMO_TRY
+  check_op(op, batch);
+  DeviceGuard dg(op->device);
+  const cudaStream_t st = S_(stream);
+  Lease lease(op, st);
+  with_prec(op, [&](auto tag) {
+    using R = decltype(tag);
+    const size_t cnt = static_cast<size_t>(batch) * op->L();
+    const size_t scnt = static_cast<size_t>(batch) * op->g.P;
+    PUpd<R> pu{};
+    if (host_pipeline(op, batch, image, op->L() * sizeof(R), samples, op->g.P * sizeof(cplx<R>), st,
+                      [&](int nb, const void* din, void* dout) {
+                        type2<R>(op, nb, din, false, pu, static_cast<cplx<R>*>(dout), nullptr, st);
+                      }))
+      return;
+    const void* din = stage_in(image, cnt * sizeof(R), op->W().sc.cin, st);
+    OutArg o(samples, scnt * sizeof(cplx<R>), op->W().sc.cout);
+    type2<R>(op, batch, din, false, pu, static_cast<cplx<R>*>(o.dev), nullptr, st);
     o.finish(st);
   });
   TOMO_CATCH
@@ -2555,7 +2632,7 @@ int tomo_fft_rows(int m, int rows, int precision, const void* in, void* out, int
   TOMO_CATCH
 }
 
-int tomo_profile_stages(tomo_op* op, int batch, int reps, double* ms, double* bytes, void* stream) {
+int tomo_profile_stages(tomo_op* op, int batch, int reps, int complex_io, double* ms, double* bytes, void* stream) {
   TOMO_TRY
   check_op(op, batch);
   if (!ms || !bytes || reps < 1) throw ConfigError("profile: bad arguments");
@@ -2588,11 +2665,26 @@ int tomo_profile_stages(tomo_op* op, int batch, int reps, double* ms, double* by
     const SysParams sp = sysp(1.0, 1.0, 0.0, 0.0);
     Reduce red = op->red();
     OpDev<R> d = op->dev<R>(batch);
+    // the path the solvers (real images) or the complex applies (complex_io) run
+    const bool herm = !complex_io && op->herm_ok() && !op->fused();
+    d.herm_in = d.herm_out = herm ? 1 : 0;
+    if (herm) d.Gt = d.Gth;
+    const size_t cbytes = sizeof(cplx<R>) * cnt;
+    if (complex_io) {
+      S.cin.ensure(cbytes);
+      S.cout.ensure(cbytes);
+      std::vector<cplx<R>> hc(cnt);
+      for (auto& v : hc) v = cplx<R>{static_cast<R>(nd(rng)), static_cast<R>(nd(rng))};
+      CK(cudaMemcpyAsync(S.cin.p, hc.data(), cbytes, cudaMemcpyHostToDevice, st));
+      CK(cudaStreamSynchronize(st));
+    }
     double acc[TOMO_NUM_STAGES] = {0};
     const bool sur = op->surrogate();
     auto launch_stage = [&](int s, cudaStream_t cs) {
       if (!sur) {
-        if (s == 0) {
+        if (s == 0 && complex_io) {
+          launch_t2_rows<R>(d, batch, S.cin.p, true, PUpd<R>{}, cs);
+        } else if (s == 0) {
           PUpd<R> pu{};
           pu.enabled = 1;
           pu.r = S.r.as<R>();
@@ -2618,6 +2710,10 @@ int tomo_profile_stages(tomo_op* op, int batch, int reps, double* ms, double* by
           if (!op->fused()) launch_wt_spread<R>(d, batch, d.s, d.Gt, op->scal(), cs);
         } else if (s == 4) {
           launch_t1_cols_only<R>(d, batch, op->scal(), cs);
+        } else if (s == 5 && complex_io) {
+          PbEpi<R> e = plain_epi<R>(PB_COMPLEX, 1.0);
+          e.out_c = S.cout.as<cplx<R>>();
+          launch_t1_rows<R>(d, batch, e, cs);
         } else if (s == 5) {
           PbEpi<R> e = plain_epi<R>(PB_CG_STEP, 1.0);
           e.p = S.p0.as<R>();
@@ -2673,21 +2769,28 @@ int tomo_profile_stages(tomo_op* op, int batch, int reps, double* ms, double* by
                  mm = static_cast<double>(m) * m, P = static_cast<double>(op->g.P), rs = sizeof(R), cs = 2 * sizeof(R);
     double by[TOMO_NUM_STAGES] = {0};
     if (!sur) {
-      by[0] = cgcg_on() && !op->sharded()
-                  ? B * (9 * rs * nn + cs * mn)            // C-G: read r, w, x, p, s; write p, s, x, r; write H
-                  : B * (3 * rs * nn + cs * mn);           // read p, r; write p; write H
-      by[1] = B * (cs * mn + cs * mm);                     // read H, write g
+      // Hermitian half grid: m/2 + 1 of the m grid rows (H, g, spread grid, K)
+      const double rows = herm ? m / 2 + 1 : m, hn = rows * n, hm = rows * m;
+      const double in0 = complex_io ? cs * nn : cgcg_on() && !op->sharded()
+                                                     ? 9 * rs * nn   // C-G: read r, w, x, p, s; write p, s, x, r
+                                                     : 3 * rs * nn;  // read p, r; write p
+      by[0] = B * (in0 + cs * hn);                         // + write H
+      by[1] = B * (cs * hn + cs * hm);                     // read H, write g
       // SURVEY.md §8(d) algorithmic bytes (payload only, no implementation padding):
       //   W:   (4 + r) nnz + c T + c P         (ELL entries, gather of the T touched nodes, samples)
       //   W^T: (4 + r) nnz + 8 (T + 1) + c P + c G  (entries, row pointers + ids, samples, grid)
       // the matrix stream is read once per launch, the vectors once per slice
+      //   (the Hermitian path: W gathers the T_h touched nodes of the half grid; the folded W^T
+      //    streams its nnz_f entries, ids of T_h nodes, writes the half grid)
       const double nnzb = static_cast<double>(op->nnz) * (4.0 + rs);
+      const double T = static_cast<double>(herm ? op->herm.touched : op->wt_rows);
+      const double nnzt = herm ? static_cast<double>(op->herm.nnz) * (4.0 + rs) : nnzb;
       by[2] = op->fused()  // Gram stream, read + write touched nodes
                   ? static_cast<double>(op->gram.bytes) + B * (2 * cs * op->wt_rows)
-                  : nnzb + B * (cs * op->wt_rows + cs * P);
-      by[3] = nnzb + 8.0 * (op->wt_rows + 1) + B * (cs * P + cs * mm);
-      by[4] = B * (cs * mm + cs * mn);                     // read spread grid, write K
-      by[5] = B * (cs * mn + 2 * rs * nn);                 // read K, p; write Ap
+                  : nnzb + B * (cs * T + cs * P);
+      by[3] = nnzt + 8.0 * (T + 1) + B * (cs * P + cs * hm);
+      by[4] = B * (cs * hm + cs * hn);                     // read spread grid, write K
+      by[5] = B * (cs * hn + (complex_io ? cs * nn : 2 * rs * nn));  // read K (+ p); write Ap / out
     } else {
       by[8] = B * 4 * rs * nn;  // read r, p; write p, Ap
     }

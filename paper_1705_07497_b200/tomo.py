@@ -302,6 +302,12 @@ class NormalBackend:
         n2, P = self.geom.n ** 2, self.info.P
         return self._unary(lib().tomo_forward, image, True, True, n2, lambda x, B: (B, P))
 
+    def forward_real(self, image):
+        """forward_transform (fourier_slice.cpp:61-64): type-2 of a real image (B, P), through the
+        Hermitian half grid."""
+        n2, P = self.geom.n ** 2, self.info.P
+        return self._unary(lib().tomo_forward_real, image, False, True, n2, lambda x, B: (B, P))
+
     def adjoint(self, samples):
         """SliceTransform::adjoint — type-1 NUFFT back to the image (B, n, n)."""
         P = self.info.P
@@ -423,18 +429,17 @@ class NormalBackend:
         _check(lib().tomo_chambolle_pock(self._h, C.byref(cfg), _ptr(f), _ptr(mu), B, _stream_ptr(f)))
         return mu
 
-    def profile_stages(self, batch=1, reps=20):
+    def profile_stages(self, batch=1, reps=20, complex_io=False):
         """Per-kernel device time (ms, CUDA events on the current stream) and algorithmic bytes
-        of one hot-path solver step; {name: (ms, bytes)} for the stages this backend runs."""
+        of one hot-path solver step (complex_io: of one complex apply); {name: (ms, bytes)} for
+        the stages this backend runs."""
         torch = _torch()
         ms = np.zeros(_lib.NUM_STAGES)
         by = np.zeros(_lib.NUM_STAGES)
         stream = C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
-        _check(lib().tomo_profile_stages(self._h, batch, reps, ms.ctypes.data_as(C.c_void_p),
+        _check(lib().tomo_profile_stages(self._h, batch, reps, int(bool(complex_io)), ms.ctypes.data_as(C.c_void_p),
                                          by.ctypes.data_as(C.c_void_p), stream))
         out = {name: (float(ms[i]), float(by[i])) for i, name in enumerate(_lib.STAGE_NAMES) if by[i] > 0}
-        if "wt_spread" in out and "t1_cols" not in out and "w_spmv" in out:
-            out["wt_t1"] = out.pop("wt_spread")  # the fused W^T + PA kernel (k_wt_t1)
         return out
 
     # ---------------------------------------------------------------- on-disk operators
