@@ -11,7 +11,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, os.environ.get("TOMO_LIB_NAME", "libtomo_b200.so"))  # variant builds for A/B runs
-SOURCES = ["nufft.cu", "solver.cu", "opbuild.cu", "tomo_capi.cu"]
+SOURCES = ["nufft.cu", "spmv.cu", "solver.cu", "opbuild.cu", "tomo_capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC,-O2",
@@ -47,9 +47,15 @@ def build(verbose: bool = False, jobs: int = 3) -> str:
     os.makedirs(objdir, exist_ok=True)
     procs = []
     objs = []
+    headers = [d for d in deps if not d.endswith(".cu")]
+    defs_now = os.environ.get("TOMO_NVCC_DEFS", "")
+    stamp = os.path.join(objdir, "defs.txt")  # objects built with other -D flags are stale
+    same_defs = os.path.exists(stamp) and open(stamp).read() == defs_now
     for src in SOURCES:
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
         objs.append(obj)
+        if same_defs and not _stale(obj, [os.path.join(CSRC, src), *headers]):
+            continue  # up to date: only the changed translation units recompile
         nccl = _nccl_dir()
         inc = ["-I", os.path.join(nccl, "include")] if nccl else []
         defs = os.environ.get("TOMO_NVCC_DEFS", "").split()
@@ -69,6 +75,8 @@ def build(verbose: bool = False, jobs: int = 3) -> str:
         for src, text in failed:
             sys.stderr.write(f"---- nvcc failed on {src}\n{text}\n")
         raise RuntimeError("nvcc build of libtomo_b200 failed")
+    with open(stamp, "w") as f:
+        f.write(defs_now)
     nccl = _nccl_dir()
     if nccl:
         lib = os.path.join(nccl, "lib")

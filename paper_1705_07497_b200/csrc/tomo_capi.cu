@@ -611,6 +611,17 @@ namespace {
 // ix); 32 sorted nodes form a block of L = max count chunks (entries chunk-major, padded with
 // weight-0 re-reads of a sample already in cache); blocks with L > max_chunks are split into
 // several warp tasks whose partial sums the last task of the block combines.
+// The task SpMV loads its entry groups unconditionally (chunks past a task's end belong to the next
+// task and gather nothing): every entry stream carries kEntPadChunks zero chunks after its last slot.
+constexpr int kEntPadChunks = 16;
+template <typename R>
+void ent_alloc(Raw& r, int64_t slots) {
+  const size_t n = static_cast<size_t>(std::max<int64_t>(slots, 0)) + static_cast<size_t>(kEntPadChunks) * 32;
+  r.ensure(sizeof(WtEnt<R>) * n);
+  CK(cudaMemset(static_cast<char*>(r.p) + sizeof(WtEnt<R>) * std::max<int64_t>(slots, 0), 0,
+                sizeof(WtEnt<R>) * static_cast<size_t>(kEntPadChunks) * 32));
+}
+
 template <typename R>
 struct TaskBuilder {
   int m, max_chunks;
@@ -685,7 +696,9 @@ struct TaskBuilder {
   }
 
   void upload(Raw& dent, Raw& dtasks, Raw& dperm, Raw& dheavy, Raw& dslot) const {
-    dent.upload(ent);
+    std::vector<WtEnt<R>> padded(ent);
+    padded.resize(ent.size() + static_cast<size_t>(kEntPadChunks) * 32, WtEnt<R>{});  // zero tail (see ent_alloc)
+    dent.upload(padded);
     dtasks.upload(tasks.empty() ? std::vector<int4>(1) : tasks);
     dperm.upload(perm);
     dheavy.upload(heavy.empty() ? std::vector<int4>(1) : heavy);
@@ -825,7 +838,7 @@ void build_gram(tomo_op* op, const Plan& pl) {
       ts.nnz = nnz;
       ts.bytes = ts.slots * static_cast<int64_t>(sizeof(WtEnt<R>)) + static_cast<int64_t>(ts.n_tasks) * 16 +
                  static_cast<int64_t>(m) * m * 2;
-      ts.ent.ensure(sizeof(WtEnt<R>) * std::max<int64_t>(ts.slots, 1));
+      ent_alloc<R>(ts.ent, ts.slots);
       ts.tasks.ensure(sizeof(int4) * std::max(ts.n_tasks, 1));
       ts.perm.ensure(sizeof(uint16_t) * static_cast<size_t>(m) * m);
       ts.heavy.ensure(sizeof(int4) * std::max(ts.n_heavy, 1));
@@ -1024,7 +1037,7 @@ void build_w_gpu(tomo_op* op) {
   op->n_tasks = sz.n_tasks;
   op->n_heavy = sz.n_heavy;
   op->n_slots = sz.n_slots;
-  op->wtent.ensure(sizeof(WtEnt<R>) * std::max<int64_t>(op->wt_slots, 1));
+  ent_alloc<R>(op->wtent, op->wt_slots);
   op->wttasks.ensure(sizeof(int4) * std::max(sz.n_tasks, 1));
   op->wtperm.ensure(sizeof(uint16_t) * static_cast<size_t>(m) * m);
   op->wtheavy.ensure(sizeof(int4) * std::max(sz.n_heavy, 1));
@@ -1042,7 +1055,7 @@ void build_w_gpu(tomo_op* op) {
   ts.n_heavy = hz.n_heavy;
   ts.n_slots = hz.n_slots;
   ts.slots = hz.chunks * 32;
-  ts.ent.ensure(sizeof(WtEnt<R>) * std::max<int64_t>(ts.slots, 1));
+  ent_alloc<R>(ts.ent, ts.slots);
   ts.tasks.ensure(sizeof(int4) * std::max(ts.n_tasks, 1));
   ts.perm.ensure(sizeof(uint16_t) * static_cast<size_t>(m / 2 + 1) * m);
   ts.heavy.ensure(sizeof(int4) * std::max(ts.n_heavy, 1));
