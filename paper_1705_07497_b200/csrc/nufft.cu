@@ -71,7 +71,6 @@ TOMO_DEV void store_transposed(const C2* sm, int rpc, int ncols, int K, C2* __re
     if (q < ncols) dst[static_cast<size_t>(k) * ld + q] = sm[q * STRIDE + pad16(k)];
   }
 }
-
 struct NoStore {
   template <typename C2>
   TOMO_DEV void operator()(int, C2) const {}
@@ -102,7 +101,7 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F3
     if (pu.red.sc && pu.red.sc[b].frozen) return;
   }
   const int rr = threadIdx.x / S::T, t = threadIdx.x % S::T;
-  const int n = d.n;
+  const int n = HALF ? M / 2 : d.n /* compile-time at 2x oversampling */;
   const int t10 = blockIdx.x * rpc;
   const int t1 = t10 + rr;
   const bool active = rr < rpc && t1 < n;
@@ -182,7 +181,7 @@ k_t2_rows_pk(OpDev<R> d, const void* __restrict__ in, PUpd<R> pu, int rpc) {
     if (pu.red.sc && pu.red.sc[b].frozen) return;
   }
   const int rr = threadIdx.x / S::T, t = threadIdx.x % S::T;
-  const int n = d.n, npair = n >> 1;
+  const int n = HALF ? M / 2 : d.n /* compile-time at 2x oversampling */, npair = n >> 1;
   const int q0 = blockIdx.x * rpc;
   const int q = q0 + rr;
   const bool active = rr < rpc && q < npair;
@@ -235,16 +234,17 @@ k_t2_rows_pk(OpDev<R> d, const void* __restrict__ in, PUpd<R> pu, int rpc) {
   // separate the two spectra; transposed store H[b][k][t1] for k in [0, M/2], 2 rpc consecutive t1
   const int ncols = 2 * max(0, min(rpc, npair - q0));
   const int w2 = 2 * rpc, lg = __ffs(w2) - 1;
-  C2* H = d.H + static_cast<size_t>(b) * M * n + 2 * q0;
+  const int c = threadIdx.x & (w2 - 1);  // loop-invariant output column (blockDim.x is a multiple of 2 rpc)
+  if (c >= ncols) return;
+  C2* H = d.H + static_cast<size_t>(b) * M * n + 2 * q0 + c;
+  const C2* rw = sm + (c >> 1) * S::STRIDE;
+  const bool odd = c & 1;
   const R h = R(0.5);
-  for (int idx = threadIdx.x; idx < ((M / 2 + 1) << lg); idx += blockDim.x) {
-    const int k = idx >> lg, c = idx & (w2 - 1);
-    if (c < ncols) {
-      const C2* rw = sm + (c >> 1) * S::STRIDE;
-      const C2 z = rw[pad16(k)], zm = rw[pad16((M - k) & (M - 1))];
-      H[static_cast<size_t>(k) * n + c] = (c & 1) ? mk<C2>(h * (z.y + zm.y), h * (zm.x - z.x))
-                                                  : mk<C2>(h * (z.x + zm.x), h * (z.y - zm.y));
-    }
+  const int step = blockDim.x >> lg;
+  for (int k = threadIdx.x >> lg; k <= M / 2; k += step) {
+    const C2 z = rw[pad16(k)], zm = rw[pad16((M - k) & (M - 1))];
+    H[static_cast<size_t>(k) * n] = odd ? mk<C2>(h * (z.y + zm.y), h * (zm.x - z.x))
+                                        : mk<C2>(h * (z.x + zm.x), h * (z.y - zm.y));
   }
 }
 
@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F3
   const int b = blockIdx.y;
   if (skip && (skip[b].done || skip[b].frozen)) return;
   const int rr = threadIdx.x / S::T, t = threadIdx.x % S::T;
-  const int n = d.n;
+  const int n = HALF ? M / 2 : d.n /* compile-time at 2x oversampling */;
   const int iy = blockIdx.x * rpc + rr;
   const bool active = rr < rpc && iy < nrows;  // nrows: m, or m/2 + 1 rows of a Hermitian spectrum
   C2* row = sm + rr * S::STRIDE;
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(kFftThreads, sizeof(R) == 4 ? TOMO_FFT_MINB_F3
   C2* sm = reinterpret_cast<C2*>(smraw);
   const int b = blockIdx.y;
   if (skip && (skip[b].done || skip[b].frozen)) return;
-  const int n = d.n;
+  const int n = HALF ? M / 2 : d.n /* compile-time at 2x oversampling */;
   const int iy0 = blockIdx.x * rpc;
   const int rr = threadIdx.x / S::T, t = threadIdx.x % S::T;
   const bool active = rr < rpc && iy0 + rr < nrows;
