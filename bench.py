@@ -391,10 +391,15 @@ class Workload:
             stages = ("t2_rows", "t2_cols", "w_spmv", "wt_spread", "t1_cols", "t1_rows")
             t_apply = sum(prof[s][0] for s in stages if s in prof)
             ab = apply_bytes(c, self.op.info.wt_rows, complex_io=(k == "apply"), B=B)
+            # the bytes the six kernels as run must move (the real-image solvers take the
+            # Hermitian half grid, so they move less than SURVEY's formula)
+            mb = sum(prof[s][1] for s in stages if s in prof)
             out["apply"] = {"bytes": int(ab), "ms": round(t_apply, 5), "slices_per_launch": B,
                             "achieved": round(ab / (t_apply * 1e-3) / 1e9, 1),
                             "frac": round(ab / (t_apply * 1e-3) / 1e9 / peak_gbs, 4),
-                            "formula": "SURVEY 8(d): 2(4+r)nnz + 8T + B(in + out + 3cG + cT + 2cP)"}
+                            "formula": "SURVEY 8(d): 2(4+r)nnz + 8T + B(in + out + 3cG + cT + 2cP)",
+                            "moved_bytes": int(mb),
+                            "moved_frac": round(mb / (t_apply * 1e-3) / 1e9 / peak_gbs, 4)}
         return top, out
 
 

@@ -85,7 +85,7 @@ typedef struct tomo_op_info {
   int64_t P;            /* local slice samples (rows of W) */
   int64_t nnz;          /* W non-zeros (= P * window^2) */
   int64_t wt_rows;      /* touched grid nodes (non-empty W^T rows) */
-  int64_t wt_slots;     /* SELL-32 slots of W^T incl. padding */
+  int64_t wt_slots;     /* W^T task-SpMV slots incl. padding (32-node blocks, count-sorted rows) */
   int64_t bytes_w;      /* device bytes of the W tables */
   int64_t bytes_wt;     /* device bytes of the W^T tables */
   double stencil[81];   /* surrogate stencil (2r+1)^2, fp64 host copy */
@@ -106,8 +106,9 @@ const char* tomo_last_error(void);
 
 /* make_direct_backend / make_fused_backend / make_surrogate_backend (normal_ops.hpp:35-39)
  * over a SliceTransform(SliceGrid, NufftParams) (fourier_slice.hpp:39). Builds W (separable
- * per-sample window factors), its row-sorted transpose W^T, deapodisation and FFT tables on
- * `device`; for the fused backend also
+ * per-sample window factors), its row-sorted transpose W^T and the Hermitian fold of W^T
+ * (real-part outputs on half the grid rows), deapodisation and FFT tables on `device`; for the
+ * fused backend also
  * the Gram W^T W (build_btb, normal_ops.hpp:47); for the surrogate also the stencil
  * (build_surrogate, normal_ops.hpp:60). */
 int tomo_op_create(const tomo_geom_desc* geom, const tomo_op_desc* desc, tomo_op** out);
@@ -251,7 +252,7 @@ int tomo_fft_rows(int m, int rows, int precision, const void* in, void* out, int
  * moves. complex_io = 0: the solvers' real-image path (the
  * Hermitian half grid where available); 1: complex applies (complex in, complex out). Stage ids:
  *   0 t2_rows (P1: p-update + deapod + pad + row iFFT)   1 t2_cols (P2: column iFFT)
- *   2 w (W SELL-32 SpMV)   3 wt_spread (W^T task SpMV + split-block fix-up)
+ *   2 w (W: separable window SpMV)   3 wt_spread (W^T task SpMV + split-block fix-up)
  *   4 t1_cols (PA: grid-row FFT, pruned)   5 t1_rows (PB: FFT + crop + deapod + CG epilogue)
  *   6 cg_update   7 sb_post   8 stencil (surrogate T + K'K + CG dots)
  * Stages that do not apply to the backend report 0. Returns TOMO_OK. */
