@@ -15,6 +15,7 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <algorithm>
 #include <cstdlib>
 #include <memory>
 #include <stdexcept>
@@ -221,8 +222,22 @@ __global__ void k_entries(int m, int64_t G32, const uint16_t* __restrict__ perm,
 bool wt_row_order(int m) {
   const std::string ord = ab_knob("TOMO_TASK_ORDER");
   if (ord == "rows") return true;
-  if (ord == "len") return false;
+  if (ord == "len" || ord == "band") return false;
   return m >= 4096;
+}
+
+int wt_task_band(int m);
+
+// Rows per task band (0: no bands) — see gpu_build_finish. Measured (B200, same box): bands of 32
+// rows, heaviest band first, c2 W^T 17.9 -> 15.8 us (31.1 -> 32.4 slices/s), c3 30.2 -> 26.7 us
+// (12.27k -> 12.63k applies/s); c1 (m = 512, batched lanes) 71.1k -> 69.6k and c5 (m = 8192, row
+// order) unchanged, so bands are the default for 1024 <= m <= 2048 only. TOMO_TASK_ORDER=band|rows|len
+// and TOMO_TASK_BAND=<rows> override (A/B runs).
+int wt_task_band(int m) {
+  const std::string ord = ab_knob("TOMO_TASK_ORDER");
+  if (ord == "rows" || ord == "len") return 0;
+  if (ord == "band") return std::max(1, ab_int("TOMO_TASK_BAND", 32));
+  return m >= 1024 && m <= 2048 ? 32 : 0;
 }
 
 namespace {
@@ -380,7 +395,30 @@ void gpu_build_finish(GpuBuild* b, WtEnt<R>* ent, int4* tasks, uint16_t* perm, i
   k_tasks<<<static_cast<unsigned>((b->G32 + 255) / 256), 256, 0, st>>>(
       b->G32, wt_max_chunks(), b->L.p, b->chunk0.p, b->toff.p, b->soff.p, b->hoff.p, traw.p, tkey.p, heavy, slot_heavy);
   BK(cudaGetLastError());
-  if (nt > 0 && wt_row_order(m)) {
+  const int band = wt_task_band(m);
+  if (nt > 0 && band > 0) {
+    // bands of `band` grid rows; the bands heaviest first (by their longest task), row order between
+    // equal bands, longest tasks first within a band: one band's tasks gather the same samples
+    // (L1 / L2 reuse) and the heavy bands around the zero frequency do not form the tail
+    std::vector<int4> h(nt);
+    BK(cudaMemcpyAsync(h.data(), traw.p, sizeof(int4) * nt, cudaMemcpyDeviceToHost, st));
+    BK(cudaStreamSynchronize(st));
+    const int bpr = m / 32;
+    std::vector<int> bmax((b->rows > 0 ? b->rows : m) / band + 1, 0);
+    for (const int4& t : h) bmax[(t.x / bpr) / band] = std::max(bmax[(t.x / bpr) / band], t.z);
+    std::vector<int> ord(nt);
+    for (int i = 0; i < nt; ++i) ord[i] = i;
+    std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) {
+      const int bx = (h[x].x / bpr) / band, by = (h[y].x / bpr) / band;
+      if (bmax[bx] != bmax[by]) return bmax[bx] > bmax[by];
+      if (bx != by) return bx < by;
+      return h[x].z > h[y].z;
+    });
+    std::vector<int4> sorted(nt);
+    for (int i = 0; i < nt; ++i) sorted[i] = h[ord[i]];
+    BK(cudaMemcpyAsync(tasks, sorted.data(), sizeof(int4) * nt, cudaMemcpyHostToDevice, st));
+    BK(cudaStreamSynchronize(st));
+  } else if (nt > 0 && wt_row_order(m)) {
     BK(cudaMemcpyAsync(tasks, traw.p, sizeof(int4) * nt, cudaMemcpyDeviceToDevice, st));
   } else if (nt > 0) {
     // longest tasks first, stable (LSD radix sort) = the host's stable_sort by nchunks desc
