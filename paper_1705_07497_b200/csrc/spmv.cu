@@ -116,6 +116,83 @@ __global__ void __launch_bounds__(256) k_w_sep(OpDev<R> d, int B, const cplx<R>*
   }
 }
 
+// fp32, width-6 windows (c3, c4): the same separable product with each window row fetched as
+// 16-byte vectors (3 or 4 float4 = the 6 nodes, two per vector) instead of 6 scalar 8-byte
+// gathers: W is bound by L1 request / sector throughput (32 samples per warp request, one node each),
+// and a vector carries two nodes of the same row. Rows that wrap around the grid edge take the
+// scalar gathers. Same arithmetic, same order as k_w_sep (bit-identical).
+template <int BT, bool BY, bool HERM>
+__global__ void __launch_bounds__(256) k_w_sep_v6(OpDev<float> d, int B, const float2* __restrict__ grid,
+                                                   float2* __restrict__ out, const SliceScalars* skip) {
+  constexpr int W = 6;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;  // table position
+  if (t >= d.P) return;
+  const int j = d.w_perm && !d.w_out_pos ? __ldg(&d.w_perm[t]) : t;  // output index
+  const int m = d.m;
+  const int base = __ldg(&d.w_base[t]);
+  const int ix0 = base & 0xffff, iy0 = base >> 16;
+  float wx[W];
+#pragma unroll
+  for (int a = 0; a < W; ++a) wx[a] = __ldg(&d.w_x[static_cast<size_t>(a) * d.Ppad + t]);
+  // contiguous (no wrap) node ranges: plain rows [ix0, ix0 + 5], mirrored rows [m - ix0 - 5, m - ix0]
+  const bool plain_ok = ix0 + W <= m, mir_ok = ix0 >= 1 && ix0 <= m - W + 1;
+  const size_t G = static_cast<size_t>(m) * m;
+  for (int b0 = BY ? static_cast<int>(blockIdx.y) * BT : 0; b0 < B; b0 += (BY ? static_cast<int>(gridDim.y) : 1) * BT) {
+    float2 acc[BT];
+#pragma unroll
+    for (int q = 0; q < BT; ++q) acc[q] = make_float2(0.f, 0.f);
+#pragma unroll 1
+    for (int bb = 0; bb < W; ++bb) {
+      const float wyv = __ldg(&d.w_y[static_cast<size_t>(bb) * d.Ppad + t]);
+      const int u0 = iy0 + bb;
+      const int u = u0 >= m ? u0 - m : u0;
+      const bool mir = HERM && u > (m >> 1);
+      const size_t rowoff = static_cast<size_t>(mir ? m - u : u) * m;
+      const int lo = mir ? m - ix0 - (W - 1) : ix0;
+      const bool vec = mir ? mir_ok : plain_ok;
+      const bool odd = lo & 1;
+#pragma unroll
+      for (int q = 0; q < BT; ++q) {
+        if (b0 + q < B) {
+          const float2* row = grid + G * (b0 + q) + rowoff;
+          float2 ra = make_float2(0.f, 0.f);
+          if (vec) {
+            const float4* p4 = reinterpret_cast<const float4*>(row + (lo & ~1));
+            const float4 v0 = __ldg(p4), v1 = __ldg(p4 + 1), v2 = __ldg(p4 + 2);
+            const float4 v3 = odd ? __ldg(p4 + 3) : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float2 nd[8] = {make_float2(v0.x, v0.y), make_float2(v0.z, v0.w), make_float2(v1.x, v1.y),
+                                  make_float2(v1.z, v1.w), make_float2(v2.x, v2.y), make_float2(v2.z, v2.w),
+                                  make_float2(v3.x, v3.y), make_float2(v3.z, v3.w)};
+#pragma unroll
+            for (int a = 0; a < W; ++a) {
+              // tap a is node a of the range (plain) or node W-1-a (mirrored), shifted by odd
+              const float2 e = mir ? (odd ? nd[W - a] : nd[W - 1 - a]) : (odd ? nd[a + 1] : nd[a]);
+              ra.x += wx[a] * e.x;
+              ra.y += wx[a] * e.y;
+            }
+          } else {
+#pragma unroll
+            for (int a = 0; a < W; ++a) {
+              const int v0 = ix0 + a;
+              const int v = v0 >= m ? v0 - m : v0;
+              const float2 gv = row[mir ? ((m - v) & (m - 1)) : v];
+              ra.x += wx[a] * gv.x;
+              ra.y += wx[a] * gv.y;
+            }
+          }
+          if (mir) ra.y = -ra.y;  // conj(sum w g) = sum w conj(g)
+          acc[q].x += wyv * ra.x;
+          acc[q].y += wyv * ra.y;
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < BT; ++q)
+      if (b0 + q < B && !(skip && (skip[b0 + q].done || skip[b0 + q].frozen)))
+        out[static_cast<size_t>(b0 + q) * d.P + j] = acc[q];
+  }
+}
+
 // Wide windows (w > 8, e.g. the digits12 preset's 25 taps): the same separable product with the
 // factor vectors read in the loops (L1-resident per thread) instead of held in registers.
 template <typename R>
@@ -359,6 +436,25 @@ void launch_w(const OpDev<R>& d, int B, const cplx<R>* grid, cplx<R>* samples, c
       else
         go2(WC, std::false_type{});
     };
+    static const int vec_on = env_int("TOMO_W_VEC", 1);  // A/B: 0 = scalar gathers for fp32 too
+    if constexpr (sizeof(R) == 4) {
+      if (vec_on && d.w == 6) {
+        auto gov = [&](auto HC) {
+          constexpr bool HM = decltype(HC)::value;
+          const unsigned ydim = batch_ydim(blocks, (B + 1) / 2);
+          if (B >= 2 && ydim > 1)
+            CK_LAUNCH(launch_k(k_w_sep_v6<2, true, HM>, dim3(blocks, ydim), threads, 0, st, d, B, grid, samples, skip));
+          else if (B >= 2)
+            CK_LAUNCH(launch_k(k_w_sep_v6<2, false, HM>, blocks, threads, 0, st, d, B, grid, samples, skip));
+          else
+            CK_LAUNCH(launch_k(k_w_sep_v6<1, false, HM>, blocks, threads, 0, st, d, B, grid, samples, skip));
+        };
+        if (d.herm_in) gov(std::true_type{});
+        else gov(std::false_type{});
+        note_launch();
+        return;
+      }
+    }
     if (d.w <= 6)
       go(std::integral_constant<int, 6>{});
     else if (d.w <= 8)
