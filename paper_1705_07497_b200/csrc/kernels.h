@@ -55,6 +55,7 @@ struct OpDev {
   int G32;                         // number of 32-node SELL blocks of W^T (= m*m/32)
   const R* apod;                   // n   : a[t]/m  (deconvolve, nufft.cpp:204-227, with 1/m per axis)
   const cplx<R>* tw;               // m   : e^{-2 pi i k/m}
+  const cplx<R>* tw_half;          // m/2 : e^{-2 pi i k/(m/2)} (the split grid-row passes' half transforms)
   // Separable ("rank-1 block") storage of W: row j's w x w block is
   // wx_j[a] * wy_j[b] at nodes ((iy0+b) mod m, (ix0+a) mod m) (nufft.cpp:185-200).
   const int* w_base;               // [Ppad] ix0 | iy0 << 16

@@ -704,6 +704,68 @@ k_t1_rows_p(OpDev<R> d, PbEpi<R> e) {
   }
 }
 
+// ================================================================ split grid rows (fp64, m = 8192)
+// A grid row of 8192 fp64 points (128 KB + padding) admits one 512-thread CTA per SM, which then
+// serialises its row load, FFT and stores. One decimation-in-frequency step splits the row over two
+// CTAs: X[2k+h] = FFT_{M/2}(y_h)[k], y_0[i] = x[i] + x[i+M/2], y_1[i] = (x[i] - x[i+M/2]) W_M^i; each
+// CTA (h = blockIdx.x & 1) loads the whole row, combines its halves on load and transforms M/2 points
+// in 70 KB of shared memory (two CTAs per SM, one loading while the other computes).
+
+// P2: inverse FFT along ix of the H row (conj in / conj out), natural stores g[iy][2k+h].
+// Q: 4n == M, the non-zero inputs of y are its first and last quarter (compile-time pruning).
+template <int M, int RB, typename R, bool Q>
+__global__ void __launch_bounds__(M / 2 / RB, 2) k_t2_cols_dif(OpDev<R> d, int nrows, const SliceScalars* skip) {
+  constexpr int MH = M / 2;
+  using C2 = cplx<R>;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  C2* row = reinterpret_cast<C2*>(smraw);
+  const int b = blockIdx.y;
+  if (skip && (skip[b].done || skip[b].frozen)) return;
+  const int iy = blockIdx.x >> 1, h = blockIdx.x & 1;
+  if (iy >= nrows) return;  // CTA-uniform
+  const int n = Q ? M / 4 : d.n, t = threadIdx.x;
+  const C2* H = d.H + (static_cast<size_t>(b) * M + iy) * n;
+  C2* g = d.g + (static_cast<size_t>(b) * M + iy) * M;
+  auto in = [&](int p) -> C2 {  // conj(x[p]): H at t1 = (p + n/2) mod M < n (pruned padding)
+    const int t1 = (p + n / 2) & (M - 1);
+    return t1 < n ? cconj(H[t1]) : czero<C2>();
+  };
+  auto load = [&](int i) -> C2 {
+    const C2 xa = in(i), xb = in(i + MH);
+    return h == 0 ? cadd(xa, xb) : cmul(csub(xa, xb), __ldg(&d.tw[i]));
+  };
+  auto store = [&](int k, C2 v) { g[2 * k + h] = cconj(v); };
+  fft_row<MH, RB, false, C2, Q ? 1 : 0>(row, d.tw_half, t, true, load, store);
+}
+
+// PA: forward FFT along ix of the spread-grid row; the kept bins of half h are t1 = 2q + par,
+// par = (h + n/2) & 1, staged at q and stored transposed to K[t1][iy].
+template <int M, int RB, typename R>
+__global__ void __launch_bounds__(M / 2 / RB, 2) k_t1_cols_dif(OpDev<R> d, int nrows, const SliceScalars* skip) {
+  constexpr int MH = M / 2;
+  using C2 = cplx<R>;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  C2* row = reinterpret_cast<C2*>(smraw);
+  const int b = blockIdx.y;
+  if (skip && (skip[b].done || skip[b].frozen)) return;
+  const int iy = blockIdx.x >> 1, h = blockIdx.x & 1;
+  if (iy >= nrows) return;  // CTA-uniform
+  const int n = d.n, t = threadIdx.x;
+  const C2* Gr = d.Gt + (static_cast<size_t>(b) * M + iy) * M;
+  auto load = [&](int i) -> C2 {
+    const C2 xa = Gr[i], xb = Gr[i + MH];
+    return h == 0 ? cadd(xa, xb) : cmul(csub(xa, xb), __ldg(&d.tw[i]));
+  };
+  auto store = [&](int kh, C2 v) {
+    const int t1 = (2 * kh + h + n / 2) & (M - 1);
+    if (t1 < n) row[pad16(t1 >> 1)] = v;
+  };
+  fft_row<MH, RB, true, C2, 0>(row, d.tw_half, t, true, load, store);
+  const int par = (h + n / 2) & 1;
+  C2* K = d.K + static_cast<size_t>(b) * n * M + iy;
+  for (int q = t; q < n / 2; q += blockDim.x) K[static_cast<size_t>(2 * q + par) * M] = row[pad16(q)];
+}
+
 template <int M, int RB, typename R>
 __global__ void k_fft_rows_test(const cplx<R>* tw, const cplx<R>* in, cplx<R>* out, int rows, int inverse) {
   using S = FftShape<M, RB>;
@@ -767,27 +829,39 @@ void dispatch_m_rb(int m, int rb, F&& f) {
 // TOMO_ROW_RB=8|16 overrides (A/B runs, TOMO_AB=1).
 int env_int(const char* name, int dflt) { return ab_int(name, dflt); }
 
-int row_rb(int m, size_t elem) {
+// `rows` = transforms per launch (image rows, or row pairs on the half grid, times slices): fp64
+// launches of at most 256 rows at m = 512 / 1024 take radix 4 (twice radix 8's threads per row; c2,
+// 256 row pairs: 32.3 -> 32.6 slices/s, PB 10.3 -> 9.9 us over 3 runs each; c1's 896 pairs per lane
+// are slower at radix 4).
+int row_rb(int m, size_t elem, int64_t rows) {
   static const int forced = env_int("TOMO_ROW_RB", 0);
   if (forced == 4 || forced == 8 || forced == 16) return forced;
+  if (elem == 16 && (m == 512 || m == 1024) && rows <= 256) return 4;
   return elem == 16 && m <= 2048 ? 8 : 16;
 }
 
 template <typename F>
-void dispatch_m_rows(int m, size_t elem, F&& f) {
+void dispatch_m_rows(int m, size_t elem, int64_t rows, F&& f) {
   dispatch_m(m, [&](auto MC) {
     constexpr int M = decltype(MC)::value;
     if constexpr (M == 512 || M == 1024) {  // radix 4 (A/B, TOMO_ROW_RB=4): c1 / c2 grid sizes only
-      if (row_rb(m, elem) == 4) {
+      if (row_rb(m, elem, rows) == 4) {
         f(MC, std::integral_constant<int, 4>{});
         return;
       }
     }
-    if (row_rb(m, elem) == 8 && M / 8 <= kFftThreads)
+    if (row_rb(m, elem, rows) == 8 && M / 8 <= kFftThreads)
       f(MC, std::integral_constant<int, 8>{});
     else
       f(MC, std::integral_constant<int, 16>{});
   });
+}
+
+// fp64 8192-point grid rows split over two CTAs by one decimation-in-frequency step (k_t2_cols_dif /
+// k_t1_cols_dif); TOMO_DIF=0 restores the whole-row kernels (A/B runs).
+bool dif_on() {
+  static const bool v = env_int("TOMO_DIF", 1) != 0;
+  return v;
 }
 
 // Grid-row passes (P2, PA): radix 16 unless TOMO_COL_RB=8 (A/B runs; one-shot kernels only).
@@ -830,7 +904,7 @@ void set_smem(K kernel, size_t bytes) {
 template <typename R>
 void launch_t2_rows(const OpDev<R>& d, int B, const void* in, bool in_complex, const PUpd<R>& pu, cudaStream_t st) {
   if (d.herm_in && !in_complex) {  // real image: two rows per complex transform, H rows [0, m/2]
-    dispatch_m_rows(d.m, sizeof(cplx<R>), [&](auto MC, auto RC) {
+    dispatch_m_rows(d.m, sizeof(cplx<R>), static_cast<int64_t>(d.n / 2) * B, [&](auto MC, auto RC) {
       constexpr int M = decltype(MC)::value, RB = decltype(RC)::value;
       using S = FftShape<M, RB>;
       // 2 rpc t1 values per H row segment: >= 32 B segments need rpc >= 16 / sizeof(C2)
@@ -856,7 +930,7 @@ void launch_t2_rows(const OpDev<R>& d, int B, const void* in, bool in_complex, c
     });
     return;
   }
-  dispatch_m_rows(d.m, sizeof(cplx<R>), [&](auto MC, auto RC) {
+  dispatch_m_rows(d.m, sizeof(cplx<R>), static_cast<int64_t>(d.n) * B, [&](auto MC, auto RC) {
     constexpr int M = decltype(MC)::value, RB = decltype(RC)::value;
     using S = FftShape<M, RB>;
     const int rpc = choose_rpc(S::T, M, d.n, B, sizeof(cplx<R>), true);
@@ -911,6 +985,20 @@ void launch_t2_cols(const OpDev<R>& d, int B, const SliceScalars* skip, cudaStre
     constexpr int M = decltype(MC)::value, RB = decltype(RC)::value;
     using S = FftShape<M, RB>;
     const int nrows = d.herm_in ? M / 2 + 1 : M;  // Hermitian spectrum: rows [0, m/2]
+    if constexpr (M == 8192 && sizeof(R) == 8) {  // fp64 8192-point rows split over two CTAs
+      if (dif_on()) {
+        using SH = FftShape<M / 2, RB>;
+        const size_t smem = static_cast<size_t>(SH::STRIDE) * sizeof(cplx<R>);
+        auto go = [&](auto kern) {
+          set_smem(kern, smem);
+          CK_LAUNCH(launch_k(kern, dim3(2 * nrows, B), SH::T, smem, st, d, nrows, skip));
+        };
+        if (4 * d.n == M) go(k_t2_cols_dif<M, RB, R, true>);
+        else go(k_t2_cols_dif<M, RB, R, false>);
+        note_launch();
+        return;
+      }
+    }
     if constexpr (M >= kPersistMinM) {
       const size_t smem = (static_cast<size_t>(S::STRIDE) + d.n) * sizeof(cplx<R>);
       set_smem(k_t2_cols_p<M, RB, R>, smem);
@@ -942,6 +1030,16 @@ void launch_t1_cols_only(const OpDev<R>& d, int B, const SliceScalars* skip, cud
     constexpr int M = decltype(MC)::value, RB = decltype(RC)::value;
     using S = FftShape<M, RB>;
     const int nrows = d.herm_out ? M / 2 + 1 : M;  // the folded (Hermitian) grid: rows [0, m/2]
+    if constexpr (M == 8192 && sizeof(R) == 8) {  // fp64 8192-point rows split over two CTAs
+      if (dif_on()) {
+        using SH = FftShape<M / 2, RB>;
+        const size_t smem = static_cast<size_t>(SH::STRIDE) * sizeof(cplx<R>);
+        set_smem(k_t1_cols_dif<M, RB, R>, smem);
+        CK_LAUNCH(launch_k(k_t1_cols_dif<M, RB, R>, dim3(2 * nrows, B), SH::T, smem, st, d, nrows, skip));
+        note_launch();
+        return;
+      }
+    }
     if constexpr (M >= kPersistMinM) {
       // transposed K stores need >= 32 B per row segment; staging holds rpc full rows
       int rpc = std::max(1, static_cast<int>(32 / sizeof(cplx<R>)));
@@ -974,7 +1072,7 @@ template <typename R>
 void launch_t1_rows(const OpDev<R>& d, int B, const PbEpi<R>& e, cudaStream_t st) {
   if (d.herm_out) {  // real-part output from the folded grid: two image rows per complex transform
     if (e.mode == PB_COMPLEX) throw std::runtime_error("launch_t1_rows: complex output from a folded grid");
-    dispatch_m_rows(d.m, sizeof(cplx<R>), [&](auto MC, auto RC) {
+    dispatch_m_rows(d.m, sizeof(cplx<R>), static_cast<int64_t>(d.n / 2) * B, [&](auto MC, auto RC) {
       constexpr int M = decltype(MC)::value, RB = decltype(RC)::value;
       using S = FftShape<M, RB>;
       const int np = d.n / 2;
@@ -998,7 +1096,7 @@ void launch_t1_rows(const OpDev<R>& d, int B, const PbEpi<R>& e, cudaStream_t st
     });
     return;
   }
-  dispatch_m_rows(d.m, sizeof(cplx<R>), [&](auto MC, auto RC) {
+  dispatch_m_rows(d.m, sizeof(cplx<R>), static_cast<int64_t>(d.n) * B, [&](auto MC, auto RC) {
     constexpr int M = decltype(MC)::value, RB = decltype(RC)::value;
     using S = FftShape<M, RB>;
     constexpr size_t smem_p = (static_cast<size_t>(S::STRIDE) + M) * sizeof(cplx<R>);

@@ -322,7 +322,7 @@ struct tomo_op {
   int64_t nnz = 0, wt_rows = 0, wt_slots = 0;
   int Ppad = 0;
   int n_tasks = 0, n_heavy = 0, n_slots = 0;
-  Raw apod, tw, wbase, wxs, wys, wtent, wttasks, wtperm, wtheavy, wtslotheavy;
+  Raw apod, tw, twh, wbase, wxs, wys, wtent, wttasks, wtperm, wtheavy, wtslotheavy;
   Raw wperm;           // separable-W table position -> sample (grid-tile order)
   bool w_sorted = false;
   TaskSet gram;  // fused backend only
@@ -382,6 +382,7 @@ struct tomo_op {
     d.G32 = static_cast<int>(static_cast<int64_t>(g.m) * g.m / 32);
     d.apod = apod.as<R>();
     d.tw = tw.as<cplx<R>>();
+    d.tw_half = twh.as<cplx<R>>();
     d.w_base = wbase.as<int>();
     d.w_x = wxs.as<R>();
     d.w_y = wys.as<R>();
@@ -1097,8 +1098,15 @@ void build_tables(tomo_op* op) {
     tw[k].x = static_cast<R>(std::cos(ang));
     tw[k].y = static_cast<R>(std::sin(ang));
   }
+  std::vector<cplx<R>> twh(m / 2);
+  for (int k = 0; k < m / 2; ++k) {
+    const double ang = -2.0 * M_PI * static_cast<double>(k) / (m / 2);
+    twh[k].x = static_cast<R>(std::cos(ang));
+    twh[k].y = static_cast<R>(std::sin(ang));
+  }
   op->apod.upload(apod);
   op->tw.upload(tw);
+  op->twh.upload(twh);
   if (op->fused()) {
     if (op->src)
       gram_from_tspm<R>(op, *op->src);

@@ -60,6 +60,9 @@ LARGE_GEOMS = {
     "n2048_m4096": dict(n=2048, n_angles=8, n_b=2049, win_lo=-2, win_hi=3, tau=3 / 2048 ** 2),
     "n1024_R4_m4096": dict(n=1024, n_angles=8, n_b=1025, oversample=4, win_lo=-2, win_hi=3,
                            tau=np.pi * 3 / (1024 ** 2 * 4 * 3.5)),
+    # m = 8192 (c5's grid): fp64 grid rows split over two CTAs (k_t2_cols_dif / k_t1_cols_dif)
+    "n2048_R4_m8192": dict(n=2048, n_angles=4, n_b=2049, oversample=4, win_lo=-2, win_hi=3,
+                           tau=np.pi * 3 / (2048 ** 2 * 4 * 3.5)),
 }
 
 
