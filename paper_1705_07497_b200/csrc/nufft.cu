@@ -520,6 +520,102 @@ k_t1_rows_pk(OpDev<R> d, PbEpi<R> e, int rpc) {
   }
 }
 
+// PB on image-row pairs with the 8192-point fp64 row split over two CTAs (decimation in frequency, as
+// k_t1_cols_dif): CTA h transforms y_h from the Hermitian-extended pair row and owns outputs 2k + h.
+template <int M, int RB, typename R, int EPI>
+__global__ void __launch_bounds__(M / 2 / RB, 2) k_t1_rows_pk_dif(OpDev<R> d, PbEpi<R> e) {
+  constexpr int MH = M / 2;
+  using S = FftShape<MH, RB>;
+  using C2 = cplx<R>;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  C2* sm = reinterpret_cast<C2*>(smraw);
+  __shared__ double red_scratch[32];
+  const int b = blockIdx.y;
+  if ((e.mode == PB_CG_STEP || e.mode == PB_CGCG) && (e.red.sc[b].done || e.red.sc[b].frozen)) return;
+  if (e.mode == PB_CG_INIT && e.red.sc[b].frozen) return;
+  const int n = d.n, npair = n >> 1;
+  const int t = threadIdx.x, h = blockIdx.x & 1;
+  const int q = blockIdx.x >> 1;
+  const bool active = q < npair;
+  const int ta = active ? 2 * q : 0;
+  C2* row = sm;
+  const C2* Ka = d.K + (static_cast<size_t>(b) * n + ta) * M;
+  const C2* Kb = Ka + M;
+  const R a1a = active ? d.apod[ta] * e.scale * R(0.5) : R(0);
+  const R a1b = active ? d.apod[ta + 1] * e.scale * R(0.5) : R(0);
+  const size_t base = (static_cast<size_t>(b) * n + ta) * n;  // row ta; row ta+1 at + n
+  const R lam = static_cast<R>(e.sys.lambda), shift = static_cast<R>(e.sys.shift);
+  const R* p = e.p ? e.p + static_cast<size_t>(b) * n * n : nullptr;
+  double acc0 = 0.0, acc1 = 0.0;
+  auto full = [&](int k) -> C2 {  // the pair row Xa + i Xb at k in [0, M)
+    C2 xa, xb;
+    if (k <= M / 2) {
+      xa = Ka[k];
+      xb = Kb[k];
+    } else {
+      xa = cconj(Ka[M - k]);
+      xb = cconj(Kb[M - k]);
+    }
+    return mk<C2>(xa.x - xb.y, xa.y + xb.x);  // xa + i xb
+  };
+  auto load = [&](int i) -> C2 {
+    const C2 x0 = full(i), x1 = full(i + MH);
+    return h == 0 ? cadd(x0, x1) : cmul(csub(x0, x1), __ldg(&d.tw[i]));
+  };
+  auto epi = [&](int t1, size_t o, int t2, R v) {
+    if constexpr (EPI == 1) {
+      e.out_r[o] = v;
+    } else {
+      const R pv = p[static_cast<size_t>(t1) * n + t2];
+      R ax = v;
+      if (lam != R(0)) ax += lam * ktk_at<R>(p, n, t1, t2, pv);
+      ax += shift * pv;
+      if (e.mode != PB_CG_INIT) {
+        e.ap[o] = ax;
+        acc0 += static_cast<double>(pv) * ax;
+        acc1 += static_cast<double>(pv) * pv;
+      } else {
+        const R bv = e.b[o];
+        const R rv = bv - ax;
+        e.ap[o] = rv;
+        e.p_out[o] = rv;
+        e.x_out[o] = pv;
+        acc0 += static_cast<double>(rv) * rv;
+        acc1 += static_cast<double>(bv) * bv;
+      }
+    }
+  };
+  auto store = [&](int kh, C2 X) {
+    const int t2 = (2 * kh + h + n / 2) & (M - 1);
+    if (t2 >= n) return;
+    const R ap = __ldg(&d.apod[t2]);
+    epi(ta, base + t2, t2, X.x * (a1a * ap));
+    epi(ta + 1, base + n + t2, t2, X.y * (a1b * ap));
+  };
+  fft_row<MH, RB, false, C2, 0>(row, d.tw_half, t, active, load, store);
+  if (EPI == 2) {
+    double t0s, t1s;
+    SliceScalars& sc = e.red.sc[b];
+    double* part = e.red.part + static_cast<size_t>(b) * MAX_PART_BLOCKS * 2;
+    if (reduce2_last(acc0, acc1, part, gridDim.x, blockIdx.x, &sc.counter[0], red_scratch, t0s, t1s) &&
+        threadIdx.x == 0) {
+      if (e.mode == PB_CGCG) {
+        cgcg_finalize(sc, t0s, t1s, e.sys, e.step);
+      } else if (e.mode == PB_CG_STEP) {
+        sc.pap = t0s;
+        sc.pp = t1s;
+      } else {
+        sc.rr[0] = t0s;
+        sc.rs_last = t0s;
+        sc.bb = t1s;
+        sc.done = 0;
+        sc.steps_run = 0;
+        sc.min_ritz = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+      }
+    }
+  }
+}
+
 // ================================================================ persistent FFT-row kernels
 // Grid (CTAs per slice, B). Each CTA walks its slice's rows g = blockIdx.x, blockIdx.x +
 // gridDim.x, ... (rpc rows per step). The next step's input rows are copied global -> smem
@@ -1072,6 +1168,22 @@ template <typename R>
 void launch_t1_rows(const OpDev<R>& d, int B, const PbEpi<R>& e, cudaStream_t st) {
   if (d.herm_out) {  // real-part output from the folded grid: two image rows per complex transform
     if (e.mode == PB_COMPLEX) throw std::runtime_error("launch_t1_rows: complex output from a folded grid");
+    if constexpr (sizeof(R) == 8) {
+    if (d.m == 8192 && dif_on()) {  // fp64 8192-point rows split over two CTAs
+      using SH = FftShape<4096, 16>;
+      const size_t smem = static_cast<size_t>(SH::STRIDE) * sizeof(cplx<R>);
+      const int np = d.n / 2;
+      if (2 * np > MAX_PART_BLOCKS) throw std::runtime_error("launch_t1_rows: too many row pairs for one reduction");
+      auto go = [&](auto kern) {
+        set_smem(kern, smem);
+        CK_LAUNCH(launch_k(kern, dim3(2 * np, B), SH::T, smem, st, d, e));
+      };
+      if (e.mode == PB_REAL) go(k_t1_rows_pk_dif<8192, 16, R, 1>);
+      else go(k_t1_rows_pk_dif<8192, 16, R, 2>);
+      note_launch();
+      return;
+    }
+    }
     dispatch_m_rows(d.m, sizeof(cplx<R>), static_cast<int64_t>(d.n / 2) * B, [&](auto MC, auto RC) {
       constexpr int M = decltype(MC)::value, RB = decltype(RC)::value;
       using S = FftShape<M, RB>;
