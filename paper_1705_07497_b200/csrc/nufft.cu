@@ -24,6 +24,7 @@
 #include "kernels.h"
 
 #include <cuda_pipeline.h>
+#include <cooperative_groups.h>
 
 namespace tomo_b200 {
 
@@ -807,6 +808,108 @@ k_t1_rows_p(OpDev<R> d, PbEpi<R> e) {
 // CTA (h = blockIdx.x & 1) loads the whole row, combines its halves on load and transforms M/2 points
 // in 70 KB of shared memory (two CTAs per SM, one loading while the other computes).
 
+// P1 on image-row pairs at fp64 m = 8192, split over a cluster of two CTAs (decimation in frequency).
+// The fused CG update must write each image element once, so CTA 0 updates (and deapodises, packs)
+// the pair's t2 in [n/2, n) and CTA 1 the t2 in [0, n/2) into its shared memory; after a cluster
+// barrier each CTA's first pass reads both halves, one of them from the peer CTA's shared memory
+// (DSMEM). Every element of y_h has at most one non-zero padded input (n <= m/2). CTA h then owns
+// the spectra Z[2k+h]: the Hermitian separation pairs Z[k] with Z[-k], same parity, same CTA.
+// Q: 4n == M (quarter-pruned first pass).
+template <int M, int RB, typename R, bool Q, int IN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(M / 2 / RB, 2)
+k_t2_rows_pk_dif(OpDev<R> d, const void* __restrict__ in, PUpd<R> pu) {
+  namespace cgr = cooperative_groups;
+  constexpr int MH = M / 2;
+  using S = FftShape<MH, RB>;
+  using C2 = cplx<R>;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  C2* row = reinterpret_cast<C2*>(smraw);
+  C2* xs = row + S::STRIDE;  // this CTA's half of the packed, updated, deapodised input (n/2 entries)
+  const int b = blockIdx.y;
+  double beta = 0.0, alpha = 0.0;
+  if constexpr (IN == 3) {
+    const SliceScalars& sc = pu.red.sc[b];
+    if (sc.done || sc.frozen) return;  // cluster-uniform (same slice)
+    beta = sc.cg_beta;
+    alpha = sc.cg_alpha;
+  } else if constexpr (IN == 2) {
+    if (!cg_step_live(pu.red, b, pu.step, beta)) return;
+  } else {
+    if (pu.red.sc && pu.red.sc[b].frozen) return;
+  }
+  const int n = Q ? M / 4 : d.n, npair = n >> 1, nh = n / 2;
+  const int q = blockIdx.x >> 1, h = blockIdx.x & 1, t = threadIdx.x;
+  if (q >= npair) return;  // cluster-uniform
+  cgr::cluster_group cluster = cgr::this_cluster();
+  const size_t base = (static_cast<size_t>(b) * n + 2 * q) * n;  // row 2q; row 2q+1 at + n
+  const R a1a = d.apod[2 * q], a1b = d.apod[2 * q + 1];
+  const R bt = static_cast<R>(beta), al = static_cast<R>(alpha);
+  auto value = [&](size_t o) -> R {
+    if constexpr (IN == 3) {
+      R rv = pu.r[o];
+      if (pu.step > 0) {
+        R pv = rv, sv = pu.w[o];
+        if (pu.step > 1) {
+          pv += bt * pu.p[o];
+          sv += bt * pu.s[o];
+        }
+        const R xv = pu.x[o] + al * pv;
+        rv -= al * sv;
+        pu.p[o] = pv;
+        pu.s[o] = sv;
+        pu.x[o] = xv;
+        pu.r[o] = rv;
+        if (!finite_r(xv)) pu.red.sc[b].nonfinite = 1;
+      }
+      return rv;
+    } else if constexpr (IN == 2) {
+      R pv = pu.p[o];
+      if (pu.step > 0) {
+        pv = pu.r[o] + bt * pv;
+        pu.p[o] = pv;
+      }
+      return pv;
+    } else {
+      return reinterpret_cast<const R*>(in)[o];
+    }
+  };
+  // CTA 0: t2 = nh + j (padded positions j in [0, n/2)); CTA 1: t2 = j (positions M - n/2 + j)
+  for (int j = t; j < nh; j += blockDim.x) {
+    const int t2 = h == 0 ? nh + j : j;
+    const R ap = __ldg(&d.apod[t2]);
+    const R va = value(base + t2) * (a1a * ap);
+    const R vb = value(base + n + t2) * (a1b * ap);
+    xs[j] = mk<C2>(va, -vb);  // inverse transform: conj in, conj out
+  }
+  cluster.sync();
+  const C2* xa = cluster.map_shared_rank(xs, 0);  // positions [0, n/2)
+  const C2* xb = cluster.map_shared_rank(xs, 1);  // positions [M - n/2, M)
+  auto load = [&](int i) -> C2 {
+    C2 v = czero<C2>();
+    if (i < nh) {
+      v = xa[i];
+    } else if (i >= MH - nh) {
+      v = xb[i - (MH - nh)];
+      if (h == 1) v = mk<C2>(-v.x, -v.y);
+    }
+    return h == 0 ? v : cmul(v, __ldg(&d.tw[i]));
+  };
+  auto store = [&](int k, C2 v) { row[pad16(k)] = cconj(v); };
+  fft_row<MH, RB, true, C2, Q ? 1 : 0>(row, d.tw_half, t, true, load, store);
+  cluster.sync();  // the peer's reads of this CTA's xs are done before either CTA exits
+  // spectra of the two rows at k = 2k' + h in [0, M/2]: Z[k] = row[k'], Z[M - k] = row[(MH - k' - h) % MH]
+  C2* H = d.H + static_cast<size_t>(b) * M * n + 2 * q;
+  const R hf = R(0.5);
+  for (int idx = t; idx < 2 * (MH / 2 + 1); idx += blockDim.x) {
+    const int kp = idx >> 1, c = idx & 1;
+    const int k = 2 * kp + h;
+    if (k > M / 2) continue;
+    const C2 z = row[pad16(kp)], zm = row[pad16((MH - kp - h) & (MH - 1))];
+    H[static_cast<size_t>(k) * n + c] = c ? mk<C2>(hf * (z.y + zm.y), hf * (zm.x - z.x))
+                                          : mk<C2>(hf * (z.x + zm.x), hf * (z.y - zm.y));
+  }
+}
+
 // P2: inverse FFT along ix of the H row (conj in / conj out), natural stores g[iy][2k+h].
 // Q: 4n == M, the non-zero inputs of y are its first and last quarter (compile-time pruning).
 template <int M, int RB, typename R, bool Q>
@@ -999,6 +1102,30 @@ void set_smem(K kernel, size_t bytes) {
 
 template <typename R>
 void launch_t2_rows(const OpDev<R>& d, int B, const void* in, bool in_complex, const PUpd<R>& pu, cudaStream_t st) {
+  if constexpr (sizeof(R) == 8) {
+    if (d.herm_in && !in_complex && d.m == 8192 && dif_on()) {  // fp64 8192: a CTA-pair cluster per row pair
+      constexpr int M = 8192, RB = 16;
+      using SH = FftShape<M / 2, RB>;
+      const size_t smem = (static_cast<size_t>(SH::STRIDE) + d.n / 2) * sizeof(cplx<R>);
+      const int mode = !pu.enabled ? 1 : pu.cgcg ? 3 : 2;
+      auto go = [&](auto kern) {
+        set_smem(kern, smem);
+        CK_LAUNCH(launch_k(kern, dim3(2 * (d.n / 2), B), SH::T, smem, st, d, in, pu));
+      };
+      auto go_q = [&](auto QC) {
+        constexpr bool QQ = decltype(QC)::value;
+        switch (mode) {
+          case 1: go(k_t2_rows_pk_dif<M, RB, R, QQ, 1>); break;
+          case 2: go(k_t2_rows_pk_dif<M, RB, R, QQ, 2>); break;
+          default: go(k_t2_rows_pk_dif<M, RB, R, QQ, 3>); break;
+        }
+      };
+      if (4 * d.n == M) go_q(std::true_type{});
+      else go_q(std::false_type{});
+      note_launch();
+      return;
+    }
+  }
   if (d.herm_in && !in_complex) {  // real image: two rows per complex transform, H rows [0, m/2]
     dispatch_m_rows(d.m, sizeof(cplx<R>), static_cast<int64_t>(d.n / 2) * B, [&](auto MC, auto RC) {
       constexpr int M = decltype(MC)::value, RB = decltype(RC)::value;
