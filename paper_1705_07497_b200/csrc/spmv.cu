@@ -436,7 +436,7 @@ void launch_w(const OpDev<R>& d, int B, const cplx<R>* grid, cplx<R>* samples, c
       else
         go2(WC, std::false_type{});
     };
-    static const int vec_on = env_int("TOMO_W_VEC", 1);  // A/B: 0 = scalar gathers for fp32 too
+    static const int vec_on = env_int("TOMO_W_VEC", 1);  // A/B: 0 = scalar gathers
     if constexpr (sizeof(R) == 4) {
       if (vec_on && d.w == 6) {
         auto gov = [&](auto HC) {

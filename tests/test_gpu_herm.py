@@ -101,23 +101,25 @@ import sys, numpy as np, torch
 sys.path.insert(0, sys.argv[1])
 import paper_1705_07497_b200 as T
 from oracle import oracle as O
-spec = eval(sys.argv[2])
+spec = eval(sys.argv[2]); prec = sys.argv[4]
 og = O.Geometry(**spec)
 op = T.make_direct_backend(T.Geometry(n=og.n, n_angles=og.n_angles, n_b=og.n_b, oversample=og.oversample,
-                                      win_lo=og.win_lo, win_hi=og.win_hi, tau=og.tau), precision="f32")
+                                      win_lo=og.win_lo, win_hi=og.win_hi, tau=og.tau), precision=prec)
+rt, ct = (np.float64, np.complex128) if prec == "f64" else (np.float32, np.complex64)
 rng = np.random.default_rng(5)
 outs = []
 for B in (1, 3, 7):
     u = rng.standard_normal((B, og.n, og.n))
     uc = u + 1j * rng.standard_normal((B, og.n, og.n))
-    outs.append(op.forward_real(torch.from_numpy(u.astype(np.float32)).cuda()).cpu().numpy().ravel())
-    outs.append(op.forward(torch.from_numpy(uc.astype(np.complex64)).cuda()).cpu().numpy().ravel())
+    outs.append(op.forward_real(torch.from_numpy(u.astype(rt)).cuda()).cpu().numpy().ravel())
+    outs.append(op.forward(torch.from_numpy(uc.astype(ct)).cuda()).cpu().numpy().ravel())
 np.save(sys.argv[3], np.concatenate(outs))
 """
 
 
+@pytest.mark.parametrize("prec", ["f32"])
 @pytest.mark.parametrize("name", ["n16_m32", "width6_n64", "n256_c1", "n1024_R4_m4096"])
-def test_w_vector_rows_bit_identical_to_scalar_gathers(T, name, tmp_path):
+def test_w_vector_rows_bit_identical_to_scalar_gathers(T, name, prec, tmp_path):
     """fp32 width-6 W with 16-byte window-row loads (k_w_sep_v6, the default) vs the scalar gathers
     (TOMO_W_VEC=0): same arithmetic in the same order, bit-identical samples on the half grid
     (mirrored rows) and the full grid, single and batched launches, incl. edge-wrapping windows."""
@@ -129,6 +131,6 @@ def test_w_vector_rows_bit_identical_to_scalar_gathers(T, name, tmp_path):
     for vec in ("1", "0"):
         env = dict(os.environ, TOMO_AB="1", TOMO_W_VEC=vec)
         path = str(tmp_path / f"w{vec}.npy")
-        subprocess.check_call([sys.executable, "-c", _W_CHILD, root, repr(GEOMS[name]), path], env=env)
+        subprocess.check_call([sys.executable, "-c", _W_CHILD, root, repr(GEOMS[name]), path, prec], env=env)
         outs.append(np.load(path))
     assert np.array_equal(outs[0], outs[1])
