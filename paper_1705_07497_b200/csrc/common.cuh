@@ -133,15 +133,45 @@ TOMO_DEV double block_sum(double v, double* scratch) {
   return r;
 }
 
+// Block-wide sums of two doubles per thread in one pass (results valid in all threads).
+TOMO_DEV void block_sum2(double& a, double& b) {
+  __shared__ double sc2[64];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nw = (blockDim.x + 31) >> 5;
+  a = warp_sum(a);
+  b = warp_sum(b);
+  __syncthreads();
+  if (lane == 0) {
+    sc2[wid] = a;
+    sc2[32 + wid] = b;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    double ta = lane < nw ? sc2[lane] : 0.0, tb = lane < nw ? sc2[32 + lane] : 0.0;
+    ta = warp_sum(ta);
+    tb = warp_sum(tb);
+    if (lane == 0) {
+      sc2[0] = ta;
+      sc2[32] = tb;
+    }
+  }
+  __syncthreads();
+  a = sc2[0];
+  b = sc2[32];
+  __syncthreads();
+}
+
 // Two-value block reduction with "last block finishes": every block writes its partial
 // pair to part[2*blk..], takes a ticket; the block that takes the last ticket sums all
-// nblk pairs in fixed order (so the result is deterministic), resets the ticket counter
-// and returns true with the totals in t0/t1 (valid in all of its threads).
+// nblk pairs in a fixed order (every thread loads its strided share, then one block tree: one
+// round trip for the partials instead of a warp walking them serially), so the result is
+// deterministic, resets the ticket counter and returns true with the totals in t0/t1 (valid in
+// all of its threads). `scratch` is unused (kept for the callers' signature).
 TOMO_DEV bool reduce2_last(double v0, double v1, double* part, int nblk, int blk, unsigned* counter,
                            double* scratch, double& t0, double& t1) {
+  (void)scratch;
   __shared__ int s_last;
-  v0 = block_sum(v0, scratch);
-  v1 = block_sum(v1, scratch);
+  block_sum2(v0, v1);
   if (threadIdx.x == 0) {
     part[2 * blk] = v0;
     part[2 * blk + 1] = v1;
@@ -153,23 +183,15 @@ TOMO_DEV bool reduce2_last(double v0, double v1, double* part, int nblk, int blk
   const bool last = s_last != 0;
   if (!last) return false;
   __threadfence();
-  if (threadIdx.x < 32) {
-    double a = 0.0, b = 0.0;
-    for (int i = threadIdx.x; i < nblk; i += 32) {
-      a += __ldcg(&part[2 * i]);
-      b += __ldcg(&part[2 * i + 1]);
-    }
-    a = warp_sum(a);
-    b = warp_sum(b);
-    if (threadIdx.x == 0) {
-      scratch[0] = a;
-      scratch[1] = b;
-      *counter = 0u;
-    }
+  double a = 0.0, b = 0.0;
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) {
+    a += __ldcg(&part[2 * i]);
+    b += __ldcg(&part[2 * i + 1]);
   }
-  __syncthreads();
-  t0 = scratch[0];
-  t1 = scratch[1];
+  block_sum2(a, b);
+  if (threadIdx.x == 0) *counter = 0u;
+  t0 = a;
+  t1 = b;
   return true;
 }
 
