@@ -598,6 +598,47 @@ def config_dict(name, c, world):
             "parallelism": f"{par} x{world}"}
 
 
+def quick_config_line(name, world, rank, local, torch, T, peak, flush, steps=3, warmup=3):
+    """A short device-timed measurement of another BASELINE config inside the default (c2) run, so
+    that all five configs appear in the driver-recorded line (`other_configs`). Same timing rules:
+    warm-up, L2 flushed between steps, CUDA events; no e2e / CPU arm (use `--config` for the full
+    line of that config)."""
+    c = dict(CONFIGS[name])
+    wl = Workload(name, c, world, rank, local, torch)
+    for _ in range(warmup):
+        wl.step()
+    torch.cuda.synchronize()
+    l0 = T.kernel_launches()
+    r0 = wl.replayed_launches
+    ms = 0.0
+    for _ in range(steps):
+        flush_l2(torch, flush)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        wl.step()
+        e1.record()
+        e1.synchronize()
+        ms += e0.elapsed_time(e1)
+    torch.cuda.synchronize()
+    launches = T.kernel_launches() - l0 + (wl.replayed_launches - r0)
+    value = wl.units_per_step * steps / (ms * 1e-3)
+    out = {"metric": c["metric"], "value": value, "unit": c["unit"], "ms_per_step": ms / steps, "steps": steps,
+           "warmup": warmup, "dtype": c["prec"], "config": config_dict(name, c, world), "gpu_launches": int(launches)}
+    k = c["kind"]
+    if k != "sb_sur":
+        applies = {"sb": c.get("iters", 1) * (c.get("cg", 0) + 1) * wl.units_per_step,
+                   "cp": wl.units_per_step, "c1": wl.units_per_step, "apply": wl.units_per_step}[k]
+        per_apply = apply_bytes(c, wl.op.info.wt_rows, complex_io=(k == "apply"), B=1)
+        gbs = per_apply * applies * steps / (ms * 1e-3) / 1e9
+        out["apply_in_step"] = {"bytes_per_apply": int(per_apply), "achieved": round(gbs, 1), "peak": peak,
+                                "unit": "GB/s", "frac": round(gbs / peak, 4)}
+    wl.op.close()
+    del wl
+    torch.cuda.empty_cache()
+    return out
+
+
 # ----------------------------------------------------------------------------- main
 def main():
     ap = argparse.ArgumentParser()
@@ -609,6 +650,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--batch", type=int, default=0,
                     help="c1/c3: independent inputs per apply call; c2: slices solved per step (0: config)")
+    ap.add_argument("--no-other-configs", action="store_true",
+                    help="default (c2) run: skip the short c1/c3/c4/c5 measurements reported in `other_configs`")
     ap.add_argument("--slices", type=int, default=0,
                     help="c4: total slices (0: config's 256); e.g. 32 on one GPU = one rank's share at N=8")
     args = ap.parse_args()
@@ -735,8 +778,21 @@ def main():
         cpu = {"value": v, "unit": c["unit"], "cores": cb.cores, "kind": cb.kind, "sample": cb.describe(),
                "cpu_model": cb.model, "nproc": host_cpu()[1], "sample_wall_s": round(wall, 2)}
 
+    info = wl.op.info
+    others = None
+    if world == 1 and args.config == "c2" and not args.no_other_configs and not args.batch:
+        # the other four BASELINE configs, briefly, in the same run (device-timed values only)
+        wl.op.close()
+        del wl
+        torch.cuda.empty_cache()
+        others = {}
+        for name in ("c1", "c3", "c4", "c5"):
+            try:
+                others[name] = quick_config_line(name, world, rank, local, torch, T, peak, flush)
+            except Exception as e:  # never lose the headline line to a side measurement
+                others[name] = {"error": f"{type(e).__name__}: {e}"}
+
     if rank == 0:
-        info = wl.op.info
         line = {
             "metric": c["metric"], "value": value, "unit": c["unit"], "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
@@ -752,6 +808,8 @@ def main():
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
+        if others is not None:
+            line["other_configs"] = others
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
