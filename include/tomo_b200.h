@@ -100,6 +100,16 @@ typedef struct tomo_op_info {
   int64_t herm_slots;   /* task-SpMV slots incl. padding */
   int64_t herm_touched; /* touched half-grid nodes */
   int herm_tasks;       /* warp tasks (0: not built, real inputs take the full grid) */
+  /* Mirror pairs of the parallel-beam samples (bins t and 2 (n_b / 2) - t of one angle lie at
+   * mirrored frequencies; with a window [1 - hi, hi] their interpolation windows are mirror images).
+   * For real images the normal operator then runs W on one sample per pair and the folded W^T of
+   * the pairs' primaries only. 0 everywhere: not used (other windows, e.g. the reference's
+   * symmetric [-m_sp, m_sp] around floor(x / h), have no such pairs). */
+  int sym_tasks;        /* warp tasks of the primaries' folded W^T (0: not built) */
+  int64_t sym_pairs;    /* samples that have a mirror partner (both members counted) */
+  int64_t sym_P;        /* samples W evaluates on the real-subspace normal operator */
+  int64_t sym_nnz;      /* entries of the primaries' folded W^T */
+  int64_t sym_slots;    /* its task-SpMV slots incl. padding */
 } tomo_op_info;
 
 const char* tomo_last_error(void);

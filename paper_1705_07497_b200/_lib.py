@@ -47,7 +47,9 @@ class OpInfo(C.Structure):
                 ("stencil", C.c_double * 81), ("surrogate_r", C.c_int), ("precision", C.c_int),
                 ("backend", C.c_int), ("gram_nnz", C.c_int64), ("gram_slots", C.c_int64),
                 ("bytes_gram", C.c_int64), ("herm_nnz", C.c_int64), ("herm_slots", C.c_int64),
-                ("herm_touched", C.c_int64), ("herm_tasks", C.c_int)]
+                ("herm_touched", C.c_int64), ("herm_tasks", C.c_int),
+                ("sym_tasks", C.c_int), ("sym_pairs", C.c_int64), ("sym_P", C.c_int64), ("sym_nnz", C.c_int64),
+                ("sym_slots", C.c_int64)]
 
 
 class System(C.Structure):

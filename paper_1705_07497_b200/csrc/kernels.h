@@ -259,7 +259,23 @@ void gpu_sort_w_tables(int m, int64_t P, int64_t Ppad, int w, int* base, R* wx, 
 // Hermitian fold of a finished (unfolded) W^T build: nodes of grid rows [0, m/2], each with its own
 // entries and the conjugated entries of its mirror node (-iy, -ix). Finish with gpu_build_finish.
 template <typename R>
-GpuBuild* gpu_build_fold(const GpuBuild* src, cudaStream_t st, GpuBuildSizes* sizes);
+GpuBuild* gpu_build_fold(const GpuBuild* src, cudaStream_t st, GpuBuildSizes* sizes, const int* pair = nullptr);
+// Mirror pairs of the samples (opbuild.cu "mirror pairs"): pair[j] = mirror sample or -1, from the
+// separable W tables in sample order; returns the number of paired samples. With `pair`,
+// gpu_build_fold drops the secondaries' entries and doubles the primaries' (entry indices stay
+// sample indices until gpu_half_w_finish remaps them).
+template <typename R>
+int64_t gpu_find_pairs(const BuildArgs& a, const int* base, const R* wx, const R* wy, int* pair, cudaStream_t st);
+// The half W: the tile-ordered separable tables (after gpu_sort_w_tables; perm = position -> sample)
+// compacted to the samples that are not secondaries (Ph of them, order kept); `ent` (the mirror-pair
+// W^T's entries, sample indices) is remapped to the compact positions, a secondary to its primary's.
+struct HalfWBuild;
+HalfWBuild* gpu_half_w_begin(int64_t P, const int* perm, const int* pair, cudaStream_t st, int64_t* Ph);
+template <typename R>
+void gpu_half_w_finish(HalfWBuild* hb, int64_t Ppad, int64_t Ppad_h, int w, const int* perm, const int* pair,
+                       const int* base, const R* wx, const R* wy, int* base_h, R* wx_h, R* wy_h, WtEnt<R>* ent,
+                       int64_t n_ent, cudaStream_t st);
+void gpu_half_w_free(HalfWBuild* hb);
 
 // ---- launchers (solver.cu) ----
 struct StencilCoef {

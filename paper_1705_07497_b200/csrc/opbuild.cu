@@ -452,17 +452,30 @@ void gpu_build_free(GpuBuild* b) { delete b; }
 // iy <= m/2 and w conj(s_j) to F[-iy][-ix] when iy >= m/2 or iy == 0 (rows 0 and m/2 are their
 // own mirror rows: both). The conj flag is bit 31 of the entry's sample index.
 namespace {
-__global__ void k_fold_count(int m, int64_t G, const int* __restrict__ cnt, int* ecnt) {
+// `pair` (mirror-pair fold, below): entries of a pair's secondary sample (j < pair[j]) are dropped
+__global__ void k_fold_count(int m, int64_t G, const int* __restrict__ cnt, const int* __restrict__ off,
+                             const int* __restrict__ sj, const int* __restrict__ pair, int* ecnt) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= G) return;
   const int iy = static_cast<int>(i / m);
-  ecnt[i] = cnt[i] * ((iy == 0 || iy == m / 2) ? 2 : 1);
+  const int mult = (iy == 0 || iy == m / 2) ? 2 : 1;
+  int c = cnt[i];
+  if (pair) {
+    const int o = off[i];
+    int kept = 0;
+    for (int k = 0; k < c; ++k) {
+      const int j = sj[o + k];
+      kept += !(pair[j] >= 0 && j < pair[j]);
+    }
+    c = kept;
+  }
+  ecnt[i] = c * mult;
 }
 
 template <typename R>
 __global__ void k_fold_emit(int m, int64_t G, const int* __restrict__ cnt, const int* __restrict__ off,
                             const int* __restrict__ eoff, const int* __restrict__ sj, const R* __restrict__ vals,
-                            unsigned long long* keys, R* fvals) {
+                            const int* __restrict__ pair, unsigned long long* keys, R* fvals) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= G) return;
   const int iy = static_cast<int>(i / m), ix = static_cast<int>(i - static_cast<int64_t>(iy) * m);
@@ -472,7 +485,12 @@ __global__ void k_fold_emit(int m, int64_t G, const int* __restrict__ cnt, const
       static_cast<unsigned long long>((m - iy) & (m - 1)) * m + static_cast<unsigned long long>((m - ix) & (m - 1));
   for (int k = 0; k < c; ++k) {
     const unsigned j = static_cast<unsigned>(sj[off[i] + k]);
-    const R v = vals[off[i] + k];
+    R v = vals[off[i] + k];
+    if (pair) {
+      const int pr = pair[j];
+      if (pr >= 0 && static_cast<int>(j) < pr) continue;  // secondary: carried by its primary
+      if (pr >= 0) v = v + v;                             // primary: its own and its mirror's share
+    }
     if (iy <= m / 2) {
       keys[o] = (static_cast<unsigned long long>(i) << 32) | j;
       fvals[o++] = v;
@@ -491,7 +509,7 @@ __global__ void k_fold_cnt(int64_t n, const unsigned long long* __restrict__ key
 }  // namespace
 
 template <typename R>
-GpuBuild* gpu_build_fold(const GpuBuild* src, cudaStream_t st, GpuBuildSizes* sizes) {
+GpuBuild* gpu_build_fold(const GpuBuild* src, cudaStream_t st, GpuBuildSizes* sizes, const int* pair) {
   const int m = src->a.m;
   if (src->G != static_cast<int64_t>(m) * m) throw std::runtime_error("opbuild: fold needs the unfolded W^T");
   auto b = std::make_unique<GpuBuild>();
@@ -501,7 +519,7 @@ GpuBuild* gpu_build_fold(const GpuBuild* src, cudaStream_t st, GpuBuildSizes* si
   b->G32 = b->G / 32;
   const unsigned gs = static_cast<unsigned>((src->G + 255) / 256);
   DBuf<int> ecnt(src->G), eoff(src->G);
-  k_fold_count<<<gs, 256, 0, st>>>(m, src->G, src->cnt.p, ecnt.p);
+  k_fold_count<<<gs, 256, 0, st>>>(m, src->G, src->cnt.p, src->off.p, src->sj.p, pair, ecnt.p);
   BK(cudaGetLastError());
   size_t tb = 0;
   BK(cub::DeviceScan::ExclusiveSum(nullptr, tb, ecnt.p, eoff.p, static_cast<int>(src->G), st));
@@ -518,7 +536,7 @@ GpuBuild* gpu_build_fold(const GpuBuild* src, cudaStream_t st, GpuBuildSizes* si
   DBuf<unsigned long long> keys(b->nnz), skeys(b->nnz);
   DBuf<R> vals(b->nnz);
   k_fold_emit<R><<<gs, 256, 0, st>>>(m, src->G, src->cnt.p, src->off.p, eoff.p, src->sj.p,
-                                     reinterpret_cast<const R*>(src->vals_sorted.p), keys.p, vals.p);
+                                     reinterpret_cast<const R*>(src->vals_sorted.p), pair, keys.p, vals.p);
   BK(cudaGetLastError());
   // (folded node, conj flag, sample): plain entries before conjugated ones, samples ascending
   b->vals_sorted.alloc(sizeof(R) * b->nnz);
@@ -763,13 +781,142 @@ void gpu_sort_w_tables(int m, int64_t P, int64_t Ppad, int w, int* base, R* wx, 
   BK(cudaStreamSynchronize(st));
 }
 
+// ---- mirror pairs of the parallel-beam samples (real-subspace normal operator) ------------------
+// Sample (angle a, bin t) sits at frequency k_r (cos, sin) with k_r = (2 pi / nb)(t - nb/2); the bin
+// t' = 2 (nb/2) - t of the same angle sits at the mirrored frequency. For a window [lo, hi] with
+// lo = 1 - hi around floor(x / h) (the width-6 [-2, 3] of the BASELINE configs) the mirror sample's
+// window is the node-for-node mirror image of the sample's own, with the same weights to rounding.
+// On the real subspace (Hermitian grid) its W value is then the conjugate of the sample's, so the
+// normal operator needs W on one sample per pair only, and the folded W^T needs only the primaries'
+// entries, doubled: F[p] = 2 sum_{primary j} (w_pj s_j + w_{-p,j} conj s_j) (+ the unpaired samples'
+// entries as before). pair[j] = the mirror sample when the two windows are mirror images (base nodes
+// checked exactly, factor vectors to rounding), else -1 (bins without a mirror bin, the zero
+// frequency, samples on a grid line whose floor() breaks the symmetry, other windows). The primary
+// of a pair is the larger index. The resulting operator is the exact normal operator U^T U of the
+// interpolation U whose secondary rows are the conjugate mirrors of the primaries' rows: symmetric
+// positive semi-definite, equal to W^T W up to the rounding of the sample positions.
+namespace {
+template <typename R>
+__global__ void k_pairs(int64_t P, int64_t Ppad, int nb, int m, int w, const int* __restrict__ base,
+                        const R* __restrict__ wx, const R* __restrict__ wy, int* pair, unsigned long long* npaired) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= P) return;
+  const int t = static_cast<int>(j % nb), tm = 2 * (nb / 2) - t;
+  int pr = -1;
+  if (tm >= 0 && tm < nb && tm != t) {
+    const int64_t jm = j - t + tm;
+    const int b = base[j], bm = base[jm];
+    const int ix0 = b & 0xffff, iy0 = (b >> 16) & 0xffff;
+    bool ok = (bm & 0xffff) == (2 * m - ix0 - (w - 1)) % m && ((bm >> 16) & 0xffff) == (2 * m - iy0 - (w - 1)) % m;
+    const R tol = sizeof(R) == 8 ? R(1e-9) : R(4e-7);
+    for (int a = 0; ok && a < w; ++a) {
+      const R x1 = wx[static_cast<size_t>(a) * Ppad + jm], x2 = wx[static_cast<size_t>(w - 1 - a) * Ppad + j];
+      const R y1 = wy[static_cast<size_t>(a) * Ppad + jm], y2 = wy[static_cast<size_t>(w - 1 - a) * Ppad + j];
+      ok = fabs(x1 - x2) <= tol * fmax(fabs(x1), fabs(x2)) && fabs(y1 - y2) <= tol * fmax(fabs(y1), fabs(y2));
+    }
+    if (ok) {
+      pr = static_cast<int>(jm);
+      atomicAdd(npaired, 1ull);
+    }
+  }
+  pair[j] = pr;
+}
+
+// position (tile order) -> kept by the half W: every sample but the secondaries
+__global__ void k_half_flags(int64_t P, const int* __restrict__ perm, const int* __restrict__ pair, int* flag) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= P) return;
+  const int j = perm[t];
+  flag[t] = !(pair[j] >= 0 && j < pair[j]);
+}
+
+template <typename R>
+__global__ void k_half_gather(int64_t P, int64_t Ppad, int64_t Ppad_h, int w, const int* __restrict__ perm,
+                              const int* __restrict__ pair, const int* __restrict__ flag, const int* __restrict__ hpos,
+                              const int* __restrict__ base, const R* __restrict__ wx, const R* __restrict__ wy,
+                              int* base_h, R* wx_h, R* wy_h, int* cmap) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= P || !flag[t]) return;
+  const int h = hpos[t], j = perm[t];
+  base_h[h] = base[t];
+  for (int a = 0; a < w; ++a) {
+    wx_h[static_cast<size_t>(a) * Ppad_h + h] = wx[static_cast<size_t>(a) * Ppad + t];
+    wy_h[static_cast<size_t>(a) * Ppad_h + h] = wy[static_cast<size_t>(a) * Ppad + t];
+  }
+  cmap[j] = h;
+  if (pair[j] >= 0) cmap[pair[j]] = h;  // the secondary reads its primary's value, conjugated
+}
+}  // namespace
+
+template <typename R>
+int64_t gpu_find_pairs(const BuildArgs& a, const int* base, const R* wx, const R* wy, int* pair, cudaStream_t st) {
+  if (a.P <= 0) return 0;
+  DBuf<unsigned long long> np(1);
+  BK(cudaMemsetAsync(np.p, 0, sizeof(unsigned long long), st));
+  k_pairs<R><<<static_cast<unsigned>((a.P + 255) / 256), 256, 0, st>>>(a.P, a.Ppad, a.nb, a.m, a.w, base, wx, wy, pair,
+                                                                        np.p);
+  BK(cudaGetLastError());
+  unsigned long long h = 0;
+  BK(cudaMemcpyAsync(&h, np.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+  BK(cudaStreamSynchronize(st));
+  return static_cast<int64_t>(h);
+}
+
+struct HalfWBuild {
+  int64_t P = 0, Ph = 0;
+  DBuf<int> flag, hpos;
+};
+
+HalfWBuild* gpu_half_w_begin(int64_t P, const int* perm, const int* pair, cudaStream_t st, int64_t* Ph) {
+  auto hb = std::make_unique<HalfWBuild>();
+  hb->P = P;
+  hb->flag.alloc(P);
+  hb->hpos.alloc(P);
+  k_half_flags<<<static_cast<unsigned>((P + 255) / 256), 256, 0, st>>>(P, perm, pair, hb->flag.p);
+  BK(cudaGetLastError());
+  size_t tb = 0;
+  BK(cub::DeviceScan::ExclusiveSum(nullptr, tb, hb->flag.p, hb->hpos.p, static_cast<int>(P), st));
+  DBuf<unsigned char> tmp(tb);
+  BK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, hb->flag.p, hb->hpos.p, static_cast<int>(P), st));
+  int lo = 0, lf = 0;
+  BK(cudaMemcpyAsync(&lo, hb->hpos.p + P - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  BK(cudaMemcpyAsync(&lf, hb->flag.p + P - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  BK(cudaStreamSynchronize(st));
+  hb->Ph = static_cast<int64_t>(lo) + lf;
+  *Ph = hb->Ph;
+  return hb.release();
+}
+
+template <typename R>
+void gpu_half_w_finish(HalfWBuild* hb, int64_t Ppad, int64_t Ppad_h, int w, const int* perm, const int* pair,
+                       const int* base, const R* wx, const R* wy, int* base_h, R* wx_h, R* wy_h, WtEnt<R>* ent,
+                       int64_t n_ent, cudaStream_t st) {
+  const int64_t P = hb->P;
+  BK(cudaMemsetAsync(base_h, 0, sizeof(int) * Ppad_h, st));  // padding rows: node 0, zero weights
+  BK(cudaMemsetAsync(wx_h, 0, sizeof(R) * w * Ppad_h, st));
+  BK(cudaMemsetAsync(wy_h, 0, sizeof(R) * w * Ppad_h, st));
+  DBuf<int> cmap(P);
+  k_half_gather<R><<<static_cast<unsigned>((P + 255) / 256), 256, 0, st>>>(
+      P, Ppad, Ppad_h, w, perm, pair, hb->flag.p, hb->hpos.p, base, wx, wy, base_h, wx_h, wy_h, cmap.p);
+  BK(cudaGetLastError());
+  if (n_ent > 0)  // the mirror-pair W^T indexes the half W's output positions
+    k_remap_ent<R><<<static_cast<unsigned>((n_ent + 255) / 256), 256, 0, st>>>(n_ent, cmap.p, ent);
+  BK(cudaGetLastError());
+  BK(cudaStreamSynchronize(st));
+}
+
+void gpu_half_w_free(HalfWBuild* hb) { delete hb; }
+
 #define TOMO_INST_BUILD(R)                                                                                     \
   template GpuBuild* gpu_build_begin<R>(const BuildArgs&, const double*, const double*, int*, R*, R*,         \
                                         cudaStream_t, GpuBuildSizes*);                                        \
   template void gpu_build_finish<R>(GpuBuild*, WtEnt<R>*, int4*, uint16_t*, int4*, int*, cudaStream_t); \
   template void gpu_sort_w_tables<R>(int, int64_t, int64_t, int, int*, R*, R*, int*, WtEnt<R>*, int64_t, WtEnt<R>*, \
                                      int64_t, cudaStream_t);                                                   \
-  template GpuBuild* gpu_build_fold<R>(const GpuBuild*, cudaStream_t, GpuBuildSizes*);                      \
+  template GpuBuild* gpu_build_fold<R>(const GpuBuild*, cudaStream_t, GpuBuildSizes*, const int*);          \
+  template int64_t gpu_find_pairs<R>(const BuildArgs&, const int*, const R*, const R*, int*, cudaStream_t);  \
+  template void gpu_half_w_finish<R>(HalfWBuild*, int64_t, int64_t, int, const int*, const int*, const int*, \
+                                     const R*, const R*, int*, R*, R*, WtEnt<R>*, int64_t, cudaStream_t);    \
   template GpuBuild* gpu_build_gram_begin<R>(int, int, int64_t, const int*, const double*, const double*, cudaStream_t, \
                                              GpuBuildSizes*, int64_t*);
 

@@ -327,6 +327,13 @@ struct tomo_op {
   bool w_sorted = false;
   TaskSet gram;  // fused backend only
   TaskSet herm;  // W^T folded onto grid rows [0, m/2] (real-subspace type-1); n_tasks == 0: not built
+  // Mirror pairs (opbuild.cu): for real images the normal operator needs W on one sample of every
+  // mirror pair only (half W: hbase / hwx / hwy, Ph samples) and the folded W^T of the primaries
+  // (sym); used by normal_core when both ends are real. n_tasks == 0: not built (no pairs).
+  TaskSet sym;
+  Raw pairs, hbase, hwx, hwy;
+  int64_t Ph = 0, n_paired = 0;
+  int Ppad_h = 0;
   const TspmFile* src = nullptr;  // during tomo_op_create_tspm: the loaded Gram / surrogate T
   // surrogate
   int rad = 0;
@@ -363,6 +370,22 @@ struct tomo_op {
   bool sharded() const { return g.a0 != 0 || g.a1 != g.A; }
   // real-subspace (Hermitian half-grid) pipeline available: folded W^T built, pairs of image rows
   bool herm_ok() const { return herm.n_tasks > 0 && g.n % 2 == 0; }
+  bool sym_ok() const { return herm_ok() && sym.n_tasks > 0 && Ph > 0; }
+  // the real-subspace normal operator through the mirror pairs: W on the half sample set (written
+  // at its compact positions), the primaries' folded W^T reading those positions
+  template <typename R>
+  void use_sym(OpDev<R>& d) const {
+    d.wth = TaskSpmv<R>{sym.ent.as<WtEnt<R>>(), sym.tasks.as<int4>(), sym.n_tasks, sym.perm.as<uint16_t>(),
+                        sym.heavy.as<int4>(), sym.slot_heavy.as<int>(), d.wth.heavy_cnt, sym.n_heavy, sym.n_slots,
+                        d.wth.part};
+    d.w_base = hbase.as<int>();
+    d.w_x = hwx.as<R>();
+    d.w_y = hwy.as<R>();
+    d.w_perm = nullptr;
+    d.w_out_pos = 1;
+    d.P = static_cast<int>(Ph);
+    d.Ppad = Ppad_h;
+  }
   bool surrogate() const { return desc.backend == TOMO_BACKEND_SURROGATE; }
   bool fused() const { return desc.backend == TOMO_BACKEND_FUSED; }
   int64_t L() const { return static_cast<int64_t>(g.n) * g.n; }
@@ -417,8 +440,8 @@ struct tomo_op {
   }
 
   // split-block partial slots / tickets per slice, shared by W^T and its Hermitian fold
-  size_t wt_slots_cap() const { return static_cast<size_t>(std::max({n_slots, herm.n_slots, 1})); }
-  size_t wt_heavy_cap() const { return static_cast<size_t>(std::max({n_heavy, herm.n_heavy, 1})); }
+  size_t wt_slots_cap() const { return static_cast<size_t>(std::max({n_slots, herm.n_slots, sym.n_slots, 1})); }
+  size_t wt_heavy_cap() const { return static_cast<size_t>(std::max({n_heavy, herm.n_heavy, sym.n_heavy, 1})); }
 
   void ensure_batch(int B) {
     Scratch& sc = W().sc;
@@ -1063,6 +1086,39 @@ void build_w_gpu(tomo_op* op) {
   ts.slot_heavy.ensure(sizeof(int) * std::max(ts.n_slots, 1));
   gpu_build_finish<R>(hb.get(), ts.ent.as<WtEnt<R>>(), ts.tasks.as<int4>(), ts.perm.as<uint16_t>(),
                       ts.heavy.as<int4>(), ts.slot_heavy.as<int>(), 0);
+  // mirror pairs of the samples: the primaries' fold (half the entries) for the normal operator
+  if (ab_knob("TOMO_SYM") == "0" || g.P <= 0) return;
+  op->pairs.ensure(sizeof(int) * g.P);
+  op->n_paired = gpu_find_pairs<R>(a, op->wbase.as<int>(), op->wxs.as<R>(), op->wys.as<R>(), op->pairs.as<int>(), 0);
+  // worth its two extra tables only when most samples pair up (the reference's symmetric window
+  // [-m_sp, m_sp] around floor(x / h) pairs nothing but the few samples that sit on a grid line)
+  if (op->n_paired * 2 < g.P) {
+    op->n_paired = 0;
+    return;
+  }
+  GpuBuildSizes yz{};
+  std::unique_ptr<GpuBuild, void (*)(GpuBuild*)> yb(gpu_build_fold<R>(b.get(), 0, &yz, op->pairs.as<int>()),
+                                                    gpu_build_free);
+  // the primaries' fold must write every node the full fold writes (they share the half grid
+  // buffer, whose untouched nodes stay zero); mirror-image windows guarantee it
+  if (yz.touched != hz.touched) {
+    op->n_paired = 0;
+    return;
+  }
+  TaskSet& ys = op->sym;
+  ys.nnz = yz.nnz;
+  ys.touched = yz.touched;
+  ys.n_tasks = yz.n_tasks;
+  ys.n_heavy = yz.n_heavy;
+  ys.n_slots = yz.n_slots;
+  ys.slots = yz.chunks * 32;
+  ent_alloc<R>(ys.ent, ys.slots);
+  ys.tasks.ensure(sizeof(int4) * std::max(ys.n_tasks, 1));
+  ys.perm.ensure(sizeof(uint16_t) * static_cast<size_t>(m / 2 + 1) * m);
+  ys.heavy.ensure(sizeof(int4) * std::max(ys.n_heavy, 1));
+  ys.slot_heavy.ensure(sizeof(int) * std::max(ys.n_slots, 1));
+  gpu_build_finish<R>(yb.get(), ys.ent.as<WtEnt<R>>(), ys.tasks.as<int4>(), ys.perm.as<uint16_t>(),
+                      ys.heavy.as<int4>(), ys.slot_heavy.as<int>(), 0);
 }
 
 template <typename R>
@@ -1084,6 +1140,21 @@ void build_tables(tomo_op* op) {
     gpu_sort_w_tables<R>(m, g.P, op->Ppad, w, op->wbase.as<int>(), op->wxs.as<R>(), op->wys.as<R>(),
                          op->wperm.as<int>(), op->wtent.as<WtEnt<R>>(), op->wt_slots, op->herm.ent.as<WtEnt<R>>(),
                          op->herm.slots, 0);
+  }
+  if (op->sym.n_tasks > 0) {
+    // the half W (one sample per mirror pair + the unpaired ones, tile order kept); the mirror-pair
+    // W^T's entries move from sample indices to the half W's output positions
+    int64_t Ph = 0;
+    std::unique_ptr<HalfWBuild, void (*)(HalfWBuild*)> hw(
+        gpu_half_w_begin(g.P, op->wperm.as<int>(), op->pairs.as<int>(), 0, &Ph), gpu_half_w_free);
+    op->Ph = Ph;
+    op->Ppad_h = static_cast<int>((Ph + 31) / 32 * 32);
+    op->hbase.ensure(sizeof(int) * op->Ppad_h);
+    op->hwx.ensure(sizeof(R) * w * op->Ppad_h);
+    op->hwy.ensure(sizeof(R) * w * op->Ppad_h);
+    gpu_half_w_finish<R>(hw.get(), op->Ppad, op->Ppad_h, w, op->wperm.as<int>(), op->pairs.as<int>(),
+                         op->wbase.as<int>(), op->wxs.as<R>(), op->wys.as<R>(), op->hbase.as<int>(),
+                         op->hwx.as<R>(), op->hwy.as<R>(), op->sym.ent.as<WtEnt<R>>(), op->sym.slots, 0);
   }
   // deapodisation a[t]/m (nufft.cpp:204-227 with the 1/m per-axis FFT scale folded in)
   std::vector<R> apod(g.n);
@@ -1188,6 +1259,8 @@ void normal_core(tomo_op* op, int B, const void* in, bool complex_in, const PUpd
   d.herm_in = op->herm_ok() && !op->fused() && !complex_in;
   d.herm_out = op->herm_ok() && !op->fused() && e.mode != PB_COMPLEX;
   if (d.herm_out) d.Gt = d.Gth;
+  // real in and real out: W on one sample per mirror pair, the primaries' folded W^T
+  if (d.herm_in && d.herm_out && op->sym_ok()) op->use_sym(d);
   launch_t2_rows<R>(d, B, in, complex_in, pu, st);
   launch_t2_cols<R>(d, B, skip, st);
   if (op->fused()) {
@@ -1954,6 +2027,11 @@ int tomo_op_get_info(const tomo_op* op, tomo_op_info* info) {
   info->herm_slots = op->herm.slots;
   info->herm_touched = op->herm.touched;
   info->herm_tasks = op->herm.n_tasks;
+  info->sym_tasks = op->sym_ok() ? op->sym.n_tasks : 0;
+  info->sym_pairs = op->sym_ok() ? op->n_paired : 0;
+  info->sym_P = op->sym_ok() ? op->Ph : 0;
+  info->sym_nnz = op->sym_ok() ? op->sym.nnz : 0;
+  info->sym_slots = op->sym_ok() ? op->sym.slots : 0;
   std::memcpy(info->stencil, op->stencil64, sizeof(info->stencil));
   TOMO_CATCH
 }
@@ -2690,6 +2768,8 @@ int tomo_profile_stages(tomo_op* op, int batch, int reps, int complex_io, double
     const bool herm = !complex_io && op->herm_ok() && !op->fused();
     d.herm_in = d.herm_out = herm ? 1 : 0;
     if (herm) d.Gt = d.Gth;
+    const bool sym = herm && op->sym_ok();
+    if (sym) op->use_sym(d);
     const size_t cbytes = sizeof(cplx<R>) * cnt;
     if (complex_io) {
       S.cin.ensure(cbytes);
@@ -2803,13 +2883,16 @@ int tomo_profile_stages(tomo_op* op, int batch, int reps, int complex_io, double
       // the matrix stream is read once per launch, the vectors once per slice
       //   (the Hermitian path: W gathers the T_h touched nodes of the half grid; the folded W^T
       //    streams its nnz_f entries, ids of T_h nodes, writes the half grid)
-      const double nnzb = static_cast<double>(op->nnz) * (4.0 + rs);
+      //   (mirror pairs: W runs on the Ph kept samples, the primaries' fold streams its entries)
+      const double Pw = sym ? static_cast<double>(op->Ph) : P;
+      const double nnzb = (sym ? Pw * op->g.w * op->g.w : static_cast<double>(op->nnz)) * (4.0 + rs);
       const double T = static_cast<double>(herm ? op->herm.touched : op->wt_rows);
-      const double nnzt = herm ? static_cast<double>(op->herm.nnz) * (4.0 + rs) : nnzb;
+      const double nnzt = sym ? static_cast<double>(op->sym.nnz) * (4.0 + rs)
+                              : herm ? static_cast<double>(op->herm.nnz) * (4.0 + rs) : nnzb;
       by[2] = op->fused()  // Gram stream, read + write touched nodes
                   ? static_cast<double>(op->gram.bytes) + B * (2 * cs * op->wt_rows)
-                  : nnzb + B * (cs * T + cs * P);
-      by[3] = nnzt + 8.0 * (T + 1) + B * (cs * P + cs * hm);
+                  : nnzb + B * (cs * T + cs * Pw);
+      by[3] = nnzt + 8.0 * (T + 1) + B * (cs * Pw + cs * hm);
       by[4] = B * (cs * hm + cs * hn);                     // read spread grid, write K
       by[5] = B * (cs * hn + (complex_io ? cs * nn : 2 * rs * nn));  // read K (+ p); write Ap / out
     } else {
