@@ -779,6 +779,7 @@ def main():
                "cpu_model": cb.model, "nproc": host_cpu()[1], "sample_wall_s": round(wall, 2)}
 
     info = wl.op.info
+    h2d, d2h = int(wl.h2d), int(wl.d2h)
     others = None
     if world == 1 and args.config == "c2" and not args.no_other_configs and not args.batch:
         # the other four BASELINE configs, briefly, in the same run (device-timed values only)
@@ -803,8 +804,8 @@ def main():
                          "nnz_local": int(info.nnz)},
             "roofline": roof,
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e_value, "unit": c["unit"], "h2d_bytes_per_step": int(wl.h2d),
-                    "d2h_bytes_per_step": int(wl.d2h)},
+            "e2e": {"value": e2e_value, "unit": c["unit"], "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }

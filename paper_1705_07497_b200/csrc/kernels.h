@@ -97,6 +97,7 @@ struct OpDev {
   TaskSpmv<R> wth;                 // W^T folded onto rows [0, m/2] (entry .j bit 31 = conjugate)
   int herm_in;                     // type-2 of a real image through the half grid
   int herm_out;                    // type-1 real-part output through the folded half grid
+  int s_stride;                    // slice stride of the sample vector (P; overlap pairs: 2P = samples | pair sums)
 
   TaskSpmv<R> wt_view() const {
     return TaskSpmv<R>{wt_ent, wt_tasks, n_tasks, wt_perm, wt_heavy, wt_slot_heavy, wt_heavy_cnt, n_heavy, n_slots,
@@ -193,6 +194,9 @@ void launch_w(const OpDev<R>& d, int B, const cplx<R>* grid, cplx<R>* samples, c
               cudaStream_t st);
 template <typename R>
 void launch_wt_rows(const OpDev<R>& d, int B, const SliceScalars* skip, cudaStream_t st);
+// Overlap pairs (opbuild.cu): s[P + t] = s[t] + conj(s[ppos[t]]) for the positions t of pair primaries
+template <typename R>
+void launch_pair_sigma(cplx<R>* s, int B, int P, int stride, const int* ppos, cudaStream_t st);
 // W^T SpMV alone: samples -> spread grid (task kernel + split-block fix-up); `grid` must hold
 // zeros at untouched nodes (they are never written).
 template <typename R>
@@ -259,7 +263,8 @@ void gpu_sort_w_tables(int m, int64_t P, int64_t Ppad, int w, int* base, R* wx, 
 // Hermitian fold of a finished (unfolded) W^T build: nodes of grid rows [0, m/2], each with its own
 // entries and the conjugated entries of its mirror node (-iy, -ix). Finish with gpu_build_finish.
 template <typename R>
-GpuBuild* gpu_build_fold(const GpuBuild* src, cudaStream_t st, GpuBuildSizes* sizes, const int* pair = nullptr);
+GpuBuild* gpu_build_fold(const GpuBuild* src, cudaStream_t st, GpuBuildSizes* sizes, const int* pair = nullptr,
+                         const int* base = nullptr);
 // Mirror pairs of the samples (opbuild.cu "mirror pairs"): pair[j] = mirror sample or -1, from the
 // separable W tables in sample order; returns the number of paired samples. With `pair`,
 // gpu_build_fold drops the secondaries' entries and doubles the primaries' (entry indices stay
@@ -269,6 +274,14 @@ int64_t gpu_find_pairs(const BuildArgs& a, const int* base, const R* wx, const R
 // The half W: the tile-ordered separable tables (after gpu_sort_w_tables; perm = position -> sample)
 // compacted to the samples that are not secondaries (Ph of them, order kept); `ent` (the mirror-pair
 // W^T's entries, sample indices) is remapped to the compact positions, a secondary to its primary's.
+// Overlap pairs (windows [-h, h] around floor(x / h): the mirror sample's window is the mirror image
+// shifted by one node): with `base` (sample order) gpu_build_fold keeps every sample's own entries
+// outside the overlap, drops the secondaries' overlap entries and points the primaries' at the pair
+// sum (index P + j). gpu_pair_sigma_setup then remaps the entries to positions (P + position for
+// pair sums) and fills ppos[t] = position of the partner of the primary at position t, else -1.
+template <typename R>
+void gpu_pair_sigma_setup(int64_t P, const int* perm, const int* pair, WtEnt<R>* ent, int64_t n_ent, int* ppos,
+                          cudaStream_t st);
 struct HalfWBuild;
 HalfWBuild* gpu_half_w_begin(int64_t P, const int* perm, const int* pair, cudaStream_t st, int64_t* Ph);
 template <typename R>

@@ -452,9 +452,23 @@ void gpu_build_free(GpuBuild* b) { delete b; }
 // iy <= m/2 and w conj(s_j) to F[-iy][-ix] when iy >= m/2 or iy == 0 (rows 0 and m/2 are their
 // own mirror rows: both). The conj flag is bit 31 of the entry's sample index.
 namespace {
-// `pair` (mirror-pair fold, below): entries of a pair's secondary sample (j < pair[j]) are dropped
+// `pair` (mirror-pair fold, below): entries of a pair's secondary sample (j < pair[j]) are dropped;
+// with `base` (overlap pairs) only those inside the pair's common window.
+struct PairWin {
+  int m, lo, hi;  // window [lo, hi] around floor(x / h)
+  // taps q = l - lo of the common window of a sample and its mirror partner: l in [max(lo, 1 - hi), min(hi, 1 - lo)]
+  __host__ __device__ int q0() const { return (lo > 1 - hi ? lo : 1 - hi) - lo; }
+  __host__ __device__ int q1() const { return (hi < 1 - lo ? hi : 1 - lo) - lo; }
+  __device__ bool common(int node, int b) const {
+    const int iy = node / m, ix = node - iy * m;
+    const int qa = (ix - (b & 0xffff) + m) % m, qb = (iy - ((b >> 16) & 0xffff) + m) % m;
+    return qa >= q0() && qa <= q1() && qb >= q0() && qb <= q1();
+  }
+};
+
 __global__ void k_fold_count(int m, int64_t G, const int* __restrict__ cnt, const int* __restrict__ off,
-                             const int* __restrict__ sj, const int* __restrict__ pair, int* ecnt) {
+                             const int* __restrict__ sj, const int* __restrict__ pair, const int* __restrict__ base,
+                             PairWin pw, int* ecnt) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= G) return;
   const int iy = static_cast<int>(i / m);
@@ -465,7 +479,8 @@ __global__ void k_fold_count(int m, int64_t G, const int* __restrict__ cnt, cons
     int kept = 0;
     for (int k = 0; k < c; ++k) {
       const int j = sj[o + k];
-      kept += !(pair[j] >= 0 && j < pair[j]);
+      const bool secondary = pair[j] >= 0 && j < pair[j];
+      kept += !(secondary && (!base || pw.common(static_cast<int>(i), base[j])));
     }
     c = kept;
   }
@@ -475,7 +490,8 @@ __global__ void k_fold_count(int m, int64_t G, const int* __restrict__ cnt, cons
 template <typename R>
 __global__ void k_fold_emit(int m, int64_t G, const int* __restrict__ cnt, const int* __restrict__ off,
                             const int* __restrict__ eoff, const int* __restrict__ sj, const R* __restrict__ vals,
-                            const int* __restrict__ pair, unsigned long long* keys, R* fvals) {
+                            const int* __restrict__ pair, const int* __restrict__ base, PairWin pw, unsigned P,
+                            unsigned long long* keys, R* fvals) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= G) return;
   const int iy = static_cast<int>(i / m), ix = static_cast<int>(i - static_cast<int64_t>(iy) * m);
@@ -484,12 +500,20 @@ __global__ void k_fold_emit(int m, int64_t G, const int* __restrict__ cnt, const
   const unsigned long long mnode =
       static_cast<unsigned long long>((m - iy) & (m - 1)) * m + static_cast<unsigned long long>((m - ix) & (m - 1));
   for (int k = 0; k < c; ++k) {
-    const unsigned j = static_cast<unsigned>(sj[off[i] + k]);
+    unsigned j = static_cast<unsigned>(sj[off[i] + k]);
     R v = vals[off[i] + k];
-    if (pair) {
+    if (pair && !base) {
       const int pr = pair[j];
       if (pr >= 0 && static_cast<int>(j) < pr) continue;  // secondary: carried by its primary
       if (pr >= 0) v = v + v;                             // primary: its own and its mirror's share
+    } else if (pair) {
+      // overlap pairs: inside the common window the primary's entry reads the pair sum
+      // s_j + conj(s_partner) (index P + j) and the secondary's is dropped
+      const int pr = pair[j];
+      if (pr >= 0 && pw.common(static_cast<int>(i), base[j])) {
+        if (static_cast<int>(j) < pr) continue;
+        j += P;
+      }
     }
     if (iy <= m / 2) {
       keys[o] = (static_cast<unsigned long long>(i) << 32) | j;
@@ -509,7 +533,8 @@ __global__ void k_fold_cnt(int64_t n, const unsigned long long* __restrict__ key
 }  // namespace
 
 template <typename R>
-GpuBuild* gpu_build_fold(const GpuBuild* src, cudaStream_t st, GpuBuildSizes* sizes, const int* pair) {
+GpuBuild* gpu_build_fold(const GpuBuild* src, cudaStream_t st, GpuBuildSizes* sizes, const int* pair,
+                         const int* base) {
   const int m = src->a.m;
   if (src->G != static_cast<int64_t>(m) * m) throw std::runtime_error("opbuild: fold needs the unfolded W^T");
   auto b = std::make_unique<GpuBuild>();
@@ -519,7 +544,9 @@ GpuBuild* gpu_build_fold(const GpuBuild* src, cudaStream_t st, GpuBuildSizes* si
   b->G32 = b->G / 32;
   const unsigned gs = static_cast<unsigned>((src->G + 255) / 256);
   DBuf<int> ecnt(src->G), eoff(src->G);
-  k_fold_count<<<gs, 256, 0, st>>>(m, src->G, src->cnt.p, src->off.p, src->sj.p, pair, ecnt.p);
+  const PairWin pw{m, src->a.lo, src->a.hi};
+  if (base && 2 * src->a.P >= (int64_t(1) << 31)) throw std::runtime_error("opbuild: too many samples for pair sums");
+  k_fold_count<<<gs, 256, 0, st>>>(m, src->G, src->cnt.p, src->off.p, src->sj.p, pair, base, pw, ecnt.p);
   BK(cudaGetLastError());
   size_t tb = 0;
   BK(cub::DeviceScan::ExclusiveSum(nullptr, tb, ecnt.p, eoff.p, static_cast<int>(src->G), st));
@@ -536,7 +563,8 @@ GpuBuild* gpu_build_fold(const GpuBuild* src, cudaStream_t st, GpuBuildSizes* si
   DBuf<unsigned long long> keys(b->nnz), skeys(b->nnz);
   DBuf<R> vals(b->nnz);
   k_fold_emit<R><<<gs, 256, 0, st>>>(m, src->G, src->cnt.p, src->off.p, eoff.p, src->sj.p,
-                                     reinterpret_cast<const R*>(src->vals_sorted.p), pair, keys.p, vals.p);
+                                     reinterpret_cast<const R*>(src->vals_sorted.p), pair, base, pw,
+                                     static_cast<unsigned>(src->a.P), keys.p, vals.p);
   BK(cudaGetLastError());
   // (folded node, conj flag, sample): plain entries before conjugated ones, samples ascending
   b->vals_sorted.alloc(sizeof(R) * b->nnz);
@@ -797,21 +825,26 @@ void gpu_sort_w_tables(int m, int64_t P, int64_t Ppad, int w, int* base, R* wx, 
 // positive semi-definite, equal to W^T W up to the rounding of the sample positions.
 namespace {
 template <typename R>
-__global__ void k_pairs(int64_t P, int64_t Ppad, int nb, int m, int w, const int* __restrict__ base,
+__global__ void k_pairs(int64_t P, int64_t Ppad, int nb, PairWin pw, int w, const int* __restrict__ base,
                         const R* __restrict__ wx, const R* __restrict__ wy, int* pair, unsigned long long* npaired) {
   const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= P) return;
+  const int m = pw.m;
   const int t = static_cast<int>(j % nb), tm = 2 * (nb / 2) - t;
   int pr = -1;
-  if (tm >= 0 && tm < nb && tm != t) {
+  if (tm >= 0 && tm < nb && tm != t && pw.q0() <= pw.q1()) {
     const int64_t jm = j - t + tm;
     const int b = base[j], bm = base[jm];
     const int ix0 = b & 0xffff, iy0 = (b >> 16) & 0xffff;
-    bool ok = (bm & 0xffff) == (2 * m - ix0 - (w - 1)) % m && ((bm >> 16) & 0xffff) == (2 * m - iy0 - (w - 1)) % m;
+    // node mj + l of the sample <-> node -(mj + l) = (-mj - 1) + (1 - l) of the mirror sample:
+    // its base node is -(ix0 - lo) - 1 + lo, its tap of the same node q' = 1 - 2 lo - q
+    const int shift = 2 * pw.lo - 1;
+    bool ok = (bm & 0xffff) == ((3 * m - ix0 + shift) % m) && ((bm >> 16) & 0xffff) == ((3 * m - iy0 + shift) % m);
     const R tol = sizeof(R) == 8 ? R(1e-9) : R(4e-7);
-    for (int a = 0; ok && a < w; ++a) {
-      const R x1 = wx[static_cast<size_t>(a) * Ppad + jm], x2 = wx[static_cast<size_t>(w - 1 - a) * Ppad + j];
-      const R y1 = wy[static_cast<size_t>(a) * Ppad + jm], y2 = wy[static_cast<size_t>(w - 1 - a) * Ppad + j];
+    for (int q = pw.q0(); ok && q <= pw.q1(); ++q) {
+      const int qm = 1 - 2 * pw.lo - q;
+      const R x1 = wx[static_cast<size_t>(qm) * Ppad + jm], x2 = wx[static_cast<size_t>(q) * Ppad + j];
+      const R y1 = wy[static_cast<size_t>(qm) * Ppad + jm], y2 = wy[static_cast<size_t>(q) * Ppad + j];
       ok = fabs(x1 - x2) <= tol * fmax(fabs(x1), fabs(x2)) && fabs(y1 - y2) <= tol * fmax(fabs(y1), fabs(y2));
     }
     if (ok) {
@@ -853,13 +886,44 @@ int64_t gpu_find_pairs(const BuildArgs& a, const int* base, const R* wx, const R
   if (a.P <= 0) return 0;
   DBuf<unsigned long long> np(1);
   BK(cudaMemsetAsync(np.p, 0, sizeof(unsigned long long), st));
-  k_pairs<R><<<static_cast<unsigned>((a.P + 255) / 256), 256, 0, st>>>(a.P, a.Ppad, a.nb, a.m, a.w, base, wx, wy, pair,
-                                                                        np.p);
+  k_pairs<R><<<static_cast<unsigned>((a.P + 255) / 256), 256, 0, st>>>(a.P, a.Ppad, a.nb, PairWin{a.m, a.lo, a.hi}, a.w,
+                                                                        base, wx, wy, pair, np.p);
   BK(cudaGetLastError());
   unsigned long long h = 0;
   BK(cudaMemcpyAsync(&h, np.p, sizeof(h), cudaMemcpyDeviceToHost, st));
   BK(cudaStreamSynchronize(st));
   return static_cast<int64_t>(h);
+}
+
+namespace {
+// entries: sample j -> position, pair sum P + j -> P + position (conj flag kept)
+template <typename R>
+__global__ void k_remap_ent_ext(int64_t n, int P, const int* __restrict__ pos, WtEnt<R>* ent) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int e = ent[i].j, flag = e & static_cast<int>(0x80000000u), j = e & 0x7fffffff;
+  ent[i].j = (j >= P ? P + pos[j - P] : pos[j]) | flag;
+}
+__global__ void k_partner_pos(int64_t P, const int* __restrict__ perm, const int* __restrict__ pair,
+                              const int* __restrict__ pos, int* ppos) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= P) return;
+  const int j = perm[t], pr = pair[j];
+  ppos[t] = pr < 0 ? -1 : (j > pr ? pos[pr] : -2 - pos[pr]);  // primary / secondary / unpaired
+}
+}  // namespace
+
+template <typename R>
+void gpu_pair_sigma_setup(int64_t P, const int* perm, const int* pair, WtEnt<R>* ent, int64_t n_ent, int* ppos,
+                          cudaStream_t st) {
+  DBuf<int> pos(P);
+  const unsigned grid = static_cast<unsigned>((P + 255) / 256);
+  k_inverse<<<grid, 256, 0, st>>>(P, perm, pos.p);
+  k_partner_pos<<<grid, 256, 0, st>>>(P, perm, pair, pos.p, ppos);
+  if (n_ent > 0)
+    k_remap_ent_ext<R><<<static_cast<unsigned>((n_ent + 255) / 256), 256, 0, st>>>(n_ent, static_cast<int>(P), pos.p, ent);
+  BK(cudaGetLastError());
+  BK(cudaStreamSynchronize(st));
 }
 
 struct HalfWBuild {
@@ -913,7 +977,8 @@ void gpu_half_w_free(HalfWBuild* hb) { delete hb; }
   template void gpu_build_finish<R>(GpuBuild*, WtEnt<R>*, int4*, uint16_t*, int4*, int*, cudaStream_t); \
   template void gpu_sort_w_tables<R>(int, int64_t, int64_t, int, int*, R*, R*, int*, WtEnt<R>*, int64_t, WtEnt<R>*, \
                                      int64_t, cudaStream_t);                                                   \
-  template GpuBuild* gpu_build_fold<R>(const GpuBuild*, cudaStream_t, GpuBuildSizes*, const int*);          \
+  template GpuBuild* gpu_build_fold<R>(const GpuBuild*, cudaStream_t, GpuBuildSizes*, const int*, const int*); \
+  template void gpu_pair_sigma_setup<R>(int64_t, const int*, const int*, WtEnt<R>*, int64_t, int*, cudaStream_t); \
   template int64_t gpu_find_pairs<R>(const BuildArgs&, const int*, const R*, const R*, int*, cudaStream_t);  \
   template void gpu_half_w_finish<R>(HalfWBuild*, int64_t, int64_t, int, const int*, const int*, const int*, \
                                      const R*, const R*, int*, R*, R*, WtEnt<R>*, int64_t, cudaStream_t);    \

@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(256) k_w_sep(OpDev<R> d, int B, const cplx<R>*
 #pragma unroll
     for (int q = 0; q < BT; ++q)
       if (b0 + q < B && !(skip && (skip[b0 + q].done || skip[b0 + q].frozen)))
-        out[static_cast<size_t>(b0 + q) * d.P + j] = acc[q];
+        out[static_cast<size_t>(b0 + q) * d.s_stride + j] = acc[q];
   }
 }
 
@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(256) k_w_sep_v6(OpDev<float> d, int B, const f
 #pragma unroll
     for (int q = 0; q < BT; ++q)
       if (b0 + q < B && !(skip && (skip[b0 + q].done || skip[b0 + q].frozen)))
-        out[static_cast<size_t>(b0 + q) * d.P + j] = acc[q];
+        out[static_cast<size_t>(b0 + q) * d.s_stride + j] = acc[q];
   }
 }
 
@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(256) k_w_sep_wide(OpDev<R> d, int B, const cpl
       acc.x += wy * ra.x;
       acc.y += wy * ra.y;
     }
-    out[static_cast<size_t>(b) * d.P + j] = acc;
+    out[static_cast<size_t>(b) * d.s_stride + j] = acc;
   }
 }
 
@@ -510,9 +510,29 @@ template <typename R>
 void launch_wt_spread(const OpDev<R>& d, int B, const cplx<R>* samples, cplx<R>* grid, const SliceScalars* skip,
                       cudaStream_t st) {
   if (d.herm_out)
-    launch_task_spmv<R>(d.wth, d.m, B, samples, static_cast<size_t>(d.P), grid, skip, st, true);
+    launch_task_spmv<R>(d.wth, d.m, B, samples, static_cast<size_t>(d.s_stride), grid, skip, st, true);
   else
-    launch_task_spmv<R>(d.wt_view(), d.m, B, samples, static_cast<size_t>(d.P), grid, skip, st);
+    launch_task_spmv<R>(d.wt_view(), d.m, B, samples, static_cast<size_t>(d.s_stride), grid, skip, st);
+}
+
+// Overlap pairs: the pair sums s_j + conj(s_partner) behind the samples of each slice.
+template <typename R>
+__global__ void k_pair_sigma(cplx<R>* __restrict__ s, int B, int P, int stride, const int* __restrict__ ppos) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= P) return;
+  const int q = __ldg(&ppos[t]);
+  if (q < 0) return;
+  for (int b = 0; b < B; ++b) {
+    cplx<R>* sb = s + static_cast<size_t>(b) * stride;
+    const cplx<R> a = sb[t], c = sb[q];
+    sb[P + t] = mk<cplx<R>>(a.x + c.x, a.y - c.y);
+  }
+}
+
+template <typename R>
+void launch_pair_sigma(cplx<R>* s, int B, int P, int stride, const int* ppos, cudaStream_t st) {
+  CK_LAUNCH(launch_k(k_pair_sigma<R>, static_cast<unsigned>((P + 255) / 256), 256, 0, st, s, B, P, stride, ppos));
+  note_launch();
 }
 
 template <typename R>
@@ -554,6 +574,7 @@ void launch_gather_samples(const cplx<R>* in, cplx<R>* out, const int* perm, int
   template void launch_wt_spread<R>(const OpDev<R>&, int, const cplx<R>*, cplx<R>*, const SliceScalars*,    \
                                     cudaStream_t);                                                          \
   template void launch_gram<R>(const OpDev<R>&, int, const cplx<R>*, cplx<R>*, const SliceScalars*, cudaStream_t); \
+  template void launch_pair_sigma<R>(cplx<R>*, int, int, int, const int*, cudaStream_t);                         \
   template void launch_wt_grid<R>(const OpDev<R>&, int, const cplx<R>*, cplx<R>*, cudaStream_t);            \
   template void launch_weight_samples<R>(cplx<R>*, int, int, int, const int*, cudaStream_t);               \
   template void launch_gather_samples<R>(const cplx<R>*, cplx<R>*, const int*, int, int, cudaStream_t);     \

@@ -330,10 +330,15 @@ struct tomo_op {
   // Mirror pairs (opbuild.cu): for real images the normal operator needs W on one sample of every
   // mirror pair only (half W: hbase / hwx / hwy, Ph samples) and the folded W^T of the primaries
   // (sym); used by normal_core when both ends are real. n_tasks == 0: not built (no pairs).
+  // sym_mode 1: mirror-image windows (lo = 1 - hi). sym_mode 2 ("overlap pairs", the reference's
+  // [-m_sp, m_sp]): the partner's window is the mirror image shifted by one node, so W stays whole,
+  // a small kernel forms the pair sums s_j + conj(s_partner) behind the samples (ppos: partner
+  // positions) and the fold reads them inside the pairs' common window.
   TaskSet sym;
-  Raw pairs, hbase, hwx, hwy;
+  Raw pairs, hbase, hwx, hwy, ppos;
   int64_t Ph = 0, n_paired = 0;
   int Ppad_h = 0;
+  int sym_mode = 0;
   const TspmFile* src = nullptr;  // during tomo_op_create_tspm: the loaded Gram / surrogate T
   // surrogate
   int rad = 0;
@@ -370,7 +375,9 @@ struct tomo_op {
   bool sharded() const { return g.a0 != 0 || g.a1 != g.A; }
   // real-subspace (Hermitian half-grid) pipeline available: folded W^T built, pairs of image rows
   bool herm_ok() const { return herm.n_tasks > 0 && g.n % 2 == 0; }
-  bool sym_ok() const { return herm_ok() && sym.n_tasks > 0 && Ph > 0; }
+  bool sym_ok() const { return herm_ok() && sym.n_tasks > 0 && sym_mode > 0; }
+  // sample vector entries per slice (overlap pairs keep the pair sums behind the samples)
+  size_t s_len() const { return static_cast<size_t>(g.P) * (sym_mode == 2 ? 2 : 1); }
   // the real-subspace normal operator through the mirror pairs: W on the half sample set (written
   // at its compact positions), the primaries' folded W^T reading those positions
   template <typename R>
@@ -378,6 +385,10 @@ struct tomo_op {
     d.wth = TaskSpmv<R>{sym.ent.as<WtEnt<R>>(), sym.tasks.as<int4>(), sym.n_tasks, sym.perm.as<uint16_t>(),
                         sym.heavy.as<int4>(), sym.slot_heavy.as<int>(), d.wth.heavy_cnt, sym.n_heavy, sym.n_slots,
                         d.wth.part};
+    if (sym_mode == 2) {
+      d.s_stride = 2 * d.P;
+      return;
+    }
     d.w_base = hbase.as<int>();
     d.w_x = hwx.as<R>();
     d.w_y = hwy.as<R>();
@@ -385,6 +396,7 @@ struct tomo_op {
     d.w_out_pos = 1;
     d.P = static_cast<int>(Ph);
     d.Ppad = Ppad_h;
+    d.s_stride = d.P;
   }
   bool surrogate() const { return desc.backend == TOMO_BACKEND_SURROGATE; }
   bool fused() const { return desc.backend == TOMO_BACKEND_FUSED; }
@@ -401,6 +413,7 @@ struct tomo_op {
     d.m = g.m;
     d.nb = g.nb;
     d.P = static_cast<int>(g.P);
+    d.s_stride = d.P;
     d.Ppad = Ppad;
     d.G32 = static_cast<int>(static_cast<int64_t>(g.m) * g.m / 32);
     d.apod = apod.as<R>();
@@ -464,7 +477,7 @@ struct tomo_op {
       sc.heavy_cnt_gram.ensure(hb);
       CK(cudaMemset(sc.heavy_cnt_gram.p, 0, hb));
     }
-    sc.s.ensure(B * static_cast<size_t>(g.P) * cz);
+    sc.s.ensure(B * s_len() * cz);
     sc.K.ensure(B * n * m * cz);
     sc.sc.ensure(sizeof(SliceScalars) * B);
     CK(cudaMemset(sc.sc.p, 0, sizeof(SliceScalars) * B));
@@ -502,7 +515,7 @@ struct tomo_op {
       ln.heavy_cnt_gram.ensure(hb);
       CK(cudaMemset(ln.heavy_cnt_gram.p, 0, hb));
     }
-    ln.s.ensure(B * static_cast<size_t>(g.P) * cz);
+    ln.s.ensure(B * s_len() * cz);
     ln.K.ensure(B * n * m * cz);
     ln.cap = B;
     clear_graphs();
@@ -1096,9 +1109,15 @@ void build_w_gpu(tomo_op* op) {
     op->n_paired = 0;
     return;
   }
+  const int mode = g.lo == 1 - g.hi ? 1 : 2;
+  if (mode == 2 && ab_knob("TOMO_SYM") == "1") {  // A/B: mirror-image windows only
+    op->n_paired = 0;
+    return;
+  }
   GpuBuildSizes yz{};
-  std::unique_ptr<GpuBuild, void (*)(GpuBuild*)> yb(gpu_build_fold<R>(b.get(), 0, &yz, op->pairs.as<int>()),
-                                                    gpu_build_free);
+  std::unique_ptr<GpuBuild, void (*)(GpuBuild*)> yb(
+      gpu_build_fold<R>(b.get(), 0, &yz, op->pairs.as<int>(), mode == 2 ? op->wbase.as<int>() : nullptr),
+      gpu_build_free);
   // the primaries' fold must write every node the full fold writes (they share the half grid
   // buffer, whose untouched nodes stay zero); mirror-image windows guarantee it
   if (yz.touched != hz.touched) {
@@ -1119,6 +1138,7 @@ void build_w_gpu(tomo_op* op) {
   ys.slot_heavy.ensure(sizeof(int) * std::max(ys.n_slots, 1));
   gpu_build_finish<R>(yb.get(), ys.ent.as<WtEnt<R>>(), ys.tasks.as<int4>(), ys.perm.as<uint16_t>(),
                       ys.heavy.as<int4>(), ys.slot_heavy.as<int>(), 0);
+  op->sym_mode = mode;
 }
 
 template <typename R>
@@ -1141,7 +1161,12 @@ void build_tables(tomo_op* op) {
                          op->wperm.as<int>(), op->wtent.as<WtEnt<R>>(), op->wt_slots, op->herm.ent.as<WtEnt<R>>(),
                          op->herm.slots, 0);
   }
-  if (op->sym.n_tasks > 0) {
+  if (op->sym.n_tasks > 0 && op->sym_mode == 2) {
+    // overlap pairs: entries to positions (pair sums behind the samples), partner positions
+    op->ppos.ensure(sizeof(int) * g.P);
+    gpu_pair_sigma_setup<R>(g.P, op->wperm.as<int>(), op->pairs.as<int>(), op->sym.ent.as<WtEnt<R>>(), op->sym.slots,
+                            op->ppos.as<int>(), 0);
+  } else if (op->sym.n_tasks > 0) {
     // the half W (one sample per mirror pair + the unpaired ones, tile order kept); the mirror-pair
     // W^T's entries move from sample indices to the half W's output positions
     int64_t Ph = 0;
@@ -1268,6 +1293,8 @@ void normal_core(tomo_op* op, int B, const void* in, bool complex_in, const PUpd
     launch_t1_cols_only<R>(d, B, skip, st);
   } else {
     launch_w<R>(d, B, d.g, d.s, skip, st);
+    if (d.s_stride == 2 * d.P)  // overlap pairs: the pair sums behind each slice's samples
+      launch_pair_sigma<R>(d.s, B, d.P, d.s_stride, op->ppos.as<int>(), st);
     launch_wt_rows<R>(d, B, skip, st);  // W^T + PA (one fused kernel where available)
   }
   launch_t1_rows<R>(d, B, e, st);
@@ -2029,7 +2056,7 @@ int tomo_op_get_info(const tomo_op* op, tomo_op_info* info) {
   info->herm_tasks = op->herm.n_tasks;
   info->sym_tasks = op->sym_ok() ? op->sym.n_tasks : 0;
   info->sym_pairs = op->sym_ok() ? op->n_paired : 0;
-  info->sym_P = op->sym_ok() ? op->Ph : 0;
+  info->sym_P = op->sym_ok() ? (op->sym_mode == 2 ? op->g.P : op->Ph) : 0;
   info->sym_nnz = op->sym_ok() ? op->sym.nnz : 0;
   info->sym_slots = op->sym_ok() ? op->sym.slots : 0;
   std::memcpy(info->stencil, op->stencil64, sizeof(info->stencil));
@@ -2805,8 +2832,11 @@ int tomo_profile_stages(tomo_op* op, int batch, int reps, int complex_io, double
         } else if (s == 2) {
           if (op->fused())
             launch_gram<R>(d, batch, d.g, d.Gt, op->scal(), cs);
-          else
+          else {
             launch_w<R>(d, batch, d.g, d.s, op->scal(), cs);
+            if (d.s_stride == 2 * d.P)
+              launch_pair_sigma<R>(d.s, batch, d.P, d.s_stride, op->ppos.as<int>(), cs);
+          }
         } else if (s == 3) {
           if (!op->fused()) launch_wt_spread<R>(d, batch, d.s, d.Gt, op->scal(), cs);
         } else if (s == 4) {
@@ -2884,15 +2914,18 @@ int tomo_profile_stages(tomo_op* op, int batch, int reps, int complex_io, double
       //   (the Hermitian path: W gathers the T_h touched nodes of the half grid; the folded W^T
       //    streams its nnz_f entries, ids of T_h nodes, writes the half grid)
       //   (mirror pairs: W runs on the Ph kept samples, the primaries' fold streams its entries)
-      const double Pw = sym ? static_cast<double>(op->Ph) : P;
-      const double nnzb = (sym ? Pw * op->g.w * op->g.w : static_cast<double>(op->nnz)) * (4.0 + rs);
+      //   (overlap pairs: W runs on every sample, + the pair-sum pass: read 2, write 1 per pair)
+      const bool half_w = sym && op->sym_mode == 1;
+      const double Pw = half_w ? static_cast<double>(op->Ph) : P;
+      const double nnzb = (half_w ? Pw * op->g.w * op->g.w : static_cast<double>(op->nnz)) * (4.0 + rs);
+      const double sig = sym && op->sym_mode == 2 ? B * 1.5 * cs * static_cast<double>(op->n_paired) : 0.0;
       const double T = static_cast<double>(herm ? op->herm.touched : op->wt_rows);
       const double nnzt = sym ? static_cast<double>(op->sym.nnz) * (4.0 + rs)
                               : herm ? static_cast<double>(op->herm.nnz) * (4.0 + rs) : nnzb;
       by[2] = op->fused()  // Gram stream, read + write touched nodes
                   ? static_cast<double>(op->gram.bytes) + B * (2 * cs * op->wt_rows)
-                  : nnzb + B * (cs * T + cs * Pw);
-      by[3] = nnzt + 8.0 * (T + 1) + B * (cs * Pw + cs * hm);
+                  : nnzb + B * (cs * T + cs * Pw) + sig;
+      by[3] = nnzt + 8.0 * (T + 1) + B * (cs * (Pw + (sig > 0 ? op->n_paired / 2.0 : 0.0)) + cs * hm);
       by[4] = B * (cs * hm + cs * hn);                     // read spread grid, write K
       by[5] = B * (cs * hn + (complex_io ? cs * nn : 2 * rs * nn));  // read K (+ p); write Ap / out
     } else {

@@ -1,6 +1,8 @@
 """Mirror pairs of the parallel-beam samples: with a window [1 - hi, hi] the bins
 t and 2 (n_b / 2) - t of one angle have mirror-image interpolation windows, so for real images the
-normal operator runs W on one sample per pair and the folded W^T of the pairs' primaries. Checked
+normal operator runs W on one sample per pair and the folded W^T of the pairs' primaries; with the
+reference's symmetric window [-m_sp, m_sp] the partner's window is shifted by one node and the fold
+reads pair sums inside the common window ("overlap pairs"). Checked
 against the same op built without the pairs (TOMO_AB=1 TOMO_SYM=0: the full folded W^T and the full
 W) and against the fp64 oracle, for single slices, slice groups and the solvers."""
 import os
@@ -23,9 +25,16 @@ GEOMS = {
     "R4_n64": dict(n=64, n_angles=20, n_b=91, oversample=4, win_lo=-2, win_hi=3, tau=np.pi * 3 / (64 ** 2 * 4 * 3.5)),
     "n256_c1": dict(n=256, n_angles=60, n_b=367, win_lo=-2, win_hi=3, tau=3 / 256 ** 2),
 }
-NO_PAIRS = {
+# symmetric windows [-m_sp, m_sp] around floor(x / h) (the reference's): the partner's window is the
+# mirror image shifted by one node -> "overlap pairs" (W whole, pair sums, 62/98 of the fold at m_sp = 3)
+OVERLAP = {
     "msp3_n32": dict(n=32, n_angles=25, win_lo=-3, win_hi=3),
+    "msp3_n64": dict(n=64, n_angles=30, n_b=91, win_lo=-3, win_hi=3, tau=3 / 64 ** 2),
     "msp2_n64": dict(n=64, n_angles=30, n_b=65, win_lo=-2, win_hi=2, tau=3 / 64 ** 2),
+    "msp3_even_nb": dict(n=64, n_angles=24, n_b=92, win_lo=-3, win_hi=3, tau=3 / 64 ** 2),
+    "R4_msp3_n32": dict(n=32, n_angles=20, n_b=33, oversample=4, win_lo=-3, win_hi=3,
+                        tau=np.pi * 3 / (32 ** 2 * 4 * 3.5)),
+    "n128_c2_like": dict(n=128, n_angles=45, n_b=181, win_lo=-3, win_hi=3, tau=3 / 128 ** 2),
 }
 
 
@@ -86,35 +95,55 @@ def test_pairs_found_and_apply_matches(T, name, prec):
         assert err < 1e-10
 
 
-@pytest.mark.parametrize("name", list(NO_PAIRS))
-def test_symmetric_windows_have_no_pairs(T, name):
-    """[-m_sp, m_sp] around floor(x / h) (the reference's window) is not mirror-symmetric (only
-    samples that sit exactly on a grid line pair up): the pairs are not used, the op runs the full
-    fold."""
-    og = O.Geometry(**NO_PAIRS[name])
-    op = T.make_direct_backend(pgeom(T, og), precision="f64")
-    assert op.info.sym_tasks == 0 and op.info.herm_tasks > 0
-    u = RNG.standard_normal((og.n, og.n))
-    got = op.apply_normal_real(dev(u, True)).cpu().numpy().reshape(og.n, og.n)
-    assert rel(got, O.apply_normal_real(og, u)) < 1e-10
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("name", list(OVERLAP))
+def test_overlap_pairs_apply_matches(T, name, prec):
+    f64 = prec == "f64"
+    og = O.Geometry(**OVERLAP[name])
+    op, ref = make_ops(T, og, prec)
+    inf, rinf = op.info, ref.info
+    assert rinf.sym_tasks == 0 and inf.sym_tasks > 0 and inf.herm_tasks > 0
+    assert inf.sym_pairs > 0.8 * inf.P and inf.sym_P == inf.P  # W stays whole
+    assert inf.sym_nnz < 0.72 * inf.herm_nnz
+    n = og.n
+    for B in (1, 3, 7):
+        u = RNG.standard_normal((B, n, n))
+        a = op.apply_normal_real(dev(u, f64)).cpu().numpy().reshape(B, n, n)
+        b = ref.apply_normal_real(dev(u, f64)).cpu().numpy().reshape(B, n, n)
+        err = rel(a, b)
+        print(f"{name} {prec} B={B}: overlap pairs vs full fold rel-L2 {err:.2e} "
+              f"(fold nnz {inf.herm_nnz} -> {inf.sym_nnz})")
+        assert err < (2e-11 if f64 else 3e-6)
+    if f64:
+        u = RNG.standard_normal((n, n))
+        got = op.apply_normal_real(dev(u, True)).cpu().numpy().reshape(n, n)
+        err = rel(got, O.apply_normal_real(og, u))
+        print(f"{name}: overlap pairs vs oracle rel-L2 {err:.2e}")
+        assert err < 1e-10
 
 
 def test_operator_is_symmetric(T):
-    """<N u, v> = <u, N v>: the pair operator is U^T U of one interpolation U."""
-    og = O.Geometry(**GEOMS["width6_n64"])
+    """<N u, v> = <u, N v>: the mirror-pair operator is U^T U of one interpolation U; the overlap-pair
+    operator is symmetric to the rounding of the sample positions."""
+    _operator_is_symmetric(T, GEOMS["width6_n64"], 1e-13)
+    _operator_is_symmetric(T, OVERLAP["msp3_n64"], 1e-11)
+
+
+def _operator_is_symmetric(T, geom, tol):
+    og = O.Geometry(**geom)
     op = T.make_direct_backend(pgeom(T, og), precision="f64")
     n = og.n
     u, v = RNG.standard_normal((n, n)), RNG.standard_normal((n, n))
     nu = op.apply_normal_real(dev(u, True)).cpu().numpy().ravel()
     nv = op.apply_normal_real(dev(v, True)).cpu().numpy().ravel()
     a, b = float(nu @ v.ravel()), float(nv @ u.ravel())
-    assert abs(a - b) <= 1e-13 * max(abs(a), abs(b))
+    assert abs(a - b) <= tol * max(abs(a), abs(b))
     assert float(nu @ u.ravel()) > 0
 
 
-@pytest.mark.parametrize("name", ["width6_n64", "R4_n64"])
+@pytest.mark.parametrize("name", ["width6_n64", "R4_n64", "msp3_n64"])
 def test_solvers_match_full_fold(T, name):
-    og = O.Geometry(**GEOMS[name])
+    og = O.Geometry(**{**GEOMS, **OVERLAP}[name])
     op, ref = make_ops(T, og, "f64")
     ph = O.random_ellipses(og.n, 10, 3)
     f, _ = O.synthesize(og, ph, 0.01, 3)
