@@ -378,11 +378,20 @@ class Workload:
             counts = {"stencil": c["iters"] * (c["cg"] + 1), "cg_update": c["iters"] * c["cg"], "sb_post": c["iters"]}
         share = {s: counts.get(s, 0) * prof[s][0] for s in prof}
         top = max(share, key=share.get)
-        ms, by = prof[top]
+        ms, by_run = prof[top]
+        # algorithmic bytes of the dominant kernel: for the two SpMVs SURVEY §8(d)'s "SpMV metric"
+        # (the reference algorithm's stage: all nnz entries, T touched nodes, the whole grid), which
+        # the kernels as run undercut on the real subspace (half grid, mirror pairs: `as_run`); for
+        # the other stages §8(d) has no per-stage figure and the bytes are those of the kernel as run
+        by = spmv_bytes(c, self.op.info, top, B) or by_run
         achieved = by / (ms * 1e-3) / 1e9
         out = {"bound": "hbm", "kernel": top, "achieved": round(achieved, 1), "peak": peak_gbs,
                "unit": "GB/s", "frac": round(achieved / peak_gbs, 4), "traffic": None,
                "algorithmic_bytes_per_launch": int(by), "ms_per_launch": round(ms, 5),
+               "bytes_formula": ("SURVEY 8(d) SpMV metric: W (4+r)nnz + cT + B cP; W^T (4+r)nnz + 8(T+1) + B(cP + cG)"
+                                 if by != by_run else "kernel as run (tomo_profile_stages)"),
+               "as_run": {"bytes": int(by_run), "achieved": round(by_run / (ms * 1e-3) / 1e9, 1),
+                          "frac": round(by_run / (ms * 1e-3) / 1e9 / peak_gbs, 4)},
                "stage_ms": {s: round(v[0], 5) for s, v in prof.items()},
                "stage_share_of_step": {s: round(v / max(sum(share.values()), 1e-12), 4) for s, v in share.items()}}
         if k != "sb_sur":
@@ -401,6 +410,20 @@ class Workload:
                             "moved_bytes": int(mb),
                             "moved_frac": round(mb / (t_apply * 1e-3) / 1e9 / peak_gbs, 4)}
         return top, out
+
+
+def spmv_bytes(c, info, stage, B=1):
+    """SURVEY.md §8(d) "SpMV metric" bytes of one W / W^T launch over B slices (None for other
+    stages): every entry of the (local) matrix once per launch, the vectors once per slice."""
+    if stage not in ("w_spmv", "wt_spread"):
+        return None
+    r = 8 if c["prec"] == "f64" else 4
+    cb = 2 * r
+    nnz, P, T = int(info.nnz), int(info.P), int(info.wt_rows)
+    G = (c["R"] * c["n"]) ** 2
+    if stage == "w_spmv":
+        return (4 + r) * nnz + B * (cb * T + cb * P)
+    return (4 + r) * nnz + 8 * (T + 1) + B * (cb * P + cb * G)
 
 
 def apply_bytes(c, T, complex_io, B=1):
