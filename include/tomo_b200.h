@@ -104,9 +104,10 @@ typedef struct tomo_op_info {
    * mirrored frequencies; with a window [1 - hi, hi] their interpolation windows are mirror images).
    * For real images the normal operator then runs W on one sample per pair and the folded W^T of
    * the pairs' primaries only. With a symmetric window [-m_sp, m_sp] around floor(x / h) (the
-   * reference's) the partner's window is the mirror image shifted by one node: W runs on every
-   * sample (sym_P = P), a pair-sum pass follows, and the fold reads the pair sums inside the pairs'
-   * common window (63 % of the entries at m_sp = 3). 0 everywhere: no pairs, the full fold runs. */
+   * reference's) the partner's window is the mirror image shifted by one node: W evaluates every
+   * sample (sym_P = P) and the pair sums, reading each pair's union window once, and the fold reads
+   * the pair sums inside the pairs' common window (63 % of the entries at m_sp = 3). 0 everywhere:
+   * no pairs, the full fold runs. */
   int sym_tasks;        /* warp tasks of the primaries' folded W^T (0: not built) */
   int64_t sym_pairs;    /* samples that have a mirror partner (both members counted) */
   int64_t sym_P;        /* samples W evaluates on the real-subspace normal operator */

@@ -194,6 +194,21 @@ void launch_w(const OpDev<R>& d, int B, const cplx<R>* grid, cplx<R>* samples, c
               cudaStream_t st);
 template <typename R>
 void launch_wt_rows(const OpDev<R>& d, int B, const SliceScalars* skip, cudaStream_t st);
+// Overlap pairs, W by units (a mirror pair, or an unpaired sample): one thread reads the pair's
+// (w + 1) x (w + 1) union window once and writes s_primary, s_partner = conj(sum with the shifted
+// factors) and the pair sum. Tables in unit order (the tile order of the primaries / unpaired).
+template <typename R>
+struct PairW {
+  int U, Upad;           // units, padded to 32
+  const int* base;       // [Upad] the primary's (unpaired sample's) window base ix0 | iy0 << 16
+  const R* fx;           // [w + 1][Upad] taps 0..w-1: the primary's x factors; tap w: the partner's own tap 0
+  const R* fy;           // [w + 1][Upad]
+  const int* pos;        // [Upad] output position of the primary (unpaired sample)
+  const int* ppos;       // [Upad] output position of the partner, -1: unpaired
+};
+template <typename R>
+void launch_w_pair(const OpDev<R>& d, const PairW<R>& pw, int B, const cplx<R>* grid, cplx<R>* samples,
+                   const SliceScalars* skip, cudaStream_t st);
 // Overlap pairs (opbuild.cu): s[P + t] = s[t] + conj(s[ppos[t]]) for the positions t of pair primaries
 template <typename R>
 void launch_pair_sigma(cplx<R>* s, int B, int P, int stride, const int* ppos, cudaStream_t st);
@@ -289,6 +304,12 @@ void gpu_half_w_finish(HalfWBuild* hb, int64_t Ppad, int64_t Ppad_h, int w, cons
                        const int* base, const R* wx, const R* wy, int* base_h, R* wx_h, R* wy_h, WtEnt<R>* ent,
                        int64_t n_ent, cudaStream_t st);
 void gpu_half_w_free(HalfWBuild* hb);
+// Overlap pairs: the unit tables of PairW from the tile-ordered W tables, the kept flags / compact
+// indices of gpu_half_w_begin (units = the samples that are not secondaries) and the partner
+// positions `ppos` of gpu_pair_sigma_setup.
+template <typename R>
+void gpu_pair_w_finish(HalfWBuild* hb, int64_t Ppad, int64_t Upad, int w, const int* ppos, const int* base,
+                       const R* wx, const R* wy, int* ubase, R* ufx, R* ufy, int* upos, int* uppos, cudaStream_t st);
 
 // ---- launchers (solver.cu) ----
 struct StencilCoef {

@@ -971,6 +971,43 @@ void gpu_half_w_finish(HalfWBuild* hb, int64_t Ppad, int64_t Ppad_h, int w, cons
 
 void gpu_half_w_free(HalfWBuild* hb) { delete hb; }
 
+namespace {
+template <typename R>
+__global__ void k_pair_units(int64_t P, int64_t Ppad, int64_t Upad, int w, const int* __restrict__ flag,
+                             const int* __restrict__ hpos, const int* __restrict__ ppos, const int* __restrict__ base,
+                             const R* __restrict__ wx, const R* __restrict__ wy, int* ubase, R* ufx, R* ufy, int* upos,
+                             int* uppos) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= P || !flag[t]) return;
+  const int u = hpos[t], pp = ppos[t] >= 0 ? ppos[t] : -1;
+  ubase[u] = base[t];
+  for (int a = 0; a < w; ++a) {
+    ufx[static_cast<size_t>(a) * Upad + u] = wx[static_cast<size_t>(a) * Ppad + t];
+    ufy[static_cast<size_t>(a) * Upad + u] = wy[static_cast<size_t>(a) * Ppad + t];
+  }
+  // union tap w = the partner's own tap 0 (its node there is the mirror of the primary's node w)
+  ufx[static_cast<size_t>(w) * Upad + u] = pp >= 0 ? wx[pp] : R(0);
+  ufy[static_cast<size_t>(w) * Upad + u] = pp >= 0 ? wy[pp] : R(0);
+  upos[u] = static_cast<int>(t);
+  uppos[u] = pp;
+}
+}  // namespace
+
+template <typename R>
+void gpu_pair_w_finish(HalfWBuild* hb, int64_t Ppad, int64_t Upad, int w, const int* ppos, const int* base,
+                       const R* wx, const R* wy, int* ubase, R* ufx, R* ufy, int* upos, int* uppos, cudaStream_t st) {
+  const int64_t P = hb->P;
+  BK(cudaMemsetAsync(ubase, 0, sizeof(int) * Upad, st));  // padding units: node 0, zero factors, no output
+  BK(cudaMemsetAsync(ufx, 0, sizeof(R) * (w + 1) * Upad, st));
+  BK(cudaMemsetAsync(ufy, 0, sizeof(R) * (w + 1) * Upad, st));
+  BK(cudaMemsetAsync(upos, 0xff, sizeof(int) * Upad, st));
+  BK(cudaMemsetAsync(uppos, 0xff, sizeof(int) * Upad, st));
+  k_pair_units<R><<<static_cast<unsigned>((P + 255) / 256), 256, 0, st>>>(P, Ppad, Upad, w, hb->flag.p, hb->hpos.p, ppos,
+                                                                          base, wx, wy, ubase, ufx, ufy, upos, uppos);
+  BK(cudaGetLastError());
+  BK(cudaStreamSynchronize(st));
+}
+
 #define TOMO_INST_BUILD(R)                                                                                     \
   template GpuBuild* gpu_build_begin<R>(const BuildArgs&, const double*, const double*, int*, R*, R*,         \
                                         cudaStream_t, GpuBuildSizes*);                                        \
@@ -980,6 +1017,8 @@ void gpu_half_w_free(HalfWBuild* hb) { delete hb; }
   template GpuBuild* gpu_build_fold<R>(const GpuBuild*, cudaStream_t, GpuBuildSizes*, const int*, const int*); \
   template void gpu_pair_sigma_setup<R>(int64_t, const int*, const int*, WtEnt<R>*, int64_t, int*, cudaStream_t); \
   template int64_t gpu_find_pairs<R>(const BuildArgs&, const int*, const R*, const R*, int*, cudaStream_t);  \
+  template void gpu_pair_w_finish<R>(HalfWBuild*, int64_t, int64_t, int, const int*, const int*, const R*, const R*, \
+                                     int*, R*, R*, int*, int*, cudaStream_t);                                 \
   template void gpu_half_w_finish<R>(HalfWBuild*, int64_t, int64_t, int, const int*, const int*, const int*, \
                                      const R*, const R*, int*, R*, R*, WtEnt<R>*, int64_t, cudaStream_t);    \
   template GpuBuild* gpu_build_gram_begin<R>(int, int, int64_t, const int*, const double*, const double*, cudaStream_t, \

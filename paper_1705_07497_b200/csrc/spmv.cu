@@ -395,6 +395,95 @@ __global__ void k_feedback_samples(int64_t n, cplx<R>* __restrict__ fk, const cp
   s[i] = v;
 }
 
+// ---------------------------------------------------------------- W by mirror-pair units (overlap pairs)
+// LN lanes per unit. The primary's window is taps [0, w) of the (w + 1)-wide union window, the
+// partner's conjugate-mirrored window taps [1, w]; the two share the factors of taps [1, w): each
+// grid row is read once, its common part summed once.
+//   s_primary = sum_{b < w} fy[b] (sum_{a < w} fx[a] g[b][a])
+//   t         = sum_{b >= 1} fy[b] (sum_{a >= 1} fx[a] g[b][a])      (= conj(s_partner))
+// Outputs s[pos] = s_primary, s[ppos] = conj(t), s[P + pos] = s_primary + t (the pair sum the
+// overlap-pair fold reads). HERM as in k_w_sep (this path is used on the half grid only).
+template <int WMAX, int LN, typename R>
+__global__ void __launch_bounds__(256) k_w_pair(OpDev<R> d, PairW<R> pw, int B, const cplx<R>* __restrict__ grid,
+                                                 cplx<R>* __restrict__ out, const SliceScalars* skip) {
+  using C2 = cplx<R>;
+  // LN lanes per unit: lane h sums the union window's rows [h * nr, (h + 1) * nr), nr = ceil((w + 1) / LN)
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int u = tid / LN, h = tid % LN;
+  if (u >= pw.Upad) return;  // Upad is a multiple of 32: both lanes of a unit stay (padding units: zero factors)
+  const int m = d.m, w = d.w;  // union window: w + 1 <= WMAX taps
+  const int nr = (w + LN) / LN;
+  const int base = __ldg(&pw.base[u]);
+  const int ix0 = base & 0xffff, iy0 = base >> 16;
+  const int po = __ldg(&pw.pos[u]), pp = __ldg(&pw.ppos[u]);
+  R fx[WMAX];
+  int ix[WMAX];
+#pragma unroll
+  for (int a = 0; a < WMAX; ++a) {
+    if (a <= w) {
+      fx[a] = __ldg(&pw.fx[static_cast<size_t>(a) * pw.Upad + u]);
+      const int v = ix0 + a;
+      ix[a] = v >= m ? v - m : v;
+    }
+  }
+  const size_t G = static_cast<size_t>(m) * m;
+  for (int b = static_cast<int>(blockIdx.y); b < B; b += static_cast<int>(gridDim.y)) {
+    if (skip && (skip[b].done || skip[b].frozen)) continue;
+    C2 s = czero<C2>(), t = czero<C2>();
+#pragma unroll 1
+    for (int bb = h * nr; bb < min((h + 1) * nr, w + 1); ++bb) {
+      const R fyv = __ldg(&pw.fy[static_cast<size_t>(bb) * pw.Upad + u]);
+      const int v0 = iy0 + bb;
+      const int v = v0 >= m ? v0 - m : v0;
+      const bool mir = v > (m >> 1);
+      const C2* row = grid + G * b + static_cast<size_t>(mir ? m - v : v) * m;
+      C2 g0 = czero<C2>(), gw = czero<C2>(), mid = czero<C2>();
+#pragma unroll
+      for (int a = 0; a < WMAX; ++a) {
+        if (a <= w) {
+          const C2 gv = row[mir ? ((m - ix[a]) & (m - 1)) : ix[a]];
+          if (a == 0) {
+            g0 = mk<C2>(fx[0] * gv.x, fx[0] * gv.y);
+          } else if (a == w) {
+            gw = mk<C2>(fx[a] * gv.x, fx[a] * gv.y);
+          } else {
+            mid.x += fx[a] * gv.x;
+            mid.y += fx[a] * gv.y;
+          }
+        }
+      }
+      if (mir) {  // conj(sum f g) = sum f conj(g)
+        g0.y = -g0.y;
+        gw.y = -gw.y;
+        mid.y = -mid.y;
+      }
+      if (bb < w) {
+        s.x += fyv * (g0.x + mid.x);
+        s.y += fyv * (g0.y + mid.y);
+      }
+      if (bb >= 1) {
+        t.x += fyv * (mid.x + gw.x);
+        t.y += fyv * (mid.y + gw.y);
+      }
+    }
+#pragma unroll
+    for (int o = 1; o < LN; o <<= 1) {
+      s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
+      s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
+      t.x += __shfl_xor_sync(0xffffffffu, t.x, o);
+      t.y += __shfl_xor_sync(0xffffffffu, t.y, o);
+    }
+    if (po < 0) continue;  // padding unit
+    C2* sb = out + static_cast<size_t>(b) * d.s_stride;
+    if (h == 0) {
+      sb[po] = s;
+    } else if (h == 1 && pp >= 0) {
+      sb[pp] = mk<C2>(t.x, -t.y);
+      sb[d.P + po] = mk<C2>(s.x + t.x, s.y + t.y);
+    }
+  }
+}
+
 }  // namespace
 
 // Batched calls (B slices per launch) of the small-grid SpMVs: slice groups go to grid.y
@@ -515,6 +604,18 @@ void launch_wt_spread(const OpDev<R>& d, int B, const cplx<R>* samples, cplx<R>*
     launch_task_spmv<R>(d.wt_view(), d.m, B, samples, static_cast<size_t>(d.s_stride), grid, skip, st);
 }
 
+template <typename R>
+void launch_w_pair(const OpDev<R>& d, const PairW<R>& pw, int B, const cplx<R>* grid, cplx<R>* samples,
+                   const SliceScalars* skip, cudaStream_t st) {
+  // measured at c2 (slices/s): 1 lane per unit 30.2, 2 lanes 33.9, 4 lanes in 128-thread CTAs 35.2
+  // (64 threads 34.8, 256 threads 33.5), 8 lanes 33.1; the pair-sum pass behind the plain W 33.5
+  constexpr int kLanes = 4, kThreads = 128;
+  const int blocks = (kLanes * pw.Upad + kThreads - 1) / kThreads;
+  const unsigned ydim = batch_ydim(blocks, B);
+  CK_LAUNCH(launch_k(k_w_pair<8, kLanes, R>, dim3(blocks, ydim), kThreads, 0, st, d, pw, B, grid, samples, skip));
+  note_launch();
+}
+
 // Overlap pairs: the pair sums s_j + conj(s_partner) behind the samples of each slice.
 template <typename R>
 __global__ void k_pair_sigma(cplx<R>* __restrict__ s, int B, int P, int stride, const int* __restrict__ ppos) {
@@ -575,6 +676,8 @@ void launch_gather_samples(const cplx<R>* in, cplx<R>* out, const int* perm, int
                                     cudaStream_t);                                                          \
   template void launch_gram<R>(const OpDev<R>&, int, const cplx<R>*, cplx<R>*, const SliceScalars*, cudaStream_t); \
   template void launch_pair_sigma<R>(cplx<R>*, int, int, int, const int*, cudaStream_t);                         \
+  template void launch_w_pair<R>(const OpDev<R>&, const PairW<R>&, int, const cplx<R>*, cplx<R>*, const SliceScalars*, \
+                                 cudaStream_t);                                                                  \
   template void launch_wt_grid<R>(const OpDev<R>&, int, const cplx<R>*, cplx<R>*, cudaStream_t);            \
   template void launch_weight_samples<R>(cplx<R>*, int, int, int, const int*, cudaStream_t);               \
   template void launch_gather_samples<R>(const cplx<R>*, cplx<R>*, const int*, int, int, cudaStream_t);     \

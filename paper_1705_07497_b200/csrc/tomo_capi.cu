@@ -336,6 +336,16 @@ struct tomo_op {
   // positions) and the fold reads them inside the pairs' common window.
   TaskSet sym;
   Raw pairs, hbase, hwx, hwy, ppos;
+  // overlap pairs, W by units (PairW; built for windows of at most 7 nodes): hbase / hwx / hwy hold
+  // the unit tables ((w + 1) factors per axis), upos / uppos the output positions
+  Raw upos, uppos;
+  int64_t n_units = 0;
+  int Upad = 0;
+  template <typename R>
+  PairW<R> pair_w() const {
+    return PairW<R>{static_cast<int>(n_units), Upad, hbase.as<int>(), hwx.as<R>(), hwy.as<R>(), upos.as<int>(),
+                    uppos.as<int>()};
+  }
   int64_t Ph = 0, n_paired = 0;
   int Ppad_h = 0;
   int sym_mode = 0;
@@ -1166,6 +1176,23 @@ void build_tables(tomo_op* op) {
     op->ppos.ensure(sizeof(int) * g.P);
     gpu_pair_sigma_setup<R>(g.P, op->wperm.as<int>(), op->pairs.as<int>(), op->sym.ent.as<WtEnt<R>>(), op->sym.slots,
                             op->ppos.as<int>(), 0);
+    if (g.lo == -g.hi && w + 1 <= 8 && ab_knob("TOMO_PAIR_W") != "0") {
+      // W by units: one thread per mirror pair / unpaired sample over the (w + 1)^2 union window
+      // (symmetric windows: the partner's mirrored window is the primary's shifted up by one node)
+      int64_t U = 0;
+      std::unique_ptr<HalfWBuild, void (*)(HalfWBuild*)> hw(
+          gpu_half_w_begin(g.P, op->wperm.as<int>(), op->pairs.as<int>(), 0, &U), gpu_half_w_free);
+      op->n_units = U;
+      op->Upad = static_cast<int>((U + 31) / 32 * 32);
+      op->hbase.ensure(sizeof(int) * op->Upad);
+      op->hwx.ensure(sizeof(R) * (w + 1) * op->Upad);
+      op->hwy.ensure(sizeof(R) * (w + 1) * op->Upad);
+      op->upos.ensure(sizeof(int) * op->Upad);
+      op->uppos.ensure(sizeof(int) * op->Upad);
+      gpu_pair_w_finish<R>(hw.get(), op->Ppad, op->Upad, w, op->ppos.as<int>(), op->wbase.as<int>(), op->wxs.as<R>(),
+                           op->wys.as<R>(), op->hbase.as<int>(), op->hwx.as<R>(), op->hwy.as<R>(),
+                           op->upos.as<int>(), op->uppos.as<int>(), 0);
+    }
   } else if (op->sym.n_tasks > 0) {
     // the half W (one sample per mirror pair + the unpaired ones, tile order kept); the mirror-pair
     // W^T's entries move from sample indices to the half W's output positions
@@ -1292,9 +1319,13 @@ void normal_core(tomo_op* op, int B, const void* in, bool complex_in, const PUpd
     launch_gram<R>(d, B, d.g, d.Gt, skip, st);
     launch_t1_cols_only<R>(d, B, skip, st);
   } else {
-    launch_w<R>(d, B, d.g, d.s, skip, st);
-    if (d.s_stride == 2 * d.P)  // overlap pairs: the pair sums behind each slice's samples
-      launch_pair_sigma<R>(d.s, B, d.P, d.s_stride, op->ppos.as<int>(), st);
+    if (d.s_stride == 2 * d.P && op->n_units > 0) {
+      launch_w_pair<R>(d, op->pair_w<R>(), B, d.g, d.s, skip, st);  // overlap pairs: W by units, pair sums included
+    } else {
+      launch_w<R>(d, B, d.g, d.s, skip, st);
+      if (d.s_stride == 2 * d.P)  // overlap pairs: the pair sums behind each slice's samples
+        launch_pair_sigma<R>(d.s, B, d.P, d.s_stride, op->ppos.as<int>(), st);
+    }
     launch_wt_rows<R>(d, B, skip, st);  // W^T + PA (one fused kernel where available)
   }
   launch_t1_rows<R>(d, B, e, st);
@@ -2833,9 +2864,13 @@ int tomo_profile_stages(tomo_op* op, int batch, int reps, int complex_io, double
           if (op->fused())
             launch_gram<R>(d, batch, d.g, d.Gt, op->scal(), cs);
           else {
-            launch_w<R>(d, batch, d.g, d.s, op->scal(), cs);
-            if (d.s_stride == 2 * d.P)
-              launch_pair_sigma<R>(d.s, batch, d.P, d.s_stride, op->ppos.as<int>(), cs);
+            if (d.s_stride == 2 * d.P && op->n_units > 0) {
+              launch_w_pair<R>(d, op->pair_w<R>(), batch, d.g, d.s, op->scal(), cs);
+            } else {
+              launch_w<R>(d, batch, d.g, d.s, op->scal(), cs);
+              if (d.s_stride == 2 * d.P)
+                launch_pair_sigma<R>(d.s, batch, d.P, d.s_stride, op->ppos.as<int>(), cs);
+            }
           }
         } else if (s == 3) {
           if (!op->fused()) launch_wt_spread<R>(d, batch, d.s, d.Gt, op->scal(), cs);
@@ -2914,11 +2949,14 @@ int tomo_profile_stages(tomo_op* op, int batch, int reps, int complex_io, double
       //   (the Hermitian path: W gathers the T_h touched nodes of the half grid; the folded W^T
       //    streams its nnz_f entries, ids of T_h nodes, writes the half grid)
       //   (mirror pairs: W runs on the Ph kept samples, the primaries' fold streams its entries)
-      //   (overlap pairs: W runs on every sample, + the pair-sum pass: read 2, write 1 per pair)
+      //   (overlap pairs: W evaluates every sample and the pair sums)
       const bool half_w = sym && op->sym_mode == 1;
       const double Pw = half_w ? static_cast<double>(op->Ph) : P;
       const double nnzb = (half_w ? Pw * op->g.w * op->g.w : static_cast<double>(op->nnz)) * (4.0 + rs);
-      const double sig = sym && op->sym_mode == 2 ? B * 1.5 * cs * static_cast<double>(op->n_paired) : 0.0;
+      // (pair sums: one write per pair from the unit W, or the pass: two reads and a write per pair)
+      const double sig = sym && op->sym_mode == 2
+                             ? B * (op->n_units > 0 ? 0.5 : 1.5) * cs * static_cast<double>(op->n_paired) / 2.0
+                             : 0.0;
       const double T = static_cast<double>(herm ? op->herm.touched : op->wt_rows);
       const double nnzt = sym ? static_cast<double>(op->sym.nnz) * (4.0 + rs)
                               : herm ? static_cast<double>(op->herm.nnz) * (4.0 + rs) : nnzb;

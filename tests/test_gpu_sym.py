@@ -122,6 +122,37 @@ def test_overlap_pairs_apply_matches(T, name, prec):
         assert err < 1e-10
 
 
+@pytest.mark.parametrize("name", ["msp3_n64", "R4_msp3_n32"])
+def test_pair_sum_pass_matches_unit_w(T, name):
+    """The fallback of wide (w > 7) windows — the plain W followed by the pair-sum pass
+    (TOMO_AB=1 TOMO_PAIR_W=0) — against the default W by mirror-pair units: the same operator."""
+    og = O.Geometry(**OVERLAP[name])
+    op = T.make_direct_backend(pgeom(T, og), precision="f64", max_batch=8)
+    os.environ["TOMO_AB"], os.environ["TOMO_PAIR_W"] = "1", "0"
+    try:
+        alt = T.make_direct_backend(pgeom(T, og), precision="f64", max_batch=8)
+    finally:
+        del os.environ["TOMO_PAIR_W"], os.environ["TOMO_AB"]
+    assert alt.info.sym_tasks == op.info.sym_tasks > 0
+    n = og.n
+    for B in (1, 5):
+        u = RNG.standard_normal((B, n, n))
+        a = op.apply_normal_real(dev(u, True)).cpu().numpy()
+        b = alt.apply_normal_real(dev(u, True)).cpu().numpy()
+        print(f"{name} B={B}: unit W vs W + pair-sum pass rel-L2 {rel(a, b):.2e}")
+        assert rel(a, b) < 2e-11
+
+
+def test_wide_symmetric_window_uses_the_pass(T):
+    """m_sp = 6 (13-node windows): no unit W (union window > 8 nodes), the pass runs; vs the oracle."""
+    og = O.Geometry(n=32, n_angles=20, n_b=47, win_lo=-6, win_hi=6)
+    op = T.make_direct_backend(pgeom(T, og), precision="f64")
+    assert op.info.sym_tasks > 0
+    u = RNG.standard_normal((og.n, og.n))
+    got = op.apply_normal_real(dev(u, True)).cpu().numpy().reshape(og.n, og.n)
+    assert rel(got, O.apply_normal_real(og, u)) < 1e-10
+
+
 def test_operator_is_symmetric(T):
     """<N u, v> = <u, N v>: the mirror-pair operator is U^T U of one interpolation U; the overlap-pair
     operator is symmetric to the rounding of the sample positions."""

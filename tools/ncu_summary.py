@@ -8,7 +8,7 @@ import sys
 from collections import defaultdict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-STAGES = [("k_task_spmv", "wt_spread"), ("k_t2_rows", "t2_rows"), ("k_t2_cols", "t2_cols"), ("k_w_sep", "w_spmv"), ("k_pair_sigma", "pair_sigma"),
+STAGES = [("k_task_spmv", "wt_spread"), ("k_t2_rows", "t2_rows"), ("k_t2_cols", "t2_cols"), ("k_w_sep", "w_spmv"), ("k_w_pair", "w_spmv"), ("k_pair_sigma", "pair_sigma"),
           ("k_t1_cols", "t1_cols"), ("k_t1_rows", "t1_rows"), ("k_cg_update", "cg_update"), ("k_sb_post", "sb_post"),
           ("k_stencil", "stencil"), ("k_cp_dual", "cp_dual")]
 

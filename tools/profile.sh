@@ -7,7 +7,7 @@ TAG=${1:-r01}
 OUT=gpurun_out
 REP=/tmp/ncu
 mkdir -p $OUT $REP
-K='k_(t2_rows|t2_cols|w_sep|pair_sigma|task_spmv|t1_cols|t1_rows)|k_cg_update|k_sb_post|k_stencil|k_cp_dual'
+K='k_(t2_rows|t2_cols|w_sep|w_pair|pair_sigma|task_spmv|t1_cols|t1_rows)|k_cg_update|k_sb_post|k_stencil|k_cp_dual'
 # launch list of the default bench (c2) inside the timed solve: cold-cache, serialised per-launch times
 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"$K" -s 600 -c 400 --csv \
     --log-file $OUT/${TAG}_launches_c2.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-other-configs > $OUT/${TAG}_launches_c2.log 2>&1
