@@ -558,7 +558,11 @@ template <typename R>
 void launch_task_spmv(const TaskSpmv<R>& ts, int m, int B, const cplx<R>* x, size_t in_stride, cplx<R>* grid,
                       const SliceScalars* skip, cudaStream_t st, bool herm = false) {
   if (ts.n_tasks <= 0) return;
-  const int threads = 256;
+  // CTA size (a warp per task either way), measured: c2 35.0 / 34.7 / 34.6 slices/s and c1 81k / 81k /
+  // 76k applies/s at 256 / 128 / 64 threads; c5 (m = 8192, row-ordered tasks) 959 / 965 / 967 applies/s
+  // (W^T 177 -> 170 us); c3 equal. TOMO_WT_THREADS overrides (A/B).
+  static const int env_wt_thr = env_int("TOMO_WT_THREADS", 0);
+  const int threads = env_wt_thr == 64 || env_wt_thr == 128 || env_wt_thr == 256 ? env_wt_thr : (m >= 4096 ? 64 : 256);
   const int blocks = (ts.n_tasks * 32 + threads - 1) / threads;
   // group depth and software pipelining measured on B200 (c2/c3/c5): fp32 6 chunks, not
   // pipelined (32 registers, full occupancy); fp64 4 chunks, pipelined for m <= 2048 (c2 W^T
