@@ -35,6 +35,8 @@ OVERLAP = {
     "R4_msp3_n32": dict(n=32, n_angles=20, n_b=33, oversample=4, win_lo=-3, win_hi=3,
                         tau=np.pi * 3 / (32 ** 2 * 4 * 3.5)),
     "n128_c2_like": dict(n=128, n_angles=45, n_b=181, win_lo=-3, win_hi=3, tau=3 / 128 ** 2),
+    # neither symmetric nor its own mirror image: common window [-1, 2], plain W + pair-sum pass
+    "asym_m1p3": dict(n=64, n_angles=26, n_b=77, win_lo=-1, win_hi=3, tau=3 / 64 ** 2),
 }
 
 
